@@ -1,0 +1,234 @@
+"""O2 -- pure-Python brute-force oracle for the KV conversion (tiny shapes only).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/ (and nothing in the product path).
+It shares no code with O1 (oracle/kv_oracle.c) beyond the plain integer
+encoding of axes/dtypes, and none with the CUDA path.
+
+It deliberately computes the same result as O1 by a *different* route, so that
+a slip in either one shows up as a disagreement:
+
+* **Index mapping is source-driven.**  O1 walks the destination and computes
+  strided offsets with a formula.  O2 enumerates every physical position of
+  every source pool in memory order (``itertools.product`` over the extents in
+  ``axis_order``), recovers the logical element KV[r][l][c][h][t][d] through
+  the *inverse* block table, then enumerates every destination position the same
+  way and looks the logical element up.  No stride arithmetic appears.
+* **Casts are nearest-code searches.**  O1 rounds with frexp/nearbyint.  O2
+  decodes every finite code of the target format to an exact ``Fraction``,
+  bisects for the neighbours of the exact input value and picks the nearer one,
+  ties to the even code (RNE, IEEE 754 roundTiesToEven).  Overflow: a virtual
+  code one quantum past the largest finite value stands for Inf (fp16/bf16) or
+  saturates to +-448 (e4m3fn satfinite).
+
+Passages: P:113 (III-B2, Fig. 5 layout alignment), P:125 (III-B3, Fig. 4 TP
+merge/split), P:65 (precision alignment), SPEC S:255/S:280 (zero-filled tail),
+S:279 (head-contiguous TP), readings in DESIGN.md.
+"""
+from __future__ import annotations
+
+import bisect
+import itertools
+from fractions import Fraction
+
+import numpy as np
+
+LAYER, KV, BLOCK, SLOT, HEAD, DIM = range(6)
+F16, BF16, E4M3, F32 = range(4)
+
+# (exp_bits, mantissa_bits, bias, has_inf)
+_FMT = {F16: (5, 10, 15, True), BF16: (8, 7, 127, True), E4M3: (4, 3, 7, False), F32: (8, 23, 127, True)}
+NBYTES = {F16: 2, BF16: 2, E4M3: 1, F32: 4}
+
+
+def decode(code: int, dt: int):
+    """Exact value of an encoding as a Fraction; 'nan' / '+inf' / '-inf' / '-0' strings for specials."""
+    eb, mb, bias, has_inf = _FMT[dt]
+    sign = (code >> (eb + mb)) & 1
+    e = (code >> mb) & ((1 << eb) - 1)
+    m = code & ((1 << mb) - 1)
+    if has_inf and e == (1 << eb) - 1:
+        if m:
+            return "nan"
+        return "-inf" if sign else "+inf"
+    if not has_inf and e == (1 << eb) - 1 and m == (1 << mb) - 1:
+        return "nan"  # OCP e4m3fn: S.1111.111 is the only NaN, no infinities
+    if e == 0 and m == 0:
+        return "-0" if sign else Fraction(0)
+    if e == 0:
+        mag = Fraction(m, 1 << mb) * Fraction(2) ** (1 - bias)
+    else:
+        mag = (1 + Fraction(m, 1 << mb)) * Fraction(2) ** (e - bias)
+    return -mag if sign else mag
+
+
+_TABLES: dict = {}
+
+
+def _table(dt):
+    """Sorted (value, code) of all finite non-negative codes + virtual overflow code."""
+    if dt not in _TABLES:
+        assert dt != F32, "O2 enumerates code tables; fp32 targets are O1-only"
+        eb, mb, bias, has_inf = _FMT[dt]
+        vals = []
+        for code in range(1 << (eb + mb)):  # sign bit clear
+            v = decode(code, dt)
+            if isinstance(v, Fraction):
+                vals.append((v, code))
+        vals.sort()
+        top_v, top_c = vals[-1]
+        quantum = top_v - vals[-2][0]
+        vals.append((top_v + quantum, "overflow"))
+        _TABLES[dt] = ([v for v, _ in vals], [c for _, c in vals])
+    return _TABLES[dt]
+
+
+def round_to(x, dt: int) -> int:
+    """Round an exact value (Fraction, or 'nan'/'+inf'/'-inf') to format dt.
+
+    fp16/bf16/fp32: IEEE RNE, overflow -> +-Inf, NaN -> 0x7FFF / 0x7FFFFFFF
+    (canonical NaN, reading 12).  e4m3fn: RNE with satfinite
+    (overflow and +-Inf -> +-448), NaN -> 0x7F.
+    """
+    eb, mb, bias, has_inf = _FMT[dt]
+    sbit = 1 << (eb + mb)
+    inf_code = ((1 << eb) - 1) << mb
+    if x == "nan":
+        return 0x7F if dt == E4M3 else (0x7FFFFFFF if dt == F32 else 0x7FFF)
+    if x == "-0":
+        return sbit
+    if x in ("+inf", "-inf"):
+        neg = x == "-inf"
+        mag = 0x7E if dt == E4M3 else inf_code
+        return mag | (sbit if neg else 0)
+    neg = x < 0
+    ax = -x if neg else x
+    vals, codes = _table(dt)
+    i = bisect.bisect_left(vals, ax)
+    if i < len(vals) and vals[i] == ax:
+        code = codes[i]
+    else:
+        lo_v, lo_c = vals[i - 1], codes[i - 1]
+        if i >= len(vals):
+            code = "overflow"
+        else:
+            hi_v, hi_c = vals[i], codes[i]
+            dl, dh = ax - lo_v, hi_v - ax
+            if dl < dh:
+                code = lo_c
+            elif dh < dl:
+                code = hi_c
+            else:  # tie: even code; the virtual overflow code follows an odd max code
+                code = lo_c if (lo_c % 2 == 0) else hi_c
+    if code == "overflow":
+        code = 0x7E if dt == E4M3 else inf_code
+    if neg:
+        code |= sbit  # sign kept, including -0
+    return code
+
+
+def _f32(frac_or_special) -> np.float32:
+    if isinstance(frac_or_special, Fraction):
+        return np.float32(float(frac_or_special))  # exact for <= 24 significant bits
+    return {"nan": np.float32("nan"), "+inf": np.float32("inf"), "-inf": np.float32("-inf"),
+            "-0": np.float32(-0.0)}[frac_or_special]
+
+
+def _exact(v: np.float32):
+    if np.isnan(v):
+        return "nan"
+    if np.isinf(v):
+        return "-inf" if v < 0 else "+inf"
+    if v == 0 and np.signbit(v):
+        return "-0"
+    return Fraction(float(v))
+
+
+def cast(code: int, src_dt: int, dst_dt: int, src_scale: float = 1.0, dst_scale: float = 1.0) -> int:
+    """Element cast (readings 10-13).  Same dtype: bits unchanged."""
+    if src_dt == dst_dt:
+        return code
+    x = decode(code, src_dt)
+    with np.errstate(all="ignore"):
+        if src_dt == E4M3:
+            x = _exact(_f32(x) * np.float32(src_scale))
+        if dst_dt == E4M3:
+            inv = np.float32(1.0) / np.float32(dst_scale)
+            x = _exact(_f32(x) * inv)
+    return round_to(x, dst_dt)
+
+
+def _extents(lay):
+    return {LAYER: lay["L"], KV: 2, BLOCK: lay["NB"], SLOT: lay["B"], HEAD: lay["H"] // lay["tp"], DIM: lay["D"]}
+
+
+def positions(lay):
+    """Yield (linear position, {axis: index}) over the pool in memory order."""
+    ext = _extents(lay)
+    order = lay["order"]
+    for pos, idx in enumerate(itertools.product(*[range(ext[a]) for a in order])):
+        yield pos, dict(zip(order, idx))
+
+
+def _inverse_table(tables):
+    inv = {}
+    for r, ids in enumerate(tables):
+        for j, b in enumerate(ids):
+            assert b not in inv, "block id used twice"
+            inv[b] = (r, j)
+    return inv
+
+
+def _scale(lay, l, c, hl):
+    s = lay.get("scales")
+    if s is None:
+        return 1.0
+    return float(s[l][c][hl])
+
+
+def convert(src_lays, src_pools, dst_lays, dst_pools, n_tokens, src_tables, dst_tables, layer_range=None):
+    """Brute-force P -> D conversion.  Pools are flat lists of int codes; dst_pools
+    are modified in place (prior values survive where nothing is written)."""
+    L = src_lays[0]["L"]
+    lb, le = layer_range if layer_range else (0, L)
+    # 1. logical tensor from every source pool, source-driven
+    logical = {}
+    src_inv = _inverse_table(src_tables)
+    for lay, pool in zip(src_lays, src_pools):
+        hp_n = lay["H"] // lay["tp"]
+        for pos, ix in positions(lay):
+            if ix[BLOCK] not in src_inv:
+                continue
+            r, jb = src_inv[ix[BLOCK]]
+            t = jb * lay["B"] + ix[SLOT]
+            if t >= n_tokens[r]:
+                continue  # source tail: never read
+            h = lay["rank"] * hp_n + ix[HEAD]
+            logical[(r, ix[LAYER], ix[KV], h, t, ix[DIM])] = (pool[pos], lay, ix[HEAD])
+    # 2. every destination position, destination-driven by enumeration
+    dst_inv = _inverse_table(dst_tables)
+    for lay, pool in zip(dst_lays, dst_pools):
+        hd_n = lay["H"] // lay["tp"]
+        for pos, ix in positions(lay):
+            if ix[BLOCK] not in dst_inv or not (lb <= ix[LAYER] < le):
+                continue
+            r, j = dst_inv[ix[BLOCK]]
+            t = j * lay["B"] + ix[SLOT]
+            h = lay["rank"] * hd_n + ix[HEAD]
+            if t >= n_tokens[r]:
+                pool[pos] = 0  # zero-filled tail
+                continue
+            code, slay, shl = logical[(r, ix[LAYER], ix[KV], h, t, ix[DIM])]
+            pool[pos] = cast(code, slay["dtype"], lay["dtype"],
+                             _scale(slay, ix[LAYER], ix[KV], shl), _scale(lay, ix[LAYER], ix[KV], ix[HEAD]))
+    return dst_pools
+
+
+def plan(tp_p: int, tp_d: int, H: int):
+    """A2 by enumeration of heads: {(p, q): [heads]} (Fig. 4)."""
+    if H % tp_p or H % tp_d:
+        raise ValueError("tp degree does not divide num_kv_heads")
+    pairs = {}
+    for h in range(H):
+        p, q = h // (H // tp_p), h // (H // tp_d)
+        pairs.setdefault((p, q), []).append(h)
+    return pairs
