@@ -174,3 +174,17 @@ def test_o1_vs_o2_bruteforce_casts(o1, pair):
         got = o1.cast_array(codes, src, dst, s_src, s_dst)
         ref = np.array([o2.cast(int(c), src, dst, s_src, s_dst) for c in codes])
         assert np.array_equal(got.astype(np.int64), ref.astype(np.int64)), (pair, scale)
+
+
+@pytest.mark.parametrize("src", [F16, BF16])
+@pytest.mark.parametrize("scale", [1.0, 0.25, 8.0, 0.0123456, 3.3, 0.7071, 5.5 / 448, 0.05])
+def test_e4m3_scaled_op_order_exhaustive(o1, src, scale):
+    """Reading 10 fixes the op order v = RN_f32(f32(x) * RN_f32(1/s)); numpy float32 arithmetic
+    (IEEE binary32) computes v, ml_dtypes rounds it after the satfinite clamp.  x/s differs
+    from x*(1/s) on a few patterns (e.g. s = 5.5/448), so this pins the order as well."""
+    nan = _is_nan16(ALL16, src)
+    xf = ALL16.view(np.float16).astype(np.float32) if src == F16 else (ALL16.astype(np.uint32) << 16).view(np.float32)
+    with np.errstate(all="ignore"):
+        v = xf * (np.float32(1.0) / np.float32(scale))
+    got = o1.cast_array(ALL16, src, E4M3, 1.0, scale)
+    assert np.array_equal(got[~nan], _ml_e4m3(v)[~nan])
