@@ -1,0 +1,567 @@
+#!/usr/bin/env python
+"""bench.py -- KV transfer GB/s and ms/request (P -> D, device-timed) vs the HBM/NVLink
+roofline, for the heterogeneous-compatible KV transmission path (arXiv 2509.17542, III-B).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode push|nccl]
+
+N = 1 (default): BASELINE configs[1] (c2: Llama-2-7B KV, one 2048-token prompt, P TP=2 -> D TP=1,
+  fp16, block 16 -> 16, P layout NHD-per-layer -> D layout block-major HND) with all three
+  ranks' pools on one GPU: one fused kv_convert_reshard launch per step, HBM-bound.
+N >= 2 (torchrun, one process per GPU): BASELINE configs[3] (c4: Llama-3-70B GQA KV,
+  32 x 4096 tokens, P TP=4 -> D TP=4, bf16 -> fp8-e4m3 per-head scale) as N/2 independent
+  (P rank p -> D rank p) pairs on disjoint GPUs (P = ranks 0..N/2-1): N=8 is the full c4,
+  N=2/4 its per-GPU-equivalent sub-configs; per-pair work fixed -> weak
+  scaling.  Default mode "push": the fused gather+convert kernel stores into the D rank's
+  IPC-mapped pool over NVLink, then a release flag (K4/K5); "nccl": pack -> ncclSend /
+  ncclRecv -> unpack, per-layer pipelined.
+
+One JSON line on rank 0 (contract in the task statement); `value` = logical source KV
+GB (2*L*H*D*T*bytes_src summed over all requests and pairs) / max-over-ranks device time.
+Inputs are larger than L2 (GBs per step), so no L2 flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "KV transfer GB/s and ms/request (P->D, device-timed) vs HBM/NVLink roofline"
+NVLINK_MEASURED_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction
+NVLINK_NOMINAL_GBS = 900.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mode", default="push", choices=["push", "nccl"])
+    ap.add_argument("--layer-chunk", type=int, default=0, help="layers per chunk (0 = whole model)")
+    ap.add_argument("--workload", default=None, help="override: c1..c5")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--cpu-sample-layers", type=int, default=0)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+# ------------------------------------------------------------------------------------
+# clocks during the timed region (pynvml polling thread)
+# ------------------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, torch_dev):
+        self.samples, self.reasons, self.ok = [], 0, False
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            try:
+                import torch
+                pr = torch.cuda.get_device_properties(torch_dev)
+                bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(int(torch_dev))
+            self.h, self.nv = h, pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # no NVML: report it, never fake numbers
+            self.err = repr(e)
+
+    def _poll(self):
+        nv = self.nv
+        getr = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(getr(self.h))
+            except Exception:
+                pass
+            time.sleep(0.01)
+
+    def start(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+
+    def stop(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "note": getattr(self, "err", "nvml off")}
+        self._stop.set()
+        self.t.join()
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------
+# workload construction (inputs from synth; device memory from torch)
+# ------------------------------------------------------------------------------------
+class Workload:
+    """One instance pair's layouts, pools, tables for the P ranks / D ranks on this process."""
+
+    def __init__(self, cfg, p_ranks, d_ranks, device, contiguous=False):
+        import torch
+        import paper_2509_17542_b200 as kvx
+        self.cfg, self.device = cfg, device
+        c = cfg
+        self.NB_p = synth.pool_capacity(c.n_tokens, c.B_p)
+        self.NB_d = synth.pool_capacity(c.n_tokens, c.B_d)
+        self.src_tables = synth.block_tables(c.seed + 1, c.n_tokens, c.B_p, self.NB_p, contiguous)
+        self.dst_tables = synth.block_tables(c.seed + 2, c.n_tokens, c.B_d, self.NB_d, contiguous)
+        self.p_ranks, self.d_ranks = list(p_ranks), list(d_ranks)
+        self.src_dicts, self.src_lays, self.src_pools = {}, {}, {}
+        for p in self.p_ranks:
+            d = synth.layout(c.L, c.H, c.D, c.tp_p, p, c.B_p, self.NB_p, c.src_dtype, c.p_order)
+            lay = kvx.Layout.from_dict(d)
+            pool = lay.new_pool(device)
+            view = pool.view(torch.uint8 if synth.NBYTES[c.src_dtype] == 1 else torch.int16)
+            synth.fill_random_finite_(view, c.seed + 100 + p, c.src_dtype)
+            self.src_dicts[p], self.src_lays[p], self.src_pools[p] = d, lay, pool
+        self.dst_dicts, self.dst_lays, self.dst_pools, self.scales = {}, {}, {}, {}
+        for q in self.d_ranks:
+            sc_np = None
+            sc = None
+            if c.dst_dtype == synth.E4M3:
+                sc_np = synth.pow2_scales(c.seed + 200 + q, c.L, c.H // c.tp_d)
+                sc = torch.from_numpy(sc_np).to(device)
+            d = synth.layout(c.L, c.H, c.D, c.tp_d, q, c.B_d, self.NB_d, c.dst_dtype, c.d_order, sc_np)
+            lay = kvx.Layout.from_dict(d, sc)
+            self.dst_dicts[q], self.dst_lays[q] = d, lay
+            self.dst_pools[q] = lay.new_pool(device, fill=synth.CANARY)
+        any_src = self.src_lays[self.p_ranks[0]] if self.p_ranks else kvx.Layout.from_dict(
+            synth.layout(c.L, c.H, c.D, c.tp_p, 0, c.B_p, self.NB_p, c.src_dtype, c.p_order))
+        any_dst = self.dst_lays[self.d_ranks[0]] if self.d_ranks else kvx.Layout.from_dict(
+            synth.layout(c.L, c.H, c.D, c.tp_d, 0, c.B_d, self.NB_d, c.dst_dtype, c.d_order,
+                         np.ones((c.L, 2, c.H // c.tp_d), np.float32)),
+            torch.ones(c.L * 2 * (c.H // c.tp_d), device=device))
+        self._keep = (any_src, any_dst)
+        self.src_bt = kvx.Batch(any_src, c.n_tokens, self.src_tables, device)
+        self.dst_bt = kvx.Batch(any_dst, c.n_tokens, self.dst_tables, device)
+
+    # algorithmic bytes: what the method must move
+    def src_bytes(self, p_ranks=None):
+        c = self.cfg
+        n = len(p_ranks) if p_ranks is not None else c.tp_p
+        return 2 * c.L * (c.H // c.tp_p) * n * c.D * c.total_tokens * synth.NBYTES[c.src_dtype]
+
+    def dst_bytes(self, d_ranks=None):
+        c = self.cfg
+        n = len(d_ranks) if d_ranks is not None else c.tp_d
+        padded = sum(synth.blocks_for(t, c.B_d) * c.B_d for t in c.n_tokens)
+        return 2 * c.L * (c.H // c.tp_d) * n * c.D * padded * synth.NBYTES[c.dst_dtype]
+
+
+def extract(pool_t, d, layers, block_ids):
+    """Compact host copy of a pool restricted to layers [lb, le) and the given blocks
+    (same axis order) -> (numpy codes, layout dict).  Bench/test infrastructure."""
+    import torch
+    nb = synth.NBYTES[d["dtype"]]
+    tdt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[nb]
+    ext = {synth.LAYER: d["L"], synth.KV: 2, synth.BLOCK: d["NB"], synth.SLOT: d["B"],
+           synth.HEAD: d["H"] // d["tp"], synth.DIM: d["D"]}
+    t = pool_t.view(tdt).view([ext[a] for a in d["order"]])
+    t = t.index_select(d["order"].index(synth.LAYER), torch.arange(layers[0], layers[1], device=t.device))
+    t = t.index_select(d["order"].index(synth.BLOCK), torch.as_tensor(block_ids, device=t.device, dtype=torch.long))
+    a = t.contiguous().cpu().numpy().reshape(-1)
+    a = a.view({1: np.uint8, 2: np.uint16, 4: np.uint32}[nb])
+    nd = dict(d)
+    nd["L"], nd["NB"] = layers[1] - layers[0], len(block_ids)
+    if d.get("scales") is not None:
+        nd["scales"] = np.asarray(d["scales"])[layers[0]:layers[1]]
+    return a, nd
+
+
+def sample_parity(w: Workload, layers, req, p_ranks, d_ranks, dst_pool_of=None):
+    """Oracle check of the measured buffers on a sample: request `req`, layers [lb, le),
+    the given ranks.  Returns (ok, detail)."""
+    from oracle import o1
+    dst_pool_of = dst_pool_of or (lambda q: w.dst_pools[q])
+    c = w.cfg
+    st, dt = w.src_tables[req], w.dst_tables[req]
+    src_lays, src_pools = [], []
+    for p in p_ranks:
+        a, nd = extract(w.src_pools[p], w.src_dicts[p], layers, st)
+        src_lays.append(nd)
+        src_pools.append(a)
+    dst_lays, dst_pools, got = [], [], []
+    for q in d_ranks:
+        g, nd = extract(dst_pool_of(q), w.dst_dicts[q], layers, dt)
+        dst_lays.append(nd)
+        got.append(g)
+        dst_pools.append(np.full_like(g, 0).view(np.uint8).copy().view(g.dtype))
+        dst_pools[-1][:] = np.frombuffer(bytes([synth.CANARY]) * g.nbytes, dtype=g.dtype)
+    o1.convert(src_lays, src_pools, dst_lays, dst_pools, [c.n_tokens[req]], [list(range(len(st)))],
+               [list(range(len(dt)))])
+    bad = 0
+    maxulp = 0
+    for g, want in zip(got, dst_pools):
+        if c.dst_dtype == synth.E4M3:
+            def ordv(x):
+                x = x.astype(np.int32)
+                return np.where(x & 0x80, -(x & 0x7F), x & 0x7F)
+            dd = np.abs(ordv(g) - ordv(want))
+            maxulp = max(maxulp, int(dd.max(initial=0)))
+            bad += int((dd > 1).sum())
+        else:
+            bad += int((g != want).sum())
+    n = sum(g.size for g in got)
+    return bad == 0, {"elements": int(n), "mismatches": bad, "max_e4m3_ulp": maxulp if c.dst_dtype == synth.E4M3 else None,
+                      "sample": f"request {req}, layers [{layers[0]},{layers[1]}), P ranks {list(p_ranks)} -> D ranks {list(d_ranks)}"}
+
+
+def cpu_baseline(cfg, layers, p_ranks, d_ranks, req=0):
+    """Time the oracle O1 (as it stands, single thread) on a bounded sample of the workload."""
+    from oracle import o1
+    from tests.kvcase import make_case
+    case = make_case(layers, cfg.H, cfg.D, cfg.tp_p, cfg.tp_d, cfg.B_p, cfg.B_d, [cfg.n_tokens[req]], cfg.src_dtype,
+                     cfg.dst_dtype, cfg.p_order, cfg.d_order, seed=cfg.seed, scales="pow2", tail_garbage=False)
+    src_l = [case["src_lays"][p] for p in p_ranks]
+    src_p = [case["src_pools"][p] for p in p_ranks]
+    dst_l = [case["dst_lays"][q] for q in d_ranks]
+    dst_p = [case["dst_pools"][q] for q in d_ranks]
+    t0 = time.perf_counter()
+    o1.convert(src_l, src_p, dst_l, dst_p, case["n_tokens"], case["src_tables"], case["dst_tables"])
+    dt = time.perf_counter() - t0
+    nbytes = 2 * layers * (cfg.H // cfg.tp_p) * len(p_ranks) * cfg.D * cfg.n_tokens[req] * synth.NBYTES[cfg.src_dtype]
+    return nbytes, dt
+
+
+# ------------------------------------------------------------------------------------
+# N = 1: c2 on one GPU (HBM-bound fused convert)
+# ------------------------------------------------------------------------------------
+def run_single(args):
+    import torch
+    import paper_2509_17542_b200 as kvx
+    torch.cuda.set_device(0)
+    cfgs = synth.configs()
+    wl_name = args.workload or "c2"
+    cfg = cfgs[wl_name]
+    dev = torch.device("cuda", 0)
+    w = Workload(cfg, range(cfg.tp_p), range(cfg.tp_d), dev)
+    S = [w.src_lays[p] for p in w.p_ranks]
+    SP = [w.src_pools[p] for p in w.p_ranks]
+    Dl = [w.dst_lays[q] for q in w.d_ranks]
+    DP = [w.dst_pools[q] for q in w.d_ranks]
+    stream = torch.cuda.current_stream()
+    lc = args.layer_chunk or cfg.L
+
+    def step(ev=None):
+        for l0 in range(0, cfg.L, lc):
+            if ev is not None:
+                ev[0].record(stream)
+            kvx.convert_reshard(S, SP, w.src_bt, Dl, DP, w.dst_bt, (l0, min(cfg.L, l0 + lc)), stream)
+            if ev is not None:
+                ev[1].record(stream)
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    K = args.steps
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(0)
+    clocks.start()
+    kvx.launch_count_reset()
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for i in range(K):
+        step(kev[i] if lc == cfg.L else None)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = kvx.launch_count()
+    clk = clocks.stop()
+    total_ms = t0.elapsed_time(t1)
+    ms = total_ms / K
+    src_b, dst_b = w.src_bytes(), w.dst_bytes()
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev) if lc == cfg.L else ms
+    peaks = load_peaks()
+    alg = src_b + dst_b  # HBM read + write per launch
+    achieved = alg / (kern_ms * 1e-3) / 1e9
+    out = {
+        "metric": METRIC, "value": round(src_b / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+        "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 5),
+        "ms_per_request": round(ms / len(cfg.n_tokens), 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype_name(cfg),
+        "data": "synthetic (seeded random finite bit patterns, Fisher-Yates block tables)",
+        "config": {"workload": f"{wl_name} one GPU: {cfg.note}; all P and D ranks' pools on cuda:0",
+                   "requests": len(cfg.n_tokens), "tokens": cfg.total_tokens,
+                   "layout": "P (L,KV,BLK,SLOT,H,D) -> D (BLK,L,KV,H,SLOT,D)",
+                   "src_bytes_per_step": src_b, "dst_bytes_per_step": dst_b,
+                   "l2": "inputs larger than L2 (no flush)", "parallelism": "none (1 GPU)"},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _traffic(wl_name, 1),
+                     "kernel": "k_convert", "kernel_ms": round(kern_ms, 5),
+                     "algorithmic_bytes_per_launch": alg, "peak_source": peaks["source"],
+                     "frac_vs_nominal_8TBs": round(achieved / 8000.0, 4)},
+        "clocks": clk, "gpu_launches": int(launches),
+    }
+    if not args.no_parity:
+        ok, det = sample_parity(w, (0, min(2, cfg.L)), 0, w.p_ranks, w.d_ranks)
+        out["parity"] = {"ok": ok, **det}
+    if not args.no_e2e:
+        out["e2e"] = e2e_single(w, S, Dl, min(K, 5), stream, src_b)
+    if not args.no_cpu_baseline:
+        nl = args.cpu_sample_layers or min(cfg.L, 12)
+        nb, dt = cpu_baseline(cfg, nl, w.p_ranks, w.d_ranks)
+        out["cpu_baseline"] = {"value": round(nb / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                               "sample": f"O1 (plain C, 1 thread) on {wl_name} request 0, layers [0,{nl}) of {cfg.L}, "
+                                         f"{nb} source bytes in {dt:.2f} s"}
+    print(json.dumps(out), flush=True)
+
+
+def e2e_single(w, S, Dl, K, stream, src_b):
+    """Same metric through the public API with HOST buffers: H2D of the source pools from
+    pinned memory, the convert call, D2H of the destination pool, all inside the timed region."""
+    import torch
+    import paper_2509_17542_b200 as kvx
+    hs = [w.src_pools[p].cpu().pin_memory() for p in w.p_ranks]
+    hd = [torch.empty_like(w.dst_pools[q], device="cpu").pin_memory() for q in w.d_ranks]
+    DP = [w.dst_pools[q] for q in w.d_ranks]
+    SP = [w.src_pools[p] for p in w.p_ranks]
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(K):
+        for d, h in zip(SP, hs):
+            d.copy_(h, non_blocking=True)
+        kvx.convert_reshard(S, SP, w.src_bt, Dl, DP, w.dst_bt, None, stream)
+        for d, h in zip(DP, hd):
+            h.copy_(d, non_blocking=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / K
+    return {"value": round(src_b / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": int(sum(h.numel() for h in hs)), "d2h_bytes_per_step": int(sum(h.numel() for h in hd)),
+            "steps": K}
+
+
+def _dtype_name(cfg):
+    a, b = synth.DTYPE_NAMES[cfg.src_dtype], synth.DTYPE_NAMES[cfg.dst_dtype]
+    return a if a == b else f"{a}->{b}"
+
+
+def _traffic(workload, n):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(f"{workload}@{n}")
+    return None
+
+
+# ------------------------------------------------------------------------------------
+# N >= 2: c4 pairs across NVLink
+# ------------------------------------------------------------------------------------
+def run_multi(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2509_17542_b200 as kvx
+    from paper_2509_17542_b200 import transfer as tr
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    wl_name = args.workload or "c4"
+    cfg = synth.configs()[wl_name]
+    if world % 2:
+        raise SystemExit("bench.py multi-GPU needs an even number of GPUs (P and D halves)")
+    npair = world // 2
+    roles = tr.roles(world, npair, npair)
+    me = roles[rank]
+    p_ranks = list(range(npair))
+    pairs = tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks=set(p_ranks), d_ranks=set(range(npair)))
+    mine_p = [me.tp_rank] if me.kind == "P" else []
+    mine_d = [me.tp_rank] if me.kind == "D" else []
+    w = Workload(cfg, mine_p, mine_d, dev)
+    stream = torch.cuda.current_stream()
+    barrier_t = torch.zeros(1, device=dev)
+
+    def barrier():
+        dist.all_reduce(barrier_t)
+
+    flag = torch.zeros(4, dtype=torch.int32, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    epoch = [0]
+    lc = args.layer_chunk or cfg.L
+    if args.mode == "push":
+        ch = tr.PushChannel(me, w.dst_pools.get(me.tp_rank), flag if me.kind == "D" else None)
+        my_pairs = [(p, q) for p, q, _, _ in pairs if me.kind == "P" and p == me.tp_rank]
+        dst_lays = {q: kvx.Layout.from_dict(
+            synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, w.NB_d, cfg.dst_dtype, cfg.d_order,
+                         np.ones((1,), np.float32)),
+            torch.from_numpy(synth.pow2_scales(cfg.seed + 200 + q, cfg.L, cfg.H // cfg.tp_d)).to(dev))
+            for _, q in my_pairs}
+
+        def step(ev=None):
+            epoch[0] += 1
+            if me.kind == "P":
+                if ev is not None:
+                    ev[0].record(stream)
+                tr.push_step(w.src_lays[me.tp_rank], w.src_pools[me.tp_rank], w.src_bt, dst_lays, ch.peer_pool,
+                             w.dst_bt, ch.peer_flag, epoch[0], lc, stream)
+                if ev is not None:
+                    ev[1].record(stream)
+            else:
+                kvx.wait(flag, epoch[0], err, 30.0, stream)
+    else:
+        raise SystemExit("--mode nccl: see run_multi_nccl")
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    K = args.steps
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(local)
+    clocks.start()
+    kvx.launch_count_reset()
+    barrier()
+    t0.record(stream)
+    for i in range(K):
+        step(kev[i])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = kvx.launch_count()
+    clk = clocks.stop()
+    barrier()
+    my_ms = t0.elapsed_time(t1)
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev) if me.kind == "P" else 0.0
+    if int(err.item()):
+        raise SystemExit(f"rank {rank}: flag wait timed out")
+    stats = torch.tensor([my_ms, kern_ms, float(launches)], device=dev, dtype=torch.float64)
+    allst = [torch.zeros_like(stats) for _ in range(world)]
+    dist.all_gather(allst, stats)
+    allst = [s.tolist() for s in allst]
+    parity = None
+    if not args.no_parity:
+        # D ranks check their own pool on a sample against the oracle (inputs regenerated
+        # from the same seeds on the D rank's GPU)
+        parity = parity_multi(args, cfg, w, me, dev)
+    allpar = tr.exchange(parity)
+    if rank == 0:
+        max_ms = max(s[0] for s in allst)
+        ms = max_ms / K
+        kms = statistics.mean(s[1] for s in allst[:npair])
+        src_b = w.src_bytes(range(npair))
+        nvl_b = w.dst_bytes(range(1)) if cfg.tp_p == cfg.tp_d else None
+        achieved = nvl_b / (kms * 1e-3) / 1e9
+        out = {
+            "metric": METRIC, "value": round(src_b / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "ms_per_request": round(ms / len(cfg.n_tokens), 5), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": _dtype_name(cfg),
+            "data": "synthetic (seeded random finite bit patterns, Fisher-Yates block tables, pow2 fp8 scales)",
+            "config": {"workload": f"{wl_name} pairs: {cfg.note}; {npair} (P rank p -> D rank p) pair(s), "
+                                   f"P on GPUs 0..{npair - 1}, D on GPUs {npair}..{world - 1}"
+                                   + (" (full c4)" if npair == 4 else " (per-GPU-equivalent sub-config)"),
+                       "mode": args.mode, "layer_chunk": lc, "requests": len(cfg.n_tokens),
+                       "tokens": cfg.total_tokens, "src_bytes_per_step": src_b,
+                       "nvlink_bytes_per_pair_per_step": nvl_b, "l2": "inputs larger than L2 (no flush)",
+                       "parallelism": f"P TP{cfg.tp_p} x D TP{cfg.tp_d}, {npair} pair(s)"},
+            "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED_GBS,
+                         "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED_GBS, 4),
+                         "traffic": _traffic(wl_name, world), "kernel": "k_convert (peer-store push)",
+                         "kernel_ms": round(kms, 4), "algorithmic_bytes_per_launch": nvl_b,
+                         "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)",
+                         "frac_vs_nominal_900": round(achieved / NVLINK_NOMINAL_GBS, 4)},
+            "clocks": clk, "gpu_launches": int(sum(s[2] for s in allst)),
+            "parity": [p for p in allpar if p is not None],
+        }
+        print(json.dumps(out), flush=True)
+    barrier()
+    dist.destroy_process_group()
+
+
+def parity_multi(args, cfg, w, me, dev):
+    if me.kind != "D":
+        return None
+    q = me.tp_rank
+    p = q  # identity pairing (tp_p == tp_d)
+    src = Workload.__new__(Workload)
+    # regenerate P rank p's pool from its seed on this GPU (same generator, same seed)
+    import torch
+    import paper_2509_17542_b200 as kvx
+    d = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, w.NB_p, cfg.src_dtype, cfg.p_order)
+    lay = kvx.Layout.from_dict(d)
+    pool = lay.new_pool(dev)
+    view = pool.view(torch.uint8 if synth.NBYTES[cfg.src_dtype] == 1 else torch.int16)
+    synth.fill_random_finite_(view, cfg.seed + 100 + p, cfg.src_dtype)
+    w.src_dicts[p], w.src_pools[p] = d, pool
+    ok, det = sample_parity(w, (0, 2), 0, [p], [q])
+    det["rank"] = f"D{q}"
+    del w.src_pools[p]
+    return {"ok": ok, **det}
+
+
+# ------------------------------------------------------------------------------------
+# reference arm: the oracle on the host cores
+# ------------------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg = synth.configs()[args.workload or ("c2" if world == 1 else "c4")]
+    nl = args.cpu_sample_layers or 2
+    p_ranks = list(range(cfg.tp_p)) if world == 1 else [0]
+    d_ranks = list(range(cfg.tp_d)) if world == 1 else [0]
+    for _ in range(max(args.warmup, 0)):
+        cpu_baseline(cfg, 1, p_ranks, d_ranks)
+    tot_b, tot_t = 0, 0.0
+    for _ in range(args.steps):
+        b, t = cpu_baseline(cfg, nl, p_ranks, d_ranks)
+        tot_b += b
+        tot_t += t
+    v = tot_b / tot_t / 1e9
+    sample = (f"O1 (plain C, 1 thread) per step: {cfg.name} request 0, layers [0,{nl}) of {cfg.L}, "
+              f"P ranks {p_ranks} -> D ranks {d_ranks}")
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "GB/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_t / args.steps * 1e3, 2),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype_name(cfg),
+           "data": "synthetic", "config": {"workload": f"{cfg.name}: {cfg.note} (oracle on host, bounded sample)"},
+           "cpu_baseline": {"value": round(v, 5), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": round(v, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        return run_multi(args)
+    return run_single(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,233 @@
+/*
+ * kvx.h -- C ABI of the B200-native heterogeneous-compatible KV transmission path
+ * (arXiv 2509.17542, "Disaggregated Prefill and Decoding Inference System for LLM
+ * Serving on Multi-Vendor GPUs", section III-B).
+ *
+ * The path: gather a finished prefill's paged KV blocks, convert them from the
+ * prefill (P) instance's layout (block size, axis order, dtype, TP sharding of
+ * KV heads) to the decode (D) instance's, and deliver them into D's paged KV pool
+ * (on the same GPU, or across NVLink).  Passages (PAPER.md line, section):
+ *   P:109  III-B1 transfer engine read(local addr, remote addr, remote location)
+ *   P:113  III-B2 VRAM management alignment: block size + tensor layout, flatten
+ *          to 1-D before transmission, restore "according to the demand of D"
+ *   P:125  III-B3 parallel strategy alignment (Fig. 4): TP merge / split
+ *   P:65   I     precision alignment component (semantics: DESIGN.md readings)
+ *   P:289  V     by-layer transmission (per-layer pipelining)
+ *
+ * Conventions (all calls):
+ *   - Ownership: the caller owns every device buffer (pools, tables, wire and
+ *     scratch).  Hot calls allocate no device memory.  Handles hold host
+ *     metadata only.
+ *   - Asynchrony: calls validate synchronously, then enqueue on `stream` (a
+ *     cudaStream_t passed as void*; NULL = legacy default stream) and return
+ *     before device work completes.  Buffers must outlive the stream work.
+ *   - Errors: a kv_status; the message of the last failure on the calling thread
+ *     is kv_last_error().  Validation fails before anything is enqueued (no
+ *     partial work).  Asynchronous CUDA/NCCL errors surface on a later call.
+ *   - No exception crosses the ABI.  Calls on distinct streams and handles are
+ *     thread-safe.
+ *   - Device pointers may be local or peer-mapped (kv_ipc_open, or peer access):
+ *     a destination pool on another GPU turns kv_convert_reshard into the fused
+ *     gather + convert + NVLink push (P-side push, D-controlled placement).
+ */
+#ifndef KVX_H_
+#define KVX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KV_OK = 0,
+  KV_EINVAL = 1,        /* bad argument (null pointer, bad enum, bad range) */
+  KV_ESHAPE = 2,        /* tp does not divide heads, pool/table/buffer too small, bad block id */
+  KV_EUNSUPPORTED = 3,  /* valid but not implemented (e.g. pipeline-parallel mismatch) */
+  KV_ECUDA = 4,         /* CUDA runtime error (message has the CUDA string) */
+  KV_ENCCL = 5,         /* NCCL error */
+  KV_ETIMEOUT = 6       /* flag wait timed out */
+} kv_status;
+
+/* Element types.  KV_F8E4M3 is OCP e4m3fn (max 448, no Inf, NaN = S.1111.111). */
+typedef enum { KV_F16 = 0, KV_BF16 = 1, KV_F8E4M3 = 2, KV_F32 = 3 } kv_dtype;
+
+/* Physical axes of a paged KV pool; extents (L, 2, num_blocks, block_size, H/tp, head_dim). */
+typedef enum {
+  KV_AX_LAYER = 0, KV_AX_KV = 1, KV_AX_BLOCK = 2, KV_AX_SLOT = 3, KV_AX_HEAD = 4, KV_AX_DIM = 5
+} kv_axis;
+
+typedef void* kv_stream; /* cudaStream_t */
+
+/* One TP rank's pool layout ("block size of page attention and the layout of
+ * tensor data").  The rank owns global KV heads
+ * [tp_rank*H/tp_degree, (tp_rank+1)*H/tp_degree) (head-contiguous TP). */
+typedef struct {
+  int32_t num_layers;    /* L */
+  int32_t num_kv_heads;  /* global H */
+  int32_t head_dim;      /* D */
+  int32_t tp_degree;
+  int32_t tp_rank;
+  int32_t block_size;    /* tokens per page-attention block */
+  int32_t num_blocks;    /* pool capacity in blocks */
+  int32_t dtype;         /* kv_dtype */
+  int32_t axis_order[6]; /* kv_axis, outermost -> innermost; the pool is dense row-major in it */
+  const float* scales;   /* KV_F8E4M3 only: DEVICE fp32 [L][2][H/tp] dequant scales s
+                          * (real value = code * s); NULL for other dtypes */
+} kv_layout_desc;
+
+typedef struct kv_layout kv_layout; /* opaque, immutable after describe */
+
+/* A batch of requests' block tables for one instance (one table per request,
+ * shared by all TP ranks of the instance).  All pointers are DEVICE pointers into
+ * the caller's buffer, filled by kv_block_table_update; the scalars are host copies. */
+typedef struct {
+  int32_t n_req;
+  int32_t block_size;      /* of the layout the tables were validated against */
+  int32_t num_blocks;      /* pool capacity the ids were validated against */
+  int32_t max_tokens;      /* max_r T_r */
+  int64_t total_tokens;    /* sum_r T_r */
+  int64_t total_blocks;    /* sum_r ceil(T_r / block_size) */
+  uint64_t token_digest;   /* FNV-1a of the T_r list: the P and D tables of one transfer must agree */
+  const int32_t* tok_off;  /* [n_req + 1] prefix sum of T_r */
+  const int32_t* blk_off;  /* [n_req + 1] prefix sum of ceil(T_r / block_size) */
+  const int32_t* blk_ids;  /* [total_blocks] physical block ids, request-major */
+  const int32_t* blk_req;  /* [total_blocks] request index of each table entry */
+  const int32_t* tok_req;  /* [total_tokens] request index of each token (batch order) */
+} kv_batch;
+
+/* ---- A1: layout ------------------------------------------------------------ */
+
+/* Validate `desc` and derive strides.  *pool_bytes = 2*L*num_blocks*block_size*(H/tp)*D*bytes.
+ * KV_ESHAPE if tp_degree does not divide num_kv_heads or tp_rank >= tp_degree;
+ * KV_EINVAL on a non-permutation axis_order, bad dtype, non-positive extent, or
+ * scales == NULL for KV_F8E4M3.  *out must be released with kv_layout_destroy. */
+kv_status kv_layout_describe(const kv_layout_desc* desc, kv_layout** out, size_t* pool_bytes);
+void kv_layout_destroy(kv_layout* lay);
+
+/* ---- A3: block tables ------------------------------------------------------- */
+
+/* Device bytes kv_block_table_update needs for a batch of this size. */
+size_t kv_batch_bytes(int32_t n_req, int64_t total_blocks, int64_t total_tokens);
+
+/* Validate one instance's block tables and upload them (D picks its
+ * blocks and tells P through the control plane).  host_n_tokens[n_req] are T_r >= 0;
+ * host_block_ids holds, request after request, exactly ceil(T_r/B) ids each (n_ids in
+ * total).  Errors (nothing enqueued): KV_ESHAPE if n_ids != sum ceil(T_r/B), an id is
+ * outside [0, num_blocks) or appears twice, or dev_buf_bytes < kv_batch_bytes(...);
+ * KV_EINVAL on null pointers.  Host arrays may be freed on return; dev_buf (caller-owned,
+ * 16-byte aligned) must outlive every use of *out. */
+kv_status kv_block_table_update(const kv_layout* lay, int32_t n_req, const int32_t* host_n_tokens,
+                                const int32_t* host_block_ids, int64_t n_ids, void* dev_buf,
+                                size_t dev_buf_bytes, kv_batch* out, kv_stream stream);
+
+/* ---- A2: re-shard plan ------------------------------------------------------- */
+
+/* Pairs (p, q) whose head ranges overlap (Fig. 4): writes up to max_pairs
+ * entries {p, q, h_begin, h_end} (global heads) to out[4*i..4*i+3] and returns the pair
+ * count, or -1 if a degree does not divide num_kv_heads. */
+int32_t kv_plan_pairs(int32_t tp_p, int32_t tp_d, int32_t num_kv_heads, int32_t* out, int32_t max_pairs);
+
+/* ---- A4-A9: fused convert ------------------------------------------------------ */
+
+/* Pool -> pool conversion of every request in the batch for layers [layer_begin,
+ * layer_end): gather from the P ranks' pools, TP merge/split by head range (A7),
+ * permute to D's axis order and block size, cast (A6), scatter into the D ranks' pools,
+ * zero-fill the tail slots of each request's last D block.  Nothing else
+ * in any D pool is written; P tail slots are never read.
+ *   src[n_src]: P layouts (same model/desc except tp_rank and scales); src_pools[i] is
+ *     the DEVICE pool of src[i].  Every P rank whose heads overlap a listed D rank must
+ *     be present (KV_ESHAPE otherwise).
+ *   dst[n_dst], dst_pools[n_dst]: D layouts / DEVICE pools (may be peer-mapped: the
+ *     kernel stores across NVLink -- the fused P-side push).
+ *   src_bt / dst_bt: the two instances' tables for the same requests (same n_req and
+ *     T_r), validated against src[0] / dst[0].
+ * Casts: same dtype = bit copy; fp16<->bf16/fp32 IEEE RNE (NaN -> 0x7FFF); to e4m3
+ * q = satfinite_RNE(RN_f32(f32(x) * RN_f32(1/s))) with s = dst scale of (l, c, D-local
+ * head); from e4m3 RN_f32(f32(q) * s_src) then RNE.  n_src, n_dst <= 16. */
+kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                             const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst,
+                             void* const* dst_pools, const kv_batch* dst_bt, int32_t layer_begin,
+                             int32_t layer_end, kv_stream stream);
+
+/* ---- A5 / A9: wire format (Fig. 5 flatten / restore) ----------------------------- */
+
+/* Wire dtype of a (src, dst) pair: the narrower of the two (dst on a tie), so a
+ * narrowing cast happens on the sender and a widening one on the receiver. */
+int32_t kv_wire_dtype(const kv_layout* src, const kv_layout* dst);
+
+/* Bytes of the (src rank -> dst rank) wire buffer for `total_tokens` tokens and layers
+ * [layer_begin, layer_end): 2 * (layer_end-layer_begin) * |head overlap| * total_tokens
+ * * D * bytes(wire dtype) (the KV size formula).  0 if the ranks do not overlap. */
+size_t kv_wire_bytes(const kv_layout* src, const kv_layout* dst, int64_t total_tokens, int32_t layer_begin,
+                     int32_t layer_end);
+
+/* Gather + (narrowing) cast into the wire buffer, canonical order (layer, kv, head in
+ * overlap, token, dim), tokens of all requests concatenated in batch order ("a
+ * one-dimensional tensor before transmission").  wire is DEVICE memory of at least
+ * kv_wire_bytes(...) bytes, 16-byte aligned.  KV_ESHAPE if the ranks do not overlap or
+ * wire_bytes is short. */
+kv_status kv_pack(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, const kv_layout* dst,
+                  int32_t layer_begin, int32_t layer_end, void* wire, size_t wire_bytes, kv_stream stream);
+
+/* Restore ("converts the one-dimensional tensor into the required memory layout
+ * after transmission"): scatter a wire buffer produced by kv_pack(src -> dst) into the D
+ * pool (+ widening cast), zero-filling tail slots of the overlap heads. */
+kv_status kv_unpack(const kv_layout* src, const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt,
+                    int32_t layer_begin, int32_t layer_end, const void* wire, size_t wire_bytes,
+                    kv_stream stream);
+
+/* ---- A8: transport over NVLink ------------------------------------------------- */
+
+typedef struct kv_comm kv_comm; /* an NCCL communicator owned by the library */
+
+/* NCCL unique id (128 bytes) created on one rank and shared through the caller's
+ * control plane (e.g. torch.distributed store). */
+kv_status kv_comm_unique_id(uint8_t out_id[128]);
+kv_status kv_comm_init(int32_t nranks, int32_t rank, const uint8_t id[128], int32_t device, kv_comm** out);
+void kv_comm_destroy(kv_comm* comm);
+kv_status kv_comm_group_start(void);
+kv_status kv_comm_group_end(void);
+
+/* Point-to-point byte transfer of a packed wire buffer (ncclSend / ncclRecv over
+ * NVLink).  Matching calls on the two ranks must use the same byte count. */
+kv_status kv_send(kv_comm* comm, int32_t peer, const void* wire, size_t bytes, kv_stream stream);
+kv_status kv_recv(kv_comm* comm, int32_t peer, void* wire, size_t bytes, kv_stream stream);
+
+/* kv_recv into wire_scratch followed by kv_unpack on the same stream. */
+kv_status kv_recv_unpack(kv_comm* comm, int32_t peer, void* wire_scratch, size_t bytes, const kv_layout* src,
+                         const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt, int32_t layer_begin,
+                         int32_t layer_end, kv_stream stream);
+
+/* CUDA IPC for the direct-store (push) mode.  kv_ipc_export writes the 64-byte handle of
+ * the allocation containing dev_ptr and dev_ptr's offset inside it; kv_ipc_open maps it in
+ * this process (the current device must have peer access to the owner) and returns the
+ * peer-mapped address of the original pointer.  kv_ipc_close(base) unmaps (base =
+ * returned pointer - offset). */
+kv_status kv_ipc_export(const void* dev_ptr, uint8_t out_handle[64], uint64_t* out_offset);
+kv_status kv_ipc_open(const uint8_t handle[64], uint64_t offset, void** out_ptr);
+kv_status kv_ipc_close(void* mapped_base);
+
+/* A11 completion.  kv_signal: after all prior work on `stream`, a system-scope release
+ * store of `value` to *flag (local or peer-mapped 4-byte device word).  kv_wait: enqueue
+ * a one-warp kernel that spins (acquire, system scope) until *flag >= value or timeout_ns
+ * elapses; on timeout it sets *err = 1 (device int32) and returns.  Do not place a kv_wait
+ * and the kv_signal it waits for on the same GPU. */
+kv_status kv_signal(uint32_t* flag, uint32_t value, kv_stream stream);
+kv_status kv_wait(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, int32_t* err, kv_stream stream);
+
+/* ---- misc ------------------------------------------------------------------------- */
+
+/* Number of device kernels this library launched on the calling thread since the last
+ * call to kv_launch_count_reset (for the bench's gpu_launches field). */
+uint64_t kv_launch_count(void);
+void kv_launch_count_reset(void);
+
+const char* kv_last_error(void); /* thread-local, valid until the next failing call */
+const char* kv_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVX_H_ */

@@ -1,0 +1,101 @@
+"""Thin ctypes binding of libkvx.so (include/kvx.h).  Argument marshalling only: every
+step of the data path runs in the library's CUDA kernels.  There is no CPU fallback --
+if the shared library is missing or fails to load, importing this module raises.
+
+PyTorch is used only for device memory (pools, tables, wire buffers are torch tensors
+whose data_ptr() is passed through), streams (``torch.cuda.current_stream().cuda_stream``)
+and, in ``transfer.py``, process groups for the control plane.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libkvx.so")
+
+KV_OK, KV_EINVAL, KV_ESHAPE, KV_EUNSUPPORTED, KV_ECUDA, KV_ENCCL, KV_ETIMEOUT = range(7)
+STATUS_NAMES = ["KV_OK", "KV_EINVAL", "KV_ESHAPE", "KV_EUNSUPPORTED", "KV_ECUDA", "KV_ENCCL", "KV_ETIMEOUT"]
+KV_F16, KV_BF16, KV_F8E4M3, KV_F32 = range(4)
+AX_LAYER, AX_KV, AX_BLOCK, AX_SLOT, AX_HEAD, AX_DIM = range(6)
+DTYPE_BYTES = {KV_F16: 2, KV_BF16: 2, KV_F8E4M3: 1, KV_F32: 4}
+
+
+class KvError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 7 else status}: {msg}")
+        self.status = status
+
+
+class LayoutDesc(C.Structure):
+    _fields_ = [("num_layers", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("tp_degree", C.c_int32), ("tp_rank", C.c_int32), ("block_size", C.c_int32),
+                ("num_blocks", C.c_int32), ("dtype", C.c_int32), ("axis_order", C.c_int32 * 6),
+                ("scales", C.c_void_p)]
+
+
+class Batch_t(C.Structure):
+    _fields_ = [("n_req", C.c_int32), ("block_size", C.c_int32), ("num_blocks", C.c_int32),
+                ("max_tokens", C.c_int32), ("total_tokens", C.c_int64), ("total_blocks", C.c_int64),
+                ("token_digest", C.c_uint64),
+                ("tok_off", C.c_void_p), ("blk_off", C.c_void_p), ("blk_ids", C.c_void_p),
+                ("blk_req", C.c_void_p), ("tok_req", C.c_void_p)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    import torch  # noqa: F401  -- load torch's libnccl.so.2 first (same soname)
+    lib = C.CDLL(LIB_PATH, mode=C.RTLD_GLOBAL)
+    i32, i64, u64, p, st = C.c_int32, C.c_int64, C.c_uint64, C.c_void_p, C.c_int
+    pp = C.POINTER(C.c_void_p)
+    sig = {
+        "kv_layout_describe": (st, [C.POINTER(LayoutDesc), C.POINTER(p), C.POINTER(C.c_size_t)]),
+        "kv_layout_destroy": (None, [p]),
+        "kv_batch_bytes": (C.c_size_t, [i32, i64, i64]),
+        "kv_block_table_update": (st, [p, i32, p, p, i64, p, C.c_size_t, C.POINTER(Batch_t), p]),
+        "kv_plan_pairs": (i32, [i32, i32, i32, C.POINTER(i32), i32]),
+        "kv_convert_reshard": (st, [i32, pp, pp, C.POINTER(Batch_t), i32, pp, pp, C.POINTER(Batch_t), i32, i32, p]),
+        "kv_wire_dtype": (i32, [p, p]),
+        "kv_wire_bytes": (C.c_size_t, [p, p, i64, i32, i32]),
+        "kv_pack": (st, [p, p, C.POINTER(Batch_t), p, i32, i32, p, C.c_size_t, p]),
+        "kv_unpack": (st, [p, p, p, C.POINTER(Batch_t), i32, i32, p, C.c_size_t, p]),
+        "kv_comm_unique_id": (st, [p]),
+        "kv_comm_init": (st, [i32, i32, p, i32, C.POINTER(p)]),
+        "kv_comm_destroy": (None, [p]),
+        "kv_comm_group_start": (st, []),
+        "kv_comm_group_end": (st, []),
+        "kv_send": (st, [p, i32, p, C.c_size_t, p]),
+        "kv_recv": (st, [p, i32, p, C.c_size_t, p]),
+        "kv_recv_unpack": (st, [p, i32, p, C.c_size_t, p, p, p, C.POINTER(Batch_t), i32, i32, p]),
+        "kv_ipc_export": (st, [p, p, C.POINTER(u64)]),
+        "kv_ipc_open": (st, [p, u64, C.POINTER(p)]),
+        "kv_ipc_close": (st, [p]),
+        "kv_signal": (st, [p, C.c_uint32, p]),
+        "kv_wait": (st, [p, C.c_uint32, u64, p, p]),
+        "kv_launch_count": (u64, []),
+        "kv_launch_count_reset": (None, []),
+        "kv_last_error": (C.c_char_p, []),
+        "kv_version": (C.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype = res
+        f.argtypes = args
+    return lib
+
+
+lib = _load()
+
+# Every symbol include/kvx.h declares (checked by tests/test_abi.py).
+EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_block_table_update", "kv_plan_pairs",
+           "kv_convert_reshard", "kv_wire_dtype", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
+           "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
+           "kv_recv_unpack", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_signal", "kv_wait",
+           "kv_launch_count", "kv_launch_count_reset", "kv_last_error", "kv_version")
+
+
+def check(status):
+    if status != KV_OK:
+        raise KvError(status, lib.kv_last_error().decode())

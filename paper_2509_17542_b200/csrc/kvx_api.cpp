@@ -1,0 +1,502 @@
+// Host side of the C ABI (include/kvx.h): validation, strides, block tables, re-shard
+// planning and kernel dispatch.  Every step of the data path runs in the kernels of
+// kvx_kernels.cu; this file only checks arguments and marshals them.
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "kvx_internal.h"
+
+namespace kvx {
+
+static thread_local std::string t_err;
+std::atomic<uint64_t> g_launches{0};
+
+kv_status fail(kv_status st, const std::string& msg) {
+  t_err = msg;
+  return st;
+}
+
+kv_status cuda_fail(cudaError_t e, const char* what) {
+  t_err = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return KV_ECUDA;
+}
+
+int32_t dtype_bytes(int32_t dt) {
+  switch (dt) {
+    case KV_F16:
+    case KV_BF16: return 2;
+    case KV_F8E4M3: return 1;
+    case KV_F32: return 4;
+  }
+  return 0;
+}
+
+FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0, 0};
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  f.shr = l;
+  f.mul = (uint32_t)((((1ull << 32) * ((1ull << l) - d)) / d) + 1);
+  return f;
+}
+
+}  // namespace kvx
+
+using namespace kvx;
+
+namespace {
+
+bool ptr_aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
+
+// Two layouts describe the same instance (same model, blocks, order, dtype, tp degree).
+bool same_instance(const kv_layout* a, const kv_layout* b) {
+  const kv_layout_desc &x = a->d, &y = b->d;
+  if (x.num_layers != y.num_layers || x.num_kv_heads != y.num_kv_heads || x.head_dim != y.head_dim ||
+      x.tp_degree != y.tp_degree || x.block_size != y.block_size || x.num_blocks != y.num_blocks ||
+      x.dtype != y.dtype)
+    return false;
+  for (int i = 0; i < 6; ++i)
+    if (x.axis_order[i] != y.axis_order[i]) return false;
+  return true;
+}
+
+kv_status check_batch(const kv_batch* bt, const kv_layout* lay, const char* name) {
+  if (!bt) return fail(KV_EINVAL, std::string(name) + " is NULL");
+  if (bt->block_size != lay->d.block_size || bt->num_blocks != lay->d.num_blocks)
+    return fail(KV_ESHAPE, std::string(name) + " was built for another block size / pool");
+  if (bt->n_req < 0 || (bt->n_req > 0 && (!bt->tok_off || !bt->blk_off || !bt->blk_ids || !bt->blk_req)))
+    return fail(KV_EINVAL, std::string(name) + " has null device arrays");
+  return KV_OK;
+}
+
+kv_status check_layers(const kv_layout* lay, int32_t lb, int32_t le) {
+  if (lb < 0 || le < lb || le > lay->d.num_layers)
+    return fail(KV_EINVAL, "layer range [" + std::to_string(lb) + ", " + std::to_string(le) + ") outside [0, " +
+                               std::to_string(lay->d.num_layers) + ")");
+  return KV_OK;
+}
+
+void head_overlap(const kv_layout* s, const kv_layout* d, int32_t* hb, int32_t* he) {
+  const int32_t H = s->d.num_kv_heads;
+  const int32_t Hp = H / s->d.tp_degree, Hd = H / d->d.tp_degree;
+  const int32_t p = s->d.tp_rank, q = d->d.tp_rank;
+  *hb = std::max(p * Hp, q * Hd);
+  *he = std::min((p + 1) * Hp, (q + 1) * Hd);
+}
+
+// The fast path needs head_dim innermost and contiguous with 8-element chunks.
+bool fast_ok(const kv_layout* lay) { return lay->stride[KV_AX_DIM] == 1 && lay->d.head_dim % 8 == 0; }
+
+kv_status same_model(const kv_layout* s, const kv_layout* d) {
+  if (s->d.num_layers != d->d.num_layers || s->d.num_kv_heads != d->d.num_kv_heads ||
+      s->d.head_dim != d->d.head_dim)
+    return fail(KV_ESHAPE, "P and D layouts describe different models (layers / kv heads / head_dim)");
+  return KV_OK;
+}
+
+kv_status scales_ok(const kv_layout* s, const kv_layout* d) {
+  // widening from e4m3 needs the source's scales; narrowing to e4m3 needs the destination's
+  if (d->d.dtype == KV_F8E4M3 && s->d.dtype != KV_F8E4M3 && !d->d.scales)
+    return fail(KV_EINVAL, "e4m3 destination without scales");
+  if (s->d.dtype == KV_F8E4M3 && d->d.dtype != KV_F8E4M3 && !s->d.scales)
+    return fail(KV_EINVAL, "e4m3 source without scales");
+  return KV_OK;
+}
+
+// slot/head order: whichever of the two is inner in the destination layout
+int32_t slot_inner_of(const kv_layout* d) {
+  int ps = 0, ph = 0;
+  for (int i = 0; i < 6; ++i) {
+    if (d->d.axis_order[i] == KV_AX_SLOT) ps = i;
+    if (d->d.axis_order[i] == KV_AX_HEAD) ph = i;
+  }
+  return ps > ph ? 1 : 0;
+}
+
+constexpr uint64_t kMaxChunks = 0x7FFFFFFFull;  // per launch (32-bit decode)
+
+}  // namespace
+
+extern "C" {
+
+const char* kv_last_error(void) { return t_err.c_str(); }
+const char* kv_version(void) { return "kvx 0.1 (sm_100a)"; }
+uint64_t kv_launch_count(void) { return g_launches.load(); }
+void kv_launch_count_reset(void) { g_launches.store(0); }
+
+kv_status kv_layout_describe(const kv_layout_desc* desc, kv_layout** out, size_t* pool_bytes) {
+  if (!desc || !out) return fail(KV_EINVAL, "kv_layout_describe: null argument");
+  const kv_layout_desc& d = *desc;
+  if (d.num_layers <= 0 || d.num_kv_heads <= 0 || d.head_dim <= 0 || d.tp_degree <= 0 || d.block_size <= 0 ||
+      d.num_blocks <= 0)
+    return fail(KV_EINVAL, "kv_layout_describe: non-positive extent");
+  if (dtype_bytes(d.dtype) == 0) return fail(KV_EINVAL, "kv_layout_describe: bad dtype");
+  if (d.num_kv_heads % d.tp_degree != 0)
+    return fail(KV_ESHAPE, "kv_layout_describe: tp_degree " + std::to_string(d.tp_degree) +
+                               " does not divide num_kv_heads " + std::to_string(d.num_kv_heads));
+  if (d.tp_rank < 0 || d.tp_rank >= d.tp_degree) return fail(KV_ESHAPE, "kv_layout_describe: tp_rank out of range");
+  bool seen[6] = {false, false, false, false, false, false};
+  for (int i = 0; i < 6; ++i) {
+    int a = d.axis_order[i];
+    if (a < 0 || a > 5 || seen[a]) return fail(KV_EINVAL, "kv_layout_describe: axis_order is not a permutation");
+    seen[a] = true;
+  }
+  if (d.dtype == KV_F8E4M3 && !d.scales) return fail(KV_EINVAL, "kv_layout_describe: e4m3 layout needs scales");
+  kv_layout* L = new (std::nothrow) kv_layout;
+  if (!L) return fail(KV_EINVAL, "kv_layout_describe: out of host memory");
+  L->d = d;
+  L->h_local = d.num_kv_heads / d.tp_degree;
+  L->elem_bytes = dtype_bytes(d.dtype);
+  L->extent[KV_AX_LAYER] = d.num_layers;
+  L->extent[KV_AX_KV] = 2;
+  L->extent[KV_AX_BLOCK] = d.num_blocks;
+  L->extent[KV_AX_SLOT] = d.block_size;
+  L->extent[KV_AX_HEAD] = L->h_local;
+  L->extent[KV_AX_DIM] = d.head_dim;
+  int64_t s = 1;
+  for (int i = 5; i >= 0; --i) {
+    L->stride[d.axis_order[i]] = s;
+    s *= L->extent[d.axis_order[i]];
+  }
+  L->pool_bytes = (size_t)s * (size_t)L->elem_bytes;
+  if (pool_bytes) *pool_bytes = L->pool_bytes;
+  *out = L;
+  return KV_OK;
+}
+
+void kv_layout_destroy(kv_layout* lay) { delete lay; }
+
+size_t kv_batch_bytes(int32_t n_req, int64_t total_blocks, int64_t total_tokens) {
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  return al(4 * (size_t)(n_req + 1)) * 2 + al(4 * (size_t)total_blocks) * 2 + al(4 * (size_t)total_tokens);
+}
+
+kv_status kv_block_table_update(const kv_layout* lay, int32_t n_req, const int32_t* host_n_tokens,
+                                const int32_t* host_block_ids, int64_t n_ids, void* dev_buf, size_t dev_buf_bytes,
+                                kv_batch* out, kv_stream stream) {
+  if (!lay || !out || n_req < 0 || (n_req > 0 && !host_n_tokens) || (n_ids > 0 && !host_block_ids))
+    return fail(KV_EINVAL, "kv_block_table_update: null argument");
+  const int32_t B = lay->d.block_size, NB = lay->d.num_blocks;
+  std::vector<int32_t> tok_off(n_req + 1), blk_off(n_req + 1);
+  int64_t tt = 0, tb = 0;
+  int32_t maxT = 0;
+  uint64_t digest = 1469598103934665603ull;
+  for (int32_t r = 0; r < n_req; ++r) {
+    const int32_t T = host_n_tokens[r];
+    if (T < 0) return fail(KV_EINVAL, "kv_block_table_update: negative token count");
+    tok_off[r] = (int32_t)tt;
+    blk_off[r] = (int32_t)tb;
+    tt += T;
+    tb += (T + B - 1) / B;
+    maxT = std::max(maxT, T);
+    for (int i = 0; i < 4; ++i) {
+      digest ^= (uint64_t)((T >> (8 * i)) & 0xFF);
+      digest *= 1099511628211ull;
+    }
+    if (tt > 0x7FFFFFFF || tb > 0x7FFFFFFF) return fail(KV_ESHAPE, "kv_block_table_update: batch too large");
+  }
+  tok_off[n_req] = (int32_t)tt;
+  blk_off[n_req] = (int32_t)tb;
+  if (tb != n_ids)
+    return fail(KV_ESHAPE, "kv_block_table_update: " + std::to_string(n_ids) + " block ids given, sum ceil(T/B) = " +
+                               std::to_string(tb));
+  std::vector<uint8_t> used((size_t)NB, 0);
+  for (int64_t i = 0; i < n_ids; ++i) {
+    const int32_t b = host_block_ids[i];
+    if (b < 0 || b >= NB)
+      return fail(KV_ESHAPE, "kv_block_table_update: block id " + std::to_string(b) + " outside [0, " +
+                                 std::to_string(NB) + ")");
+    if (used[b]) return fail(KV_ESHAPE, "kv_block_table_update: block id " + std::to_string(b) + " used twice");
+    used[b] = 1;
+  }
+  const size_t need = kv_batch_bytes(n_req, tb, tt);
+  if (!dev_buf || dev_buf_bytes < need || !ptr_aligned(dev_buf, 16))
+    return fail(KV_ESHAPE, "kv_block_table_update: device buffer of " + std::to_string(dev_buf_bytes) +
+                               " bytes is null, short or misaligned (need " + std::to_string(need) + ")");
+  // host staging image of [tok_off | blk_off | blk_ids | blk_req | tok_req], 16-B aligned parts
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  const size_t o_tok = 0, o_blk = al(4 * (size_t)(n_req + 1)), o_ids = o_blk + al(4 * (size_t)(n_req + 1)),
+               o_req = o_ids + al(4 * (size_t)tb), o_treq = o_req + al(4 * (size_t)tb);
+  std::vector<uint8_t> img(need, 0);
+  memcpy(img.data() + o_tok, tok_off.data(), 4 * (size_t)(n_req + 1));
+  memcpy(img.data() + o_blk, blk_off.data(), 4 * (size_t)(n_req + 1));
+  if (tb) memcpy(img.data() + o_ids, host_block_ids, 4 * (size_t)tb);
+  int32_t* breq = reinterpret_cast<int32_t*>(img.data() + o_req);
+  int32_t* treq = reinterpret_cast<int32_t*>(img.data() + o_treq);
+  for (int32_t r = 0; r < n_req; ++r) {
+    for (int32_t j = blk_off[r]; j < blk_off[r + 1]; ++j) breq[j] = r;
+    for (int32_t t = tok_off[r]; t < tok_off[r + 1]; ++t) treq[t] = r;
+  }
+  cudaError_t e = cudaMemcpyAsync(dev_buf, img.data(), need, cudaMemcpyHostToDevice, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_block_table_update: upload");
+  // the host image is pageable: the copy is staged before cudaMemcpyAsync returns, but make
+  // the lifetime rule trivially true by waiting for this small upload
+  e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_block_table_update: sync");
+  uint8_t* base = static_cast<uint8_t*>(dev_buf);
+  out->n_req = n_req;
+  out->block_size = B;
+  out->num_blocks = NB;
+  out->max_tokens = maxT;
+  out->total_tokens = tt;
+  out->total_blocks = tb;
+  out->token_digest = digest;
+  out->tok_off = reinterpret_cast<const int32_t*>(base + o_tok);
+  out->blk_off = reinterpret_cast<const int32_t*>(base + o_blk);
+  out->blk_ids = reinterpret_cast<const int32_t*>(base + o_ids);
+  out->blk_req = reinterpret_cast<const int32_t*>(base + o_req);
+  out->tok_req = reinterpret_cast<const int32_t*>(base + o_treq);
+  return KV_OK;
+}
+
+int32_t kv_plan_pairs(int32_t tp_p, int32_t tp_d, int32_t H, int32_t* out, int32_t max_pairs) {
+  if (tp_p <= 0 || tp_d <= 0 || H <= 0 || H % tp_p || H % tp_d) {
+    fail(KV_ESHAPE, "kv_plan_pairs: a tp degree does not divide num_kv_heads");
+    return -1;
+  }
+  const int32_t Hp = H / tp_p, Hd = H / tp_d;
+  int32_t n = 0;
+  // walk heads once; a new pair starts wherever p or q changes (head-contiguous TP)
+  int32_t cur_p = -1, cur_q = -1;
+  for (int32_t h = 0; h < H; ++h) {
+    const int32_t p = h / Hp, q = h / Hd;
+    if (p != cur_p || q != cur_q) {
+      if (out && n < max_pairs) {
+        out[4 * n + 0] = p;
+        out[4 * n + 1] = q;
+        out[4 * n + 2] = h;
+      }
+      if (out && n > 0 && n - 1 < max_pairs) out[4 * (n - 1) + 3] = h;
+      ++n;
+      cur_p = p;
+      cur_q = q;
+    }
+  }
+  if (out && n > 0 && n - 1 < max_pairs) out[4 * (n - 1) + 3] = H;
+  return n;
+}
+
+kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                             const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst,
+                             void* const* dst_pools, const kv_batch* dst_bt, int32_t lb, int32_t le,
+                             kv_stream stream) {
+  if (n_src < 1 || n_src > KVX_MAX_RANKS || n_dst < 1 || n_dst > KVX_MAX_RANKS)
+    return fail(KV_EINVAL, "kv_convert_reshard: need 1..16 source and destination ranks");
+  if (!src || !src_pools || !dst || !dst_pools) return fail(KV_EINVAL, "kv_convert_reshard: null array");
+  for (int i = 0; i < n_src; ++i)
+    if (!src[i] || !src_pools[i]) return fail(KV_EINVAL, "kv_convert_reshard: null source layout/pool");
+  for (int i = 0; i < n_dst; ++i)
+    if (!dst[i] || !dst_pools[i]) return fail(KV_EINVAL, "kv_convert_reshard: null destination layout/pool");
+  const kv_layout *S = src[0], *D = dst[0];
+  for (int i = 1; i < n_src; ++i)
+    if (!same_instance(src[i], S)) return fail(KV_ESHAPE, "kv_convert_reshard: source layouts differ beyond rank");
+  for (int i = 1; i < n_dst; ++i)
+    if (!same_instance(dst[i], D)) return fail(KV_ESHAPE, "kv_convert_reshard: destination layouts differ");
+  kv_status st;
+  if (S->d.tp_degree > KVX_MAX_RANKS || D->d.tp_degree > KVX_MAX_RANKS)
+    return fail(KV_EUNSUPPORTED, "kv_convert_reshard: tp degree above 16");
+  if ((st = same_model(S, D)) != KV_OK) return st;
+  if ((st = check_layers(S, lb, le)) != KV_OK) return st;
+  if ((st = check_batch(src_bt, S, "src_bt")) != KV_OK) return st;
+  if ((st = check_batch(dst_bt, D, "dst_bt")) != KV_OK) return st;
+  if (src_bt->n_req != dst_bt->n_req || src_bt->total_tokens != dst_bt->total_tokens ||
+      src_bt->token_digest != dst_bt->token_digest)
+    return fail(KV_ESHAPE, "kv_convert_reshard: P and D tables describe different requests");
+  ConvArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int i = 0; i < KVX_MAX_RANKS; ++i) a.src_of_p[i] = -1;
+  for (int i = 0; i < n_src; ++i) {
+    const int p = src[i]->d.tp_rank;
+    if (a.src_of_p[p] != -1) return fail(KV_EINVAL, "kv_convert_reshard: source rank listed twice");
+    if ((st = scales_ok(src[i], D)) != KV_OK) return st;
+    a.src_of_p[p] = (int8_t)i;
+    a.src[i] = static_cast<const uint8_t*>(src_pools[i]);
+    a.sscale[i] = src[i]->d.scales;
+  }
+  const int32_t H = S->d.num_kv_heads;
+  const int32_t Hp = S->h_local, Hd = D->h_local;
+  bool seen_q[KVX_MAX_RANKS] = {false};
+  for (int i = 0; i < n_dst; ++i) {
+    const int q = dst[i]->d.tp_rank;
+    if (q >= KVX_MAX_RANKS || seen_q[q]) return fail(KV_EINVAL, "kv_convert_reshard: destination rank listed twice");
+    seen_q[q] = true;
+    if ((st = scales_ok(S, dst[i])) != KV_OK) return st;
+    for (int32_t h = q * Hd; h < (q + 1) * Hd; ++h)
+      if (a.src_of_p[h / Hp] < 0)
+        return fail(KV_ESHAPE, "kv_convert_reshard: missing source shard for P rank " + std::to_string(h / Hp) +
+                                   " (needed by D rank " + std::to_string(q) + ")");
+    a.dst[i] = static_cast<uint8_t*>(dst_pools[i]);
+    a.dst_rank[i] = (int8_t)q;
+    a.dscale[i] = dst[i]->d.scales;
+  }
+  (void)H;
+  bool fast = fast_ok(S) && fast_ok(D);
+  for (int i = 0; i < n_src && fast; ++i) fast = ptr_aligned(src_pools[i], 16);
+  for (int i = 0; i < n_dst && fast; ++i) fast = ptr_aligned(dst_pools[i], 16);
+  const int vec = fast ? 8 : 1;
+  for (int ax = 0; ax < 6; ++ax) {
+    a.ss[ax] = S->stride[ax];
+    a.ds[ax] = D->stride[ax];
+  }
+  a.Hp = Hp;
+  a.Hd = Hd;
+  a.D = S->d.head_dim;
+  a.Bp = S->d.block_size;
+  a.Bd = D->d.block_size;
+  a.s_blk_off = src_bt->blk_off;
+  a.s_blk_ids = src_bt->blk_ids;
+  a.d_blk_off = dst_bt->blk_off;
+  a.d_blk_ids = dst_bt->blk_ids;
+  a.d_blk_req = dst_bt->blk_req;
+  a.tok_off = dst_bt->tok_off;
+  a.slot_inner = slot_inner_of(D);
+  const uint32_t ndch = (uint32_t)(a.D / vec);
+  a.f_dch = make_fastdiv(ndch);
+  a.f_in0 = make_fastdiv(a.slot_inner ? a.Bd : Hd);
+  a.f_in1 = make_fastdiv(a.slot_inner ? Hd : a.Bd);
+  a.f_hp = make_fastdiv(Hp);
+  a.f_bp = make_fastdiv(a.Bp);
+  a.f_bd = make_fastdiv(a.Bd);
+  a.f_bl = make_fastdiv((uint32_t)std::max<int64_t>(dst_bt->total_blocks, 1));
+  if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
+  // per-layer chunk count; split the layer range so each launch stays under 2^31 chunks
+  const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * 2 * Hd * a.Bd * ndch;
+  int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / std::max<uint64_t>(per_layer, 1));
+  if (per_layer > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_convert_reshard: one layer exceeds 2^31 chunks");
+  for (int32_t l0 = lb; l0 < le; l0 += step) {
+    const int32_t l1 = std::min(le, l0 + step);
+    a.lb = l0;
+    a.Lc = l1 - l0;
+    a.f_l = make_fastdiv((uint32_t)a.Lc);
+    a.total = (uint32_t)(per_layer * (uint64_t)a.Lc);
+    cudaError_t e = launch_convert(a, vec, S->d.dtype, D->d.dtype, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "kv_convert_reshard: launch");
+  }
+  return KV_OK;
+}
+
+int32_t kv_wire_dtype(const kv_layout* s, const kv_layout* d) {
+  if (!s || !d) return -1;
+  return dtype_bytes(d->d.dtype) <= dtype_bytes(s->d.dtype) ? d->d.dtype : s->d.dtype;
+}
+
+size_t kv_wire_bytes(const kv_layout* s, const kv_layout* d, int64_t total_tokens, int32_t lb, int32_t le) {
+  if (!s || !d || le < lb || total_tokens < 0) return 0;
+  int32_t hb, he;
+  head_overlap(s, d, &hb, &he);
+  if (he <= hb) return 0;
+  return (size_t)2 * (size_t)(le - lb) * (size_t)(he - hb) * (size_t)total_tokens * (size_t)s->d.head_dim *
+         (size_t)dtype_bytes(kv_wire_dtype(s, d));
+}
+
+kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_bt, const kv_layout* d, int32_t lb,
+                  int32_t le, void* wire, size_t wire_bytes, kv_stream stream) {
+  if (!s || !d || !src_pool || !wire) return fail(KV_EINVAL, "kv_pack: null argument");
+  kv_status st;
+  if ((st = same_model(s, d)) != KV_OK) return st;
+  if ((st = check_layers(s, lb, le)) != KV_OK) return st;
+  if ((st = check_batch(src_bt, s, "src_bt")) != KV_OK) return st;
+  if ((st = scales_ok(s, d)) != KV_OK) return st;
+  int32_t hb, he;
+  head_overlap(s, d, &hb, &he);
+  if (he <= hb) return fail(KV_ESHAPE, "kv_pack: source and destination ranks share no heads");
+  const size_t need = kv_wire_bytes(s, d, src_bt->total_tokens, lb, le);
+  if (wire_bytes < need)
+    return fail(KV_ESHAPE, "kv_pack: wire buffer " + std::to_string(wire_bytes) + " < " + std::to_string(need));
+  if (need == 0) return KV_OK;
+  if (src_bt->n_req > 0 && !src_bt->tok_req) return fail(KV_EINVAL, "kv_pack: src_bt has no token map");
+  PackArgs a;
+  memset(&a, 0, sizeof(a));
+  const int vec = (fast_ok(s) && ptr_aligned(src_pool, 16) && ptr_aligned(wire, 16)) ? 8 : 1;
+  a.src = static_cast<const uint8_t*>(src_pool);
+  a.wire = static_cast<uint8_t*>(wire);
+  a.sscale = s->d.scales;
+  a.dscale = d->d.scales;
+  for (int ax = 0; ax < 6; ++ax) a.ss[ax] = s->stride[ax];
+  a.Hp = s->h_local;
+  a.Hd = d->h_local;
+  a.D = s->d.head_dim;
+  a.Bp = s->d.block_size;
+  a.lb = lb;
+  a.Lc = le - lb;
+  a.p = s->d.tp_rank;
+  a.q = d->d.tp_rank;
+  a.hb = hb;
+  a.nh = he - hb;
+  a.s_blk_off = src_bt->blk_off;
+  a.s_blk_ids = src_bt->blk_ids;
+  a.tok_off = src_bt->tok_off;
+  a.tok_req = src_bt->tok_req;
+  const uint32_t ndch = (uint32_t)(a.D / vec);
+  a.f_dch = make_fastdiv(ndch);
+  a.f_tok = make_fastdiv((uint32_t)src_bt->total_tokens);
+  a.f_nh = make_fastdiv((uint32_t)a.nh);
+  a.f_bp = make_fastdiv((uint32_t)a.Bp);
+  const uint64_t total = (uint64_t)a.Lc * 2 * a.nh * src_bt->total_tokens * ndch;
+  if (total > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_pack: more than 2^31 chunks in one call; split layers");
+  a.total = (uint32_t)total;
+  a.f_l = make_fastdiv((uint32_t)a.Lc);
+  cudaError_t e = launch_pack(a, vec, s->d.dtype, kv_wire_dtype(s, d), (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_pack: launch");
+  return KV_OK;
+}
+
+kv_status kv_unpack(const kv_layout* s, const kv_layout* d, void* dst_pool, const kv_batch* dst_bt, int32_t lb,
+                    int32_t le, const void* wire, size_t wire_bytes, kv_stream stream) {
+  if (!s || !d || !dst_pool || !wire) return fail(KV_EINVAL, "kv_unpack: null argument");
+  kv_status st;
+  if ((st = same_model(s, d)) != KV_OK) return st;
+  if ((st = check_layers(d, lb, le)) != KV_OK) return st;
+  if ((st = check_batch(dst_bt, d, "dst_bt")) != KV_OK) return st;
+  if ((st = scales_ok(s, d)) != KV_OK) return st;
+  int32_t hb, he;
+  head_overlap(s, d, &hb, &he);
+  if (he <= hb) return fail(KV_ESHAPE, "kv_unpack: source and destination ranks share no heads");
+  const size_t need = kv_wire_bytes(s, d, dst_bt->total_tokens, lb, le);
+  if (wire_bytes < need)
+    return fail(KV_ESHAPE, "kv_unpack: wire buffer " + std::to_string(wire_bytes) + " < " + std::to_string(need));
+  if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
+  UnpackArgs a;
+  memset(&a, 0, sizeof(a));
+  const int vec = (fast_ok(d) && ptr_aligned(dst_pool, 16) && ptr_aligned(wire, 16)) ? 8 : 1;
+  a.dst = static_cast<uint8_t*>(dst_pool);
+  a.wire = static_cast<const uint8_t*>(wire);
+  a.sscale = s->d.scales;
+  a.dscale = d->d.scales;
+  for (int ax = 0; ax < 6; ++ax) a.ds[ax] = d->stride[ax];
+  a.Hp = s->h_local;
+  a.Hd = d->h_local;
+  a.D = d->d.head_dim;
+  a.Bd = d->d.block_size;
+  a.lb = lb;
+  a.Lc = le - lb;
+  a.p = s->d.tp_rank;
+  a.q = d->d.tp_rank;
+  a.hb = hb;
+  a.nh = he - hb;
+  a.total_tokens = dst_bt->total_tokens;
+  a.d_blk_off = dst_bt->blk_off;
+  a.d_blk_ids = dst_bt->blk_ids;
+  a.d_blk_req = dst_bt->blk_req;
+  a.tok_off = dst_bt->tok_off;
+  a.slot_inner = slot_inner_of(d);
+  const uint32_t ndch = (uint32_t)(a.D / vec);
+  a.f_dch = make_fastdiv(ndch);
+  a.f_in0 = make_fastdiv(a.slot_inner ? a.Bd : a.nh);
+  a.f_in1 = make_fastdiv(a.slot_inner ? a.nh : a.Bd);
+  a.f_l = make_fastdiv((uint32_t)a.Lc);
+  a.f_bd = make_fastdiv((uint32_t)a.Bd);
+  const uint64_t total = (uint64_t)dst_bt->total_blocks * a.Lc * 2 * a.nh * a.Bd * ndch;
+  if (total > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_unpack: more than 2^31 chunks in one call; split layers");
+  a.total = (uint32_t)total;
+  a.f_bl = make_fastdiv((uint32_t)dst_bt->total_blocks);
+  cudaError_t e = launch_unpack(a, vec, kv_wire_dtype(s, d), d->d.dtype, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_unpack: launch");
+  return KV_OK;
+}
+
+}  // extern "C"

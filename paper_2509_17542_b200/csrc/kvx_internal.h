@@ -1,0 +1,97 @@
+// Internal declarations shared by the library's translation units (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "kvx.h"
+
+#define KVX_MAX_RANKS 16
+
+struct kv_layout {
+  kv_layout_desc d;
+  int64_t extent[6];  // per kv_axis
+  int64_t stride[6];  // element stride per kv_axis (dense row-major in axis_order)
+  int32_t h_local;
+  int32_t elem_bytes;
+  size_t pool_bytes;
+};
+
+namespace kvx {
+
+// thread-local error message + status helpers
+kv_status fail(kv_status st, const std::string& msg);
+kv_status cuda_fail(cudaError_t e, const char* what);
+extern std::atomic<uint64_t> g_launches;
+
+int32_t dtype_bytes(int32_t dt);
+
+// n / d for 32-bit n via one umulhi (Granlund-Montgomery round-up method).
+struct FastDiv {
+  uint32_t d, mul, shr;
+};
+FastDiv make_fastdiv(uint32_t d);
+
+// ---- kernel argument blocks (by value) -------------------------------------------
+struct ConvArgs {
+  const uint8_t* src[KVX_MAX_RANKS];
+  uint8_t* dst[KVX_MAX_RANKS];
+  const float* sscale[KVX_MAX_RANKS];  // per source index (e4m3 sources)
+  const float* dscale[KVX_MAX_RANKS];  // per destination index (e4m3 destinations)
+  int8_t src_of_p[KVX_MAX_RANKS];      // P tp_rank -> index into src[], -1 if absent
+  int8_t dst_rank[KVX_MAX_RANKS];      // index -> D tp_rank
+  int64_t ss[6], ds[6];                // element strides by axis
+  int32_t Hp, Hd, D, Bp, Bd, lb, Lc;
+  const int32_t* s_blk_off;
+  const int32_t* s_blk_ids;
+  const int32_t* d_blk_off;
+  const int32_t* d_blk_ids;
+  const int32_t* d_blk_req;
+  const int32_t* tok_off;
+  FastDiv f_dch, f_in0, f_in1, f_l, f_bl, f_hp, f_bp, f_bd;
+  int32_t slot_inner;  // 1: slot is the faster of (slot, head)
+  uint32_t total;      // chunks in this launch
+};
+
+struct PackArgs {
+  const uint8_t* src;
+  uint8_t* wire;
+  const float* sscale;  // source scales (unused unless the wire cast needs them)
+  const float* dscale;  // destination scales (narrowing to e4m3 on the sender)
+  int64_t ss[6];
+  int32_t Hp, Hd, D, Bp, lb, Lc, p, q, hb, nh;
+  const int32_t* s_blk_off;
+  const int32_t* s_blk_ids;
+  const int32_t* tok_off;
+  const int32_t* tok_req;
+  FastDiv f_dch, f_tok, f_nh, f_l, f_bp;
+  uint32_t total;
+};
+
+struct UnpackArgs {
+  uint8_t* dst;
+  const uint8_t* wire;
+  const float* sscale;  // source scales (widening from e4m3 on the receiver)
+  const float* dscale;
+  int64_t ds[6];
+  int32_t Hp, Hd, D, Bd, lb, Lc, p, q, hb, nh;
+  int64_t total_tokens;
+  const int32_t* d_blk_off;
+  const int32_t* d_blk_ids;
+  const int32_t* d_blk_req;
+  const int32_t* tok_off;
+  FastDiv f_dch, f_in0, f_in1, f_l, f_bl, f_bd;
+  int32_t slot_inner;
+  uint32_t total;
+};
+
+// launchers (kvx_kernels.cu); vec = 8 (fast path, DIM innermost) or 1 (generic)
+cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s);
+cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s);
+cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaStream_t s);
+cudaError_t launch_signal(uint32_t* flag, uint32_t value, cudaStream_t s);
+cudaError_t launch_wait(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, int32_t* err, cudaStream_t s);
+
+}  // namespace kvx

@@ -1,0 +1,547 @@
+// sm_100a kernels of the KV convert / reshard / transfer path (arXiv 2509.17542, III-B).
+//
+// Everything on the path is data movement plus an elementwise cast, so nothing here is a
+// dense contraction: no tensor cores.  The kernels are HBM-bound (intra-GPU) or
+// NVLink-bound (peer stores).  Design:
+//   * a launch covers a flat space of "chunks": VEC=8 consecutive head_dim elements of
+//     one (request, layer, K/V, head, token) row, i.e. 16 B of a 2-byte source;
+//   * each warp takes segments of 32*U consecutive chunks (grid-stride over segments),
+//     issues all U 16-byte loads per lane before any store (U loads in flight per
+//     thread, ~64 KB in flight per SM at full occupancy), then converts and stores;
+//   * chunk order is destination-driven with head_dim fastest, so a warp's stores are
+//     contiguous; every source row is >= 128 B contiguous (full sectors);
+//   * the decode of a chunk index into (dst block, layer, K/V, head, slot, dim) uses
+//     32-bit multiply-high divisions (FastDiv), block tables are tiny and L1/L2-resident;
+//   * a destination pointer may be peer-mapped (CUDA IPC): the same kernel then stores
+//     across NVLink -- the fused gather + convert + push (K4);
+//   * VEC=1 instantiations are the generic path for layouts whose head_dim is not the
+//     innermost axis on both sides (element-wise, correct for all 720 axis orders).
+// Casts (readings 10-13): same dtype = bit copy; f16/bf16/f32 narrowing via
+// cvt.rn (RNE, canonical NaN); e4m3 via cvt.rn.satfinite.e4m3x2.f32 of x * RN(1/s)
+// with __fmul_rn (never contracted into an FMA); e4m3 widening = cvt.rn.f16x2.e4m3x2
+// (exact) then * s.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "kvx_internal.h"
+
+namespace kvx {
+
+namespace {
+
+__device__ __forceinline__ uint32_t fdiv(uint32_t n, const FastDiv& f) {
+  uint32_t t = __umulhi(n, f.mul);
+  return (uint32_t)(((uint64_t)t + n) >> f.shr);
+}
+
+template <int DT>
+struct Tr;
+template <>
+struct Tr<KV_F16> { static constexpr int B = 2; };
+template <>
+struct Tr<KV_BF16> { static constexpr int B = 2; };
+template <>
+struct Tr<KV_F8E4M3> { static constexpr int B = 1; };
+template <>
+struct Tr<KV_F32> { static constexpr int B = 4; };
+
+// A chunk of VEC elements of dtype DT in 32-bit words.
+template <int DT, int VEC>
+struct Chunk {
+  static constexpr int BYTES = VEC * Tr<DT>::B;
+  static constexpr int WORDS = (BYTES + 3) / 4;
+  uint32_t w[WORDS];
+};
+
+template <int DT, int VEC>
+__device__ __forceinline__ void load_chunk(Chunk<DT, VEC>& c, const uint8_t* p) {
+  constexpr int N = Chunk<DT, VEC>::BYTES;
+  if constexpr (N == 32) {
+    uint4 a, b;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(p + 16));
+    c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w;
+    c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;
+  } else if constexpr (N == 16) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3]) : "l"(p));
+  } else if constexpr (N == 8) {
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(c.w[0]), "=r"(c.w[1]) : "l"(p));
+  } else if constexpr (N == 4) {
+    c.w[0] = *reinterpret_cast<const uint32_t*>(p);
+  } else if constexpr (N == 2) {
+    c.w[0] = *reinterpret_cast<const uint16_t*>(p);
+  } else {
+    c.w[0] = *p;
+  }
+}
+
+template <int DT, int VEC>
+__device__ __forceinline__ void store_chunk(uint8_t* p, const Chunk<DT, VEC>& c) {
+  constexpr int N = Chunk<DT, VEC>::BYTES;
+  if constexpr (N == 32) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(c.w[0]), "r"(c.w[1]), "r"(c.w[2]),
+                 "r"(c.w[3]) : "memory");
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p + 16), "r"(c.w[4]), "r"(c.w[5]), "r"(c.w[6]),
+                 "r"(c.w[7]) : "memory");
+  } else if constexpr (N == 16) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(c.w[0]), "r"(c.w[1]), "r"(c.w[2]),
+                 "r"(c.w[3]) : "memory");
+  } else if constexpr (N == 8) {
+    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(c.w[0]), "r"(c.w[1]) : "memory");
+  } else if constexpr (N == 4) {
+    *reinterpret_cast<uint32_t*>(p) = c.w[0];
+  } else if constexpr (N == 2) {
+    *reinterpret_cast<uint16_t*>(p) = (uint16_t)c.w[0];
+  } else {
+    *p = (uint8_t)c.w[0];
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ uint32_t get_elem(const uint32_t* w, int i) {
+  if constexpr (Tr<DT>::B == 4) return w[i];
+  if constexpr (Tr<DT>::B == 2) return (w[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu;
+  return (w[i >> 2] >> ((i & 3) * 8)) & 0xFFu;
+}
+
+template <int DT>
+__device__ __forceinline__ float to_f32(uint32_t b) {
+  if constexpr (DT == KV_F16) {
+    return __half2float(__ushort_as_half((unsigned short)b));
+  } else if constexpr (DT == KV_BF16) {
+    return __uint_as_float(b << 16);
+  } else if constexpr (DT == KV_F32) {
+    return __uint_as_float(b);
+  } else {
+    uint32_t h2;
+    unsigned short in = (unsigned short)b;
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(in));
+    return __half2float(__ushort_as_half((unsigned short)(h2 & 0xFFFFu)));
+  }
+}
+
+__device__ __forceinline__ uint32_t f32_to_f16(float f) {
+  uint32_t r;
+  unsigned short h;
+  asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(f));
+  r = h;
+  return r;
+}
+__device__ __forceinline__ uint32_t f32_to_bf16(float f) {
+  unsigned short h;
+  asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(f));
+  return h;
+}
+// two e4m3 codes: lo -> bits 0..7, hi -> bits 8..15
+__device__ __forceinline__ uint32_t f32x2_to_e4m3x2(float lo, float hi) {
+  unsigned short r;
+  asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
+// Cast a chunk SDT -> DDT.  ssc: dequant scale of an e4m3 source; inv: RN(1/s) of an
+// e4m3 destination.
+template <int SDT, int DDT, int VEC>
+__device__ __forceinline__ void cast_chunk(const Chunk<SDT, VEC>& in, Chunk<DDT, VEC>& out, float ssc, float inv) {
+  if constexpr (SDT == DDT) {
+#pragma unroll
+    for (int i = 0; i < Chunk<SDT, VEC>::WORDS; ++i) out.w[i] = in.w[i];
+  } else {
+    float f[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      f[i] = to_f32<SDT>(get_elem<SDT>(in.w, i));
+      if constexpr (SDT == KV_F8E4M3) f[i] = __fmul_rn(f[i], ssc);
+      if constexpr (DDT == KV_F8E4M3) f[i] = __fmul_rn(f[i], inv);
+    }
+#pragma unroll
+    for (int i = 0; i < Chunk<DDT, VEC>::WORDS; ++i) out.w[i] = 0;
+    if constexpr (DDT == KV_F8E4M3) {
+      if constexpr (VEC == 1) {
+        out.w[0] = f32x2_to_e4m3x2(f[0], 0.0f) & 0xFFu;
+      } else {
+#pragma unroll
+        for (int i = 0; i < VEC; i += 2) out.w[i >> 2] |= f32x2_to_e4m3x2(f[i], f[i + 1]) << ((i & 3) * 8);
+      }
+    } else if constexpr (DDT == KV_F32) {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) out.w[i] = __float_as_uint(f[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        uint32_t h = (DDT == KV_F16) ? f32_to_f16(f[i]) : f32_to_bf16(f[i]);
+        out.w[i >> 1] |= h << ((i & 1) * 16);
+      }
+    }
+  }
+}
+
+template <int DT, int VEC>
+__device__ __forceinline__ void zero_chunk(Chunk<DT, VEC>& c) {
+#pragma unroll
+  for (int i = 0; i < Chunk<DT, VEC>::WORDS; ++i) c.w[i] = 0;
+}
+
+__device__ __forceinline__ uint32_t divmod(uint32_t& n, const FastDiv& f) {
+  uint32_t q = fdiv(n, f);
+  uint32_t r = n - q * f.d;
+  n = q;
+  return r;
+}
+
+constexpr int kThreads = 256;
+
+// ------------------------------------------------------------------------------------
+// K1/K4: fused pool -> pool convert (+ reshard, + cast, + tail zero-fill)
+// chunk index (fastest first): dim-chunk, {slot, head} (dst-contiguous order), K/V,
+// layer, dst block (flattened over the batch), dst rank index.
+// ------------------------------------------------------------------------------------
+template <int VEC, int SDT, int DDT, int U>
+__global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ ConvArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
+  const uint64_t total = a.total;
+  const uint64_t nseg = (total + 32u * U - 1) / (32u * U);
+  for (uint64_t seg = warp; seg < nseg; seg += nwarps) {
+    Chunk<SDT, VEC> in[U];
+    uint8_t* dp[U];
+    float ssc[U], inv[U];
+    bool act[U], zero[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint64_t g64 = seg * (32u * U) + (uint32_t)k * 32u + lane;
+      act[k] = g64 < total;
+      zero[k] = false;
+      dp[k] = nullptr;
+      ssc[k] = 1.f;
+      inv[k] = 1.f;
+      if (act[k]) {
+        uint32_t n = (uint32_t)g64;
+        const uint32_t dch = divmod(n, a.f_dch);
+        const uint32_t in0 = divmod(n, a.f_in0);
+        const uint32_t in1 = divmod(n, a.f_in1);
+        const uint32_t c = n & 1u;
+        n >>= 1;
+        const uint32_t l = divmod(n, a.f_l);
+        const uint32_t bl = divmod(n, a.f_bl);
+        const uint32_t qi = n;
+        const uint32_t slot = a.slot_inner ? in0 : in1;
+        const uint32_t hq = a.slot_inner ? in1 : in0;
+        const int32_t r = __ldg(a.d_blk_req + bl);
+        const int32_t tok0 = __ldg(a.tok_off + r);
+        const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+        const uint32_t t = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd + slot;
+        const int64_t dblk = __ldg(a.d_blk_ids + bl);
+        const int64_t layer = a.lb + (int64_t)l;
+        const int64_t doff = layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
+                             (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD] +
+                             (int64_t)dch * VEC * a.ds[KV_AX_DIM];
+        dp[k] = a.dst[qi] + doff * Tr<DDT>::B;
+        if ((int32_t)t >= T) {
+          zero[k] = true;
+        } else {
+          const uint32_t h = (uint32_t)a.dst_rank[qi] * (uint32_t)a.Hd + hq;
+          const uint32_t p = fdiv(h, a.f_hp);
+          const uint32_t hp = h - p * (uint32_t)a.Hp;
+          const int si = a.src_of_p[p];
+          uint32_t tb = t;
+          const uint32_t sslot = divmod(tb, a.f_bp);
+          const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + tb);
+          const int64_t soff = layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
+                               sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
+                               (int64_t)hp * a.ss[KV_AX_HEAD] + (int64_t)dch * VEC * a.ss[KV_AX_DIM];
+          load_chunk<SDT, VEC>(in[k], a.src[si] + soff * Tr<SDT>::B);
+          if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3)
+            ssc[k] = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
+          if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3)
+            inv[k] = 1.0f / __ldg(a.dscale[qi] + (layer * 2 + c) * a.Hd + hq);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (!act[k]) continue;
+      Chunk<DDT, VEC> o;
+      if (zero[k])
+        zero_chunk(o);
+      else
+        cast_chunk<SDT, DDT, VEC>(in[k], o, ssc[k], inv[k]);
+      store_chunk<DDT, VEC>(dp[k], o);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K2: pack (Fig. 5 flatten) -- wire order (layer, K/V, head in overlap, token, dim)
+// ------------------------------------------------------------------------------------
+template <int VEC, int SDT, int WDT, int U>
+__global__ void __launch_bounds__(kThreads) k_pack(const __grid_constant__ PackArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
+  const uint64_t total = a.total;
+  const uint64_t nseg = (total + 32u * U - 1) / (32u * U);
+  for (uint64_t seg = warp; seg < nseg; seg += nwarps) {
+    Chunk<SDT, VEC> in[U];
+    float ssc[U], inv[U];
+    uint64_t gg[U];
+    bool act[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint64_t g64 = seg * (32u * U) + (uint32_t)k * 32u + lane;
+      gg[k] = g64;
+      act[k] = g64 < total;
+      ssc[k] = 1.f;
+      inv[k] = 1.f;
+      if (act[k]) {
+        uint32_t n = (uint32_t)g64;
+        const uint32_t dch = divmod(n, a.f_dch);
+        const uint32_t tok = divmod(n, a.f_tok);
+        const uint32_t hh = divmod(n, a.f_nh);
+        const uint32_t c = n & 1u;
+        n >>= 1;
+        const uint32_t l = n;
+        const int32_t r = __ldg(a.tok_req + tok);
+        uint32_t t = tok - (uint32_t)__ldg(a.tok_off + r);
+        const uint32_t sslot = divmod(t, a.f_bp);
+        const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + t);
+        const uint32_t h = (uint32_t)a.hb + hh;
+        const uint32_t hp = h - (uint32_t)a.p * (uint32_t)a.Hp;
+        const int64_t layer = a.lb + (int64_t)l;
+        const int64_t soff = layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
+                             (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD] +
+                             (int64_t)dch * VEC * a.ss[KV_AX_DIM];
+        load_chunk<SDT, VEC>(in[k], a.src + soff * Tr<SDT>::B);
+        if constexpr (SDT == KV_F8E4M3 && WDT != KV_F8E4M3) ssc[k] = __ldg(a.sscale + (layer * 2 + c) * a.Hp + hp);
+        if constexpr (WDT == KV_F8E4M3 && SDT != KV_F8E4M3)
+          inv[k] = 1.0f / __ldg(a.dscale + (layer * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (!act[k]) continue;
+      Chunk<WDT, VEC> o;
+      cast_chunk<SDT, WDT, VEC>(in[k], o, ssc[k], inv[k]);
+      store_chunk<WDT, VEC>(a.wire + gg[k] * (uint64_t)Chunk<WDT, VEC>::BYTES, o);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K3: unpack (Fig. 5 restore) -- destination-driven over the overlap heads
+// ------------------------------------------------------------------------------------
+template <int VEC, int WDT, int DDT, int U>
+__global__ void __launch_bounds__(kThreads) k_unpack(const __grid_constant__ UnpackArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
+  const uint64_t total = a.total;
+  const uint64_t nseg = (total + 32u * U - 1) / (32u * U);
+  for (uint64_t seg = warp; seg < nseg; seg += nwarps) {
+    Chunk<WDT, VEC> in[U];
+    uint8_t* dp[U];
+    float ssc[U], inv[U];
+    bool act[U], zero[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint64_t g64 = seg * (32u * U) + (uint32_t)k * 32u + lane;
+      act[k] = g64 < total;
+      zero[k] = false;
+      dp[k] = nullptr;
+      ssc[k] = 1.f;
+      inv[k] = 1.f;
+      if (act[k]) {
+        uint32_t n = (uint32_t)g64;
+        const uint32_t dch = divmod(n, a.f_dch);
+        const uint32_t in0 = divmod(n, a.f_in0);
+        const uint32_t in1 = divmod(n, a.f_in1);
+        const uint32_t c = n & 1u;
+        n >>= 1;
+        const uint32_t l = divmod(n, a.f_l);
+        const uint32_t bl = n;
+        const uint32_t slot = a.slot_inner ? in0 : in1;
+        const uint32_t hh = a.slot_inner ? in1 : in0;
+        const int32_t r = __ldg(a.d_blk_req + bl);
+        const int32_t tok0 = __ldg(a.tok_off + r);
+        const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+        const uint32_t t = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd + slot;
+        const int64_t dblk = __ldg(a.d_blk_ids + bl);
+        const int64_t layer = a.lb + (int64_t)l;
+        const uint32_t h = (uint32_t)a.hb + hh;
+        const uint32_t hq = h - (uint32_t)a.q * (uint32_t)a.Hd;
+        const int64_t doff = layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
+                             (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD] +
+                             (int64_t)dch * VEC * a.ds[KV_AX_DIM];
+        dp[k] = a.dst + doff * Tr<DDT>::B;
+        if ((int32_t)t >= T) {
+          zero[k] = true;
+        } else {
+          const int64_t woff = ((((int64_t)l * 2 + c) * a.nh + hh) * a.total_tokens + tok0 + t) * a.D + (int64_t)dch * VEC;
+          load_chunk<WDT, VEC>(in[k], a.wire + woff * Tr<WDT>::B);
+          if constexpr (WDT == KV_F8E4M3 && DDT != KV_F8E4M3)
+            ssc[k] = __ldg(a.sscale + (layer * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
+          if constexpr (DDT == KV_F8E4M3 && WDT != KV_F8E4M3)
+            inv[k] = 1.0f / __ldg(a.dscale + (layer * 2 + c) * a.Hd + hq);
+        }
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (!act[k]) continue;
+      Chunk<DDT, VEC> o;
+      if (zero[k])
+        zero_chunk(o);
+      else
+        cast_chunk<WDT, DDT, VEC>(in[k], o, ssc[k], inv[k]);
+      store_chunk<DDT, VEC>(dp[k], o);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K5: completion flags (A11)
+// ------------------------------------------------------------------------------------
+__global__ void k_signal(uint32_t* flag, uint32_t value) {
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_wait(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, int32_t* err) {
+  if (threadIdx.x != 0) return;
+  const uint64_t t0 = globaltimer();
+  while (true) {
+    uint32_t x;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(flag) : "memory");
+    if ((int32_t)(x - value) >= 0) break;
+    if (globaltimer() - t0 > timeout_ns) {
+      *err = 1;
+      break;
+    }
+    __nanosleep(64);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// launch helpers
+// ------------------------------------------------------------------------------------
+int num_sms() {
+  static thread_local int dev = -1, sms = 0;
+  int d = 0;
+  cudaGetDevice(&d);
+  if (d != dev) {
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
+    dev = d;
+  }
+  return sms;
+}
+
+template <typename K>
+int grid_for(K kernel, uint64_t total, int per_thread) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0);
+  if (occ < 1) occ = 1;
+  const uint64_t need = (total + (uint64_t)kThreads * per_thread - 1) / ((uint64_t)kThreads * per_thread);
+  uint64_t cap = (uint64_t)num_sms() * occ;
+  uint64_t g = need < cap ? need : cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+// U chunks per thread per segment: keep ~64 B of loads in flight per thread.
+template <int SDT, int VEC>
+constexpr int unroll_for() {
+  return VEC == 1 ? 4 : (Tr<SDT>::B == 1 ? 8 : (Tr<SDT>::B == 2 ? 4 : 2));
+}
+
+template <int VEC, int SDT, int DDT>
+cudaError_t conv_t(const ConvArgs& a, cudaStream_t s) {
+  constexpr int U = unroll_for<SDT, VEC>();
+  auto k = k_convert<VEC, SDT, DDT, U>;
+  k<<<grid_for(k, a.total, U), kThreads, 0, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+template <int VEC, int SDT, int WDT>
+cudaError_t pack_t(const PackArgs& a, cudaStream_t s) {
+  constexpr int U = unroll_for<SDT, VEC>();
+  auto k = k_pack<VEC, SDT, WDT, U>;
+  k<<<grid_for(k, a.total, U), kThreads, 0, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+template <int VEC, int WDT, int DDT>
+cudaError_t unpack_t(const UnpackArgs& a, cudaStream_t s) {
+  constexpr int U = unroll_for<WDT, VEC>();
+  auto k = k_unpack<VEC, WDT, DDT, U>;
+  k<<<grid_for(k, a.total, U), kThreads, 0, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+// dtype dispatch: F(vec, sdt, ddt)
+#define KVX_DISPATCH_DDT(FN, VEC, SDT, ddt, ...)                       \
+  switch (ddt) {                                                       \
+    case KV_F16: return FN<VEC, SDT, KV_F16>(__VA_ARGS__);             \
+    case KV_BF16: return FN<VEC, SDT, KV_BF16>(__VA_ARGS__);           \
+    case KV_F8E4M3: return FN<VEC, SDT, KV_F8E4M3>(__VA_ARGS__);       \
+    case KV_F32: return FN<VEC, SDT, KV_F32>(__VA_ARGS__);             \
+  }                                                                    \
+  return cudaErrorInvalidValue;
+
+#define KVX_DISPATCH(FN, VEC, sdt, ddt, ...)                                   \
+  switch (sdt) {                                                               \
+    case KV_F16: { KVX_DISPATCH_DDT(FN, VEC, KV_F16, ddt, __VA_ARGS__) }       \
+    case KV_BF16: { KVX_DISPATCH_DDT(FN, VEC, KV_BF16, ddt, __VA_ARGS__) }     \
+    case KV_F8E4M3: { KVX_DISPATCH_DDT(FN, VEC, KV_F8E4M3, ddt, __VA_ARGS__) } \
+    case KV_F32: { KVX_DISPATCH_DDT(FN, VEC, KV_F32, ddt, __VA_ARGS__) }       \
+  }                                                                            \
+  return cudaErrorInvalidValue;
+
+template <int VEC>
+cudaError_t conv_v(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
+  KVX_DISPATCH(conv_t, VEC, sdt, ddt, a, s)
+}
+template <int VEC>
+cudaError_t pack_v(const PackArgs& a, int sdt, int wdt, cudaStream_t s) {
+  KVX_DISPATCH(pack_t, VEC, sdt, wdt, a, s)
+}
+template <int VEC>
+cudaError_t unpack_v(const UnpackArgs& a, int wdt, int ddt, cudaStream_t s) {
+  KVX_DISPATCH(unpack_t, VEC, wdt, ddt, a, s)
+}
+
+}  // namespace
+
+cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s) {
+  if (a.total == 0) return cudaSuccess;
+  return vec == 8 ? conv_v<8>(a, sdt, ddt, s) : conv_v<1>(a, sdt, ddt, s);
+}
+cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s) {
+  if (a.total == 0) return cudaSuccess;
+  return vec == 8 ? pack_v<8>(a, sdt, wdt, s) : pack_v<1>(a, sdt, wdt, s);
+}
+cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaStream_t s) {
+  if (a.total == 0) return cudaSuccess;
+  return vec == 8 ? unpack_v<8>(a, wdt, ddt, s) : unpack_v<1>(a, wdt, ddt, s);
+}
+cudaError_t launch_signal(uint32_t* flag, uint32_t value, cudaStream_t s) {
+  k_signal<<<1, 1, 0, s>>>(flag, value);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+cudaError_t launch_wait(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, int32_t* err, cudaStream_t s) {
+  k_wait<<<1, 32, 0, s>>>(flag, value, timeout_ns, err);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
+}  // namespace kvx

@@ -1,0 +1,240 @@
+"""Python face of the C ABI: layouts, block tables, convert / pack / unpack, transport.
+
+Same names as include/kvx.h (without the ``kv_`` prefix).  Pools, tables, wire buffers
+and flags are torch CUDA tensors (or raw device addresses as ints, e.g. a peer-mapped
+pool from ``ipc_open``); this module only marshals pointers and sizes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from contextlib import contextmanager
+
+from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BYTES, KV_BF16, KV_F8E4M3, KV_F16,
+                   KV_F32, Batch_t, KvError, LayoutDesc, check, lib)
+
+__all__ = ["Layout", "Batch", "convert_reshard", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
+           "Comm", "ipc_export", "ipc_open", "ipc_close", "signal", "wait", "launch_count", "launch_count_reset",
+           "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "DTYPE_BYTES",
+           "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class Layout:
+    """kv_layout_describe: one TP rank's paged pool layout."""
+
+    def __init__(self, num_layers, num_kv_heads, head_dim, tp_degree, tp_rank, block_size, num_blocks, dtype,
+                 axis_order, scales=None):
+        d = LayoutDesc()
+        d.num_layers, d.num_kv_heads, d.head_dim = num_layers, num_kv_heads, head_dim
+        d.tp_degree, d.tp_rank = tp_degree, tp_rank
+        d.block_size, d.num_blocks, d.dtype = block_size, num_blocks, dtype
+        for i, a in enumerate(axis_order):
+            d.axis_order[i] = a
+        self.scales = scales  # keep the device tensor alive
+        d.scales = _ptr(scales)
+        h = C.c_void_p()
+        nbytes = C.c_size_t()
+        check(lib.kv_layout_describe(C.byref(d), C.byref(h), C.byref(nbytes)))
+        self._h = h
+        self.desc = d
+        self.pool_bytes = nbytes.value
+        self.num_layers, self.num_kv_heads, self.head_dim = num_layers, num_kv_heads, head_dim
+        self.tp_degree, self.tp_rank, self.block_size, self.num_blocks = tp_degree, tp_rank, block_size, num_blocks
+        self.dtype, self.axis_order = dtype, tuple(axis_order)
+        self.h_local = num_kv_heads // tp_degree
+
+    @classmethod
+    def from_dict(cls, d, scales=None):
+        return cls(d["L"], d["H"], d["D"], d["tp"], d["rank"], d["B"], d["NB"], d["dtype"], d["order"], scales)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def new_pool(self, device="cuda", fill=None):
+        import torch
+        t = torch.empty(self.pool_bytes, dtype=torch.uint8, device=device)
+        if fill is not None:
+            t.fill_(fill)
+        return t
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.kv_layout_destroy(h)
+            self._h = None
+
+
+class Batch:
+    """kv_block_table_update: one instance's validated, device-resident block tables."""
+
+    def __init__(self, layout: Layout, n_tokens, tables, device="cuda", stream=None):
+        import numpy as np
+        import torch
+        n_tokens = [int(t) for t in n_tokens]
+        ids = np.concatenate([np.asarray(t, dtype=np.int32) for t in tables]) if len(tables) else np.zeros(0, np.int32)
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        nt = np.ascontiguousarray(np.asarray(n_tokens, dtype=np.int32))
+        tb = int(sum(-(-t // layout.block_size) for t in n_tokens))
+        need = lib.kv_batch_bytes(len(n_tokens), tb, int(sum(n_tokens)))
+        self.buf = torch.empty(max(need, 16), dtype=torch.uint8, device=device)
+        self.bt = Batch_t()
+        check(lib.kv_block_table_update(layout.handle, len(n_tokens), nt.ctypes.data, ids.ctypes.data, len(ids),
+                                        self.buf.data_ptr(), self.buf.numel(), C.byref(self.bt), _stream(stream)))
+        self.n_tokens = n_tokens
+        self.tables = [list(map(int, t)) for t in tables]
+        self.layout = layout
+
+    @property
+    def total_tokens(self):
+        return self.bt.total_tokens
+
+    @property
+    def total_blocks(self):
+        return self.bt.total_blocks
+
+
+def plan_pairs(tp_p, tp_d, num_kv_heads):
+    """kv_plan_pairs: [(p, q, h_begin, h_end)] with non-empty head overlap (Fig. 4)."""
+    buf = (C.c_int32 * (4 * 256))()
+    n = lib.kv_plan_pairs(tp_p, tp_d, num_kv_heads, buf, 256)
+    if n < 0:
+        raise KvError(2, lib.kv_last_error().decode())
+    return [tuple(buf[4 * i:4 * i + 4]) for i in range(n)]
+
+
+def convert_reshard(src_layouts, src_pools, src_batch: Batch, dst_layouts, dst_pools, dst_batch: Batch,
+                    layer_range=None, stream=None):
+    """kv_convert_reshard: fused gather + TP re-shard + permute/block remap + cast + scatter."""
+    ns, nd = len(src_layouts), len(dst_layouts)
+    S = (C.c_void_p * ns)(*[l.handle.value for l in src_layouts])
+    SP = (C.c_void_p * ns)(*[_ptr(p) for p in src_pools])
+    Dl = (C.c_void_p * nd)(*[l.handle.value for l in dst_layouts])
+    DP = (C.c_void_p * nd)(*[_ptr(p) for p in dst_pools])
+    lb, le = layer_range if layer_range else (0, src_layouts[0].num_layers)
+    check(lib.kv_convert_reshard(ns, S, SP, C.byref(src_batch.bt), nd, Dl, DP, C.byref(dst_batch.bt), lb, le,
+                                 _stream(stream)))
+
+
+def wire_dtype(src: Layout, dst: Layout):
+    return lib.kv_wire_dtype(src.handle, dst.handle)
+
+
+def wire_bytes(src: Layout, dst: Layout, total_tokens, layer_range=None):
+    lb, le = layer_range if layer_range else (0, src.num_layers)
+    return lib.kv_wire_bytes(src.handle, dst.handle, int(total_tokens), lb, le)
+
+
+def pack(src: Layout, src_pool, src_batch: Batch, dst: Layout, wire, layer_range=None, stream=None, wire_nbytes=None):
+    """kv_pack: Fig. 5 flatten of the (src rank -> dst rank) share into `wire`."""
+    lb, le = layer_range if layer_range else (0, src.num_layers)
+    nb = wire_nbytes if wire_nbytes is not None else wire.numel() * wire.element_size()
+    check(lib.kv_pack(src.handle, _ptr(src_pool), C.byref(src_batch.bt), dst.handle, lb, le, _ptr(wire), nb,
+                      _stream(stream)))
+
+
+def unpack(src: Layout, dst: Layout, dst_pool, dst_batch: Batch, wire, layer_range=None, stream=None,
+           wire_nbytes=None):
+    """kv_unpack: Fig. 5 restore of a wire buffer into the D pool (+ tail zero-fill)."""
+    lb, le = layer_range if layer_range else (0, src.num_layers)
+    nb = wire_nbytes if wire_nbytes is not None else wire.numel() * wire.element_size()
+    check(lib.kv_unpack(src.handle, dst.handle, _ptr(dst_pool), C.byref(dst_batch.bt), lb, le, _ptr(wire), nb,
+                        _stream(stream)))
+
+
+class Comm:
+    """NCCL communicator owned by libkvx (kv_comm_*); the unique id travels through the
+    caller's control plane (e.g. torch.distributed broadcast_object_list)."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (C.c_uint8 * 128)()
+        check(lib.kv_comm_unique_id(buf))
+        return bytes(buf)
+
+    def __init__(self, nranks, rank, uid: bytes, device: int):
+        buf = (C.c_uint8 * 128).from_buffer_copy(uid)
+        h = C.c_void_p()
+        check(lib.kv_comm_init(nranks, rank, buf, device, C.byref(h)))
+        self._h = h
+        self.nranks, self.rank = nranks, rank
+
+    def send(self, peer, wire, nbytes=None, stream=None):
+        nb = nbytes if nbytes is not None else wire.numel() * wire.element_size()
+        check(lib.kv_send(self._h, peer, _ptr(wire), nb, _stream(stream)))
+
+    def recv(self, peer, wire, nbytes=None, stream=None):
+        nb = nbytes if nbytes is not None else wire.numel() * wire.element_size()
+        check(lib.kv_recv(self._h, peer, _ptr(wire), nb, _stream(stream)))
+
+    def recv_unpack(self, peer, wire, nbytes, src: Layout, dst: Layout, dst_pool, dst_batch: Batch,
+                    layer_range=None, stream=None):
+        lb, le = layer_range if layer_range else (0, src.num_layers)
+        check(lib.kv_recv_unpack(self._h, peer, _ptr(wire), nbytes, src.handle, dst.handle, _ptr(dst_pool),
+                                 C.byref(dst_batch.bt), lb, le, _stream(stream)))
+
+    @staticmethod
+    @contextmanager
+    def group():
+        check(lib.kv_comm_group_start())
+        try:
+            yield
+        finally:
+            check(lib.kv_comm_group_end())
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.kv_comm_destroy(self._h)
+            self._h = None
+
+
+def ipc_export(tensor):
+    """kv_ipc_export -> (64-byte handle, offset of the tensor inside its allocation)."""
+    h = (C.c_uint8 * 64)()
+    off = C.c_uint64()
+    check(lib.kv_ipc_export(_ptr(tensor), h, C.byref(off)))
+    return bytes(h), off.value
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    """kv_ipc_open -> peer-mapped device address (int) of the exporter's pointer."""
+    h = (C.c_uint8 * 64).from_buffer_copy(handle)
+    out = C.c_void_p()
+    check(lib.kv_ipc_open(h, offset, C.byref(out)))
+    return out.value
+
+
+def ipc_close(mapped_ptr: int, offset: int):
+    check(lib.kv_ipc_close(mapped_ptr - offset))
+
+
+def signal(flag, value, stream=None):
+    check(lib.kv_signal(_ptr(flag), value, _stream(stream)))
+
+
+def wait(flag, value, err, timeout_s=10.0, stream=None):
+    check(lib.kv_wait(_ptr(flag), value, int(timeout_s * 1e9), _ptr(err), _stream(stream)))
+
+
+def launch_count():
+    return lib.kv_launch_count()
+
+
+def launch_count_reset():
+    lib.kv_launch_count_reset()

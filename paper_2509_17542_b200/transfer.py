@@ -1,0 +1,148 @@
+"""P -> D transfer across GPUs of one box (A8, A10, A11): roles, pair plan, control-plane
+exchange and the two data-plane modes.
+
+* ``push`` (default, the fused kernel K4): each D rank exports its pool and a completion
+  flag through CUDA IPC; each P rank maps them and runs ``convert_reshard`` with the
+  *peer-mapped* D pool as destination -- one kernel gathers from local HBM, converts and
+  stores straight into the D rank's HBM across NVLink -- then ``signal``s the flag with a
+  system-scope release.  The D rank ``wait``s (acquire) on its local flag.  The cast
+  happens on the sender, so a narrowing cast halves the NVLink bytes (hard
+  part 2).  D keeps control of placement: its block table travels to P (A3).
+* ``nccl`` (baseline): P ``pack``s each pair's share into a wire buffer (canonical
+  Fig. 5 order), ``Comm.send``s it; D ``recv``s and ``unpack``s; per-layer chunks are
+  pipelined on two streams (pack chunk k+1 while chunk k is on the wire).
+
+Ranks: the first ``n_p`` ranks of the job are the P instance's TP ranks, the next ``n_d``
+the D instance's (disjoint GPU groups, north_star).  The pair plan is A2.
+torch.distributed is the control plane only (object exchange, barriers).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from . import kv
+
+
+@dataclass
+class Role:
+    kind: str        # "P" or "D"
+    tp_rank: int     # rank inside its instance
+    world_rank: int
+
+
+def roles(world_size: int, n_p: int, n_d: int):
+    """Global rank -> Role; P ranks first, then D ranks (disjoint GPU groups)."""
+    if n_p + n_d != world_size:
+        raise ValueError(f"world_size {world_size} != n_p {n_p} + n_d {n_d}")
+    return [Role("P", r, r) if r < n_p else Role("D", r - n_p, r) for r in range(world_size)]
+
+
+def pair_plan(tp_p: int, tp_d: int, num_kv_heads: int, p_ranks=None, d_ranks=None):
+    """A2 pairs restricted to the ranks present: [(p, q, h_begin, h_end)]."""
+    pairs = kv.plan_pairs(tp_p, tp_d, num_kv_heads)
+    return [x for x in pairs if (p_ranks is None or x[0] in p_ranks) and (d_ranks is None or x[1] in d_ranks)]
+
+
+def exchange(obj, group=None):
+    """all_gather_object over the control-plane group (gloo or nccl)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+class PushChannel:
+    """IPC-mapped D pools + flags for the fused push (K4/K5).
+
+    Every rank calls the constructor collectively.  D ranks pass their pool tensor and a
+    4-byte flag tensor; P ranks pass None.  Afterwards P ranks hold ``peer_pool[q]`` and
+    ``peer_flag[q]`` (device addresses in the P process) for every D rank q."""
+
+    def __init__(self, role: Role, pool=None, flag=None, group=None, ipc_export=None, ipc_open=None):
+        ipc_export = ipc_export or kv.ipc_export
+        ipc_open = ipc_open or kv.ipc_open
+        mine = None
+        if role.kind == "D":
+            mine = {"q": role.tp_rank, "pool": ipc_export(pool), "flag": ipc_export(flag)}
+        allv = exchange(mine, group)
+        self.role = role
+        self.peer_pool, self.peer_flag, self._mapped = {}, {}, []
+        if role.kind == "P":
+            for ent in allv:
+                if ent is None:
+                    continue
+                q = ent["q"]
+                self.peer_pool[q] = ipc_open(*ent["pool"])
+                self.peer_flag[q] = ipc_open(*ent["flag"])
+                self._mapped += [(self.peer_pool[q], ent["pool"][1]), (self.peer_flag[q], ent["flag"][1])]
+
+    def close(self):
+        for ptr, off in self._mapped:
+            kv.ipc_close(ptr, off)
+        self._mapped = []
+
+
+def push_step(src_layout, src_pool, src_batch, dst_layouts, peer_pools, dst_batch, peer_flags, epoch,
+              layer_chunk=None, stream=None):
+    """P side of one push transfer: fused gather/convert/NVLink-store into each paired D
+    pool (optionally per layer chunk, A10), then a release flag per D rank (A11)."""
+    L = src_layout.num_layers
+    chunk = layer_chunk or L
+    for q, dl in dst_layouts.items():
+        for l0 in range(0, L, chunk):
+            kv.convert_reshard([src_layout], [src_pool], src_batch, [dl], [peer_pools[q]], dst_batch,
+                               (l0, min(L, l0 + chunk)), stream)
+        kv.signal(peer_flags[q], epoch, stream)
+
+
+def nccl_send_step(comm, src_layout, src_pool, src_batch, dst_layouts, dst_world, wires, layer_chunk, pack_stream,
+                   send_stream, events):
+    """P side of the NCCL mode: pack layer chunk k on pack_stream, send it on send_stream
+    after the pack's event; double-buffered wires[(q, k % 2)]."""
+    import torch
+    L = src_layout.num_layers
+    nchunks = (L + layer_chunk - 1) // layer_chunk
+    for k in range(nchunks):
+        lr = (k * layer_chunk, min(L, (k + 1) * layer_chunk))
+        buf = k % 2
+        for q, dl in dst_layouts.items():
+            w = wires[(q, buf)]
+            nb = kv.wire_bytes(src_layout, dl, src_batch.total_tokens, lr)
+            if k >= 2:
+                pack_stream.wait_event(events[("sent", q, buf)])
+            kv.pack(src_layout, src_pool, src_batch, dl, w, lr, pack_stream, wire_nbytes=nb)
+            ev = torch.cuda.Event()
+            ev.record(pack_stream)
+            send_stream.wait_event(ev)
+            comm.send(dst_world[q], w, nb, send_stream)
+            ev2 = torch.cuda.Event()
+            ev2.record(send_stream)
+            events[("sent", q, buf)] = ev2
+
+
+def nccl_recv_step(comm, src_layouts, dst_layout, dst_pool, dst_batch, src_world, wires, layer_chunk, recv_stream,
+                   unpack_stream, events):
+    """D side of the NCCL mode: receive layer chunk k from every paired P rank (grouped,
+    so fan-in links run concurrently), then unpack it while chunk k+1 arrives."""
+    import torch
+    L = dst_layout.num_layers
+    nchunks = (L + layer_chunk - 1) // layer_chunk
+    for k in range(nchunks):
+        lr = (k * layer_chunk, min(L, (k + 1) * layer_chunk))
+        buf = k % 2
+        if k >= 2:
+            for p in src_layouts:
+                recv_stream.wait_event(events[("unpacked", p, buf)])
+        with kv.Comm.group():
+            for p, sl in src_layouts.items():
+                nb = kv.wire_bytes(sl, dst_layout, dst_batch.total_tokens, lr)
+                comm.recv(src_world[p], wires[(p, buf)], nb, recv_stream)
+        ev = torch.cuda.Event()
+        ev.record(recv_stream)
+        unpack_stream.wait_event(ev)
+        for p, sl in src_layouts.items():
+            nb = kv.wire_bytes(sl, dst_layout, dst_batch.total_tokens, lr)
+            kv.unpack(sl, dst_layout, dst_pool, dst_batch, wires[(p, buf)], lr, unpack_stream, wire_nbytes=nb)
+            ev2 = torch.cuda.Event()
+            ev2.record(unpack_stream)
+            events[("unpacked", p, buf)] = ev2

@@ -1,0 +1,163 @@
+"""CPU checks of the C-ABI library: it loads, exports every symbol include/kvx.h declares,
+and its host-side logic (validation, strides, re-shard plan, wire sizes, block-table
+validation) behaves -- all without a GPU (no compute calls)."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def kvx():
+    from paper_2509_17542_b200 import build as b
+    b.build()
+    import paper_2509_17542_b200 as k
+    return k
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "kvx.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(kv_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(kvx):
+    from paper_2509_17542_b200 import _lib
+    declared = _declared()
+    assert len(declared) >= 25
+    for name in declared:
+        assert hasattr(_lib.lib, name), name
+    assert sorted(_lib.EXPORTS) == declared
+    assert b"sm_100a" in _lib.lib.kv_version()
+
+
+def test_library_is_sm100a_only():
+    """The shipped cubin targets sm_100a (cuobjdump lists the ELF arch)."""
+    import subprocess
+    so = os.path.join(ROOT, "paper_2509_17542_b200", "libkvx.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert "sm_90" not in out and "sm_80" not in out
+
+
+def _lay(kvx, **kw):
+    d = dict(num_layers=2, num_kv_heads=8, head_dim=16, tp_degree=2, tp_rank=0, block_size=4, num_blocks=10,
+             dtype=kvx.KV_BF16, axis_order=(0, 1, 2, 3, 4, 5))
+    d.update(kw)
+    return kvx.Layout(**d)
+
+
+def test_describe_pool_bytes_and_errors(kvx):
+    l = _lay(kvx)
+    assert l.pool_bytes == 2 * 2 * 10 * 4 * 4 * 16 * 2
+    with pytest.raises(kvx.KvError, match="KV_ESHAPE"):
+        _lay(kvx, tp_degree=3)
+    with pytest.raises(kvx.KvError, match="KV_ESHAPE"):
+        _lay(kvx, tp_rank=2)
+    with pytest.raises(kvx.KvError, match="KV_EINVAL"):
+        _lay(kvx, axis_order=(0, 1, 2, 3, 4, 4))
+    with pytest.raises(kvx.KvError, match="KV_EINVAL"):
+        _lay(kvx, dtype=7)
+    with pytest.raises(kvx.KvError, match="KV_EINVAL"):
+        _lay(kvx, dtype=kvx.KV_F8E4M3)  # fp8 needs scales
+    with pytest.raises(kvx.KvError, match="KV_EINVAL"):
+        _lay(kvx, block_size=0)
+
+
+@pytest.mark.parametrize("tp_p,tp_d,H", [(4, 2, 8), (2, 4, 8), (4, 4, 8), (1, 8, 8), (8, 1, 8), (6, 4, 12), (2, 1, 32)])
+def test_plan_pairs_matches_oracle(kvx, o1, tp_p, tp_d, H):
+    assert sorted(kvx.plan_pairs(tp_p, tp_d, H)) == sorted(o1.plan(tp_p, tp_d, H))
+
+
+def test_plan_pairs_error(kvx):
+    with pytest.raises(kvx.KvError):
+        kvx.plan_pairs(3, 2, 8)
+
+
+def test_wire_bytes_is_kv_size_formula(kvx, o1):
+    """Per pair: 2 * L * |overlap| * T * D * bytes(wire dtype); summed over pairs = whole KV."""
+    for tp_p, tp_d in [(4, 2), (2, 4), (4, 4), (1, 1)]:
+        tot = 0
+        for p, q, hb, he in kvx.plan_pairs(tp_p, tp_d, 8):
+            s = _lay(kvx, tp_degree=tp_p, tp_rank=p, dtype=kvx.KV_BF16)
+            d = _lay(kvx, tp_degree=tp_d, tp_rank=q, dtype=kvx.KV_F16)
+            tot += kvx.wire_bytes(s, d, 100)
+        assert tot == o1.kv_bytes(2, 8, 16, 100, 2)
+    # narrowing: the wire carries the narrow dtype (cast on the sender)
+    sc = 0x1000  # any non-null pointer value: describe never dereferences scales
+    s = _lay(kvx, tp_degree=1, tp_rank=0)
+    d = kvx.Layout(2, 8, 16, 1, 0, 4, 10, kvx.KV_F8E4M3, (0, 1, 2, 3, 4, 5), sc)
+    assert kvx.wire_dtype(s, d) == kvx.KV_F8E4M3
+    assert kvx.wire_bytes(s, d, 100) == o1.kv_bytes(2, 8, 16, 100, 1)
+    assert kvx.wire_dtype(d, s) == kvx.KV_F8E4M3  # widening happens on the receiver
+    # ranks without overlap move nothing
+    s = _lay(kvx, tp_degree=2, tp_rank=0)
+    d = _lay(kvx, tp_degree=2, tp_rank=1)
+    assert kvx.wire_bytes(s, d, 100) == 0
+
+
+def _table_update(kvx, lay, n_tokens, ids, buf_bytes=4096):
+    from paper_2509_17542_b200._lib import Batch_t, lib
+    bt = Batch_t()
+    nt = np.asarray(n_tokens, np.int32)
+    ids = np.asarray(ids, np.int32)
+    return lib.kv_block_table_update(lay.handle, len(nt), nt.ctypes.data, ids.ctypes.data, len(ids), 0x10000,
+                                     buf_bytes, C.byref(bt), None), lib.kv_last_error().decode()
+
+
+def test_block_table_validation_fails_before_enqueue(kvx):
+    lay = _lay(kvx)  # B=4, NB=10
+    st, msg = _table_update(kvx, lay, [5, 4], [0, 1])
+    assert st == 2 and "sum ceil" in msg
+    st, msg = _table_update(kvx, lay, [5, 4], [0, 1, 10])
+    assert st == 2 and "outside" in msg
+    st, msg = _table_update(kvx, lay, [5, 4], [3, 1, 3])
+    assert st == 2 and "twice" in msg
+    st, msg = _table_update(kvx, lay, [5, -1], [3, 1])
+    assert st == 1
+    st, msg = _table_update(kvx, lay, [5, 4], [0, 1, 2], buf_bytes=8)
+    assert st == 2 and "device buffer" in msg
+
+
+def test_convert_validation(kvx):
+    from paper_2509_17542_b200._lib import Batch_t, lib
+    s0 = _lay(kvx, tp_degree=2, tp_rank=0)
+    d0 = _lay(kvx, tp_degree=1, tp_rank=0)
+
+    def bt(lay, n_req=1, tokens=5, digest=7):
+        b = Batch_t()
+        b.n_req, b.block_size, b.num_blocks = n_req, lay.block_size, lay.num_blocks
+        b.total_tokens, b.total_blocks, b.token_digest = tokens, 2, digest
+        b.tok_off = b.blk_off = b.blk_ids = b.blk_req = b.tok_req = 0x10000
+        return b
+
+    def call(src, dst, sbt, dbt, lb=0, le=2):
+        S = (C.c_void_p * len(src))(*[l.handle.value for l in src])
+        SP = (C.c_void_p * len(src))(*([0x20000] * len(src)))
+        D = (C.c_void_p * len(dst))(*[l.handle.value for l in dst])
+        DP = (C.c_void_p * len(dst))(*([0x30000] * len(dst)))
+        st = lib.kv_convert_reshard(len(src), S, SP, C.byref(sbt), len(dst), D, DP, C.byref(dbt), lb, le, None)
+        return st, lib.kv_last_error().decode()
+
+    # merge 2 -> 1 with P rank 1 missing
+    st, msg = call([s0], [d0], bt(s0), bt(d0))
+    assert st == 2 and "missing source shard for P rank 1" in msg
+    # mismatched requests between the P and D tables
+    s1 = _lay(kvx, tp_degree=2, tp_rank=1)
+    st, msg = call([s0, s1], [d0], bt(s0), bt(d0, digest=8))
+    assert st == 2 and "different requests" in msg
+    # layer range
+    st, msg = call([s0, s1], [d0], bt(s0), bt(d0), 1, 3)
+    assert st == 1
+    # different models
+    dm = _lay(kvx, tp_degree=1, tp_rank=0, head_dim=32)
+    st, msg = call([s0, s1], [dm], bt(s0), bt(dm))
+    assert st == 2 and "different models" in msg
+    # table built for another pool
+    d_other = _lay(kvx, tp_degree=1, tp_rank=0, num_blocks=11)
+    st, msg = call([s0, s1], [d0], bt(s0), bt(d_other))
+    assert st == 2 and "another block size" in msg

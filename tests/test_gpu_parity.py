@@ -1,0 +1,218 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle O1, element by element.
+
+Bar (BASELINE north_star): bit-exact for layout / reshard / fp16 / bf16 / fp32 work; fp8
+within 1 e4m3 ulp (ordered-integer distance on sign-magnitude codes, +-0 equal, NaN only
+with NaN).  The fp8 path is in fact expected bit-exact (same op order on both sides,
+reading 10), and the tests assert the 1-ulp bar plus report the exact-match count.
+Whole destination pools are compared, so canary bytes outside the written blocks,
+zero-filled tails and never-read source tails are all covered.
+"""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from synth import BF16, E4M3, F16, F32, LAYER, KV, BLOCK, SLOT, HEAD, DIM
+from tests.kvcase import coord_fill, expected, make_case
+
+pytestmark = pytest.mark.gpu
+
+ALL_ORDERS = list(itertools.permutations(range(6)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2509_17542_b200 import build
+    build.build()
+
+
+def e4m3_ulp_distance(a, b):
+    """Ordered-integer distance between e4m3 codes (sign-magnitude -> two's-line)."""
+    def ordv(x):
+        x = x.astype(np.int32)
+        mag = x & 0x7F
+        return np.where(x & 0x80, -mag, mag)
+    return np.abs(ordv(a) - ordv(b))
+
+
+def assert_pools_match(got, want, dtype):
+    for g, w in zip(got, want):
+        assert g.shape == w.shape
+        if dtype != E4M3:
+            if not np.array_equal(g, w):
+                bad = np.nonzero(g != w)[0]
+                raise AssertionError(f"{len(bad)} mismatches, first at {bad[:5]}: got {g[bad[:5]]} want {w[bad[:5]]}")
+        else:
+            nan_w = (w & 0x7F) == 0x7F
+            nan_g = (g & 0x7F) == 0x7F
+            assert np.array_equal(nan_w, nan_g), "NaN positions differ"
+            d = e4m3_ulp_distance(g[~nan_w], w[~nan_w])
+            assert d.max(initial=0) <= 1, f"fp8 beyond 1 ulp: max {d.max()}"
+
+
+def run_case(o1, case, layer_range=None):
+    from tests.gpu_util import DevCase
+    dc = DevCase(case)
+    dc.convert(layer_range)
+    want = expected(case, o1, layer_range)
+    got = dc.dst_numpy()
+    assert_pools_match(got, want, case["dst_lays"][0]["dtype"])
+    return dc, got, want
+
+
+def test_c1_tiny(o1):
+    """configs[0]: 2 layers, 2 kv heads, D 64, 32 tokens, block 16 -> 32, fp16 -> bf16, TP1 -> 1."""
+    c = synth.configs()["c1"]
+    case = make_case(c.L, c.H, c.D, c.tp_p, c.tp_d, c.B_p, c.B_d, c.n_tokens, c.src_dtype, c.dst_dtype,
+                     seed=c.seed, o1=o1)
+    run_case(o1, case)
+
+
+@pytest.mark.parametrize("sdt,ddt", [(s, d) for s in (F16, BF16, E4M3, F32) for d in (F16, BF16, E4M3, F32)])
+def test_all_dtype_pairs(o1, sdt, ddt):
+    """Every (src, dst) dtype pair, fast path, ragged requests, TP 2 -> 4 split."""
+    case = make_case(3, 8, 64, 2, 4, 8, 16, [37, 5, 64, 1], sdt, ddt, seed=10 + 4 * sdt + ddt, o1=o1,
+                     scales="amax")
+    if sdt == E4M3:  # e4m3 sources need their own dequant scales
+        for i, lay in enumerate(case["src_lays"]):
+            lay["scales"] = synth.pow2_scales(500 + i, lay["L"], lay["H"] // lay["tp"], -4, 4) * np.float32(0.75)
+    run_case(o1, case)
+
+
+@pytest.mark.parametrize("src_dt", [F16, BF16])
+def test_exhaustive_cast_table_on_device(o1, src_dt):
+    """All 65536 source bit patterns through the device cast (pins the NaN encodings,
+    reading 12, by device observation)."""
+    for dst_dt, scale in [(BF16 if src_dt == F16 else F16, None), (E4M3, 1.0), (E4M3, 5.5 / 448), (F32, None)]:
+        L, H, D, B, T = 1, 1, 128, 16, 256
+        src = synth.layout(L, H, D, 1, 0, B, T // B, src_dt, (LAYER, KV, BLOCK, SLOT, HEAD, DIM))
+        sc = None if scale is None else np.full((L, 2, H), scale, np.float32)
+        dst = synth.layout(L, H, D, 1, 0, B, T // B, dst_dt, (LAYER, KV, BLOCK, SLOT, HEAD, DIM), sc)
+        pool = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+        from tests.kvcase import NPTYPE
+        out = np.zeros(2 * T * D, dtype=NPTYPE[synth.NBYTES[dst_dt]])
+        case = dict(src_lays=[src], src_pools=[pool], dst_lays=[dst], dst_pools=[out], n_tokens=[T],
+                    src_tables=[list(range(T // B))], dst_tables=[list(range(T // B))])
+        dc, got, want = run_case(o1, case)
+        if dst_dt == E4M3:
+            assert np.array_equal(got[0], want[0]), "fp8 path is expected bit-exact (reading 10)"
+
+
+def test_s532_grid_coordinates(o1):
+    """SPEC S:532 grid on the GPU: (tp_p, tp_d) in {1,2,4,8}^2, the 24 layouts, blocks {2,4,8,16},
+    2 layers / 8 heads / 16 tokens; coordinate-coded values; D=8 keeps the fast path."""
+    orders = [(KV, BLOCK) + p for p in itertools.permutations((LAYER, HEAD, SLOT, DIM))]
+    k = 0
+    for tp_p in (1, 2, 4, 8):
+        for tp_d in (1, 2, 4, 8):
+            for i in range(0, 24, 5):
+                so, do = orders[i], orders[(i * 7 + tp_p + tp_d) % 24]
+                Bp, Bd = (2, 4, 8, 16)[i % 4], (2, 4, 8, 16)[(i // 4 + tp_d) % 4]
+                k += 1
+                case = make_case(2, 8, 8, tp_p, tp_d, Bp, Bd, [16, 11], F16, F16, so, do, seed=k, o1=o1,
+                                 tail_garbage=False)
+                coord_fill(case, o1)
+                run_case(o1, case)
+
+
+@pytest.mark.parametrize("i", range(0, 720, 7))
+def test_generic_axis_orders(o1, i):
+    """Axis orders where head_dim is not innermost take the element-wise path; 103 src/dst
+    order pairs spread over all 720 permutations."""
+    so, do = ALL_ORDERS[i], ALL_ORDERS[(i * 13 + 5) % 720]
+    case = make_case(2, 4, 8, 2, 1, 4, 2, [7, 3], BF16, F16, so, do, seed=i, o1=o1)
+    run_case(o1, case)
+
+
+def test_fast_path_many_layouts(o1):
+    """DIM innermost on both sides: all 120 orders of the other five axes as the destination."""
+    for i, p in enumerate(itertools.permutations((LAYER, KV, BLOCK, SLOT, HEAD))):
+        case = make_case(2, 4, 16, 1, 2, 4, 8, [9, 20], BF16, E4M3, synth.P_ORDER, p + (DIM,), seed=i, o1=o1)
+        run_case(o1, case)
+
+
+def test_layer_chunk_invariance(o1):
+    """A10: converting layer chunks separately == all at once (bit-identical)."""
+    from tests.gpu_util import DevCase
+    case = make_case(6, 8, 32, 4, 2, 16, 64, [100, 33, 64], BF16, BF16, seed=77, o1=o1)
+    whole = DevCase(case)
+    whole.convert()
+    parts = DevCase(case)
+    for lr in ((0, 1), (1, 4), (4, 6)):
+        parts.convert(lr)
+    for a, b in zip(whole.dst_numpy(), parts.dst_numpy()):
+        assert np.array_equal(a, b)
+    assert_pools_match(whole.dst_numpy(), expected(case, o1), BF16)
+
+
+def test_subset_of_destination_ranks(o1):
+    """Converting only D rank 1 touches only D rank 1 (per-pair dispatch)."""
+    from tests.gpu_util import DevCase
+    case = make_case(2, 8, 16, 4, 2, 4, 8, [13, 8], F16, BF16, seed=5, o1=o1)
+    dc = DevCase(case)
+    dc.convert(dst_idx=[1], src_idx=[2, 3])
+    got = dc.dst_numpy()
+    want = expected(case, o1)
+    assert np.array_equal(got[0], case["dst_pools"][0])  # untouched canary
+    assert np.array_equal(got[1], want[1])
+
+
+def test_empty_and_degenerate(o1):
+    """T_r = 0 requests, a single token, T a multiple of the block, B_p=1."""
+    for n_tokens, Bp, Bd in [([0, 5, 0], 4, 4), ([1], 1, 16), ([32, 16], 16, 16), ([3], 16, 1)]:
+        case = make_case(2, 2, 8, 1, 1, Bp, Bd, n_tokens, BF16, F16, seed=len(n_tokens), o1=o1)
+        run_case(o1, case)
+
+
+def test_pack_unpack_vs_flatten_restore(o1):
+    """K2/K3 against the oracle's Fig. 5 flatten / restore, per pair, with a narrowing cast."""
+    from tests.gpu_util import DevCase, dev_to_np
+    import paper_2509_17542_b200 as kvx
+    case = make_case(3, 8, 32, 2, 4, 8, 16, [21, 40, 7], BF16, E4M3, seed=3, o1=o1)
+    dc = DevCase(case)
+    for p, q, _, _ in kvx.plan_pairs(2, 4, 8):
+        S, Dl = dc.src_lays[p], dc.dst_lays[q]
+        nb = kvx.wire_bytes(S, Dl, dc.src_bt.total_tokens)
+        wire = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        kvx.pack(S, dc.src_pools[p], dc.src_bt, Dl, wire)
+        torch.cuda.synchronize()
+        want_wire = o1.flatten(case["src_lays"][p], case["src_pools"][p], case["dst_lays"][q], case["n_tokens"],
+                               case["src_tables"])
+        assert np.array_equal(dev_to_np(wire, E4M3), want_wire)
+        kvx.unpack(S, Dl, dc.dst_pools[q], dc.dst_bt, wire)
+    torch.cuda.synchronize()
+    assert_pools_match(dc.dst_numpy(), expected(case, o1), E4M3)
+
+
+def test_pack_unpack_widening_on_receiver(o1):
+    """fp8 source -> bf16 destination: the wire carries fp8, the receiver dequantises."""
+    from tests.gpu_util import DevCase
+    import paper_2509_17542_b200 as kvx
+    case = make_case(2, 4, 16, 1, 2, 4, 4, [9, 4], E4M3, BF16, seed=8, o1=o1)
+    case["src_lays"][0]["scales"] = synth.pow2_scales(1, 2, 4, -3, 3) * np.float32(1.5)
+    dc = DevCase(case)
+    for q in range(2):
+        S, Dl = dc.src_lays[0], dc.dst_lays[q]
+        assert kvx.wire_dtype(S, Dl) == kvx.KV_F8E4M3
+        wire = torch.empty(kvx.wire_bytes(S, Dl, dc.src_bt.total_tokens), dtype=torch.uint8, device="cuda")
+        kvx.pack(S, dc.src_pools[0], dc.src_bt, Dl, wire)
+        kvx.unpack(S, Dl, dc.dst_pools[q], dc.dst_bt, wire)
+    torch.cuda.synchronize()
+    assert_pools_match(dc.dst_numpy(), expected(case, o1), BF16)
+
+
+def test_launch_count_and_errors():
+    import paper_2509_17542_b200 as kvx
+    kvx.launch_count_reset()
+    lay = kvx.Layout(1, 2, 8, 1, 0, 4, 4, kvx.KV_BF16, synth.P_ORDER)
+    bt = kvx.Batch(lay, [5], [[0, 1]])
+    pools = [lay.new_pool(fill=0), lay.new_pool(fill=0)]
+    kvx.convert_reshard([lay], [pools[0]], bt, [lay], [pools[1]], bt)
+    torch.cuda.synchronize()
+    assert kvx.launch_count() == 1
+    with pytest.raises(kvx.KvError, match="KV_ESHAPE"):
+        kvx.Batch(lay, [5], [[0, 9]])
