@@ -103,7 +103,7 @@ class ClockSampler:
                 self.reasons |= int(getr(self.h))
             except Exception:
                 pass
-            time.sleep(0.01)
+            time.sleep(0.002)
 
     def start(self):
         if self.ok:

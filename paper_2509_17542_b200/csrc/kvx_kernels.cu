@@ -167,8 +167,10 @@ __device__ __forceinline__ void cast_chunk(const Chunk<SDT, VEC>& in, Chunk<DDT,
         for (int i = 0; i < VEC; i += 2) out.w[i >> 2] |= f32x2_to_e4m3x2(f[i], f[i + 1]) << ((i & 3) * 8);
       }
     } else if constexpr (DDT == KV_F32) {
+      // bf16 -> f32 is a bit shift that would keep NaN payloads; reading 12 wants the
+      // canonical NaN on every cast output (cvt.f32.f16 and FMUL already canonicalise)
 #pragma unroll
-      for (int i = 0; i < VEC; ++i) out.w[i] = __float_as_uint(f[i]);
+      for (int i = 0; i < VEC; ++i) out.w[i] = (f[i] != f[i]) ? 0x7FFFFFFFu : __float_as_uint(f[i]);
     } else {
 #pragma unroll
       for (int i = 0; i < VEC; ++i) {

@@ -1,0 +1,87 @@
+"""Host-side logic of the multi-GPU path, on CPU with world_size-2 gloo process groups:
+roles, the pair plan each rank derives, and the IPC handle exchange of PushChannel (with
+the CUDA IPC calls replaced by fakes -- the control plane is what is under test)."""
+import os
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2509_17542_b200 import transfer as tr
+        roles = tr.roles(world, world // 2, world // 2)
+        me = roles[rank]
+        # every rank derives the same plan independently
+        plan = tr.pair_plan(4, 4, 8, p_ranks=set(range(world // 2)), d_ranks=set(range(world // 2)))
+        plans = tr.exchange(plan)
+        exported, opened = [], []
+
+        def fake_export(t):
+            exported.append(t)
+            return (bytes([rank]) * 64, 4096 * rank + len(exported))
+
+        def fake_open(handle, off):
+            opened.append((handle[0], off))
+            return 0x7000_0000 + handle[0] * 0x100000 + off
+
+        pool = "pool" if me.kind == "D" else None
+        flag = "flag" if me.kind == "D" else None
+        ch = tr.PushChannel(me, pool, flag, ipc_export=fake_export, ipc_open=fake_open)
+        q.put((rank, me.kind, me.tp_rank, plans, exported, opened, ch.peer_pool, ch.peer_flag))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_roles_plan_and_handle_exchange(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    res.sort()
+    npair = world // 2
+    for rank, kind, tpr, plans, exported, opened, peer_pool, peer_flag in res:
+        assert kind == ("P" if rank < npair else "D") and tpr == rank % npair
+        assert all(pl == plans[0] for pl in plans)
+        assert sorted((p, q) for p, q, _, _ in plans[0]) == [(i, i) for i in range(npair)]
+        if kind == "D":
+            assert exported == ["pool", "flag"] and opened == []
+            assert peer_pool == {}
+        else:
+            assert exported == []
+            # one pool + one flag handle per D rank, mapped with the exporter's offsets
+            assert sorted(peer_pool) == list(range(npair)) and sorted(peer_flag) == list(range(npair))
+            for qd in range(npair):
+                owner = npair + qd
+                assert peer_pool[qd] == 0x7000_0000 + owner * 0x100000 + 4096 * owner + 1
+                assert peer_flag[qd] == 0x7000_0000 + owner * 0x100000 + 4096 * owner + 2
+
+
+def test_roles_validation():
+    from paper_2509_17542_b200 import transfer as tr
+    with pytest.raises(ValueError):
+        tr.roles(4, 1, 2)
+    r = tr.roles(8, 4, 4)
+    assert [x.kind for x in r] == ["P"] * 4 + ["D"] * 4
+    # c3: TP4 -> TP2 merge; c5 per P instance: TP2 -> TP4 split
+    assert sorted((p, q) for p, q, _, _ in tr.pair_plan(4, 2, 8)) == [(0, 0), (1, 0), (2, 1), (3, 1)]
+    assert sorted((p, q) for p, q, _, _ in tr.pair_plan(2, 4, 8)) == [(0, 0), (0, 1), (1, 2), (1, 3)]
