@@ -362,6 +362,7 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
   a.f_bp = make_fastdiv(a.Bp);
   a.f_bd = make_fastdiv(a.Bd);
   a.f_bl = make_fastdiv((uint32_t)std::max<int64_t>(dst_bt->total_blocks, 1));
+  a.f_cpr = make_fastdiv(ndch);
   if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
   // per-layer chunk count; split the layer range so each launch stays under 2^31 chunks
   const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * 2 * Hd * a.Bd * ndch;

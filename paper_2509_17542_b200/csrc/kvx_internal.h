@@ -52,7 +52,12 @@ struct ConvArgs {
   const int32_t* tok_off;
   FastDiv f_dch, f_in0, f_in1, f_l, f_bl, f_hp, f_bp, f_bd;
   int32_t slot_inner;  // 1: slot is the faster of (slot, head)
-  uint32_t total;      // chunks in this launch
+  uint32_t total;      // chunks in this launch (flat kernel)
+  // row-tiled fast path: work item = (dst rank, dst block, layer, K/V, row group)
+  FastDiv f_cpr;       // 8-element chunks per head_dim row (D / 8)
+  FastDiv f_items;     // row groups per (dst rank, dst block, layer, K/V) tile
+  int32_t rows_per_tile, rows_per_item, npass;
+  uint32_t n_items;
 };
 
 struct PackArgs {

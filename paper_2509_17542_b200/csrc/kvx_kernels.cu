@@ -21,6 +21,7 @@
 // with __fmul_rn (never contracted into an FMA); e4m3 widening = cvt.rn.f16x2.e4m3x2
 // (exact) then * s.
 #include <cuda_bf16.h>
+#include <algorithm>
 #include <cuda_fp16.h>
 
 #include "kvx_internal.h"
@@ -278,6 +279,101 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
 }
 
 // ------------------------------------------------------------------------------------
+// K1/K4 fast path (head_dim innermost on both sides): row-tiled.
+// A work item is a group of `rows_per_item` head_dim rows of one (dst rank, dst block,
+// layer, K/V) tile; the tile-level decode (request, block ids, base pointers) is done once
+// per item and is warp-uniform, so the per-16-byte work is a row decode plus addressing.
+// Lane `lane` handles chunk `lane % cpr` of rows row0 + lane / cpr + k * (32 / cpr) (when
+// cpr divides 32), so every warp instruction moves 32 x 16 contiguous-per-row bytes.
+// ------------------------------------------------------------------------------------
+template <int SDT, int DDT, int U>
+__global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant__ ConvArgs a) {
+  constexpr int VEC = 8;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
+  const uint32_t cpr = a.f_cpr.d;
+  for (uint32_t item = warp; item < a.n_items; item += nwarps) {
+    uint32_t n = item;
+    const uint32_t rg = divmod(n, a.f_items);
+    const uint32_t c = n & 1u;
+    n >>= 1;
+    const uint32_t l = divmod(n, a.f_l);
+    const uint32_t bl = divmod(n, a.f_bl);
+    const uint32_t qi = n;
+    const int32_t r = __ldg(a.d_blk_req + bl);
+    const int32_t tok0 = __ldg(a.tok_off + r);
+    const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+    const uint32_t tb0 = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd;  // first token of the block
+    const int32_t* sids = a.s_blk_ids + __ldg(a.s_blk_off + r);
+    const int64_t dblk = __ldg(a.d_blk_ids + bl);
+    const int64_t layer = a.lb + (int64_t)l;
+    uint8_t* dtile = a.dst[qi] + (layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK]) *
+                                     Tr<DDT>::B;
+    const int64_t s_lc = layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV];
+    const uint32_t hq0 = (uint32_t)a.dst_rank[qi] * (uint32_t)a.Hd;
+    const uint32_t row0 = rg * (uint32_t)a.rows_per_item;
+    const uint32_t row_end = min(row0 + (uint32_t)a.rows_per_item, (uint32_t)a.rows_per_tile);
+    const float* dsc = nullptr;
+    if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3) dsc = a.dscale[qi] + (layer * 2 + c) * a.Hd;
+#pragma unroll 1
+    for (int pass = 0; pass < a.npass; ++pass) {
+      Chunk<SDT, VEC> in[U];
+      uint8_t* dp[U];
+      float ssc[U], inv[U];
+      bool act[U], zero[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const uint32_t idx = (uint32_t)(pass * U + k) * 32u + lane;
+        uint32_t rr = idx;
+        const uint32_t ch = divmod(rr, a.f_cpr);
+        const uint32_t row = row0 + rr;
+        act[k] = row < row_end;
+        zero[k] = false;
+        ssc[k] = 1.f;
+        inv[k] = 1.f;
+        dp[k] = dtile;
+        if (act[k]) {
+          uint32_t m = row;
+          const uint32_t in0 = divmod(m, a.f_in0);
+          const uint32_t slot = a.slot_inner ? in0 : m;
+          const uint32_t hq = a.slot_inner ? m : in0;
+          dp[k] = dtile + ((int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD] + ch * VEC) * Tr<DDT>::B;
+          const uint32_t t = tb0 + slot;
+          if ((int32_t)t >= T) {
+            zero[k] = true;
+          } else {
+            const uint32_t h = hq0 + hq;
+            const uint32_t p = fdiv(h, a.f_hp);
+            const uint32_t hp = h - p * (uint32_t)a.Hp;
+            const int si = a.src_of_p[p];
+            uint32_t tb = t;
+            const uint32_t sslot = divmod(tb, a.f_bp);
+            const int64_t sblk = __ldg(sids + tb);
+            const int64_t soff = s_lc + sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
+                                 (int64_t)hp * a.ss[KV_AX_HEAD] + ch * VEC;
+            load_chunk<SDT, VEC>(in[k], a.src[si] + soff * Tr<SDT>::B);
+            if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3)
+              ssc[k] = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
+            if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3) inv[k] = 1.0f / __ldg(dsc + hq);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (!act[k]) continue;
+        Chunk<DDT, VEC> o;
+        if (zero[k])
+          zero_chunk(o);
+        else
+          cast_chunk<SDT, DDT, VEC>(in[k], o, ssc[k], inv[k]);
+        store_chunk<DDT, VEC>(dp[k], o);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // K2: pack (Fig. 5 flatten) -- wire order (layer, K/V, head in overlap, token, dim)
 // ------------------------------------------------------------------------------------
 template <int VEC, int SDT, int WDT, int U>
@@ -465,10 +561,36 @@ constexpr int unroll_for() {
 }
 
 template <int VEC, int SDT, int DDT>
-cudaError_t conv_t(const ConvArgs& a, cudaStream_t s) {
+cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
   constexpr int U = unroll_for<SDT, VEC>();
-  auto k = k_convert<VEC, SDT, DDT, U>;
-  k<<<grid_for(k, a.total, U), kThreads, 0, s>>>(a);
+  if constexpr (VEC == 8) {
+    // row-tiled fast path: size work items to ~kPasses passes of U chunks per lane
+    constexpr int kPasses = 4;
+    ConvArgs a = a0;
+    const uint32_t cpr = a.f_cpr.d;
+    const uint32_t rows_per_tile = (uint32_t)a.Bd * (uint32_t)a.Hd;
+    uint32_t rpi = (32u * U * kPasses) / cpr;
+    if (rpi < 1) rpi = 1;
+    if (rpi > rows_per_tile) rpi = rows_per_tile;
+    a.rows_per_tile = (int32_t)rows_per_tile;
+    a.rows_per_item = (int32_t)rpi;
+    a.npass = (int32_t)((rpi * cpr + 32u * U - 1) / (32u * U));
+    const uint32_t items_per_tile = (rows_per_tile + rpi - 1) / rpi;
+    a.f_items = make_fastdiv(items_per_tile);
+    const uint64_t n_items = (uint64_t)a.total / ((uint64_t)rows_per_tile * cpr) * items_per_tile;
+    a.n_items = (uint32_t)n_items;
+    auto k = k_convert_rows<SDT, DDT, U>;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0);
+    if (occ < 1) occ = 1;
+    const uint64_t need = (n_items + (kThreads / 32) - 1) / (kThreads / 32);
+    const uint64_t cap = (uint64_t)num_sms() * occ;
+    const int grid = (int)std::max<uint64_t>(1, std::min(need, cap));
+    k<<<grid, kThreads, 0, s>>>(a);
+  } else {
+    auto k = k_convert<VEC, SDT, DDT, U>;
+    k<<<grid_for(k, a0.total, U), kThreads, 0, s>>>(a0);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

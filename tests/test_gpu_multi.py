@@ -1,0 +1,109 @@
+"""Multi-GPU parity (needs >= 2 GPUs): P instance on cuda:0, D instance on cuda:1, one
+process each.  Both transports against the oracle:
+  * push: the fused convert kernel stores into the D pools mapped through CUDA IPC, then
+    a release flag; D acquires it and checks its pools;
+  * nccl: kv_pack -> ncclSend / ncclRecv -> kv_unpack per (p, q) pair and layer chunk.
+Control plane: a gloo process group (object exchange)."""
+import os
+import pickle
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, port, blob, mode, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=2)
+    try:
+        import paper_2509_17542_b200 as kvx
+        from paper_2509_17542_b200 import transfer as tr
+        from tests.gpu_util import DevCase
+        case = pickle.loads(blob)
+        dc = DevCase(case, device=f"cuda:{rank}")
+        flag = torch.zeros(4, dtype=torch.int32, device=f"cuda:{rank}")
+        err = torch.zeros(1, dtype=torch.int32, device=f"cuda:{rank}")
+        if mode == "push":
+            exp = None
+            if rank == 1:
+                exp = [kvx.ipc_export(p) for p in dc.dst_pools] + [kvx.ipc_export(flag)]
+            allx = tr.exchange(exp)
+            if rank == 0:
+                mapped = [kvx.ipc_open(h, o) for h, o in allx[1]]
+                # one launch: all P ranks -> all D ranks, stores over NVLink
+                kvx.convert_reshard(dc.src_lays, dc.src_pools, dc.src_bt, dc.dst_lays, mapped[:-1], dc.dst_bt)
+                kvx.signal(mapped[-1], 1)
+                torch.cuda.synchronize()
+                dist.barrier()
+                for (h, o), m in zip(allx[1], mapped):
+                    kvx.ipc_close(m, o)
+                q.put((rank, None))
+            else:
+                kvx.wait(flag, 1, err, 20.0)
+                torch.cuda.synchronize()
+                assert int(err.item()) == 0, "flag wait timed out"
+                q.put((rank, [a.copy() for a in dc.dst_numpy()]))
+                dist.barrier()
+        else:
+            uid = kvx.Comm.unique_id() if rank == 0 else None
+            lst = [uid]
+            dist.broadcast_object_list(lst, src=0)
+            comm = kvx.Comm(2, rank, lst[0], rank)
+            pairs = kvx.plan_pairs(dc.src_lays[0].tp_degree, dc.dst_lays[0].tp_degree, dc.src_lays[0].num_kv_heads)
+            L = dc.src_lays[0].num_layers
+            for l0 in range(0, L, 2):  # layer chunks of 2
+                lr = (l0, min(L, l0 + 2))
+                for p, qq, _, _ in pairs:
+                    S, D = dc.src_lays[p], dc.dst_lays[qq]
+                    nb = kvx.wire_bytes(S, D, dc.src_bt.total_tokens, lr)
+                    wire = torch.empty(nb, dtype=torch.uint8, device=f"cuda:{rank}")
+                    if rank == 0:
+                        kvx.pack(S, dc.src_pools[p], dc.src_bt, D, wire, lr)
+                        comm.send(1, wire, nb)
+                    else:
+                        comm.recv_unpack(0, wire, nb, S, D, dc.dst_pools[qq], dc.dst_bt, lr)
+                    torch.cuda.synchronize()
+            comm.close()
+            q.put((rank, None if rank == 0 else [a.copy() for a in dc.dst_numpy()]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["push", "nccl"])
+@pytest.mark.parametrize("shape", ["merge", "split_fp8"])
+def test_p_to_d_across_gpus(o1, mode, shape):
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    import torch.multiprocessing as mp
+    from synth import BF16, E4M3, F16
+    from tests.kvcase import expected, make_case
+    from tests.test_gpu_parity import assert_pools_match
+    if shape == "merge":   # c3-like: TP4 -> TP2, block 16 -> 64
+        case = make_case(4, 8, 128, 4, 2, 16, 64, [300, 77, 1], BF16, BF16, seed=3, o1=o1)
+    else:                  # c5-like split TP2 -> TP4 with a c4-like fp8 cast
+        case = make_case(4, 8, 128, 2, 4, 16, 16, [129, 40], F16, E4M3, seed=4, o1=o1, scales="pow2")
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    blob = pickle.dumps(case)
+    ps = [ctx.Process(target=_worker, args=(r, port, blob, mode, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in ps:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert_pools_match(res[1], expected(case, o1), case["dst_lays"][0]["dtype"])
