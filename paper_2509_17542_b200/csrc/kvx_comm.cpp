@@ -7,7 +7,9 @@
 #include <nccl.h>
 #include <string.h>
 
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "kvx_internal.h"
 
@@ -125,20 +127,48 @@ kv_status kv_ipc_export(const void* dev_ptr, uint8_t out_handle[64], uint64_t* o
   return KV_OK;
 }
 
+// One mapping per exported allocation per process: several exported tensors may live in
+// the same caching-allocator segment (same handle), and a handle must not be opened twice.
+namespace {
+struct Mapping {
+  std::string key;
+  void* base;
+  int refs;
+};
+std::mutex g_map_mu;
+std::vector<Mapping> g_maps;
+}  // namespace
+
 kv_status kv_ipc_open(const uint8_t handle[64], uint64_t offset, void** out_ptr) {
   if (!handle || !out_ptr) return fail(KV_EINVAL, "kv_ipc_open: null argument");
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  const std::string key(reinterpret_cast<const char*>(handle), 64);
+  for (auto& m : g_maps)
+    if (m.key == key) {
+      ++m.refs;
+      *out_ptr = static_cast<uint8_t*>(m.base) + offset;
+      return KV_OK;
+    }
   cudaIpcMemHandle_t h;
   memcpy(&h, handle, 64);
   void* base = nullptr;
   cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
   if (e != cudaSuccess) return cuda_fail(e, "cudaIpcOpenMemHandle");
+  g_maps.push_back({key, base, 1});
   *out_ptr = static_cast<uint8_t*>(base) + offset;
   return KV_OK;
 }
 
 kv_status kv_ipc_close(void* mapped_base) {
-  cudaError_t e = cudaIpcCloseMemHandle(mapped_base);
-  return e == cudaSuccess ? KV_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  for (size_t i = 0; i < g_maps.size(); ++i)
+    if (g_maps[i].base == mapped_base) {
+      if (--g_maps[i].refs > 0) return KV_OK;
+      g_maps.erase(g_maps.begin() + (long)i);
+      cudaError_t e = cudaIpcCloseMemHandle(mapped_base);
+      return e == cudaSuccess ? KV_OK : cuda_fail(e, "cudaIpcCloseMemHandle");
+    }
+  return fail(KV_EINVAL, "kv_ipc_close: address was not returned by kv_ipc_open (pass pointer - offset)");
 }
 
 kv_status kv_signal(uint32_t* flag, uint32_t value, kv_stream stream) {

@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
           if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3)
             ssc[k] = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
           if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3)
-            inv[k] = 1.0f / __ldg(a.dscale[qi] + (layer * 2 + c) * a.Hd + hq);
+            inv[k] = __frcp_rn(__ldg(a.dscale[qi] + (layer * 2 + c) * a.Hd + hq));
         }
       }
     }
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant
             load_chunk<SDT, VEC>(in[k], a.src[si] + soff * Tr<SDT>::B);
             if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3)
               ssc[k] = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
-            if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3) inv[k] = 1.0f / __ldg(dsc + hq);
+            if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3) inv[k] = __frcp_rn(__ldg(dsc + hq));
           }
         }
       }
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(kThreads) k_pack(const __grid_constant__ PackA
         load_chunk<SDT, VEC>(in[k], a.src + soff * Tr<SDT>::B);
         if constexpr (SDT == KV_F8E4M3 && WDT != KV_F8E4M3) ssc[k] = __ldg(a.sscale + (layer * 2 + c) * a.Hp + hp);
         if constexpr (WDT == KV_F8E4M3 && SDT != KV_F8E4M3)
-          inv[k] = 1.0f / __ldg(a.dscale + (layer * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd));
+          inv[k] = __frcp_rn(__ldg(a.dscale + (layer * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)));
       }
     }
 #pragma unroll
@@ -483,7 +483,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack(const __grid_constant__ Unp
           if constexpr (WDT == KV_F8E4M3 && DDT != KV_F8E4M3)
             ssc[k] = __ldg(a.sscale + (layer * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
           if constexpr (DDT == KV_F8E4M3 && WDT != KV_F8E4M3)
-            inv[k] = 1.0f / __ldg(a.dscale + (layer * 2 + c) * a.Hd + hq);
+            inv[k] = __frcp_rn(__ldg(a.dscale + (layer * 2 + c) * a.Hd + hq));
         }
       }
     }

@@ -105,11 +105,15 @@ def fill_random_finite_(t, seed, dtype):
         t ^= bad.to(torch.uint8)
         return t
     if nb == 2:
-        v = torch.randint(-(1 << 15), 1 << 15, t.shape, generator=g, device=t.device, dtype=torch.int16)
         m, low = (0x7C00, 0x0400) if dtype == F16 else (0x7F80, 0x0080)
-        bad = (v & m) == m
-        v ^= bad.to(torch.int16) * low
-        t.copy_(v.view(t.dtype) if t.dtype != torch.int16 else v)
+        flat = t.view(-1)
+        step = 1 << 28  # fill in 512 MiB pieces: no pool-sized temporaries
+        for i in range(0, flat.numel(), step):
+            part = flat[i:i + step]
+            v = torch.randint(-(1 << 15), 1 << 15, part.shape, generator=g, device=t.device, dtype=torch.int16)
+            bad = (v & m) == m
+            v ^= bad.to(torch.int16) * low
+            part.copy_(v.view(t.dtype) if t.dtype != torch.int16 else v)
         return t
     raise NotImplementedError("fp32 device fill")
 

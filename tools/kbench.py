@@ -83,8 +83,11 @@ def main():
     if "c4c" in sel:
         case("c4 one pair, contiguous tables", cf["c4"], [0], [0], contiguous=True, parity=False)
     if "c5" in sel:
+        import dataclasses
         c5 = cf["c5"]
-        case("c5 one P inst rank0 -> D0,D1 (split) bf16", c5, [0], [0, 1])
+        inst_a = dataclasses.replace(c5, n_tokens=c5.n_tokens[0::2])  # P instance A's requests
+        case(f"c5 instance A ({len(inst_a.n_tokens)} req, {inst_a.total_tokens} tok) rank0 -> D0,D1 split bf16",
+             inst_a, [0], [0, 1], parity=True)
 
 
 if __name__ == "__main__":
