@@ -432,7 +432,52 @@ def run_multi(args):
             else:
                 kvx.wait(flag, epoch[0], err, 30.0, stream)
     else:
-        raise SystemExit("--mode nccl: see run_multi_nccl")
+        # NCCL baseline: pack -> ncclSend / ncclRecv -> unpack, per-layer double-buffered
+        uid = [kvx.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = kvx.Comm(world, rank, uid[0], local)
+        lc = args.layer_chunk or 4
+        s_a, s_b = torch.cuda.Stream(), torch.cuda.Stream()
+        events, wires = {}, {}
+        if me.kind == "P":
+            peers = {q: kvx.Layout.from_dict(
+                synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, w.NB_d, cfg.dst_dtype, cfg.d_order),
+                torch.ones(cfg.L * 2 * (cfg.H // cfg.tp_d), device=dev))
+                for p, q, _, _ in pairs if p == me.tp_rank}
+            S = w.src_lays[me.tp_rank]
+            for q, dl in peers.items():
+                nb = max(kvx.wire_bytes(S, dl, cfg.total_tokens, (l0, min(cfg.L, l0 + lc))) for l0 in range(0, cfg.L, lc))
+                for b in range(2):
+                    wires[(q, b)] = torch.empty(nb, dtype=torch.uint8, device=dev)
+        else:
+            peers = {p: kvx.Layout.from_dict(
+                synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, w.NB_p, cfg.src_dtype, cfg.p_order))
+                for p, q, _, _ in pairs if q == me.tp_rank}
+            Dl = w.dst_lays[me.tp_rank]
+            for p, sl in peers.items():
+                nb = max(kvx.wire_bytes(sl, Dl, cfg.total_tokens, (l0, min(cfg.L, l0 + lc))) for l0 in range(0, cfg.L, lc))
+                for b in range(2):
+                    wires[(p, b)] = torch.empty(nb, dtype=torch.uint8, device=dev)
+
+        def step(ev=None):
+            st = torch.cuda.Event()
+            st.record(stream)
+            s_a.wait_event(st)
+            s_b.wait_event(st)
+            if ev is not None:
+                ev[0].record(stream)
+            if me.kind == "P":
+                tr.nccl_send_step(comm, w.src_lays[me.tp_rank], w.src_pools[me.tp_rank], w.src_bt, peers,
+                                  {q: npair + q for q in peers}, wires, lc, s_a, s_b, events)
+            else:
+                tr.nccl_recv_step(comm, peers, w.dst_lays[me.tp_rank], w.dst_pools[me.tp_rank], w.dst_bt,
+                                  {p: p for p in peers}, wires, lc, s_a, s_b, events)
+            for s in (s_a, s_b):
+                e = torch.cuda.Event()
+                e.record(s)
+                stream.wait_event(e)
+            if ev is not None:
+                ev[1].record(stream)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -468,6 +513,42 @@ def run_multi(args):
         # from the same seeds on the D rank's GPU)
         parity = parity_multi(args, cfg, w, me, dev)
     allpar = tr.exchange(parity)
+    e2e = None
+    if not args.no_e2e and args.mode == "push":
+        # end to end through the public API with host buffers: every step the P rank
+        # uploads its source pool from pinned memory, pushes, and the D rank reads its
+        # pool back to pinned memory
+        ke = min(K, 3)
+        if me.kind == "P":
+            host = w.src_pools[me.tp_rank].cpu().pin_memory()
+        else:
+            host = torch.empty(w.dst_pools[me.tp_rank].numel(), dtype=torch.uint8).pin_memory()
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ke):
+            if me.kind == "P":
+                w.src_pools[me.tp_rank].copy_(host, non_blocking=True)
+                step()
+            else:
+                step()
+                host.copy_(w.dst_pools[me.tp_rank], non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if int(err.item()):
+            raise SystemExit(f"rank {rank}: flag wait timed out (e2e)")
+        st2 = torch.tensor([e0.elapsed_time(e1), float(host.numel() if me.kind == "P" else 0),
+                            float(host.numel() if me.kind == "D" else 0)], device=dev, dtype=torch.float64)
+        al2 = [torch.zeros_like(st2) for _ in range(world)]
+        dist.all_gather(al2, st2)
+        al2 = [s.tolist() for s in al2]
+        ms_e = max(s[0] for s in al2) / ke
+        e2e = {"value": round(w.src_bytes(range(npair)) / (ms_e * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "ms_per_step": round(ms_e, 3), "h2d_bytes_per_step": int(sum(s[1] for s in al2)),
+               "d2h_bytes_per_step": int(sum(s[2] for s in al2)), "steps": ke}
+        del host
     if rank == 0:
         max_ms = max(s[0] for s in allst)
         ms = max_ms / K
@@ -490,13 +571,17 @@ def run_multi(args):
                        "parallelism": f"P TP{cfg.tp_p} x D TP{cfg.tp_d}, {npair} pair(s)"},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED_GBS,
                          "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED_GBS, 4),
-                         "traffic": _traffic(wl_name, world), "kernel": "k_convert (peer-store push)",
+                         "traffic": _traffic(wl_name, world),
+                         "kernel": "k_convert_rows (peer-store push)" if args.mode == "push"
+                         else "pack + ncclSend/Recv + unpack (whole P step)",
                          "kernel_ms": round(kms, 4), "algorithmic_bytes_per_launch": nvl_b,
                          "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)",
                          "frac_vs_nominal_900": round(achieved / NVLINK_NOMINAL_GBS, 4)},
             "clocks": clk, "gpu_launches": int(sum(s[2] for s in allst)),
             "parity": [p for p in allpar if p is not None],
         }
+        if e2e is not None:
+            out["e2e"] = e2e
         print(json.dumps(out), flush=True)
     barrier()
     dist.destroy_process_group()
@@ -507,7 +592,6 @@ def parity_multi(args, cfg, w, me, dev):
         return None
     q = me.tp_rank
     p = q  # identity pairing (tp_p == tp_d)
-    src = Workload.__new__(Workload)
     # regenerate P rank p's pool from its seed on this GPU (same generator, same seed)
     import torch
     import paper_2509_17542_b200 as kvx

@@ -89,7 +89,10 @@ void head_overlap(const kv_layout* s, const kv_layout* d, int32_t* hb, int32_t* 
 }
 
 // The fast path needs head_dim innermost and contiguous with 8-element chunks.
-bool fast_ok(const kv_layout* lay) { return lay->stride[KV_AX_DIM] == 1 && lay->d.head_dim % 8 == 0; }
+bool fast_ok(const kv_layout* lay) {
+  const int32_t cpr = lay->d.head_dim / 8;  // 8-element chunks per row; a power of two for the row kernel
+  return lay->stride[KV_AX_DIM] == 1 && lay->d.head_dim % 8 == 0 && (cpr & (cpr - 1)) == 0;
+}
 
 kv_status same_model(const kv_layout* s, const kv_layout* d) {
   if (s->d.num_layers != d->d.num_layers || s->d.num_kv_heads != d->d.num_kv_heads ||

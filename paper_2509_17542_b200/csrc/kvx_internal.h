@@ -56,7 +56,7 @@ struct ConvArgs {
   // row-tiled fast path: work item = (dst rank, dst block, layer, K/V, row group)
   FastDiv f_cpr;       // 8-element chunks per head_dim row (D / 8)
   FastDiv f_items;     // row groups per (dst rank, dst block, layer, K/V) tile
-  int32_t rows_per_tile, rows_per_item, npass;
+  int32_t rows_per_tile, rows_per_item, npass, cpr_shift;
   uint32_t n_items;
 };
 

@@ -279,12 +279,14 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
 }
 
 // ------------------------------------------------------------------------------------
-// K1/K4 fast path (head_dim innermost on both sides): row-tiled.
-// A work item is a group of `rows_per_item` head_dim rows of one (dst rank, dst block,
-// layer, K/V) tile; the tile-level decode (request, block ids, base pointers) is done once
-// per item and is warp-uniform, so the per-16-byte work is a row decode plus addressing.
-// Lane `lane` handles chunk `lane % cpr` of rows row0 + lane / cpr + k * (32 / cpr) (when
-// cpr divides 32), so every warp instruction moves 32 x 16 contiguous-per-row bytes.
+// K1/K4 fast path (head_dim innermost on both sides, D/8 a power of two): row-tiled.
+// A work item is 32 head_dim rows of one (dst rank, dst block, layer, K/V) tile.  The
+// tile-level decode (request, block ids, base pointers) is warp-uniform; then each lane
+// decodes ONE row (source / destination row pointers, tail flag, fp8 scale) and the warp
+// streams the item's 32 x cpr chunks, fetching row state with register shuffles -- so
+// the per-16-byte work is a few shuffles, one load, the cast and one store.  Each warp
+// instruction covers cpr consecutive chunks of 32/cpr rows: contiguous per row on both
+// sides.  U chunk loads per lane are in flight before the first store.
 // ------------------------------------------------------------------------------------
 template <int SDT, int DDT, int U>
 __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant__ ConvArgs a) {
@@ -292,7 +294,8 @@ __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
-  const uint32_t cpr = a.f_cpr.d;
+  const uint32_t cs = (uint32_t)a.cpr_shift;
+  const uint32_t cmask = (1u << cs) - 1u;
   for (uint32_t item = warp; item < a.n_items; item += nwarps) {
     uint32_t n = item;
     const uint32_t rg = divmod(n, a.f_items);
@@ -305,69 +308,68 @@ __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant
     const int32_t tok0 = __ldg(a.tok_off + r);
     const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
     const uint32_t tb0 = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd;  // first token of the block
-    const int32_t* sids = a.s_blk_ids + __ldg(a.s_blk_off + r);
     const int64_t dblk = __ldg(a.d_blk_ids + bl);
     const int64_t layer = a.lb + (int64_t)l;
-    uint8_t* dtile = a.dst[qi] + (layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK]) *
-                                     Tr<DDT>::B;
-    const int64_t s_lc = layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV];
-    const uint32_t hq0 = (uint32_t)a.dst_rank[qi] * (uint32_t)a.Hd;
-    const uint32_t row0 = rg * (uint32_t)a.rows_per_item;
-    const uint32_t row_end = min(row0 + (uint32_t)a.rows_per_item, (uint32_t)a.rows_per_tile);
-    const float* dsc = nullptr;
-    if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3) dsc = a.dscale[qi] + (layer * 2 + c) * a.Hd;
-#pragma unroll 1
-    for (int pass = 0; pass < a.npass; ++pass) {
+    const uint32_t row0 = rg * 32u;
+    const uint32_t nrows = min(32u, (uint32_t)a.rows_per_tile - row0);
+    // ---- per-lane row state (lane = row within the item) ----
+    uint64_t sp = 0, dp = 0;
+    float rsc = 1.f;  // e4m3 destination: RN(1/s); e4m3 source: s
+    uint32_t rz = 0;  // tail slot: store zeros
+    if (lane < nrows) {
+      uint32_t m = row0 + lane;
+      const uint32_t in0 = divmod(m, a.f_in0);
+      const uint32_t slot = a.slot_inner ? in0 : m;
+      const uint32_t hq = a.slot_inner ? m : in0;
+      dp = (uint64_t)(a.dst[qi] + (layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] +
+                                   dblk * a.ds[KV_AX_BLOCK] + (int64_t)slot * a.ds[KV_AX_SLOT] +
+                                   (int64_t)hq * a.ds[KV_AX_HEAD]) * Tr<DDT>::B);
+      const uint32_t t = tb0 + slot;
+      if ((int32_t)t >= T) {
+        rz = 1;
+      } else {
+        const uint32_t h = (uint32_t)a.dst_rank[qi] * (uint32_t)a.Hd + hq;
+        const uint32_t p = fdiv(h, a.f_hp);
+        const uint32_t hp = h - p * (uint32_t)a.Hp;
+        const int si = a.src_of_p[p];
+        uint32_t tb = t;
+        const uint32_t sslot = divmod(tb, a.f_bp);
+        const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + tb);
+        sp = (uint64_t)(a.src[si] + (layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
+                                     sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
+                                     (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
+        if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3) rsc = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
+        if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3)
+          rsc = __frcp_rn(__ldg(a.dscale[qi] + (layer * 2 + c) * a.Hd + hq));
+      }
+    }
+    // ---- stream the item's chunks ----
+    const uint32_t nch = nrows << cs;
+    for (uint32_t base = 0; base < nch; base += 32u * U) {
       Chunk<SDT, VEC> in[U];
-      uint8_t* dp[U];
-      float ssc[U], inv[U];
-      bool act[U], zero[U];
+      uint64_t d[U];
+      float sc[U];
+      uint32_t z[U], ch[U];
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        const uint32_t idx = (uint32_t)(pass * U + k) * 32u + lane;
-        uint32_t rr = idx;
-        const uint32_t ch = divmod(rr, a.f_cpr);
-        const uint32_t row = row0 + rr;
-        act[k] = row < row_end;
-        zero[k] = false;
-        ssc[k] = 1.f;
-        inv[k] = 1.f;
-        dp[k] = dtile;
-        if (act[k]) {
-          uint32_t m = row;
-          const uint32_t in0 = divmod(m, a.f_in0);
-          const uint32_t slot = a.slot_inner ? in0 : m;
-          const uint32_t hq = a.slot_inner ? m : in0;
-          dp[k] = dtile + ((int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD] + ch * VEC) * Tr<DDT>::B;
-          const uint32_t t = tb0 + slot;
-          if ((int32_t)t >= T) {
-            zero[k] = true;
-          } else {
-            const uint32_t h = hq0 + hq;
-            const uint32_t p = fdiv(h, a.f_hp);
-            const uint32_t hp = h - p * (uint32_t)a.Hp;
-            const int si = a.src_of_p[p];
-            uint32_t tb = t;
-            const uint32_t sslot = divmod(tb, a.f_bp);
-            const int64_t sblk = __ldg(sids + tb);
-            const int64_t soff = s_lc + sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
-                                 (int64_t)hp * a.ss[KV_AX_HEAD] + ch * VEC;
-            load_chunk<SDT, VEC>(in[k], a.src[si] + soff * Tr<SDT>::B);
-            if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3)
-              ssc[k] = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
-            if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3) inv[k] = __frcp_rn(__ldg(dsc + hq));
-          }
-        }
+        const uint32_t idx = base + (uint32_t)k * 32u + lane;
+        const uint32_t rr = (idx >> cs) & 31u;
+        ch[k] = idx & cmask;
+        const uint64_t s = __shfl_sync(0xffffffffu, sp, rr);
+        d[k] = __shfl_sync(0xffffffffu, dp, rr);
+        z[k] = __shfl_sync(0xffffffffu, rz, rr) | (idx >= nch ? 2u : 0u);
+        sc[k] = __shfl_sync(0xffffffffu, rsc, rr);
+        if (z[k] == 0) load_chunk<SDT, VEC>(in[k], reinterpret_cast<const uint8_t*>(s) + ch[k] * (VEC * Tr<SDT>::B));
       }
 #pragma unroll
       for (int k = 0; k < U; ++k) {
-        if (!act[k]) continue;
+        if (z[k] & 2u) continue;
         Chunk<DDT, VEC> o;
-        if (zero[k])
+        if (z[k])
           zero_chunk(o);
         else
-          cast_chunk<SDT, DDT, VEC>(in[k], o, ssc[k], inv[k]);
-        store_chunk<DDT, VEC>(dp[k], o);
+          cast_chunk<SDT, DDT, VEC>(in[k], o, sc[k], sc[k]);
+        store_chunk<DDT, VEC>(reinterpret_cast<uint8_t*>(d[k]) + ch[k] * (VEC * Tr<DDT>::B), o);
       }
     }
   }
@@ -564,17 +566,15 @@ template <int VEC, int SDT, int DDT>
 cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
   constexpr int U = unroll_for<SDT, VEC>();
   if constexpr (VEC == 8) {
-    // row-tiled fast path: size work items to ~kPasses passes of U chunks per lane
-    constexpr int kPasses = 4;
+    // row-tiled fast path: work items of 32 rows (one per lane)
     ConvArgs a = a0;
     const uint32_t cpr = a.f_cpr.d;
     const uint32_t rows_per_tile = (uint32_t)a.Bd * (uint32_t)a.Hd;
-    uint32_t rpi = (32u * U * kPasses) / cpr;
-    if (rpi < 1) rpi = 1;
-    if (rpi > rows_per_tile) rpi = rows_per_tile;
+    const uint32_t rpi = 32u;
     a.rows_per_tile = (int32_t)rows_per_tile;
     a.rows_per_item = (int32_t)rpi;
-    a.npass = (int32_t)((rpi * cpr + 32u * U - 1) / (32u * U));
+    a.cpr_shift = 0;
+    while ((1u << a.cpr_shift) < cpr) ++a.cpr_shift;
     const uint32_t items_per_tile = (rows_per_tile + rpi - 1) / rpi;
     a.f_items = make_fastdiv(items_per_tile);
     const uint64_t n_items = (uint64_t)a.total / ((uint64_t)rows_per_tile * cpr) * items_per_tile;
