@@ -57,6 +57,8 @@ struct ConvArgs {
   FastDiv f_cpr;       // 8-element chunks per head_dim row (D / 8)
   FastDiv f_items;     // row groups per (dst rank, dst block, layer, K/V) tile
   int32_t rows_per_tile, rows_per_item, npass, cpr_shift;
+  FastDiv f_sb;     // slot sub-tiles per tile
+  int32_t ts_log2;  // sub-tile = 2^ts_log2 slots x 2^(5-ts_log2) heads
   uint32_t n_items;
 };
 
@@ -73,6 +75,10 @@ struct PackArgs {
   const int32_t* tok_req;
   FastDiv f_dch, f_tok, f_nh, f_l, f_bp;
   uint32_t total;
+  // row kernel: item = 32 consecutive wire rows (tokens) of one (layer, K/V, head)
+  FastDiv f_tg;  // token groups of 32
+  int32_t cpr_shift;
+  uint32_t n_items;
 };
 
 struct UnpackArgs {
@@ -90,6 +96,10 @@ struct UnpackArgs {
   FastDiv f_dch, f_in0, f_in1, f_l, f_bl, f_bd;
   int32_t slot_inner;
   uint32_t total;
+  // row kernel: item = (dst block, layer, K/V, 2-D sub-tile of slots x overlap heads)
+  FastDiv f_sb, f_items;
+  int32_t cpr_shift, ts_log2;
+  uint32_t n_items;
 };
 
 // launchers (kvx_kernels.cu); vec = 8 (fast path, DIM innermost) or 1 (generic)

@@ -310,17 +310,21 @@ __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant
     const uint32_t tb0 = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd;  // first token of the block
     const int64_t dblk = __ldg(a.d_blk_ids + bl);
     const int64_t layer = a.lb + (int64_t)l;
-    const uint32_t row0 = rg * 32u;
-    const uint32_t nrows = min(32u, (uint32_t)a.rows_per_tile - row0);
+    // the item is a 2-D sub-tile of ts slots x th heads (ts * th = 32): both the source
+    // and the destination see runs of several rows instead of single 256-B rows
+    uint32_t sbk = rg;
+    const uint32_t s_blk = divmod(sbk, a.f_sb);  // sub-tile index along slots; sbk = along heads
+    const uint32_t ts_log2 = (uint32_t)a.ts_log2;
+    const uint32_t ls = a.slot_inner ? (lane & ((1u << ts_log2) - 1u)) : (lane >> (5u - ts_log2));
+    const uint32_t lh = a.slot_inner ? (lane >> ts_log2) : (lane & ((1u << (5u - ts_log2)) - 1u));
+    const uint32_t slot = (s_blk << ts_log2) + ls;
+    const uint32_t hq = (sbk << (5u - ts_log2)) + lh;
     // ---- per-lane row state (lane = row within the item) ----
     uint64_t sp = 0, dp = 0;
     float rsc = 1.f;  // e4m3 destination: RN(1/s); e4m3 source: s
-    uint32_t rz = 0;  // tail slot: store zeros
-    if (lane < nrows) {
-      uint32_t m = row0 + lane;
-      const uint32_t in0 = divmod(m, a.f_in0);
-      const uint32_t slot = a.slot_inner ? in0 : m;
-      const uint32_t hq = a.slot_inner ? m : in0;
+    uint32_t rz = 2;  // 2: no row (outside the tile); 1: tail slot, store zeros; 0: copy
+    if (slot < (uint32_t)a.Bd && hq < (uint32_t)a.Hd) {
+      rz = 0;
       dp = (uint64_t)(a.dst[qi] + (layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] +
                                    dblk * a.ds[KV_AX_BLOCK] + (int64_t)slot * a.ds[KV_AX_SLOT] +
                                    (int64_t)hq * a.ds[KV_AX_HEAD]) * Tr<DDT>::B);
@@ -344,7 +348,7 @@ __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant
       }
     }
     // ---- stream the item's chunks ----
-    const uint32_t nch = nrows << cs;
+    const uint32_t nch = 32u << cs;
     for (uint32_t base = 0; base < nch; base += 32u * U) {
       Chunk<SDT, VEC> in[U];
       uint64_t d[U];
@@ -575,7 +579,27 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
     a.rows_per_item = (int32_t)rpi;
     a.cpr_shift = 0;
     while ((1u << a.cpr_shift) < cpr) ++a.cpr_shift;
-    const uint32_t items_per_tile = (rows_per_tile + rpi - 1) / rpi;
+    // sub-tile shape: up to 8 heads x (32 / heads) slots, fewer slots for small blocks
+    auto pow2ceil = [](uint32_t x) { uint32_t p = 1; while (p < x) p <<= 1; return p; };
+    uint32_t th = pow2ceil(std::min<uint32_t>((uint32_t)a.Hd, 8u));
+    uint32_t ts = 32u / th;
+    if (ts > pow2ceil((uint32_t)a.Bd)) {
+      ts = pow2ceil((uint32_t)a.Bd);
+      th = 32u / ts;
+    }
+    if (const char* e = getenv("KVX_TS")) {  // experiment override: slots per sub-tile
+      const uint32_t v = (uint32_t)atoi(e);
+      if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) {
+        ts = v;
+        th = 32u / v;
+      }
+    }
+    a.ts_log2 = 0;
+    while ((1u << a.ts_log2) < ts) ++a.ts_log2;
+    const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.Hd + th - 1) / th;
+    a.f_sb = make_fastdiv(nsb);
+    const uint32_t items_per_tile = nsb * nhb;
+    (void)rpi;
     a.f_items = make_fastdiv(items_per_tile);
     const uint64_t n_items = (uint64_t)a.total / ((uint64_t)rows_per_tile * cpr) * items_per_tile;
     a.n_items = (uint32_t)n_items;
