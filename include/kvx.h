@@ -209,6 +209,11 @@ kv_status kv_ipc_export(const void* dev_ptr, uint8_t out_handle[64], uint64_t* o
 kv_status kv_ipc_open(const uint8_t handle[64], uint64_t offset, void** out_ptr);
 kv_status kv_ipc_close(void* mapped_base);
 
+/* Single-process multi-GPU alternative to IPC: let the current device access peer_device's
+ * memory directly (cudaDeviceEnablePeerAccess; already-enabled is not an error).
+ * KV_EUNSUPPORTED if the pair has no peer path. */
+kv_status kv_peer_enable(int32_t peer_device);
+
 /* A11 completion.  kv_signal: after all prior work on `stream`, a system-scope release
  * store of `value` to *flag (local or peer-mapped 4-byte device word).  kv_wait: enqueue
  * a one-warp kernel that spins (acquire, system scope) until *flag >= value or timeout_ns

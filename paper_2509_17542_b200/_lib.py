@@ -72,6 +72,7 @@ def _load():
         "kv_ipc_export": (st, [p, p, C.POINTER(u64)]),
         "kv_ipc_open": (st, [p, u64, C.POINTER(p)]),
         "kv_ipc_close": (st, [p]),
+        "kv_peer_enable": (st, [i32]),
         "kv_signal": (st, [p, C.c_uint32, p]),
         "kv_wait": (st, [p, C.c_uint32, u64, p, p]),
         "kv_launch_count": (u64, []),
@@ -92,7 +93,7 @@ lib = _load()
 EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_block_table_update", "kv_plan_pairs",
            "kv_convert_reshard", "kv_wire_dtype", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
            "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
-           "kv_recv_unpack", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_signal", "kv_wait",
+           "kv_recv_unpack", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",
            "kv_launch_count", "kv_launch_count_reset", "kv_last_error", "kv_version")
 
 

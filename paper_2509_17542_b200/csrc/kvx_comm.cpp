@@ -171,6 +171,21 @@ kv_status kv_ipc_close(void* mapped_base) {
   return fail(KV_EINVAL, "kv_ipc_close: address was not returned by kv_ipc_open (pass pointer - offset)");
 }
 
+kv_status kv_peer_enable(int32_t peer_device) {
+  int dev = 0, ok = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_peer_enable: cudaGetDevice");
+  e = cudaDeviceCanAccessPeer(&ok, dev, peer_device);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_peer_enable: cudaDeviceCanAccessPeer");
+  if (!ok) return fail(KV_EUNSUPPORTED, "kv_peer_enable: no peer path between the devices");
+  e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();
+    return KV_OK;
+  }
+  return e == cudaSuccess ? KV_OK : cuda_fail(e, "cudaDeviceEnablePeerAccess");
+}
+
 kv_status kv_signal(uint32_t* flag, uint32_t value, kv_stream stream) {
   if (!flag) return fail(KV_EINVAL, "kv_signal: null flag");
   cudaError_t e = launch_signal(flag, value, (cudaStream_t)stream);

@@ -279,6 +279,47 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
 }
 
 // ------------------------------------------------------------------------------------
+// Shared inner loop of the row kernels.  Lane i holds the state of row i of a 32-row
+// item: source row address sp, destination row address dp, its scale rsc and rz
+// (0 copy, 1 zero-fill tail row, 2 no row).  The warp streams the 32 x 2^cs chunks of
+// 16 B (source side) with U loads in flight per lane, fetching row state by shuffles.
+// ------------------------------------------------------------------------------------
+template <int SDT, int DDT, int U>
+__device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t sp, uint64_t dp, float rsc,
+                                            uint32_t rz) {
+  constexpr int VEC = 8;
+  const uint32_t cmask = (1u << cs) - 1u;
+  const uint32_t nch = 32u << cs;
+  for (uint32_t base = 0; base < nch; base += 32u * U) {
+    Chunk<SDT, VEC> in[U];
+    uint64_t d[U];
+    float sc[U];
+    uint32_t z[U], ch[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t idx = base + (uint32_t)k * 32u + lane;
+      const uint32_t rr = (idx >> cs) & 31u;
+      ch[k] = idx & cmask;
+      const uint64_t s = __shfl_sync(0xffffffffu, sp, rr);
+      d[k] = __shfl_sync(0xffffffffu, dp, rr);
+      z[k] = __shfl_sync(0xffffffffu, rz, rr) | (idx >= nch ? 2u : 0u);
+      sc[k] = __shfl_sync(0xffffffffu, rsc, rr);
+      if (z[k] == 0) load_chunk<SDT, VEC>(in[k], reinterpret_cast<const uint8_t*>(s) + ch[k] * (VEC * Tr<SDT>::B));
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      if (z[k] & 2u) continue;
+      Chunk<DDT, VEC> o;
+      if (z[k])
+        zero_chunk(o);
+      else
+        cast_chunk<SDT, DDT, VEC>(in[k], o, sc[k], sc[k]);
+      store_chunk<DDT, VEC>(reinterpret_cast<uint8_t*>(d[k]) + ch[k] * (VEC * Tr<DDT>::B), o);
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // K1/K4 fast path (head_dim innermost on both sides, D/8 a power of two): row-tiled.
 // A work item is 32 head_dim rows of one (dst rank, dst block, layer, K/V) tile.  The
 // tile-level decode (request, block ids, base pointers) is warp-uniform; then each lane
@@ -290,12 +331,10 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
 // ------------------------------------------------------------------------------------
 template <int SDT, int DDT, int U>
 __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant__ ConvArgs a) {
-  constexpr int VEC = 8;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
   const uint32_t cs = (uint32_t)a.cpr_shift;
-  const uint32_t cmask = (1u << cs) - 1u;
   for (uint32_t item = warp; item < a.n_items; item += nwarps) {
     uint32_t n = item;
     const uint32_t rg = divmod(n, a.f_items);
@@ -347,35 +386,102 @@ __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant
           rsc = __frcp_rn(__ldg(a.dscale[qi] + (layer * 2 + c) * a.Hd + hq));
       }
     }
-    // ---- stream the item's chunks ----
-    const uint32_t nch = 32u << cs;
-    for (uint32_t base = 0; base < nch; base += 32u * U) {
-      Chunk<SDT, VEC> in[U];
-      uint64_t d[U];
-      float sc[U];
-      uint32_t z[U], ch[U];
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        const uint32_t idx = base + (uint32_t)k * 32u + lane;
-        const uint32_t rr = (idx >> cs) & 31u;
-        ch[k] = idx & cmask;
-        const uint64_t s = __shfl_sync(0xffffffffu, sp, rr);
-        d[k] = __shfl_sync(0xffffffffu, dp, rr);
-        z[k] = __shfl_sync(0xffffffffu, rz, rr) | (idx >= nch ? 2u : 0u);
-        sc[k] = __shfl_sync(0xffffffffu, rsc, rr);
-        if (z[k] == 0) load_chunk<SDT, VEC>(in[k], reinterpret_cast<const uint8_t*>(s) + ch[k] * (VEC * Tr<SDT>::B));
-      }
-#pragma unroll
-      for (int k = 0; k < U; ++k) {
-        if (z[k] & 2u) continue;
-        Chunk<DDT, VEC> o;
-        if (z[k])
-          zero_chunk(o);
-        else
-          cast_chunk<SDT, DDT, VEC>(in[k], o, sc[k], sc[k]);
-        store_chunk<DDT, VEC>(reinterpret_cast<uint8_t*>(d[k]) + ch[k] * (VEC * Tr<DDT>::B), o);
+    stream_rows<SDT, DDT, U>(lane, cs, sp, dp, rsc, rz);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K2 fast path: pack (Fig. 5 flatten) with the row machinery.  Item = 32 consecutive
+// tokens of one (layer, K/V, overlap head): the wire side is one contiguous 32-row run,
+// each lane gathers its token's row through the block table.
+// ------------------------------------------------------------------------------------
+template <int SDT, int WDT, int U>
+__global__ void __launch_bounds__(kThreads) k_pack_rows(const __grid_constant__ PackArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
+  const uint32_t cs = (uint32_t)a.cpr_shift;
+  const uint32_t T_all = a.f_tok.d;
+  for (uint32_t item = warp; item < a.n_items; item += nwarps) {
+    uint32_t n = item;
+    const uint32_t tg = divmod(n, a.f_tg);
+    const uint32_t hh = divmod(n, a.f_nh);
+    const uint32_t c = n & 1u;
+    const uint32_t l = n >> 1;
+    const int64_t layer = a.lb + (int64_t)l;
+    const uint32_t tok = tg * 32u + lane;
+    uint64_t sp = 0, dp = 0;
+    float rsc = 1.f;
+    uint32_t rz = 2;
+    if (tok < T_all) {
+      rz = 0;
+      const int32_t r = __ldg(a.tok_req + tok);
+      uint32_t t = tok - (uint32_t)__ldg(a.tok_off + r);
+      const uint32_t sslot = divmod(t, a.f_bp);
+      const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + t);
+      const uint32_t h = (uint32_t)a.hb + hh;
+      const uint32_t hp = h - (uint32_t)a.p * (uint32_t)a.Hp;
+      sp = (uint64_t)(a.src + (layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
+                               (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
+      dp = (uint64_t)(a.wire + ((((uint64_t)l * 2 + c) * (uint64_t)a.nh + hh) * T_all + tok) * (uint64_t)a.D * Tr<WDT>::B);
+      if constexpr (SDT == KV_F8E4M3 && WDT != KV_F8E4M3) rsc = __ldg(a.sscale + (layer * 2 + c) * a.Hp + hp);
+      if constexpr (WDT == KV_F8E4M3 && SDT != KV_F8E4M3)
+        rsc = __frcp_rn(__ldg(a.dscale + (layer * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)));
+    }
+    stream_rows<SDT, WDT, U>(lane, cs, sp, dp, rsc, rz);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K3 fast path: unpack (Fig. 5 restore).  Item = (dst block, layer, K/V, sub-tile of
+// slots x overlap heads); each lane owns one destination row and finds its wire row.
+// ------------------------------------------------------------------------------------
+template <int WDT, int DDT, int U>
+__global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant__ UnpackArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
+  const uint32_t cs = (uint32_t)a.cpr_shift;
+  for (uint32_t item = warp; item < a.n_items; item += nwarps) {
+    uint32_t n = item;
+    uint32_t sbk = divmod(n, a.f_items);
+    const uint32_t c = n & 1u;
+    n >>= 1;
+    const uint32_t l = divmod(n, a.f_l);
+    const uint32_t bl = n;
+    const uint32_t s_blk = divmod(sbk, a.f_sb);
+    const uint32_t ts_log2 = (uint32_t)a.ts_log2;
+    const uint32_t ls = a.slot_inner ? (lane & ((1u << ts_log2) - 1u)) : (lane >> (5u - ts_log2));
+    const uint32_t lh = a.slot_inner ? (lane >> ts_log2) : (lane & ((1u << (5u - ts_log2)) - 1u));
+    const uint32_t slot = (s_blk << ts_log2) + ls;
+    const uint32_t hh = (sbk << (5u - ts_log2)) + lh;
+    const int32_t r = __ldg(a.d_blk_req + bl);
+    const int32_t tok0 = __ldg(a.tok_off + r);
+    const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+    const int64_t layer = a.lb + (int64_t)l;
+    uint64_t sp = 0, dp = 0;
+    float rsc = 1.f;
+    uint32_t rz = 2;
+    if (slot < (uint32_t)a.Bd && hh < (uint32_t)a.nh) {
+      rz = 0;
+      const uint32_t t = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd + slot;
+      const int64_t dblk = __ldg(a.d_blk_ids + bl);
+      const uint32_t h = (uint32_t)a.hb + hh;
+      const uint32_t hq = h - (uint32_t)a.q * (uint32_t)a.Hd;
+      dp = (uint64_t)(a.dst + (layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
+                               (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD]) * Tr<DDT>::B);
+      if ((int32_t)t >= T) {
+        rz = 1;
+      } else {
+        sp = (uint64_t)(a.wire + ((((uint64_t)l * 2 + c) * (uint64_t)a.nh + hh) * (uint64_t)a.total_tokens +
+                                  (uint64_t)(tok0 + t)) * (uint64_t)a.D * Tr<WDT>::B);
+        if constexpr (WDT == KV_F8E4M3 && DDT != KV_F8E4M3)
+          rsc = __ldg(a.sscale + (layer * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
+        if constexpr (DDT == KV_F8E4M3 && WDT != KV_F8E4M3)
+          rsc = __frcp_rn(__ldg(a.dscale + (layer * 2 + c) * a.Hd + hq));
       }
     }
+    stream_rows<WDT, DDT, U>(lane, cs, sp, dp, rsc, rz);
   }
 }
 
@@ -560,6 +666,49 @@ int grid_for(K kernel, uint64_t total, int per_thread) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// Row kernels: one warp per 32-row item; grid = min(items / 8 warps, SMs x occupancy).
+template <typename K>
+int grid_for_items(K kernel, uint64_t n_items) {
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, 0);
+  if (occ < 1) occ = 1;
+  const uint64_t need = (n_items + (kThreads / 32) - 1) / (kThreads / 32);
+  const uint64_t cap = (uint64_t)num_sms() * occ;
+  return (int)std::max<uint64_t>(1, std::min(need, cap));
+}
+
+int32_t log2_pow2(uint32_t x) {
+  int32_t l = 0;
+  while ((1u << l) < x) ++l;
+  return l;
+}
+
+// Sub-tile of an item: ts slots x th heads, ts * th = 32.  Up to 8 heads (so a P-side
+// run of several heads and a D-side run of several slots are both >= 1 KB for D = 128),
+// fewer slots when blocks are small.  KVX_TS overrides ts (experiments only).
+void subtile_shape(uint32_t Bd, uint32_t H, uint32_t* ts_out, uint32_t* th_out) {
+  auto pow2ceil = [](uint32_t x) {
+    uint32_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+  };
+  uint32_t th = pow2ceil(std::min<uint32_t>(H, 8u));
+  uint32_t ts = 32u / th;
+  if (ts > pow2ceil(Bd)) {
+    ts = pow2ceil(Bd);
+    th = 32u / ts;
+  }
+  if (const char* e = getenv("KVX_TS")) {
+    const uint32_t v = (uint32_t)atoi(e);
+    if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) {
+      ts = v;
+      th = 32u / v;
+    }
+  }
+  *ts_out = ts;
+  *th_out = th;
+}
+
 // U chunks per thread per segment: keep ~64 B of loads in flight per thread.
 template <int SDT, int VEC>
 constexpr int unroll_for() {
@@ -570,47 +719,21 @@ template <int VEC, int SDT, int DDT>
 cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
   constexpr int U = unroll_for<SDT, VEC>();
   if constexpr (VEC == 8) {
-    // row-tiled fast path: work items of 32 rows (one per lane)
+    // row-tiled fast path: work items of 32 rows (one per lane) = 2-D sub-tiles
     ConvArgs a = a0;
     const uint32_t cpr = a.f_cpr.d;
-    const uint32_t rows_per_tile = (uint32_t)a.Bd * (uint32_t)a.Hd;
-    const uint32_t rpi = 32u;
-    a.rows_per_tile = (int32_t)rows_per_tile;
-    a.rows_per_item = (int32_t)rpi;
-    a.cpr_shift = 0;
-    while ((1u << a.cpr_shift) < cpr) ++a.cpr_shift;
-    // sub-tile shape: up to 8 heads x (32 / heads) slots, fewer slots for small blocks
-    auto pow2ceil = [](uint32_t x) { uint32_t p = 1; while (p < x) p <<= 1; return p; };
-    uint32_t th = pow2ceil(std::min<uint32_t>((uint32_t)a.Hd, 8u));
-    uint32_t ts = 32u / th;
-    if (ts > pow2ceil((uint32_t)a.Bd)) {
-      ts = pow2ceil((uint32_t)a.Bd);
-      th = 32u / ts;
-    }
-    if (const char* e = getenv("KVX_TS")) {  // experiment override: slots per sub-tile
-      const uint32_t v = (uint32_t)atoi(e);
-      if (v >= 1 && v <= 32 && (v & (v - 1)) == 0) {
-        ts = v;
-        th = 32u / v;
-      }
-    }
-    a.ts_log2 = 0;
-    while ((1u << a.ts_log2) < ts) ++a.ts_log2;
+    a.rows_per_tile = a.Bd * a.Hd;
+    a.rows_per_item = 32;
+    a.cpr_shift = log2_pow2(cpr);
+    uint32_t ts, th;
+    subtile_shape((uint32_t)a.Bd, (uint32_t)a.Hd, &ts, &th);
+    a.ts_log2 = log2_pow2(ts);
     const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.Hd + th - 1) / th;
     a.f_sb = make_fastdiv(nsb);
-    const uint32_t items_per_tile = nsb * nhb;
-    (void)rpi;
-    a.f_items = make_fastdiv(items_per_tile);
-    const uint64_t n_items = (uint64_t)a.total / ((uint64_t)rows_per_tile * cpr) * items_per_tile;
-    a.n_items = (uint32_t)n_items;
+    a.f_items = make_fastdiv(nsb * nhb);
+    a.n_items = (uint32_t)((uint64_t)a.total / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);
     auto k = k_convert_rows<SDT, DDT, U>;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, 0);
-    if (occ < 1) occ = 1;
-    const uint64_t need = (n_items + (kThreads / 32) - 1) / (kThreads / 32);
-    const uint64_t cap = (uint64_t)num_sms() * occ;
-    const int grid = (int)std::max<uint64_t>(1, std::min(need, cap));
-    k<<<grid, kThreads, 0, s>>>(a);
+    k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
   } else {
     auto k = k_convert<VEC, SDT, DDT, U>;
     k<<<grid_for(k, a0.total, U), kThreads, 0, s>>>(a0);
@@ -619,18 +742,43 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
   return cudaGetLastError();
 }
 template <int VEC, int SDT, int WDT>
-cudaError_t pack_t(const PackArgs& a, cudaStream_t s) {
+cudaError_t pack_t(const PackArgs& a0, cudaStream_t s) {
   constexpr int U = unroll_for<SDT, VEC>();
-  auto k = k_pack<VEC, SDT, WDT, U>;
-  k<<<grid_for(k, a.total, U), kThreads, 0, s>>>(a);
+  if constexpr (VEC == 8) {
+    PackArgs a = a0;
+    a.cpr_shift = log2_pow2(a.f_dch.d);
+    const uint32_t T_all = a.f_tok.d;
+    const uint32_t ntg = (T_all + 31u) / 32u;
+    a.f_tg = make_fastdiv(ntg);
+    a.n_items = (uint32_t)a.Lc * 2u * (uint32_t)a.nh * ntg;
+    auto k = k_pack_rows<SDT, WDT, U>;
+    k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
+  } else {
+    auto k = k_pack<VEC, SDT, WDT, U>;
+    k<<<grid_for(k, a0.total, U), kThreads, 0, s>>>(a0);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
 template <int VEC, int WDT, int DDT>
-cudaError_t unpack_t(const UnpackArgs& a, cudaStream_t s) {
+cudaError_t unpack_t(const UnpackArgs& a0, cudaStream_t s) {
   constexpr int U = unroll_for<WDT, VEC>();
-  auto k = k_unpack<VEC, WDT, DDT, U>;
-  k<<<grid_for(k, a.total, U), kThreads, 0, s>>>(a);
+  if constexpr (VEC == 8) {
+    UnpackArgs a = a0;
+    a.cpr_shift = log2_pow2(a.f_dch.d);
+    uint32_t ts, th;
+    subtile_shape((uint32_t)a.Bd, (uint32_t)a.nh, &ts, &th);
+    a.ts_log2 = log2_pow2(ts);
+    const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.nh + th - 1) / th;
+    a.f_sb = make_fastdiv(nsb);
+    a.f_items = make_fastdiv(nsb * nhb);
+    a.n_items = a.f_bl.d * (uint32_t)a.Lc * 2u * nsb * nhb;
+    auto k = k_unpack_rows<WDT, DDT, U>;
+    k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
+  } else {
+    auto k = k_unpack<VEC, WDT, DDT, U>;
+    k<<<grid_for(k, a0.total, U), kThreads, 0, s>>>(a0);
+  }
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

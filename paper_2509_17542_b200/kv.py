@@ -13,7 +13,7 @@ from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BY
                    KV_F32, Batch_t, KvError, LayoutDesc, check, lib)
 
 __all__ = ["Layout", "Batch", "convert_reshard", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
-           "Comm", "ipc_export", "ipc_open", "ipc_close", "signal", "wait", "launch_count", "launch_count_reset",
+           "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "launch_count", "launch_count_reset",
            "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "DTYPE_BYTES",
            "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
 
@@ -222,6 +222,11 @@ def ipc_open(handle: bytes, offset: int) -> int:
 
 def ipc_close(mapped_ptr: int, offset: int):
     check(lib.kv_ipc_close(mapped_ptr - offset))
+
+
+def peer_enable(peer_device: int):
+    """kv_peer_enable: the current device may access peer_device's memory (single process)."""
+    check(lib.kv_peer_enable(peer_device))
 
 
 def signal(flag, value, stream=None):
