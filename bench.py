@@ -317,7 +317,7 @@ def run_single(args):
                    "l2": "inputs larger than L2 (no flush)", "parallelism": "none (1 GPU)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _traffic(wl_name, 1),
-                     "kernel": "k_convert", "kernel_ms": round(kern_ms, 5),
+                     "kernel": "k_convert_rows", "kernel_ms": round(kern_ms, 5),
                      "algorithmic_bytes_per_launch": alg, "peak_source": peaks["source"],
                      "frac_vs_nominal_8TBs": round(achieved / 8000.0, 4)},
         "clocks": clk, "gpu_launches": int(launches),
@@ -638,11 +638,166 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def run_stream(args):
+    """c5: mixed-length request stream (T ~ logU[512, 32k], 64 requests) from two P instances
+    (TP2 each, requests alternate A/B) to one D instance (TP4), per-layer pipelined push.
+    N GPUs: N/2 P ranks (instances A, B; ranks 0.. of each) and N/2 D ranks (0..N/2-1); N=8 is
+    the full c5, N=4 its per-GPU-equivalent sub-config c5' (A0 + B0 -> D0, D1).  Every request
+    is ready at t=0 and pushed in order, one fused convert launch per (request, layer chunk)
+    covering all of the P rank's D peers; per-request completion is a release flag."""
+    import dataclasses
+    import torch
+    import torch.distributed as dist
+    import paper_2509_17542_b200 as kvx
+    from paper_2509_17542_b200 import transfer as tr
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.configs()["c5"]
+    n_p = n_d = world // 2
+    n_inst = 2 if n_p >= 2 else 1
+    per_inst = n_p // n_inst
+    inst_req = [list(range(i, len(cfg.n_tokens), 2)) for i in range(n_inst)]
+    is_p = rank < n_p
+    d_ranks = list(range(n_d))
+    stream = torch.cuda.current_stream()
+    K = args.steps
+    # D side: one pool for all requests of both instances; flags[p_world] = requests landed
+    d_cfg = cfg
+    NB_d = synth.pool_capacity(cfg.n_tokens, cfg.B_d)
+    dst_tables = synth.block_tables(cfg.seed + 2, cfg.n_tokens, cfg.B_d, NB_d)
+    flags = torch.zeros(max(n_p, 1) * 8, dtype=torch.int32, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    mine = None
+    if not is_p:
+        q = rank - n_p
+        dd = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, NB_d, cfg.dst_dtype, cfg.d_order)
+        dl = kvx.Layout.from_dict(dd)
+        pool = dl.new_pool(dev, fill=synth.CANARY)
+        mine = {"q": q, "pool": kvx.ipc_export(pool), "flags": kvx.ipc_export(flags)}
+    allx = tr.exchange(mine)
+    peers = {e["q"]: e for e in allx if e is not None}
+    src_bytes = 0
+    lat = []
+    if is_p:
+        inst, p = rank // per_inst, rank % per_inst
+        reqs = inst_req[inst]
+        icfg = dataclasses.replace(cfg, n_tokens=[cfg.n_tokens[r] for r in reqs], seed=cfg.seed + 10 * inst)
+        NB_p = synth.pool_capacity(icfg.n_tokens, cfg.B_p)
+        src_tables = synth.block_tables(icfg.seed + 1, icfg.n_tokens, cfg.B_p, NB_p)
+        sd = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, NB_p, cfg.src_dtype, cfg.p_order)
+        sl = kvx.Layout.from_dict(sd)
+        spool = sl.new_pool(dev)
+        synth.fill_random_finite_(spool.view(torch.int16), icfg.seed + 100 + p, cfg.src_dtype)
+        pairs = tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks={p}, d_ranks=set(d_ranks))
+        qs = [q for _, q, _, _ in pairs]
+        dls = [kvx.Layout.from_dict(synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, NB_d, cfg.dst_dtype,
+                                                 cfg.d_order)) for q in qs]
+        ppools = [kvx.ipc_open(*peers[q]["pool"]) for q in qs]
+        pflags = [kvx.ipc_open(*peers[q]["flags"]) + 4 * rank for q in qs]
+        # per-request tables (one Batch per request on each side)
+        sbt = [kvx.Batch(sl, [icfg.n_tokens[i]], [src_tables[i]], dev) for i in range(len(reqs))]
+        dbt = [kvx.Batch(dls[0], [cfg.n_tokens[r]], [dst_tables[r]], dev) for r in reqs]
+        per_tok_layer = 2 * cfg.D * (cfg.H // cfg.tp_p) * synth.NBYTES[cfg.src_dtype]
+        chunks = [max(1, -(-(8 << 20) // (per_tok_layer * t))) for t in icfg.n_tokens]
+        src_bytes = sum(cfg.L * per_tok_layer * t for t in icfg.n_tokens)
+        count = [0]
+
+        def step(evs=None):
+            for i in range(len(reqs)):
+                lc = args.layer_chunk or chunks[i]
+                for l0 in range(0, cfg.L, lc):
+                    kvx.convert_reshard([sl], [spool], sbt[i], dls, ppools, dbt[i], (l0, min(cfg.L, l0 + lc)), stream)
+                count[0] += 1
+                for f in pflags:
+                    kvx.signal(f, count[0], stream)
+                if evs is not None:
+                    evs[i].record(stream)
+        expected_per_step = 0
+    else:
+        q = rank - n_p
+        srcs = [pr for pr in range(n_p) if any(qq == q for _, qq, _, _ in
+                                               tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks={pr % per_inst}))]
+        n_req_of = {pr: len(inst_req[pr // per_inst]) for pr in srcs}
+        count = [0]
+
+        def step(evs=None):
+            count[0] += 1
+            for pr in srcs:
+                kvx.wait(flags[pr:pr + 1], count[0] * n_req_of[pr], err, 60.0, stream)
+    barrier_t = torch.zeros(1, device=dev)
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    dist.all_reduce(barrier_t)
+    torch.cuda.synchronize()
+    nreq_mine = len(inst_req[rank // per_inst]) if is_p else 0
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nreq_mine)] for _ in range(K)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    kvx.launch_count_reset()
+    dist.all_reduce(barrier_t)
+    t0.record(stream)
+    for k in range(K):
+        step(evs[k] if is_p else None)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = kvx.launch_count()
+    if int(err.item()):
+        raise SystemExit(f"rank {rank}: flag wait timed out")
+    my_ms = t0.elapsed_time(t1)
+    if is_p:
+        # latency of request i in step k = its completion - the step's start (previous step end)
+        prev = t0
+        for k in range(K):
+            for i in range(nreq_mine):
+                lat.append(prev.elapsed_time(evs[k][i]))
+            prev = evs[k][-1] if nreq_mine else prev
+    info = tr.exchange({"ms": my_ms, "src_bytes": src_bytes, "lat": lat, "launches": launches,
+                        "nreq": nreq_mine})
+    if rank == 0:
+        max_ms = max(x["ms"] for x in info)
+        ms = max_ms / K
+        tot_b = sum(x["src_bytes"] for x in info)
+        nreq = sum(x["nreq"] for x in info) // max(per_inst, 1)
+        alll = sorted(l for x in info for l in x["lat"])
+        # NVLink roofline: the busiest D rank's ingress (all its heads of every request moved)
+        d_in = 2 * cfg.L * (cfg.H // cfg.tp_d) * cfg.D * synth.NBYTES[cfg.dst_dtype] * sum(
+            synth.blocks_for(cfg.n_tokens[r], cfg.B_d) * cfg.B_d for i in range(n_inst) for r in inst_req[i])
+        t_roof = d_in / (NVLINK_MEASURED_GBS * 1e9) * 1e3
+        out = {"metric": METRIC, "value": round(tot_b / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "n_gpus": world,
+               "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+               "ms_per_request": round(ms / max(nreq, 1), 4), "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": _dtype_name(cfg), "data": "synthetic (seeded)",
+               "config": {"workload": f"c5 stream: {cfg.note}; {n_inst} P instance(s) x {per_inst} rank(s) -> "
+                                      f"D ranks {d_ranks}" + (" (full c5)" if world == 8 else " (c5' sub-config)"),
+                          "requests": nreq, "src_bytes_per_step": tot_b, "mode": "push per request, layer chunks "
+                          ">= 8 MiB", "l2": "inputs larger than L2 (no flush)"},
+               "latency_ms": {"p50": round(alll[len(alll) // 2], 3) if alll else None,
+                              "p99": round(alll[min(len(alll) - 1, int(0.99 * len(alll)))], 3) if alll else None,
+                              "note": "per request, from the step start, requests issued in order"},
+               "roofline": {"bound": "nvlink", "achieved": round(d_in / (ms * 1e-3) / 1e9, 1),
+                            "peak": NVLINK_MEASURED_GBS, "unit": "GB/s", "frac": round(t_roof / ms, 4),
+                            "traffic": None, "kernel": "k_convert_rows (peer-store push, per request)",
+                            "algorithmic_bytes_per_step": d_in, "note": "busiest D rank ingress / step time"},
+               "clocks": clk, "gpu_launches": int(sum(x["launches"] for x in info))}
+        print(json.dumps(out), flush=True)
+    dist.all_reduce(barrier_t)
+    torch.cuda.synchronize()
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        if args.workload == "c5":
+            return run_stream(args)
         return run_multi(args)
     return run_single(args)
 

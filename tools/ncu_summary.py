@@ -48,7 +48,7 @@ def full(rep, out, traffic_key=None):
         r = res[0]
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         tb = sum(r[k]["value"] * scale.get(r[k]["unit"], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
-        p = os.path.join(os.path.dirname(out), "traffic.json")
+        p = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "profiles", "traffic.json")
         t = json.load(open(p)) if os.path.exists(p) else {}
         t[traffic_key] = int(tb)
         json.dump(t, open(p, "w"), indent=1)
