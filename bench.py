@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="push", choices=["push", "nccl"])
     ap.add_argument("--layer-chunk", type=int, default=0, help="layers per chunk (0 = whole model)")
+    ap.add_argument("--chunk-mib", type=int, default=64, help="c5: merge layers until a chunk moves this much")
     ap.add_argument("--workload", default=None, help="override: c1..c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -701,7 +702,8 @@ def run_stream(args):
         sbt = [kvx.Batch(sl, [icfg.n_tokens[i]], [src_tables[i]], dev) for i in range(len(reqs))]
         dbt = [kvx.Batch(dls[0], [cfg.n_tokens[r]], [dst_tables[r]], dev) for r in reqs]
         per_tok_layer = 2 * cfg.D * (cfg.H // cfg.tp_p) * synth.NBYTES[cfg.src_dtype]
-        chunks = [max(1, -(-(8 << 20) // (per_tok_layer * t))) for t in icfg.n_tokens]
+        chunk_bytes = args.chunk_mib << 20
+        chunks = [max(1, -(-chunk_bytes // (per_tok_layer * t))) for t in icfg.n_tokens]
         src_bytes = sum(cfg.L * per_tok_layer * t for t in icfg.n_tokens)
         count = [0]
 
@@ -775,8 +777,9 @@ def run_stream(args):
                "vs_baseline": None, "dtype": _dtype_name(cfg), "data": "synthetic (seeded)",
                "config": {"workload": f"c5 stream: {cfg.note}; {n_inst} P instance(s) x {per_inst} rank(s) -> "
                                       f"D ranks {d_ranks}" + (" (full c5)" if world == 8 else " (c5' sub-config)"),
-                          "requests": nreq, "src_bytes_per_step": tot_b, "mode": "push per request, layer chunks "
-                          ">= 8 MiB", "l2": "inputs larger than L2 (no flush)"},
+                          "requests": nreq, "src_bytes_per_step": tot_b,
+                          "mode": f"push per request, layer chunks >= {args.chunk_mib} MiB",
+                          "l2": "inputs larger than L2 (no flush)"},
                "latency_ms": {"p50": round(alll[len(alll) // 2], 3) if alll else None,
                               "p99": round(alll[min(len(alll) - 1, int(0.99 * len(alll)))], 3) if alll else None,
                               "note": "per request, from the step start, requests issued in order"},

@@ -151,6 +151,19 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
                              void* const* dst_pools, const kv_batch* dst_bt, int32_t layer_begin,
                              int32_t layer_end, kv_stream stream);
 
+/* ---- NEXT-1: dynamic fp8 scales --------------------------------------------------- */
+
+/* Per-batch dequant scales for the heads of D rank `dst` (precision alignment):
+ *   s[l][c][hq] = RN_f32(amax / 448),  amax = max |x| over every finite source element of
+ *   the batch's valid tokens (x as f32; e4m3 sources dequantised with their own scale),
+ * for layers [layer_begin, layer_end); s = 1 where amax is 0 or no finite element exists.
+ * Reads the P pools that hold dst's heads (every needed P rank must be listed, KV_ESHAPE
+ * otherwise).  out_scales: DEVICE float [L][2][H/tp_d]; entries outside the layer range are
+ * untouched.  Pass the array as the scales of an e4m3 destination layout for the convert. */
+kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                            const kv_batch* src_bt, const kv_layout* dst, float* out_scales, int32_t layer_begin,
+                            int32_t layer_end, kv_stream stream);
+
 /* ---- A5 / A9: wire format (Fig. 5 flatten / restore) ----------------------------- */
 
 /* Wire dtype of a (src, dst) pair: the narrower of the two (dst on a tie), so a

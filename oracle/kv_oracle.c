@@ -467,3 +467,40 @@ void okv_cast_array(int64_t n, const void* in, int32_t src_dt, int32_t dst_dt, f
   for (int64_t i = 0; i < n; ++i)
     store_elem(out, i, dst_dt, okv_cast(load_elem(in, i, src_dt), src_dt, dst_dt, src_scale, dst_scale));
 }
+
+/* NEXT-1 dynamic scales (precision alignment; reading 21):
+ * s[l][c][hq] = RN_f32(amax / 448) with amax = max |x| (x as f32, e4m3 sources dequantised
+ * with their own scale) over every finite source element of the valid tokens of all
+ * requests for the heads of D rank dst; s = 1 if amax is 0.  Layers [lb, le) are written
+ * into out[L][2][H_d]; other entries untouched.  Returns 0, or <0 if a shard is missing. */
+int32_t okv_amax_scales(int32_t n_src, const okv_layout* src, void* const* src_pools, const okv_layout* dst,
+                        int32_t n_req, const int32_t* n_tokens, const int32_t* src_bt_off,
+                        const int32_t* src_bt_ids, int32_t layer_begin, int32_t layer_end, float* out) {
+  int32_t H = src[0].num_kv_heads, D = src[0].head_dim;
+  int32_t Hp = H / src[0].tp_degree, Hd = H / dst->tp_degree, q = dst->tp_rank;
+  int32_t Bp = src[0].block_size;
+  for (int32_t l = layer_begin; l < layer_end; ++l)
+    for (int32_t c = 0; c < 2; ++c)
+      for (int32_t hq = 0; hq < Hd; ++hq) {
+        int32_t h = q * Hd + hq, p = h / Hp, hp = h - p * Hp, pi = -1;
+        for (int32_t i = 0; i < n_src; ++i)
+          if (src[i].tp_rank == p) pi = i;
+        if (pi < 0) return -2 - p;
+        const okv_layout* Lp = &src[pi];
+        float amax = 0.0f;
+        for (int32_t r = 0; r < n_req; ++r)
+          for (int64_t t = 0; t < n_tokens[r]; ++t) {
+            int32_t sb = src_bt_ids[src_bt_off[r] + t / Bp];
+            for (int32_t d = 0; d < D; ++d) {
+              uint32_t x = load_elem(src_pools[pi], okv_offset(Lp, l, c, sb, t % Bp, hp, d), Lp->dtype);
+              float v = Lp->dtype == ODT_E4M3 ? e4m3_dequant(x, scale_of(Lp, l, c, hp))
+                                              : (float)okv_decode(x, Lp->dtype);
+              v = fabsf(v);
+              if (isfinite(v) && v > amax) amax = v;
+            }
+          }
+        float s = amax / 448.0f;
+        out[(l * 2 + c) * Hd + hq] = s > 0.0f ? s : 1.0f;
+      }
+  return 0;
+}

@@ -199,3 +199,28 @@ def restore(src_lay, dst_lay, dst_pool, wire, n_tokens, dst_tables, layer_range=
                           lb, le)
     assert w == len(wire), (w, len(wire))
     return dst_pool
+
+
+def amax_scales(src_lays, src_pools, dst_lay, n_tokens, src_tables, layer_range=None, out=None):
+    """O1 dynamic fp8 scales for D rank dst_lay -> float32 [L][2][H_d] (NEXT-1)."""
+    keep = []
+    L = lib()
+    if not hasattr(L.okv_amax_scales, "_typed"):
+        L.okv_amax_scales.restype = C.c_int32
+        L.okv_amax_scales.argtypes = [C.c_int32, C.POINTER(_Layout), C.POINTER(C.c_void_p), C.POINTER(_Layout),
+                                      C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                      C.c_int32, C.c_int32, C.c_void_p]
+        L.okv_amax_scales._typed = True
+    ns = len(src_lays)
+    S = (_Layout * ns)(*[_mk(l, keep) for l in src_lays])
+    sp = (C.c_void_p * ns)(*[a.ctypes.data for a in src_pools])
+    so, si = csr(src_tables)
+    Hd = dst_lay["H"] // dst_lay["tp"]
+    if out is None:
+        out = np.full((dst_lay["L"], 2, Hd), -1.0, dtype=np.float32)
+    lb, le = layer_range if layer_range else (0, dst_lay["L"])
+    rc = L.okv_amax_scales(ns, S, sp, C.byref(_mk(dst_lay, keep)), len(n_tokens), _i32(n_tokens, keep),
+                           _i32(so, keep), _i32(si, keep), lb, le, out.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"okv_amax_scales failed: {rc}")
+    return out

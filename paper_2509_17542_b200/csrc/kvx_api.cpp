@@ -383,6 +383,64 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
   return KV_OK;
 }
 
+kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                            const kv_batch* src_bt, const kv_layout* dst, float* out_scales, int32_t lb, int32_t le,
+                            kv_stream stream) {
+  if (n_src < 1 || n_src > KVX_MAX_RANKS || !src || !src_pools || !dst || !out_scales)
+    return fail(KV_EINVAL, "kv_compute_scales: bad argument");
+  for (int i = 0; i < n_src; ++i)
+    if (!src[i] || !src_pools[i]) return fail(KV_EINVAL, "kv_compute_scales: null source layout/pool");
+  const kv_layout* S = src[0];
+  for (int i = 1; i < n_src; ++i)
+    if (!same_instance(src[i], S)) return fail(KV_ESHAPE, "kv_compute_scales: source layouts differ beyond rank");
+  kv_status st;
+  if (S->d.tp_degree > KVX_MAX_RANKS) return fail(KV_EUNSUPPORTED, "kv_compute_scales: tp degree above 16");
+  if ((st = same_model(S, dst)) != KV_OK) return st;
+  if ((st = check_layers(S, lb, le)) != KV_OK) return st;
+  if ((st = check_batch(src_bt, S, "src_bt")) != KV_OK) return st;
+  if (src_bt->n_req > 0 && !src_bt->tok_req) return fail(KV_EINVAL, "kv_compute_scales: src_bt has no token map");
+  AmaxArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int i = 0; i < KVX_MAX_RANKS; ++i) a.src_of_p[i] = -1;
+  for (int i = 0; i < n_src; ++i) {
+    const int p = src[i]->d.tp_rank;
+    if (a.src_of_p[p] != -1) return fail(KV_EINVAL, "kv_compute_scales: source rank listed twice");
+    if (S->d.dtype == KV_F8E4M3 && !src[i]->d.scales) return fail(KV_EINVAL, "kv_compute_scales: e4m3 source without scales");
+    a.src_of_p[p] = (int8_t)i;
+    a.src[i] = static_cast<const uint8_t*>(src_pools[i]);
+    a.sscale[i] = src[i]->d.scales;
+  }
+  const int32_t Hp = S->h_local, Hd = dst->h_local, q = dst->d.tp_rank;
+  for (int32_t h = q * Hd; h < (q + 1) * Hd; ++h)
+    if (a.src_of_p[h / Hp] < 0)
+      return fail(KV_ESHAPE, "kv_compute_scales: missing source shard for P rank " + std::to_string(h / Hp));
+  for (int ax = 0; ax < 6; ++ax) a.ss[ax] = S->stride[ax];
+  a.Hp = Hp;
+  a.Hd = Hd;
+  a.D = S->d.head_dim;
+  a.q = q;
+  a.lb = lb;
+  a.Lc = le - lb;
+  a.s_blk_off = src_bt->blk_off;
+  a.s_blk_ids = src_bt->blk_ids;
+  a.tok_off = src_bt->tok_off;
+  a.tok_req = src_bt->tok_req;
+  a.amax_bits = reinterpret_cast<uint32_t*>(out_scales);
+  a.n_tok = (uint32_t)src_bt->total_tokens;
+  const uint32_t ntg = (a.n_tok + 31u) / 32u;
+  a.f_tg = make_fastdiv(std::max<uint32_t>(ntg, 1));
+  a.f_hd = make_fastdiv((uint32_t)Hd);
+  a.f_bp = make_fastdiv((uint32_t)S->d.block_size);
+  a.f_hp = make_fastdiv((uint32_t)Hp);
+  const uint64_t items = (uint64_t)ntg * Hd * 2 * (uint64_t)(le - lb);
+  if (items > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_compute_scales: batch too large for one call");
+  a.n_items = (uint32_t)items;
+  if (le == lb) return KV_OK;
+  cudaError_t e = launch_amax(a, S->d.dtype, out_scales, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_compute_scales: launch");
+  return KV_OK;
+}
+
 int32_t kv_wire_dtype(const kv_layout* s, const kv_layout* d) {
   if (!s || !d) return -1;
   return dtype_bytes(d->d.dtype) <= dtype_bytes(s->d.dtype) ? d->d.dtype : s->d.dtype;

@@ -102,7 +102,23 @@ struct UnpackArgs {
   uint32_t n_items;
 };
 
+struct AmaxArgs {
+  const uint8_t* src[KVX_MAX_RANKS];
+  const float* sscale[KVX_MAX_RANKS];
+  int8_t src_of_p[KVX_MAX_RANKS];
+  int64_t ss[6];
+  int32_t Hp, Hd, D, q, lb, Lc;
+  const int32_t* s_blk_off;
+  const int32_t* s_blk_ids;
+  const int32_t* tok_off;
+  const int32_t* tok_req;
+  uint32_t* amax_bits;  // [L][2][Hd] float bits (non-negative floats order like uints)
+  FastDiv f_tg, f_hd, f_bp, f_hp;
+  uint32_t n_tok, n_items;
+};
+
 // launchers (kvx_kernels.cu); vec = 8 (fast path, DIM innermost) or 1 (generic)
+cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out_scales, cudaStream_t s);
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s);
 cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaStream_t s);

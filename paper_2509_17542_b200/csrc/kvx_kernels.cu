@@ -613,6 +613,64 @@ __global__ void __launch_bounds__(kThreads) k_unpack(const __grid_constant__ Unp
 }
 
 // ------------------------------------------------------------------------------------
+// NEXT-1: dynamic fp8 scales.  Pass 1: max |x| over the valid tokens of every (layer,
+// K/V, D-local head), one lane per token row, warp max, one atomicMax per item on the
+// float bits (non-negative floats order like unsigned ints) written in place into the
+// output array.  Pass 2: s = RN(amax / 448), or 1 when amax is 0.  Element-wise so any
+// axis order works; this is a one-read side pass, not the hot path.
+// ------------------------------------------------------------------------------------
+template <int SDT>
+__global__ void __launch_bounds__(kThreads) k_amax(const __grid_constant__ AmaxArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
+  for (uint32_t item = warp; item < a.n_items; item += nwarps) {
+    uint32_t n = item;
+    const uint32_t tg = divmod(n, a.f_tg);
+    const uint32_t hq = divmod(n, a.f_hd);
+    const uint32_t c = n & 1u;
+    const int64_t layer = a.lb + (int64_t)(n >> 1);
+    const uint32_t tok = tg * 32u + lane;
+    float m = 0.f;
+    if (tok < a.n_tok) {
+      const int32_t r = __ldg(a.tok_req + tok);
+      uint32_t t = tok - (uint32_t)__ldg(a.tok_off + r);
+      const uint32_t sslot = divmod(t, a.f_bp);
+      const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + t);
+      const uint32_t h = (uint32_t)a.q * (uint32_t)a.Hd + hq;
+      const uint32_t p = fdiv(h, a.f_hp);
+      const uint32_t hp = h - p * (uint32_t)a.Hp;
+      const int si = a.src_of_p[p];
+      const uint8_t* base = a.src[si] + (layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
+                                         sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
+                                         (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B;
+      float sc = 1.f;
+      if constexpr (SDT == KV_F8E4M3) sc = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
+      const int64_t sd = a.ss[KV_AX_DIM] * Tr<SDT>::B;
+      for (int32_t d = 0; d < a.D; ++d) {
+        Chunk<SDT, 1> e;
+        load_chunk<SDT, 1>(e, base + d * sd);
+        float v = to_f32<SDT>(e.w[0]);
+        if constexpr (SDT == KV_F8E4M3) v = __fmul_rn(v, sc);
+        v = fabsf(v);
+        if (v <= 3.402823466e38f) m = fmaxf(m, v);  // skips NaN and Inf
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0 && m > 0.f) atomicMax(a.amax_bits + (layer * 2 + c) * a.Hd + hq, __float_as_uint(m));
+  }
+}
+
+__global__ void k_amax_finalize(uint32_t* bits, int64_t begin, int64_t end) {
+  for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end; i += (int64_t)gridDim.x * blockDim.x) {
+    const float amax = __uint_as_float(bits[i]);
+    const float s = __fdiv_rn(amax, 448.0f);
+    reinterpret_cast<float*>(bits)[i] = s > 0.f ? s : 1.0f;
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // K5: completion flags (A11)
 // ------------------------------------------------------------------------------------
 __global__ void k_signal(uint32_t* flag, uint32_t value) {
@@ -829,6 +887,26 @@ cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaSt
   if (a.total == 0) return cudaSuccess;
   return vec == 8 ? unpack_v<8>(a, wdt, ddt, s) : unpack_v<1>(a, wdt, ddt, s);
 }
+cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) {
+  const int64_t begin = (int64_t)a.lb * 2 * a.Hd, end = (int64_t)(a.lb + a.Lc) * 2 * a.Hd;
+  cudaError_t e = cudaMemsetAsync(out + begin, 0, (size_t)(end - begin) * sizeof(float), s);
+  if (e != cudaSuccess) return e;
+  if (a.n_items) {
+    switch (sdt) {
+      case KV_F16: k_amax<KV_F16><<<grid_for_items(k_amax<KV_F16>, a.n_items), kThreads, 0, s>>>(a); break;
+      case KV_BF16: k_amax<KV_BF16><<<grid_for_items(k_amax<KV_BF16>, a.n_items), kThreads, 0, s>>>(a); break;
+      case KV_F8E4M3: k_amax<KV_F8E4M3><<<grid_for_items(k_amax<KV_F8E4M3>, a.n_items), kThreads, 0, s>>>(a); break;
+      case KV_F32: k_amax<KV_F32><<<grid_for_items(k_amax<KV_F32>, a.n_items), kThreads, 0, s>>>(a); break;
+      default: return cudaErrorInvalidValue;
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  k_amax_finalize<<<(int)std::min<int64_t>(1024, (end - begin + 255) / 256 + 1), 256, 0, s>>>(
+      reinterpret_cast<uint32_t*>(out), begin, end);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_signal(uint32_t* flag, uint32_t value, cudaStream_t s) {
   k_signal<<<1, 1, 0, s>>>(flag, value);
   g_launches.fetch_add(1, std::memory_order_relaxed);

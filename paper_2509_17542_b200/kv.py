@@ -12,7 +12,7 @@ from contextlib import contextmanager
 from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BYTES, KV_BF16, KV_F8E4M3, KV_F16,
                    KV_F32, Batch_t, KvError, LayoutDesc, check, lib)
 
-__all__ = ["Layout", "Batch", "convert_reshard", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
+__all__ = ["Layout", "Batch", "convert_reshard", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
            "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "launch_count", "launch_count_reset",
            "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "DTYPE_BYTES",
            "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
@@ -130,6 +130,17 @@ def convert_reshard(src_layouts, src_pools, src_batch: Batch, dst_layouts, dst_p
     lb, le = layer_range if layer_range else (0, src_layouts[0].num_layers)
     check(lib.kv_convert_reshard(ns, S, SP, C.byref(src_batch.bt), nd, Dl, DP, C.byref(dst_batch.bt), lb, le,
                                  _stream(stream)))
+
+
+def compute_scales(src_layouts, src_pools, src_batch: Batch, dst_layout: Layout, out, layer_range=None, stream=None):
+    """kv_compute_scales: per-batch fp8 dequant scales amax/448 for dst_layout's heads,
+    written into `out` (device float32 [L][2][H_d])."""
+    ns = len(src_layouts)
+    S = (C.c_void_p * ns)(*[l.handle.value for l in src_layouts])
+    SP = (C.c_void_p * ns)(*[_ptr(p) for p in src_pools])
+    lb, le = layer_range if layer_range else (0, src_layouts[0].num_layers)
+    check(lib.kv_compute_scales(ns, S, SP, C.byref(src_batch.bt), dst_layout.handle, _ptr(out), lb, le,
+                                _stream(stream)))
 
 
 def wire_dtype(src: Layout, dst: Layout):

@@ -216,3 +216,27 @@ def test_launch_count_and_errors():
     assert kvx.launch_count() == 1
     with pytest.raises(kvx.KvError, match="KV_ESHAPE"):
         kvx.Batch(lay, [5], [[0, 9]])
+
+
+@pytest.mark.parametrize("sdt", [F16, BF16, E4M3])
+def test_dynamic_scales_then_convert(o1, sdt):
+    """NEXT-1: device amax/448 scales == oracle bit-exactly; converting with them == oracle."""
+    from tests.gpu_util import DevCase
+    import paper_2509_17542_b200 as kvx
+    case = make_case(3, 8, 64, 4, 2, 16, 32, [70, 13, 1], sdt, E4M3, seed=60 + sdt, o1=o1, scales=1.0)
+    if sdt == E4M3:
+        for i, lay in enumerate(case["src_lays"]):
+            lay["scales"] = synth.pow2_scales(80 + i, 3, 2, -3, 3) * np.float32(1.25)
+    dc = DevCase(case)
+    for q, dl in enumerate(dc.dst_lays):
+        out = torch.full((3, 2, 4), -1.0, dtype=torch.float32, device="cuda")
+        kvx.compute_scales(dc.src_lays, dc.src_pools, dc.src_bt, dl, out)
+        torch.cuda.synchronize()
+        want = o1.amax_scales(case["src_lays"], case["src_pools"], case["dst_lays"][q], case["n_tokens"],
+                              case["src_tables"])
+        assert np.array_equal(out.cpu().numpy(), want)
+        # use them: the destination layout now carries the dynamic scales
+        case["dst_lays"][q]["scales"] = want
+        dl.scales.copy_(out.view(-1))
+    dc.convert()
+    assert_pools_match(dc.dst_numpy(), expected(case, o1), E4M3)
