@@ -790,8 +790,21 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
     a.f_sb = make_fastdiv(nsb);
     a.f_items = make_fastdiv(nsb * nhb);
     a.n_items = (uint32_t)((uint64_t)a.total / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);
-    auto k = k_convert_rows<SDT, DDT, U>;
-    k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
+    // loads in flight per lane: U (default) or 2U (KVX_U2=1 experiment: fewer warps, more
+    // bytes in flight per warp -- the register file, not the warp count, bounds the bytes)
+    static const bool u2 = getenv("KVX_U2") && atoi(getenv("KVX_U2")) == 1;
+    bool launched = false;
+    if constexpr (Tr<SDT>::B == 2) {
+      if (u2) {
+        auto k = k_convert_rows<SDT, DDT, 2 * U>;
+        k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
+        launched = true;
+      }
+    }
+    if (!launched) {
+      auto k = k_convert_rows<SDT, DDT, U>;
+      k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
+    }
   } else {
     auto k = k_convert<VEC, SDT, DDT, U>;
     k<<<grid_for(k, a0.total, U), kThreads, 0, s>>>(a0);

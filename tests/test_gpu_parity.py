@@ -237,6 +237,6 @@ def test_dynamic_scales_then_convert(o1, sdt):
         assert np.array_equal(out.cpu().numpy(), want)
         # use them: the destination layout now carries the dynamic scales
         case["dst_lays"][q]["scales"] = want
-        dl.scales.copy_(out.view(-1))
+        dl.scales.copy_(out.view(dl.scales.shape))
     dc.convert()
     assert_pools_match(dc.dst_numpy(), expected(case, o1), E4M3)
