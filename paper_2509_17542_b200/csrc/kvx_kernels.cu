@@ -329,6 +329,61 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
 // instruction covers cpr consecutive chunks of 32/cpr rows: contiguous per row on both
 // sides.  U chunk loads per lane are in flight before the first store.
 // ------------------------------------------------------------------------------------
+// Per-lane row state of convert item `item` (see k_convert_rows): lane = row of the
+// 2-D sub-tile.  rz: 0 copy, 1 zero-fill tail row, 2 no row.
+template <int SDT, int DDT>
+__device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint32_t lane, uint64_t& sp,
+                                         uint64_t& dp, float& rsc, uint32_t& rz) {
+  uint32_t n = item;
+  const uint32_t rg = divmod(n, a.f_items);
+  const uint32_t c = n & 1u;
+  n >>= 1;
+  const uint32_t l = divmod(n, a.f_l);
+  const uint32_t bl = divmod(n, a.f_bl);
+  const uint32_t qi = n;
+  const int32_t r = __ldg(a.d_blk_req + bl);
+  const int32_t tok0 = __ldg(a.tok_off + r);
+  const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+  const uint32_t tb0 = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd;  // first token of the block
+  const int64_t layer = a.lb + (int64_t)l;
+  // the item is a 2-D sub-tile of ts slots x th heads (ts * th = 32): both the source
+  // and the destination see runs of several rows instead of single 256-B rows
+  uint32_t sbk = rg;
+  const uint32_t s_blk = divmod(sbk, a.f_sb);  // sub-tile index along slots; sbk = along heads
+  const uint32_t ts_log2 = (uint32_t)a.ts_log2;
+  const uint32_t ls = a.slot_inner ? (lane & ((1u << ts_log2) - 1u)) : (lane >> (5u - ts_log2));
+  const uint32_t lh = a.slot_inner ? (lane >> ts_log2) : (lane & ((1u << (5u - ts_log2)) - 1u));
+  const uint32_t slot = (s_blk << ts_log2) + ls;
+  const uint32_t hq = (sbk << (5u - ts_log2)) + lh;
+  sp = 0;
+  dp = 0;
+  rsc = 1.f;  // e4m3 destination: RN(1/s); e4m3 source: s
+  rz = 2;
+  if (slot < (uint32_t)a.Bd && hq < (uint32_t)a.Hd) {
+    rz = 0;
+    const int64_t dblk = __ldg(a.d_blk_ids + bl);
+    dp = (uint64_t)(a.dst[qi] + (layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
+                                 (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD]) * Tr<DDT>::B);
+    const uint32_t t = tb0 + slot;
+    if ((int32_t)t >= T) {
+      rz = 1;
+    } else {
+      const uint32_t h = (uint32_t)a.dst_rank[qi] * (uint32_t)a.Hd + hq;
+      const uint32_t p = fdiv(h, a.f_hp);
+      const uint32_t hp = h - p * (uint32_t)a.Hp;
+      const int si = a.src_of_p[p];
+      uint32_t tb = t;
+      const uint32_t sslot = divmod(tb, a.f_bp);
+      const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + tb);
+      sp = (uint64_t)(a.src[si] + (layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
+                                   (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
+      if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3) rsc = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
+      if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3)
+        rsc = __frcp_rn(__ldg(a.dscale[qi] + (layer * 2 + c) * a.Hd + hq));
+    }
+  }
+}
+
 template <int SDT, int DDT, int U>
 __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant__ ConvArgs a) {
   const uint32_t lane = threadIdx.x & 31u;
@@ -336,58 +391,147 @@ __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant
   const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
   const uint32_t cs = (uint32_t)a.cpr_shift;
   for (uint32_t item = warp; item < a.n_items; item += nwarps) {
-    uint32_t n = item;
-    const uint32_t rg = divmod(n, a.f_items);
-    const uint32_t c = n & 1u;
-    n >>= 1;
-    const uint32_t l = divmod(n, a.f_l);
-    const uint32_t bl = divmod(n, a.f_bl);
-    const uint32_t qi = n;
-    const int32_t r = __ldg(a.d_blk_req + bl);
-    const int32_t tok0 = __ldg(a.tok_off + r);
-    const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
-    const uint32_t tb0 = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd;  // first token of the block
-    const int64_t dblk = __ldg(a.d_blk_ids + bl);
-    const int64_t layer = a.lb + (int64_t)l;
-    // the item is a 2-D sub-tile of ts slots x th heads (ts * th = 32): both the source
-    // and the destination see runs of several rows instead of single 256-B rows
-    uint32_t sbk = rg;
-    const uint32_t s_blk = divmod(sbk, a.f_sb);  // sub-tile index along slots; sbk = along heads
-    const uint32_t ts_log2 = (uint32_t)a.ts_log2;
-    const uint32_t ls = a.slot_inner ? (lane & ((1u << ts_log2) - 1u)) : (lane >> (5u - ts_log2));
-    const uint32_t lh = a.slot_inner ? (lane >> ts_log2) : (lane & ((1u << (5u - ts_log2)) - 1u));
-    const uint32_t slot = (s_blk << ts_log2) + ls;
-    const uint32_t hq = (sbk << (5u - ts_log2)) + lh;
-    // ---- per-lane row state (lane = row within the item) ----
-    uint64_t sp = 0, dp = 0;
-    float rsc = 1.f;  // e4m3 destination: RN(1/s); e4m3 source: s
-    uint32_t rz = 2;  // 2: no row (outside the tile); 1: tail slot, store zeros; 0: copy
-    if (slot < (uint32_t)a.Bd && hq < (uint32_t)a.Hd) {
-      rz = 0;
-      dp = (uint64_t)(a.dst[qi] + (layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] +
-                                   dblk * a.ds[KV_AX_BLOCK] + (int64_t)slot * a.ds[KV_AX_SLOT] +
-                                   (int64_t)hq * a.ds[KV_AX_HEAD]) * Tr<DDT>::B);
-      const uint32_t t = tb0 + slot;
-      if ((int32_t)t >= T) {
-        rz = 1;
-      } else {
-        const uint32_t h = (uint32_t)a.dst_rank[qi] * (uint32_t)a.Hd + hq;
-        const uint32_t p = fdiv(h, a.f_hp);
-        const uint32_t hp = h - p * (uint32_t)a.Hp;
-        const int si = a.src_of_p[p];
-        uint32_t tb = t;
-        const uint32_t sslot = divmod(tb, a.f_bp);
-        const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + tb);
-        sp = (uint64_t)(a.src[si] + (layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
-                                     sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
-                                     (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
-        if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3) rsc = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
-        if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3)
-          rsc = __frcp_rn(__ldg(a.dscale[qi] + (layer * 2 + c) * a.Hd + hq));
-      }
-    }
+    uint64_t sp, dp;
+    float rsc;
+    uint32_t rz;
+    conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz);
     stream_rows<SDT, DDT, U>(lane, cs, sp, dp, rsc, rz);
   }
+}
+
+// ------------------------------------------------------------------------------------
+// K1/K4 TMA-staged variant.  Same items and per-lane row decode as k_convert_rows, but
+// the source rows travel HBM -> shared memory through the TMA engine (cp.async.bulk, one
+// bulk copy per row, completion counted on a per-stage mbarrier), so the bytes in flight
+// are bounded by shared memory (kTmaStages stages x 32 rows per warp), not registers.
+// Same dtype: rows go back out smem -> global (or peer) by bulk stores, no register pass.
+// With a cast: lanes read 16-B pieces from smem, convert, and store from registers.
+// ------------------------------------------------------------------------------------
+constexpr int kTmaWarps = 4;
+constexpr int kTmaStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx_arrive(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+template <int SDT, int DDT>
+__global__ void __launch_bounds__(kTmaWarps * 32) k_convert_tma(const __grid_constant__ ConvArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int VEC = 8;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t wl = threadIdx.x >> 5;  // warp within the CTA
+  const uint32_t wpc = blockDim.x >> 5;  // warps per CTA (<= kTmaWarps, set by smem)
+  const uint32_t warp = blockIdx.x * wpc + wl;
+  const uint32_t nwarps = gridDim.x * wpc;
+  const uint32_t cs = (uint32_t)a.cpr_shift;
+  const uint32_t RB = (uint32_t)a.D * Tr<SDT>::B;  // source row bytes (multiple of 16)
+  // per-warp region: [stages][32 rows][RB] data, then per-stage row state, then barriers
+  uint8_t* wbase = smem + (size_t)wl * (kTmaStages * 32u * RB + kTmaStages * 32u * 16u + kTmaStages * 8u);
+  uint8_t* data = wbase;
+  uint64_t* st_dp = reinterpret_cast<uint64_t*>(wbase + kTmaStages * 32u * RB);
+  float* st_sc = reinterpret_cast<float*>(st_dp + kTmaStages * 32);
+  uint32_t* st_rz = reinterpret_cast<uint32_t*>(st_sc + kTmaStages * 32);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(st_rz + kTmaStages * 32);
+  if (lane == 0)
+    for (int s = 0; s < kTmaStages; ++s) mbar_init(bars + s, 1);
+  fence_proxy_async();
+  __syncwarp();
+  // issue the loads of the k-th item of this warp into stage s
+  auto issue = [&](uint32_t k, int s) {
+    const uint32_t item = warp + k * nwarps;
+    uint64_t sp, dp;
+    float rsc;
+    uint32_t rz;
+    conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz);
+    st_dp[s * 32 + lane] = dp;
+    st_sc[s * 32 + lane] = rsc;
+    st_rz[s * 32 + lane] = rz;
+    const uint32_t ncopy = __popc(__ballot_sync(0xffffffffu, rz == 0));
+    if (lane == 0) mbar_expect_tx_arrive(bars + s, ncopy * RB);
+    __syncwarp();
+    if (rz == 0) bulk_load(data + ((size_t)s * 32 + lane) * RB, reinterpret_cast<const void*>(sp), RB, bars + s);
+  };
+  const uint32_t my_items = warp < a.n_items ? (a.n_items - warp + nwarps - 1) / nwarps : 0;
+  for (uint32_t k = 0; k < my_items && k < (uint32_t)kTmaStages; ++k) issue(k, (int)k);
+  for (uint32_t k = 0; k < my_items; ++k) {
+    const int s = (int)(k % kTmaStages);
+    mbar_wait(bars + s, (k / kTmaStages) & 1u);
+    const uint64_t dp = st_dp[s * 32 + lane];
+    const uint32_t rz = st_rz[s * 32 + lane];
+    const uint8_t* sbuf = data + (size_t)s * 32 * RB;
+    if constexpr (SDT == DDT) {
+      if (rz == 0) {
+        bulk_store(reinterpret_cast<void*>(dp), sbuf + lane * RB, RB);
+      } else if (rz == 1) {
+        for (uint32_t o = 0; o < RB; o += 16)
+          asm volatile("st.global.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(dp + o), "r"(0u) : "memory");
+      }
+      bulk_commit();
+      // the stage is reloaded only after its bulk stores have read it: reload the stage
+      // consumed in the previous iteration, whose store group is now the older one
+      bulk_wait_read<1>();
+      __syncwarp();
+      if (k >= 1 && k - 1 + kTmaStages < my_items) issue(k - 1 + kTmaStages, (int)((k - 1) % kTmaStages));
+    } else {
+      const uint32_t cmask = (1u << cs) - 1u;
+      const uint32_t nch = 32u << cs;
+      for (uint32_t idx = lane; idx < nch; idx += 32u) {
+        const uint32_t rr = idx >> cs, ch = idx & cmask;
+        const uint32_t z = st_rz[s * 32 + rr];
+        if (z == 2) continue;
+        const uint64_t d = st_dp[s * 32 + rr];
+        Chunk<DDT, VEC> o;
+        if (z == 1) {
+          zero_chunk(o);
+        } else {
+          Chunk<SDT, VEC> in;
+          const uint8_t* src = sbuf + rr * RB + ch * (VEC * Tr<SDT>::B);
+#pragma unroll
+          for (int w = 0; w < Chunk<SDT, VEC>::WORDS; ++w) in.w[w] = reinterpret_cast<const uint32_t*>(src)[w];
+          const float sc = st_sc[s * 32 + rr];
+          cast_chunk<SDT, DDT, VEC>(in, o, sc, sc);
+        }
+        store_chunk<DDT, VEC>(reinterpret_cast<uint8_t*>(d) + ch * (VEC * Tr<DDT>::B), o);
+      }
+      fence_proxy_async();  // generic-proxy reads of the stage before the async refill
+      __syncwarp();
+      if (k + kTmaStages < my_items) issue(k + kTmaStages, s);
+    }
+  }
+  if constexpr (SDT == DDT) bulk_wait_all();
 }
 
 // ------------------------------------------------------------------------------------
@@ -790,18 +934,24 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
     a.f_sb = make_fastdiv(nsb);
     a.f_items = make_fastdiv(nsb * nhb);
     a.n_items = (uint32_t)((uint64_t)a.total / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);
-    // loads in flight per lane: U (default) or 2U (KVX_U2=1 experiment: fewer warps, more
-    // bytes in flight per warp -- the register file, not the warp count, bounds the bytes)
-    static const bool u2 = getenv("KVX_U2") && atoi(getenv("KVX_U2")) == 1;
-    bool launched = false;
-    if constexpr (Tr<SDT>::B == 2) {
-      if (u2) {
-        auto k = k_convert_rows<SDT, DDT, 2 * U>;
-        k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
-        launched = true;
-      }
-    }
-    if (!launched) {
+    // TMA-staged variant (KVX_TMA=1, experiment until measured): source rows must be whole
+    // 16-byte multiples for cp.async.bulk
+    static const int tma = getenv("KVX_TMA") ? atoi(getenv("KVX_TMA")) : 0;
+    const uint32_t RB = (uint32_t)a.D * Tr<SDT>::B;
+    if (tma == 1 && RB % 16 == 0) {
+      auto k = k_convert_tma<SDT, DDT>;
+      const size_t per_warp = (size_t)kTmaStages * 32 * RB + (size_t)kTmaStages * 32 * 16 + kTmaStages * 8;
+      int nw = (int)std::min<size_t>(kTmaWarps, (200u * 1024u) / per_warp);
+      if (nw < 1) nw = 1;
+      const size_t smem = per_warp * nw;
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, nw * 32, smem);
+      if (occ < 1) occ = 1;
+      const uint64_t need = (a.n_items + nw - 1) / nw;
+      const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms() * occ));
+      k<<<grid, nw * 32, smem, s>>>(a);
+    } else {
       auto k = k_convert_rows<SDT, DDT, U>;
       k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
     }
