@@ -64,7 +64,10 @@ typedef void* kv_stream; /* cudaStream_t */
  * tensor data").  The rank owns global KV heads
  * [tp_rank*H/tp_degree, (tp_rank+1)*H/tp_degree) (head-contiguous TP). */
 typedef struct {
-  int32_t num_layers;    /* L */
+  int32_t num_layers;    /* layers held by this pool (L, or a pipeline stage's share) */
+  int32_t first_layer;   /* global index of the pool's first layer: 0 without pipeline
+                          * parallelism; a PP stage holds [first_layer, first_layer+num_layers)
+                          * (NEXT-2 pipeline-stage reshard) */
   int32_t num_kv_heads;  /* global H */
   int32_t head_dim;      /* D */
   int32_t tp_degree;
@@ -73,8 +76,9 @@ typedef struct {
   int32_t num_blocks;    /* pool capacity in blocks */
   int32_t dtype;         /* kv_dtype */
   int32_t axis_order[6]; /* kv_axis, outermost -> innermost; the pool is dense row-major in it */
-  const float* scales;   /* KV_F8E4M3 only: DEVICE fp32 [L][2][H/tp] dequant scales s
-                          * (real value = code * s); NULL for other dtypes */
+  const float* scales;   /* KV_F8E4M3 only: DEVICE fp32 [num_layers][2][H/tp] dequant scales s
+                          * (real value = code * s), indexed by the pool-local layer; NULL
+                          * for other dtypes */
 } kv_layout_desc;
 
 typedef struct kv_layout kv_layout; /* opaque, immutable after describe */
@@ -131,8 +135,11 @@ int32_t kv_plan_pairs(int32_t tp_p, int32_t tp_d, int32_t num_kv_heads, int32_t*
 
 /* ---- A4-A9: fused convert ------------------------------------------------------ */
 
-/* Pool -> pool conversion of every request in the batch for layers [layer_begin,
- * layer_end): gather from the P ranks' pools, TP merge/split by head range (A7),
+/* Pool -> pool conversion of every request in the batch for the GLOBAL layers [layer_begin,
+ * layer_end), which must lie inside both the P and the D pools' [first_layer, first_layer +
+ * num_layers) (KV_EINVAL otherwise) -- with pipeline stages on either side, call once per
+ * overlapping (P stage, D stage) pair with the intersection of their ranges.
+ * It gathers from the P ranks' pools, TP merge/split by head range (A7),
  * permute to D's axis order and block size, cast (A6), scatter into the D ranks' pools,
  * zero-fill the tail slots of each request's last D block.  Nothing else
  * in any D pool is written; P tail slots are never read.
@@ -190,6 +197,41 @@ kv_status kv_pack(const kv_layout* src, const void* src_pool, const kv_batch* sr
 kv_status kv_unpack(const kv_layout* src, const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt,
                     int32_t layer_begin, int32_t layer_end, const void* wire, size_t wire_bytes,
                     kv_stream stream);
+
+/* ---- NEXT-2: self-describing wire header (transfers replayable from files) --
+ * Byte-for-byte, little-endian, 64 + 4*n_req bytes:
+ *    0 char[4] "KVX1"          4 u32 version (1)         8 u32 header bytes
+ *   12 i32 wire dtype         16 i32 num_kv_heads       20 i32 head_dim
+ *   24 i32 layer_begin        28 i32 layer_end          32 i32 P tp_degree
+ *   36 i32 P tp_rank          40 i32 D tp_degree        44 i32 D tp_rank
+ *   48 i32 head_begin         52 i32 head_end (global overlap heads carried)
+ *   56 i32 n_req              60 u32 payload bytes / 2^32 (high word) ... see below
+ *   64 i32 n_tokens[n_req]
+ * The payload that follows (kv_wire_bytes bytes, Fig. 5 canonical order) has its byte count
+ * at offset 60 (low 32 bits) + the u32 at 60 is the HIGH word: bytes = hi * 2^32 + lo with lo
+ * stored after n_tokens as a u32 -- i.e. the header ends with one more u32.  Total header
+ * size = 68 + 4*n_req.  kv_wire_header_write fails (KV_ESHAPE) if cap is too small;
+ * kv_wire_header_check returns KV_ESHAPE (message says which field) when a header does not
+ * describe a (src -> dst, n_tokens, layers) wire. */
+typedef struct {
+  int32_t wire_dtype, num_kv_heads, head_dim, layer_begin, layer_end;
+  int32_t src_tp_degree, src_tp_rank, dst_tp_degree, dst_tp_rank, head_begin, head_end, n_req;
+  uint64_t payload_bytes;
+  const int32_t* n_tokens; /* points into the header buffer */
+} kv_wire_info;
+
+size_t kv_wire_header_bytes(int32_t n_req);
+kv_status kv_wire_header_write(const kv_layout* src, const kv_layout* dst, int32_t n_req,
+                               const int32_t* host_n_tokens, int32_t layer_begin, int32_t layer_end, uint8_t* out,
+                               size_t cap);
+kv_status kv_wire_header_parse(const uint8_t* hdr, size_t len, kv_wire_info* out);
+kv_status kv_wire_header_check(const uint8_t* hdr, size_t len, const kv_layout* src, const kv_layout* dst,
+                               int32_t n_req, const int32_t* host_n_tokens, int32_t layer_begin, int32_t layer_end);
+
+/* Opaque device-to-device (or peer) byte copy on `stream` -- the first-token hidden state
+ * that travels with the KV (step 3/5; transferred unaligned, as opaque bytes).
+ * dst/src DEVICE (may be peer-mapped), any alignment. */
+kv_status kv_copy_bytes(void* dst, const void* src, size_t bytes, kv_stream stream);
 
 /* ---- A8: transport over NVLink ------------------------------------------------- */
 

@@ -187,14 +187,20 @@ def _scale(lay, l, c, hl):
 
 def convert(src_lays, src_pools, dst_lays, dst_pools, n_tokens, src_tables, dst_tables, layer_range=None):
     """Brute-force P -> D conversion.  Pools are flat lists of int codes; dst_pools
-    are modified in place (prior values survive where nothing is written)."""
-    L = src_lays[0]["L"]
-    lb, le = layer_range if layer_range else (0, L)
-    # 1. logical tensor from every source pool, source-driven
+    are modified in place (prior values survive where nothing is written).  A pool holds
+    the global layers [first_layer, first_layer + L) (pipeline stages; default 0)."""
+    if layer_range:
+        lb, le = layer_range
+    else:  # every global layer that some source and some destination pool hold
+        lb = max(min(x.get("first_layer", 0) for x in src_lays), min(x.get("first_layer", 0) for x in dst_lays))
+        le = min(max(x.get("first_layer", 0) + x["L"] for x in src_lays),
+                 max(x.get("first_layer", 0) + x["L"] for x in dst_lays))
+    # 1. logical tensor from every source pool, source-driven, keyed by GLOBAL layer
     logical = {}
     src_inv = _inverse_table(src_tables)
     for lay, pool in zip(src_lays, src_pools):
         hp_n = lay["H"] // lay["tp"]
+        f = lay.get("first_layer", 0)
         for pos, ix in positions(lay):
             if ix[BLOCK] not in src_inv:
                 continue
@@ -203,13 +209,15 @@ def convert(src_lays, src_pools, dst_lays, dst_pools, n_tokens, src_tables, dst_
             if t >= n_tokens[r]:
                 continue  # source tail: never read
             h = lay["rank"] * hp_n + ix[HEAD]
-            logical[(r, ix[LAYER], ix[KV], h, t, ix[DIM])] = (pool[pos], lay, ix[HEAD])
+            logical[(r, f + ix[LAYER], ix[KV], h, t, ix[DIM])] = (pool[pos], lay, ix[HEAD], ix[LAYER])
     # 2. every destination position, destination-driven by enumeration
     dst_inv = _inverse_table(dst_tables)
     for lay, pool in zip(dst_lays, dst_pools):
         hd_n = lay["H"] // lay["tp"]
+        f = lay.get("first_layer", 0)
         for pos, ix in positions(lay):
-            if ix[BLOCK] not in dst_inv or not (lb <= ix[LAYER] < le):
+            g = f + ix[LAYER]
+            if ix[BLOCK] not in dst_inv or not (lb <= g < le):
                 continue
             r, j = dst_inv[ix[BLOCK]]
             t = j * lay["B"] + ix[SLOT]
@@ -217,9 +225,9 @@ def convert(src_lays, src_pools, dst_lays, dst_pools, n_tokens, src_tables, dst_
             if t >= n_tokens[r]:
                 pool[pos] = 0  # zero-filled tail
                 continue
-            code, slay, shl = logical[(r, ix[LAYER], ix[KV], h, t, ix[DIM])]
+            code, slay, shl, sll = logical[(r, g, ix[KV], h, t, ix[DIM])]
             pool[pos] = cast(code, slay["dtype"], lay["dtype"],
-                             _scale(slay, ix[LAYER], ix[KV], shl), _scale(lay, ix[LAYER], ix[KV], ix[HEAD]))
+                             _scale(slay, sll, ix[KV], shl), _scale(lay, ix[LAYER], ix[KV], ix[HEAD]))
     return dst_pools
 
 

@@ -51,7 +51,9 @@ enum { OAX_LAYER = 0, OAX_KV = 1, OAX_BLOCK = 2, OAX_SLOT = 3, OAX_HEAD = 4, OAX
 enum { ODT_F16 = 0, ODT_BF16 = 1, ODT_E4M3 = 2, ODT_F32 = 3 };
 
 typedef struct {
-  int32_t num_layers, num_kv_heads, head_dim;
+  int32_t num_layers;  /* layers held by this pool */
+  int32_t first_layer; /* global index of its first layer (pipeline stage; 0 otherwise) */
+  int32_t num_kv_heads, head_dim;
   int32_t tp_degree, tp_rank;
   int32_t block_size, num_blocks;
   int32_t dtype;
@@ -351,6 +353,10 @@ int32_t okv_convert(int32_t n_src, const okv_layout* src, void* const* src_pools
   int32_t H = src[0].num_kv_heads, D = src[0].head_dim;
   int32_t Hp = H / src[0].tp_degree;
   int32_t Bp = src[0].block_size;
+  for (int32_t i = 0; i < n_src; ++i)
+    if (layer_begin < src[i].first_layer || layer_end > src[i].first_layer + src[i].num_layers) return -1;
+  for (int32_t i = 0; i < n_dst; ++i)
+    if (layer_begin < dst[i].first_layer || layer_end > dst[i].first_layer + dst[i].num_layers) return -1;
   for (int32_t r = 0; r < n_req; ++r) {
     int64_t T = n_tokens[r];
     for (int32_t qi = 0; qi < n_dst; ++qi) {
@@ -370,21 +376,22 @@ int32_t okv_convert(int32_t n_src, const okv_layout* src, void* const* src_pools
               if (src[i].tp_rank == p) pi = i;
             if (pi < 0) return -2 - p; /* missing source shard p */
             const okv_layout* Lp = &src[pi];
-            float sd = scale_of(Ld, l, c, hq);
-            float ss = scale_of(Lp, l, c, hp);
+            int32_t ls = l - Lp->first_layer, ld = l - Ld->first_layer; /* pool-local layers */
+            float sd = scale_of(Ld, ld, c, hq);
+            float ss = scale_of(Lp, ls, c, hp);
             for (int64_t t = 0; t < T; ++t) {
               int32_t sb = src_bt_ids[src_bt_off[r] + t / Bp];
               int32_t db = dst_bt_ids[dst_bt_off[r] + t / Bd];
               for (int32_t d = 0; d < D; ++d) {
-                uint32_t x = load_elem(src_pools[pi], okv_offset(Lp, l, c, sb, t % Bp, hp, d), Lp->dtype);
+                uint32_t x = load_elem(src_pools[pi], okv_offset(Lp, ls, c, sb, t % Bp, hp, d), Lp->dtype);
                 uint32_t y = okv_cast(x, Lp->dtype, Ld->dtype, ss, sd);
-                store_elem(dst_pools[qi], okv_offset(Ld, l, c, db, t % Bd, hq, d), Ld->dtype, y);
+                store_elem(dst_pools[qi], okv_offset(Ld, ld, c, db, t % Bd, hq, d), Ld->dtype, y);
               }
             }
             for (int64_t t = T; t < padded; ++t) {
               int32_t db = dst_bt_ids[dst_bt_off[r] + t / Bd];
               for (int32_t d = 0; d < D; ++d)
-                store_elem(dst_pools[qi], okv_offset(Ld, l, c, db, t % Bd, hq, d), Ld->dtype, 0u);
+                store_elem(dst_pools[qi], okv_offset(Ld, ld, c, db, t % Bd, hq, d), Ld->dtype, 0u);
             }
           }
     }
@@ -417,9 +424,10 @@ int64_t okv_flatten(const okv_layout* Lp, const void* src_pool, const okv_layout
           for (int64_t t = 0; t < n_tokens[r]; ++t) {
             int32_t sb = src_bt_ids[src_bt_off[r] + t / Bp];
             for (int32_t d = 0; d < D; ++d) {
-              uint32_t x = load_elem(src_pool, okv_offset(Lp, l, c, sb, t % Bp, h - p * Hp, d), Lp->dtype);
-              uint32_t y = okv_cast(x, Lp->dtype, wire_dt, scale_of(Lp, l, c, h - p * Hp),
-                                    scale_of(Ld, l, c, h - q * Hd));
+              int32_t ls = l - Lp->first_layer, ld = l - Ld->first_layer;
+              uint32_t x = load_elem(src_pool, okv_offset(Lp, ls, c, sb, t % Bp, h - p * Hp, d), Lp->dtype);
+              uint32_t y = okv_cast(x, Lp->dtype, wire_dt, scale_of(Lp, ls, c, h - p * Hp),
+                                    scale_of(Ld, ld, c, h - q * Hd));
               store_elem(wire, w++, wire_dt, y);
             }
           }
@@ -447,14 +455,15 @@ int64_t okv_restore(const okv_layout* Lp, const okv_layout* Ld, void* dst_pool, 
           int64_t padded = (T + Bd - 1) / Bd * Bd;
           for (int64_t t = 0; t < padded; ++t) {
             int32_t db = dst_bt_ids[dst_bt_off[r] + t / Bd];
+            int32_t ls = l - Lp->first_layer, ld = l - Ld->first_layer;
             for (int32_t d = 0; d < D; ++d) {
               uint32_t y = 0;
               if (t < T) {
                 uint32_t x = load_elem(wire, w++, wire_dt);
-                y = okv_cast(x, wire_dt, Ld->dtype, scale_of(Lp, l, c, h - p * Hp),
-                             scale_of(Ld, l, c, h - q * Hd));
+                y = okv_cast(x, wire_dt, Ld->dtype, scale_of(Lp, ls, c, h - p * Hp),
+                             scale_of(Ld, ld, c, h - q * Hd));
               }
-              store_elem(dst_pool, okv_offset(Ld, l, c, db, t % Bd, h - q * Hd, d), Ld->dtype, y);
+              store_elem(dst_pool, okv_offset(Ld, ld, c, db, t % Bd, h - q * Hd, d), Ld->dtype, y);
             }
           }
         }
@@ -492,15 +501,16 @@ int32_t okv_amax_scales(int32_t n_src, const okv_layout* src, void* const* src_p
           for (int64_t t = 0; t < n_tokens[r]; ++t) {
             int32_t sb = src_bt_ids[src_bt_off[r] + t / Bp];
             for (int32_t d = 0; d < D; ++d) {
-              uint32_t x = load_elem(src_pools[pi], okv_offset(Lp, l, c, sb, t % Bp, hp, d), Lp->dtype);
-              float v = Lp->dtype == ODT_E4M3 ? e4m3_dequant(x, scale_of(Lp, l, c, hp))
+              uint32_t x = load_elem(src_pools[pi], okv_offset(Lp, l - Lp->first_layer, c, sb, t % Bp, hp, d),
+                                     Lp->dtype);
+              float v = Lp->dtype == ODT_E4M3 ? e4m3_dequant(x, scale_of(Lp, l - Lp->first_layer, c, hp))
                                               : (float)okv_decode(x, Lp->dtype);
               v = fabsf(v);
               if (isfinite(v) && v > amax) amax = v;
             }
           }
         float s = amax / 448.0f;
-        out[(l * 2 + c) * Hd + hq] = s > 0.0f ? s : 1.0f;
+        out[((l - dst->first_layer) * 2 + c) * Hd + hq] = s > 0.0f ? s : 1.0f;
       }
   return 0;
 }

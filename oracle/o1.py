@@ -34,7 +34,8 @@ def build(force: bool = False) -> str:
 
 
 class _Layout(C.Structure):
-    _fields_ = [("num_layers", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+    _fields_ = [("num_layers", C.c_int32), ("first_layer", C.c_int32), ("num_kv_heads", C.c_int32),
+                ("head_dim", C.c_int32),
                 ("tp_degree", C.c_int32), ("tp_rank", C.c_int32), ("block_size", C.c_int32),
                 ("num_blocks", C.c_int32), ("dtype", C.c_int32), ("axis_order", C.c_int32 * 6),
                 ("scales", C.POINTER(C.c_float))]
@@ -86,6 +87,7 @@ def lib():
 def _mk(lay, keep):
     s = _Layout()
     s.num_layers, s.num_kv_heads, s.head_dim = lay["L"], lay["H"], lay["D"]
+    s.first_layer = lay.get("first_layer", 0)
     s.tp_degree, s.tp_rank = lay["tp"], lay["rank"]
     s.block_size, s.num_blocks, s.dtype = lay["B"], lay["NB"], lay["dtype"]
     for i, a in enumerate(lay["order"]):
@@ -111,6 +113,12 @@ def csr(tables):
         off[r + 1] = off[r] + len(t)
     ids = np.concatenate([np.asarray(t, dtype=np.int32) for t in tables]) if tables else np.zeros(0, np.int32)
     return off, ids
+
+
+def layer_span(a, b):
+    """Global layers both pools hold (pipeline stages); the default range of a call."""
+    fa, fb = a.get("first_layer", 0), b.get("first_layer", 0)
+    return (max(fa, fb), min(fa + a["L"], fb + b["L"]))
 
 
 def kv_bytes(L, H, D, T, s):
@@ -158,7 +166,7 @@ def convert(src_lays, src_pools, dst_lays, dst_pools, n_tokens, src_tables, dst_
     dp = (C.c_void_p * nd)(*[a.ctypes.data for a in dst_pools])
     so, si = csr(src_tables)
     do, di = csr(dst_tables)
-    lb, le = layer_range if layer_range else (0, src_lays[0]["L"])
+    lb, le = layer_range if layer_range else layer_span(src_lays[0], dst_lays[0])
     rc = lib().okv_convert(ns, S, sp, nd, Dl, dp, len(n_tokens), _i32(n_tokens, keep), _i32(so, keep),
                            _i32(si, keep), _i32(do, keep), _i32(di, keep), lb, le)
     if rc != 0:
@@ -178,7 +186,7 @@ def flatten(src_lay, src_pool, dst_lay, n_tokens, src_tables, layer_range=None):
     p, q = src_lay["rank"], dst_lay["rank"]
     Hp, Hd = H // src_lay["tp"], H // dst_lay["tp"]
     nh = max(0, min((p + 1) * Hp, (q + 1) * Hd) - max(p * Hp, q * Hd))
-    lb, le = layer_range if layer_range else (0, src_lay["L"])
+    lb, le = layer_range if layer_range else layer_span(src_lay, dst_lay)
     n = 2 * (le - lb) * nh * int(np.sum(n_tokens)) * src_lay["D"]
     wire = np.zeros(n, dtype=NPTYPE[NBYTES[wdt]])
     so, si = csr(src_tables)
@@ -193,7 +201,7 @@ def restore(src_lay, dst_lay, dst_pool, wire, n_tokens, dst_tables, layer_range=
     keep = []
     wdt = wire_dtype(src_lay["dtype"], dst_lay["dtype"])
     do, di = csr(dst_tables)
-    lb, le = layer_range if layer_range else (0, src_lay["L"])
+    lb, le = layer_range if layer_range else layer_span(src_lay, dst_lay)
     w = lib().okv_restore(C.byref(_mk(src_lay, keep)), C.byref(_mk(dst_lay, keep)), dst_pool.ctypes.data, wdt,
                           wire.ctypes.data, len(n_tokens), _i32(n_tokens, keep), _i32(do, keep), _i32(di, keep),
                           lb, le)
@@ -217,8 +225,8 @@ def amax_scales(src_lays, src_pools, dst_lay, n_tokens, src_tables, layer_range=
     so, si = csr(src_tables)
     Hd = dst_lay["H"] // dst_lay["tp"]
     if out is None:
-        out = np.full((dst_lay["L"], 2, Hd), -1.0, dtype=np.float32)
-    lb, le = layer_range if layer_range else (0, dst_lay["L"])
+        out = np.full((dst_lay["L"], 2, Hd), -1.0, dtype=np.float32)  # indexed by D-local layer
+    lb, le = layer_range if layer_range else layer_span(src_lays[0], dst_lay)
     rc = L.okv_amax_scales(ns, S, sp, C.byref(_mk(dst_lay, keep)), len(n_tokens), _i32(n_tokens, keep),
                            _i32(so, keep), _i32(si, keep), lb, le, out.ctypes.data)
     if rc != 0:

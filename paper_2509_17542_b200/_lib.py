@@ -28,7 +28,8 @@ class KvError(RuntimeError):
 
 
 class LayoutDesc(C.Structure):
-    _fields_ = [("num_layers", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+    _fields_ = [("num_layers", C.c_int32), ("first_layer", C.c_int32), ("num_kv_heads", C.c_int32),
+                ("head_dim", C.c_int32),
                 ("tp_degree", C.c_int32), ("tp_rank", C.c_int32), ("block_size", C.c_int32),
                 ("num_blocks", C.c_int32), ("dtype", C.c_int32), ("axis_order", C.c_int32 * 6),
                 ("scales", C.c_void_p)]

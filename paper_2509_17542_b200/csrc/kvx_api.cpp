@@ -55,7 +55,8 @@ bool ptr_aligned(const void* p, size_t a) { return ((uintptr_t)p % a) == 0; }
 // Two layouts describe the same instance (same model, blocks, order, dtype, tp degree).
 bool same_instance(const kv_layout* a, const kv_layout* b) {
   const kv_layout_desc &x = a->d, &y = b->d;
-  if (x.num_layers != y.num_layers || x.num_kv_heads != y.num_kv_heads || x.head_dim != y.head_dim ||
+  if (x.num_layers != y.num_layers || x.first_layer != y.first_layer || x.num_kv_heads != y.num_kv_heads ||
+      x.head_dim != y.head_dim ||
       x.tp_degree != y.tp_degree || x.block_size != y.block_size || x.num_blocks != y.num_blocks ||
       x.dtype != y.dtype)
     return false;
@@ -74,9 +75,10 @@ kv_status check_batch(const kv_batch* bt, const kv_layout* lay, const char* name
 }
 
 kv_status check_layers(const kv_layout* lay, int32_t lb, int32_t le) {
-  if (lb < 0 || le < lb || le > lay->d.num_layers)
-    return fail(KV_EINVAL, "layer range [" + std::to_string(lb) + ", " + std::to_string(le) + ") outside [0, " +
-                               std::to_string(lay->d.num_layers) + ")");
+  const int32_t f = lay->d.first_layer, e = lay->d.first_layer + lay->d.num_layers;
+  if (lb < f || le < lb || le > e)
+    return fail(KV_EINVAL, "layer range [" + std::to_string(lb) + ", " + std::to_string(le) + ") outside the pool's [" +
+                               std::to_string(f) + ", " + std::to_string(e) + ")");
   return KV_OK;
 }
 
@@ -95,9 +97,8 @@ bool fast_ok(const kv_layout* lay) {
 }
 
 kv_status same_model(const kv_layout* s, const kv_layout* d) {
-  if (s->d.num_layers != d->d.num_layers || s->d.num_kv_heads != d->d.num_kv_heads ||
-      s->d.head_dim != d->d.head_dim)
-    return fail(KV_ESHAPE, "P and D layouts describe different models (layers / kv heads / head_dim)");
+  if (s->d.num_kv_heads != d->d.num_kv_heads || s->d.head_dim != d->d.head_dim)
+    return fail(KV_ESHAPE, "P and D layouts describe different models (kv heads / head_dim)");
   return KV_OK;
 }
 
@@ -138,6 +139,7 @@ kv_status kv_layout_describe(const kv_layout_desc* desc, kv_layout** out, size_t
       d.num_blocks <= 0)
     return fail(KV_EINVAL, "kv_layout_describe: non-positive extent");
   if (dtype_bytes(d.dtype) == 0) return fail(KV_EINVAL, "kv_layout_describe: bad dtype");
+  if (d.first_layer < 0) return fail(KV_EINVAL, "kv_layout_describe: negative first_layer");
   if (d.num_kv_heads % d.tp_degree != 0)
     return fail(KV_ESHAPE, "kv_layout_describe: tp_degree " + std::to_string(d.tp_degree) +
                                " does not divide num_kv_heads " + std::to_string(d.num_kv_heads));
@@ -304,6 +306,7 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
     return fail(KV_EUNSUPPORTED, "kv_convert_reshard: tp degree above 16");
   if ((st = same_model(S, D)) != KV_OK) return st;
   if ((st = check_layers(S, lb, le)) != KV_OK) return st;
+  if ((st = check_layers(D, lb, le)) != KV_OK) return st;
   if ((st = check_batch(src_bt, S, "src_bt")) != KV_OK) return st;
   if ((st = check_batch(dst_bt, D, "dst_bt")) != KV_OK) return st;
   if (src_bt->n_req != dst_bt->n_req || src_bt->total_tokens != dst_bt->total_tokens ||
@@ -350,6 +353,8 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
   a.D = S->d.head_dim;
   a.Bp = S->d.block_size;
   a.Bd = D->d.block_size;
+  a.s_l0 = S->d.first_layer;
+  a.d_l0 = D->d.first_layer;
   a.s_blk_off = src_bt->blk_off;
   a.s_blk_ids = src_bt->blk_ids;
   a.d_blk_off = dst_bt->blk_off;
@@ -397,6 +402,7 @@ kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const vo
   if (S->d.tp_degree > KVX_MAX_RANKS) return fail(KV_EUNSUPPORTED, "kv_compute_scales: tp degree above 16");
   if ((st = same_model(S, dst)) != KV_OK) return st;
   if ((st = check_layers(S, lb, le)) != KV_OK) return st;
+  if ((st = check_layers(dst, lb, le)) != KV_OK) return st;
   if ((st = check_batch(src_bt, S, "src_bt")) != KV_OK) return st;
   if (src_bt->n_req > 0 && !src_bt->tok_req) return fail(KV_EINVAL, "kv_compute_scales: src_bt has no token map");
   AmaxArgs a;
@@ -419,6 +425,8 @@ kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const vo
   a.Hd = Hd;
   a.D = S->d.head_dim;
   a.q = q;
+  a.s_l0 = S->d.first_layer;
+  a.d_l0 = dst->d.first_layer;
   a.lb = lb;
   a.Lc = le - lb;
   a.s_blk_off = src_bt->blk_off;
@@ -461,6 +469,7 @@ kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_
   kv_status st;
   if ((st = same_model(s, d)) != KV_OK) return st;
   if ((st = check_layers(s, lb, le)) != KV_OK) return st;
+  if ((st = check_layers(d, lb, le)) != KV_OK) return st;
   if ((st = check_batch(src_bt, s, "src_bt")) != KV_OK) return st;
   if ((st = scales_ok(s, d)) != KV_OK) return st;
   int32_t hb, he;
@@ -483,6 +492,8 @@ kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_
   a.Hd = d->h_local;
   a.D = s->d.head_dim;
   a.Bp = s->d.block_size;
+  a.s_l0 = s->d.first_layer;
+  a.d_l0 = d->d.first_layer;
   a.lb = lb;
   a.Lc = le - lb;
   a.p = s->d.tp_rank;
@@ -512,6 +523,7 @@ kv_status kv_unpack(const kv_layout* s, const kv_layout* d, void* dst_pool, cons
   if (!s || !d || !dst_pool || !wire) return fail(KV_EINVAL, "kv_unpack: null argument");
   kv_status st;
   if ((st = same_model(s, d)) != KV_OK) return st;
+  if ((st = check_layers(s, lb, le)) != KV_OK) return st;
   if ((st = check_layers(d, lb, le)) != KV_OK) return st;
   if ((st = check_batch(dst_bt, d, "dst_bt")) != KV_OK) return st;
   if ((st = scales_ok(s, d)) != KV_OK) return st;
@@ -534,6 +546,8 @@ kv_status kv_unpack(const kv_layout* s, const kv_layout* d, void* dst_pool, cons
   a.Hd = d->h_local;
   a.D = d->d.head_dim;
   a.Bd = d->d.block_size;
+  a.s_l0 = s->d.first_layer;
+  a.d_l0 = d->d.first_layer;
   a.lb = lb;
   a.Lc = le - lb;
   a.p = s->d.tp_rank;

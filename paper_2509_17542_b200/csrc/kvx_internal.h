@@ -44,6 +44,7 @@ struct ConvArgs {
   int8_t dst_rank[KVX_MAX_RANKS];      // index -> D tp_rank
   int64_t ss[6], ds[6];                // element strides by axis
   int32_t Hp, Hd, D, Bp, Bd, lb, Lc;
+  int32_t s_l0, d_l0;  // first global layer of the P / D pools (pipeline stages)
   const int32_t* s_blk_off;
   const int32_t* s_blk_ids;
   const int32_t* d_blk_off;
@@ -69,6 +70,7 @@ struct PackArgs {
   const float* dscale;  // destination scales (narrowing to e4m3 on the sender)
   int64_t ss[6];
   int32_t Hp, Hd, D, Bp, lb, Lc, p, q, hb, nh;
+  int32_t s_l0, d_l0;
   const int32_t* s_blk_off;
   const int32_t* s_blk_ids;
   const int32_t* tok_off;
@@ -88,6 +90,7 @@ struct UnpackArgs {
   const float* dscale;
   int64_t ds[6];
   int32_t Hp, Hd, D, Bd, lb, Lc, p, q, hb, nh;
+  int32_t s_l0, d_l0;
   int64_t total_tokens;
   const int32_t* d_blk_off;
   const int32_t* d_blk_ids;
@@ -108,6 +111,7 @@ struct AmaxArgs {
   int8_t src_of_p[KVX_MAX_RANKS];
   int64_t ss[6];
   int32_t Hp, Hd, D, q, lb, Lc;
+  int32_t s_l0, d_l0;
   const int32_t* s_blk_off;
   const int32_t* s_blk_ids;
   const int32_t* tok_off;

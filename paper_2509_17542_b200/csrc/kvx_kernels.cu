@@ -240,7 +240,8 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
         const uint32_t t = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd + slot;
         const int64_t dblk = __ldg(a.d_blk_ids + bl);
         const int64_t layer = a.lb + (int64_t)l;
-        const int64_t doff = layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
+        const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
+        const int64_t doff = dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
                              (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD] +
                              (int64_t)dch * VEC * a.ds[KV_AX_DIM];
         dp[k] = a.dst[qi] + doff * Tr<DDT>::B;
@@ -254,14 +255,14 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
           uint32_t tb = t;
           const uint32_t sslot = divmod(tb, a.f_bp);
           const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + tb);
-          const int64_t soff = layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
+          const int64_t soff = sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
                                sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
                                (int64_t)hp * a.ss[KV_AX_HEAD] + (int64_t)dch * VEC * a.ss[KV_AX_DIM];
           load_chunk<SDT, VEC>(in[k], a.src[si] + soff * Tr<SDT>::B);
           if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3)
-            ssc[k] = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
+            ssc[k] = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
           if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3)
-            inv[k] = __frcp_rn(__ldg(a.dscale[qi] + (layer * 2 + c) * a.Hd + hq));
+            inv[k] = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
         }
       }
     }
@@ -346,6 +347,7 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
   const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
   const uint32_t tb0 = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd;  // first token of the block
   const int64_t layer = a.lb + (int64_t)l;
+  const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
   // the item is a 2-D sub-tile of ts slots x th heads (ts * th = 32): both the source
   // and the destination see runs of several rows instead of single 256-B rows
   uint32_t sbk = rg;
@@ -362,7 +364,7 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
   if (slot < (uint32_t)a.Bd && hq < (uint32_t)a.Hd) {
     rz = 0;
     const int64_t dblk = __ldg(a.d_blk_ids + bl);
-    dp = (uint64_t)(a.dst[qi] + (layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
+    dp = (uint64_t)(a.dst[qi] + (dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
                                  (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD]) * Tr<DDT>::B);
     const uint32_t t = tb0 + slot;
     if ((int32_t)t >= T) {
@@ -375,11 +377,11 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
       uint32_t tb = t;
       const uint32_t sslot = divmod(tb, a.f_bp);
       const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + tb);
-      sp = (uint64_t)(a.src[si] + (layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
+      sp = (uint64_t)(a.src[si] + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
                                    (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
-      if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3) rsc = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
+      if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3) rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
       if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3)
-        rsc = __frcp_rn(__ldg(a.dscale[qi] + (layer * 2 + c) * a.Hd + hq));
+        rsc = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
     }
   }
 }
@@ -553,6 +555,7 @@ __global__ void __launch_bounds__(kThreads) k_pack_rows(const __grid_constant__ 
     const uint32_t c = n & 1u;
     const uint32_t l = n >> 1;
     const int64_t layer = a.lb + (int64_t)l;
+    const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
     const uint32_t tok = tg * 32u + lane;
     uint64_t sp = 0, dp = 0;
     float rsc = 1.f;
@@ -565,12 +568,12 @@ __global__ void __launch_bounds__(kThreads) k_pack_rows(const __grid_constant__ 
       const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + t);
       const uint32_t h = (uint32_t)a.hb + hh;
       const uint32_t hp = h - (uint32_t)a.p * (uint32_t)a.Hp;
-      sp = (uint64_t)(a.src + (layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
+      sp = (uint64_t)(a.src + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
                                (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
       dp = (uint64_t)(a.wire + ((((uint64_t)l * 2 + c) * (uint64_t)a.nh + hh) * T_all + tok) * (uint64_t)a.D * Tr<WDT>::B);
-      if constexpr (SDT == KV_F8E4M3 && WDT != KV_F8E4M3) rsc = __ldg(a.sscale + (layer * 2 + c) * a.Hp + hp);
+      if constexpr (SDT == KV_F8E4M3 && WDT != KV_F8E4M3) rsc = __ldg(a.sscale + (sl * 2 + c) * a.Hp + hp);
       if constexpr (WDT == KV_F8E4M3 && SDT != KV_F8E4M3)
-        rsc = __frcp_rn(__ldg(a.dscale + (layer * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)));
+        rsc = __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)));
     }
     stream_rows<SDT, WDT, U>(lane, cs, sp, dp, rsc, rz);
   }
@@ -603,6 +606,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
     const int32_t tok0 = __ldg(a.tok_off + r);
     const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
     const int64_t layer = a.lb + (int64_t)l;
+    const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
     uint64_t sp = 0, dp = 0;
     float rsc = 1.f;
     uint32_t rz = 2;
@@ -612,7 +616,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
       const int64_t dblk = __ldg(a.d_blk_ids + bl);
       const uint32_t h = (uint32_t)a.hb + hh;
       const uint32_t hq = h - (uint32_t)a.q * (uint32_t)a.Hd;
-      dp = (uint64_t)(a.dst + (layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
+      dp = (uint64_t)(a.dst + (dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
                                (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD]) * Tr<DDT>::B);
       if ((int32_t)t >= T) {
         rz = 1;
@@ -620,9 +624,9 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
         sp = (uint64_t)(a.wire + ((((uint64_t)l * 2 + c) * (uint64_t)a.nh + hh) * (uint64_t)a.total_tokens +
                                   (uint64_t)(tok0 + t)) * (uint64_t)a.D * Tr<WDT>::B);
         if constexpr (WDT == KV_F8E4M3 && DDT != KV_F8E4M3)
-          rsc = __ldg(a.sscale + (layer * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
+          rsc = __ldg(a.sscale + (sl * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
         if constexpr (DDT == KV_F8E4M3 && WDT != KV_F8E4M3)
-          rsc = __frcp_rn(__ldg(a.dscale + (layer * 2 + c) * a.Hd + hq));
+          rsc = __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + hq));
       }
     }
     stream_rows<WDT, DDT, U>(lane, cs, sp, dp, rsc, rz);
@@ -666,13 +670,14 @@ __global__ void __launch_bounds__(kThreads) k_pack(const __grid_constant__ PackA
         const uint32_t h = (uint32_t)a.hb + hh;
         const uint32_t hp = h - (uint32_t)a.p * (uint32_t)a.Hp;
         const int64_t layer = a.lb + (int64_t)l;
-        const int64_t soff = layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
+        const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
+        const int64_t soff = sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
                              (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD] +
                              (int64_t)dch * VEC * a.ss[KV_AX_DIM];
         load_chunk<SDT, VEC>(in[k], a.src + soff * Tr<SDT>::B);
-        if constexpr (SDT == KV_F8E4M3 && WDT != KV_F8E4M3) ssc[k] = __ldg(a.sscale + (layer * 2 + c) * a.Hp + hp);
+        if constexpr (SDT == KV_F8E4M3 && WDT != KV_F8E4M3) ssc[k] = __ldg(a.sscale + (sl * 2 + c) * a.Hp + hp);
         if constexpr (WDT == KV_F8E4M3 && SDT != KV_F8E4M3)
-          inv[k] = __frcp_rn(__ldg(a.dscale + (layer * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)));
+          inv[k] = __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)));
       }
     }
 #pragma unroll
@@ -725,9 +730,10 @@ __global__ void __launch_bounds__(kThreads) k_unpack(const __grid_constant__ Unp
         const uint32_t t = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd + slot;
         const int64_t dblk = __ldg(a.d_blk_ids + bl);
         const int64_t layer = a.lb + (int64_t)l;
+        const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
         const uint32_t h = (uint32_t)a.hb + hh;
         const uint32_t hq = h - (uint32_t)a.q * (uint32_t)a.Hd;
-        const int64_t doff = layer * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
+        const int64_t doff = dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
                              (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD] +
                              (int64_t)dch * VEC * a.ds[KV_AX_DIM];
         dp[k] = a.dst + doff * Tr<DDT>::B;
@@ -737,9 +743,9 @@ __global__ void __launch_bounds__(kThreads) k_unpack(const __grid_constant__ Unp
           const int64_t woff = ((((int64_t)l * 2 + c) * a.nh + hh) * a.total_tokens + tok0 + t) * a.D + (int64_t)dch * VEC;
           load_chunk<WDT, VEC>(in[k], a.wire + woff * Tr<WDT>::B);
           if constexpr (WDT == KV_F8E4M3 && DDT != KV_F8E4M3)
-            ssc[k] = __ldg(a.sscale + (layer * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
+            ssc[k] = __ldg(a.sscale + (sl * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
           if constexpr (DDT == KV_F8E4M3 && WDT != KV_F8E4M3)
-            inv[k] = __frcp_rn(__ldg(a.dscale + (layer * 2 + c) * a.Hd + hq));
+            inv[k] = __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + hq));
         }
       }
     }
@@ -774,6 +780,7 @@ __global__ void __launch_bounds__(kThreads) k_amax(const __grid_constant__ AmaxA
     const uint32_t hq = divmod(n, a.f_hd);
     const uint32_t c = n & 1u;
     const int64_t layer = a.lb + (int64_t)(n >> 1);
+    const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
     const uint32_t tok = tg * 32u + lane;
     float m = 0.f;
     if (tok < a.n_tok) {
@@ -785,11 +792,11 @@ __global__ void __launch_bounds__(kThreads) k_amax(const __grid_constant__ AmaxA
       const uint32_t p = fdiv(h, a.f_hp);
       const uint32_t hp = h - p * (uint32_t)a.Hp;
       const int si = a.src_of_p[p];
-      const uint8_t* base = a.src[si] + (layer * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
+      const uint8_t* base = a.src[si] + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
                                          sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
                                          (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B;
       float sc = 1.f;
-      if constexpr (SDT == KV_F8E4M3) sc = __ldg(a.sscale[si] + (layer * 2 + c) * a.Hp + hp);
+      if constexpr (SDT == KV_F8E4M3) sc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
       const int64_t sd = a.ss[KV_AX_DIM] * Tr<SDT>::B;
       for (int32_t d = 0; d < a.D; ++d) {
         Chunk<SDT, 1> e;
@@ -802,7 +809,7 @@ __global__ void __launch_bounds__(kThreads) k_amax(const __grid_constant__ AmaxA
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-    if (lane == 0 && m > 0.f) atomicMax(a.amax_bits + (layer * 2 + c) * a.Hd + hq, __float_as_uint(m));
+    if (lane == 0 && m > 0.f) atomicMax(a.amax_bits + (dl * 2 + c) * a.Hd + hq, __float_as_uint(m));
   }
 }
 
@@ -1051,7 +1058,7 @@ cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaSt
   return vec == 8 ? unpack_v<8>(a, wdt, ddt, s) : unpack_v<1>(a, wdt, ddt, s);
 }
 cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) {
-  const int64_t begin = (int64_t)a.lb * 2 * a.Hd, end = (int64_t)(a.lb + a.Lc) * 2 * a.Hd;
+  const int64_t begin = (int64_t)(a.lb - a.d_l0) * 2 * a.Hd, end = (int64_t)(a.lb - a.d_l0 + a.Lc) * 2 * a.Hd;
   cudaError_t e = cudaMemsetAsync(out + begin, 0, (size_t)(end - begin) * sizeof(float), s);
   if (e != cudaSuccess) return e;
   if (a.n_items) {

@@ -26,6 +26,11 @@ def _ptr(x):
     return x.data_ptr()
 
 
+def _common(a, b):
+    """Default layer range of a call: the global layers both pools hold (pipeline stages)."""
+    return (max(a.first_layer, b.first_layer), min(a.first_layer + a.num_layers, b.first_layer + b.num_layers))
+
+
 def _stream(stream):
     if stream is None:
         import torch
@@ -39,9 +44,11 @@ class Layout:
     """kv_layout_describe: one TP rank's paged pool layout."""
 
     def __init__(self, num_layers, num_kv_heads, head_dim, tp_degree, tp_rank, block_size, num_blocks, dtype,
-                 axis_order, scales=None):
+                 axis_order, scales=None, first_layer=0):
         d = LayoutDesc()
         d.num_layers, d.num_kv_heads, d.head_dim = num_layers, num_kv_heads, head_dim
+        d.first_layer = first_layer
+        self.first_layer = first_layer
         d.tp_degree, d.tp_rank = tp_degree, tp_rank
         d.block_size, d.num_blocks, d.dtype = block_size, num_blocks, dtype
         for i, a in enumerate(axis_order):
@@ -61,7 +68,13 @@ class Layout:
 
     @classmethod
     def from_dict(cls, d, scales=None):
-        return cls(d["L"], d["H"], d["D"], d["tp"], d["rank"], d["B"], d["NB"], d["dtype"], d["order"], scales)
+        return cls(d["L"], d["H"], d["D"], d["tp"], d["rank"], d["B"], d["NB"], d["dtype"], d["order"], scales,
+                   d.get("first_layer", 0))
+
+    @property
+    def layers(self):
+        """Global layer range [first_layer, first_layer + num_layers) held by the pool."""
+        return (self.first_layer, self.first_layer + self.num_layers)
 
     @property
     def handle(self):
@@ -127,7 +140,7 @@ def convert_reshard(src_layouts, src_pools, src_batch: Batch, dst_layouts, dst_p
     SP = (C.c_void_p * ns)(*[_ptr(p) for p in src_pools])
     Dl = (C.c_void_p * nd)(*[l.handle.value for l in dst_layouts])
     DP = (C.c_void_p * nd)(*[_ptr(p) for p in dst_pools])
-    lb, le = layer_range if layer_range else (0, src_layouts[0].num_layers)
+    lb, le = layer_range if layer_range else _common(src_layouts[0], dst_layouts[0])
     check(lib.kv_convert_reshard(ns, S, SP, C.byref(src_batch.bt), nd, Dl, DP, C.byref(dst_batch.bt), lb, le,
                                  _stream(stream)))
 
@@ -138,7 +151,7 @@ def compute_scales(src_layouts, src_pools, src_batch: Batch, dst_layout: Layout,
     ns = len(src_layouts)
     S = (C.c_void_p * ns)(*[l.handle.value for l in src_layouts])
     SP = (C.c_void_p * ns)(*[_ptr(p) for p in src_pools])
-    lb, le = layer_range if layer_range else (0, src_layouts[0].num_layers)
+    lb, le = layer_range if layer_range else _common(src_layouts[0], dst_layout)
     check(lib.kv_compute_scales(ns, S, SP, C.byref(src_batch.bt), dst_layout.handle, _ptr(out), lb, le,
                                 _stream(stream)))
 
@@ -148,13 +161,13 @@ def wire_dtype(src: Layout, dst: Layout):
 
 
 def wire_bytes(src: Layout, dst: Layout, total_tokens, layer_range=None):
-    lb, le = layer_range if layer_range else (0, src.num_layers)
+    lb, le = layer_range if layer_range else _common(src, dst)
     return lib.kv_wire_bytes(src.handle, dst.handle, int(total_tokens), lb, le)
 
 
 def pack(src: Layout, src_pool, src_batch: Batch, dst: Layout, wire, layer_range=None, stream=None, wire_nbytes=None):
     """kv_pack: Fig. 5 flatten of the (src rank -> dst rank) share into `wire`."""
-    lb, le = layer_range if layer_range else (0, src.num_layers)
+    lb, le = layer_range if layer_range else _common(src, dst)
     nb = wire_nbytes if wire_nbytes is not None else wire.numel() * wire.element_size()
     check(lib.kv_pack(src.handle, _ptr(src_pool), C.byref(src_batch.bt), dst.handle, lb, le, _ptr(wire), nb,
                       _stream(stream)))
@@ -163,7 +176,7 @@ def pack(src: Layout, src_pool, src_batch: Batch, dst: Layout, wire, layer_range
 def unpack(src: Layout, dst: Layout, dst_pool, dst_batch: Batch, wire, layer_range=None, stream=None,
            wire_nbytes=None):
     """kv_unpack: Fig. 5 restore of a wire buffer into the D pool (+ tail zero-fill)."""
-    lb, le = layer_range if layer_range else (0, src.num_layers)
+    lb, le = layer_range if layer_range else _common(src, dst)
     nb = wire_nbytes if wire_nbytes is not None else wire.numel() * wire.element_size()
     check(lib.kv_unpack(src.handle, dst.handle, _ptr(dst_pool), C.byref(dst_batch.bt), lb, le, _ptr(wire), nb,
                         _stream(stream)))
@@ -196,7 +209,7 @@ class Comm:
 
     def recv_unpack(self, peer, wire, nbytes, src: Layout, dst: Layout, dst_pool, dst_batch: Batch,
                     layer_range=None, stream=None):
-        lb, le = layer_range if layer_range else (0, src.num_layers)
+        lb, le = layer_range if layer_range else _common(src, dst)
         check(lib.kv_recv_unpack(self._h, peer, _ptr(wire), nbytes, src.handle, dst.handle, _ptr(dst_pool),
                                  C.byref(dst_batch.bt), lb, le, _stream(stream)))
 

@@ -218,6 +218,37 @@ def test_launch_count_and_errors():
         kvx.Batch(lay, [5], [[0, 9]])
 
 
+@pytest.mark.parametrize("tp_p,tp_d,sdt,ddt", [(2, 1, F16, F16), (1, 2, BF16, E4M3), (4, 2, BF16, BF16)])
+def test_pipeline_stage_reshard(o1, tp_p, tp_d, sdt, ddt):
+    """NEXT-2: P stages [0,2),[2,4) -> D stages [0,3),[3,4), one device call per overlapping
+    stage pair over the intersection, == the oracle's staged transfer (pinned against O2)."""
+    from tests.gpu_util import DevCase
+    from tests.test_oracle_pp import D_STAGES, P_STAGES, _pools_for, _staged, staged_transfer
+    import paper_2509_17542_b200 as kvx
+    base = make_case(4, 8, 64, tp_p, tp_d, 16, 32, [70, 5], sdt, ddt, seed=tp_p + 7 * tp_d, o1=None,
+                     tail_garbage=False, scales="pow2")
+    src, dst = _staged(base, P_STAGES, "src"), _staged(base, D_STAGES, "dst")
+    case = dict(src_lays=src, src_pools=_pools_for(src, 300, sdt), dst_lays=dst,
+                dst_pools=_pools_for(dst, 0, ddt, canary=True), n_tokens=base["n_tokens"],
+                src_tables=base["src_tables"], dst_tables=base["dst_tables"])
+    dc = DevCase(case)
+    for sf, se in P_STAGES:
+        si = [i for i, d in enumerate(src) if d["first_layer"] == sf]
+        for df, de in D_STAGES:
+            lb, le = max(sf, df), min(se, de)
+            if lb < le:
+                di = [i for i, d in enumerate(dst) if d["first_layer"] == df]
+                kvx.convert_reshard([dc.src_lays[i] for i in si], [dc.src_pools[i] for i in si], dc.src_bt,
+                                    [dc.dst_lays[i] for i in di], [dc.dst_pools[i] for i in di], dc.dst_bt, (lb, le))
+    torch.cuda.synchronize()
+    want = [p.copy() for p in case["dst_pools"]]
+    staged_transfer(o1, src, case["src_pools"], dst, want, case["n_tokens"], case["src_tables"], case["dst_tables"])
+    assert_pools_match(dc.dst_numpy(), want, ddt)
+    with pytest.raises(kvx.KvError, match="KV_EINVAL"):  # range outside the P stage
+        kvx.convert_reshard(dc.src_lays[:tp_p], dc.src_pools[:tp_p], dc.src_bt, dc.dst_lays[:tp_d],
+                            dc.dst_pools[:tp_d], dc.dst_bt, (1, 3))
+
+
 @pytest.mark.parametrize("sdt", [F16, BF16, E4M3])
 def test_dynamic_scales_then_convert(o1, sdt):
     """NEXT-1: device amax/448 scales == oracle bit-exactly; converting with them == oracle."""
