@@ -199,20 +199,19 @@ kv_status kv_unpack(const kv_layout* src, const kv_layout* dst, void* dst_pool, 
                     kv_stream stream);
 
 /* ---- NEXT-2: self-describing wire header (transfers replayable from files) --
- * Byte-for-byte, little-endian, 64 + 4*n_req bytes:
- *    0 char[4] "KVX1"          4 u32 version (1)         8 u32 header bytes
+ * Byte-for-byte, little-endian, 72 + 4*n_req bytes:
+ *    0 char[4] "KVX1"          4 u32 version (1)         8 u32 header bytes (72 + 4*n_req)
  *   12 i32 wire dtype         16 i32 num_kv_heads       20 i32 head_dim
  *   24 i32 layer_begin        28 i32 layer_end          32 i32 P tp_degree
  *   36 i32 P tp_rank          40 i32 D tp_degree        44 i32 D tp_rank
- *   48 i32 head_begin         52 i32 head_end (global overlap heads carried)
- *   56 i32 n_req              60 u32 payload bytes / 2^32 (high word) ... see below
- *   64 i32 n_tokens[n_req]
- * The payload that follows (kv_wire_bytes bytes, Fig. 5 canonical order) has its byte count
- * at offset 60 (low 32 bits) + the u32 at 60 is the HIGH word: bytes = hi * 2^32 + lo with lo
- * stored after n_tokens as a u32 -- i.e. the header ends with one more u32.  Total header
- * size = 68 + 4*n_req.  kv_wire_header_write fails (KV_ESHAPE) if cap is too small;
- * kv_wire_header_check returns KV_ESHAPE (message says which field) when a header does not
- * describe a (src -> dst, n_tokens, layers) wire. */
+ *   48 i32 head_begin         52 i32 head_end (the global overlap heads carried)
+ *   56 i32 n_req              60 u32 reserved (0)       64 u64 payload bytes
+ *   72 i32 n_tokens[n_req]
+ * The payload that follows in a file is the kv_pack output (kv_wire_bytes bytes, Fig. 5
+ * canonical order).  kv_wire_header_write: KV_ESHAPE if cap is too small or the ranks share
+ * no heads.  kv_wire_header_parse: KV_EINVAL on a bad magic/version/length.
+ * kv_wire_header_check: KV_ESHAPE (the message names the field) when the header does not
+ * describe the (src -> dst, n_tokens, layers) wire an unpack with these arguments expects. */
 typedef struct {
   int32_t wire_dtype, num_kv_heads, head_dim, layer_begin, layer_end;
   int32_t src_tp_degree, src_tp_rank, dst_tp_degree, dst_tp_rank, head_begin, head_end, n_req;

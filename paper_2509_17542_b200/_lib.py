@@ -43,6 +43,14 @@ class Batch_t(C.Structure):
                 ("blk_req", C.c_void_p), ("tok_req", C.c_void_p)]
 
 
+class WireInfo(C.Structure):
+    _fields_ = [("wire_dtype", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
+                ("layer_begin", C.c_int32), ("layer_end", C.c_int32), ("src_tp_degree", C.c_int32),
+                ("src_tp_rank", C.c_int32), ("dst_tp_degree", C.c_int32), ("dst_tp_rank", C.c_int32),
+                ("head_begin", C.c_int32), ("head_end", C.c_int32), ("n_req", C.c_int32),
+                ("payload_bytes", C.c_uint64), ("n_tokens", C.POINTER(C.c_int32))]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -60,6 +68,11 @@ def _load():
         "kv_convert_reshard": (st, [i32, pp, pp, C.POINTER(Batch_t), i32, pp, pp, C.POINTER(Batch_t), i32, i32, p]),
         "kv_compute_scales": (st, [i32, pp, pp, C.POINTER(Batch_t), p, p, i32, i32, p]),
         "kv_wire_dtype": (i32, [p, p]),
+        "kv_wire_header_bytes": (C.c_size_t, [i32]),
+        "kv_wire_header_write": (st, [p, p, i32, p, i32, i32, p, C.c_size_t]),
+        "kv_wire_header_parse": (st, [p, C.c_size_t, C.POINTER(WireInfo)]),
+        "kv_wire_header_check": (st, [p, C.c_size_t, p, p, i32, p, i32, i32]),
+        "kv_copy_bytes": (st, [p, p, C.c_size_t, p]),
         "kv_wire_bytes": (C.c_size_t, [p, p, i64, i32, i32]),
         "kv_pack": (st, [p, p, C.POINTER(Batch_t), p, i32, i32, p, C.c_size_t, p]),
         "kv_unpack": (st, [p, p, p, C.POINTER(Batch_t), i32, i32, p, C.c_size_t, p]),
@@ -93,7 +106,8 @@ lib = _load()
 
 # Every symbol include/kvx.h declares (checked by tests/test_abi.py).
 EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_block_table_update", "kv_plan_pairs",
-           "kv_convert_reshard", "kv_compute_scales", "kv_wire_dtype", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
+           "kv_convert_reshard", "kv_compute_scales", "kv_wire_dtype", "kv_wire_header_bytes",
+           "kv_wire_header_write", "kv_wire_header_parse", "kv_wire_header_check", "kv_copy_bytes", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
            "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
            "kv_recv_unpack", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",
            "kv_launch_count", "kv_launch_count_reset", "kv_last_error", "kv_version")

@@ -127,6 +127,7 @@ cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStr
 cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaStream_t s);
 cudaError_t launch_signal(uint32_t* flag, uint32_t value, cudaStream_t s);
+cudaError_t launch_copy_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t launch_wait(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, int32_t* err, cudaStream_t s);
 
 }  // namespace kvx

@@ -1077,6 +1077,26 @@ cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) 
   return cudaGetLastError();
 }
 
+// Opaque byte copy (hidden state): 16-B vectors when both ends are 16-B aligned, bytes
+// otherwise; a few KiB per request, one small grid.
+__global__ void k_copy_bytes(uint8_t* dst, const uint8_t* src, size_t n) {
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
+  if ((((uintptr_t)dst | (uintptr_t)src) & 15u) == 0) {
+    const size_t nv = n / 16;
+    for (size_t i = tid; i < nv; i += nth) reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(src)[i];
+    for (size_t i = nv * 16 + tid; i < n; i += nth) dst[i] = src[i];
+  } else {
+    for (size_t i = tid; i < n; i += nth) dst[i] = src[i];
+  }
+}
+
+cudaError_t launch_copy_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+  const int blocks = (int)std::min<size_t>(256, (bytes / 16 + 255) / 256 + 1);
+  k_copy_bytes<<<blocks, 256, 0, s>>>(static_cast<uint8_t*>(dst), static_cast<const uint8_t*>(src), bytes);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_signal(uint32_t* flag, uint32_t value, cudaStream_t s) {
   k_signal<<<1, 1, 0, s>>>(flag, value);
   g_launches.fetch_add(1, std::memory_order_relaxed);

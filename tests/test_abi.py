@@ -161,3 +161,35 @@ def test_convert_validation(kvx):
     d_other = _lay(kvx, tp_degree=1, tp_rank=0, num_blocks=11)
     st, msg = call([s0, s1], [d0], bt(s0), bt(d_other))
     assert st == 2 and "another block size" in msg
+
+
+def test_wire_header_layout_roundtrip_and_check(kvx):
+    """NEXT-2 wire header: documented byte offsets, parse round trip, and the
+    check rejects every field that differs."""
+    import struct
+    from paper_2509_17542_b200 import replay
+    s = _lay(kvx, tp_degree=4, tp_rank=1, dtype=kvx.KV_BF16)
+    d = kvx.Layout(2, 8, 16, 2, 0, 4, 10, kvx.KV_F8E4M3, (0, 1, 2, 3, 4, 5), 0x1000)
+    hdr = replay.header(s, d, [5, 7, 1])
+    assert len(hdr) == 72 + 12
+    magic, ver, hlen, wdt, H, D, lb, le, tps, tpr, tpd, tqr, hb, he, nreq, res, pay = struct.unpack_from(
+        "<4sIIiiiiiiiiiiiiIQ", hdr, 0)
+    assert (magic, ver, hlen) == (b"KVX1", 1, 84)
+    assert (wdt, H, D, lb, le) == (kvx.KV_F8E4M3, 8, 16, 0, 2)
+    assert (tps, tpr, tpd, tqr, hb, he, nreq, res) == (4, 1, 2, 0, 2, 4, 3, 0)
+    assert pay == kvx.wire_bytes(s, d, 13) == 2 * 2 * 2 * 13 * 16 * 1
+    assert struct.unpack_from("<3i", hdr, 72) == (5, 7, 1)
+    info = replay.parse(hdr)
+    assert info["n_tokens"] == [5, 7, 1] and info["payload_bytes"] == pay and info["head_end"] == 4
+    replay.check_header(hdr, s, d, [5, 7, 1])
+    with pytest.raises(kvx.KvError, match="token counts"):
+        replay.check_header(hdr, s, d, [5, 7, 2])
+    with pytest.raises(kvx.KvError, match="layer range"):
+        replay.check_header(hdr, s, d, [5, 7, 1], (0, 1))
+    s2 = _lay(kvx, tp_degree=4, tp_rank=0)
+    with pytest.raises(kvx.KvError, match="P parallel strategy"):
+        replay.check_header(hdr, s2, d, [5, 7, 1])
+    with pytest.raises(kvx.KvError, match="bad magic"):
+        replay.parse(b"XXXX" + hdr[4:])
+    with pytest.raises(kvx.KvError, match="share no heads"):
+        replay.header(_lay(kvx, tp_degree=4, tp_rank=3), d, [1])

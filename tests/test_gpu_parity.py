@@ -249,6 +249,31 @@ def test_pipeline_stage_reshard(o1, tp_p, tp_d, sdt, ddt):
                             dc.dst_pools[:tp_d], dc.dst_bt, (1, 3))
 
 
+def test_replay_from_file_and_hidden_state(o1, tmp_path):
+    """NEXT-2: every (p, q) share packed, saved as header + payload, loaded back, header-checked
+    and unpacked == the oracle; a mismatching receiver is refused.  Plus the opaque hidden
+    state copy."""
+    from tests.gpu_util import DevCase
+    import paper_2509_17542_b200 as kvx
+    from paper_2509_17542_b200 import replay
+    case = make_case(3, 8, 32, 4, 2, 8, 16, [19, 40], BF16, E4M3, seed=12, o1=o1, scales="pow2")
+    dc = DevCase(case)
+    for p, q, _, _ in kvx.plan_pairs(4, 2, 8):
+        path = str(tmp_path / f"kv_{p}_{q}.kvx")
+        replay.save(path, dc.src_lays[p], dc.src_pools[p], dc.src_bt, dc.dst_lays[q])
+        info = replay.load(path, dc.src_lays[p], dc.dst_lays[q], dc.dst_pools[q], dc.dst_bt)
+        assert info["src_tp_rank"] == p and info["dst_tp_rank"] == q
+    torch.cuda.synchronize()
+    assert_pools_match(dc.dst_numpy(), expected(case, o1), E4M3)
+    with pytest.raises(kvx.KvError, match="P parallel strategy"):
+        replay.load(str(tmp_path / "kv_0_0.kvx"), dc.src_lays[1], dc.dst_lays[0], dc.dst_pools[0], dc.dst_bt)
+    h = torch.randint(0, 255, (16384 + 3,), dtype=torch.uint8, device="cuda")
+    out = torch.zeros(16384 + 8, dtype=torch.uint8, device="cuda")
+    replay.copy_hidden(out[5:], h)  # misaligned destination on purpose
+    torch.cuda.synchronize()
+    assert torch.equal(out[5:5 + h.numel()], h) and int(out[:5].sum()) == 0
+
+
 @pytest.mark.parametrize("sdt", [F16, BF16, E4M3])
 def test_dynamic_scales_then_convert(o1, sdt):
     """NEXT-1: device amax/448 scales == oracle bit-exactly; converting with them == oracle."""
