@@ -441,9 +441,10 @@ def run_multi(args):
         s_a, s_b = torch.cuda.Stream(), torch.cuda.Stream()
         events, wires = {}, {}
         if me.kind == "P":
+            # P's view of each D rank's layout, with D's fp8 scales on P's GPU (sender cast)
             peers = {q: kvx.Layout.from_dict(
                 synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, w.NB_d, cfg.dst_dtype, cfg.d_order),
-                torch.ones(cfg.L * 2 * (cfg.H // cfg.tp_d), device=dev))
+                torch.from_numpy(synth.pow2_scales(cfg.seed + 200 + q, cfg.L, cfg.H // cfg.tp_d)).to(dev))
                 for p, q, _, _ in pairs if p == me.tp_rank}
             S = w.src_lays[me.tp_rank]
             for q, dl in peers.items():

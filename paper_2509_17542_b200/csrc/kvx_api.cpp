@@ -14,6 +14,7 @@ namespace kvx {
 
 static thread_local std::string t_err;
 std::atomic<uint64_t> g_launches{0};
+std::atomic<int32_t> g_sm_budget{0};
 
 kv_status fail(kv_status st, const std::string& msg) {
   t_err = msg;
@@ -131,6 +132,7 @@ const char* kv_last_error(void) { return t_err.c_str(); }
 const char* kv_version(void) { return "kvx 0.1 (sm_100a)"; }
 uint64_t kv_launch_count(void) { return g_launches.load(); }
 void kv_launch_count_reset(void) { g_launches.store(0); }
+int32_t kv_set_sm_budget(int32_t n_sms) { return g_sm_budget.exchange(n_sms < 0 ? 0 : n_sms); }
 
 kv_status kv_layout_describe(const kv_layout_desc* desc, kv_layout** out, size_t* pool_bytes) {
   if (!desc || !out) return fail(KV_EINVAL, "kv_layout_describe: null argument");

@@ -861,7 +861,8 @@ int num_sms() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
     dev = d;
   }
-  return sms;
+  const int budget = g_sm_budget.load(std::memory_order_relaxed);
+  return (budget > 0 && budget < sms) ? budget : sms;
 }
 
 template <typename K>

@@ -13,7 +13,7 @@ from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BY
                    KV_F32, Batch_t, KvError, LayoutDesc, check, lib)
 
 __all__ = ["Layout", "Batch", "convert_reshard", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
-           "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "launch_count", "launch_count_reset",
+           "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "launch_count", "launch_count_reset", "set_sm_budget",
            "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "DTYPE_BYTES",
            "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
 
@@ -263,6 +263,11 @@ def wait(flag, value, err, timeout_s=10.0, stream=None):
 
 def launch_count():
     return lib.kv_launch_count()
+
+
+def set_sm_budget(n_sms: int) -> int:
+    """kv_set_sm_budget: cap the SMs later data-path launches may use (0 = all)."""
+    return lib.kv_set_sm_budget(int(n_sms))
 
 
 def launch_count_reset():

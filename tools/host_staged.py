@@ -41,6 +41,9 @@ def main():
     dst = Workload(cfg, [], [0], torch.device("cuda", 1))
     S, SP = src.src_lays[0], src.src_pools[0]
     Dl, DP = dst.dst_lays[0], dst.dst_pools[0]
+    # P's view of the D layout: the fp8 scales must live on P's GPU (the sender casts)
+    sc = dst.dst_dicts[0].get("scales")
+    Dl_p = kvx.Layout.from_dict(dst.dst_dicts[0], None if sc is None else torch.from_numpy(sc).to("cuda:0"))
     lc = args.layer_chunk
     chunks = [(l0, min(cfg.L, l0 + lc)) for l0 in range(0, cfg.L, lc)]
     nb = max(kvx.wire_bytes(S, Dl, cfg.total_tokens, c) for c in chunks)
@@ -59,7 +62,7 @@ def main():
             lr = chunks[k]
             n = kvx.wire_bytes(S, Dl, cfg.total_tokens, lr)
             with torch.cuda.device(0), torch.cuda.stream(s0):
-                kvx.pack(S, SP, src.src_bt, Dl, w0[k % 2], lr, s0, wire_nbytes=n)
+                kvx.pack(S, SP, src.src_bt, Dl_p, w0[k % 2], lr, s0, wire_nbytes=n)
                 hA[k % 2][:n].copy_(w0[k % 2][:n], non_blocking=True)
                 e0[k] = torch.cuda.Event()
                 e0[k].record(s0)
