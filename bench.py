@@ -573,7 +573,7 @@ def run_multi(args):
                        "parallelism": f"P TP{cfg.tp_p} x D TP{cfg.tp_d}, {npair} pair(s)"},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED_GBS,
                          "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED_GBS, 4),
-                         "traffic": _traffic(wl_name, world),
+                         "traffic": _traffic(wl_name, world) if args.mode == "push" else None,
                          "kernel": "k_convert_rows (peer-store push)" if args.mode == "push"
                          else "pack + ncclSend/Recv + unpack (whole P step)",
                          "kernel_ms": round(kms, 4), "algorithmic_bytes_per_launch": nvl_b,

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--copy", action="store_true", help="also time a cudaMemcpyPeer-style torch copy 0 -> 1")
     ap.add_argument("--layer-chunk", type=int, default=0)
+    ap.add_argument("--budgets", default="0", help="comma list of SM budgets to sweep (0 = all SMs)")
     args = ap.parse_args()
     import paper_2509_17542_b200 as kvx
     cfg = synth.configs()[args.workload]
@@ -36,33 +37,40 @@ def main():
     dst = Workload(cfg, [], [0], torch.device("cuda", 1))
     torch.cuda.set_device(0)
     S, SP = src.src_lays[0], src.src_pools[0]
-    Dl, DP = dst.dst_lays[0], dst.dst_pools[0]
+    DP = dst.dst_pools[0]
+    # P's view of the D layout: D's fp8 scales on P's GPU (the sender casts)
+    sc = dst.dst_dicts[0].get("scales")
+    Dl = kvx.Layout.from_dict(dst.dst_dicts[0], None if sc is None else torch.from_numpy(sc).to("cuda:0"))
     lc = args.layer_chunk or cfg.L
 
     def fn():
         for l0 in range(0, cfg.L, lc):
             kvx.convert_reshard([S], [SP], src.src_bt, [Dl], [DP], src.dst_bt, (l0, min(cfg.L, l0 + lc)))
 
-    for _ in range(3):
-        fn()
-    torch.cuda.synchronize(0)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.iters)]
-    for a, b in ev:
-        a.record()
-        fn()
-        b.record()
-    torch.cuda.synchronize(0)
-    ts = [a.elapsed_time(b) for a, b in ev]
     nvl = dst.dst_bytes([0])
-    med = statistics.median(ts)
-    out = {"case": f"{args.workload} pair push cuda:0 -> cuda:1", "ms_med": round(med, 4), "ms_min": round(min(ts), 4),
-           "nvlink_GBs": round(nvl / med / 1e6, 1), "frac_770": round(nvl / med / 1e6 / 770, 4),
-           "src_GBs": round(src.src_bytes([0]) / med / 1e6, 1), "nvlink_bytes": nvl, "layer_chunk": lc}
-    torch.cuda.synchronize(1)
-    dst.src_pools[0], dst.src_dicts[0] = SP, src.src_dicts[0]
-    ok, det = sample_parity(dst, (0, 1), 0, [0], [0])
-    out["parity_ok"] = ok
-    print(json.dumps(out), flush=True)
+    for budget in [int(x) for x in args.budgets.split(",")]:
+        kvx.set_sm_budget(budget)
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(0)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.iters)]
+        for a, b in ev:
+            a.record()
+            fn()
+            b.record()
+        torch.cuda.synchronize(0)
+        ts = [a.elapsed_time(b) for a, b in ev]
+        med = statistics.median(ts)
+        out = {"case": f"{args.workload} pair push cuda:0 -> cuda:1", "sm_budget": budget or "all",
+               "ms_med": round(med, 4), "ms_min": round(min(ts), 4),
+               "nvlink_GBs": round(nvl / med / 1e6, 1), "frac_770": round(nvl / med / 1e6 / 770, 4),
+               "src_GBs": round(src.src_bytes([0]) / med / 1e6, 1), "nvlink_bytes": nvl, "layer_chunk": lc}
+        torch.cuda.synchronize(1)
+        dst.src_pools[0], dst.src_dicts[0] = SP, src.src_dicts[0]
+        ok, det = sample_parity(dst, (0, 1), 0, [0], [0])
+        out["parity_ok"] = ok
+        print(json.dumps(out), flush=True)
+    kvx.set_sm_budget(0)
     if args.copy:
         n = 1 << 30
         a = torch.empty(n, dtype=torch.uint8, device="cuda:0")
