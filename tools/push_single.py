@@ -27,9 +27,14 @@ def main():
     ap.add_argument("--copy", action="store_true", help="also time a cudaMemcpyPeer-style torch copy 0 -> 1")
     ap.add_argument("--layer-chunk", type=int, default=0)
     ap.add_argument("--budgets", default="0", help="comma list of SM budgets to sweep (0 = all SMs)")
+    ap.add_argument("--dst-dtype", default="", help="override the destination dtype (f16|bf16|e4m3|f32)")
     args = ap.parse_args()
     import paper_2509_17542_b200 as kvx
     cfg = synth.configs()[args.workload]
+    if args.dst_dtype:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, dst_dtype={"f16": synth.F16, "bf16": synth.BF16, "e4m3": synth.E4M3,
+                                                  "f32": synth.F32}[args.dst_dtype])
     torch.cuda.set_device(0)
     kvx.peer_enable(1)
     src = Workload(cfg, [0], [], torch.device("cuda", 0))  # also holds D's tables on cuda:0
