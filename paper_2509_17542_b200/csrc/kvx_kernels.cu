@@ -285,10 +285,9 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
 // (0 copy, 1 zero-fill tail row, 2 no row).  The warp streams the 32 x 2^cs chunks of
 // 16 B (source side) with U loads in flight per lane, fetching row state by shuffles.
 // ------------------------------------------------------------------------------------
-template <int SDT, int DDT, int U>
+template <int SDT, int DDT, int U, int VEC = 8>
 __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t sp, uint64_t dp, float rsc,
                                             uint32_t rz) {
-  constexpr int VEC = 8;
   const uint32_t cmask = (1u << cs) - 1u;
   const uint32_t nch = 32u << cs;
   for (uint32_t base = 0; base < nch; base += 32u * U) {
@@ -386,7 +385,7 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
   }
 }
 
-template <int SDT, int DDT, int U>
+template <int SDT, int DDT, int U, int VEC = 8>
 __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant__ ConvArgs a) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
@@ -397,7 +396,7 @@ __global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant
     float rsc;
     uint32_t rz;
     conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz);
-    stream_rows<SDT, DDT, U>(lane, cs, sp, dp, rsc, rz);
+    stream_rows<SDT, DDT, U, VEC>(lane, cs, sp, dp, rsc, rz);
   }
 }
 
@@ -945,6 +944,7 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
     // TMA-staged variant (KVX_TMA=1, experiment until measured): source rows must be whole
     // 16-byte multiples for cp.async.bulk
     static const int tma = getenv("KVX_TMA") ? atoi(getenv("KVX_TMA")) : 0;
+    static const bool wide = getenv("KVX_VEC16") ? atoi(getenv("KVX_VEC16")) == 1 : false;
     const uint32_t RB = (uint32_t)a.D * Tr<SDT>::B;
     if (tma == 1 && RB % 16 == 0) {
       auto k = k_convert_tma<SDT, DDT>;
@@ -960,8 +960,21 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
       const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms() * occ));
       k<<<grid, nw * 32, smem, s>>>(a);
     } else {
-      auto k = k_convert_rows<SDT, DDT, U>;
-      k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
+      bool done = false;
+      if constexpr (Tr<SDT>::B == 2 && DDT == KV_F8E4M3) {
+        if (wide && cpr >= 2) {
+          // 16 elements per chunk: two 16-B loads, one 16-B store (peer writes go out as
+          // full 16-B vectors); half the chunks per row, same bytes in flight per lane
+          a.cpr_shift = log2_pow2(cpr / 2);
+          auto k = k_convert_rows<SDT, DDT, (U > 1 ? U / 2 : 1), 16>;
+          k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
+          done = true;
+        }
+      }
+      if (!done) {
+        auto k = k_convert_rows<SDT, DDT, U>;
+        k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
+      }
     }
   } else {
     auto k = k_convert<VEC, SDT, DDT, U>;
