@@ -381,6 +381,11 @@ def _traffic(workload, n):
 # N >= 2: c4 pairs across NVLink
 # ------------------------------------------------------------------------------------
 def run_multi(args):
+    """N >= 2: a configuration's P -> D transfer across NVLink, P and D on disjoint GPUs.
+    Ranks [0, n_p) are P TP ranks 0..n_p-1, [n_p, n_p + n_d) D TP ranks 0..n_d-1, the rest
+    idle (transfer.present_ranks: the largest complete sub-transfer that fits; the full one
+    when N >= tp_p + tp_d).  c4 (default): N/2 1:1 pairs; c3: P0,P1 -> D0 per 3 GPUs (fan-in
+    2); c2: P0,P1 -> D0."""
     import torch
     import torch.distributed as dist
     import paper_2509_17542_b200 as kvx
@@ -392,34 +397,36 @@ def run_multi(args):
     dist.init_process_group("nccl", device_id=dev)
     wl_name = args.workload or "c4"
     cfg = synth.configs()[wl_name]
-    if world % 2:
-        raise SystemExit("bench.py multi-GPU needs an even number of GPUs (P and D halves)")
-    npair = world // 2
-    roles = tr.roles(world, npair, npair)
+    n_p, n_d = tr.present_ranks(cfg.tp_p, cfg.tp_d, world)
+    if n_p < 1 or n_d < 1:
+        raise SystemExit(f"{wl_name} needs at least {1 + max(cfg.tp_p // cfg.tp_d, cfg.tp_d // cfg.tp_p, 1)} GPUs")
+    roles = tr.roles(world, n_p, n_d, allow_idle=True)
     me = roles[rank]
-    p_ranks = list(range(npair))
-    pairs = tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks=set(p_ranks), d_ranks=set(range(npair)))
-    mine_p = [me.tp_rank] if me.kind == "P" else []
-    mine_d = [me.tp_rank] if me.kind == "D" else []
-    w = Workload(cfg, mine_p, mine_d, dev)
+    pairs = tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks=set(range(n_p)), d_ranks=set(range(n_d)))
+    my_q = sorted({q for p, q, _, _ in pairs if me.kind == "P" and p == me.tp_rank})
+    my_p = sorted({p for p, q, _, _ in pairs if me.kind == "D" and q == me.tp_rank})
+    w = Workload(cfg, [me.tp_rank] if me.kind == "P" else [], [me.tp_rank] if me.kind == "D" else [], dev)
     stream = torch.cuda.current_stream()
     barrier_t = torch.zeros(1, device=dev)
 
     def barrier():
         dist.all_reduce(barrier_t)
 
-    flag = torch.zeros(4, dtype=torch.int32, device=dev)
+    flags = torch.zeros(max(n_p, 1), dtype=torch.int32, device=dev)  # one word per P source
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     epoch = [0]
     lc = args.layer_chunk or cfg.L
+
+    def d_view(q):  # P's view of D rank q's layout (D's fp8 scales on P's GPU: the sender casts)
+        sc = None
+        if cfg.dst_dtype == synth.E4M3:
+            sc = torch.from_numpy(synth.pow2_scales(cfg.seed + 200 + q, cfg.L, cfg.H // cfg.tp_d)).to(dev)
+        return kvx.Layout.from_dict(
+            synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, w.NB_d, cfg.dst_dtype, cfg.d_order), sc)
+
     if args.mode == "push":
-        ch = tr.PushChannel(me, w.dst_pools.get(me.tp_rank), flag if me.kind == "D" else None)
-        my_pairs = [(p, q) for p, q, _, _ in pairs if me.kind == "P" and p == me.tp_rank]
-        dst_lays = {q: kvx.Layout.from_dict(
-            synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, w.NB_d, cfg.dst_dtype, cfg.d_order,
-                         np.ones((1,), np.float32)),
-            torch.from_numpy(synth.pow2_scales(cfg.seed + 200 + q, cfg.L, cfg.H // cfg.tp_d)).to(dev))
-            for _, q in my_pairs}
+        ch = tr.PushChannel(me, w.dst_pools.get(me.tp_rank), flags if me.kind == "D" else None)
+        dst_lays = {q: d_view(q) for q in my_q}
 
         def step(ev=None):
             epoch[0] += 1
@@ -427,11 +434,12 @@ def run_multi(args):
                 if ev is not None:
                     ev[0].record(stream)
                 tr.push_step(w.src_lays[me.tp_rank], w.src_pools[me.tp_rank], w.src_bt, dst_lays, ch.peer_pool,
-                             w.dst_bt, ch.peer_flag, epoch[0], lc, stream)
+                             w.dst_bt, ch.peer_flag, epoch[0], lc, stream, flag_slot=me.tp_rank)
                 if ev is not None:
                     ev[1].record(stream)
-            else:
-                kvx.wait(flag, epoch[0], err, 30.0, stream)
+            elif me.kind == "D":
+                for p in my_p:
+                    kvx.wait(flags[p:p + 1], epoch[0], err, 30.0, stream)
     else:
         # NCCL baseline: pack -> ncclSend / ncclRecv -> unpack, per-layer double-buffered
         uid = [kvx.Comm.unique_id() if rank == 0 else None]
@@ -441,25 +449,17 @@ def run_multi(args):
         s_a, s_b = torch.cuda.Stream(), torch.cuda.Stream()
         events, wires = {}, {}
         if me.kind == "P":
-            # P's view of each D rank's layout, with D's fp8 scales on P's GPU (sender cast)
-            peers = {q: kvx.Layout.from_dict(
-                synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, w.NB_d, cfg.dst_dtype, cfg.d_order),
-                torch.from_numpy(synth.pow2_scales(cfg.seed + 200 + q, cfg.L, cfg.H // cfg.tp_d)).to(dev))
-                for p, q, _, _ in pairs if p == me.tp_rank}
+            peers = {q: d_view(q) for q in my_q}
             S = w.src_lays[me.tp_rank]
-            for q, dl in peers.items():
-                nb = max(kvx.wire_bytes(S, dl, cfg.total_tokens, (l0, min(cfg.L, l0 + lc))) for l0 in range(0, cfg.L, lc))
-                for b in range(2):
-                    wires[(q, b)] = torch.empty(nb, dtype=torch.uint8, device=dev)
         else:
             peers = {p: kvx.Layout.from_dict(
                 synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, w.NB_p, cfg.src_dtype, cfg.p_order))
-                for p, q, _, _ in pairs if q == me.tp_rank}
-            Dl = w.dst_lays[me.tp_rank]
-            for p, sl in peers.items():
-                nb = max(kvx.wire_bytes(sl, Dl, cfg.total_tokens, (l0, min(cfg.L, l0 + lc))) for l0 in range(0, cfg.L, lc))
-                for b in range(2):
-                    wires[(p, b)] = torch.empty(nb, dtype=torch.uint8, device=dev)
+                for p in my_p}
+        for k, other in peers.items():
+            sl, dl = (S, other) if me.kind == "P" else (other, w.dst_lays[me.tp_rank])
+            nb = max(kvx.wire_bytes(sl, dl, cfg.total_tokens, (l0, min(cfg.L, l0 + lc))) for l0 in range(0, cfg.L, lc))
+            for b in range(2):
+                wires[(k, b)] = torch.empty(nb, dtype=torch.uint8, device=dev)
 
         def step(ev=None):
             st = torch.cuda.Event()
@@ -470,13 +470,13 @@ def run_multi(args):
                 ev[0].record(stream)
             if me.kind == "P":
                 tr.nccl_send_step(comm, w.src_lays[me.tp_rank], w.src_pools[me.tp_rank], w.src_bt, peers,
-                                  {q: npair + q for q in peers}, wires, lc, s_a, s_b, events)
-            else:
+                                  {q: n_p + q for q in peers}, wires, lc, s_a, s_b, events)
+            elif me.kind == "D":
                 tr.nccl_recv_step(comm, peers, w.dst_lays[me.tp_rank], w.dst_pools[me.tp_rank], w.dst_bt,
                                   {p: p for p in peers}, wires, lc, s_a, s_b, events)
-            for s in (s_a, s_b):
+            for s_ in (s_a, s_b):
                 e = torch.cuda.Event()
-                e.record(s)
+                e.record(s_)
                 stream.wait_event(e)
             if ev is not None:
                 ev[1].record(stream)
@@ -505,113 +505,114 @@ def run_multi(args):
     kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev) if me.kind == "P" else 0.0
     if int(err.item()):
         raise SystemExit(f"rank {rank}: flag wait timed out")
-    stats = torch.tensor([my_ms, kern_ms, float(launches)], device=dev, dtype=torch.float64)
-    allst = [torch.zeros_like(stats) for _ in range(world)]
-    dist.all_gather(allst, stats)
-    allst = [s.tolist() for s in allst]
+    # busiest link: P egress = bytes it sends, D ingress = bytes it receives (wire dtype = dst)
+    nvl_in = w.dst_bytes([0]) if me.kind == "D" else 0
+    nvl_out = sum(w.dst_bytes([0]) * (len([1 for p2, q2, _, _ in pairs if q2 == q and p2 == me.tp_rank])) //
+                  max(1, len([1 for p2, q2, _, _ in pairs if q2 == q])) for q in my_q) if me.kind == "P" else 0
+    stats = {"ms": my_ms, "kern_ms": kern_ms, "launches": launches, "kind": me.kind, "nvl": max(nvl_in, nvl_out),
+             "clk": clk}
     parity = None
-    if not args.no_parity:
-        # D ranks check their own pool on a sample against the oracle (inputs regenerated
-        # from the same seeds on the D rank's GPU)
-        parity = parity_multi(args, cfg, w, me, dev)
-    allpar = tr.exchange(parity)
+    if not args.no_parity and me.kind == "D":
+        parity = parity_multi(cfg, w, me, my_p, dev)
     e2e = None
     if not args.no_e2e and args.mode == "push":
-        # end to end through the public API with host buffers: every step the P rank
-        # uploads its source pool from pinned memory, pushes, and the D rank reads its
-        # pool back to pinned memory
-        ke = min(K, 3)
-        if me.kind == "P":
-            host = w.src_pools[me.tp_rank].cpu().pin_memory()
-        else:
-            host = torch.empty(w.dst_pools[me.tp_rank].numel(), dtype=torch.uint8).pin_memory()
-        torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(ke):
-            if me.kind == "P":
-                w.src_pools[me.tp_rank].copy_(host, non_blocking=True)
-                step()
-            else:
-                step()
-                host.copy_(w.dst_pools[me.tp_rank], non_blocking=True)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        if int(err.item()):
-            raise SystemExit(f"rank {rank}: flag wait timed out (e2e)")
-        st2 = torch.tensor([e0.elapsed_time(e1), float(host.numel() if me.kind == "P" else 0),
-                            float(host.numel() if me.kind == "D" else 0)], device=dev, dtype=torch.float64)
-        al2 = [torch.zeros_like(st2) for _ in range(world)]
-        dist.all_gather(al2, st2)
-        al2 = [s.tolist() for s in al2]
-        ms_e = max(s[0] for s in al2) / ke
-        e2e = {"value": round(w.src_bytes(range(npair)) / (ms_e * 1e-3) / 1e9, 3), "unit": "GB/s",
-               "ms_per_step": round(ms_e, 3), "h2d_bytes_per_step": int(sum(s[1] for s in al2)),
-               "d2h_bytes_per_step": int(sum(s[2] for s in al2)), "steps": ke}
-        del host
+        e2e = e2e_multi(w, me, step, stream, barrier, err, min(K, 3), rank)
+    allx = tr.exchange({"stats": stats, "parity": parity, "e2e": e2e})
     if rank == 0:
-        max_ms = max(s[0] for s in allst)
+        sts = [x["stats"] for x in allx]
+        max_ms = max(x["ms"] for x in sts)
         ms = max_ms / K
-        kms = statistics.mean(s[1] for s in allst[:npair])
-        src_b = w.src_bytes(range(npair))
-        nvl_b = w.dst_bytes(range(1)) if cfg.tp_p == cfg.tp_d else None
-        achieved = nvl_b / (kms * 1e-3) / 1e9
+        kms = max(x["kern_ms"] for x in sts if x["kind"] == "P")
+        src_b = w.src_bytes(range(n_p))
+        nvl_b = max(x["nvl"] for x in sts)
+        achieved = nvl_b / (ms * 1e-3) / 1e9
+        full = n_p == cfg.tp_p and n_d == cfg.tp_d
         out = {
             "metric": METRIC, "value": round(src_b / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "n_gpus": world,
             "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "ms_per_request": round(ms / len(cfg.n_tokens), 5), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": _dtype_name(cfg),
             "data": "synthetic (seeded random finite bit patterns, Fisher-Yates block tables, pow2 fp8 scales)",
-            "config": {"workload": f"{wl_name} pairs: {cfg.note}; {npair} (P rank p -> D rank p) pair(s), "
-                                   f"P on GPUs 0..{npair - 1}, D on GPUs {npair}..{world - 1}"
-                                   + (" (full c4)" if npair == 4 else " (per-GPU-equivalent sub-config)"),
+            "config": {"workload": f"{wl_name}: {cfg.note}; P ranks 0..{n_p - 1} on GPUs 0..{n_p - 1}, D ranks "
+                                   f"0..{n_d - 1} on GPUs {n_p}..{n_p + n_d - 1}"
+                                   + (" (full transfer)" if full else " (per-GPU-equivalent sub-config)")
+                                   + (f", {world - n_p - n_d} idle GPU(s)" if world > n_p + n_d else ""),
                        "mode": args.mode, "layer_chunk": lc, "requests": len(cfg.n_tokens),
                        "tokens": cfg.total_tokens, "src_bytes_per_step": src_b,
-                       "nvlink_bytes_per_pair_per_step": nvl_b, "l2": "inputs larger than L2 (no flush)",
-                       "parallelism": f"P TP{cfg.tp_p} x D TP{cfg.tp_d}, {npair} pair(s)"},
+                       "busiest_link_bytes_per_step": nvl_b, "pairs": [list(x[:2]) for x in pairs],
+                       "l2": "inputs larger than L2 (no flush)",
+                       "parallelism": f"P TP{cfg.tp_p} x D TP{cfg.tp_d}, {n_p}+{n_d} ranks present"},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED_GBS,
                          "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED_GBS, 4),
                          "traffic": _traffic(wl_name, world) if args.mode == "push" else None,
                          "kernel": "k_convert_rows (peer-store push)" if args.mode == "push"
                          else "pack + ncclSend/Recv + unpack (whole P step)",
-                         "kernel_ms": round(kms, 4), "algorithmic_bytes_per_launch": nvl_b,
+                         "kernel_ms": round(kms, 4), "algorithmic_bytes_per_step": nvl_b,
+                         "note": "busiest GPU link (P egress or D ingress) bytes / step time",
                          "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)",
                          "frac_vs_nominal_900": round(achieved / NVLINK_NOMINAL_GBS, 4)},
-            "clocks": clk, "gpu_launches": int(sum(s[2] for s in allst)),
-            "parity": [p for p in allpar if p is not None],
+            "clocks": sts[0]["clk"], "clocks_all_ranks": [x["clk"].get("reasons") for x in sts],
+            "gpu_launches": int(sum(x["launches"] for x in sts)),
+            "parity": [x["parity"] for x in allx if x["parity"] is not None],
         }
-        if e2e is not None:
-            out["e2e"] = e2e
+        es = [x["e2e"] for x in allx if x["e2e"] is not None]
+        if es:
+            ms_e = max(e["ms"] for e in es) / es[0]["steps"]
+            out["e2e"] = {"value": round(src_b / (ms_e * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms_e, 3),
+                          "h2d_bytes_per_step": int(sum(e["h2d"] for e in es)),
+                          "d2h_bytes_per_step": int(sum(e["d2h"] for e in es)), "steps": es[0]["steps"]}
         print(json.dumps(out), flush=True)
     barrier()
     dist.destroy_process_group()
 
 
-def parity_multi(args, cfg, w, me, dev):
-    if me.kind != "D":
-        return None
-    q = me.tp_rank
-    p = q  # identity pairing (tp_p == tp_d)
-    # regenerate P rank p's pool from its seed on this GPU (same generator, same seed)
+def e2e_multi(w, me, step, stream, barrier, err, ke, rank):
+    """Same metric through the public API with host buffers: every step the P rank uploads
+    its source pool from pinned memory before pushing, the D rank reads its pool back."""
+    import torch
+    host = None
+    if me.kind == "P":
+        host = w.src_pools[me.tp_rank].cpu().pin_memory()
+    elif me.kind == "D":
+        host = torch.empty(w.dst_pools[me.tp_rank].numel(), dtype=torch.uint8).pin_memory()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(ke):
+        if me.kind == "P":
+            w.src_pools[me.tp_rank].copy_(host, non_blocking=True)
+        step()
+        if me.kind == "D":
+            host.copy_(w.dst_pools[me.tp_rank], non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if int(err.item()):
+        raise SystemExit(f"rank {rank}: flag wait timed out (e2e)")
+    return {"ms": e0.elapsed_time(e1), "steps": ke, "h2d": host.numel() if me.kind == "P" else 0,
+            "d2h": host.numel() if me.kind == "D" else 0}
+
+
+def parity_multi(cfg, w, me, my_p, dev):
+    """D rank: regenerate its P sources' pools from their seeds on this GPU and check a
+    sample of the received pool against the oracle."""
     import torch
     import paper_2509_17542_b200 as kvx
-    d = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, w.NB_p, cfg.src_dtype, cfg.p_order)
-    lay = kvx.Layout.from_dict(d)
-    pool = lay.new_pool(dev)
-    view = pool.view(torch.uint8 if synth.NBYTES[cfg.src_dtype] == 1 else torch.int16)
-    synth.fill_random_finite_(view, cfg.seed + 100 + p, cfg.src_dtype)
-    w.src_dicts[p], w.src_pools[p] = d, pool
-    ok, det = sample_parity(w, (0, 2), 0, [p], [q])
+    q = me.tp_rank
+    for p in my_p:
+        d = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, w.NB_p, cfg.src_dtype, cfg.p_order)
+        pool = kvx.Layout.from_dict(d).new_pool(dev)
+        view = pool.view(torch.uint8 if synth.NBYTES[cfg.src_dtype] == 1 else torch.int16)
+        synth.fill_random_finite_(view, cfg.seed + 100 + p, cfg.src_dtype)
+        w.src_dicts[p], w.src_pools[p] = d, pool
+    ok, det = sample_parity(w, (0, 2), 0, my_p, [q])
     det["rank"] = f"D{q}"
-    del w.src_pools[p]
+    for p in my_p:
+        del w.src_pools[p]
     return {"ok": ok, **det}
 
 
-# ------------------------------------------------------------------------------------
-# reference arm: the oracle on the host cores
-# ------------------------------------------------------------------------------------
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:

@@ -30,11 +30,27 @@ class Role:
     world_rank: int
 
 
-def roles(world_size: int, n_p: int, n_d: int):
-    """Global rank -> Role; P ranks first, then D ranks (disjoint GPU groups)."""
-    if n_p + n_d != world_size:
+def roles(world_size: int, n_p: int, n_d: int, allow_idle: bool = False):
+    """Global rank -> Role; P ranks first, then D ranks (disjoint GPU groups); with
+    allow_idle, ranks beyond n_p + n_d are idle ("X": they only join the barriers)."""
+    if n_p + n_d != world_size and not (allow_idle and n_p + n_d < world_size):
         raise ValueError(f"world_size {world_size} != n_p {n_p} + n_d {n_d}")
-    return [Role("P", r, r) if r < n_p else Role("D", r - n_p, r) for r in range(world_size)]
+    return [Role("P", r, r) if r < n_p else Role("D", r - n_p, r) if r < n_p + n_d else Role("X", -1, r)
+            for r in range(world_size)]
+
+
+def present_ranks(tp_p: int, tp_d: int, world_size: int):
+    """How many P and D TP ranks a job of world_size GPUs can run as a complete sub-transfer
+    (every present D rank has all the P ranks holding its heads): (n_p, n_d).
+    Merge (tp_p >= tp_d): each D rank needs tp_p/tp_d P ranks; split: each P rank feeds
+    tp_d/tp_p D ranks.  With world_size >= tp_p + tp_d this is the full transfer."""
+    if tp_p >= tp_d:
+        ratio = tp_p // tp_d
+        n_d = min(tp_d, world_size // (1 + ratio))
+        return n_d * ratio, n_d
+    ratio = tp_d // tp_p
+    n_p = min(tp_p, world_size // (1 + ratio))
+    return n_p, n_p * ratio
 
 
 def pair_plan(tp_p: int, tp_d: int, num_kv_heads: int, p_ranks=None, d_ranks=None):
@@ -83,16 +99,19 @@ class PushChannel:
 
 
 def push_step(src_layout, src_pool, src_batch, dst_layouts, peer_pools, dst_batch, peer_flags, epoch,
-              layer_chunk=None, stream=None):
-    """P side of one push transfer: fused gather/convert/NVLink-store into each paired D
-    pool (optionally per layer chunk, A10), then a release flag per D rank (A11)."""
-    L = src_layout.num_layers
-    chunk = layer_chunk or L
-    for q, dl in dst_layouts.items():
-        for l0 in range(0, L, chunk):
-            kv.convert_reshard([src_layout], [src_pool], src_batch, [dl], [peer_pools[q]], dst_batch,
-                               (l0, min(L, l0 + chunk)), stream)
-        kv.signal(peer_flags[q], epoch, stream)
+              layer_chunk=None, stream=None, flag_slot=0):
+    """P side of one push transfer: ONE fused gather/convert/NVLink-store launch per layer
+    chunk covering every paired D rank (A10), then a release flag per D rank (A11).  With
+    fan-in (several P ranks feeding one D rank) each P rank writes its own flag word
+    ``flag_slot`` of the D rank's flag array."""
+    L0, L1 = src_layout.layers
+    chunk = layer_chunk or (L1 - L0)
+    qs = sorted(dst_layouts)
+    for l0 in range(L0, L1, chunk):
+        kv.convert_reshard([src_layout], [src_pool], src_batch, [dst_layouts[q] for q in qs],
+                           [peer_pools[q] for q in qs], dst_batch, (l0, min(L1, l0 + chunk)), stream)
+    for q in qs:
+        kv.signal(peer_flags[q] + 4 * flag_slot, epoch, stream)
 
 
 def nccl_send_step(comm, src_layout, src_pool, src_batch, dst_layouts, dst_world, wires, layer_chunk, pack_stream,

@@ -85,3 +85,25 @@ def test_roles_validation():
     # c3: TP4 -> TP2 merge; c5 per P instance: TP2 -> TP4 split
     assert sorted((p, q) for p, q, _, _ in tr.pair_plan(4, 2, 8)) == [(0, 0), (1, 0), (2, 1), (3, 1)]
     assert sorted((p, q) for p, q, _, _ in tr.pair_plan(2, 4, 8)) == [(0, 0), (0, 1), (1, 2), (1, 3)]
+
+
+def test_present_ranks_sub_transfers():
+    """The largest complete sub-transfer per GPU count: every present D rank has all the P
+    ranks holding its heads; N >= tp_p + tp_d is the full transfer."""
+    from paper_2509_17542_b200 import transfer as tr
+    assert tr.present_ranks(2, 1, 2) == (0, 0)   # c2 needs 3 GPUs
+    assert tr.present_ranks(2, 1, 3) == (2, 1)   # c2 full
+    assert tr.present_ranks(4, 2, 4) == (2, 1)   # c3' (fan-in 2) + 1 idle GPU
+    assert tr.present_ranks(4, 2, 6) == (4, 2)   # c3 full
+    assert tr.present_ranks(4, 4, 2) == (1, 1)   # c4 one pair
+    assert tr.present_ranks(4, 4, 8) == (4, 4)   # c4 full
+    assert tr.present_ranks(2, 4, 3) == (1, 2)   # split: one P rank feeds two D ranks
+    for tp_p, tp_d in [(2, 1), (4, 2), (4, 4), (2, 4), (1, 8)]:
+        for n in range(2, 10):
+            n_p, n_d = tr.present_ranks(tp_p, tp_d, n)
+            assert n_p + n_d <= n
+            if n_d:
+                heads_needed = {p for p, q, _, _ in tr.pair_plan(tp_p, tp_d, 8) if q < n_d}
+                assert heads_needed <= set(range(n_p))
+    r = tr.roles(4, 2, 1, allow_idle=True)
+    assert [x.kind for x in r] == ["P", "P", "D", "X"]
