@@ -11,7 +11,9 @@ N >= 2 (torchrun, one process per GPU): BASELINE configs[3] (c4: Llama-3-70B GQA
   32 x 4096 tokens, P TP=4 -> D TP=4, bf16 -> fp8-e4m3 per-head scale) as N/2 independent
   (P rank p -> D rank p) pairs on disjoint GPUs (P = ranks 0..N/2-1): N=8 is the full c4,
   N=2/4 its per-GPU-equivalent sub-configs; per-pair work fixed -> weak
-  scaling.  Default mode "push": the fused gather+convert kernel stores into the D rank's
+  scaling.  `--workload c3|c2` runs the largest complete sub-transfer that fits (c3 at N=4:
+  P0,P1 -> D0, fan-in 2; N=6 the full c3); `--workload c5` the mixed-length stream.
+  Default mode "push": the fused gather+convert kernel stores into the D rank's
   IPC-mapped pool over NVLink, then a release flag (K4/K5); "nccl": pack -> ncclSend /
   ncclRecv -> unpack, per-layer pipelined.
 

@@ -158,6 +158,17 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
                              void* const* dst_pools, const kv_batch* dst_bt, int32_t layer_begin,
                              int32_t layer_end, kv_stream stream);
 
+/* One P rank's share of a distributed transfer: like kv_convert_reshard with n_src = 1,
+ * but only the heads of each listed D rank that P rank `src` holds are written (their tail
+ * slots included); the D ranks' other heads are left to the P ranks that hold them (fan-in,
+ * P:125 "combine the TP1 and TP2 of P instance").  Every listed D rank must share heads with
+ * src (KV_ESHAPE otherwise) and the overlaps must have equal size (always true when one
+ * degree divides the other; KV_EUNSUPPORTED otherwise -- call once per D rank).  This is the
+ * call each P rank makes in the fused NVLink push. */
+kv_status kv_convert_share(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, int32_t n_dst,
+                           const kv_layout* const* dst, void* const* dst_pools, const kv_batch* dst_bt,
+                           int32_t layer_begin, int32_t layer_end, kv_stream stream);
+
 /* ---- NEXT-1: dynamic fp8 scales --------------------------------------------------- */
 
 /* Per-batch dequant scales for the heads of D rank `dst` (precision alignment):

@@ -67,6 +67,7 @@ def _load():
         "kv_plan_pairs": (i32, [i32, i32, i32, C.POINTER(i32), i32]),
         "kv_convert_reshard": (st, [i32, pp, pp, C.POINTER(Batch_t), i32, pp, pp, C.POINTER(Batch_t), i32, i32, p]),
         "kv_compute_scales": (st, [i32, pp, pp, C.POINTER(Batch_t), p, p, i32, i32, p]),
+        "kv_convert_share": (st, [p, p, C.POINTER(Batch_t), i32, pp, pp, C.POINTER(Batch_t), i32, i32, p]),
         "kv_wire_dtype": (i32, [p, p]),
         "kv_wire_header_bytes": (C.c_size_t, [i32]),
         "kv_wire_header_write": (st, [p, p, i32, p, i32, i32, p, C.c_size_t]),
@@ -107,7 +108,7 @@ lib = _load()
 
 # Every symbol include/kvx.h declares (checked by tests/test_abi.py).
 EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_block_table_update", "kv_plan_pairs",
-           "kv_convert_reshard", "kv_compute_scales", "kv_wire_dtype", "kv_wire_header_bytes",
+           "kv_convert_reshard", "kv_convert_share", "kv_compute_scales", "kv_wire_dtype", "kv_wire_header_bytes",
            "kv_wire_header_write", "kv_wire_header_parse", "kv_wire_header_check", "kv_copy_bytes", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
            "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
            "kv_recv_unpack", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",

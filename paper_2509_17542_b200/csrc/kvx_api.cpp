@@ -287,10 +287,14 @@ int32_t kv_plan_pairs(int32_t tp_p, int32_t tp_d, int32_t H, int32_t* out, int32
   return n;
 }
 
-kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
-                             const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst,
-                             void* const* dst_pools, const kv_batch* dst_bt, int32_t lb, int32_t le,
-                             kv_stream stream) {
+}  // extern "C"
+
+namespace {
+// share == false: kv_convert_reshard (every P rank a listed D rank needs must be listed);
+// share == true: kv_convert_share (one P rank converts only the D heads it holds).
+kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                       const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst, void* const* dst_pools,
+                       const kv_batch* dst_bt, int32_t lb, int32_t le, kv_stream stream, bool share) {
   if (n_src < 1 || n_src > KVX_MAX_RANKS || n_dst < 1 || n_dst > KVX_MAX_RANKS)
     return fail(KV_EINVAL, "kv_convert_reshard: need 1..16 source and destination ranks");
   if (!src || !src_pools || !dst || !dst_pools) return fail(KV_EINVAL, "kv_convert_reshard: null array");
@@ -328,15 +332,30 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
   const int32_t H = S->d.num_kv_heads;
   const int32_t Hp = S->h_local, Hd = D->h_local;
   bool seen_q[KVX_MAX_RANKS] = {false};
+  a.Hd_eff = share ? -1 : Hd;
   for (int i = 0; i < n_dst; ++i) {
     const int q = dst[i]->d.tp_rank;
     if (q >= KVX_MAX_RANKS || seen_q[q]) return fail(KV_EINVAL, "kv_convert_reshard: destination rank listed twice");
     seen_q[q] = true;
     if ((st = scales_ok(S, dst[i])) != KV_OK) return st;
-    for (int32_t h = q * Hd; h < (q + 1) * Hd; ++h)
-      if (a.src_of_p[h / Hp] < 0)
-        return fail(KV_ESHAPE, "kv_convert_reshard: missing source shard for P rank " + std::to_string(h / Hp) +
-                                   " (needed by D rank " + std::to_string(q) + ")");
+    if (share) {
+      // the D-local heads of q that P rank p holds: one contiguous range (head-contiguous TP)
+      const int32_t p = S->d.tp_rank;
+      const int32_t hb = std::max(p * Hp, q * Hd), he = std::min((p + 1) * Hp, (q + 1) * Hd);
+      if (he <= hb)
+        return fail(KV_ESHAPE, "kv_convert_share: P rank " + std::to_string(p) + " holds no head of D rank " +
+                                   std::to_string(q));
+      if (a.Hd_eff >= 0 && a.Hd_eff != he - hb)
+        return fail(KV_EUNSUPPORTED, "kv_convert_share: unequal head overlaps across the listed D ranks; "
+                                     "call once per D rank");
+      a.Hd_eff = he - hb;
+      a.hq_off[i] = (int8_t)(hb - q * Hd);
+    } else {
+      for (int32_t h = q * Hd; h < (q + 1) * Hd; ++h)
+        if (a.src_of_p[h / Hp] < 0)
+          return fail(KV_ESHAPE, "kv_convert_reshard: missing source shard for P rank " + std::to_string(h / Hp) +
+                                     " (needed by D rank " + std::to_string(q) + ")");
+    }
     a.dst[i] = static_cast<uint8_t*>(dst_pools[i]);
     a.dst_rank[i] = (int8_t)q;
     a.dscale[i] = dst[i]->d.scales;
@@ -366,8 +385,8 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
   a.slot_inner = slot_inner_of(D);
   const uint32_t ndch = (uint32_t)(a.D / vec);
   a.f_dch = make_fastdiv(ndch);
-  a.f_in0 = make_fastdiv(a.slot_inner ? a.Bd : Hd);
-  a.f_in1 = make_fastdiv(a.slot_inner ? Hd : a.Bd);
+  a.f_in0 = make_fastdiv(a.slot_inner ? a.Bd : a.Hd_eff);
+  a.f_in1 = make_fastdiv(a.slot_inner ? a.Hd_eff : a.Bd);
   a.f_hp = make_fastdiv(Hp);
   a.f_bp = make_fastdiv(a.Bp);
   a.f_bd = make_fastdiv(a.Bd);
@@ -375,7 +394,7 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
   a.f_cpr = make_fastdiv(ndch);
   if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
   // per-layer chunk count; split the layer range so each launch stays under 2^31 chunks
-  const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * 2 * Hd * a.Bd * ndch;
+  const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * 2 * a.Hd_eff * a.Bd * ndch;
   int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / std::max<uint64_t>(per_layer, 1));
   if (per_layer > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_convert_reshard: one layer exceeds 2^31 chunks");
   for (int32_t l0 = lb; l0 < le; l0 += step) {
@@ -388,6 +407,24 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
     if (e != cudaSuccess) return cuda_fail(e, "kv_convert_reshard: launch");
   }
   return KV_OK;
+}
+}  // namespace
+
+extern "C" {
+
+kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                             const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst,
+                             void* const* dst_pools, const kv_batch* dst_bt, int32_t lb, int32_t le,
+                             kv_stream stream) {
+  return convert_impl(n_src, src, src_pools, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, false);
+}
+
+kv_status kv_convert_share(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, int32_t n_dst,
+                           const kv_layout* const* dst, void* const* dst_pools, const kv_batch* dst_bt, int32_t lb,
+                           int32_t le, kv_stream stream) {
+  const kv_layout* s1[1] = {src};
+  const void* p1[1] = {src_pool};
+  return convert_impl(1, s1, p1, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, true);
 }
 
 kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,

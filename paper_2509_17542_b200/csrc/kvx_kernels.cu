@@ -233,7 +233,7 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
         const uint32_t bl = divmod(n, a.f_bl);
         const uint32_t qi = n;
         const uint32_t slot = a.slot_inner ? in0 : in1;
-        const uint32_t hq = a.slot_inner ? in1 : in0;
+        const uint32_t hq = (uint32_t)a.hq_off[qi] + (a.slot_inner ? in1 : in0);
         const int32_t r = __ldg(a.d_blk_req + bl);
         const int32_t tok0 = __ldg(a.tok_off + r);
         const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
@@ -355,12 +355,13 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
   const uint32_t ls = a.slot_inner ? (lane & ((1u << ts_log2) - 1u)) : (lane >> (5u - ts_log2));
   const uint32_t lh = a.slot_inner ? (lane >> ts_log2) : (lane & ((1u << (5u - ts_log2)) - 1u));
   const uint32_t slot = (s_blk << ts_log2) + ls;
-  const uint32_t hq = (sbk << (5u - ts_log2)) + lh;
+  const uint32_t hl = (sbk << (5u - ts_log2)) + lh;  // head within the converted range
+  const uint32_t hq = (uint32_t)a.hq_off[qi] + hl;      // D-local head
   sp = 0;
   dp = 0;
   rsc = 1.f;  // e4m3 destination: RN(1/s); e4m3 source: s
   rz = 2;
-  if (slot < (uint32_t)a.Bd && hq < (uint32_t)a.Hd) {
+  if (slot < (uint32_t)a.Bd && hl < (uint32_t)a.Hd_eff) {
     rz = 0;
     const int64_t dblk = __ldg(a.d_blk_ids + bl);
     dp = (uint64_t)(a.dst[qi] + (dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
@@ -931,13 +932,13 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
     // row-tiled fast path: work items of 32 rows (one per lane) = 2-D sub-tiles
     ConvArgs a = a0;
     const uint32_t cpr = a.f_cpr.d;
-    a.rows_per_tile = a.Bd * a.Hd;
+    a.rows_per_tile = a.Bd * a.Hd_eff;
     a.rows_per_item = 32;
     a.cpr_shift = log2_pow2(cpr);
     uint32_t ts, th;
-    subtile_shape((uint32_t)a.Bd, (uint32_t)a.Hd, &ts, &th);
+    subtile_shape((uint32_t)a.Bd, (uint32_t)a.Hd_eff, &ts, &th);
     a.ts_log2 = log2_pow2(ts);
-    const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.Hd + th - 1) / th;
+    const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.Hd_eff + th - 1) / th;
     a.f_sb = make_fastdiv(nsb);
     a.f_items = make_fastdiv(nsb * nhb);
     a.n_items = (uint32_t)((uint64_t)a.total / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);

@@ -12,7 +12,7 @@ from contextlib import contextmanager
 from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BYTES, KV_BF16, KV_F8E4M3, KV_F16,
                    KV_F32, Batch_t, KvError, LayoutDesc, check, lib)
 
-__all__ = ["Layout", "Batch", "convert_reshard", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
+__all__ = ["Layout", "Batch", "convert_reshard", "convert_share", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
            "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "launch_count", "launch_count_reset", "set_sm_budget",
            "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "DTYPE_BYTES",
            "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
@@ -143,6 +143,17 @@ def convert_reshard(src_layouts, src_pools, src_batch: Batch, dst_layouts, dst_p
     lb, le = layer_range if layer_range else _common(src_layouts[0], dst_layouts[0])
     check(lib.kv_convert_reshard(ns, S, SP, C.byref(src_batch.bt), nd, Dl, DP, C.byref(dst_batch.bt), lb, le,
                                  _stream(stream)))
+
+
+def convert_share(src_layout, src_pool, src_batch: Batch, dst_layouts, dst_pools, dst_batch: Batch,
+                  layer_range=None, stream=None):
+    """kv_convert_share: one P rank's share -- only the D heads it holds (distributed push)."""
+    nd = len(dst_layouts)
+    Dl = (C.c_void_p * nd)(*[l.handle.value for l in dst_layouts])
+    DP = (C.c_void_p * nd)(*[_ptr(p) for p in dst_pools])
+    lb, le = layer_range if layer_range else _common(src_layout, dst_layouts[0])
+    check(lib.kv_convert_share(src_layout.handle, _ptr(src_pool), C.byref(src_batch.bt), nd, Dl, DP,
+                               C.byref(dst_batch.bt), lb, le, _stream(stream)))
 
 
 def compute_scales(src_layouts, src_pools, src_batch: Batch, dst_layout: Layout, out, layer_range=None, stream=None):

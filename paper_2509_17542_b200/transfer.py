@@ -108,8 +108,8 @@ def push_step(src_layout, src_pool, src_batch, dst_layouts, peer_pools, dst_batc
     chunk = layer_chunk or (L1 - L0)
     qs = sorted(dst_layouts)
     for l0 in range(L0, L1, chunk):
-        kv.convert_reshard([src_layout], [src_pool], src_batch, [dst_layouts[q] for q in qs],
-                           [peer_pools[q] for q in qs], dst_batch, (l0, min(L1, l0 + chunk)), stream)
+        kv.convert_share(src_layout, src_pool, src_batch, [dst_layouts[q] for q in qs],
+                         [peer_pools[q] for q in qs], dst_batch, (l0, min(L1, l0 + chunk)), stream)
     for q in qs:
         kv.signal(peer_flags[q] + 4 * flag_slot, epoch, stream)
 

@@ -249,6 +249,28 @@ def test_pipeline_stage_reshard(o1, tp_p, tp_d, sdt, ddt):
                             dc.dst_pools[:tp_d], dc.dst_bt, (1, 3))
 
 
+@pytest.mark.parametrize("tp_p,tp_d,ddt", [(4, 2, BF16), (2, 4, E4M3), (4, 4, E4M3), (2, 1, F16), (1, 2, F16)])
+def test_convert_share_per_p_rank(o1, tp_p, tp_d, ddt):
+    """Distributed push primitive: each P rank converts only its own heads into every D rank
+    it shares heads with (fan-in and fan-out); all shares together == the whole transfer."""
+    from tests.gpu_util import DevCase
+    import paper_2509_17542_b200 as kvx
+    case = make_case(3, 8, 64, tp_p, tp_d, 16, 32, [45, 16, 3], F16 if ddt == F16 else BF16, ddt,
+                     seed=30 + tp_p * 5 + tp_d, o1=o1, scales="pow2")
+    dc = DevCase(case)
+    pairs = kvx.plan_pairs(tp_p, tp_d, 8)
+    for p in range(tp_p):
+        qs = sorted(q for pp, q, _, _ in pairs if pp == p)
+        kvx.convert_share(dc.src_lays[p], dc.src_pools[p], dc.src_bt, [dc.dst_lays[q] for q in qs],
+                          [dc.dst_pools[q] for q in qs], dc.dst_bt)
+    torch.cuda.synchronize()
+    assert_pools_match(dc.dst_numpy(), expected(case, o1), ddt)
+    if tp_p > tp_d:  # a D rank that P rank 0 does not feed is refused
+        with pytest.raises(kvx.KvError, match="holds no head"):
+            kvx.convert_share(dc.src_lays[0], dc.src_pools[0], dc.src_bt, [dc.dst_lays[tp_d - 1]],
+                              [dc.dst_pools[tp_d - 1]], dc.dst_bt)
+
+
 def test_replay_from_file_and_hidden_state(o1, tmp_path):
     """NEXT-2: every (p, q) share packed, saved as header + payload, loaded back, header-checked
     and unpacked == the oracle; a mismatching receiver is refused.  Plus the opaque hidden
