@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--mode", default="push", choices=["push", "nccl"])
     ap.add_argument("--layer-chunk", type=int, default=0, help="layers per chunk (0 = whole model)")
     ap.add_argument("--chunk-mib", type=int, default=64, help="c5: merge layers until a chunk moves this much")
+    ap.add_argument("--c5-batch", action="store_true", help="c5: push each instance's requests as one batch")
     ap.add_argument("--workload", default=None, help="override: c1..c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -711,11 +712,26 @@ def run_stream(args):
         src_bytes = sum(cfg.L * per_tok_layer * t for t in icfg.n_tokens)
         count = [0]
 
+        if args.c5_batch:  # the whole instance batch in one launch per layer chunk (no per-request handoff)
+            sbt_all = kvx.Batch(sl, icfg.n_tokens, src_tables, dev)
+            dbt_all = kvx.Batch(dls[0], [cfg.n_tokens[r] for r in reqs], [dst_tables[r] for r in reqs], dev)
+
         def step(evs=None):
+            if args.c5_batch:
+                lc = args.layer_chunk or cfg.L
+                for l0 in range(0, cfg.L, lc):
+                    kvx.convert_share(sl, spool, sbt_all, dls, ppools, dbt_all, (l0, min(cfg.L, l0 + lc)), stream)
+                count[0] += len(reqs)
+                for f in pflags:
+                    kvx.signal(f, count[0], stream)
+                if evs is not None:
+                    for e in evs:
+                        e.record(stream)
+                return
             for i in range(len(reqs)):
                 lc = args.layer_chunk or chunks[i]
                 for l0 in range(0, cfg.L, lc):
-                    kvx.convert_reshard([sl], [spool], sbt[i], dls, ppools, dbt[i], (l0, min(cfg.L, l0 + lc)), stream)
+                    kvx.convert_share(sl, spool, sbt[i], dls, ppools, dbt[i], (l0, min(cfg.L, l0 + lc)), stream)
                 count[0] += 1
                 for f in pflags:
                     kvx.signal(f, count[0], stream)
@@ -782,7 +798,8 @@ def run_stream(args):
                "config": {"workload": f"c5 stream: {cfg.note}; {n_inst} P instance(s) x {per_inst} rank(s) -> "
                                       f"D ranks {d_ranks}" + (" (full c5)" if world == 8 else " (c5' sub-config)"),
                           "requests": nreq, "src_bytes_per_step": tot_b,
-                          "mode": f"push per request, layer chunks >= {args.chunk_mib} MiB",
+                          "mode": "push, whole instance batch per launch" if args.c5_batch else
+                          f"push per request, layer chunks >= {args.chunk_mib} MiB",
                           "l2": "inputs larger than L2 (no flush)"},
                "latency_ms": {"p50": round(alll[len(alll) // 2], 3) if alll else None,
                               "p99": round(alll[min(len(alll) - 1, int(0.99 * len(alll)))], 3) if alll else None,
