@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xcompiler", "-fPIC,-O3,-Wall", "-shared", "--expt-relaxed-constexpr",
            "-I", INCLUDE, "-I", CSRC, "-I", nccl_inc,
            "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + nccl_lib,
-           "-o", LIB + ".tmp"] + sources()
+           "-o", LIB + ".tmp"] + os.environ.get("KVX_NVCC_FLAGS", "").split() + sources()
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

@@ -196,6 +196,9 @@ __device__ __forceinline__ uint32_t divmod(uint32_t& n, const FastDiv& f) {
 }
 
 constexpr int kThreads = 256;
+#ifndef KVX_MINB
+#define KVX_MINB 1  // min CTAs/SM for the row kernel (register cap); tuning knob
+#endif
 
 // ------------------------------------------------------------------------------------
 // K1/K4: fused pool -> pool convert (+ reshard, + cast, + tail zero-fill)
@@ -387,7 +390,7 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
 }
 
 template <int SDT, int DDT, int U, int VEC = 8>
-__global__ void __launch_bounds__(kThreads) k_convert_rows(const __grid_constant__ ConvArgs a) {
+__global__ void __launch_bounds__(kThreads, KVX_MINB) k_convert_rows(const __grid_constant__ ConvArgs a) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
