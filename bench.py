@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--layer-chunk", type=int, default=0, help="layers per chunk (0 = whole model)")
     ap.add_argument("--chunk-mib", type=int, default=64, help="c5: merge layers until a chunk moves this much")
     ap.add_argument("--c5-batch", action="store_true", help="c5: push each instance's requests as one batch")
+    ap.add_argument("--requests", type=int, default=0,
+                    help="use only the first N requests of the workload (e.g. 1: batch-1 latency of c3/c4)")
     ap.add_argument("--workload", default=None, help="override: c1..c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -266,7 +268,7 @@ def run_single(args):
     torch.cuda.set_device(0)
     cfgs = synth.configs()
     wl_name = args.workload or "c2"
-    cfg = cfgs[wl_name]
+    cfg = _subset(cfgs[wl_name], args)
     dev = torch.device("cuda", 0)
     w = Workload(cfg, range(cfg.tp_p), range(cfg.tp_d), dev)
     S = [w.src_lays[p] for p in w.p_ranks]
@@ -366,6 +368,14 @@ def e2e_single(w, S, Dl, K, stream, src_b):
             "steps": K}
 
 
+def _subset(cfg, args):
+    """--requests N: the first N requests of the configuration (batch-1 latency runs)."""
+    if getattr(args, "requests", 0):
+        import dataclasses
+        return dataclasses.replace(cfg, n_tokens=cfg.n_tokens[:args.requests])
+    return cfg
+
+
 def _dtype_name(cfg):
     a, b = synth.DTYPE_NAMES[cfg.src_dtype], synth.DTYPE_NAMES[cfg.dst_dtype]
     return a if a == b else f"{a}->{b}"
@@ -399,7 +409,7 @@ def run_multi(args):
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     wl_name = args.workload or "c4"
-    cfg = synth.configs()[wl_name]
+    cfg = _subset(synth.configs()[wl_name], args)
     n_p, n_d = tr.present_ranks(cfg.tp_p, cfg.tp_d, world)
     if n_p < 1 or n_d < 1:
         raise SystemExit(f"{wl_name} needs at least {1 + max(cfg.tp_p // cfg.tp_d, cfg.tp_d // cfg.tp_p, 1)} GPUs")

@@ -392,6 +392,7 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
   a.f_bd = make_fastdiv(a.Bd);
   a.f_bl = make_fastdiv((uint32_t)std::max<int64_t>(dst_bt->total_blocks, 1));
   a.f_cpr = make_fastdiv(ndch);
+  a.f_nd = make_fastdiv((uint32_t)n_dst);
   if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
   // per-layer chunk count; split the layer range so each launch stays under 2^31 chunks
   const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * 2 * a.Hd_eff * a.Bd * ndch;

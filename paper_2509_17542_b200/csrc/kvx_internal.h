@@ -45,6 +45,7 @@ struct ConvArgs {
   int8_t dst_rank[KVX_MAX_RANKS];      // index -> D tp_rank
   int8_t hq_off[KVX_MAX_RANKS];        // first D-local head converted for each destination
   int32_t Hd_eff;                      // D-local heads converted per destination (<= Hd)
+  FastDiv f_nd;                        // number of destinations (row kernel: fastest item index)
   int64_t ss[6], ds[6];                // element strides by axis
   int32_t Hp, Hd, D, Bp, Bd, lb, Lc;
   int32_t s_l0, d_l0;  // first global layer of the P / D pools (pipeline stages)

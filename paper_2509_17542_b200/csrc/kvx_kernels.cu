@@ -337,13 +337,17 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
 template <int SDT, int DDT>
 __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint32_t lane, uint64_t& sp,
                                          uint64_t& dp, float& rsc, uint32_t& rz) {
+  // destination fastest: with several D ranks (fan-out, e.g. a TP split pushed over
+  // NVLink) concurrent warps write every destination at once instead of one link after
+  // the other -- with the D rank outermost, all P ranks of a fan-in/fan-out hit the same
+  // D rank's ingress together and c5' ran at 0.56 of the link
   uint32_t n = item;
+  const uint32_t qi = divmod(n, a.f_nd);
   const uint32_t rg = divmod(n, a.f_items);
   const uint32_t c = n & 1u;
   n >>= 1;
   const uint32_t l = divmod(n, a.f_l);
-  const uint32_t bl = divmod(n, a.f_bl);
-  const uint32_t qi = n;
+  const uint32_t bl = n;
   const int32_t r = __ldg(a.d_blk_req + bl);
   const int32_t tok0 = __ldg(a.tok_off + r);
   const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
