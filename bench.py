@@ -242,8 +242,11 @@ def sample_parity(w: Workload, layers, req, p_ranks, d_ranks, dst_pool_of=None):
                       "sample": f"request {req}, layers [{layers[0]},{layers[1]}), P ranks {list(p_ranks)} -> D ranks {list(d_ranks)}"}
 
 
-def cpu_baseline(cfg, layers, p_ranks, d_ranks, req=0):
-    """Time the oracle O1 (as it stands, single thread) on a bounded sample of the workload."""
+def cpu_baseline(cfg, layers, p_ranks, d_ranks, req=0, threads=1):
+    """Time the oracle O1 (as it stands) on a bounded sample of the workload.  threads > 1
+    runs the same function on disjoint layer ranges in parallel (ctypes releases the GIL),
+    the split SURVEY 8(d) names; threads = 1 is the plain single-thread oracle."""
+    from concurrent.futures import ThreadPoolExecutor
     from oracle import o1
     from tests.kvcase import make_case
     case = make_case(layers, cfg.H, cfg.D, cfg.tp_p, cfg.tp_d, cfg.B_p, cfg.B_d, [cfg.n_tokens[req]], cfg.src_dtype,
@@ -252,8 +255,16 @@ def cpu_baseline(cfg, layers, p_ranks, d_ranks, req=0):
     src_p = [case["src_pools"][p] for p in p_ranks]
     dst_l = [case["dst_lays"][q] for q in d_ranks]
     dst_p = [case["dst_pools"][q] for q in d_ranks]
+    ranges = [(i * layers // threads, (i + 1) * layers // threads) for i in range(threads)]
+    ranges = [r for r in ranges if r[1] > r[0]]
+    o1.lib()
     t0 = time.perf_counter()
-    o1.convert(src_l, src_p, dst_l, dst_p, case["n_tokens"], case["src_tables"], case["dst_tables"])
+    if len(ranges) == 1:
+        o1.convert(src_l, src_p, dst_l, dst_p, case["n_tokens"], case["src_tables"], case["dst_tables"])
+    else:
+        with ThreadPoolExecutor(len(ranges)) as ex:
+            list(ex.map(lambda lr: o1.convert(src_l, src_p, dst_l, dst_p, case["n_tokens"], case["src_tables"],
+                                              case["dst_tables"], lr), ranges))
     dt = time.perf_counter() - t0
     nbytes = 2 * layers * (cfg.H // cfg.tp_p) * len(p_ranks) * cfg.D * cfg.n_tokens[req] * synth.NBYTES[cfg.src_dtype]
     return nbytes, dt
@@ -339,6 +350,13 @@ def run_single(args):
         out["cpu_baseline"] = {"value": round(nb / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                                "sample": f"O1 (plain C, 1 thread) on {wl_name} request 0, layers [0,{nl}) of {cfg.L}, "
                                          f"{nb} source bytes in {dt:.2f} s"}
+        ncores = len(os.sched_getaffinity(0))
+        nl_mt = min(cfg.L, max(nl, 2 * ncores))
+        nb2, dt2 = cpu_baseline(cfg, nl_mt, w.p_ranks, w.d_ranks, threads=ncores)
+        out["cpu_baseline_threads"] = {"value": round(nb2 / dt2 / 1e9, 4), "unit": "GB/s", "cores": ncores,
+                                       "kind": "oracle",
+                                       "sample": f"same O1 split by layer over {ncores} threads, layers [0,{nl_mt}), "
+                                                 f"{nb2} source bytes in {dt2:.2f} s"}
     print(json.dumps(out), flush=True)
 
 
