@@ -26,6 +26,14 @@
 
 #include "kvx_internal.h"
 
+// cache-policy knobs for the streaming loads/stores (experiments; default: none)
+#ifndef KVX_LD_HINT
+#define KVX_LD_HINT ""
+#endif
+#ifndef KVX_ST_HINT
+#define KVX_ST_HINT ""
+#endif
+
 namespace kvx {
 
 namespace {
@@ -59,17 +67,17 @@ __device__ __forceinline__ void load_chunk(Chunk<DT, VEC>& c, const uint8_t* p) 
   constexpr int N = Chunk<DT, VEC>::BYTES;
   if constexpr (N == 32) {
     uint4 a, b;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate" KVX_LD_HINT ".v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(p));
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate" KVX_LD_HINT ".v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(p + 16));
     c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w;
     c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;
   } else if constexpr (N == 16) {
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+    asm volatile("ld.global.nc.L1::no_allocate" KVX_LD_HINT ".v4.u32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3]) : "l"(p));
   } else if constexpr (N == 8) {
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(c.w[0]), "=r"(c.w[1]) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate" KVX_LD_HINT ".v2.u32 {%0,%1}, [%2];" : "=r"(c.w[0]), "=r"(c.w[1]) : "l"(p));
   } else if constexpr (N == 4) {
     c.w[0] = *reinterpret_cast<const uint32_t*>(p);
   } else if constexpr (N == 2) {
@@ -83,15 +91,15 @@ template <int DT, int VEC>
 __device__ __forceinline__ void store_chunk(uint8_t* p, const Chunk<DT, VEC>& c) {
   constexpr int N = Chunk<DT, VEC>::BYTES;
   if constexpr (N == 32) {
-    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(c.w[0]), "r"(c.w[1]), "r"(c.w[2]),
+    asm volatile("st.global" KVX_ST_HINT ".v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(c.w[0]), "r"(c.w[1]), "r"(c.w[2]),
                  "r"(c.w[3]) : "memory");
-    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p + 16), "r"(c.w[4]), "r"(c.w[5]), "r"(c.w[6]),
+    asm volatile("st.global" KVX_ST_HINT ".v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p + 16), "r"(c.w[4]), "r"(c.w[5]), "r"(c.w[6]),
                  "r"(c.w[7]) : "memory");
   } else if constexpr (N == 16) {
-    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(c.w[0]), "r"(c.w[1]), "r"(c.w[2]),
+    asm volatile("st.global" KVX_ST_HINT ".v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(c.w[0]), "r"(c.w[1]), "r"(c.w[2]),
                  "r"(c.w[3]) : "memory");
   } else if constexpr (N == 8) {
-    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(c.w[0]), "r"(c.w[1]) : "memory");
+    asm volatile("st.global" KVX_ST_HINT ".v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(c.w[0]), "r"(c.w[1]) : "memory");
   } else if constexpr (N == 4) {
     *reinterpret_cast<uint32_t*>(p) = c.w[0];
   } else if constexpr (N == 2) {
