@@ -265,6 +265,32 @@ kv_status kv_recv_unpack(kv_comm* comm, int32_t peer, void* wire_scratch, size_t
                          const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt, int32_t layer_begin,
                          int32_t layer_end, kv_stream stream);
 
+/* A10 chunk schedulers (the host core runs the per-layer pipeline natively).
+ *
+ * kv_push: P side of the fused push.  For layer chunks [l, l+layer_chunk) of [layer_begin,
+ * layer_end) (layer_chunk <= 0: one chunk) enqueue kv_convert_share(src -> every listed D
+ * rank) on `stream`, then kv_signal(peer_flags[i], epoch) for each D rank.  peer_flags[i]
+ * is the (peer-mapped) flag word this P rank owns in D rank i's flag array.
+ *
+ * kv_send_pipelined / kv_recv_pipelined: the NCCL mode with per-layer double buffering --
+ * pack chunk k+1 on pack_stream while chunk k is on the wire (send_stream); on D, receive
+ * chunk k+1 while chunk k is unpacked.  wires[2*i + b] (b = 0, 1) are DEVICE buffers of
+ * wire_cap bytes for peer i (>= the largest chunk's kv_wire_bytes).  peer_ranks[i] is the
+ * communicator rank of peer i.  The calls return after enqueueing; the caller's `stream`
+ * is made to wait for all of the work (events created and destroyed inside). */
+kv_status kv_push(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, int32_t n_dst,
+                  const kv_layout* const* dst, void* const* dst_pools, const kv_batch* dst_bt,
+                  uint32_t* const* peer_flags, uint32_t epoch, int32_t layer_begin, int32_t layer_end,
+                  int32_t layer_chunk, kv_stream stream);
+kv_status kv_send_pipelined(kv_comm* comm, const kv_layout* src, const void* src_pool, const kv_batch* src_bt,
+                            int32_t n_dst, const kv_layout* const* dst, const int32_t* peer_ranks,
+                            void* const* wires, size_t wire_cap, int32_t layer_begin, int32_t layer_end,
+                            int32_t layer_chunk, kv_stream stream, kv_stream pack_stream, kv_stream send_stream);
+kv_status kv_recv_pipelined(kv_comm* comm, int32_t n_src, const kv_layout* const* src, const int32_t* peer_ranks,
+                            const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt, void* const* wires,
+                            size_t wire_cap, int32_t layer_begin, int32_t layer_end, int32_t layer_chunk,
+                            kv_stream stream, kv_stream recv_stream, kv_stream unpack_stream);
+
 /* CUDA IPC for the direct-store (push) mode.  kv_ipc_export writes the 64-byte handle of
  * the allocation containing dev_ptr and dev_ptr's offset inside it; kv_ipc_open maps it in
  * this process (the current device must have peer access to the owner) and returns the

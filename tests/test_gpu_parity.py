@@ -205,6 +205,46 @@ def test_pack_unpack_widening_on_receiver(o1):
     assert_pools_match(dc.dst_numpy(), expected(case, o1), BF16)
 
 
+@pytest.mark.parametrize("vec_path", [True, False])
+def test_redzones_untouched(o1, vec_path):
+    """compute-sanitizer is closed on this pool, so out-of-bounds writes are caught with
+    red zones: every pool (and the wire) sits inside a larger canary-filled buffer and the
+    bytes around it must survive a convert, a pack and an unpack."""
+    import paper_2509_17542_b200 as kvx
+    RZ = 4096
+    order_p = synth.P_ORDER if vec_path else (LAYER, KV, BLOCK, DIM, SLOT, HEAD)
+    case = make_case(3, 8, 32, 2, 4, 8, 16, [21, 9], BF16, E4M3, order_p, synth.D_ORDER, seed=17, o1=o1,
+                     scales="pow2")
+
+    def embed(arr):
+        raw = np.ascontiguousarray(arr).view(np.uint8)
+        big = torch.full((raw.size + 2 * RZ,), 0x5A, dtype=torch.uint8, device="cuda")
+        big[RZ:RZ + raw.size] = torch.from_numpy(raw.copy()).cuda()
+        return big, big[RZ:RZ + raw.size]
+
+    def intact(big, n):
+        return bool((big[:RZ] == 0x5A).all()) and bool((big[RZ + n:] == 0x5A).all())
+
+    src = [embed(p) for p in case["src_pools"]]
+    dst = [embed(p) for p in case["dst_pools"]]
+    S = [kvx.Layout.from_dict(l) for l in case["src_lays"]]
+    Dl = [kvx.Layout.from_dict(l, torch.from_numpy(np.asarray(l["scales"], np.float32)).cuda()) for l in case["dst_lays"]]
+    sbt = kvx.Batch(S[0], case["n_tokens"], case["src_tables"])
+    dbt = kvx.Batch(Dl[0], case["n_tokens"], case["dst_tables"])
+    kvx.convert_reshard(S, [v for _, v in src], sbt, Dl, [v for _, v in dst], dbt)
+    nb = kvx.wire_bytes(S[0], Dl[0], sbt.total_tokens)
+    wbig = torch.full((nb + 2 * RZ,), 0x5A, dtype=torch.uint8, device="cuda")
+    kvx.pack(S[0], src[0][1], sbt, Dl[0], wbig[RZ:RZ + nb])
+    kvx.unpack(S[0], Dl[0], dst[0][1], dbt, wbig[RZ:RZ + nb])
+    torch.cuda.synchronize()
+    for big, view in src + dst:
+        assert intact(big, view.numel())
+    assert intact(wbig, nb)
+    got = [v.cpu().numpy().view(np.uint8) for _, v in dst]
+    want = expected(case, o1)
+    assert_pools_match([g for g in got], [w.view(np.uint8) for w in want], E4M3)
+
+
 def test_launch_count_and_errors():
     import paper_2509_17542_b200 as kvx
     kvx.launch_count_reset()
