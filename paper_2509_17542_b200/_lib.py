@@ -85,6 +85,12 @@ def _load():
         "kv_send": (st, [p, i32, p, C.c_size_t, p]),
         "kv_recv": (st, [p, i32, p, C.c_size_t, p]),
         "kv_recv_unpack": (st, [p, i32, p, C.c_size_t, p, p, p, C.POINTER(Batch_t), i32, i32, p]),
+        "kv_push": (st, [p, p, C.POINTER(Batch_t), i32, pp, pp, C.POINTER(Batch_t), pp, C.c_uint32, i32, i32, i32,
+                         p]),
+        "kv_send_pipelined": (st, [p, p, p, C.POINTER(Batch_t), i32, pp, C.POINTER(i32), pp, C.c_size_t, i32, i32,
+                                   i32, p, p, p]),
+        "kv_recv_pipelined": (st, [p, i32, pp, C.POINTER(i32), p, p, C.POINTER(Batch_t), pp, C.c_size_t, i32, i32,
+                                   i32, p, p, p]),
         "kv_ipc_export": (st, [p, p, C.POINTER(u64)]),
         "kv_ipc_open": (st, [p, u64, C.POINTER(p)]),
         "kv_ipc_close": (st, [p]),
@@ -111,7 +117,7 @@ EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_bloc
            "kv_convert_reshard", "kv_convert_share", "kv_compute_scales", "kv_wire_dtype", "kv_wire_header_bytes",
            "kv_wire_header_write", "kv_wire_header_parse", "kv_wire_header_check", "kv_copy_bytes", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
            "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
-           "kv_recv_unpack", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",
+           "kv_recv_unpack", "kv_push", "kv_send_pipelined", "kv_recv_pipelined", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",
            "kv_launch_count", "kv_launch_count_reset", "kv_set_sm_budget", "kv_last_error", "kv_version")
 
 

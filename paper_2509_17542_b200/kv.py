@@ -156,6 +156,19 @@ def convert_share(src_layout, src_pool, src_batch: Batch, dst_layouts, dst_pools
                                C.byref(dst_batch.bt), lb, le, _stream(stream)))
 
 
+def push(src_layout, src_pool, src_batch: Batch, dst_layouts, dst_pools, dst_batch: Batch, peer_flags, epoch,
+         layer_range=None, layer_chunk=0, stream=None):
+    """kv_push: the P side of the fused NVLink push -- convert_share per layer chunk into
+    every (peer-mapped) D pool, then a release flag per D rank (A10/A11)."""
+    nd = len(dst_layouts)
+    Dl = (C.c_void_p * nd)(*[l.handle.value for l in dst_layouts])
+    DP = (C.c_void_p * nd)(*[_ptr(p) for p in dst_pools])
+    FL = (C.c_void_p * nd)(*[_ptr(f) for f in peer_flags])
+    lb, le = layer_range if layer_range else _common(src_layout, dst_layouts[0])
+    check(lib.kv_push(src_layout.handle, _ptr(src_pool), C.byref(src_batch.bt), nd, Dl, DP, C.byref(dst_batch.bt),
+                      FL, epoch, lb, le, layer_chunk, _stream(stream)))
+
+
 def compute_scales(src_layouts, src_pools, src_batch: Batch, dst_layout: Layout, out, layer_range=None, stream=None):
     """kv_compute_scales: per-batch fp8 dequant scales amax/448 for dst_layout's heads,
     written into `out` (device float32 [L][2][H_d])."""
@@ -223,6 +236,30 @@ class Comm:
         lb, le = layer_range if layer_range else _common(src, dst)
         check(lib.kv_recv_unpack(self._h, peer, _ptr(wire), nbytes, src.handle, dst.handle, _ptr(dst_pool),
                                  C.byref(dst_batch.bt), lb, le, _stream(stream)))
+
+    def send_pipelined(self, src: Layout, src_pool, src_batch: Batch, dst_layouts, peer_ranks, wires, wire_cap,
+                       layer_chunk, layer_range=None, stream=None, pack_stream=None, send_stream=None):
+        """kv_send_pipelined: pack chunk k+1 while chunk k is on the wire (wires: 2 per peer)."""
+        nd = len(dst_layouts)
+        Dl = (C.c_void_p * nd)(*[l.handle.value for l in dst_layouts])
+        PR = (C.c_int32 * nd)(*peer_ranks)
+        W = (C.c_void_p * (2 * nd))(*[_ptr(w) for w in wires])
+        lb, le = layer_range if layer_range else _common(src, dst_layouts[0])
+        check(lib.kv_send_pipelined(self._h, src.handle, _ptr(src_pool), C.byref(src_batch.bt), nd, Dl, PR, W,
+                                    wire_cap, lb, le, layer_chunk, _stream(stream), _stream(pack_stream),
+                                    _stream(send_stream)))
+
+    def recv_pipelined(self, src_layouts, peer_ranks, dst: Layout, dst_pool, dst_batch: Batch, wires, wire_cap,
+                       layer_chunk, layer_range=None, stream=None, recv_stream=None, unpack_stream=None):
+        """kv_recv_pipelined: receive chunk k+1 while chunk k is unpacked (wires: 2 per peer)."""
+        ns = len(src_layouts)
+        S = (C.c_void_p * ns)(*[l.handle.value for l in src_layouts])
+        PR = (C.c_int32 * ns)(*peer_ranks)
+        W = (C.c_void_p * (2 * ns))(*[_ptr(w) for w in wires])
+        lb, le = layer_range if layer_range else _common(src_layouts[0], dst)
+        check(lib.kv_recv_pipelined(self._h, ns, S, PR, dst.handle, _ptr(dst_pool), C.byref(dst_batch.bt), W,
+                                    wire_cap, lb, le, layer_chunk, _stream(stream), _stream(recv_stream),
+                                    _stream(unpack_stream)))
 
     @staticmethod
     @contextmanager

@@ -100,68 +100,33 @@ class PushChannel:
 
 def push_step(src_layout, src_pool, src_batch, dst_layouts, peer_pools, dst_batch, peer_flags, epoch,
               layer_chunk=None, stream=None, flag_slot=0):
-    """P side of one push transfer: ONE fused gather/convert/NVLink-store launch per layer
-    chunk covering every paired D rank (A10), then a release flag per D rank (A11).  With
-    fan-in (several P ranks feeding one D rank) each P rank writes its own flag word
-    ``flag_slot`` of the D rank's flag array."""
-    L0, L1 = src_layout.layers
-    chunk = layer_chunk or (L1 - L0)
+    """P side of one push transfer (native kv_push): one fused gather/convert/NVLink-store
+    launch per layer chunk covering every paired D rank (A10), then a release flag per D
+    rank (A11).  With fan-in (several P ranks feeding one D rank) each P rank writes its own
+    flag word ``flag_slot`` of the D rank's flag array."""
     qs = sorted(dst_layouts)
-    for l0 in range(L0, L1, chunk):
-        kv.convert_share(src_layout, src_pool, src_batch, [dst_layouts[q] for q in qs],
-                         [peer_pools[q] for q in qs], dst_batch, (l0, min(L1, l0 + chunk)), stream)
-    for q in qs:
-        kv.signal(peer_flags[q] + 4 * flag_slot, epoch, stream)
+    kv.push(src_layout, src_pool, src_batch, [dst_layouts[q] for q in qs], [peer_pools[q] for q in qs], dst_batch,
+            [peer_flags[q] + 4 * flag_slot for q in qs], epoch, None, layer_chunk or 0, stream)
 
 
 def nccl_send_step(comm, src_layout, src_pool, src_batch, dst_layouts, dst_world, wires, layer_chunk, pack_stream,
-                   send_stream, events):
-    """P side of the NCCL mode: pack layer chunk k on pack_stream, send it on send_stream
-    after the pack's event; double-buffered wires[(q, k % 2)]."""
-    import torch
-    L = src_layout.num_layers
-    nchunks = (L + layer_chunk - 1) // layer_chunk
-    for k in range(nchunks):
-        lr = (k * layer_chunk, min(L, (k + 1) * layer_chunk))
-        buf = k % 2
-        for q, dl in dst_layouts.items():
-            w = wires[(q, buf)]
-            nb = kv.wire_bytes(src_layout, dl, src_batch.total_tokens, lr)
-            if k >= 2:
-                pack_stream.wait_event(events[("sent", q, buf)])
-            kv.pack(src_layout, src_pool, src_batch, dl, w, lr, pack_stream, wire_nbytes=nb)
-            ev = torch.cuda.Event()
-            ev.record(pack_stream)
-            send_stream.wait_event(ev)
-            comm.send(dst_world[q], w, nb, send_stream)
-            ev2 = torch.cuda.Event()
-            ev2.record(send_stream)
-            events[("sent", q, buf)] = ev2
+                   send_stream, events=None, stream=None):
+    """P side of the NCCL mode (native kv_send_pipelined): pack layer chunk k+1 on
+    pack_stream while chunk k is on the wire; wires[(q, b)] double buffers per peer."""
+    qs = sorted(dst_layouts)
+    cap = min(wires[(q, b)].numel() for q in qs for b in range(2))
+    comm.send_pipelined(src_layout, src_pool, src_batch, [dst_layouts[q] for q in qs], [dst_world[q] for q in qs],
+                        [wires[(q, b)] for q in qs for b in range(2)], cap, layer_chunk, None, stream, pack_stream,
+                        send_stream)
 
 
 def nccl_recv_step(comm, src_layouts, dst_layout, dst_pool, dst_batch, src_world, wires, layer_chunk, recv_stream,
-                   unpack_stream, events):
-    """D side of the NCCL mode: receive layer chunk k from every paired P rank (grouped,
-    so fan-in links run concurrently), then unpack it while chunk k+1 arrives."""
-    import torch
-    L = dst_layout.num_layers
-    nchunks = (L + layer_chunk - 1) // layer_chunk
-    for k in range(nchunks):
-        lr = (k * layer_chunk, min(L, (k + 1) * layer_chunk))
-        buf = k % 2
-        if k >= 2:
-            for p in src_layouts:
-                recv_stream.wait_event(events[("unpacked", p, buf)])
-        with kv.Comm.group():
-            for p, sl in src_layouts.items():
-                nb = kv.wire_bytes(sl, dst_layout, dst_batch.total_tokens, lr)
-                comm.recv(src_world[p], wires[(p, buf)], nb, recv_stream)
-        ev = torch.cuda.Event()
-        ev.record(recv_stream)
-        unpack_stream.wait_event(ev)
-        for p, sl in src_layouts.items():
-            nb = kv.wire_bytes(sl, dst_layout, dst_batch.total_tokens, lr)
-            kv.unpack(sl, dst_layout, dst_pool, dst_batch, wires[(p, buf)], lr, unpack_stream, wire_nbytes=nb)
-            ev2 = torch.cuda.Event()
-            ev2.record(unpack_stream)
-            events[("unpacked", p, buf)] = ev2
+                   unpack_stream, events=None, stream=None):
+    """D side of the NCCL mode (native kv_recv_pipelined): receive layer chunk k+1 from
+    every paired P rank (grouped, so fan-in links run concurrently) while chunk k is
+    unpacked."""
+    ps = sorted(src_layouts)
+    cap = min(wires[(p, b)].numel() for p in ps for b in range(2))
+    comm.recv_pipelined([src_layouts[p] for p in ps], [src_world[p] for p in ps], dst_layout, dst_pool, dst_batch,
+                        [wires[(p, b)] for p in ps for b in range(2)], cap, layer_chunk, None, stream, recv_stream,
+                        unpack_stream)
