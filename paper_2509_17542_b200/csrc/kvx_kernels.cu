@@ -205,7 +205,8 @@ __device__ __forceinline__ uint32_t divmod(uint32_t& n, const FastDiv& f) {
 
 constexpr int kThreads = 256;
 #ifndef KVX_MINB
-#define KVX_MINB 1  // min CTAs/SM for the row kernel (register cap); tuning knob
+#define KVX_MINB 4  // >= 4 CTAs/SM for the row kernel: caps it at 64 registers (the 2-byte -> e4m3
+                    // instantiation otherwise takes 76 and drops to 3 CTAs/SM, 0.87 instead of 0.95)
 #endif
 
 // ------------------------------------------------------------------------------------
@@ -937,7 +938,7 @@ void subtile_shape(uint32_t Bd, uint32_t H, uint32_t* ts_out, uint32_t* th_out) 
 // U chunks per thread per segment: keep ~64 B of loads in flight per thread.
 template <int SDT, int VEC>
 constexpr int unroll_for() {
-  return VEC == 1 ? 4 : (Tr<SDT>::B == 1 ? 8 : (Tr<SDT>::B == 2 ? 4 : 2));
+  return VEC == 1 ? 4 : (Tr<SDT>::B == 4 ? 2 : 4);
 }
 
 template <int VEC, int SDT, int DDT>

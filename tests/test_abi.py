@@ -193,3 +193,16 @@ def test_wire_header_layout_roundtrip_and_check(kvx):
         replay.parse(b"XXXX" + hdr[4:])
     with pytest.raises(kvx.KvError, match="share no heads"):
         replay.header(_lay(kvx, tp_degree=4, tp_rank=3), d, [1])
+
+
+def test_row_kernels_fit_four_ctas_per_sm():
+    """Occupancy guard (CPU, from the cubin): every row-kernel instantiation uses <= 64
+    registers and no local memory, so 4 CTAs of 256 threads fit an SM (the bf16 -> e4m3 one
+    took 76 registers once and lost 8% of bandwidth)."""
+    import subprocess
+    so = os.path.join(ROOT, "paper_2509_17542_b200", "libkvx.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-res-usage", so], capture_output=True, text=True).stdout
+    fns = re.findall(r"Function (\S*k_convert_rows\S*):\s*\n\s*REG:(\d+) STACK:(\d+) SHARED:\d+ LOCAL:(\d+)", out)
+    assert len(fns) >= 16
+    for name, reg, stack, local in fns:
+        assert int(reg) <= 64 and int(stack) == 0 and int(local) == 0, (name, reg, stack, local)
