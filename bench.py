@@ -365,8 +365,8 @@ def e2e_single(w, S, Dl, K, stream, src_b):
     pinned memory, the convert call, D2H of the destination pool, all inside the timed region."""
     import torch
     import paper_2509_17542_b200 as kvx
-    hs = [w.src_pools[p].cpu().pin_memory() for p in w.p_ranks]
-    hd = [torch.empty_like(w.dst_pools[q], device="cpu").pin_memory() for q in w.d_ranks]
+    hs = [_pinned_copy(w.src_pools[p]) for p in w.p_ranks]
+    hd = [torch.empty(w.dst_pools[q].numel(), dtype=torch.uint8, pin_memory=True) for q in w.d_ranks]
     DP = [w.dst_pools[q] for q in w.d_ranks]
     SP = [w.src_pools[p] for p in w.p_ranks]
     torch.cuda.synchronize()
@@ -384,6 +384,14 @@ def e2e_single(w, S, Dl, K, stream, src_b):
     return {"value": round(src_b / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 3),
             "h2d_bytes_per_step": int(sum(h.numel() for h in hs)), "d2h_bytes_per_step": int(sum(h.numel() for h in hd)),
             "steps": K}
+
+
+def _pinned_copy(dev_tensor):
+    """Pinned host copy of a device tensor without a pageable intermediate (GB-sized pools)."""
+    import torch
+    h = torch.empty(dev_tensor.numel(), dtype=dev_tensor.dtype, pin_memory=True)
+    h.copy_(dev_tensor.view(-1))
+    return h
 
 
 def _subset(cfg, args):
@@ -603,9 +611,9 @@ def e2e_multi(w, me, step, stream, barrier, err, ke, rank):
     import torch
     host = None
     if me.kind == "P":
-        host = w.src_pools[me.tp_rank].cpu().pin_memory()
+        host = _pinned_copy(w.src_pools[me.tp_rank])
     elif me.kind == "D":
-        host = torch.empty(w.dst_pools[me.tp_rank].numel(), dtype=torch.uint8).pin_memory()
+        host = torch.empty(w.dst_pools[me.tp_rank].numel(), dtype=torch.uint8, pin_memory=True)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
