@@ -290,6 +290,130 @@ int32_t kv_plan_pairs(int32_t tp_p, int32_t tp_d, int32_t H, int32_t* out, int32
 }  // extern "C"
 
 namespace {
+// ---- same-dtype TMA tile path (k_tile_copy) ---------------------------------------
+typedef CUresult (*encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+encode_tiled_fn encode_fn() {
+  static encode_tiled_fn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess && p)
+      fn = reinterpret_cast<encode_tiled_fn>(p);
+    else
+      cudaGetLastError();
+  }
+  return fn;
+}
+
+// KVX_TILE=0 disables the tile path (A/B experiments); default on.
+bool tile_enabled() {
+  static const int v = getenv("KVX_TILE") ? atoi(getenv("KVX_TILE")) : 1;
+  return v != 0;
+}
+
+// Same dtype, head_dim innermost on both sides, D's three innermost axes {HEAD, SLOT} x DIM,
+// B_d a multiple of B_p, head counts dividing each other: one TMA tensor load per source
+// sub-tile whose map enumerates the source in D's order, bulk stores of D's runs.  Sets
+// *used = false (and launches nothing) when the case does not fit.
+kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                        const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst, void* const* dst_pools,
+                        const kv_batch* dst_bt, int32_t lb, int32_t le, kv_stream stream, bool share, bool* used) {
+  *used = false;
+  if (!tile_enabled()) return KV_OK;
+  const kv_layout *S = src[0], *D = dst[0];
+  const int32_t* o = D->d.axis_order;
+  int head_major;
+  if (o[5] != KV_AX_DIM) return KV_OK;
+  if (o[3] == KV_AX_HEAD && o[4] == KV_AX_SLOT)
+    head_major = 1;
+  else if (o[3] == KV_AX_SLOT && o[4] == KV_AX_HEAD)
+    head_major = 0;
+  else
+    return KV_OK;
+  const int32_t Hp = S->h_local, Hd = D->h_local, Bp = S->d.block_size, Bd = D->d.block_size, Dm = S->d.head_dim;
+  const int32_t esize = S->elem_bytes;
+  const int32_t nh = std::min(Hp, Hd);
+  if (Bd % Bp != 0 || Bp > 256 || Dm > 256 || nh > 256 || (Hp % nh) || (Hd % nh)) return KV_OK;
+  const int64_t row_bytes = (int64_t)Dm * esize;
+  if (row_bytes % 16) return KV_OK;
+  const int64_t stage = (int64_t)nh * Bp * row_bytes;
+  if (stage > 100 * 1024) return KV_OK;
+  encode_tiled_fn enc = encode_fn();
+  if (!enc) return KV_OK;
+  TileArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int i = 0; i < KVX_MAX_RANKS; ++i) a.src_of_p[i] = -1;
+  const CUtensorMapDataType dt = esize == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                 : esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                              : CU_TENSOR_MAP_DATA_TYPE_UINT32;
+  for (int i = 0; i < n_src; ++i) {
+    const kv_layout* L = src[i];
+    a.src_of_p[L->d.tp_rank] = (int8_t)i;
+    const int64_t* st = L->stride;
+    cuuint64_t dims[5] = {(cuuint64_t)Dm, (cuuint64_t)(head_major ? Bp : Hp), (cuuint64_t)(head_major ? Hp : Bp),
+                          (cuuint64_t)L->d.num_blocks, (cuuint64_t)L->d.num_layers};
+    cuuint64_t strides[4] = {(cuuint64_t)((head_major ? st[KV_AX_SLOT] : st[KV_AX_HEAD]) * esize),
+                             (cuuint64_t)((head_major ? st[KV_AX_HEAD] : st[KV_AX_SLOT]) * esize),
+                             (cuuint64_t)(st[KV_AX_BLOCK] * esize), (cuuint64_t)(st[KV_AX_LAYER] * esize)};
+    cuuint32_t box[5] = {(cuuint32_t)Dm, (cuuint32_t)(head_major ? Bp : nh), (cuuint32_t)(head_major ? nh : Bp), 1, 1};
+    cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    for (int c = 0; c < 2; ++c) {
+      void* base = (uint8_t*)src_pools[i] + (size_t)c * (size_t)st[KV_AX_KV] * (size_t)esize;
+      if (enc(&a.maps[i][c], dt, 5, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+          CUDA_SUCCESS)
+        return KV_OK;  // this layout cannot be described by a tensor map: use the row kernel
+    }
+  }
+  for (int i = 0; i < n_dst; ++i) {
+    a.dst[i] = static_cast<uint8_t*>(dst_pools[i]);
+    a.dst_rank[i] = (int8_t)dst[i]->d.tp_rank;
+  }
+  for (int ax = 0; ax < 6; ++ax) a.ds[ax] = D->stride[ax];
+  a.Hp = Hp;
+  a.Hd = Hd;
+  a.Bp = Bp;
+  a.Bd = Bd;
+  a.D = Dm;
+  a.esize = esize;
+  a.nh = nh;
+  a.s_l0 = S->d.first_layer;
+  a.d_l0 = D->d.first_layer;
+  a.head_major = head_major;
+  a.share_p = share ? S->d.tp_rank : -1;
+  a.stage_bytes = (int32_t)stage;
+  a.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(8, (200 * 1024) / stage));
+  a.s_blk_off = src_bt->blk_off;
+  a.s_blk_ids = src_bt->blk_ids;
+  a.d_blk_off = dst_bt->blk_off;
+  a.d_blk_ids = dst_bt->blk_ids;
+  a.d_blk_req = dst_bt->blk_req;
+  a.tok_off = dst_bt->tok_off;
+  const uint32_t nparts = share ? 1u : (uint32_t)(Hd / nh), nsub = (uint32_t)(Bd / Bp);
+  a.f_nd = make_fastdiv((uint32_t)n_dst);
+  a.f_parts = make_fastdiv(nparts);
+  a.f_sub = make_fastdiv(nsub);
+  const uint64_t per_layer = (uint64_t)n_dst * nparts * nsub * 2 * (uint64_t)dst_bt->total_blocks;
+  if (per_layer > kMaxChunks) return KV_OK;
+  const int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / per_layer);
+  for (int32_t l0 = lb; l0 < le; l0 += step) {
+    const int32_t l1 = std::min(le, l0 + step);
+    a.lb = l0;
+    a.Lc = l1 - l0;
+    a.f_l = make_fastdiv((uint32_t)a.Lc);
+    a.n_items = (uint32_t)(per_layer * (uint64_t)a.Lc);
+    cudaError_t e = launch_tile_copy(a, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "kv_convert_reshard: tile launch");
+  }
+  *used = true;
+  return KV_OK;
+}
+
 // share == false: kv_convert_reshard (every P rank a listed D rank needs must be listed);
 // share == true: kv_convert_share (one P rank converts only the D heads it holds).
 kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
@@ -394,6 +518,13 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
   a.f_cpr = make_fastdiv(ndch);
   a.f_nd = make_fastdiv((uint32_t)n_dst);
   if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
+  if (fast && S->d.dtype == D->d.dtype) {
+    bool used = false;
+    if ((st = try_tile_copy(n_src, src, src_pools, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, share,
+                            &used)) != KV_OK)
+      return st;
+    if (used) return KV_OK;
+  }
   // per-layer chunk count; split the layer range so each launch stays under 2^31 chunks
   const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * 2 * a.Hd_eff * a.Bd * ndch;
   int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / std::max<uint64_t>(per_layer, 1));

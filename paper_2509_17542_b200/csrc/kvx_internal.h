@@ -1,5 +1,6 @@
 // Internal declarations shared by the library's translation units (not part of the ABI).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -67,6 +68,29 @@ struct ConvArgs {
   uint32_t n_items;
 };
 
+// TMA tile path (same dtype): one cp.async.bulk.tensor load per (dst block, layer, K/V,
+// P rank, source block) lands the sub-tile in smem already in D's order (the tensor map's
+// dimension order is D's), then bulk stores write D's contiguous runs.
+struct TileArgs {
+  CUtensorMap maps[KVX_MAX_RANKS][2];  // [source index][K/V]: dims (DIM, A, B, BLOCK, LAYER)
+  uint8_t* dst[KVX_MAX_RANKS];
+  int8_t dst_rank[KVX_MAX_RANKS];
+  int8_t src_of_p[KVX_MAX_RANKS];
+  int64_t ds[6];                        // destination element strides
+  int32_t Hp, Hd, Bp, Bd, D, esize, nh, lb, Lc, s_l0, d_l0;
+  int32_t head_major;  // D inner order (HEAD, SLOT, DIM): smem [nh][Bp][D]; else (SLOT, HEAD, DIM): [Bp][nh][D]
+  int32_t share_p;     // >= 0: only this P rank (kv_convert_share); -1: every P rank of each D rank
+  int32_t stage_bytes, stages;
+  const int32_t* s_blk_off;
+  const int32_t* s_blk_ids;
+  const int32_t* d_blk_off;
+  const int32_t* d_blk_ids;
+  const int32_t* d_blk_req;
+  const int32_t* tok_off;
+  FastDiv f_nd, f_parts, f_sub, f_l;
+  uint32_t n_items;
+};
+
 struct PackArgs {
   const uint8_t* src;
   uint8_t* wire;
@@ -128,6 +152,7 @@ struct AmaxArgs {
 // launchers (kvx_kernels.cu); vec = 8 (fast path, DIM innermost) or 1 (generic)
 cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out_scales, cudaStream_t s);
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s);
+cudaError_t launch_tile_copy(const TileArgs& a, cudaStream_t s);
 cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaStream_t s);
 cudaError_t launch_signal(uint32_t* flag, uint32_t value, cudaStream_t s);

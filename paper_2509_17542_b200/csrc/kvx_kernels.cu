@@ -553,6 +553,139 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_convert_tma(const __grid_con
 }
 
 // ------------------------------------------------------------------------------------
+// K1/K4 same-dtype TMA tile path (k_tile_copy).  One warp per CTA is a copy engine: per
+// item (dst rank, P rank share, source block within the dst block, K/V, layer, dst block)
+// lane 0 issues ONE cp.async.bulk.tensor.5d load of the whole source sub-tile (nh heads x Bp
+// slots x D) whose tensor map enumerates the source pool in the DESTINATION's inner order,
+// so the sub-tile lands in smem already permuted; tail slots are zeroed in smem; then the
+// lanes issue cp.async.bulk stores of D's contiguous runs (one run when the sub-tile is a
+// whole dst head range).  No register pass, 8-64 KB per TMA operation, `stages` items in
+// flight per CTA.  Source tail slots of the last block are read (inside the pool) but zeroed
+// before they are written.
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ void tma_load_5d(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            int32_t c2, int32_t c3, int32_t c4, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(32) k_tile_copy(const __grid_constant__ TileArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t S = (uint32_t)a.stages;
+  const uint32_t SB = (uint32_t)a.stage_bytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)S * SB);
+  if (lane == 0)
+    for (uint32_t s = 0; s < S; ++s) mbar_init(bars + s, 1);
+  fence_proxy_async();
+  __syncwarp();
+  const uint32_t my = blockIdx.x < a.n_items ? (a.n_items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  const uint32_t row_bytes = (uint32_t)a.D * (uint32_t)a.esize;
+
+  struct Item {
+    uint8_t* dbase;    // destination address of the sub-tile's first run
+    int64_t run_gap;   // bytes between consecutive runs in the destination
+    uint32_t nruns, run_bytes, valid;  // valid: source slots < T in this block (0 = no source)
+  };
+  auto decode = [&](uint32_t item, Item& it, int& si, int32_t& c0, int32_t& c1, int32_t& c2, int32_t& c3,
+                    int32_t& c4, uint32_t& c) {
+    uint32_t n = item;
+    const uint32_t qi = divmod(n, a.f_nd);
+    const uint32_t part = divmod(n, a.f_parts);
+    const uint32_t sub = divmod(n, a.f_sub);
+    c = n & 1u;
+    n >>= 1;
+    const uint32_t l = divmod(n, a.f_l);
+    const uint32_t bl = n;
+    const int32_t r = __ldg(a.d_blk_req + bl);
+    const int32_t tok0 = __ldg(a.tok_off + r);
+    const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+    const int32_t j = bl - __ldg(a.d_blk_off + r);
+    const int64_t dblk = __ldg(a.d_blk_ids + bl);
+    const int32_t layer = a.lb + (int32_t)l;
+    const int32_t q = a.dst_rank[qi];
+    const int32_t p = a.share_p >= 0 ? a.share_p : (q * a.Hd) / a.Hp + (int32_t)part;
+    const int32_t hp0 = max(q * a.Hd - p * a.Hp, 0), hq0 = max(p * a.Hp - q * a.Hd, 0);
+    si = a.src_of_p[p];
+    const int32_t t0 = j * a.Bd + (int32_t)sub * a.Bp;
+    it.valid = t0 >= T ? 0u : (uint32_t)min(a.Bp, T - t0);
+    int32_t sblk = 0;
+    if (it.valid) sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + (j * (a.Bd / a.Bp) + (int32_t)sub));
+    const int64_t dl = layer - a.d_l0;
+    uint8_t* tile = a.dst[qi] + (dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK]) * a.esize;
+    if (a.head_major) {  // D inner (HEAD, SLOT, DIM): one run per head of Bp rows
+      it.dbase = tile + ((int64_t)hq0 * a.ds[KV_AX_HEAD] + (int64_t)sub * a.Bp * a.ds[KV_AX_SLOT]) * a.esize;
+      it.run_gap = a.ds[KV_AX_HEAD] * a.esize;
+      it.nruns = (uint32_t)a.nh;
+      it.run_bytes = (uint32_t)a.Bp * row_bytes;
+      if (a.Bp == a.Bd) {  // whole head rows: the nh runs are back to back
+        it.run_bytes *= it.nruns;
+        it.nruns = 1;
+      }
+      c1 = 0;
+      c2 = hp0;
+    } else {  // D inner (SLOT, HEAD, DIM): one run per slot of nh rows
+      it.dbase = tile + ((int64_t)sub * a.Bp * a.ds[KV_AX_SLOT] + (int64_t)hq0 * a.ds[KV_AX_HEAD]) * a.esize;
+      it.run_gap = a.ds[KV_AX_SLOT] * a.esize;
+      it.nruns = (uint32_t)a.Bp;
+      it.run_bytes = (uint32_t)a.nh * row_bytes;
+      if (a.nh == a.Hd) {
+        it.run_bytes *= it.nruns;
+        it.nruns = 1;
+      }
+      c1 = hp0;
+      c2 = 0;
+    }
+    c0 = 0;
+    c3 = sblk;
+    c4 = layer - a.s_l0;
+  };
+
+  Item it[8];  // per stage (S <= 8)
+  auto issue = [&](uint32_t k, uint32_t s) {
+    int si;
+    int32_t c0, c1, c2, c3, c4;
+    uint32_t c;
+    decode(blockIdx.x + k * gridDim.x, it[s], si, c0, c1, c2, c3, c4, c);
+    if (lane == 0) {
+      mbar_expect_tx_arrive(bars + s, it[s].valid ? SB : 0u);
+      if (it[s].valid) tma_load_5d(smem + (size_t)s * SB, &a.maps[si][c], c0, c1, c2, c3, c4, bars + s);
+    }
+  };
+  for (uint32_t k = 0; k < my && k < S; ++k) issue(k, k);
+  for (uint32_t k = 0; k < my; ++k) {
+    const uint32_t s = k % S;
+    mbar_wait(bars + s, (k / S) & 1u);
+    uint8_t* buf = smem + (size_t)s * SB;
+    const Item& cur = it[s];
+    if (cur.valid < (uint32_t)a.Bp) {  // zero the rows of slots >= T (and whole sub-tiles past T)
+      const uint32_t v = cur.valid, nh = (uint32_t)a.nh, Bp = (uint32_t)a.Bp;
+      const uint32_t r16 = row_bytes / 16;
+      const uint32_t zrows = (Bp - v) * nh;
+      for (uint32_t z = lane; z < zrows * r16; z += 32) {
+        const uint32_t row = z / r16, piece = z - row * r16;
+        const uint32_t slot = v + row / nh, head = row - (row / nh) * nh;
+        const uint32_t ri = a.head_major ? head * Bp + slot : slot * nh + head;
+        *reinterpret_cast<uint4*>(buf + (size_t)ri * row_bytes + piece * 16) = make_uint4(0, 0, 0, 0);
+      }
+      fence_proxy_async();  // generic writes visible to the bulk stores
+      __syncwarp();
+    }
+    for (uint32_t run = lane; run < cur.nruns; run += 32)
+      bulk_store(cur.dbase + (int64_t)run * cur.run_gap, buf + (size_t)run * cur.run_bytes, cur.run_bytes);
+    bulk_commit();
+    // reload the stage consumed in the previous iteration once its stores have read it
+    bulk_wait_read<1>();
+    __syncwarp();
+    if (k >= 1 && k - 1 + S < my) issue(k - 1 + S, (k - 1) % S);
+  }
+  bulk_wait_all();
+}
+
+// ------------------------------------------------------------------------------------
 // K2 fast path: pack (Fig. 5 flatten) with the row machinery.  Item = 32 consecutive
 // tokens of one (layer, K/V, overlap head): the wire side is one contiguous 32-row run,
 // each lane gathers its token's row through the block table.
@@ -1088,6 +1221,21 @@ cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaSt
   if (a.total == 0) return cudaSuccess;
   return vec == 8 ? unpack_v<8>(a, wdt, ddt, s) : unpack_v<1>(a, wdt, ddt, s);
 }
+cudaError_t launch_tile_copy(const TileArgs& a, cudaStream_t s) {
+  if (a.n_items == 0) return cudaSuccess;
+  const size_t smem = (size_t)a.stages * (size_t)a.stage_bytes + 8 * (size_t)a.stages;
+  cudaError_t e = cudaFuncSetAttribute(k_tile_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_copy, 32, smem);
+  if (occ < 1) occ = 1;
+  const uint64_t cap = (uint64_t)num_sms() * (uint64_t)occ;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(a.n_items, cap));
+  k_tile_copy<<<grid, 32, smem, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) {
   const int64_t begin = (int64_t)(a.lb - a.d_l0) * 2 * a.Hd, end = (int64_t)(a.lb - a.d_l0 + a.Lc) * 2 * a.Hd;
   cudaError_t e = cudaMemsetAsync(out + begin, 0, (size_t)(end - begin) * sizeof(float), s);
