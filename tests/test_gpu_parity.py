@@ -205,6 +205,51 @@ def test_pack_unpack_widening_on_receiver(o1):
     assert_pools_match(dc.dst_numpy(), expected(case, o1), BF16)
 
 
+@pytest.mark.parametrize("tp_p,tp_d,Bp,Bd,dorder,dt", [
+    (4, 2, 16, 64, "head", BF16),   # merge, 4 source blocks per destination block (c3 shape)
+    (2, 1, 16, 16, "head", F16),    # merge into one D rank, whole head rows (c2 shape)
+    (2, 4, 8, 8, "slot", F16),      # split, D inner (SLOT, HEAD, DIM)
+    (4, 4, 16, 32, "slot", BF16),   # 1:1, two source blocks per destination block
+    (1, 1, 4, 4, "head", F32),      # fp32 rows
+])
+def test_tma_tile_path_forced(o1, monkeypatch, tp_p, tp_d, Bp, Bd, dorder, dt):
+    """The same-dtype TMA tile path (KVX_TILE=2 forces it for every sub-tile size): tensor
+    map in D's order, tail rows zeroed in smem, bulk stores; ragged requests incl. T = 0 and
+    requests shorter than a block; also per-P-rank shares."""
+    from tests.gpu_util import DevCase
+    import paper_2509_17542_b200 as kvx
+    monkeypatch.setenv("KVX_TILE", "2")
+    d_order = synth.D_ORDER if dorder == "head" else (BLOCK, LAYER, KV, SLOT, HEAD, DIM)
+    n_tokens = [Bd * 3 + 5, 0, 1, Bp - 1, Bd]
+    case = make_case(3, 8, 64, tp_p, tp_d, Bp, Bd, n_tokens, dt, dt, synth.P_ORDER, d_order,
+                     seed=40 + tp_p + Bd, o1=o1)
+    kvx.launch_count_reset()
+    run_case(o1, case)
+    # the same transfer as per-P-rank shares (distributed push primitive)
+    case2 = make_case(3, 8, 64, tp_p, tp_d, Bp, Bd, n_tokens, dt, dt, synth.P_ORDER, d_order,
+                      seed=40 + tp_p + Bd, o1=o1)
+    dc = DevCase(case2)
+    for p, q, _, _ in kvx.plan_pairs(tp_p, tp_d, 8):
+        kvx.convert_share(dc.src_lays[p], dc.src_pools[p], dc.src_bt, [dc.dst_lays[q]], [dc.dst_pools[q]], dc.dst_bt)
+    torch.cuda.synchronize()
+    assert_pools_match(dc.dst_numpy(), expected(case2, o1), dt)
+
+
+def test_tma_tile_and_row_paths_agree(o1, monkeypatch):
+    """KVX_TILE=0 (row kernel) and KVX_TILE=2 (TMA tile) give identical pools on a c2-shaped case."""
+    from tests.gpu_util import DevCase
+    case = make_case(4, 32, 128, 2, 1, 16, 16, [300, 17], F16, F16, seed=9, o1=o1)
+    outs = []
+    for mode in ("0", "2"):
+        monkeypatch.setenv("KVX_TILE", mode)
+        dc = DevCase(case)
+        dc.convert()
+        outs.append(dc.dst_numpy())
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    assert_pools_match(outs[1], expected(case, o1), F16)
+
+
 @pytest.mark.parametrize("vec_path", [True, False])
 def test_redzones_untouched(o1, vec_path):
     """compute-sanitizer is closed on this pool, so out-of-bounds writes are caught with
