@@ -334,7 +334,7 @@ def run_single(args):
                    "l2": "inputs larger than L2 (no flush)", "parallelism": "none (1 GPU)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _traffic(wl_name, 1),
-                     "kernel": "k_convert_rows", "kernel_ms": round(kern_ms, 5),
+                     "kernel": kvx.last_kernel(), "kernel_ms": round(kern_ms, 5),
                      "algorithmic_bytes_per_launch": alg, "peak_source": peaks["source"],
                      "frac_vs_nominal_8TBs": round(achieved / 8000.0, 4)},
         "clocks": clk, "gpu_launches": int(launches),
@@ -549,6 +549,7 @@ def run_multi(args):
     nvl_out = sum(w.dst_bytes([0]) * (len([1 for p2, q2, _, _ in pairs if q2 == q and p2 == me.tp_rank])) //
                   max(1, len([1 for p2, q2, _, _ in pairs if q2 == q])) for q in my_q) if me.kind == "P" else 0
     stats = {"ms": my_ms, "kern_ms": kern_ms, "launches": launches, "kind": me.kind, "nvl": max(nvl_in, nvl_out),
+             "kernel": kvx.last_kernel(),
              "clk": clk}
     parity = None
     if not args.no_parity and me.kind == "D":
@@ -584,7 +585,8 @@ def run_multi(args):
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED_GBS,
                          "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED_GBS, 4),
                          "traffic": _traffic(wl_name, world) if args.mode == "push" else None,
-                         "kernel": "k_convert_rows (peer-store push)" if args.mode == "push"
+                         "kernel": f"{[x['kernel'] for x in sts if x['kind'] == 'P'][0]} (peer-store push)"
+                         if args.mode == "push"
                          else "pack + ncclSend/Recv + unpack (whole P step)",
                          "kernel_ms": round(kms, 4), "algorithmic_bytes_per_step": nvl_b,
                          "note": "busiest GPU link (P egress or D ingress) bytes / step time",

@@ -327,6 +327,10 @@ uint64_t kv_launch_count(void);
 void kv_launch_count_reset(void);
 
 const char* kv_last_error(void); /* thread-local, valid until the next failing call */
+/* Name of the data-path kernel the calling thread's last convert / pack / unpack call
+ * launched ("k_tile_copy", "k_convert_rows", "k_convert", "k_pack_rows", ...); for the
+ * bench's roofline line and for tests that pin which path a case takes. */
+const char* kv_last_kernel(void);
 const char* kv_version(void);
 
 #ifdef __cplusplus

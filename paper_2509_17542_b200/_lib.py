@@ -101,6 +101,7 @@ def _load():
         "kv_set_sm_budget": (i32, [i32]),
         "kv_launch_count_reset": (None, []),
         "kv_last_error": (C.c_char_p, []),
+        "kv_last_kernel": (C.c_char_p, []),
         "kv_version": (C.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -118,7 +119,7 @@ EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_bloc
            "kv_wire_header_write", "kv_wire_header_parse", "kv_wire_header_check", "kv_copy_bytes", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
            "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
            "kv_recv_unpack", "kv_push", "kv_send_pipelined", "kv_recv_pipelined", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",
-           "kv_launch_count", "kv_launch_count_reset", "kv_set_sm_budget", "kv_last_error", "kv_version")
+           "kv_launch_count", "kv_launch_count_reset", "kv_set_sm_budget", "kv_last_error", "kv_last_kernel", "kv_version")
 
 
 def check(status):

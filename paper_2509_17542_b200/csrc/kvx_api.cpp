@@ -13,6 +13,7 @@
 namespace kvx {
 
 static thread_local std::string t_err;
+static thread_local const char* t_last_kernel = "";
 std::atomic<uint64_t> g_launches{0};
 std::atomic<int32_t> g_sm_budget{0};
 
@@ -129,6 +130,7 @@ constexpr uint64_t kMaxChunks = 0x7FFFFFFFull;  // per launch (32-bit decode)
 extern "C" {
 
 const char* kv_last_error(void) { return t_err.c_str(); }
+const char* kv_last_kernel(void) { return t_last_kernel; }
 const char* kv_version(void) { return "kvx 0.1 (sm_100a)"; }
 uint64_t kv_launch_count(void) { return g_launches.load(); }
 void kv_launch_count_reset(void) { g_launches.store(0); }
@@ -526,7 +528,10 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
     if ((st = try_tile_copy(n_src, src, src_pools, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, share,
                             &used)) != KV_OK)
       return st;
-    if (used) return KV_OK;
+    if (used) {
+      t_last_kernel = "k_tile_copy";
+      return KV_OK;
+    }
   }
   // per-layer chunk count; split the layer range so each launch stays under 2^31 chunks
   const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * 2 * a.Hd_eff * a.Bd * ndch;
@@ -538,6 +543,7 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
     a.Lc = l1 - l0;
     a.f_l = make_fastdiv((uint32_t)a.Lc);
     a.total = (uint32_t)(per_layer * (uint64_t)a.Lc);
+    t_last_kernel = vec == 8 ? "k_convert_rows" : "k_convert";
     cudaError_t e = launch_convert(a, vec, S->d.dtype, D->d.dtype, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "kv_convert_reshard: launch");
   }
@@ -687,6 +693,7 @@ kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_
   if (total > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_pack: more than 2^31 chunks in one call; split layers");
   a.total = (uint32_t)total;
   a.f_l = make_fastdiv((uint32_t)a.Lc);
+  t_last_kernel = vec == 8 ? "k_pack_rows" : "k_pack";
   cudaError_t e = launch_pack(a, vec, s->d.dtype, kv_wire_dtype(s, d), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kv_pack: launch");
   return KV_OK;
@@ -744,6 +751,7 @@ kv_status kv_unpack(const kv_layout* s, const kv_layout* d, void* dst_pool, cons
   if (total > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_unpack: more than 2^31 chunks in one call; split layers");
   a.total = (uint32_t)total;
   a.f_bl = make_fastdiv((uint32_t)dst_bt->total_blocks);
+  t_last_kernel = vec == 8 ? "k_unpack_rows" : "k_unpack";
   cudaError_t e = launch_unpack(a, vec, kv_wire_dtype(s, d), d->d.dtype, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kv_unpack: launch");
   return KV_OK;

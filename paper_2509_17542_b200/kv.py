@@ -13,7 +13,7 @@ from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BY
                    KV_F32, Batch_t, KvError, LayoutDesc, check, lib)
 
 __all__ = ["Layout", "Batch", "convert_reshard", "convert_share", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
-           "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "launch_count", "launch_count_reset", "set_sm_budget",
+           "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "launch_count", "launch_count_reset", "set_sm_budget", "last_kernel",
            "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "DTYPE_BYTES",
            "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
 
@@ -311,6 +311,11 @@ def wait(flag, value, err, timeout_s=10.0, stream=None):
 
 def launch_count():
     return lib.kv_launch_count()
+
+
+def last_kernel() -> str:
+    """kv_last_kernel: the data-path kernel this thread's last convert/pack/unpack launched."""
+    return lib.kv_last_kernel().decode()
 
 
 def set_sm_budget(n_sms: int) -> int:
