@@ -49,7 +49,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default="push", choices=["push", "nccl"])
+    ap.add_argument("--mode", default="pull", choices=["push", "pull", "nccl"])
+    ap.add_argument("--ring-slots", type=int, default=3, help="pull mode, narrowing cast: staging ring depth")
     ap.add_argument("--layer-chunk", type=int, default=0, help="layers per chunk (0 = whole model)")
     ap.add_argument("--chunk-mib", type=int, default=64, help="c5: merge layers until a chunk moves this much")
     ap.add_argument("--c5-batch", action="store_true", help="c5: push each instance's requests as one batch")
@@ -479,6 +480,63 @@ def run_multi(args):
             elif me.kind == "D":
                 for p in my_p:
                     kvx.wait(flags[p:p + 1], epoch[0], err, 30.0, stream)
+    elif args.mode == "pull":
+        # D-initiated read: D maps P's pool (or P's staging ring when the cast narrows)
+        narrowing = synth.NBYTES[cfg.dst_dtype] < synth.NBYTES[cfg.src_dtype]
+        p_lays = {p: kvx.Layout.from_dict(
+            synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, w.NB_p, cfg.src_dtype, cfg.p_order))
+            for p in my_p}
+        R = max(1, args.ring_slots)
+        if narrowing and not args.layer_chunk:
+            lc = max(1, cfg.L // 20)
+        ring, slot_bytes, dst_lays = None, 0, {}
+        if me.kind == "P":
+            dst_lays = {q: d_view(q) for q in my_q}
+            S = w.src_lays[me.tp_rank]
+            if narrowing:
+                slot_bytes = max(kvx.wire_bytes(S, dst_lays[q], cfg.total_tokens, (l0, min(cfg.L, l0 + lc)))
+                                 for q in my_q for l0 in range(0, cfg.L, lc))
+                slot_bytes = (slot_bytes + 255) // 256 * 256
+                ring = torch.empty(len(my_q) * R * slot_bytes, dtype=torch.uint8, device=dev)
+                ring_ptrs = [ring.data_ptr() + (i * R + b) * slot_bytes for i in range(len(my_q)) for b in range(R)]
+        pflags = torch.zeros(max(n_p, n_d, 1), dtype=torch.int32, device=dev)
+        pch = tr.PullChannel(me, pflags, pool=w.src_pools[me.tp_rank] if me.kind == "P" and not narrowing else None,
+                             ring=ring, ring_dst=my_q if ring is not None else (), ring_slots=R, slot_bytes=slot_bytes)
+        if me.kind == "D" and narrowing:
+            slot_bytes = min(pch.slot_bytes[p] for p in my_p)
+        nchunks = kvx.chunk_count((0, cfg.L), lc)
+        counters = torch.zeros(2 * nchunks, dtype=torch.int32, device=dev)
+        seq = [0]
+
+        def step(ev=None):
+            epoch[0] += 1
+            if ev is not None and me.kind == "D":
+                ev[0].record(stream)
+            if me.kind == "P":
+                if narrowing:
+                    kvx.stage(S, w.src_pools[me.tp_rank], w.src_bt, [dst_lays[q] for q in my_q],
+                              ring_ptrs, R,
+                              slot_bytes, [pch.peer_flag[q] for q in my_q], [pflags[q:q + 1] for q in my_q],
+                              seq[0], err, (0, cfg.L), lc, 30.0, stream)
+                else:
+                    for q in my_q:   # my KV is resident: D may read it; then wait until it has
+                        kvx.signal(pch.peer_flag[q], epoch[0], stream)
+                    for q in my_q:
+                        kvx.wait(pflags[q:q + 1], epoch[0], err, 30.0, stream)
+            elif me.kind == "D":
+                q = me.tp_rank
+                if narrowing:
+                    kvx.pull_staged([p_lays[p] for p in my_p], [a for p in my_p for a in pch.src_ring[p]], R,
+                                    slot_bytes, w.dst_lays[q], w.dst_pools[q], w.dst_bt,
+                                    [pflags[p:p + 1] for p in my_p], [pch.peer_flag[p] for p in my_p], seq[0], err,
+                                    (0, cfg.L), lc, 30.0, stream, counters=counters)
+                else:
+                    kvx.pull([p_lays[p] for p in my_p], [pch.src_pool[p] for p in my_p], w.src_bt, w.dst_lays[q],
+                             w.dst_pools[q], w.dst_bt, [pflags[p:p + 1] for p in my_p],
+                             [pch.peer_flag[p] for p in my_p], epoch[0], err, (0, cfg.L), lc, 30.0, stream)
+            seq[0] += nchunks
+            if ev is not None and me.kind == "D":
+                ev[1].record(stream)
     else:
         # NCCL baseline: pack -> ncclSend / ncclRecv -> unpack, per-layer double-buffered
         uid = [kvx.Comm.unique_id() if rank == 0 else None]
@@ -541,7 +599,8 @@ def run_multi(args):
     clk = clocks.stop()
     barrier()
     my_ms = t0.elapsed_time(t1)
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev) if me.kind == "P" else 0.0
+    mover = "D" if args.mode == "pull" else "P"   # the rank whose stream runs the data-path kernels
+    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev) if me.kind == mover else 0.0
     if int(err.item()):
         raise SystemExit(f"rank {rank}: flag wait timed out")
     # busiest link: P egress = bytes it sends, D ingress = bytes it receives (wire dtype = dst)
@@ -555,14 +614,15 @@ def run_multi(args):
     if not args.no_parity and me.kind == "D":
         parity = parity_multi(cfg, w, me, my_p, dev)
     e2e = None
-    if not args.no_e2e and args.mode == "push":
+    if not args.no_e2e and args.mode in ("push", "pull"):
         e2e = e2e_multi(w, me, step, stream, barrier, err, min(K, 3), rank)
     allx = tr.exchange({"stats": stats, "parity": parity, "e2e": e2e})
     if rank == 0:
         sts = [x["stats"] for x in allx]
         max_ms = max(x["ms"] for x in sts)
         ms = max_ms / K
-        kms = max(x["kern_ms"] for x in sts if x["kind"] == "P")
+        mover = "D" if args.mode == "pull" else "P"
+        kms = max(x["kern_ms"] for x in sts if x["kind"] == mover)
         src_b = w.src_bytes(range(n_p))
         nvl_b = max(x["nvl"] for x in sts)
         achieved = nvl_b / (ms * 1e-3) / 1e9
@@ -587,6 +647,8 @@ def run_multi(args):
                          "traffic": _traffic(wl_name, world) if args.mode == "push" else None,
                          "kernel": f"{[x['kernel'] for x in sts if x['kind'] == 'P'][0]} (peer-store push)"
                          if args.mode == "push"
+                         else f"{[x['kernel'] for x in sts if x['kind'] == 'D'][0]} (peer-load pull on D)"
+                         if args.mode == "pull"
                          else "pack + ncclSend/Recv + unpack (whole P step)",
                          "kernel_ms": round(kms, 4), "algorithmic_bytes_per_step": nvl_b,
                          "note": "busiest GPU link (P egress or D ingress) bytes / step time",

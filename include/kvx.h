@@ -291,6 +291,53 @@ kv_status kv_recv_pipelined(kv_comm* comm, int32_t n_src, const kv_layout* const
                             size_t wire_cap, int32_t layer_begin, int32_t layer_end, int32_t layer_chunk,
                             kv_stream stream, kv_stream recv_stream, kv_stream unpack_stream);
 
+/* D-initiated read over NVLink -- the paper's direction (D calls read(local buffer,
+ * remote buffer, remote location) once P's KV is ready; P:95 step 5).  SM loads of a
+ * peer-mapped source move more user bytes per second over NVLink than SM stores to a
+ * peer-mapped destination, so a D rank pulls whenever the cast does not
+ * narrow; a narrowing cast is done by the sender into a staging ring that D pulls from, so
+ * the link still carries the narrow bytes.
+ *
+ * kv_pull (same-width or widening cast): on `stream` (D's GPU) wait until every
+ * *ready_flags[i] >= epoch (local words that P rank i signals when its KV is resident),
+ * then kv_convert_reshard(src -> {dst}) per layer chunk with src_pools[i] the IPC-mapped P
+ * pools (src_bt: D's copy of P's block table), then kv_signal(done_flags[i], epoch) into
+ * each P rank's memory (P may reuse its blocks after acquiring it).
+ *
+ * kv_stage (P side of a narrowing pull) / kv_pull_staged (D side).  Chunks of
+ * [layer_begin, layer_end) carry global sequence numbers seq = seq0, seq0 + 1, ...; chunk seq
+ * of the pair (P rank, D rank i) lives in ring slot seq % ring_slots.  rings[i*ring_slots+b]
+ * are slot_bytes device buffers owned by the P rank (on D: the peer-mapped addresses of P
+ * rank i's slots for this D rank), each >= the largest chunk's kv_wire_bytes.
+ *   P: wait *free_flags[i] >= seq + 1 - ring_slots (local word D writes), kv_pack into the
+ *      slot, then kv_signal(ready_flags[i], seq + 1) (peer word in D's memory);
+ *   D: wait *ready_flags[i] >= seq + 1 (local), kv_unpack from the peer slot (NVLink reads),
+ *      kv_signal(free_flags[i], seq + 1) (peer word in P's memory).
+ * When wire and pool share the dtype (the narrowing case this exists for), kv_pull_staged
+ * is ONE persistent launch (k_pull_rows): warps take items chunk after chunk from a
+ * shared counter, wait in-kernel for each chunk's ready words, and the warp completing a
+ * chunk frees its slots -- no per-chunk launch gap.  It needs `counters`, a caller-owned
+ * DEVICE scratch of >= 2 x (number of chunks) uint32 that the call zeroes on its stream
+ * (NULL: one kv_wait / kv_unpack / kv_signal launch triple per chunk instead).
+ * The caller advances seq0 by the number of chunks per call.  All three validate before
+ * enqueueing; a wait that times out sets *err = 1 (device int32 on the waiting GPU) and the
+ * stream goes on (the data are then undefined).  Waiter and signaller must be different
+ * GPUs (kv_wait). */
+kv_status kv_pull(int32_t n_src, const kv_layout* const* src, const void* const* src_pools, const kv_batch* src_bt,
+                  const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt, const uint32_t* const* ready_flags,
+                  uint32_t* const* done_flags, uint32_t epoch, int32_t layer_begin, int32_t layer_end,
+                  int32_t layer_chunk, uint64_t timeout_ns, int32_t* err, kv_stream stream);
+kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, int32_t n_dst,
+                   const kv_layout* const* dst, void* const* rings, int32_t ring_slots, size_t slot_bytes,
+                   uint32_t* const* ready_flags, const uint32_t* const* free_flags, uint32_t seq0,
+                   int32_t layer_begin, int32_t layer_end, int32_t layer_chunk, uint64_t timeout_ns, int32_t* err,
+                   kv_stream stream);
+kv_status kv_pull_staged(int32_t n_src, const kv_layout* const* src, const void* const* rings, int32_t ring_slots,
+                         size_t slot_bytes, const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt,
+                         const uint32_t* const* ready_flags, uint32_t* const* free_flags, uint32_t* counters,
+                         uint32_t seq0, int32_t layer_begin, int32_t layer_end, int32_t layer_chunk,
+                         uint64_t timeout_ns, int32_t* err, kv_stream stream);
+
 /* CUDA IPC for the direct-store (push) mode.  kv_ipc_export writes the 64-byte handle of
  * the allocation containing dev_ptr and dev_ptr's offset inside it; kv_ipc_open maps it in
  * this process (the current device must have peer access to the owner) and returns the

@@ -91,6 +91,12 @@ def _load():
                                    i32, p, p, p]),
         "kv_recv_pipelined": (st, [p, i32, pp, C.POINTER(i32), p, p, C.POINTER(Batch_t), pp, C.c_size_t, i32, i32,
                                    i32, p, p, p]),
+        "kv_pull": (st, [i32, pp, pp, C.POINTER(Batch_t), p, p, C.POINTER(Batch_t), pp, pp, C.c_uint32, i32, i32, i32,
+                         u64, p, p]),
+        "kv_stage": (st, [p, p, C.POINTER(Batch_t), i32, pp, pp, i32, C.c_size_t, pp, pp, C.c_uint32, i32, i32, i32,
+                          u64, p, p]),
+        "kv_pull_staged": (st, [i32, pp, pp, i32, C.c_size_t, p, p, C.POINTER(Batch_t), pp, pp, p, C.c_uint32, i32,
+                                i32, i32, u64, p, p]),
         "kv_ipc_export": (st, [p, p, C.POINTER(u64)]),
         "kv_ipc_open": (st, [p, u64, C.POINTER(p)]),
         "kv_ipc_close": (st, [p]),
@@ -118,7 +124,8 @@ EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_bloc
            "kv_convert_reshard", "kv_convert_share", "kv_compute_scales", "kv_wire_dtype", "kv_wire_header_bytes",
            "kv_wire_header_write", "kv_wire_header_parse", "kv_wire_header_check", "kv_copy_bytes", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
            "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
-           "kv_recv_unpack", "kv_push", "kv_send_pipelined", "kv_recv_pipelined", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",
+           "kv_recv_unpack", "kv_push", "kv_send_pipelined", "kv_recv_pipelined", "kv_pull", "kv_stage",
+           "kv_pull_staged", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",
            "kv_launch_count", "kv_launch_count_reset", "kv_set_sm_budget", "kv_last_error", "kv_last_kernel", "kv_version")
 
 

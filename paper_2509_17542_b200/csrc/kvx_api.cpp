@@ -758,3 +758,80 @@ kv_status kv_unpack(const kv_layout* s, const kv_layout* d, void* dst_pool, cons
 }
 
 }  // extern "C"
+
+namespace kvx {
+
+// kv_pull_staged's one-launch path (k_pull_rows): taken when wire and pool share the dtype,
+// head_dim is innermost with 16-B aligned rows, the ring slots are 16-B aligned and every
+// source overlaps the destination in the same number of heads.  Otherwise *used = false.
+kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void* const* rings, int32_t R,
+                         const kv_layout* d, void* dst_pool, const kv_batch* dst_bt, const uint32_t* const* ready,
+                         uint32_t* const* freef, uint32_t* counters, uint32_t seq0, int32_t lb, int32_t le,
+                         int32_t step, uint64_t timeout_ns, int32_t* err, kv_stream stream, bool* used) {
+  *used = false;
+  if (!counters || n_src > KVX_MAX_RANKS || R > KVX_MAX_RING || !fast_ok(d) || !ptr_aligned(dst_pool, 16)) return KV_OK;
+  if (getenv("KVX_PULL_CHUNKED")) return KV_OK;  // A/B switch: per-chunk launches
+  PullArgs a;
+  memset(&a, 0, sizeof(a));
+  int32_t nh = -1;
+  for (int i = 0; i < n_src; ++i) {
+    if (kv_wire_dtype(src[i], d) != d->d.dtype) return KV_OK;
+    int32_t hb, he;
+    head_overlap(src[i], d, &hb, &he);
+    if (nh >= 0 && he - hb != nh) return KV_OK;
+    nh = he - hb;
+    a.hb[i] = hb;
+    for (int b = 0; b < R; ++b) {
+      const void* r = rings[(size_t)i * R + b];
+      if (!ptr_aligned(r, 16)) return KV_OK;
+      a.ring[i][b] = static_cast<const uint8_t*>(r);
+    }
+    a.ready[i] = ready[i];
+    a.freef[i] = freef[i];
+  }
+  if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;  // the chunked path handles the flags
+  a.dst = static_cast<uint8_t*>(dst_pool);
+  a.counters = counters;
+  a.err = err;
+  a.timeout_ns = timeout_ns;
+  for (int ax = 0; ax < 6; ++ax) a.ds[ax] = d->stride[ax];
+  a.nsrc = n_src;
+  a.R = R;
+  a.Hd = d->h_local;
+  a.D = d->d.head_dim;
+  a.Bd = d->d.block_size;
+  a.lb = lb;
+  a.le = le;
+  a.step = step;
+  a.nchunks = (le - lb + step - 1) / step;
+  a.q = d->d.tp_rank;
+  a.nh = nh;
+  a.d_l0 = d->d.first_layer;
+  a.seq0 = seq0;
+  a.total_tokens = dst_bt->total_tokens;
+  a.d_blk_off = dst_bt->blk_off;
+  a.d_blk_ids = dst_bt->blk_ids;
+  a.d_blk_req = dst_bt->blk_req;
+  a.tok_off = dst_bt->tok_off;
+  a.f_src = make_fastdiv((uint32_t)n_src);
+  a.slot_inner = slot_inner_of(d);
+  a.n_blk = (uint32_t)dst_bt->total_blocks;
+  const uint64_t items = (uint64_t)n_src * 2 * (uint64_t)step * dst_bt->total_blocks * (uint64_t)a.Bd * (uint64_t)nh;
+  if (items > kMaxChunks) return KV_OK;
+  a.spin_ns = getenv("KVX_PULL_SPIN_NS") ? (uint32_t)atoi(getenv("KVX_PULL_SPIN_NS")) : 128u;
+  // Wait for the first chunk with a one-thread kernel before the persistent launch: warps
+  // spinning in-kernel while P packs chunk 0 cost ~4x the wait itself (c4: lc=10, 8.6 vs
+  // 7.3 ms, profiles/r01/pull_probe*.jsonl); later chunks are normally ready when reached.
+  if (!getenv("KVX_PULL_NOPREWAIT"))
+    for (int i = 0; i < n_src; ++i) {
+      kv_status w = kv_wait(ready[i], seq0 + 1, timeout_ns, err, stream);
+      if (w != KV_OK) return w;
+    }
+  t_last_kernel = "k_pull_rows";
+  cudaError_t e = launch_pull_rows(a, d->d.dtype, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_pull_staged: launch");
+  *used = true;
+  return KV_OK;
+}
+
+}  // namespace kvx

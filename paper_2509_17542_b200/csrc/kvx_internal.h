@@ -133,6 +133,35 @@ struct UnpackArgs {
   uint32_t n_items;
 };
 
+// Persistent D-side staged pull (k_pull_rows): one launch covers every layer chunk of a
+// kv_pull_staged call; warps wait in-kernel for each chunk's ready flags and the last warp
+// out of a chunk releases its ring slots.  Item (chunk-relative) =
+// ((((dst block, local layer), K/V), sub-tile), source).  Same dtype on wire and pool.
+#define KVX_MAX_RING 8
+struct PullArgs {
+  uint8_t* dst;
+  const uint8_t* ring[KVX_MAX_RANKS][KVX_MAX_RING];  // [source][slot] peer-mapped
+  const uint32_t* ready[KVX_MAX_RANKS];               // local words P writes
+  uint32_t* freef[KVX_MAX_RANKS];                     // peer words in P's memory
+  int32_t hb[KVX_MAX_RANKS];                          // first global head of each overlap
+  uint32_t* counters;                                 // [nchunks] warps done, zero on entry
+  int32_t* err;
+  uint64_t timeout_ns;
+  uint32_t spin_ns;  // back-off between polls
+  int64_t ds[6];
+  int32_t nsrc, R, Hd, D, Bd, lb, le, step, nchunks, q, nh, d_l0;
+  uint32_t seq0;
+  int64_t total_tokens;
+  const int32_t* d_blk_off;
+  const int32_t* d_blk_ids;
+  const int32_t* d_blk_req;
+  const int32_t* tok_off;
+  FastDiv f_src, f_sb, f_items, f_l_full, f_l_last;
+  int32_t slot_inner, cpr_shift, ts_log2;
+  uint32_t n_blk;                   // dst blocks of the batch
+  uint32_t items_full, items_last;  // items per chunk (all sources), set by the launcher
+};
+
 struct AmaxArgs {
   const uint8_t* src[KVX_MAX_RANKS];
   const float* sscale[KVX_MAX_RANKS];
@@ -150,6 +179,13 @@ struct AmaxArgs {
 };
 
 // launchers (kvx_kernels.cu); vec = 8 (fast path, DIM innermost) or 1 (generic)
+// kvx_api.cpp: kv_pull_staged's one-launch path (sets *used when it took it)
+kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void* const* rings, int32_t R,
+                         const kv_layout* d, void* dst_pool, const kv_batch* dst_bt, const uint32_t* const* ready,
+                         uint32_t* const* freef, uint32_t* counters, uint32_t seq0, int32_t lb, int32_t le,
+                         int32_t step, uint64_t timeout_ns, int32_t* err, kv_stream stream, bool* used);
+// dt: the (common) wire / pool dtype; vec-8 row machinery only
+cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s);
 cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out_scales, cudaStream_t s);
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s);
 cudaError_t launch_tile_copy(const TileArgs& a, cudaStream_t s);

@@ -62,22 +62,36 @@ struct Chunk {
   uint32_t w[WORDS];
 };
 
-template <int DT, int VEC>
+// COH = false: the read-only (.nc) path -- the source is not written during the kernel.
+// COH = true: ordinary weak loads, ordered after an acquire in the same kernel (the
+// persistent pull reads ring slots the P rank rewrites while the kernel runs).
+template <bool COH>
+__device__ __forceinline__ void ld_v4(uint32_t& x, uint32_t& y, uint32_t& z, uint32_t& w, const uint8_t* p) {
+  if constexpr (COH)
+    asm volatile("ld.global.L1::no_allocate" KVX_LD_HINT ".v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "l"(p) : "memory");
+  else
+    asm volatile("ld.global.nc.L1::no_allocate" KVX_LD_HINT ".v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "l"(p));
+}
+template <bool COH>
+__device__ __forceinline__ void ld_v2(uint32_t& x, uint32_t& y, const uint8_t* p) {
+  if constexpr (COH)
+    asm volatile("ld.global.L1::no_allocate" KVX_LD_HINT ".v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "l"(p) : "memory");
+  else
+    asm volatile("ld.global.nc.L1::no_allocate" KVX_LD_HINT ".v2.u32 {%0,%1}, [%2];" : "=r"(x), "=r"(y) : "l"(p));
+}
+
+template <int DT, int VEC, bool COH = false>
 __device__ __forceinline__ void load_chunk(Chunk<DT, VEC>& c, const uint8_t* p) {
   constexpr int N = Chunk<DT, VEC>::BYTES;
   if constexpr (N == 32) {
-    uint4 a, b;
-    asm volatile("ld.global.nc.L1::no_allocate" KVX_LD_HINT ".v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(p));
-    asm volatile("ld.global.nc.L1::no_allocate" KVX_LD_HINT ".v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(b.x), "=r"(b.y), "=r"(b.z), "=r"(b.w) : "l"(p + 16));
-    c.w[0] = a.x; c.w[1] = a.y; c.w[2] = a.z; c.w[3] = a.w;
-    c.w[4] = b.x; c.w[5] = b.y; c.w[6] = b.z; c.w[7] = b.w;
+    ld_v4<COH>(c.w[0], c.w[1], c.w[2], c.w[3], p);
+    ld_v4<COH>(c.w[4], c.w[5], c.w[6], c.w[7], p + 16);
   } else if constexpr (N == 16) {
-    asm volatile("ld.global.nc.L1::no_allocate" KVX_LD_HINT ".v4.u32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3]) : "l"(p));
+    ld_v4<COH>(c.w[0], c.w[1], c.w[2], c.w[3], p);
   } else if constexpr (N == 8) {
-    asm volatile("ld.global.nc.L1::no_allocate" KVX_LD_HINT ".v2.u32 {%0,%1}, [%2];" : "=r"(c.w[0]), "=r"(c.w[1]) : "l"(p));
+    ld_v2<COH>(c.w[0], c.w[1], p);
   } else if constexpr (N == 4) {
     c.w[0] = *reinterpret_cast<const uint32_t*>(p);
   } else if constexpr (N == 2) {
@@ -297,7 +311,7 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
 // (0 copy, 1 zero-fill tail row, 2 no row).  The warp streams the 32 x 2^cs chunks of
 // 16 B (source side) with U loads in flight per lane, fetching row state by shuffles.
 // ------------------------------------------------------------------------------------
-template <int SDT, int DDT, int U, int VEC = 8>
+template <int SDT, int DDT, int U, int VEC = 8, bool COH = false>
 __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t sp, uint64_t dp, float rsc,
                                             uint32_t rz) {
   const uint32_t cmask = (1u << cs) - 1u;
@@ -316,7 +330,7 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
       d[k] = __shfl_sync(0xffffffffu, dp, rr);
       z[k] = __shfl_sync(0xffffffffu, rz, rr) | (idx >= nch ? 2u : 0u);
       sc[k] = __shfl_sync(0xffffffffu, rsc, rr);
-      if (z[k] == 0) load_chunk<SDT, VEC>(in[k], reinterpret_cast<const uint8_t*>(s) + ch[k] * (VEC * Tr<SDT>::B));
+      if (z[k] == 0) load_chunk<SDT, VEC, COH>(in[k], reinterpret_cast<const uint8_t*>(s) + ch[k] * (VEC * Tr<SDT>::B));
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -783,6 +797,118 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
 }
 
 // ------------------------------------------------------------------------------------
+// K3 persistent staged pull (kv_pull_staged, D side): the unpack row machinery over every
+// layer chunk of the call in ONE launch.  Warps take kPullGrab items at a time from a
+// per-chunk counter (chunk after chunk), so all warps leave a chunk within one grab of each
+// other.  Before its first item of chunk k a warp waits (lane 0, acquire, system scope)
+// for every source's ready word >= seq0 + k + 1; the warp whose items complete chunk k
+// releases the ring slot back to the P ranks (system-scope release stores into their
+// memory).  One ramp-up and one tail per call instead of one per chunk; loads come over
+// NVLink from the P ranks' ring slots (weak loads, ordered after the acquire).
+// ------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+constexpr uint32_t kPullGrab = 4;  // items (32 rows each) per hand-out
+
+__device__ __forceinline__ void spin_until(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, int32_t* err,
+                                           uint32_t spin_ns) {
+  const uint64_t t0 = globaltimer_ns();
+  while (true) {
+    uint32_t x;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(flag) : "memory");
+    if ((int32_t)(x - value) >= 0) return;
+    if (globaltimer_ns() - t0 > timeout_ns) {
+      *err = 1;
+      return;
+    }
+    __nanosleep(spin_ns);
+  }
+}
+
+template <int DT, int U>
+__global__ void __launch_bounds__(kThreads) k_pull_rows(const __grid_constant__ PullArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t cs = (uint32_t)a.cpr_shift;
+  const uint32_t ts_log2 = (uint32_t)a.ts_log2;
+  const uint32_t ls = a.slot_inner ? (lane & ((1u << ts_log2) - 1u)) : (lane >> (5u - ts_log2));
+  const uint32_t lh = a.slot_inner ? (lane >> ts_log2) : (lane & ((1u << (5u - ts_log2)) - 1u));
+  uint32_t* next = a.counters;               // [nchunks] items handed out
+  uint32_t* done = a.counters + a.nchunks;   // [nchunks] items finished
+  for (int32_t k = 0; k < a.nchunks; ++k) {
+    const bool last = k == a.nchunks - 1;
+    const uint32_t n_k = last ? a.items_last : a.items_full;
+    const FastDiv& f_l = last ? a.f_l_last : a.f_l_full;
+    const uint32_t slot_idx = (a.seq0 + (uint32_t)k) % (uint32_t)a.R;
+    const int64_t l0 = (int64_t)a.lb + (int64_t)k * a.step;
+    bool waited = false;
+    while (true) {
+      // dynamic hand-out: every warp leaves chunk k within one grab of the others, so the
+      // ring slots come back in order and no warp runs R chunks ahead of the slowest
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(next + k, kPullGrab);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= n_k) break;
+      if (!waited) {
+        if (lane == 0)
+          for (int s = 0; s < a.nsrc; ++s) spin_until(a.ready[s], a.seq0 + (uint32_t)k + 1u, a.timeout_ns, a.err, a.spin_ns);
+        __syncwarp();
+        waited = true;
+      }
+      const uint32_t end = min(n_k, base + kPullGrab);
+      for (uint32_t item = base; item < end; ++item) {
+        uint32_t n = item;
+        const uint32_t src = divmod(n, a.f_src);
+        uint32_t sbk = divmod(n, a.f_items);
+        const uint32_t c = n & 1u;
+        n >>= 1;
+        const uint32_t lk = divmod(n, f_l);
+        const uint32_t bl = n;
+        const uint32_t s_blk = divmod(sbk, a.f_sb);
+        const uint32_t slot = (s_blk << ts_log2) + ls;
+        const uint32_t hh = (sbk << (5u - ts_log2)) + lh;
+        const int32_t r = __ldg(a.d_blk_req + bl);
+        const int32_t tok0 = __ldg(a.tok_off + r);
+        const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+        const int64_t dl = l0 + (int64_t)lk - a.d_l0;
+        uint64_t sp = 0, dp = 0;
+        uint32_t rz = 2;
+        if (slot < (uint32_t)a.Bd && hh < (uint32_t)a.nh) {
+          rz = 0;
+          const uint32_t t = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd + slot;
+          const int64_t dblk = __ldg(a.d_blk_ids + bl);
+          const uint32_t hq = (uint32_t)a.hb[src] + hh - (uint32_t)a.q * (uint32_t)a.Hd;
+          dp = (uint64_t)(a.dst + (dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
+                                   (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD]) * Tr<DT>::B);
+          if ((int32_t)t >= T)
+            rz = 1;
+          else
+            sp = (uint64_t)(a.ring[src][slot_idx] +
+                            ((((uint64_t)lk * 2 + c) * (uint64_t)a.nh + hh) * (uint64_t)a.total_tokens +
+                             (uint64_t)(tok0 + t)) * (uint64_t)a.D * Tr<DT>::B);
+        }
+        stream_rows<DT, DT, U, 8, true>(lane, cs, sp, dp, 1.f, rz);
+      }
+      // the warp that completes chunk k releases its ring slot to every source
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        const uint32_t cnt = end - base;
+        if (atomicAdd(done + k, cnt) + cnt == n_k) {
+          __threadfence_system();
+          for (int s = 0; s < a.nsrc; ++s)
+            asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.freef[s]), "r"(a.seq0 + (uint32_t)k + 1u)
+                         : "memory");
+        }
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // K2: pack (Fig. 5 flatten) -- wire order (layer, K/V, head in overlap, token, dim)
 // ------------------------------------------------------------------------------------
 template <int VEC, int SDT, int WDT, int U>
@@ -1234,6 +1360,45 @@ cudaError_t launch_tile_copy(const TileArgs& a, cudaStream_t s) {
   k_tile_copy<<<grid, 32, smem, s>>>(a);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
+}
+
+namespace {
+template <int DT>
+cudaError_t pull_rows_t(PullArgs& a, cudaStream_t s) {
+  constexpr int U = unroll_for<DT, 8>();
+  auto k = k_pull_rows<DT, U>;
+  // no co-residency needed: a warp only waits for chunk k holding items it grabbed from k,
+  // and the slots chunk k waits on are freed by items already grabbed (hence resident)
+  k<<<grid_for_items(k, a.items_full > a.items_last ? a.items_full : a.items_last), kThreads, 0, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+}  // namespace
+
+cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s) {
+  if (a.nchunks <= 0) return cudaSuccess;
+  cudaError_t e0 = cudaMemsetAsync(a.counters, 0, 2 * sizeof(uint32_t) * (size_t)a.nchunks, s);
+  if (e0 != cudaSuccess) return e0;
+  a.cpr_shift = log2_pow2((uint32_t)(a.D / 8));
+  uint32_t ts, th;
+  subtile_shape((uint32_t)a.Bd, (uint32_t)a.nh, &ts, &th);
+  a.ts_log2 = log2_pow2(ts);
+  const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.nh + th - 1) / th;
+  a.f_sb = make_fastdiv(nsb);
+  a.f_items = make_fastdiv(nsb * nhb);
+  const uint32_t per_layer = a.f_src.d * 2u * nsb * nhb * a.n_blk;
+  const uint32_t nl_last = (uint32_t)(a.le - a.lb - (a.nchunks - 1) * a.step);
+  a.items_last = per_layer * nl_last;
+  a.items_full = per_layer * (uint32_t)a.step;
+  a.f_l_full = make_fastdiv((uint32_t)a.step);
+  a.f_l_last = make_fastdiv(nl_last);
+  switch (dt) {
+    case KV_F16: return pull_rows_t<KV_F16>(a, s);
+    case KV_BF16: return pull_rows_t<KV_BF16>(a, s);
+    case KV_F8E4M3: return pull_rows_t<KV_F8E4M3>(a, s);
+    case KV_F32: return pull_rows_t<KV_F32>(a, s);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) {

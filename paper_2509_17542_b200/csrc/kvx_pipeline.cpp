@@ -4,6 +4,13 @@
 //                      one release flag per D rank (A11).
 //   kv_send_pipelined  NCCL mode, P side: pack chunk k+1 while chunk k is on the wire.
 //   kv_recv_pipelined  NCCL mode, D side: receive chunk k+1 while chunk k is unpacked.
+//   kv_pull            D-initiated read: wait for every source's ready flag, then
+//                      kv_convert_reshard per layer chunk with the P pools peer-mapped as
+//                      sources (NVLink reads), then a done flag back to each P rank.
+//   kv_stage           narrowing pull, P side: per chunk, wait for a free ring slot, kv_pack
+//                      (the sender-side cast) into it, release a ready flag to the D rank.
+//   kv_pull_staged     narrowing pull, D side: per chunk, wait for the ready flags, kv_unpack
+//                      straight from the peer-mapped ring slots, release the slots.
 #include <nccl.h>
 
 #include <algorithm>
@@ -165,6 +172,116 @@ kv_status kv_recv_pipelined(kv_comm* comm, int32_t n_src, const kv_layout* const
     }
   }
   return join(s, E.ev[1], E.ev[2], rs, us);
+}
+
+kv_status kv_pull(int32_t n_src, const kv_layout* const* src, const void* const* src_pools, const kv_batch* src_bt,
+                  const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt, const uint32_t* const* ready_flags,
+                  uint32_t* const* done_flags, uint32_t epoch, int32_t lb, int32_t le, int32_t layer_chunk,
+                  uint64_t timeout_ns, int32_t* err, kv_stream stream) {
+  if (n_src < 1 || !ready_flags || !done_flags || !err) return fail(KV_EINVAL, "kv_pull: bad argument");
+  for (int i = 0; i < n_src; ++i)
+    if (!ready_flags[i] || !done_flags[i]) return fail(KV_EINVAL, "kv_pull: null flag");
+  const kv_layout* const D[1] = {dst};
+  void* const DP[1] = {dst_pool};
+  // validate everything before the first enqueue (empty ranges validate and return)
+  kv_status st = kv_convert_reshard(n_src, src, src_pools, src_bt, 1, D, DP, dst_bt, lb, lb, stream);
+  if (st != KV_OK) return st;
+  if ((st = kv_convert_reshard(n_src, src, src_pools, src_bt, 1, D, DP, dst_bt, le, le, stream)) != KV_OK) return st;
+  for (int i = 0; i < n_src; ++i)
+    if ((st = kv_wait(ready_flags[i], epoch, timeout_ns, err, stream)) != KV_OK) return st;
+  const int32_t step = layer_chunk > 0 ? layer_chunk : std::max(1, le - lb);
+  for (int32_t l0 = lb; l0 < le; l0 += step)
+    if ((st = kv_convert_reshard(n_src, src, src_pools, src_bt, 1, D, DP, dst_bt, l0, std::min(le, l0 + step),
+                                 stream)) != KV_OK)
+      return st;
+  for (int i = 0; i < n_src; ++i)
+    if ((st = kv_signal(done_flags[i], epoch, stream)) != KV_OK) return st;
+  return KV_OK;
+}
+
+namespace {
+// ring slot of global chunk sequence number `seq` (0-based) and the free-count it needs
+inline int32_t ring_slot(uint64_t seq, int32_t R) { return (int32_t)(seq % (uint64_t)R); }
+}  // namespace
+
+kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, int32_t n_dst,
+                   const kv_layout* const* dst, void* const* rings, int32_t ring_slots, size_t slot_bytes,
+                   uint32_t* const* ready_flags, const uint32_t* const* free_flags, uint32_t seq0, int32_t lb,
+                   int32_t le, int32_t layer_chunk, uint64_t timeout_ns, int32_t* err, kv_stream stream) {
+  if (!src || !src_bt || !dst || n_dst < 1 || !rings || ring_slots < 1 || !ready_flags || !free_flags || !err)
+    return fail(KV_EINVAL, "kv_stage: bad argument");
+  for (int i = 0; i < n_dst; ++i) {
+    if (!ready_flags[i] || !free_flags[i]) return fail(KV_EINVAL, "kv_stage: null flag");
+    for (int b = 0; b < ring_slots; ++b)
+      if (!rings[(size_t)i * ring_slots + b]) return fail(KV_EINVAL, "kv_stage: null ring slot");
+  }
+  const int32_t step = layer_chunk > 0 ? layer_chunk : std::max(1, le - lb);
+  for (int32_t l0 = lb; l0 < le; l0 += step)
+    for (int i = 0; i < n_dst; ++i)
+      if (kv_wire_bytes(src, dst[i], src_bt->total_tokens, l0, std::min(le, l0 + step)) > slot_bytes)
+        return fail(KV_ESHAPE, "kv_stage: ring slots smaller than a layer chunk");
+  kv_status st;
+  uint64_t seq = seq0;
+  for (int32_t l0 = lb; l0 < le; l0 += step, ++seq) {
+    const int32_t l1 = std::min(le, l0 + step), b = ring_slot(seq, ring_slots);
+    for (int i = 0; i < n_dst; ++i) {
+      // slot b last held chunk seq - R: the D rank must have released it (free >= seq - R + 1)
+      if (seq + 1 > (uint64_t)ring_slots &&
+          (st = kv_wait(free_flags[i], (uint32_t)(seq + 1 - ring_slots), timeout_ns, err, stream)) != KV_OK)
+        return st;
+      if ((st = kv_pack(src, src_pool, src_bt, dst[i], l0, l1, rings[(size_t)i * ring_slots + b], slot_bytes,
+                        stream)) != KV_OK)
+        return st;
+    }
+    for (int i = 0; i < n_dst; ++i)
+      if ((st = kv_signal(ready_flags[i], (uint32_t)(seq + 1), stream)) != KV_OK) return st;
+  }
+  return KV_OK;
+}
+
+kv_status kv_pull_staged(int32_t n_src, const kv_layout* const* src, const void* const* rings, int32_t ring_slots,
+                         size_t slot_bytes, const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt,
+                         const uint32_t* const* ready_flags, uint32_t* const* free_flags, uint32_t* counters,
+                         uint32_t seq0, int32_t lb, int32_t le, int32_t layer_chunk, uint64_t timeout_ns, int32_t* err,
+                         kv_stream stream) {
+  if (n_src < 1 || !src || !rings || ring_slots < 1 || !dst || !dst_bt || !ready_flags || !free_flags || !err)
+    return fail(KV_EINVAL, "kv_pull_staged: bad argument");
+  for (int i = 0; i < n_src; ++i) {
+    if (!ready_flags[i] || !free_flags[i]) return fail(KV_EINVAL, "kv_pull_staged: null flag");
+    for (int b = 0; b < ring_slots; ++b)
+      if (!rings[(size_t)i * ring_slots + b]) return fail(KV_EINVAL, "kv_pull_staged: null ring slot");
+  }
+  const int32_t step = layer_chunk > 0 ? layer_chunk : std::max(1, le - lb);
+  for (int32_t l0 = lb; l0 < le; l0 += step)
+    for (int i = 0; i < n_src; ++i)
+      if (kv_wire_bytes(src[i], dst, dst_bt->total_tokens, l0, std::min(le, l0 + step)) > slot_bytes)
+        return fail(KV_ESHAPE, "kv_pull_staged: ring slots smaller than a layer chunk");
+  for (int i = 0; i < n_src; ++i) {  // validate the unpacks once (empty ranges)
+    kv_status v = kv_unpack(src[i], dst, dst_pool, dst_bt, lb, lb, rings[(size_t)i * ring_slots], slot_bytes, stream);
+    if (v != KV_OK) return v;
+    if ((v = kv_unpack(src[i], dst, dst_pool, dst_bt, le, le, rings[(size_t)i * ring_slots], slot_bytes, stream)) !=
+        KV_OK)
+      return v;
+  }
+  bool used = false;
+  kv_status st = pull_rows_fast(n_src, src, rings, ring_slots, dst, dst_pool, dst_bt, ready_flags, free_flags,
+                                counters, seq0, lb, le, step, timeout_ns, err, stream, &used);
+  if (st != KV_OK || used) return st;
+  uint64_t seq = seq0;
+  for (int32_t l0 = lb; l0 < le; l0 += step, ++seq) {
+    const int32_t l1 = std::min(le, l0 + step), b = ring_slot(seq, ring_slots);
+    for (int i = 0; i < n_src; ++i)
+      if ((st = kv_wait(ready_flags[i], (uint32_t)(seq + 1), timeout_ns, err, stream)) != KV_OK) return st;
+    for (int i = 0; i < n_src; ++i) {
+      const size_t nb = kv_wire_bytes(src[i], dst, dst_bt->total_tokens, l0, l1);
+      if ((st = kv_unpack(src[i], dst, dst_pool, dst_bt, l0, l1, rings[(size_t)i * ring_slots + b], nb, stream)) !=
+          KV_OK)
+        return st;
+    }
+    for (int i = 0; i < n_src; ++i)
+      if ((st = kv_signal(free_flags[i], (uint32_t)(seq + 1), stream)) != KV_OK) return st;
+  }
+  return KV_OK;
 }
 
 }  // extern "C"

@@ -12,7 +12,7 @@ from contextlib import contextmanager
 from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BYTES, KV_BF16, KV_F8E4M3, KV_F16,
                    KV_F32, Batch_t, KvError, LayoutDesc, check, lib)
 
-__all__ = ["Layout", "Batch", "convert_reshard", "convert_share", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
+__all__ = ["Layout", "Batch", "convert_reshard", "convert_share", "push", "pull", "stage", "pull_staged", "chunk_count", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
            "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "launch_count", "launch_count_reset", "set_sm_budget", "last_kernel",
            "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "DTYPE_BYTES",
            "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
@@ -167,6 +167,60 @@ def push(src_layout, src_pool, src_batch: Batch, dst_layouts, dst_pools, dst_bat
     lb, le = layer_range if layer_range else _common(src_layout, dst_layouts[0])
     check(lib.kv_push(src_layout.handle, _ptr(src_pool), C.byref(src_batch.bt), nd, Dl, DP, C.byref(dst_batch.bt),
                       FL, epoch, lb, le, layer_chunk, _stream(stream)))
+
+
+def pull(src_layouts, src_pools, src_batch: Batch, dst_layout: Layout, dst_pool, dst_batch: Batch, ready_flags,
+         done_flags, epoch, err, layer_range=None, layer_chunk=0, timeout_s=30.0, stream=None):
+    """kv_pull: D side of the D-initiated read -- wait for every P rank's ready
+    flag, convert_reshard from the peer-mapped P pools into the local D pool per layer
+    chunk, then a done flag back into each P rank's memory."""
+    ns = len(src_layouts)
+    S = (C.c_void_p * ns)(*[l.handle.value for l in src_layouts])
+    SP = (C.c_void_p * ns)(*[_ptr(p) for p in src_pools])
+    RF = (C.c_void_p * ns)(*[_ptr(f) for f in ready_flags])
+    DF = (C.c_void_p * ns)(*[_ptr(f) for f in done_flags])
+    lb, le = layer_range if layer_range else _common(src_layouts[0], dst_layout)
+    check(lib.kv_pull(ns, S, SP, C.byref(src_batch.bt), dst_layout.handle, _ptr(dst_pool), C.byref(dst_batch.bt),
+                      RF, DF, epoch, lb, le, layer_chunk, int(timeout_s * 1e9), _ptr(err), _stream(stream)))
+
+
+def stage(src_layout, src_pool, src_batch: Batch, dst_layouts, rings, ring_slots, slot_bytes, ready_flags,
+          free_flags, seq0, err, layer_range=None, layer_chunk=0, timeout_s=30.0, stream=None):
+    """kv_stage: P side of a narrowing pull -- pack (sender-side cast) each layer chunk
+    into ring slot seq % ring_slots of every D rank once D freed it, then signal ready.
+    rings: flat list, rings[i * ring_slots + b] = slot b for D rank i."""
+    nd = len(dst_layouts)
+    Dl = (C.c_void_p * nd)(*[l.handle.value for l in dst_layouts])
+    RG = (C.c_void_p * len(rings))(*[_ptr(r) for r in rings])
+    RF = (C.c_void_p * nd)(*[_ptr(f) for f in ready_flags])
+    FF = (C.c_void_p * nd)(*[_ptr(f) for f in free_flags])
+    lb, le = layer_range if layer_range else _common(src_layout, dst_layouts[0])
+    check(lib.kv_stage(src_layout.handle, _ptr(src_pool), C.byref(src_batch.bt), nd, Dl, RG, ring_slots, slot_bytes,
+                       RF, FF, seq0, lb, le, layer_chunk, int(timeout_s * 1e9), _ptr(err), _stream(stream)))
+
+
+def pull_staged(src_layouts, rings, ring_slots, slot_bytes, dst_layout: Layout, dst_pool, dst_batch: Batch,
+                ready_flags, free_flags, seq0, err, layer_range=None, layer_chunk=0, timeout_s=30.0, stream=None,
+                counters=None):
+    """kv_pull_staged: D side of a narrowing pull -- per layer chunk wait for every P
+    rank's ready flag, unpack straight from its peer-mapped ring slot, free the slot.
+    counters (device uint32/int32 scratch, >= 2 * chunk_count words): one persistent launch."""
+    ns = len(src_layouts)
+    S = (C.c_void_p * ns)(*[l.handle.value for l in src_layouts])
+    RG = (C.c_void_p * len(rings))(*[_ptr(r) for r in rings])
+    RF = (C.c_void_p * ns)(*[_ptr(f) for f in ready_flags])
+    FF = (C.c_void_p * ns)(*[_ptr(f) for f in free_flags])
+    lb, le = layer_range if layer_range else _common(src_layouts[0], dst_layout)
+    check(lib.kv_pull_staged(ns, S, RG, ring_slots, slot_bytes, dst_layout.handle, _ptr(dst_pool),
+                             C.byref(dst_batch.bt), RF, FF, _ptr(counters), seq0, lb, le, layer_chunk,
+                             int(timeout_s * 1e9), _ptr(err), _stream(stream)))
+
+
+def chunk_count(layer_range, layer_chunk):
+    """Chunks a kv_stage / kv_pull_staged call over layer_range takes (seq0 advances by it)."""
+    lb, le = layer_range
+    step = layer_chunk if layer_chunk > 0 else max(1, le - lb)
+    return (le - lb + step - 1) // step
 
 
 def compute_scales(src_layouts, src_pools, src_batch: Batch, dst_layout: Layout, out, layer_range=None, stream=None):

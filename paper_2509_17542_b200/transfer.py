@@ -8,6 +8,14 @@ exchange and the two data-plane modes.
   system-scope release.  The D rank ``wait``s (acquire) on its local flag.  The cast
   happens on the sender, so a narrowing cast halves the NVLink bytes (hard
   part 2).  D keeps control of placement: its block table travels to P (A3).
+* ``pull`` (the paper's direction, "read(local, remote, location)"): each P rank
+  exports its pool (same-width / widening cast) or a staging ring (narrowing cast) plus a
+  flag array; each D rank maps them and reads across NVLink.  Without narrowing, D runs
+  ``kv.pull`` -- one convert_reshard per layer chunk with the peer-mapped P pools as
+  sources -- after P's ready flag, then releases P with a done flag.  With narrowing, P
+  ``kv.stage``s (packs + casts) each layer chunk into a ring slot and D ``kv.pull_staged``s
+  it (unpack reading the peer slot), so the link carries the narrow bytes.  SM loads from
+  a peer move more user bytes per second than SM stores to a peer.
 * ``nccl`` (baseline): P ``pack``s each pair's share into a wire buffer (canonical
   Fig. 5 order), ``Comm.send``s it; D ``recv``s and ``unpack``s; per-layer chunks are
   pipelined on two streams (pack chunk k+1 while chunk k is on the wire).
@@ -91,6 +99,63 @@ class PushChannel:
                 self.peer_pool[q] = ipc_open(*ent["pool"])
                 self.peer_flag[q] = ipc_open(*ent["flag"])
                 self._mapped += [(self.peer_pool[q], ent["pool"][1]), (self.peer_flag[q], ent["flag"][1])]
+
+    def close(self):
+        for ptr, off in self._mapped:
+            kv.ipc_close(ptr, off)
+        self._mapped = []
+
+
+class PullChannel:
+    """IPC maps for the D-initiated read (kv_pull / kv_stage + kv_pull_staged).
+
+    Collective.  Every rank passes its role and a local int32 flag array: on a D rank one
+    ready word per P rank (P writes it), on a P rank one done / free word per D rank (D
+    writes it).  P ranks also pass ``pool`` (direct pull) or ``ring`` (a uint8 tensor of
+    len(ring_dst) * ring_slots * slot_bytes bytes; slot b for D rank ring_dst[i] starts at
+    (i * ring_slots + b) * slot_bytes).  Afterwards a D rank holds, per P rank p,
+    ``src_pool[p]`` / ``src_ring[p]`` (its ring_slots slot addresses) and ``peer_flag[p]``
+    (the word it signals in p's flag array); a P rank holds ``peer_flag[q]`` per D rank q."""
+
+    def __init__(self, role: Role, flags, pool=None, ring=None, ring_dst=(), ring_slots=0, slot_bytes=0,
+                 group=None, ipc_export=None, ipc_open=None):
+        ipc_export = ipc_export or kv.ipc_export
+        ipc_open = ipc_open or kv.ipc_open
+        mine = {"kind": role.kind, "r": role.tp_rank, "flags": ipc_export(flags) if role.kind in "PD" else None,
+                "pool": ipc_export(pool) if pool is not None else None,
+                "ring": ipc_export(ring) if ring is not None else None, "ring_dst": list(ring_dst),
+                "ring_slots": ring_slots, "slot_bytes": slot_bytes}
+        allv = exchange(mine, group)
+        self.role = role
+        self.src_pool, self.src_ring, self.peer_flag, self._mapped = {}, {}, {}, []
+        self.slot_bytes = {}   # D side: P rank p's ring slot size
+        if role.kind not in "PD":
+            return
+        other = "P" if role.kind == "D" else "D"
+        for ent in allv:
+            if ent["kind"] != other:
+                continue
+            if role.kind == "P":
+                # my word in D rank q's ready array is index p
+                base = ipc_open(*ent["flags"])
+                self._mapped.append((base, ent["flags"][1]))
+                self.peer_flag[ent["r"]] = base + 4 * role.tp_rank
+                continue
+            p, q = ent["r"], role.tp_rank
+            if ent["pool"] is None and (ent["ring"] is None or q not in ent["ring_dst"]):
+                continue
+            base = ipc_open(*ent["flags"])
+            self._mapped.append((base, ent["flags"][1]))
+            self.peer_flag[p] = base + 4 * q
+            if ent["pool"] is not None:
+                self.src_pool[p] = ipc_open(*ent["pool"])
+                self._mapped.append((self.src_pool[p], ent["pool"][1]))
+            if ent["ring"] is not None:
+                rb = ipc_open(*ent["ring"])
+                self._mapped.append((rb, ent["ring"][1]))
+                i, R, sb = ent["ring_dst"].index(q), ent["ring_slots"], ent["slot_bytes"]
+                self.src_ring[p] = [rb + (i * R + b) * sb for b in range(R)]
+                self.slot_bytes[p] = sb
 
     def close(self):
         for ptr, off in self._mapped:

@@ -2,7 +2,12 @@
 process each.  Both transports against the oracle:
   * push: the fused convert kernel stores into the D pools mapped through CUDA IPC, then
     a release flag; D acquires it and checks its pools;
-  * nccl: kv_pack -> ncclSend / ncclRecv -> kv_unpack per (p, q) pair and layer chunk.
+  * nccl: kv_pack -> ncclSend / ncclRecv -> kv_unpack per (p, q) pair and layer chunk;
+  * pull: D maps the P pools through CUDA IPC and kv_pull reads them after P's ready flag;
+  * pull_staged: P kv_stage-s layer chunks into 2-slot rings, D kv_pull_staged-s them from
+    the peer-mapped slots (4 chunks: every slot is reused behind a free flag) -- one
+    persistent k_pull_rows launch with chunk counters, or (pull_staged_chunked) one
+    wait / unpack / signal triple per chunk.
 Control plane: a gloo process group (object exchange)."""
 import os
 import pickle
@@ -57,6 +62,8 @@ def _worker(rank, port, blob, mode, q):
                 assert int(err.item()) == 0, "flag wait timed out"
                 q.put((rank, [a.copy() for a in dc.dst_numpy()]))
                 dist.barrier()
+        elif mode.startswith("pull"):
+            _pull_worker(rank, dc, kvx, tr, dist, q, mode.startswith("pull_staged"), mode == "pull_staged")
         else:
             uid = kvx.Comm.unique_id() if rank == 0 else None
             lst = [uid]
@@ -82,7 +89,88 @@ def _worker(rank, port, blob, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("mode", ["push", "nccl"])
+def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent):
+    """P = rank 0 (all P ranks, one stream each), D = rank 1 (all D ranks, one stream each).
+    Flag words: D's ready[q * 8 + p] (P writes), P's done / free[p * 8 + q] (D writes)."""
+    dev = f"cuda:{rank}"
+    flags = torch.zeros(64, dtype=torch.int32, device=dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    S, D = dc.src_lays, dc.dst_lays
+    pairs = kvx.plan_pairs(S[0].tp_degree, D[0].tp_degree, S[0].num_kv_heads)
+    L = S[0].num_layers
+    R, lc = 2, 1
+    nb = 0
+    for p, qq, _, _ in pairs:
+        nb = max(nb, max(kvx.wire_bytes(S[p], D[qq], dc.src_bt.total_tokens, (l, l + 1)) for l in range(L)))
+    rings = {}
+    if rank == 0 and staged:
+        for p, qq, _, _ in pairs:
+            rings[(p, qq)] = torch.empty(R * nb, dtype=torch.uint8, device=dev)
+    exp = {"flags": kvx.ipc_export(flags)}
+    if rank == 0:
+        exp["src"] = {k: kvx.ipc_export(v) for k, v in rings.items()} if staged else \
+            [kvx.ipc_export(pl) for pl in dc.src_pools]
+    allx = tr.exchange(exp)
+    other = allx[1 - rank]
+    fbase = kvx.ipc_open(*other["flags"])
+    maps = [(fbase, other["flags"][1])]
+    streams = {}
+    if rank == 0:
+        for p in range(len(S)):
+            qs = [qq for pp, qq, _, _ in pairs if pp == p]
+            st = streams[p] = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                if staged:
+                    kvx.stage(S[p], dc.src_pools[p], dc.src_bt, [D[qq] for qq in qs],
+                              [rings[(p, qq)].data_ptr() + b * nb for qq in qs for b in range(R)], R, nb,
+                              [fbase + 4 * (qq * 8 + p) for qq in qs], [flags[p * 8 + qq:p * 8 + qq + 1] for qq in qs],
+                              0, err, (0, L), lc, 20.0, st)
+                    for qq in qs:   # all chunks consumed: free >= number of chunks
+                        kvx.wait(flags[p * 8 + qq:p * 8 + qq + 1], L, err, 20.0, st)
+                else:
+                    for qq in qs:
+                        kvx.signal(fbase + 4 * (qq * 8 + p), 1, st)
+                    for qq in qs:
+                        kvx.wait(flags[p * 8 + qq:p * 8 + qq + 1], 1, err, 20.0, st)
+        torch.cuda.synchronize()
+        assert int(err.item()) == 0, "P-side wait timed out"
+        dist.barrier()
+        q.put((rank, None))
+    else:
+        if staged:
+            src = {k: kvx.ipc_open(h, o) for k, (h, o) in other["src"].items()}
+            maps += [(src[k], other["src"][k][1]) for k in src]
+        else:
+            src = [kvx.ipc_open(h, o) for h, o in other["src"]]
+            maps += [(a, o) for a, (h, o) in zip(src, other["src"])]
+        counters = {qq: torch.zeros(2 * L, dtype=torch.int32, device=dev) for qq in range(len(D))}
+        for qq in range(len(D)):
+            ps = [pp for pp, q2, _, _ in pairs if q2 == qq]
+            st = streams[qq] = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                if staged:
+                    kvx.pull_staged([S[p] for p in ps], [src[(p, qq)] + b * nb for p in ps for b in range(R)], R, nb,
+                                    D[qq], dc.dst_pools[qq], dc.dst_bt, [flags[qq * 8 + p:qq * 8 + p + 1] for p in ps],
+                                    [fbase + 4 * (p * 8 + qq) for p in ps], 0, err, (0, L), lc, 20.0, st,
+                                    counters=counters[qq] if persistent else None)
+                else:
+                    kvx.pull([S[p] for p in ps], [src[p] for p in ps], dc.src_bt, D[qq], dc.dst_pools[qq], dc.dst_bt,
+                             [flags[qq * 8 + p:qq * 8 + p + 1] for p in ps], [fbase + 4 * (p * 8 + qq) for p in ps],
+                             1, err, (0, L), lc, 20.0, st)
+        torch.cuda.synchronize()
+        assert int(err.item()) == 0, "D-side wait timed out"
+        assert kvx.last_kernel() == ("k_pull_rows" if persistent else "k_unpack_rows" if staged else kvx.last_kernel())
+        if persistent:   # every chunk handed out and completed in full
+            for c in counters.values():
+                nxt, done = c[:L].cpu(), c[L:].cpu()
+                assert bool((done > 0).all()) and bool((nxt >= done).all())
+        q.put((rank, [a.copy() for a in dc.dst_numpy()]))
+        dist.barrier()
+    for a, o in maps:
+        kvx.ipc_close(a, o)
+
+
+@pytest.mark.parametrize("mode", ["push", "nccl", "pull", "pull_staged", "pull_staged_chunked"])
 @pytest.mark.parametrize("shape", ["merge", "split_fp8"])
 def test_p_to_d_across_gpus(o1, mode, shape):
     if torch.cuda.device_count() < 2:

@@ -107,3 +107,63 @@ def test_present_ranks_sub_transfers():
                 assert heads_needed <= set(range(n_p))
     r = tr.roles(4, 2, 1, allow_idle=True)
     assert [x.kind for x in r] == ["P", "P", "D", "X"]
+
+
+def _pull_worker(rank, world, port, q, staged):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2509_17542_b200 import transfer as tr
+        n_p = world - 1
+        me = tr.roles(world, n_p, 1)[rank]   # fan-in: P0..P{n_p-1} -> D0 (c2 / c3' shape)
+        exported = []
+
+        def fake_export(t):
+            exported.append(t)
+            return (bytes([rank]) * 64, 100 * len(exported))
+
+        def fake_open(handle, off):
+            return 0x7000_0000 + handle[0] * 0x100000 + off
+
+        kw = {}
+        if me.kind == "P":
+            kw = dict(ring="ring", ring_dst=[0], ring_slots=2, slot_bytes=1000) if staged else dict(pool="pool")
+        ch = tr.PullChannel(me, "flags", ipc_export=fake_export, ipc_open=fake_open, **kw)
+        q.put((rank, me.kind, me.tp_rank, exported, ch.src_pool, ch.src_ring, ch.peer_flag))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,staged", [(2, False), (3, False), (3, True)])
+def test_pull_channel_exchange(world, staged):
+    """PullChannel: D maps every P rank's pool (or its ring slots for this D rank) and the
+    word it owns in P's flag array; P maps its word in D's ready array."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pull_worker, args=(r, world, port, q, staged)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n_p = world - 1
+    d_rank = n_p
+    for rank, kind, tpr, exported, src_pool, src_ring, peer_flag in res:
+        if kind == "P":
+            assert exported == ["flags", "ring" if staged else "pool"]
+            # P rank tpr signals word tpr of D0's ready array (D exported flags at offset 100)
+            assert peer_flag == {0: 0x7000_0000 + d_rank * 0x100000 + 100 + 4 * tpr}
+            assert src_pool == {} and src_ring == {}
+        else:
+            assert exported == ["flags"]
+            assert sorted(peer_flag) == list(range(n_p))
+            for p in range(n_p):
+                base = 0x7000_0000 + p * 0x100000
+                assert peer_flag[p] == base + 100 + 4 * 0   # D0's word in P's done/free array
+                if staged:
+                    assert src_pool == {}
+                    assert src_ring[p] == [base + 200 + b * 1000 for b in range(2)]
+                else:
+                    assert src_pool[p] == base + 200 and src_ring == {}

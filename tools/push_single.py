@@ -27,6 +27,8 @@ def main():
     ap.add_argument("--copy", action="store_true", help="also time a cudaMemcpyPeer-style torch copy 0 -> 1")
     ap.add_argument("--layer-chunk", type=int, default=0)
     ap.add_argument("--budgets", default="0", help="comma list of SM budgets to sweep (0 = all SMs)")
+    ap.add_argument("--pull", action="store_true",
+                    help="D-initiated read (the paper's direction): the kernel runs on cuda:1 and loads from cuda:0")
     ap.add_argument("--dst-dtype", default="", help="override the destination dtype (f16|bf16|e4m3|f32)")
     args = ap.parse_args()
     import paper_2509_17542_b200 as kvx
@@ -48,32 +50,51 @@ def main():
     Dl = kvx.Layout.from_dict(dst.dst_dicts[0], None if sc is None else torch.from_numpy(sc).to("cuda:0"))
     lc = args.layer_chunk or cfg.L
 
-    def fn():
-        for l0 in range(0, cfg.L, lc):
-            kvx.convert_reshard([S], [SP], src.src_bt, [Dl], [DP], src.dst_bt, (l0, min(cfg.L, l0 + lc)))
+    dev = 0
+    if args.pull:
+        torch.cuda.set_device(1)
+        kvx.peer_enable(0)
+        torch.cuda.set_device(0)
+        dev, Dl = 1, dst.dst_lays[0]
 
-    nvl = dst.dst_bytes([0])
+    def fn():
+        with torch.cuda.device(dev):
+            for l0 in range(0, cfg.L, lc):
+                if args.pull:
+                    kvx.convert_share(S, SP, dst.src_bt, [Dl], [DP], dst.dst_bt, (l0, min(cfg.L, l0 + lc)))
+                else:
+                    kvx.convert_share(S, SP, src.src_bt, [Dl], [DP], src.dst_bt, (l0, min(cfg.L, l0 + lc)))
+
+    # P rank 0's share of D rank 0 (all of it when tp_p <= tp_d; half of c2's fan-in 2)
+    nvl = src.src_bytes([0]) * synth.NBYTES[cfg.dst_dtype] // synth.NBYTES[cfg.src_dtype]
+    whole = cfg.tp_p <= cfg.tp_d
     for budget in [int(x) for x in args.budgets.split(",")]:
         kvx.set_sm_budget(budget)
         for _ in range(3):
             fn()
         torch.cuda.synchronize(0)
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.iters)]
-        for a, b in ev:
-            a.record()
-            fn()
-            b.record()
-        torch.cuda.synchronize(0)
+        torch.cuda.synchronize(1)
+        with torch.cuda.device(dev):
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                  for _ in range(args.iters)]
+            for a, b in ev:
+                a.record()
+                fn()
+                b.record()
+        torch.cuda.synchronize(dev)
         ts = [a.elapsed_time(b) for a, b in ev]
         med = statistics.median(ts)
-        out = {"case": f"{args.workload} pair push cuda:0 -> cuda:1", "sm_budget": budget or "all",
+        out = {"case": f"{args.workload} pair {'pull (kernel on cuda:1)' if args.pull else 'push'} cuda:0 -> cuda:1", "sm_budget": budget or "all",
                "ms_med": round(med, 4), "ms_min": round(min(ts), 4),
                "nvlink_GBs": round(nvl / med / 1e6, 1), "frac_770": round(nvl / med / 1e6 / 770, 4),
                "src_GBs": round(src.src_bytes([0]) / med / 1e6, 1), "nvlink_bytes": nvl, "layer_chunk": lc}
         torch.cuda.synchronize(1)
         dst.src_pools[0], dst.src_dicts[0] = SP, src.src_dicts[0]
-        ok, det = sample_parity(dst, (0, 1), 0, [0], [0])
-        out["parity_ok"] = ok
+        out["kernel"] = kvx.last_kernel()
+        out["tile_env"] = os.environ.get("KVX_TILE", "1")
+        if whole:
+            ok, det = sample_parity(dst, (0, 1), 0, [0], [0])
+            out["parity_ok"] = ok
         print(json.dumps(out), flush=True)
     kvx.set_sm_budget(0)
     if args.copy:
