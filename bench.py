@@ -334,7 +334,7 @@ def run_single(args):
                    "src_bytes_per_step": src_b, "dst_bytes_per_step": dst_b,
                    "l2": "inputs larger than L2 (no flush)", "parallelism": "none (1 GPU)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _traffic(wl_name, 1),
+                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _traffic(f"{wl_name}@1"),
                      "kernel": kvx.last_kernel(), "kernel_ms": round(kern_ms, 5),
                      "algorithmic_bytes_per_launch": alg, "peak_source": peaks["source"],
                      "frac_vs_nominal_8TBs": round(achieved / 8000.0, 4)},
@@ -408,12 +408,13 @@ def _dtype_name(cfg):
     return a if a == b else f"{a}->{b}"
 
 
-def _traffic(workload, n):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture."""
+def _traffic(key):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture
+    (profiles/traffic.json: "c2@1" single GPU, "<workload>:<mode>" for the NVLink modes)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
         with open(p) as f:
-            return json.load(f).get(f"{workload}@{n}")
+            return json.load(f).get(key)
     return None
 
 
@@ -644,7 +645,7 @@ def run_multi(args):
                        "parallelism": f"P TP{cfg.tp_p} x D TP{cfg.tp_d}, {n_p}+{n_d} ranks present"},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED_GBS,
                          "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED_GBS, 4),
-                         "traffic": _traffic(wl_name, world) if args.mode == "push" else None,
+                         "traffic": _traffic(f"{wl_name}:{args.mode}"),
                          "kernel": f"{[x['kernel'] for x in sts if x['kind'] == 'P'][0]} (peer-store push)"
                          if args.mode == "push"
                          else f"{[x['kernel'] for x in sts if x['kind'] == 'D'][0]} (peer-load pull on D)"
@@ -777,17 +778,97 @@ def run_stream(args):
     flags = torch.zeros(max(n_p, 1) * 8, dtype=torch.int32, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     mine = None
-    if not is_p:
+    pull = args.mode == "pull"
+
+    def inst_setup(inst):
+        """P rank tables / layout of instance `inst` (rebuilt from the seeds on D in pull mode)."""
+        reqs = inst_req[inst]
+        icfg = dataclasses.replace(cfg, n_tokens=[cfg.n_tokens[r] for r in reqs], seed=cfg.seed + 10 * inst)
+        NB_p = synth.pool_capacity(icfg.n_tokens, cfg.B_p)
+        return reqs, icfg, NB_p, synth.block_tables(icfg.seed + 1, icfg.n_tokens, cfg.B_p, NB_p)
+
+    if pull:
+        if is_p:
+            inst, p = rank // per_inst, rank % per_inst
+            reqs, icfg, NB_p, src_tables = inst_setup(inst)
+            sd = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, NB_p, cfg.src_dtype, cfg.p_order)
+            spool = kvx.Layout.from_dict(sd).new_pool(dev)
+            synth.fill_random_finite_(spool.view(torch.int16), icfg.seed + 100 + p, cfg.src_dtype)
+            mine = {"kind": "P", "r": rank, "pool": kvx.ipc_export(spool), "flags": kvx.ipc_export(flags)}
+        else:
+            q = rank - n_p
+            dd = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, NB_d, cfg.dst_dtype, cfg.d_order)
+            dl = kvx.Layout.from_dict(dd)
+            pool = dl.new_pool(dev, fill=synth.CANARY)
+            mine = {"kind": "D", "r": q, "flags": kvx.ipc_export(flags)}
+    elif not is_p:
         q = rank - n_p
         dd = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, NB_d, cfg.dst_dtype, cfg.d_order)
         dl = kvx.Layout.from_dict(dd)
         pool = dl.new_pool(dev, fill=synth.CANARY)
         mine = {"q": q, "pool": kvx.ipc_export(pool), "flags": kvx.ipc_export(flags)}
     allx = tr.exchange(mine)
-    peers = {e["q"]: e for e in allx if e is not None}
+    peers = {e["q"]: e for e in allx if e is not None and "q" in e}
     src_bytes = 0
     lat = []
-    if is_p:
+    if pull and is_p:
+        # my KV is resident: release it to the D ranks, then wait until they have read it
+        d_flag = {e["r"]: kvx.ipc_open(*e["flags"]) + 4 * rank for e in allx if e["kind"] == "D"}
+        pairs = tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks={p}, d_ranks=set(d_ranks))
+        qs = [q for _, q, _, _ in pairs]
+        src_bytes = sum(cfg.L * 2 * cfg.D * (cfg.H // cfg.tp_p) * synth.NBYTES[cfg.src_dtype] * t
+                        for t in icfg.n_tokens)
+        count = [0]
+
+        def step(evs=None):
+            count[0] += 1
+            for q in qs:
+                kvx.signal(d_flag[q], count[0], stream)
+            for q in qs:
+                kvx.wait(flags[q:q + 1], count[0], err, 60.0, stream)
+        expected_per_step = 0
+    elif pull:
+        # D rank q: pull every request, in order, from the P rank of its instance holding q's heads
+        srcs = [pr for pr in range(n_p) if any(qq == q for _, qq, _, _ in
+                                               tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks={pr % per_inst}))]
+        p_ent = {e["r"]: e for e in allx if e["kind"] == "P"}
+        src_pool = {pr: kvx.ipc_open(*p_ent[pr]["pool"]) for pr in srcs}
+        p_flag = {pr: kvx.ipc_open(*p_ent[pr]["flags"]) + 4 * q for pr in srcs}
+        order = []   # (source P world rank, its layout, src Batch, dst Batch) per request, stream order
+        setups = {inst: inst_setup(inst) for inst in range(n_inst)}
+        for r in range(len(cfg.n_tokens)):
+            inst = r % n_inst if n_inst > 1 else 0
+            reqs, icfg, NB_p, src_tables = setups[inst]
+            i = reqs.index(r)
+            pr = [x for x in srcs if x // per_inst == inst][0]
+            sl = kvx.Layout.from_dict(synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, pr % per_inst, cfg.B_p, NB_p,
+                                                   cfg.src_dtype, cfg.p_order))
+            order.append((pr, sl, kvx.Batch(sl, [icfg.n_tokens[i]], [src_tables[i]], dev),
+                          kvx.Batch(dl, [cfg.n_tokens[r]], [dst_tables[r]], dev)))
+        count = [0]
+        # one stream per source P rank, each on its share of the SMs: D pulls the two
+        # instances' requests concurrently, so no P rank's egress carries two D ranks at once
+        side = {pr: torch.cuda.Stream() for pr in srcs}
+        if len(srcs) > 1:
+            kvx.set_sm_budget(torch.cuda.get_device_properties(dev).multi_processor_count // len(srcs))
+
+        def step(evs=None):
+            count[0] += 1
+            st = torch.cuda.Event()
+            st.record(stream)
+            for pr in srcs:
+                side[pr].wait_event(st)
+                kvx.wait(flags[pr:pr + 1], count[0], err, 60.0, side[pr])
+            for j, (pr, sl, sbt, dbt) in enumerate(order):
+                kvx.convert_reshard([sl], [src_pool[pr]], sbt, [dl], [pool], dbt, None, side[pr])
+                if evs is not None:
+                    evs[j].record(side[pr])
+            for pr in srcs:
+                kvx.signal(p_flag[pr], count[0], side[pr])
+                e = torch.cuda.Event()
+                e.record(side[pr])
+                stream.wait_event(e)
+    elif is_p:
         inst, p = rank // per_inst, rank % per_inst
         reqs = inst_req[inst]
         icfg = dataclasses.replace(cfg, n_tokens=[cfg.n_tokens[r] for r in reqs], seed=cfg.seed + 10 * inst)
@@ -855,7 +936,10 @@ def run_stream(args):
     torch.cuda.synchronize()
     dist.all_reduce(barrier_t)
     torch.cuda.synchronize()
-    nreq_mine = len(inst_req[rank // per_inst]) if is_p else 0
+    if pull:   # the D ranks run the data path: per-request completion events there
+        nreq_mine = len(cfg.n_tokens) if not is_p else 0
+    else:
+        nreq_mine = len(inst_req[rank // per_inst]) if is_p else 0
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nreq_mine)] for _ in range(K)]
     clocks = ClockSampler(local)
@@ -864,7 +948,7 @@ def run_stream(args):
     dist.all_reduce(barrier_t)
     t0.record(stream)
     for k in range(K):
-        step(evs[k] if is_p else None)
+        step(evs[k] if nreq_mine else None)
     t1.record(stream)
     torch.cuda.synchronize()
     clk = clocks.stop()
@@ -872,25 +956,32 @@ def run_stream(args):
     if int(err.item()):
         raise SystemExit(f"rank {rank}: flag wait timed out")
     my_ms = t0.elapsed_time(t1)
-    if is_p:
+    if nreq_mine:
         # latency of request i in step k = its completion - the step's start (previous step end)
         prev = t0
         for k in range(K):
             for i in range(nreq_mine):
                 lat.append(prev.elapsed_time(evs[k][i]))
-            prev = evs[k][-1] if nreq_mine else prev
+            prev = max(evs[k], key=lambda e: t0.elapsed_time(e))  # the step's last completion
     info = tr.exchange({"ms": my_ms, "src_bytes": src_bytes, "lat": lat, "launches": launches,
                         "nreq": nreq_mine})
     if rank == 0:
         max_ms = max(x["ms"] for x in info)
         ms = max_ms / K
         tot_b = sum(x["src_bytes"] for x in info)
-        nreq = sum(x["nreq"] for x in info) // max(per_inst, 1)
+        nreq = len(cfg.n_tokens) if pull else sum(x["nreq"] for x in info) // max(per_inst, 1)
         alll = sorted(l for x in info for l in x["lat"])
         # NVLink roofline: the busiest D rank's ingress (all its heads of every request moved)
-        d_in = 2 * cfg.L * (cfg.H // cfg.tp_d) * cfg.D * synth.NBYTES[cfg.dst_dtype] * sum(
-            synth.blocks_for(cfg.n_tokens[r], cfg.B_d) * cfg.B_d for i in range(n_inst) for r in inst_req[i])
-        t_roof = d_in / (NVLINK_MEASURED_GBS * 1e9) * 1e3
+        # NVLink bytes (wire dtype, valid tokens): each present D rank's ingress, and each P
+        # rank's egress to the present D ranks -- with unequal instance loads the busier P
+        # rank's egress, not a D rank's ingress, is the bound
+        per_head = 2 * cfg.L * cfg.D * min(synth.NBYTES[cfg.src_dtype], synth.NBYTES[cfg.dst_dtype])
+        d_in = per_head * (cfg.H // cfg.tp_d) * sum(cfg.n_tokens[r] for i in range(n_inst) for r in inst_req[i])
+        heads_out = sum(he - hb for pp, qq, hb, he in tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks={0},
+                                                                  d_ranks=set(d_ranks)))
+        p_out = max(per_head * heads_out * sum(cfg.n_tokens[r] for r in inst_req[i]) for i in range(n_inst))
+        busiest = max(d_in, p_out)
+        t_roof = busiest / (NVLINK_MEASURED_GBS * 1e9) * 1e3
         out = {"metric": METRIC, "value": round(tot_b / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "n_gpus": world,
                "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 3),
                "ms_per_request": round(ms / max(nreq, 1), 4), "higher_is_better": True, "scaling": "weak",
@@ -898,16 +989,20 @@ def run_stream(args):
                "config": {"workload": f"c5 stream: {cfg.note}; {n_inst} P instance(s) x {per_inst} rank(s) -> "
                                       f"D ranks {d_ranks}" + (" (full c5)" if world == 8 else " (c5' sub-config)"),
                           "requests": nreq, "src_bytes_per_step": tot_b,
-                          "mode": "push, whole instance batch per launch" if args.c5_batch else
+                          "mode": "pull per request (D-initiated NVLink reads, one launch per request)" if pull
+                          else "push, whole instance batch per launch" if args.c5_batch else
                           f"push per request, layer chunks >= {args.chunk_mib} MiB",
                           "l2": "inputs larger than L2 (no flush)"},
                "latency_ms": {"p50": round(alll[len(alll) // 2], 3) if alll else None,
                               "p99": round(alll[min(len(alll) - 1, int(0.99 * len(alll)))], 3) if alll else None,
                               "note": "per request, from the step start, requests issued in order"},
-               "roofline": {"bound": "nvlink", "achieved": round(d_in / (ms * 1e-3) / 1e9, 1),
+               "roofline": {"bound": "nvlink", "achieved": round(busiest / (ms * 1e-3) / 1e9, 1),
                             "peak": NVLINK_MEASURED_GBS, "unit": "GB/s", "frac": round(t_roof / ms, 4),
-                            "traffic": None, "kernel": "k_convert_rows (peer-store push, per request)",
-                            "algorithmic_bytes_per_step": d_in, "note": "busiest D rank ingress / step time"},
+                            "traffic": None,
+                            "kernel": "k_convert_rows (peer-load pull on D, per request)" if pull
+                            else "k_convert_rows (peer-store push, per request)",
+                            "algorithmic_bytes_per_step": busiest, "d_ingress_bytes": d_in, "p_egress_bytes": p_out,
+                            "note": "busiest GPU link (max of D ingress, P egress) / step time"},
                "clocks": clk, "gpu_launches": int(sum(x["launches"] for x in info))}
         print(json.dumps(out), flush=True)
     dist.all_reduce(barrier_t)
