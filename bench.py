@@ -489,7 +489,13 @@ def run_multi(args):
             for p in my_p}
         R = max(1, args.ring_slots)
         if narrowing and not args.layer_chunk:
-            lc = max(1, cfg.L // 20)
+            # ~64 MiB of wire per chunk, at most 20 chunks (c4 full batch: 4 layers per chunk;
+            # one request: 3 chunks), so the pipeline fill stays small and per-chunk launch
+            # costs on P stay hidden behind D's reads
+            pair_wire = 2 * cfg.L * min(cfg.H // cfg.tp_p, cfg.H // cfg.tp_d) * cfg.D * \
+                synth.NBYTES[cfg.dst_dtype] * cfg.total_tokens
+            n_ch = min(20, max(1, round(pair_wire / (64 << 20))))
+            lc = -(-cfg.L // n_ch)
         ring, slot_bytes, dst_lays = None, 0, {}
         if me.kind == "P":
             dst_lays = {q: d_view(q) for q in my_q}

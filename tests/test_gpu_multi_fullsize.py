@@ -1,0 +1,54 @@
+"""Multi-GPU parity at BASELINE.json's full sizes, in exactly the launch configuration
+bench.py times: torchrun of bench.py itself (one process per GPU, NCCL control plane),
+each D rank checking a sample of its received pool against the oracle (bench's
+parity_multi: request 0, layers [0, 2), regenerated sources) -- for the default pull
+transport and the push / NCCL baselines."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+import torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _bench(n, *args):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"), "--gpus", str(n),
+           "--steps", "2", "--warmup", "1", "--no-e2e", *args]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.parametrize("mode", ["pull", "push", "nccl"])
+def test_c4_pair_fullsize(mode):
+    """c4 (70B GQA, 32 x 4096 tokens, bf16 -> e4m3) on one 1:1 pair."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    d = _bench(2, "--mode", mode)
+    assert d["parity"] and all(p["ok"] for p in d["parity"]), d["parity"]
+    assert d["parity"][0]["mismatches"] == 0
+
+
+@pytest.mark.parametrize("workload", ["c3", "c2"])
+def test_fan_in_fullsize_pull(workload):
+    """c3' / c2: two P ranks -> one D rank (fan-in 2), the D rank pulling both peer pools."""
+    if torch.cuda.device_count() < 3:
+        pytest.skip("needs 3 GPUs")
+    d = _bench(min(4, torch.cuda.device_count()), "--workload", workload, "--mode", "pull")
+    assert d["parity"] and all(p["ok"] for p in d["parity"]), d["parity"]
