@@ -50,8 +50,13 @@ typedef enum {
   KV_ETIMEOUT = 6       /* flag wait timed out */
 } kv_status;
 
-/* Element types.  KV_F8E4M3 is OCP e4m3fn (max 448, no Inf, NaN = S.1111.111). */
-typedef enum { KV_F16 = 0, KV_BF16 = 1, KV_F8E4M3 = 2, KV_F32 = 3 } kv_dtype;
+/* Element types.  KV_F8E4M3 is OCP e4m3fn (max 448, no Inf, NaN = S.1111.111).
+ * KV_F8E4M3FNUZ is the e4m3 "fnuz" fp8 other GPU vendors' engines keep their KV cache in
+ * (NEXT-3, the multi-vendor P/D pairing of the paper's title): bias 8, max 240, no Inf, no
+ * negative zero, 0x80 the only NaN.  Both fp8 types carry per-head dequant scales; casts
+ * between them dequantise with the source's and quantise with the destination's scales
+ * (readings 24-26). */
+typedef enum { KV_F16 = 0, KV_BF16 = 1, KV_F8E4M3 = 2, KV_F32 = 3, KV_F8E4M3FNUZ = 4 } kv_dtype;
 
 /* Physical axes of a paged KV pool; extents (L, 2, num_blocks, block_size, H/tp, head_dim). */
 typedef enum {
@@ -76,7 +81,7 @@ typedef struct {
   int32_t num_blocks;    /* pool capacity in blocks */
   int32_t dtype;         /* kv_dtype */
   int32_t axis_order[6]; /* kv_axis, outermost -> innermost; the pool is dense row-major in it */
-  const float* scales;   /* KV_F8E4M3 only: DEVICE fp32 [num_layers][2][H/tp] dequant scales s
+  const float* scales;   /* fp8 dtypes only: DEVICE fp32 [num_layers][2][H/tp] dequant scales s
                           * (real value = code * s), indexed by the pool-local layer; NULL
                           * for other dtypes */
 } kv_layout_desc;
@@ -106,7 +111,7 @@ typedef struct {
 /* Validate `desc` and derive strides.  *pool_bytes = 2*L*num_blocks*block_size*(H/tp)*D*bytes.
  * KV_ESHAPE if tp_degree does not divide num_kv_heads or tp_rank >= tp_degree;
  * KV_EINVAL on a non-permutation axis_order, bad dtype, non-positive extent, or
- * scales == NULL for KV_F8E4M3.  *out must be released with kv_layout_destroy. */
+ * scales == NULL for an fp8 dtype.  *out must be released with kv_layout_destroy. */
 kv_status kv_layout_describe(const kv_layout_desc* desc, kv_layout** out, size_t* pool_bytes);
 void kv_layout_destroy(kv_layout* lay);
 
@@ -172,8 +177,9 @@ kv_status kv_convert_share(const kv_layout* src, const void* src_pool, const kv_
 /* ---- NEXT-1: dynamic fp8 scales --------------------------------------------------- */
 
 /* Per-batch dequant scales for the heads of D rank `dst` (precision alignment):
- *   s[l][c][hq] = RN_f32(amax / 448),  amax = max |x| over every finite source element of
- *   the batch's valid tokens (x as f32; e4m3 sources dequantised with their own scale),
+ *   s[l][c][hq] = RN_f32(amax / M),  amax = max |x| over every finite source element of
+ *   the batch's valid tokens (x as f32; fp8 sources dequantised with their own scale), M
+ *   the largest finite value of dst's fp8 type (448 e4m3fn, 240 e4m3fnuz),
  * for layers [layer_begin, layer_end); s = 1 where amax is 0 or no finite element exists.
  * Reads the P pools that hold dst's heads (every needed P rank must be listed, KV_ESHAPE
  * otherwise).  out_scales: DEVICE float [L][2][H/tp_d]; entries outside the layer range are

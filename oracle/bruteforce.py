@@ -18,7 +18,7 @@ a slip in either one shows up as a disagreement:
   bisects for the neighbours of the exact input value and picks the nearer one,
   ties to the even code (RNE, IEEE 754 roundTiesToEven).  Overflow: a virtual
   code one quantum past the largest finite value stands for Inf (fp16/bf16) or
-  saturates to +-448 (e4m3fn satfinite).
+  saturates to +-448 (e4m3fn satfinite) / +-240 (e4m3fnuz satfinite).
 
 Passages: P:113 (III-B2, Fig. 5 layout alignment), P:125 (III-B3, Fig. 4 TP
 merge/split), P:65 (precision alignment), SPEC S:255/S:280 (zero-filled tail),
@@ -33,11 +33,13 @@ from fractions import Fraction
 import numpy as np
 
 LAYER, KV, BLOCK, SLOT, HEAD, DIM = range(6)
-F16, BF16, E4M3, F32 = range(4)
+F16, BF16, E4M3, F32, FNUZ = range(5)
 
 # (exp_bits, mantissa_bits, bias, has_inf)
-_FMT = {F16: (5, 10, 15, True), BF16: (8, 7, 127, True), E4M3: (4, 3, 7, False), F32: (8, 23, 127, True)}
-NBYTES = {F16: 2, BF16: 2, E4M3: 1, F32: 4}
+_FMT = {F16: (5, 10, 15, True), BF16: (8, 7, 127, True), E4M3: (4, 3, 7, False), F32: (8, 23, 127, True),
+        FNUZ: (4, 3, 8, False)}
+NBYTES = {F16: 2, BF16: 2, E4M3: 1, F32: 4, FNUZ: 1}
+FP8 = (E4M3, FNUZ)
 
 
 def decode(code: int, dt: int):
@@ -46,11 +48,14 @@ def decode(code: int, dt: int):
     sign = (code >> (eb + mb)) & 1
     e = (code >> mb) & ((1 << eb) - 1)
     m = code & ((1 << mb) - 1)
-    if has_inf and e == (1 << eb) - 1:
+    if dt == FNUZ:
+        if code == 0x80:
+            return "nan"  # e4m3fnuz: the "negative zero" code is the only NaN; no infinities
+    elif has_inf and e == (1 << eb) - 1:
         if m:
             return "nan"
         return "-inf" if sign else "+inf"
-    if not has_inf and e == (1 << eb) - 1 and m == (1 << mb) - 1:
+    elif not has_inf and e == (1 << eb) - 1 and m == (1 << mb) - 1:
         return "nan"  # OCP e4m3fn: S.1111.111 is the only NaN, no infinities
     if e == 0 and m == 0:
         return "-0" if sign else Fraction(0)
@@ -87,18 +92,20 @@ def round_to(x, dt: int) -> int:
 
     fp16/bf16/fp32: IEEE RNE, overflow -> +-Inf, NaN -> 0x7FFF / 0x7FFFFFFF
     (canonical NaN, reading 12).  e4m3fn: RNE with satfinite
-    (overflow and +-Inf -> +-448), NaN -> 0x7F.
+    (overflow and +-Inf -> +-448), NaN -> 0x7F.  e4m3fnuz: RNE with satfinite
+    (+-240), NaN -> 0x80, a zero result is 0x00 whatever its sign (reading 25).
     """
     eb, mb, bias, has_inf = _FMT[dt]
     sbit = 1 << (eb + mb)
     inf_code = ((1 << eb) - 1) << mb
+    sat = {E4M3: 0x7E, FNUZ: 0x7F}.get(dt)
     if x == "nan":
-        return 0x7F if dt == E4M3 else (0x7FFFFFFF if dt == F32 else 0x7FFF)
+        return {E4M3: 0x7F, FNUZ: 0x80, F32: 0x7FFFFFFF}.get(dt, 0x7FFF)
     if x == "-0":
-        return sbit
+        return 0 if dt == FNUZ else sbit
     if x in ("+inf", "-inf"):
         neg = x == "-inf"
-        mag = 0x7E if dt == E4M3 else inf_code
+        mag = sat if sat is not None else inf_code
         return mag | (sbit if neg else 0)
     neg = x < 0
     ax = -x if neg else x
@@ -120,9 +127,9 @@ def round_to(x, dt: int) -> int:
             else:  # tie: even code; the virtual overflow code follows an odd max code
                 code = lo_c if (lo_c % 2 == 0) else hi_c
     if code == "overflow":
-        code = 0x7E if dt == E4M3 else inf_code
-    if neg:
-        code |= sbit  # sign kept, including -0
+        code = sat if sat is not None else inf_code
+    if neg and not (dt == FNUZ and code == 0):
+        code |= sbit  # sign kept, including -0 (fnuz has no -0)
     return code
 
 
@@ -144,14 +151,16 @@ def _exact(v: np.float32):
 
 
 def cast(code: int, src_dt: int, dst_dt: int, src_scale: float = 1.0, dst_scale: float = 1.0) -> int:
-    """Element cast (readings 10-13).  Same dtype: bits unchanged."""
+    """Element cast (DESIGN.md readings 10-13, 20, 24-26).  Same dtype: bits unchanged;
+    fp8 sources are dequantised with src_scale, fp8 destinations quantised with dst_scale
+    (so e4m3fn <-> e4m3fnuz goes through both)."""
     if src_dt == dst_dt:
         return code
     x = decode(code, src_dt)
     with np.errstate(all="ignore"):
-        if src_dt == E4M3:
+        if src_dt in FP8:
             x = _exact(_f32(x) * np.float32(src_scale))
-        if dst_dt == E4M3:
+        if dst_dt in FP8:
             inv = np.float32(1.0) / np.float32(dst_scale)
             x = _exact(_f32(x) * inv)
     return round_to(x, dst_dt)

@@ -48,7 +48,11 @@
 /* Physical axes of a pool (SURVEY 8 notation): extents (L, 2, N_blocks, B, H_local, D). */
 enum { OAX_LAYER = 0, OAX_KV = 1, OAX_BLOCK = 2, OAX_SLOT = 3, OAX_HEAD = 4, OAX_DIM = 5 };
 /* Element types. */
-enum { ODT_F16 = 0, ODT_BF16 = 1, ODT_E4M3 = 2, ODT_F32 = 3 };
+/* ODT_E4M3FNUZ (NEXT-3, another vendor's fp8; reading 24): bias 8, max 240,
+ * no infinities, no negative zero, the single NaN 0x80. */
+enum { ODT_F16 = 0, ODT_BF16 = 1, ODT_E4M3 = 2, ODT_F32 = 3, ODT_E4M3FNUZ = 4 };
+
+static int is_fp8(int32_t dt) { return dt == ODT_E4M3 || dt == ODT_E4M3FNUZ; }
 
 typedef struct {
   int32_t num_layers;  /* layers held by this pool */
@@ -71,6 +75,7 @@ int32_t okv_dtype_bytes(int32_t dt) {
     case ODT_BF16: return 2;
     case ODT_E4M3: return 1;
     case ODT_F32: return 4;
+    case ODT_E4M3FNUZ: return 1;
   }
   return 0;
 }
@@ -144,10 +149,15 @@ static const ofmt FMT_F16 = {11, -14, 15, 5, 65504.0};
 static const ofmt FMT_BF16 = {8, -126, 127, 8, 3.3895313892515355e38};
 static const ofmt FMT_E4M3 = {4, -6, 7, 4, 448.0};
 static const ofmt FMT_F32 = {24, -126, 127, 8, 3.4028234663852886e38};
+static const ofmt FMT_FNUZ = {4, -7, 8, 4, 240.0};
 
 /* Decode an encoding to its exact value (NaN -> NAN, Inf -> INFINITY).
- * e4m3fn (OCP FP8): no infinities; S.1111.111 is NaN; all other codes finite. */
-static double decode_bits(uint32_t bits, const ofmt* f, int is_e4m3) {
+ * kind 0: IEEE (all-ones exponent = Inf / NaN).
+ * kind 1: e4m3fn (OCP FP8): no infinities; S.1111.111 is NaN; all other codes finite.
+ * kind 2: e4m3fnuz: no infinities; 0x80 ("negative zero") is the only NaN. */
+static double decode_bits(uint32_t bits, const ofmt* f, int kind) {
+  const int is_e4m3 = kind == 1;
+  if (kind == 2 && bits == 0x80u) return NAN;
   int mbits = f->p - 1;
   uint32_t sign = (bits >> (f->exp_bits + mbits)) & 1u;
   uint32_t e = (bits >> mbits) & ((1u << f->exp_bits) - 1u);
@@ -156,7 +166,7 @@ static double decode_bits(uint32_t bits, const ofmt* f, int is_e4m3) {
   uint32_t emax_field = (1u << f->exp_bits) - 1u;
   if (is_e4m3) {
     if (e == emax_field && m == ((1u << mbits) - 1u)) return NAN;
-  } else if (e == emax_field) {
+  } else if (kind == 0 && e == emax_field) {
     if (m != 0) return NAN;
     return sign ? -INFINITY : INFINITY;
   }
@@ -173,6 +183,7 @@ double okv_decode(uint32_t bits, int32_t dt) {
     case ODT_BF16: return decode_bits(bits & 0xFFFFu, &FMT_BF16, 0);
     case ODT_E4M3: return decode_bits(bits & 0xFFu, &FMT_E4M3, 1);
     case ODT_F32: return decode_bits(bits, &FMT_F32, 0);
+    case ODT_E4M3FNUZ: return decode_bits(bits & 0xFFu, &FMT_FNUZ, 2);
   }
   return NAN;
 }
@@ -234,6 +245,19 @@ static uint32_t round_e4m3_satfinite(double x) {
   return encode_exact(r, sign, &FMT_E4M3);
 }
 
+/* e4m3fnuz with satfinite (reading 25): RNE on the fnuz grid (bias 8, quantum 2^-10 below
+ * 2^-7), magnitudes rounding above 240 (and +-Inf) saturate to +-240, NaN -> 0x80, and a
+ * result of zero is +0 (0x00) whatever the sign -- the format has no negative zero. */
+static uint32_t round_fnuz_satfinite(double x) {
+  if (isnan(x)) return 0x80u;
+  uint32_t sign = signbit(x) ? 1u : 0u;
+  double ax = fabs(x);
+  double r = isinf(x) ? INFINITY : rne_magnitude(ax, &FMT_FNUZ);
+  if (r > FMT_FNUZ.maxfin) r = FMT_FNUZ.maxfin;
+  if (r == 0.0) return 0u;
+  return encode_exact(r, sign, &FMT_FNUZ);
+}
+
 uint16_t okv_f16_to_bf16(uint16_t x) { return (uint16_t)round_ieee(okv_decode(x, ODT_F16), &FMT_BF16); }
 uint16_t okv_bf16_to_f16(uint16_t x) { return (uint16_t)round_ieee(okv_decode(x, ODT_BF16), &FMT_F16); }
 uint16_t okv_f32_to_f16(uint32_t x) { return (uint16_t)round_ieee(okv_decode(x, ODT_F32), &FMT_F16); }
@@ -253,19 +277,21 @@ uint8_t okv_to_e4m3_scaled(uint32_t bits, int32_t src_dt, float scale) {
   return okv_f32_to_e4m3(v);
 }
 
-/* Dequantise e4m3 with scale s into fp32: RN_f32(f32(q) * s) (NEXT-1 widening). */
-static float e4m3_dequant(uint32_t q, float scale) {
-  float qf = (float)okv_decode(q, ODT_E4M3);
+/* Dequantise an fp8 code (e4m3fn or e4m3fnuz) with scale s into fp32:
+ * RN_f32(f32(q) * s) (NEXT-1 widening, reading 20). */
+static float fp8_dequant(uint32_t q, int32_t dt, float scale) {
+  float qf = (float)okv_decode(q, dt);
   return qf * scale;
 }
 
-/* cast(x) from src dtype to dst dtype.  src_scale applies when src is e4m3,
- * dst_scale when dst is e4m3.  Same dtype: bits unchanged. */
+/* cast(x) from src dtype to dst dtype.  src_scale applies when src is fp8 (e4m3fn or
+ * e4m3fnuz), dst_scale when dst is fp8.  Same dtype: bits unchanged.  fp8 -> the
+ * other fp8 format: dequantise with src_scale, quantise with dst_scale (reading 26). */
 uint32_t okv_cast(uint32_t bits, int32_t src_dt, int32_t dst_dt, float src_scale, float dst_scale) {
   if (src_dt == dst_dt) return bits;
   double x;
-  if (src_dt == ODT_E4M3) {
-    x = (double)e4m3_dequant(bits, src_scale);
+  if (is_fp8(src_dt)) {
+    x = (double)fp8_dequant(bits, src_dt, src_scale);
   } else {
     x = okv_decode(bits, src_dt);
   }
@@ -273,12 +299,12 @@ uint32_t okv_cast(uint32_t bits, int32_t src_dt, int32_t dst_dt, float src_scale
     case ODT_F16: return round_ieee(x, &FMT_F16);
     case ODT_BF16: return round_ieee(x, &FMT_BF16);
     case ODT_F32: return round_ieee(x, &FMT_F32);
-    case ODT_E4M3: {
-      if (src_dt == ODT_E4M3) return bits; /* unreachable: same dtype handled above */
-      float xf = (float)x;
+    case ODT_E4M3:
+    case ODT_E4M3FNUZ: {
+      float xf = (float)x; /* exact: x is an f32 value or a <= 24-bit significand */
       float inv = 1.0f / dst_scale;
       float v = xf * inv;
-      return round_e4m3_satfinite((double)v);
+      return dst_dt == ODT_E4M3 ? round_e4m3_satfinite((double)v) : round_fnuz_satfinite((double)v);
     }
   }
   return 0;
@@ -478,7 +504,8 @@ void okv_cast_array(int64_t n, const void* in, int32_t src_dt, int32_t dst_dt, f
 }
 
 /* NEXT-1 dynamic scales (precision alignment; reading 21):
- * s[l][c][hq] = RN_f32(amax / 448) with amax = max |x| (x as f32, e4m3 sources dequantised
+ * s[l][c][hq] = RN_f32(amax / M) with M the destination fp8's largest finite value (448
+ * e4m3fn, 240 e4m3fnuz) and amax = max |x| (x as f32, fp8 sources dequantised
  * with their own scale) over every finite source element of the valid tokens of all
  * requests for the heads of D rank dst; s = 1 if amax is 0.  Layers [lb, le) are written
  * into out[L][2][H_d]; other entries untouched.  Returns 0, or <0 if a shard is missing. */
@@ -503,13 +530,13 @@ int32_t okv_amax_scales(int32_t n_src, const okv_layout* src, void* const* src_p
             for (int32_t d = 0; d < D; ++d) {
               uint32_t x = load_elem(src_pools[pi], okv_offset(Lp, l - Lp->first_layer, c, sb, t % Bp, hp, d),
                                      Lp->dtype);
-              float v = Lp->dtype == ODT_E4M3 ? e4m3_dequant(x, scale_of(Lp, l - Lp->first_layer, c, hp))
-                                              : (float)okv_decode(x, Lp->dtype);
+              float v = is_fp8(Lp->dtype) ? fp8_dequant(x, Lp->dtype, scale_of(Lp, l - Lp->first_layer, c, hp))
+                                          : (float)okv_decode(x, Lp->dtype);
               v = fabsf(v);
               if (isfinite(v) && v > amax) amax = v;
             }
           }
-        float s = amax / 448.0f;
+        float s = amax / (dst->dtype == ODT_E4M3FNUZ ? 240.0f : 448.0f);
         out[((l - dst->first_layer) * 2 + c) * Hd + hq] = s > 0.0f ? s : 1.0f;
       }
   return 0;

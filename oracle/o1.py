@@ -17,8 +17,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "kv_oracle.c")
 LIB = os.path.join(HERE, "libkvoracle.so")
 
-F16, BF16, E4M3, F32 = range(4)
-NBYTES = {F16: 2, BF16: 2, E4M3: 1, F32: 4}
+F16, BF16, E4M3, F32, FNUZ = range(5)
+NBYTES = {F16: 2, BF16: 2, E4M3: 1, F32: 4, FNUZ: 1}
 NPTYPE = {1: np.uint8, 2: np.uint16, 4: np.uint32}
 
 _lock = threading.Lock()

@@ -16,9 +16,9 @@ LIB_PATH = os.path.join(PKG, "libkvx.so")
 
 KV_OK, KV_EINVAL, KV_ESHAPE, KV_EUNSUPPORTED, KV_ECUDA, KV_ENCCL, KV_ETIMEOUT = range(7)
 STATUS_NAMES = ["KV_OK", "KV_EINVAL", "KV_ESHAPE", "KV_EUNSUPPORTED", "KV_ECUDA", "KV_ENCCL", "KV_ETIMEOUT"]
-KV_F16, KV_BF16, KV_F8E4M3, KV_F32 = range(4)
+KV_F16, KV_BF16, KV_F8E4M3, KV_F32, KV_F8E4M3FNUZ = range(5)
 AX_LAYER, AX_KV, AX_BLOCK, AX_SLOT, AX_HEAD, AX_DIM = range(6)
-DTYPE_BYTES = {KV_F16: 2, KV_BF16: 2, KV_F8E4M3: 1, KV_F32: 4}
+DTYPE_BYTES = {KV_F16: 2, KV_BF16: 2, KV_F8E4M3: 1, KV_F32: 4, KV_F8E4M3FNUZ: 1}
 
 
 class KvError(RuntimeError):

@@ -27,11 +27,14 @@ kv_status cuda_fail(cudaError_t e, const char* what) {
   return KV_ECUDA;
 }
 
+bool fp8(int32_t dt) { return dt == KV_F8E4M3 || dt == KV_F8E4M3FNUZ; }
+
 int32_t dtype_bytes(int32_t dt) {
   switch (dt) {
     case KV_F16:
     case KV_BF16: return 2;
-    case KV_F8E4M3: return 1;
+    case KV_F8E4M3:
+    case KV_F8E4M3FNUZ: return 1;
     case KV_F32: return 4;
   }
   return 0;
@@ -105,11 +108,12 @@ kv_status same_model(const kv_layout* s, const kv_layout* d) {
 }
 
 kv_status scales_ok(const kv_layout* s, const kv_layout* d) {
-  // widening from e4m3 needs the source's scales; narrowing to e4m3 needs the destination's
-  if (d->d.dtype == KV_F8E4M3 && s->d.dtype != KV_F8E4M3 && !d->d.scales)
-    return fail(KV_EINVAL, "e4m3 destination without scales");
-  if (s->d.dtype == KV_F8E4M3 && d->d.dtype != KV_F8E4M3 && !s->d.scales)
-    return fail(KV_EINVAL, "e4m3 source without scales");
+  // dequantising an fp8 source needs its scales; quantising to fp8 needs the destination's
+  // (same dtype is a bit copy and needs neither)
+  if (fp8(d->d.dtype) && s->d.dtype != d->d.dtype && !d->d.scales)
+    return fail(KV_EINVAL, "fp8 destination without scales");
+  if (fp8(s->d.dtype) && d->d.dtype != s->d.dtype && !s->d.scales)
+    return fail(KV_EINVAL, "fp8 source without scales");
   return KV_OK;
 }
 
@@ -154,7 +158,7 @@ kv_status kv_layout_describe(const kv_layout_desc* desc, kv_layout** out, size_t
     if (a < 0 || a > 5 || seen[a]) return fail(KV_EINVAL, "kv_layout_describe: axis_order is not a permutation");
     seen[a] = true;
   }
-  if (d.dtype == KV_F8E4M3 && !d.scales) return fail(KV_EINVAL, "kv_layout_describe: e4m3 layout needs scales");
+  if (fp8(d.dtype) && !d.scales) return fail(KV_EINVAL, "kv_layout_describe: fp8 layout needs scales");
   kv_layout* L = new (std::nothrow) kv_layout;
   if (!L) return fail(KV_EINVAL, "kv_layout_describe: out of host memory");
   L->d = d;
@@ -591,7 +595,7 @@ kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const vo
   for (int i = 0; i < n_src; ++i) {
     const int p = src[i]->d.tp_rank;
     if (a.src_of_p[p] != -1) return fail(KV_EINVAL, "kv_compute_scales: source rank listed twice");
-    if (S->d.dtype == KV_F8E4M3 && !src[i]->d.scales) return fail(KV_EINVAL, "kv_compute_scales: e4m3 source without scales");
+    if (fp8(S->d.dtype) && !src[i]->d.scales) return fail(KV_EINVAL, "kv_compute_scales: fp8 source without scales");
     a.src_of_p[p] = (int8_t)i;
     a.src[i] = static_cast<const uint8_t*>(src_pools[i]);
     a.sscale[i] = src[i]->d.scales;
@@ -614,6 +618,7 @@ kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const vo
   a.tok_off = src_bt->tok_off;
   a.tok_req = src_bt->tok_req;
   a.amax_bits = reinterpret_cast<uint32_t*>(out_scales);
+  a.qmax = dst->d.dtype == KV_F8E4M3FNUZ ? 240.0f : 448.0f;
   a.n_tok = (uint32_t)src_bt->total_tokens;
   const uint32_t ntg = (a.n_tok + 31u) / 32u;
   a.f_tg = make_fastdiv(std::max<uint32_t>(ntg, 1));

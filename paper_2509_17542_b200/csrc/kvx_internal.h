@@ -29,6 +29,7 @@ extern std::atomic<uint64_t> g_launches;
 extern std::atomic<int32_t> g_sm_budget;  // kv_set_sm_budget (0 = all SMs)
 
 int32_t dtype_bytes(int32_t dt);
+bool fp8(int32_t dt);  // KV_F8E4M3 or KV_F8E4M3FNUZ (carries per-head scales)
 
 // n / d for 32-bit n via one umulhi (Granlund-Montgomery round-up method).
 struct FastDiv {
@@ -174,6 +175,7 @@ struct AmaxArgs {
   const int32_t* tok_off;
   const int32_t* tok_req;
   uint32_t* amax_bits;  // [L][2][Hd] float bits (non-negative floats order like uints)
+  float qmax;           // largest finite value of the destination fp8 (448 e4m3fn, 240 e4m3fnuz)
   FastDiv f_tg, f_hd, f_bp, f_hp;
   uint32_t n_tok, n_items;
 };

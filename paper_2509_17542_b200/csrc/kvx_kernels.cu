@@ -53,6 +53,13 @@ template <>
 struct Tr<KV_F8E4M3> { static constexpr int B = 1; };
 template <>
 struct Tr<KV_F32> { static constexpr int B = 4; };
+template <>
+struct Tr<KV_F8E4M3FNUZ> { static constexpr int B = 1; };
+
+// fp8 formats carry a per-(layer, K/V, head) dequant scale (readings 9, 24)
+__host__ __device__ constexpr bool is_fp8(int dt) { return dt == KV_F8E4M3 || dt == KV_F8E4M3FNUZ; }
+// an fp8 -> other-fp8 cast needs both scales (dequantise, then quantise: reading 26)
+__host__ __device__ constexpr bool dual_scale(int sdt, int ddt) { return is_fp8(sdt) && is_fp8(ddt) && sdt != ddt; }
 
 // A chunk of VEC elements of dtype DT in 32-bit words.
 template <int DT, int VEC>
@@ -138,6 +145,12 @@ __device__ __forceinline__ float to_f32(uint32_t b) {
     return __uint_as_float(b << 16);
   } else if constexpr (DT == KV_F32) {
     return __uint_as_float(b);
+  } else if constexpr (DT == KV_F8E4M3FNUZ) {
+    // e4m3fnuz: bias 8, 0x80 the only NaN, no infinities (0x7F = 240)
+    const uint32_t sgn = (b & 0x80u) << 24, e = (b >> 3) & 0xFu, m = b & 7u;
+    const float sub = __uint_as_float(__float_as_uint((float)m * 0.0009765625f) | sgn);  // m * 2^-10
+    const float nrm = __uint_as_float(sgn | ((e + 119u) << 23) | (m << 20));
+    return b == 0x80u ? __uint_as_float(0x7FFFFFFFu) : (e == 0u ? sub : nrm);
   } else {
     uint32_t h2;
     unsigned short in = (unsigned short)b;
@@ -165,8 +178,24 @@ __device__ __forceinline__ uint32_t f32x2_to_e4m3x2(float lo, float hi) {
   return r;
 }
 
-// Cast a chunk SDT -> DDT.  ssc: dequant scale of an e4m3 source; inv: RN(1/s) of an
-// e4m3 destination.
+// e4m3fnuz codes of two scaled f32 values (lo -> bits 0..7, hi -> bits 8..15): RNE with
+// satfinite at +-240, NaN -> 0x80, zero results +0 (reading 25).  Every fnuz value is half
+// the e4m3fn value of the same bits (same mantissa grid, bias 8 vs 7), so the hardware
+// e4m3fn conversion of 2v gives the fnuz code except where the fn grid has its NaN slot
+// (2v > 464 <=> v > 232: saturate to 0x7F) and for -0 (0x80 is fnuz's NaN: make it +0).
+__device__ __forceinline__ uint32_t fnuz_fix(uint32_t code, float v) {
+  const float a = fabsf(v);
+  if (a != a) return 0x80u;
+  if (a > 232.0f) return 0x7Fu | ((__float_as_uint(v) >> 24) & 0x80u);
+  return code == 0x80u ? 0u : code;
+}
+__device__ __forceinline__ uint32_t f32x2_to_fnuzx2(float lo, float hi) {
+  const uint32_t r = f32x2_to_e4m3x2(__fmul_rn(lo, 2.0f), __fmul_rn(hi, 2.0f));
+  return fnuz_fix(r & 0xFFu, lo) | (fnuz_fix((r >> 8) & 0xFFu, hi) << 8);
+}
+
+// Cast a chunk SDT -> DDT.  ssc: dequant scale of an fp8 source; inv: RN(1/s) of an fp8
+// destination (an fp8 -> other-fp8 cast applies both, in that order).
 template <int SDT, int DDT, int VEC>
 __device__ __forceinline__ void cast_chunk(const Chunk<SDT, VEC>& in, Chunk<DDT, VEC>& out, float ssc, float inv) {
   if constexpr (SDT == DDT) {
@@ -177,8 +206,8 @@ __device__ __forceinline__ void cast_chunk(const Chunk<SDT, VEC>& in, Chunk<DDT,
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
       f[i] = to_f32<SDT>(get_elem<SDT>(in.w, i));
-      if constexpr (SDT == KV_F8E4M3) f[i] = __fmul_rn(f[i], ssc);
-      if constexpr (DDT == KV_F8E4M3) f[i] = __fmul_rn(f[i], inv);
+      if constexpr (is_fp8(SDT)) f[i] = __fmul_rn(f[i], ssc);
+      if constexpr (is_fp8(DDT)) f[i] = __fmul_rn(f[i], inv);
     }
 #pragma unroll
     for (int i = 0; i < Chunk<DDT, VEC>::WORDS; ++i) out.w[i] = 0;
@@ -188,6 +217,13 @@ __device__ __forceinline__ void cast_chunk(const Chunk<SDT, VEC>& in, Chunk<DDT,
       } else {
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) out.w[i >> 2] |= f32x2_to_e4m3x2(f[i], f[i + 1]) << ((i & 3) * 8);
+      }
+    } else if constexpr (DDT == KV_F8E4M3FNUZ) {
+      if constexpr (VEC == 1) {
+        out.w[0] = f32x2_to_fnuzx2(f[0], 0.0f) & 0xFFu;
+      } else {
+#pragma unroll
+        for (int i = 0; i < VEC; i += 2) out.w[i >> 2] |= f32x2_to_fnuzx2(f[i], f[i + 1]) << ((i & 3) * 8);
       }
     } else if constexpr (DDT == KV_F32) {
       // bf16 -> f32 is a bit shift that would keep NaN payloads; reading 12 wants the
@@ -285,9 +321,9 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
                                sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
                                (int64_t)hp * a.ss[KV_AX_HEAD] + (int64_t)dch * VEC * a.ss[KV_AX_DIM];
           load_chunk<SDT, VEC>(in[k], a.src[si] + soff * Tr<SDT>::B);
-          if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3)
+          if constexpr (is_fp8(SDT) && SDT != DDT)
             ssc[k] = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
-          if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3)
+          if constexpr (is_fp8(DDT) && SDT != DDT)
             inv[k] = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
         }
       }
@@ -310,16 +346,20 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
 // item: source row address sp, destination row address dp, its scale rsc and rz
 // (0 copy, 1 zero-fill tail row, 2 no row).  The warp streams the 32 x 2^cs chunks of
 // 16 B (source side) with U loads in flight per lane, fetching row state by shuffles.
+// rsc is the one fp8 scale a cast needs (source dequant scale, or RN(1/s) of an fp8
+// destination); an fp8 -> other-fp8 cast takes the source scale in rsc and RN(1/s_dst) in
+// rsc2 (the only instantiations that carry the second register).
 // ------------------------------------------------------------------------------------
 template <int SDT, int DDT, int U, int VEC = 8, bool COH = false>
 __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t sp, uint64_t dp, float rsc,
-                                            uint32_t rz) {
+                                            uint32_t rz, float rsc2 = 1.f) {
+  constexpr bool DUAL = dual_scale(SDT, DDT);
   const uint32_t cmask = (1u << cs) - 1u;
   const uint32_t nch = 32u << cs;
   for (uint32_t base = 0; base < nch; base += 32u * U) {
     Chunk<SDT, VEC> in[U];
     uint64_t d[U];
-    float sc[U];
+    float sc[U], sc2[DUAL ? U : 1];
     uint32_t z[U], ch[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -330,6 +370,7 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
       d[k] = __shfl_sync(0xffffffffu, dp, rr);
       z[k] = __shfl_sync(0xffffffffu, rz, rr) | (idx >= nch ? 2u : 0u);
       sc[k] = __shfl_sync(0xffffffffu, rsc, rr);
+      if constexpr (DUAL) sc2[k] = __shfl_sync(0xffffffffu, rsc2, rr);
       if (z[k] == 0) load_chunk<SDT, VEC, COH>(in[k], reinterpret_cast<const uint8_t*>(s) + ch[k] * (VEC * Tr<SDT>::B));
     }
 #pragma unroll
@@ -338,6 +379,8 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
       Chunk<DDT, VEC> o;
       if (z[k])
         zero_chunk(o);
+      else if constexpr (DUAL)
+        cast_chunk<SDT, DDT, VEC>(in[k], o, sc[k], sc2[k]);
       else
         cast_chunk<SDT, DDT, VEC>(in[k], o, sc[k], sc[k]);
       store_chunk<DDT, VEC>(reinterpret_cast<uint8_t*>(d[k]) + ch[k] * (VEC * Tr<DDT>::B), o);
@@ -359,7 +402,7 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
 // 2-D sub-tile.  rz: 0 copy, 1 zero-fill tail row, 2 no row.
 template <int SDT, int DDT>
 __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint32_t lane, uint64_t& sp,
-                                         uint64_t& dp, float& rsc, uint32_t& rz) {
+                                         uint64_t& dp, float& rsc, uint32_t& rz, float& rsc2) {
   // destination fastest: with several D ranks (fan-out, e.g. a TP split pushed over
   // NVLink) concurrent warps write every destination at once instead of one link after
   // the other -- with the D rank outermost, all P ranks of a fan-in/fan-out hit the same
@@ -389,7 +432,8 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
   const uint32_t hq = (uint32_t)a.hq_off[qi] + hl;      // D-local head
   sp = 0;
   dp = 0;
-  rsc = 1.f;  // e4m3 destination: RN(1/s); e4m3 source: s
+  rsc = 1.f;  // fp8 destination: RN(1/s); fp8 source: s (both fp8: s_src, and rsc2 = RN(1/s_dst))
+  rsc2 = 1.f;
   rz = 2;
   if (slot < (uint32_t)a.Bd && hl < (uint32_t)a.Hd_eff) {
     rz = 0;
@@ -409,9 +453,13 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
       const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + tb);
       sp = (uint64_t)(a.src[si] + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
                                    (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
-      if constexpr (SDT == KV_F8E4M3 && DDT != KV_F8E4M3) rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
-      if constexpr (DDT == KV_F8E4M3 && SDT != KV_F8E4M3)
-        rsc = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+      if constexpr (dual_scale(SDT, DDT)) {
+        rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+        rsc2 = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+      } else {
+        if constexpr (is_fp8(SDT) && SDT != DDT) rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+        if constexpr (is_fp8(DDT) && SDT != DDT) rsc = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+      }
     }
   }
 }
@@ -424,10 +472,10 @@ __global__ void __launch_bounds__(kThreads, KVX_MINB) k_convert_rows(const __gri
   const uint32_t cs = (uint32_t)a.cpr_shift;
   for (uint32_t item = warp; item < a.n_items; item += nwarps) {
     uint64_t sp, dp;
-    float rsc;
+    float rsc, rsc2;
     uint32_t rz;
-    conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz);
-    stream_rows<SDT, DDT, U, VEC>(lane, cs, sp, dp, rsc, rz);
+    conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz, rsc2);
+    stream_rows<SDT, DDT, U, VEC>(lane, cs, sp, dp, rsc, rz, rsc2);
   }
 }
 
@@ -505,9 +553,9 @@ __global__ void __launch_bounds__(kTmaWarps * 32) k_convert_tma(const __grid_con
   auto issue = [&](uint32_t k, int s) {
     const uint32_t item = warp + k * nwarps;
     uint64_t sp, dp;
-    float rsc;
+    float rsc, rsc2;  // dual-scale casts never take this kernel (launcher)
     uint32_t rz;
-    conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz);
+    conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz, rsc2);
     st_dp[s * 32 + lane] = dp;
     st_sc[s * 32 + lane] = rsc;
     st_rz[s * 32 + lane] = rz;
@@ -721,7 +769,7 @@ __global__ void __launch_bounds__(kThreads) k_pack_rows(const __grid_constant__ 
     const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
     const uint32_t tok = tg * 32u + lane;
     uint64_t sp = 0, dp = 0;
-    float rsc = 1.f;
+    float rsc = 1.f, rsc2 = 1.f;
     uint32_t rz = 2;
     if (tok < T_all) {
       rz = 0;
@@ -734,11 +782,16 @@ __global__ void __launch_bounds__(kThreads) k_pack_rows(const __grid_constant__ 
       sp = (uint64_t)(a.src + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
                                (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
       dp = (uint64_t)(a.wire + ((((uint64_t)l * 2 + c) * (uint64_t)a.nh + hh) * T_all + tok) * (uint64_t)a.D * Tr<WDT>::B);
-      if constexpr (SDT == KV_F8E4M3 && WDT != KV_F8E4M3) rsc = __ldg(a.sscale + (sl * 2 + c) * a.Hp + hp);
-      if constexpr (WDT == KV_F8E4M3 && SDT != KV_F8E4M3)
-        rsc = __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)));
+      const float ds_inv = is_fp8(WDT) && SDT != WDT
+                               ? __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)))
+                               : 1.f;
+      if constexpr (is_fp8(SDT) && SDT != WDT) rsc = __ldg(a.sscale + (sl * 2 + c) * a.Hp + hp);
+      if constexpr (dual_scale(SDT, WDT))
+        rsc2 = ds_inv;
+      else if constexpr (is_fp8(WDT) && SDT != WDT)
+        rsc = ds_inv;
     }
-    stream_rows<SDT, WDT, U>(lane, cs, sp, dp, rsc, rz);
+    stream_rows<SDT, WDT, U>(lane, cs, sp, dp, rsc, rz, rsc2);
   }
 }
 
@@ -771,7 +824,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
     const int64_t layer = a.lb + (int64_t)l;
     const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
     uint64_t sp = 0, dp = 0;
-    float rsc = 1.f;
+    float rsc = 1.f, rsc2 = 1.f;
     uint32_t rz = 2;
     if (slot < (uint32_t)a.Bd && hh < (uint32_t)a.nh) {
       rz = 0;
@@ -786,13 +839,15 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
       } else {
         sp = (uint64_t)(a.wire + ((((uint64_t)l * 2 + c) * (uint64_t)a.nh + hh) * (uint64_t)a.total_tokens +
                                   (uint64_t)(tok0 + t)) * (uint64_t)a.D * Tr<WDT>::B);
-        if constexpr (WDT == KV_F8E4M3 && DDT != KV_F8E4M3)
+        if constexpr (is_fp8(WDT) && WDT != DDT)
           rsc = __ldg(a.sscale + (sl * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
-        if constexpr (DDT == KV_F8E4M3 && WDT != KV_F8E4M3)
+        if constexpr (dual_scale(WDT, DDT))
+          rsc2 = __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + hq));
+        else if constexpr (is_fp8(DDT) && WDT != DDT)
           rsc = __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + hq));
       }
     }
-    stream_rows<WDT, DDT, U>(lane, cs, sp, dp, rsc, rz);
+    stream_rows<WDT, DDT, U>(lane, cs, sp, dp, rsc, rz, rsc2);
   }
 }
 
@@ -950,8 +1005,8 @@ __global__ void __launch_bounds__(kThreads) k_pack(const __grid_constant__ PackA
                              (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD] +
                              (int64_t)dch * VEC * a.ss[KV_AX_DIM];
         load_chunk<SDT, VEC>(in[k], a.src + soff * Tr<SDT>::B);
-        if constexpr (SDT == KV_F8E4M3 && WDT != KV_F8E4M3) ssc[k] = __ldg(a.sscale + (sl * 2 + c) * a.Hp + hp);
-        if constexpr (WDT == KV_F8E4M3 && SDT != KV_F8E4M3)
+        if constexpr (is_fp8(SDT) && SDT != WDT) ssc[k] = __ldg(a.sscale + (sl * 2 + c) * a.Hp + hp);
+        if constexpr (is_fp8(WDT) && SDT != WDT)
           inv[k] = __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)));
       }
     }
@@ -1017,9 +1072,9 @@ __global__ void __launch_bounds__(kThreads) k_unpack(const __grid_constant__ Unp
         } else {
           const int64_t woff = ((((int64_t)l * 2 + c) * a.nh + hh) * a.total_tokens + tok0 + t) * a.D + (int64_t)dch * VEC;
           load_chunk<WDT, VEC>(in[k], a.wire + woff * Tr<WDT>::B);
-          if constexpr (WDT == KV_F8E4M3 && DDT != KV_F8E4M3)
+          if constexpr (is_fp8(WDT) && WDT != DDT)
             ssc[k] = __ldg(a.sscale + (sl * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
-          if constexpr (DDT == KV_F8E4M3 && WDT != KV_F8E4M3)
+          if constexpr (is_fp8(DDT) && WDT != DDT)
             inv[k] = __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + hq));
         }
       }
@@ -1071,13 +1126,13 @@ __global__ void __launch_bounds__(kThreads) k_amax(const __grid_constant__ AmaxA
                                          sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
                                          (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B;
       float sc = 1.f;
-      if constexpr (SDT == KV_F8E4M3) sc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+      if constexpr (is_fp8(SDT)) sc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
       const int64_t sd = a.ss[KV_AX_DIM] * Tr<SDT>::B;
       for (int32_t d = 0; d < a.D; ++d) {
         Chunk<SDT, 1> e;
         load_chunk<SDT, 1>(e, base + d * sd);
         float v = to_f32<SDT>(e.w[0]);
-        if constexpr (SDT == KV_F8E4M3) v = __fmul_rn(v, sc);
+        if constexpr (is_fp8(SDT)) v = __fmul_rn(v, sc);
         v = fabsf(v);
         if (v <= 3.402823466e38f) m = fmaxf(m, v);  // skips NaN and Inf
       }
@@ -1088,10 +1143,11 @@ __global__ void __launch_bounds__(kThreads) k_amax(const __grid_constant__ AmaxA
   }
 }
 
-__global__ void k_amax_finalize(uint32_t* bits, int64_t begin, int64_t end) {
+// s = RN(amax / qmax), qmax = the destination fp8's largest finite value (448 / 240)
+__global__ void k_amax_finalize(uint32_t* bits, int64_t begin, int64_t end, float qmax) {
   for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end; i += (int64_t)gridDim.x * blockDim.x) {
     const float amax = __uint_as_float(bits[i]);
-    const float s = __fdiv_rn(amax, 448.0f);
+    const float s = __fdiv_rn(amax, qmax);
     reinterpret_cast<float*>(bits)[i] = s > 0.f ? s : 1.0f;
   }
 }
@@ -1222,7 +1278,7 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
     static const int tma = getenv("KVX_TMA") ? atoi(getenv("KVX_TMA")) : 0;
     static const bool wide = getenv("KVX_VEC16") ? atoi(getenv("KVX_VEC16")) == 1 : false;
     const uint32_t RB = (uint32_t)a.D * Tr<SDT>::B;
-    if (tma == 1 && RB % 16 == 0) {
+    if (tma == 1 && RB % 16 == 0 && !dual_scale(SDT, DDT)) {
       auto k = k_convert_tma<SDT, DDT>;
       const size_t per_warp = (size_t)kTmaStages * 32 * RB + (size_t)kTmaStages * 32 * 16 + kTmaStages * 8;
       int nw = (int)std::min<size_t>(kTmaWarps, (200u * 1024u) / per_warp);
@@ -1307,6 +1363,7 @@ cudaError_t unpack_t(const UnpackArgs& a0, cudaStream_t s) {
     case KV_F16: return FN<VEC, SDT, KV_F16>(__VA_ARGS__);             \
     case KV_BF16: return FN<VEC, SDT, KV_BF16>(__VA_ARGS__);           \
     case KV_F8E4M3: return FN<VEC, SDT, KV_F8E4M3>(__VA_ARGS__);       \
+    case KV_F8E4M3FNUZ: return FN<VEC, SDT, KV_F8E4M3FNUZ>(__VA_ARGS__); \
     case KV_F32: return FN<VEC, SDT, KV_F32>(__VA_ARGS__);             \
   }                                                                    \
   return cudaErrorInvalidValue;
@@ -1316,6 +1373,7 @@ cudaError_t unpack_t(const UnpackArgs& a0, cudaStream_t s) {
     case KV_F16: { KVX_DISPATCH_DDT(FN, VEC, KV_F16, ddt, __VA_ARGS__) }       \
     case KV_BF16: { KVX_DISPATCH_DDT(FN, VEC, KV_BF16, ddt, __VA_ARGS__) }     \
     case KV_F8E4M3: { KVX_DISPATCH_DDT(FN, VEC, KV_F8E4M3, ddt, __VA_ARGS__) } \
+    case KV_F8E4M3FNUZ: { KVX_DISPATCH_DDT(FN, VEC, KV_F8E4M3FNUZ, ddt, __VA_ARGS__) } \
     case KV_F32: { KVX_DISPATCH_DDT(FN, VEC, KV_F32, ddt, __VA_ARGS__) }       \
   }                                                                            \
   return cudaErrorInvalidValue;
@@ -1396,6 +1454,7 @@ cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s) {
     case KV_F16: return pull_rows_t<KV_F16>(a, s);
     case KV_BF16: return pull_rows_t<KV_BF16>(a, s);
     case KV_F8E4M3: return pull_rows_t<KV_F8E4M3>(a, s);
+    case KV_F8E4M3FNUZ: return pull_rows_t<KV_F8E4M3FNUZ>(a, s);
     case KV_F32: return pull_rows_t<KV_F32>(a, s);
   }
   return cudaErrorInvalidValue;
@@ -1410,13 +1469,16 @@ cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) 
       case KV_F16: k_amax<KV_F16><<<grid_for_items(k_amax<KV_F16>, a.n_items), kThreads, 0, s>>>(a); break;
       case KV_BF16: k_amax<KV_BF16><<<grid_for_items(k_amax<KV_BF16>, a.n_items), kThreads, 0, s>>>(a); break;
       case KV_F8E4M3: k_amax<KV_F8E4M3><<<grid_for_items(k_amax<KV_F8E4M3>, a.n_items), kThreads, 0, s>>>(a); break;
+      case KV_F8E4M3FNUZ:
+        k_amax<KV_F8E4M3FNUZ><<<grid_for_items(k_amax<KV_F8E4M3FNUZ>, a.n_items), kThreads, 0, s>>>(a);
+        break;
       case KV_F32: k_amax<KV_F32><<<grid_for_items(k_amax<KV_F32>, a.n_items), kThreads, 0, s>>>(a); break;
       default: return cudaErrorInvalidValue;
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   k_amax_finalize<<<(int)std::min<int64_t>(1024, (end - begin + 255) / 256 + 1), 256, 0, s>>>(
-      reinterpret_cast<uint32_t*>(out), begin, end);
+      reinterpret_cast<uint32_t*>(out), begin, end, a.qmax);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

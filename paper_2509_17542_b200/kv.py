@@ -10,11 +10,11 @@ import ctypes as C
 from contextlib import contextmanager
 
 from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BYTES, KV_BF16, KV_F8E4M3, KV_F16,
-                   KV_F32, Batch_t, KvError, LayoutDesc, check, lib)
+                   KV_F32, KV_F8E4M3FNUZ, Batch_t, KvError, LayoutDesc, check, lib)
 
 __all__ = ["Layout", "Batch", "convert_reshard", "convert_share", "push", "pull", "stage", "pull_staged", "chunk_count", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
            "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "launch_count", "launch_count_reset", "set_sm_budget", "last_kernel",
-           "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "DTYPE_BYTES",
+           "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "KV_F8E4M3FNUZ", "DTYPE_BYTES",
            "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
 
 

@@ -26,9 +26,10 @@ import numpy as np
 
 # Axis / dtype encodings of the C ABI (include/kvx.h) -- plain integers.
 LAYER, KV, BLOCK, SLOT, HEAD, DIM = range(6)
-F16, BF16, E4M3, F32 = range(4)
-NBYTES = {F16: 2, BF16: 2, E4M3: 1, F32: 4}
-DTYPE_NAMES = {F16: "f16", BF16: "bf16", E4M3: "e4m3", F32: "f32"}
+F16, BF16, E4M3, F32, FNUZ = range(5)   # FNUZ: e4m3fnuz (NEXT-3, another vendor's fp8)
+NBYTES = {F16: 2, BF16: 2, E4M3: 1, F32: 4, FNUZ: 1}
+DTYPE_NAMES = {F16: "f16", BF16: "bf16", E4M3: "e4m3", F32: "f32", FNUZ: "e4m3fnuz"}
+FP8 = (E4M3, FNUZ)
 
 # DESIGN.md reading 3: P = vLLM-style NHD per layer, D = block-major HND.
 P_ORDER = (LAYER, KV, BLOCK, SLOT, HEAD, DIM)
@@ -71,12 +72,13 @@ def random_finite_bits(seed, n, dtype):
     """Uniform random bit patterns of `dtype` with NaN/Inf patterns avoided.
 
     An all-ones exponent field is broken by clearing its lowest bit (so the
-    result is a finite pattern); e4m3fn only has NaN at S.1111.111."""
+    result is a finite pattern); e4m3fn only has NaN at S.1111.111, e4m3fnuz only at
+    0x80 (flipped to 0x81)."""
     rng = np.random.default_rng(seed)
     nb = NBYTES[dtype]
     if nb == 1:
         x = rng.integers(0, 256, size=n, dtype=np.uint16).astype(np.uint8)
-        bad = (x & 0x7F) == 0x7F
+        bad = (x == 0x80) if dtype == FNUZ else ((x & 0x7F) == 0x7F)
         x[bad] ^= 0x01
         return x
     if nb == 2:
@@ -101,7 +103,7 @@ def fill_random_finite_(t, seed, dtype):
     nb = NBYTES[dtype]
     if nb == 1:
         t.copy_(torch.randint(0, 256, t.shape, generator=g, device=t.device, dtype=torch.int16).to(torch.uint8))
-        bad = (t & 0x7F) == 0x7F
+        bad = (t == 0x80) if dtype == FNUZ else ((t & 0x7F) == 0x7F)
         t ^= bad.to(torch.uint8)
         return t
     if nb == 2:

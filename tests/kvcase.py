@@ -10,10 +10,10 @@ from __future__ import annotations
 import numpy as np
 
 import synth
-from synth import BF16, E4M3, F16, F32, NBYTES
+from synth import BF16, E4M3, F16, F32, FNUZ, FP8, NBYTES
 
 NPTYPE = {1: np.uint8, 2: np.uint16, 4: np.uint32}
-NAN_GARBAGE = {F16: 0x7E01, BF16: 0x7FC1, E4M3: 0x7F, F32: 0x7FC00001}
+NAN_GARBAGE = {F16: 0x7E01, BF16: 0x7FC1, E4M3: 0x7F, F32: 0x7FC00001, FNUZ: 0x80}
 
 
 def make_case(L, H, D, tp_p, tp_d, B_p, B_d, n_tokens, src_dt, dst_dt, p_order=synth.P_ORDER,
@@ -21,7 +21,7 @@ def make_case(L, H, D, tp_p, tp_d, B_p, B_d, n_tokens, src_dt, dst_dt, p_order=s
               values="random", NB_p=None, NB_d=None):
     """Build src pools (random finite bits), canary dst pools, tables, layouts.
 
-    scales: None | "amax" | "pow2" | float -- fp8 dequant scales for e4m3 dst ranks."""
+    scales: None | "amax" | "pow2" | float -- fp8 dequant scales for fp8 dst ranks."""
     NB_p = NB_p or synth.pool_capacity(n_tokens, B_p)
     NB_d = NB_d or synth.pool_capacity(n_tokens, B_d)
     src_tables = synth.block_tables(seed + 1, n_tokens, B_p, NB_p, contiguous)
@@ -41,7 +41,7 @@ def make_case(L, H, D, tp_p, tp_d, B_p, B_d, n_tokens, src_dt, dst_dt, p_order=s
     dst_lays, dst_pools = [], []
     for q in range(tp_d):
         sc = None
-        if dst_dt == E4M3 and scales is not None:
+        if dst_dt in FP8 and scales is not None:
             Hd = H // tp_d
             if scales == "pow2":
                 sc = synth.pow2_scales(seed + 200 + q, L, Hd)

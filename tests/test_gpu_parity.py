@@ -14,7 +14,7 @@ import pytest
 import torch
 
 import synth
-from synth import BF16, E4M3, F16, F32, LAYER, KV, BLOCK, SLOT, HEAD, DIM
+from synth import BF16, E4M3, F16, F32, FNUZ, FP8, LAYER, KV, BLOCK, SLOT, HEAD, DIM
 from tests.kvcase import coord_fill, expected, make_case
 
 pytestmark = pytest.mark.gpu
@@ -72,12 +72,16 @@ def test_c1_tiny(o1):
     run_case(o1, case)
 
 
-@pytest.mark.parametrize("sdt,ddt", [(s, d) for s in (F16, BF16, E4M3, F32) for d in (F16, BF16, E4M3, F32)])
+ALL_DT = (F16, BF16, E4M3, F32, FNUZ)
+
+
+@pytest.mark.parametrize("sdt,ddt", [(s, d) for s in ALL_DT for d in ALL_DT])
 def test_all_dtype_pairs(o1, sdt, ddt):
-    """Every (src, dst) dtype pair, fast path, ragged requests, TP 2 -> 4 split."""
-    case = make_case(3, 8, 64, 2, 4, 8, 16, [37, 5, 64, 1], sdt, ddt, seed=10 + 4 * sdt + ddt, o1=o1,
+    """Every (src, dst) dtype pair (incl. the e4m3fnuz vendor format, NEXT-3), fast path,
+    ragged requests, TP 2 -> 4 split."""
+    case = make_case(3, 8, 64, 2, 4, 8, 16, [37, 5, 64, 1], sdt, ddt, seed=10 + 5 * sdt + ddt, o1=o1,
                      scales="amax")
-    if sdt == E4M3:  # e4m3 sources need their own dequant scales
+    if sdt in FP8:  # fp8 sources need their own dequant scales
         for i, lay in enumerate(case["src_lays"]):
             lay["scales"] = synth.pow2_scales(500 + i, lay["L"], lay["H"] // lay["tp"], -4, 4) * np.float32(0.75)
     run_case(o1, case)
@@ -100,6 +104,32 @@ def test_exhaustive_cast_table_on_device(o1, src_dt):
         dc, got, want = run_case(o1, case)
         if dst_dt == E4M3:
             assert np.array_equal(got[0], want[0]), "fp8 path is expected bit-exact (reading 10)"
+
+
+def test_exhaustive_fnuz_tables_on_device(o1):
+    """e4m3fnuz (NEXT-3) through the device casts, compared bit for bit with O1: all 65536
+    bf16 / f16 patterns -> fnuz at scales 1 and 5.5/240; all 256 fnuz codes -> bf16 / f16 /
+    f32 / e4m3fn; all 256 e4m3fn codes -> fnuz (dequantise, then quantise: reading 26)."""
+    from tests.kvcase import NPTYPE
+    o = (LAYER, KV, BLOCK, SLOT, HEAD, DIM)
+    runs = [(F16, FNUZ, None, 1.0), (BF16, FNUZ, None, 5.5 / 240), (FNUZ, BF16, 0.75, None),
+            (FNUZ, F16, 2.0 ** -3, None), (FNUZ, F32, 1.0, None), (FNUZ, E4M3, 0.5, 1.0), (E4M3, FNUZ, 1.0, 2.0),
+            (E4M3, FNUZ, 0.37, 1.3)]
+    for sdt, ddt, ssc, dsc in runs:
+        L, H, D, B = 1, 1, 128, 16
+        n = 1 << (8 * synth.NBYTES[sdt])
+        T = 2 * n // D if synth.NBYTES[sdt] == 2 else 2 * B   # K and V halves hold the patterns
+        T = max(T // 2, B)
+        pool = np.resize(np.arange(n, dtype=np.uint32).astype(NPTYPE[synth.NBYTES[sdt]]), 2 * T * D)
+        s_sc = None if ssc is None else np.full((L, 2, H), ssc, np.float32)
+        d_sc = None if dsc is None else np.full((L, 2, H), dsc, np.float32)
+        src = synth.layout(L, H, D, 1, 0, B, T // B, sdt, o, s_sc)
+        dst = synth.layout(L, H, D, 1, 0, B, T // B, ddt, o, d_sc)
+        out = np.zeros(2 * T * D, dtype=NPTYPE[synth.NBYTES[ddt]])
+        case = dict(src_lays=[src], src_pools=[pool], dst_lays=[dst], dst_pools=[out], n_tokens=[T],
+                    src_tables=[list(range(T // B))], dst_tables=[list(range(T // B))])
+        dc, got, want = run_case(o1, case)
+        assert np.array_equal(got[0], want[0]), (sdt, ddt)
 
 
 def test_s532_grid_coordinates(o1):

@@ -188,3 +188,97 @@ def test_e4m3_scaled_op_order_exhaustive(o1, src, scale):
         v = xf * (np.float32(1.0) / np.float32(scale))
     got = o1.cast_array(ALL16, src, E4M3, 1.0, scale)
     assert np.array_equal(got[~nan], _ml_e4m3(v)[~nan])
+
+
+# ---- e4m3fnuz (NEXT-3: another vendor's fp8; readings 24-26) ---------------------------
+FNUZ = 4
+ALL8 = np.arange(256, dtype=np.uint8)
+
+
+def _fnuz_edges():
+    rows = []
+    with open(os.path.join(HERE, "golden", "e4m3fnuz_edges.txt")) as f:
+        for line in f:
+            if line.strip() and not line.startswith("#"):
+                b, c, _ = line.split()
+                rows.append((int(b, 16), int(c, 16)))
+    return rows
+
+
+@pytest.mark.parametrize("f32_bits,code", _fnuz_edges())
+def test_fnuz_satfinite_edges(o1, f32_bits, code):
+    """O1 and O2 against the hand-worked definition vectors (scale 1: f32 -> fnuz)."""
+    x = np.array([f32_bits], dtype=np.uint32)
+    assert int(o1.cast_array(x, F32, FNUZ, 1.0, 1.0)[0]) == code
+    v = np.uint32(f32_bits).view(np.float32)
+    ex = o2._exact(v)
+    assert o2.round_to(ex, FNUZ) == code
+
+
+def test_fnuz_decode_exhaustive_vs_ml_dtypes(o1):
+    """All 256 codes: widening to fp32 (scale 1) equals ml_dtypes' decode; 0x80 is the only NaN."""
+    got = o1.cast_array(ALL8, FNUZ, F32, 1.0, 1.0).view(np.float32)
+    ref = ALL8.view(ml_dtypes.float8_e4m3fnuz).astype(np.float32)
+    nan = np.isnan(ref)
+    assert list(np.nonzero(nan)[0]) == [0x80]
+    assert np.array_equal(got[~nan], ref[~nan])
+    assert np.isnan(got[0x80])
+    assert got[0x7F] == 240.0 and got[0xFF] == -240.0
+
+
+@pytest.mark.parametrize("src", [F16, BF16])
+@pytest.mark.parametrize("k", [-6, 0, 3])
+def test_fnuz_pow2_scales_exhaustive_vs_ml_dtypes(o1, src, k):
+    """Power-of-two scales make x * RN(1/s) exact, so the cast reduces to ml_dtypes' RNE
+    conversion for every 2-byte input whose scaled value is within +-240 (ml_dtypes does not
+    saturate: beyond that it returns NaN, where the satfinite reading clamps)."""
+    s = float(2.0 ** k)
+    codes = ALL16[~_is_nan16(ALL16, src)]
+    got = o1.cast_array(codes, src, FNUZ, 1.0, s)
+    xs = (codes.view(np.float16) if src == F16 else codes.view(ml_dtypes.bfloat16)).astype(np.float32)
+    v = xs * np.float32(1.0 / s)
+    inr = np.abs(v) < 240.0
+    ref = v[inr].astype(ml_dtypes.float8_e4m3fnuz).view(np.uint8)
+    assert np.array_equal(got[inr], ref)
+    big = ~inr & np.isfinite(v)
+    assert np.all(got[big] == np.where(v[big] > 0, 0x7F, 0xFF))
+
+
+def test_fnuz_never_negative_zero_never_nan_from_finite(o1):
+    codes = ALL16[~_is_nan16(ALL16, BF16)]
+    got = o1.cast_array(codes, BF16, FNUZ, 1.0, 0.37)
+    assert not np.any(got == 0x80)
+
+
+@pytest.mark.parametrize("pair", [(BF16, FNUZ), (F16, FNUZ), (FNUZ, BF16), (FNUZ, F16), (E4M3, FNUZ), (FNUZ, E4M3)])
+@pytest.mark.parametrize("scales", [(1.0, 1.0), (0.5, 2.0), (0.37, 1.9)])
+def test_fnuz_o1_vs_o2(o1, pair, scales):
+    """O1 (frexp/nearbyint) == O2 (nearest-code search over the decoded code table) on every
+    fp8 code / a 2-byte sample, with the dequant scale of an fp8 source and the quant scale
+    of an fp8 destination (fn <-> fnuz: dequantise then quantise, reading 26)."""
+    src, dst = pair
+    if o2.NBYTES[src] == 1:
+        codes = ALL8.copy()
+    else:
+        rng = np.random.default_rng(7)
+        codes = rng.integers(0, 1 << 16, size=3000).astype(np.uint16)
+        codes = codes[~_is_nan16(codes, src)]
+    ss, ds = scales
+    got = o1.cast_array(codes, src, dst, ss, ds)
+    for c, g in zip(codes.tolist(), got.tolist()):
+        assert o2.cast(int(c), src, dst, ss, ds) == g, (hex(c), hex(g))
+
+
+def test_fn_fnuz_identity_on_shared_grid(o1):
+    """Closed form: with s_fnuz = 2 * s_fn the two formats encode the same reals on the common
+    range, and e4m3fn code c (|c| <= 448, not NaN) maps to the fnuz code with the SAME bits
+    (every fnuz value is half the fn value of its bits).  Codes whose value exceeds 240 * s
+    saturate; fn's 2^-9 * s_fn subnormal is fnuz's 2^-10 * s_fnuz: all representable."""
+    sf = 0.5
+    fn = np.array([c for c in range(256) if (c & 0x7F) != 0x7F], dtype=np.uint8)
+    got = o1.cast_array(fn, E4M3, FNUZ, sf, 2 * sf)
+    want = fn.copy()
+    want[fn == 0x80] = 0x00                       # -0 has no fnuz code: +0
+    assert np.array_equal(got, want)
+    back = o1.cast_array(got, FNUZ, E4M3, 2 * sf, sf)
+    assert np.array_equal(back, np.where(fn == 0x80, 0, fn).astype(np.uint8))

@@ -60,3 +60,17 @@ def test_merge_takes_each_heads_own_scale(o1):
         per = o1.amax_scales([src[p]], [pools[p]], synth.layout(L, H, D, 2, p, B, NB, F16, synth.D_ORDER),
                              n_tokens, tabs)
         assert np.array_equal(merged[:, :, 2 * p:2 * p + 2], per)
+
+
+def test_closed_form_fnuz_destination(o1):
+    """Reading 21 for an e4m3fnuz destination: s = RN(amax / 240) (240 = its largest finite
+    value); one element -240 * 2^-3 = -30 gives exactly 2^-3, the rest 1."""
+    L, H, D, B, NB = 2, 2, 8, 4, 3
+    lay = synth.layout(L, H, D, 1, 0, B, NB, BF16, synth.P_ORDER)
+    dst = synth.layout(L, H, D, 1, 0, B, NB, synth.FNUZ, synth.D_ORDER)
+    pool = np.zeros(2 * L * H * NB * B * D, dtype=np.uint16)
+    pool[o1.offset(lay, 0, 1, 1, 2, 0, 5)] = 0xC1F0   # bf16 -30
+    got = o1.amax_scales([lay], [pool], dst, [NB * B], [list(range(NB))])
+    want = np.ones((L, 2, H), np.float32)
+    want[0, 1, 0] = 0.125
+    assert np.array_equal(got, want)
