@@ -318,7 +318,8 @@ def run_single(args):
     total_ms = t0.elapsed_time(t1)
     ms = total_ms / K
     src_b, dst_b = w.src_bytes(), w.dst_bytes()
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev) if lc == cfg.L else ms
+    kts = [a.elapsed_time(b) for a, b in kev] if lc == cfg.L else [ms]
+    kern_ms = statistics.mean(kts)
     peaks = load_peaks()
     alg = src_b + dst_b  # HBM read + write per launch
     achieved = alg / (kern_ms * 1e-3) / 1e9
@@ -336,6 +337,7 @@ def run_single(args):
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _traffic(f"{wl_name}@1"),
                      "kernel": kvx.last_kernel(), "kernel_ms": round(kern_ms, 5),
+                     "kernel_ms_median": round(statistics.median(kts), 5), "kernel_ms_min": round(min(kts), 5),
                      "algorithmic_bytes_per_launch": alg, "peak_source": peaks["source"],
                      "frac_vs_nominal_8TBs": round(achieved / 8000.0, 4)},
         "clocks": clk, "gpu_launches": int(launches),
@@ -607,14 +609,16 @@ def run_multi(args):
     barrier()
     my_ms = t0.elapsed_time(t1)
     mover = "D" if args.mode == "pull" else "P"   # the rank whose stream runs the data-path kernels
-    kern_ms = statistics.mean(a.elapsed_time(b) for a, b in kev) if me.kind == mover else 0.0
+    kts = [a.elapsed_time(b) for a, b in kev] if me.kind == mover else [0.0]
+    kern_ms = statistics.mean(kts)
     if int(err.item()):
         raise SystemExit(f"rank {rank}: flag wait timed out")
     # busiest link: P egress = bytes it sends, D ingress = bytes it receives (wire dtype = dst)
     nvl_in = w.dst_bytes([0]) if me.kind == "D" else 0
     nvl_out = sum(w.dst_bytes([0]) * (len([1 for p2, q2, _, _ in pairs if q2 == q and p2 == me.tp_rank])) //
                   max(1, len([1 for p2, q2, _, _ in pairs if q2 == q])) for q in my_q) if me.kind == "P" else 0
-    stats = {"ms": my_ms, "kern_ms": kern_ms, "launches": launches, "kind": me.kind, "nvl": max(nvl_in, nvl_out),
+    stats = {"ms": my_ms, "kern_ms": kern_ms, "kern_med": statistics.median(kts), "kern_min": min(kts),
+             "launches": launches, "kind": me.kind, "nvl": max(nvl_in, nvl_out),
              "kernel": kvx.last_kernel(),
              "clk": clk}
     parity = None
@@ -657,7 +661,10 @@ def run_multi(args):
                          else f"{[x['kernel'] for x in sts if x['kind'] == 'D'][0]} (peer-load pull on D)"
                          if args.mode == "pull"
                          else "pack + ncclSend/Recv + unpack (whole P step)",
-                         "kernel_ms": round(kms, 4), "algorithmic_bytes_per_step": nvl_b,
+                         "kernel_ms": round(kms, 4),
+                         "kernel_ms_median": round(max(x["kern_med"] for x in sts if x["kind"] == mover), 4),
+                         "kernel_ms_min": round(max(x["kern_min"] for x in sts if x["kind"] == mover), 4),
+                         "algorithmic_bytes_per_step": nvl_b,
                          "note": "busiest GPU link (P egress or D ingress) bytes / step time",
                          "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)",
                          "frac_vs_nominal_900": round(achieved / NVLINK_NOMINAL_GBS, 4)},
