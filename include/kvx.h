@@ -368,8 +368,8 @@ kv_status kv_wait(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, int
 
 /* ---- misc ------------------------------------------------------------------------- */
 
-/* Cap the SMs the data-path kernels launched afterwards by this process may occupy
- * (0 = all; the grid is min(work, n_sms x occupancy)).  NVLink pushes saturate the link with
+/* Cap the SMs the data-path kernels this process launches afterwards on the CURRENT
+ * device may occupy (0 = all; the grid is min(work, n_sms x occupancy)).  NVLink pushes saturate the link with
  * a fraction of the 148 SMs, leaving the rest to prefill compute that overlaps them (P:289
  * "parallel transmission and calculation").  Returns the previous value. */
 int32_t kv_set_sm_budget(int32_t n_sms);

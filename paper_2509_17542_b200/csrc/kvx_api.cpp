@@ -15,7 +15,7 @@ namespace kvx {
 static thread_local std::string t_err;
 static thread_local const char* t_last_kernel = "";
 std::atomic<uint64_t> g_launches{0};
-std::atomic<int32_t> g_sm_budget{0};
+std::atomic<int32_t> g_sm_budget[kMaxDevices];
 
 kv_status fail(kv_status st, const std::string& msg) {
   t_err = msg;
@@ -138,7 +138,11 @@ const char* kv_last_kernel(void) { return t_last_kernel; }
 const char* kv_version(void) { return "kvx 0.1 (sm_100a)"; }
 uint64_t kv_launch_count(void) { return g_launches.load(); }
 void kv_launch_count_reset(void) { g_launches.store(0); }
-int32_t kv_set_sm_budget(int32_t n_sms) { return g_sm_budget.exchange(n_sms < 0 ? 0 : n_sms); }
+int32_t kv_set_sm_budget(int32_t n_sms) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return g_sm_budget[dev].exchange(n_sms < 0 ? 0 : n_sms);
+}
 
 kv_status kv_layout_describe(const kv_layout_desc* desc, kv_layout** out, size_t* pool_bytes) {
   if (!desc || !out) return fail(KV_EINVAL, "kv_layout_describe: null argument");
@@ -823,15 +827,7 @@ kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void*
   a.n_blk = (uint32_t)dst_bt->total_blocks;
   const uint64_t items = (uint64_t)n_src * 2 * (uint64_t)step * dst_bt->total_blocks * (uint64_t)a.Bd * (uint64_t)nh;
   if (items > kMaxChunks) return KV_OK;
-  a.spin_ns = getenv("KVX_PULL_SPIN_NS") ? (uint32_t)atoi(getenv("KVX_PULL_SPIN_NS")) : 128u;
-  // Wait for the first chunk with a one-thread kernel before the persistent launch: warps
-  // spinning in-kernel while P packs chunk 0 cost ~4x the wait itself (c4: lc=10, 8.6 vs
-  // 7.3 ms, profiles/r01/pull_probe*.jsonl); later chunks are normally ready when reached.
-  if (!getenv("KVX_PULL_NOPREWAIT"))
-    for (int i = 0; i < n_src; ++i) {
-      kv_status w = kv_wait(ready[i], seq0 + 1, timeout_ns, err, stream);
-      if (w != KV_OK) return w;
-    }
+  a.spin_ns = 128u;
   t_last_kernel = "k_pull_rows";
   cudaError_t e = launch_pull_rows(a, d->d.dtype, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kv_pull_staged: launch");

@@ -26,7 +26,8 @@ namespace kvx {
 kv_status fail(kv_status st, const std::string& msg);
 kv_status cuda_fail(cudaError_t e, const char* what);
 extern std::atomic<uint64_t> g_launches;
-extern std::atomic<int32_t> g_sm_budget;  // kv_set_sm_budget (0 = all SMs)
+constexpr int kMaxDevices = 64;
+extern std::atomic<int32_t> g_sm_budget[kMaxDevices];  // kv_set_sm_budget per device (0 = all SMs)
 
 int32_t dtype_bytes(int32_t dt);
 bool fp8(int32_t dt);  // KV_F8E4M3 or KV_F8E4M3FNUZ (carries per-head scales)

@@ -1192,7 +1192,7 @@ int num_sms() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d);
     dev = d;
   }
-  const int budget = g_sm_budget.load(std::memory_order_relaxed);
+  const int budget = (d >= 0 && d < kMaxDevices) ? g_sm_budget[d].load(std::memory_order_relaxed) : 0;
   return (budget > 0 && budget < sms) ? budget : sms;
 }
 
