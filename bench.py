@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="pull", choices=["push", "pull", "nccl"])
     ap.add_argument("--ring-slots", type=int, default=3, help="pull mode, narrowing cast: staging ring depth")
+    ap.add_argument("--dynamic-scales", action="store_true",
+                    help="pull mode, fp8 destination: P computes per-chunk amax scales and ships them (NEXT-1 i)")
     ap.add_argument("--layer-chunk", type=int, default=0, help="layers per chunk (0 = whole model)")
     ap.add_argument("--chunk-mib", type=int, default=64, help="c5: merge layers until a chunk moves this much")
     ap.add_argument("--c5-batch", action="store_true", help="c5: push each instance's requests as one batch")
@@ -160,7 +162,7 @@ class Workload:
                 sc = torch.from_numpy(sc_np).to(device)
             d = synth.layout(c.L, c.H, c.D, c.tp_d, q, c.B_d, self.NB_d, c.dst_dtype, c.d_order, sc_np)
             lay = kvx.Layout.from_dict(d, sc)
-            self.dst_dicts[q], self.dst_lays[q] = d, lay
+            self.dst_dicts[q], self.dst_lays[q], self.scales[q] = d, lay, sc
             self.dst_pools[q] = lay.new_pool(device, fill=synth.CANARY)
         any_src = self.src_lays[self.p_ranks[0]] if self.p_ranks else kvx.Layout.from_dict(
             synth.layout(c.L, c.H, c.D, c.tp_p, 0, c.B_p, self.NB_p, c.src_dtype, c.p_order))
@@ -489,6 +491,7 @@ def run_multi(args):
         return kvx.Layout.from_dict(
             synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, w.NB_d, cfg.dst_dtype, cfg.d_order), sc)
 
+    dyn = False
     if args.mode == "push":
         ch = tr.PushChannel(me, w.dst_pools.get(me.tp_rank), flags if me.kind == "D" else None)
         dst_lays = {q: d_view(q) for q in my_q}
@@ -521,8 +524,16 @@ def run_multi(args):
             n_ch = min(20, max(1, round(pair_wire / (64 << 20))))
             lc = -(-cfg.L // n_ch)
         ring, slot_bytes, dst_lays = None, 0, {}
+        dyn = args.dynamic_scales and narrowing and synth.NBYTES[cfg.src_dtype] > 1
+        own_scales = {}
         if me.kind == "P":
-            dst_lays = {q: d_view(q) for q in my_q}
+            if dyn:   # writable scale arrays on P: kv_stage fills them chunk by chunk
+                own_scales = {q: torch.ones(cfg.L * 2 * (cfg.H // cfg.tp_d), device=dev) for q in my_q}
+                dst_lays = {q: kvx.Layout.from_dict(
+                    synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, w.NB_d, cfg.dst_dtype, cfg.d_order),
+                    own_scales[q]) for q in my_q}
+            else:
+                dst_lays = {q: d_view(q) for q in my_q}
             S = w.src_lays[me.tp_rank]
             if narrowing:
                 slot_bytes = max(kvx.wire_bytes(S, dst_lays[q], cfg.total_tokens, (l0, min(cfg.L, l0 + lc)))
@@ -532,7 +543,8 @@ def run_multi(args):
                 ring_ptrs = [ring.data_ptr() + (i * R + b) * slot_bytes for i in range(len(my_q)) for b in range(R)]
         pflags = torch.zeros(max(n_p, n_d, 1), dtype=torch.int32, device=dev)
         pch = tr.PullChannel(me, pflags, pool=w.src_pools[me.tp_rank] if me.kind == "P" and not narrowing else None,
-                             ring=ring, ring_dst=my_q if ring is not None else (), ring_slots=R, slot_bytes=slot_bytes)
+                             ring=ring, ring_dst=my_q if ring is not None else (), ring_slots=R, slot_bytes=slot_bytes,
+                             scales=w.scales.get(me.tp_rank) if dyn and me.kind == "D" else None)
         if me.kind == "D" and narrowing:
             slot_bytes = min(pch.slot_bytes[p] for p in my_p)
         nchunks = kvx.chunk_count((0, cfg.L), lc)
@@ -548,7 +560,8 @@ def run_multi(args):
                     kvx.stage(S, w.src_pools[me.tp_rank], w.src_bt, [dst_lays[q] for q in my_q],
                               ring_ptrs, R,
                               slot_bytes, [pch.peer_flag[q] for q in my_q], [pflags[q:q + 1] for q in my_q],
-                              seq[0], err, (0, cfg.L), lc, 30.0, stream)
+                              seq[0], err, (0, cfg.L), lc, 30.0, stream,
+                              peer_scales=[pch.peer_scales[q] for q in my_q] if dyn else None)
                 else:
                     for q in my_q:   # my KV is resident: D may read it; then wait until it has
                         kvx.signal(pch.peer_flag[q], epoch[0], stream)
@@ -645,7 +658,9 @@ def run_multi(args):
              "clk": clk}
     parity = None
     if not args.no_parity and me.kind == "D":
-        parity = parity_multi(cfg, w, me, my_p, dev)
+        if dyn:   # decode the received codes with the scales P shipped
+            w.dst_dicts[me.tp_rank]["scales"] = w.scales[me.tp_rank].cpu().numpy().reshape(cfg.L, 2, -1)
+        parity = parity_multi(cfg, w, me, my_p, dev, dyn)
     e2e = None
     if not args.no_e2e and args.mode in ("push", "pull"):
         e2e = e2e_multi(w, me, step, stream, barrier, err, min(K, 3), rank)
@@ -670,7 +685,8 @@ def run_multi(args):
                                    f"0..{n_d - 1} on GPUs {n_p}..{n_p + n_d - 1}"
                                    + (" (full transfer)" if full else " (per-GPU-equivalent sub-config)")
                                    + (f", {world - n_p - n_d} idle GPU(s)" if world > n_p + n_d else ""),
-                       "mode": args.mode, "layer_chunk": lc, "requests": len(cfg.n_tokens),
+                       "mode": args.mode + (" + dynamic fp8 scales (P amax per chunk, shipped)" if dyn else ""),
+                       "layer_chunk": lc, "requests": len(cfg.n_tokens),
                        "tokens": cfg.total_tokens, "src_bytes_per_step": src_b,
                        "busiest_link_bytes_per_step": nvl_b, "pairs": [list(x[:2]) for x in pairs],
                        "l2": "inputs larger than L2 (no flush)",
@@ -733,9 +749,11 @@ def e2e_multi(w, me, step, stream, barrier, err, ke, rank):
             "d2h": host.numel() if me.kind == "D" else 0}
 
 
-def parity_multi(cfg, w, me, my_p, dev):
+def parity_multi(cfg, w, me, my_p, dev, dyn=False):
     """D rank: regenerate its P sources' pools from their seeds on this GPU and check a
-    sample of the received pool against the oracle."""
+    sample of the received pool against the oracle.  dyn: the fp8 scales were computed and
+    shipped by P -- also check them against O1's amax scales over every request for the
+    sampled layers."""
     import torch
     import paper_2509_17542_b200 as kvx
     q = me.tp_rank
@@ -747,6 +765,25 @@ def parity_multi(cfg, w, me, my_p, dev):
         w.src_dicts[p], w.src_pools[p] = d, pool
     ok, det = sample_parity(w, (0, 2), 0, my_p, [q])
     det["rank"] = f"D{q}"
+    if dyn:
+        from oracle import o1
+        ids = [b for t in w.src_tables for b in t]
+        lays, pools = [], []
+        for p in my_p:
+            a, nd = extract(w.src_pools[p], w.src_dicts[p], (0, 2), ids)
+            lays.append(nd)
+            pools.append(a)
+        k, tabs = 0, []
+        for t in w.src_tables:
+            tabs.append(list(range(k, k + len(t))))
+            k += len(t)
+        dd = dict(w.dst_dicts[q])
+        dd["L"], dd["scales"] = 2, None
+        want = o1.amax_scales(lays, pools, dd, cfg.n_tokens, tabs)
+        got = np.asarray(w.dst_dicts[q]["scales"])[0:2]
+        det["dynamic_scales_ok"] = bool(np.array_equal(got, want))
+        det["dynamic_scales_sample"] = "O1 amax/448 over all requests, layers [0,2)"
+        ok = ok and det["dynamic_scales_ok"]
     for p in my_p:
         del w.src_pools[p]
     return {"ok": ok, **det}

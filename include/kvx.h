@@ -325,6 +325,12 @@ kv_status kv_recv_pipelined(kv_comm* comm, int32_t n_src, const kv_layout* const
  * chunk frees its slots -- no per-chunk launch gap.  It needs `counters`, a caller-owned
  * DEVICE scratch of >= 2 x (number of chunks) uint32 that the call zeroes on its stream
  * (NULL: one kv_wait / kv_unpack / kv_signal launch triple per chunk instead).
+ * kv_stage with peer_scales != NULL computes dynamic fp8 scales (NEXT-1 i, kv_compute_scales
+ * semantics) chunk by chunk from the P rank's data into dst[i]'s own scale array (which must
+ * be writable DEVICE memory on P's GPU; the pack quantises with it) and copies each chunk's
+ * scales to peer_scales[i] (D rank i's scale array, peer-mapped) before the ready flag, so D
+ * holds the codes and the scales that decode them.  Requires a non-fp8 source and the P
+ * rank to hold all of dst[i]'s heads (tp_p <= tp_d); NULL: dst[i]'s static scales are used.
  * The caller advances seq0 by the number of chunks per call.  All three validate before
  * enqueueing; a wait that times out sets *err = 1 (device int32 on the waiting GPU) and the
  * stream goes on (the data are then undefined).  Waiter and signaller must be different
@@ -335,9 +341,9 @@ kv_status kv_pull(int32_t n_src, const kv_layout* const* src, const void* const*
                   int32_t layer_chunk, uint64_t timeout_ns, int32_t* err, kv_stream stream);
 kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, int32_t n_dst,
                    const kv_layout* const* dst, void* const* rings, int32_t ring_slots, size_t slot_bytes,
-                   uint32_t* const* ready_flags, const uint32_t* const* free_flags, uint32_t seq0,
-                   int32_t layer_begin, int32_t layer_end, int32_t layer_chunk, uint64_t timeout_ns, int32_t* err,
-                   kv_stream stream);
+                   uint32_t* const* ready_flags, const uint32_t* const* free_flags, float* const* peer_scales,
+                   uint32_t seq0, int32_t layer_begin, int32_t layer_end, int32_t layer_chunk, uint64_t timeout_ns,
+                   int32_t* err, kv_stream stream);
 kv_status kv_pull_staged(int32_t n_src, const kv_layout* const* src, const void* const* rings, int32_t ring_slots,
                          size_t slot_bytes, const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt,
                          const uint32_t* const* ready_flags, uint32_t* const* free_flags, uint32_t* counters,

@@ -93,8 +93,8 @@ def _load():
                                    i32, p, p, p]),
         "kv_pull": (st, [i32, pp, pp, C.POINTER(Batch_t), p, p, C.POINTER(Batch_t), pp, pp, C.c_uint32, i32, i32, i32,
                          u64, p, p]),
-        "kv_stage": (st, [p, p, C.POINTER(Batch_t), i32, pp, pp, i32, C.c_size_t, pp, pp, C.c_uint32, i32, i32, i32,
-                          u64, p, p]),
+        "kv_stage": (st, [p, p, C.POINTER(Batch_t), i32, pp, pp, i32, C.c_size_t, pp, pp, pp, C.c_uint32, i32, i32,
+                          i32, u64, p, p]),
         "kv_pull_staged": (st, [i32, pp, pp, i32, C.c_size_t, p, p, C.POINTER(Batch_t), pp, pp, p, C.c_uint32, i32,
                                 i32, i32, u64, p, p]),
         "kv_ipc_export": (st, [p, p, C.POINTER(u64)]),

@@ -632,6 +632,12 @@ kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const vo
   const uint64_t items = (uint64_t)ntg * Hd * 2 * (uint64_t)(le - lb);
   if (items > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_compute_scales: batch too large for one call");
   a.n_items = (uint32_t)items;
+  // row path: head_dim innermost with 16-B rows and aligned pools (every source)
+  const int64_t rb = (int64_t)a.D * S->elem_bytes;
+  a.rows = S->d.axis_order[5] == KV_AX_DIM && rb % 16 == 0 && (rb / 16 & (rb / 16 - 1)) == 0 && rb / 16 <= 32;
+  for (int i = 0; i < n_src; ++i) a.rows = a.rows && ptr_aligned(src_pools[i], 16);
+  if (a.rows)
+    while ((1 << a.cpr_shift) < rb / 16) ++a.cpr_shift;
   if (le == lb) return KV_OK;
   cudaError_t e = launch_amax(a, S->d.dtype, out_scales, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kv_compute_scales: launch");

@@ -179,6 +179,11 @@ struct AmaxArgs {
   float qmax;           // largest finite value of the destination fp8 (448 e4m3fn, 240 e4m3fnuz)
   FastDiv f_tg, f_hd, f_bp, f_hp;
   uint32_t n_tok, n_items;
+  // row path (head_dim innermost, 16-B rows): item = (group of kAmaxG token groups, head,
+  // K/V, layer); set by the launcher
+  int32_t rows, cpr_shift;
+  FastDiv f_tgc;
+  uint32_t n_row_items;
 };
 
 // launchers (kvx_kernels.cu); vec = 8 (fast path, DIM innermost) or 1 (generic)

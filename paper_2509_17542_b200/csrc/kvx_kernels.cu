@@ -1143,6 +1143,70 @@ __global__ void __launch_bounds__(kThreads) k_amax(const __grid_constant__ AmaxA
   }
 }
 
+// Row path of the amax pass (head_dim innermost in the source, rows of 16-B multiples):
+// an item is kAmaxG consecutive groups of 32 tokens of one (layer, K/V, head); each lane
+// owns one token row, the warp streams the 32 rows' 16-B chunks with shuffled row
+// addresses (coalesced, like the convert), keeps a running max over the whole item and
+// issues ONE atomicMax -- the element-wise kernel issued one per 32 tokens, and the
+// contention on the few (layer, K/V, head) words made it ~4x slower than a read pass.
+constexpr uint32_t kAmaxG = 16;
+
+template <int SDT>
+__global__ void __launch_bounds__(kThreads) k_amax_rows(const __grid_constant__ AmaxArgs a) {
+  constexpr int VEC = 16 / Tr<SDT>::B;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
+  const uint32_t cs = (uint32_t)a.cpr_shift;
+  const uint32_t cmask = (1u << cs) - 1u, nch = 32u << cs;
+  for (uint32_t item = warp; item < a.n_row_items; item += nwarps) {
+    uint32_t n = item;
+    const uint32_t tgc = divmod(n, a.f_tgc);
+    const uint32_t hq = divmod(n, a.f_hd);
+    const uint32_t c = n & 1u;
+    const int64_t layer = a.lb + (int64_t)(n >> 1);
+    const int64_t sl = layer - a.s_l0;
+    const uint32_t h = (uint32_t)a.q * (uint32_t)a.Hd + hq;
+    const uint32_t p = fdiv(h, a.f_hp);
+    const uint32_t hp = h - p * (uint32_t)a.Hp;
+    const int si = a.src_of_p[p];
+    float sc = 1.f;
+    if constexpr (is_fp8(SDT)) sc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+    const uint8_t* lbase = a.src[si] + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
+                                        (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B;
+    float m = 0.f;
+    for (uint32_t g = 0; g < kAmaxG; ++g) {
+      const uint32_t tok = (tgc * kAmaxG + g) * 32u + lane;
+      if (__all_sync(0xffffffffu, tok >= a.n_tok)) break;
+      uint64_t rp = 0;
+      if (tok < a.n_tok) {
+        const int32_t r = __ldg(a.tok_req + tok);
+        uint32_t t = tok - (uint32_t)__ldg(a.tok_off + r);
+        const uint32_t sslot = divmod(t, a.f_bp);
+        const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + t);
+        rp = (uint64_t)(lbase + (sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT]) * Tr<SDT>::B);
+      }
+#pragma unroll 4
+      for (uint32_t idx = lane; idx < nch; idx += 32u) {
+        const uint64_t r0 = __shfl_sync(0xffffffffu, rp, (idx >> cs) & 31u);
+        if (r0 == 0) continue;
+        Chunk<SDT, VEC> e;
+        load_chunk<SDT, VEC>(e, reinterpret_cast<const uint8_t*>(r0) + (idx & cmask) * 16u);
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+          float v = to_f32<SDT>(get_elem<SDT>(e.w, i));
+          if constexpr (is_fp8(SDT)) v = __fmul_rn(v, sc);
+          v = fabsf(v);
+          if (v <= 3.402823466e38f) m = fmaxf(m, v);  // skips NaN and Inf
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0 && m > 0.f) atomicMax(a.amax_bits + (layer - a.d_l0) * 2 * a.Hd + c * a.Hd + hq, __float_as_uint(m));
+  }
+}
+
 // s = RN(amax / qmax), qmax = the destination fp8's largest finite value (448 / 240)
 __global__ void k_amax_finalize(uint32_t* bits, int64_t begin, int64_t end, float qmax) {
   for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1464,7 +1528,24 @@ cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) 
   const int64_t begin = (int64_t)(a.lb - a.d_l0) * 2 * a.Hd, end = (int64_t)(a.lb - a.d_l0 + a.Lc) * 2 * a.Hd;
   cudaError_t e = cudaMemsetAsync(out + begin, 0, (size_t)(end - begin) * sizeof(float), s);
   if (e != cudaSuccess) return e;
-  if (a.n_items) {
+  if (a.n_items && a.rows) {
+    AmaxArgs b = a;
+    b.f_tgc = make_fastdiv((a.f_tg.d + kAmaxG - 1) / kAmaxG);
+    b.n_row_items = b.f_tgc.d * (uint32_t)a.Hd * 2u * (uint32_t)a.Lc;
+    switch (sdt) {
+      case KV_F16: k_amax_rows<KV_F16><<<grid_for_items(k_amax_rows<KV_F16>, b.n_row_items), kThreads, 0, s>>>(b); break;
+      case KV_BF16: k_amax_rows<KV_BF16><<<grid_for_items(k_amax_rows<KV_BF16>, b.n_row_items), kThreads, 0, s>>>(b); break;
+      case KV_F8E4M3:
+        k_amax_rows<KV_F8E4M3><<<grid_for_items(k_amax_rows<KV_F8E4M3>, b.n_row_items), kThreads, 0, s>>>(b);
+        break;
+      case KV_F8E4M3FNUZ:
+        k_amax_rows<KV_F8E4M3FNUZ><<<grid_for_items(k_amax_rows<KV_F8E4M3FNUZ>, b.n_row_items), kThreads, 0, s>>>(b);
+        break;
+      case KV_F32: k_amax_rows<KV_F32><<<grid_for_items(k_amax_rows<KV_F32>, b.n_row_items), kThreads, 0, s>>>(b); break;
+      default: return cudaErrorInvalidValue;
+    }
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+  } else if (a.n_items) {
     switch (sdt) {
       case KV_F16: k_amax<KV_F16><<<grid_for_items(k_amax<KV_F16>, a.n_items), kThreads, 0, s>>>(a); break;
       case KV_BF16: k_amax<KV_BF16><<<grid_for_items(k_amax<KV_BF16>, a.n_items), kThreads, 0, s>>>(a); break;

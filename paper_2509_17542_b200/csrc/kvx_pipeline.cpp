@@ -206,8 +206,9 @@ inline int32_t ring_slot(uint64_t seq, int32_t R) { return (int32_t)(seq % (uint
 
 kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, int32_t n_dst,
                    const kv_layout* const* dst, void* const* rings, int32_t ring_slots, size_t slot_bytes,
-                   uint32_t* const* ready_flags, const uint32_t* const* free_flags, uint32_t seq0, int32_t lb,
-                   int32_t le, int32_t layer_chunk, uint64_t timeout_ns, int32_t* err, kv_stream stream) {
+                   uint32_t* const* ready_flags, const uint32_t* const* free_flags, float* const* peer_scales,
+                   uint32_t seq0, int32_t lb, int32_t le, int32_t layer_chunk, uint64_t timeout_ns, int32_t* err,
+                   kv_stream stream) {
   if (!src || !src_bt || !dst || n_dst < 1 || !rings || ring_slots < 1 || !ready_flags || !free_flags || !err)
     return fail(KV_EINVAL, "kv_stage: bad argument");
   for (int i = 0; i < n_dst; ++i) {
@@ -221,6 +222,18 @@ kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* s
       if (kv_wire_bytes(src, dst[i], src_bt->total_tokens, l0, std::min(le, l0 + step)) > slot_bytes)
         return fail(KV_ESHAPE, "kv_stage: ring slots smaller than a layer chunk");
   kv_status st;
+  if (peer_scales) {  // dynamic scales: validate (empty ranges) before the first enqueue
+    for (int i = 0; i < n_dst; ++i) {
+      if (!peer_scales[i] || !fp8(dst[i]->d.dtype) || fp8(src->d.dtype) || !dst[i]->d.scales)
+        return fail(KV_EINVAL, "kv_stage: dynamic scales need a non-fp8 source, fp8 destinations with scale "
+                               "arrays and a peer scale array per D rank");
+      const kv_layout* const S1[1] = {src};
+      const void* const P1[1] = {src_pool};
+      if ((st = kv_compute_scales(1, S1, P1, src_bt, dst[i], const_cast<float*>(dst[i]->d.scales), lb, lb,
+                                  stream)) != KV_OK)
+        return st;
+    }
+  }
   uint64_t seq = seq0;
   for (int32_t l0 = lb; l0 < le; l0 += step, ++seq) {
     const int32_t l1 = std::min(le, l0 + step), b = ring_slot(seq, ring_slots);
@@ -229,6 +242,18 @@ kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* s
       if (seq + 1 > (uint64_t)ring_slots &&
           (st = kv_wait(free_flags[i], (uint32_t)(seq + 1 - ring_slots), timeout_ns, err, stream)) != KV_OK)
         return st;
+      if (peer_scales) {
+        // NEXT-1 (i): this chunk's per-(layer, K/V, head) scales from the data (one read pass),
+        // into dst[i]'s own array (the pack quantises with it), then shipped to the D rank
+        // ahead of the ready flag (the codes are useless without them)
+        const kv_layout* const S1[1] = {src};
+        const void* const P1[1] = {src_pool};
+        float* own = const_cast<float*>(dst[i]->d.scales);
+        if ((st = kv_compute_scales(1, S1, P1, src_bt, dst[i], own, l0, l1, stream)) != KV_OK) return st;
+        const size_t off = (size_t)(l0 - dst[i]->d.first_layer) * 2 * dst[i]->h_local;
+        const size_t n = (size_t)(l1 - l0) * 2 * dst[i]->h_local * sizeof(float);
+        if ((st = kv_copy_bytes(peer_scales[i] + off, own + off, n, stream)) != KV_OK) return st;
+      }
       if ((st = kv_pack(src, src_pool, src_bt, dst[i], l0, l1, rings[(size_t)i * ring_slots + b], slot_bytes,
                         stream)) != KV_OK)
         return st;

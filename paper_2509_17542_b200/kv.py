@@ -185,18 +185,20 @@ def pull(src_layouts, src_pools, src_batch: Batch, dst_layout: Layout, dst_pool,
 
 
 def stage(src_layout, src_pool, src_batch: Batch, dst_layouts, rings, ring_slots, slot_bytes, ready_flags,
-          free_flags, seq0, err, layer_range=None, layer_chunk=0, timeout_s=30.0, stream=None):
+          free_flags, seq0, err, layer_range=None, layer_chunk=0, timeout_s=30.0, stream=None, peer_scales=None):
     """kv_stage: P side of a narrowing pull -- pack (sender-side cast) each layer chunk
     into ring slot seq % ring_slots of every D rank once D freed it, then signal ready.
-    rings: flat list, rings[i * ring_slots + b] = slot b for D rank i."""
+    rings: flat list, rings[i * ring_slots + b] = slot b for D rank i.  peer_scales (one
+    peer-mapped D scale array per D rank): dynamic per-chunk fp8 scales, shipped to D."""
     nd = len(dst_layouts)
     Dl = (C.c_void_p * nd)(*[l.handle.value for l in dst_layouts])
     RG = (C.c_void_p * len(rings))(*[_ptr(r) for r in rings])
     RF = (C.c_void_p * nd)(*[_ptr(f) for f in ready_flags])
     FF = (C.c_void_p * nd)(*[_ptr(f) for f in free_flags])
     lb, le = layer_range if layer_range else _common(src_layout, dst_layouts[0])
+    PS = (C.c_void_p * nd)(*[_ptr(x) for x in peer_scales]) if peer_scales is not None else None
     check(lib.kv_stage(src_layout.handle, _ptr(src_pool), C.byref(src_batch.bt), nd, Dl, RG, ring_slots, slot_bytes,
-                       RF, FF, seq0, lb, le, layer_chunk, int(timeout_s * 1e9), _ptr(err), _stream(stream)))
+                       RF, FF, PS, seq0, lb, le, layer_chunk, int(timeout_s * 1e9), _ptr(err), _stream(stream)))
 
 
 def pull_staged(src_layouts, rings, ring_slots, slot_bytes, dst_layout: Layout, dst_pool, dst_batch: Batch,

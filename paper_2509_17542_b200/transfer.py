@@ -115,20 +115,24 @@ class PullChannel:
     len(ring_dst) * ring_slots * slot_bytes bytes; slot b for D rank ring_dst[i] starts at
     (i * ring_slots + b) * slot_bytes).  Afterwards a D rank holds, per P rank p,
     ``src_pool[p]`` / ``src_ring[p]`` (its ring_slots slot addresses) and ``peer_flag[p]``
-    (the word it signals in p's flag array); a P rank holds ``peer_flag[q]`` per D rank q."""
+    (the word it signals in p's flag array); a P rank holds ``peer_flag[q]`` per D rank q and,
+    when D ranks pass ``scales`` (their fp8 scale arrays, for dynamic scales shipped by P),
+    ``peer_scales[q]``."""
 
     def __init__(self, role: Role, flags, pool=None, ring=None, ring_dst=(), ring_slots=0, slot_bytes=0,
-                 group=None, ipc_export=None, ipc_open=None):
+                 group=None, ipc_export=None, ipc_open=None, scales=None):
         ipc_export = ipc_export or kv.ipc_export
         ipc_open = ipc_open or kv.ipc_open
         mine = {"kind": role.kind, "r": role.tp_rank, "flags": ipc_export(flags) if role.kind in "PD" else None,
                 "pool": ipc_export(pool) if pool is not None else None,
                 "ring": ipc_export(ring) if ring is not None else None, "ring_dst": list(ring_dst),
-                "ring_slots": ring_slots, "slot_bytes": slot_bytes}
+                "ring_slots": ring_slots, "slot_bytes": slot_bytes,
+                "scales": ipc_export(scales) if scales is not None else None}
         allv = exchange(mine, group)
         self.role = role
         self.src_pool, self.src_ring, self.peer_flag, self._mapped = {}, {}, {}, []
         self.slot_bytes = {}   # D side: P rank p's ring slot size
+        self.peer_scales = {}  # P side: D rank q's scale array
         if role.kind not in "PD":
             return
         other = "P" if role.kind == "D" else "D"
@@ -140,6 +144,9 @@ class PullChannel:
                 base = ipc_open(*ent["flags"])
                 self._mapped.append((base, ent["flags"][1]))
                 self.peer_flag[ent["r"]] = base + 4 * role.tp_rank
+                if ent["scales"] is not None:
+                    self.peer_scales[ent["r"]] = ipc_open(*ent["scales"])
+                    self._mapped.append((self.peer_scales[ent["r"]], ent["scales"][1]))
                 continue
             p, q = ent["r"], role.tp_rank
             if ent["pool"] is None and (ent["ring"] is None or q not in ent["ring_dst"]):

@@ -63,7 +63,8 @@ def _worker(rank, port, blob, mode, q):
                 q.put((rank, [a.copy() for a in dc.dst_numpy()]))
                 dist.barrier()
         elif mode.startswith("pull"):
-            _pull_worker(rank, dc, kvx, tr, dist, q, mode.startswith("pull_staged"), mode == "pull_staged")
+            _pull_worker(rank, dc, kvx, tr, dist, q, mode.startswith("pull_staged"),
+                         mode in ("pull_staged", "pull_staged_dyn"), mode == "pull_staged_dyn")
         else:
             uid = kvx.Comm.unique_id() if rank == 0 else None
             lst = [uid]
@@ -89,7 +90,7 @@ def _worker(rank, port, blob, mode, q):
         dist.destroy_process_group()
 
 
-def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent):
+def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent, dyn=False):
     """P = rank 0 (all P ranks, one stream each), D = rank 1 (all D ranks, one stream each).
     Flag words: D's ready[q * 8 + p] (P writes), P's done / free[p * 8 + q] (D writes)."""
     dev = f"cuda:{rank}"
@@ -107,6 +108,8 @@ def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent):
         for p, qq, _, _ in pairs:
             rings[(p, qq)] = torch.empty(R * nb, dtype=torch.uint8, device=dev)
     exp = {"flags": kvx.ipc_export(flags)}
+    if rank == 1 and dyn:   # D's scale arrays: P computes the dynamic scales and writes them here
+        exp["scales"] = [kvx.ipc_export(lay.scales) for lay in D]
     if rank == 0:
         exp["src"] = {k: kvx.ipc_export(v) for k, v in rings.items()} if staged else \
             [kvx.ipc_export(pl) for pl in dc.src_pools]
@@ -115,6 +118,10 @@ def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent):
     fbase = kvx.ipc_open(*other["flags"])
     maps = [(fbase, other["flags"][1])]
     streams = {}
+    peer_sc = []
+    if rank == 0 and dyn:
+        peer_sc = [kvx.ipc_open(h, o) for h, o in other["scales"]]
+        maps += [(a, o) for a, (h, o) in zip(peer_sc, other["scales"])]
     if rank == 0:
         for p in range(len(S)):
             qs = [qq for pp, qq, _, _ in pairs if pp == p]
@@ -124,7 +131,8 @@ def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent):
                     kvx.stage(S[p], dc.src_pools[p], dc.src_bt, [D[qq] for qq in qs],
                               [rings[(p, qq)].data_ptr() + b * nb for qq in qs for b in range(R)], R, nb,
                               [fbase + 4 * (qq * 8 + p) for qq in qs], [flags[p * 8 + qq:p * 8 + qq + 1] for qq in qs],
-                              0, err, (0, L), lc, 20.0, st)
+                              0, err, (0, L), lc, 20.0, st,
+                              peer_scales=[peer_sc[qq] for qq in qs] if dyn else None)
                     for qq in qs:   # all chunks consumed: free >= number of chunks
                         kvx.wait(flags[p * 8 + qq:p * 8 + qq + 1], L, err, 20.0, st)
                 else:
@@ -164,13 +172,16 @@ def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent):
             for c in counters.values():
                 nxt, done = c[:L].cpu(), c[L:].cpu()
                 assert bool((done > 0).all()) and bool((nxt >= done).all())
-        q.put((rank, [a.copy() for a in dc.dst_numpy()]))
+        res = [a.copy() for a in dc.dst_numpy()]
+        if dyn:
+            res = (res, [lay.scales.cpu().numpy().reshape(L, 2, -1) for lay in D])
+        q.put((rank, res))
         dist.barrier()
     for a, o in maps:
         kvx.ipc_close(a, o)
 
 
-@pytest.mark.parametrize("mode", ["push", "nccl", "pull", "pull_staged", "pull_staged_chunked"])
+@pytest.mark.parametrize("mode", ["push", "nccl", "pull", "pull_staged", "pull_staged_chunked", "pull_staged_dyn"])
 @pytest.mark.parametrize("shape", ["merge", "split_fp8"])
 def test_p_to_d_across_gpus(o1, mode, shape):
     if torch.cuda.device_count() < 2:
@@ -179,6 +190,8 @@ def test_p_to_d_across_gpus(o1, mode, shape):
     from synth import BF16, E4M3, F16
     from tests.kvcase import expected, make_case
     from tests.test_gpu_parity import assert_pools_match
+    if mode == "pull_staged_dyn" and shape == "merge":
+        pytest.skip("dynamic scales need each P rank to hold all of its D ranks' heads (bf16 merge has no fp8)")
     if shape == "merge":   # c3-like: TP4 -> TP2, block 16 -> 64
         case = make_case(4, 8, 128, 4, 2, 16, 64, [300, 77, 1], BF16, BF16, seed=3, o1=o1)
     else:                  # c5-like split TP2 -> TP4 with a c4-like fp8 cast
@@ -194,4 +207,13 @@ def test_p_to_d_across_gpus(o1, mode, shape):
     for p in ps:
         p.join(timeout=120)
         assert p.exitcode == 0
+    if mode == "pull_staged_dyn":
+        # NEXT-1 (i): the shipped scales are O1's amax scales; the codes decode with them
+        got, got_sc = res[1]
+        for qq, lay in enumerate(case["dst_lays"]):
+            want_sc = o1.amax_scales(case["src_lays"], case["src_pools"], lay, case["n_tokens"], case["src_tables"])
+            assert np.array_equal(got_sc[qq], want_sc), f"D{qq} scales"
+            lay["scales"] = want_sc
+        assert_pools_match(got, expected(case, o1), case["dst_lays"][0]["dtype"])
+        return
     assert_pools_match(res[1], expected(case, o1), case["dst_lays"][0]["dtype"])

@@ -433,3 +433,21 @@ def test_dynamic_scales_then_convert(o1, sdt):
         dl.scales.copy_(out.view(dl.scales.shape))
     dc.convert()
     assert_pools_match(dc.dst_numpy(), expected(case, o1), E4M3)
+
+
+@pytest.mark.parametrize("order_i,ddt", [(0, E4M3), (201, E4M3), (0, FNUZ), (517, FNUZ)])
+def test_dynamic_scales_row_and_generic_paths(o1, order_i, ddt):
+    """kv_compute_scales on both amax kernels -- the row path (head_dim innermost) and the
+    element-wise path (any other source order) -- against O1, for e4m3fn (amax/448) and
+    e4m3fnuz (amax/240) destinations, with a ragged batch over several token groups."""
+    from tests.gpu_util import DevCase
+    import paper_2509_17542_b200 as kvx
+    so = synth.P_ORDER if order_i == 0 else ALL_ORDERS[order_i]
+    case = make_case(2, 4, 32, 2, 1, 8, 16, [700, 33, 1, 290], BF16, ddt, so, seed=90 + order_i, o1=o1, scales=1.0)
+    dc = DevCase(case)
+    out = torch.full((2, 2, 4), -1.0, dtype=torch.float32, device="cuda")
+    kvx.compute_scales(dc.src_lays, dc.src_pools, dc.src_bt, dc.dst_lays[0], out)
+    torch.cuda.synchronize()
+    want = o1.amax_scales(case["src_lays"], case["src_pools"], case["dst_lays"][0], case["n_tokens"],
+                          case["src_tables"])
+    assert np.array_equal(out.cpu().numpy(), want)
