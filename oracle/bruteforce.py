@@ -166,16 +166,36 @@ def cast(code: int, src_dt: int, dst_dt: int, src_scale: float = 1.0, dst_scale:
     return round_to(x, dst_dt)
 
 
+XLO = 6  # the innermost x part of a split head_dim (reading 27)
+
+
+def _split(lay):
+    x = lay.get("dim_split", 0)
+    return x if x > 1 else 1
+
+
+def _held(lay):
+    """Global K/V indices a pool holds (kv_part 0: both, 1: K, 2: V)."""
+    return {0: (0, 1), 1: (0,), 2: (1,)}[lay.get("kv_part", 0)]
+
+
 def _extents(lay):
-    return {LAYER: lay["L"], KV: 2, BLOCK: lay["NB"], SLOT: lay["B"], HEAD: lay["H"] // lay["tp"], DIM: lay["D"]}
+    return {LAYER: lay["L"], KV: len(_held(lay)), BLOCK: lay["NB"], SLOT: lay["B"], HEAD: lay["H"] // lay["tp"],
+            DIM: lay["D"] // _split(lay), XLO: _split(lay)}
 
 
 def positions(lay):
-    """Yield (linear position, {axis: index}) over the pool in memory order."""
+    """Yield (linear position, {axis: index}) over the pool in memory order, with the K/V
+    index global (0 K, 1 V) and DIM the full head_dim index (split parts recombined)."""
     ext = _extents(lay)
-    order = lay["order"]
+    order = tuple(lay["order"]) + (XLO,)
+    held = _held(lay)
+    x = _split(lay)
     for pos, idx in enumerate(itertools.product(*[range(ext[a]) for a in order])):
-        yield pos, dict(zip(order, idx))
+        ix = dict(zip(order, idx))
+        ix[KV] = held[ix[KV]]
+        ix[DIM] = ix[DIM] * x + ix.pop(XLO)
+        yield pos, ix
 
 
 def _inverse_table(tables):
@@ -219,14 +239,16 @@ def convert(src_lays, src_pools, dst_lays, dst_pools, n_tokens, src_tables, dst_
                 continue  # source tail: never read
             h = lay["rank"] * hp_n + ix[HEAD]
             logical[(r, f + ix[LAYER], ix[KV], h, t, ix[DIM])] = (pool[pos], lay, ix[HEAD], ix[LAYER])
-    # 2. every destination position, destination-driven by enumeration
+    # 2. every destination position, destination-driven by enumeration (only the K/V the
+    #    sources hold is written: a K-only source fills only the K part of a K+V pool)
     dst_inv = _inverse_table(dst_tables)
+    src_held = set(_held(src_lays[0]))
     for lay, pool in zip(dst_lays, dst_pools):
         hd_n = lay["H"] // lay["tp"]
         f = lay.get("first_layer", 0)
         for pos, ix in positions(lay):
             g = f + ix[LAYER]
-            if ix[BLOCK] not in dst_inv or not (lb <= g < le):
+            if ix[BLOCK] not in dst_inv or not (lb <= g < le) or ix[KV] not in src_held:
                 continue
             r, j = dst_inv[ix[BLOCK]]
             t = j * lay["B"] + ix[SLOT]

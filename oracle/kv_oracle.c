@@ -62,8 +62,17 @@ typedef struct {
   int32_t block_size, num_blocks;
   int32_t dtype;
   int32_t axis_order[6]; /* outermost -> innermost, dense row-major */
+  int32_t kv_part;       /* 0: the pool holds K and V; 1: K only; 2: V only (KV extent 1) */
+  int32_t dim_split;     /* x > 1: head_dim stored as (D/x at DIM's place, x innermost) */
   const float* scales;   /* host [L][2][H_local] fp32 dequant scales (fp8 only) */
 } okv_layout;
+
+/* NEXT-3 layout variants (reading 27): a pool may hold only K or only V (engines
+ * that keep separate K and V tensors, with different axis orders), and head_dim may be split
+ * into (D/x, ..., x) with the x part innermost -- the "x-packed" key cache of the paged-
+ * attention kernels other vendors' engines use, K [blocks, heads, D/x, block, x]. */
+static int holds(const okv_layout* L, int32_t c) { return L->kv_part == 0 || L->kv_part == c + 1; }
+static int64_t split_of(const okv_layout* L) { return L->dim_split > 1 ? L->dim_split : 1; }
 
 /* ------------------------------------------------------------------------ */
 /* Sizes                                                                    */
@@ -93,36 +102,37 @@ int64_t okv_kv_bytes(int64_t layers, int64_t kv_heads, int64_t head_dim, int64_t
 static int64_t extent_of(const okv_layout* L, int axis) {
   switch (axis) {
     case OAX_LAYER: return L->num_layers;
-    case OAX_KV: return 2;
+    case OAX_KV: return L->kv_part ? 1 : 2;
     case OAX_BLOCK: return L->num_blocks;
     case OAX_SLOT: return L->block_size;
     case OAX_HEAD: return L->num_kv_heads / L->tp_degree;
-    case OAX_DIM: return L->head_dim;
+    case OAX_DIM: return L->head_dim / split_of(L);
   }
   return 0;
 }
 
 /* Element offset of (l, c, block, slot, local head, d): sum over axes of
- * index * stride, strides row-major over axis_order. */
+ * index * stride, strides row-major over axis_order (then the x part of a split head_dim,
+ * innermost).  c is the global K/V index; a K-only or V-only pool stores it at 0. */
 int64_t okv_offset(const okv_layout* L, int64_t l, int64_t c, int64_t blk, int64_t slot,
                    int64_t hl, int64_t d) {
   int64_t idx[6];
   idx[OAX_LAYER] = l;
-  idx[OAX_KV] = c;
+  idx[OAX_KV] = L->kv_part ? 0 : c;
   idx[OAX_BLOCK] = blk;
   idx[OAX_SLOT] = slot;
   idx[OAX_HEAD] = hl;
-  idx[OAX_DIM] = d;
+  idx[OAX_DIM] = d / split_of(L);
   int64_t off = 0;
   for (int i = 0; i < 6; ++i) {
     int a = L->axis_order[i];
     off = off * extent_of(L, a) + idx[a];
   }
-  return off;
+  return off * split_of(L) + d % split_of(L);
 }
 
 int64_t okv_pool_elems(const okv_layout* L) {
-  int64_t n = 1;
+  int64_t n = split_of(L);
   for (int a = 0; a < 6; ++a) n *= extent_of(L, a);
   return n;
 }
@@ -402,6 +412,7 @@ int32_t okv_convert(int32_t n_src, const okv_layout* src, void* const* src_pools
               if (src[i].tp_rank == p) pi = i;
             if (pi < 0) return -2 - p; /* missing source shard p */
             const okv_layout* Lp = &src[pi];
+            if (!holds(Lp, c) || !holds(Ld, c)) continue; /* K/V the two pools share only */
             int32_t ls = l - Lp->first_layer, ld = l - Ld->first_layer; /* pool-local layers */
             float sd = scale_of(Ld, ld, c, hq);
             float ss = scale_of(Lp, ls, c, hp);
@@ -445,6 +456,7 @@ int64_t okv_flatten(const okv_layout* Lp, const void* src_pool, const okv_layout
   int64_t w = 0;
   for (int32_t l = layer_begin; l < layer_end; ++l)
     for (int32_t c = 0; c < 2; ++c)
+      if (holds(Lp, c) && holds(Ld, c)) /* the wire carries the K/V both pools hold */
       for (int32_t h = hb; h < he; ++h)
         for (int32_t r = 0; r < n_req; ++r)
           for (int64_t t = 0; t < n_tokens[r]; ++t) {
@@ -475,6 +487,7 @@ int64_t okv_restore(const okv_layout* Lp, const okv_layout* Ld, void* dst_pool, 
   int64_t w = 0;
   for (int32_t l = layer_begin; l < layer_end; ++l)
     for (int32_t c = 0; c < 2; ++c)
+      if (holds(Lp, c) && holds(Ld, c))
       for (int32_t h = hb; h < he; ++h)
         for (int32_t r = 0; r < n_req; ++r) {
           int64_t T = n_tokens[r];
@@ -508,7 +521,8 @@ void okv_cast_array(int64_t n, const void* in, int32_t src_dt, int32_t dst_dt, f
  * e4m3fn, 240 e4m3fnuz) and amax = max |x| (x as f32, fp8 sources dequantised
  * with their own scale) over every finite source element of the valid tokens of all
  * requests for the heads of D rank dst; s = 1 if amax is 0.  Layers [lb, le) are written
- * into out[L][2][H_d]; other entries untouched.  Returns 0, or <0 if a shard is missing. */
+ * into out[L][2][H_d] for the K/V both layouts hold; other entries untouched.  Returns 0,
+ * or <0 if a shard is missing. */
 int32_t okv_amax_scales(int32_t n_src, const okv_layout* src, void* const* src_pools, const okv_layout* dst,
                         int32_t n_req, const int32_t* n_tokens, const int32_t* src_bt_off,
                         const int32_t* src_bt_ids, int32_t layer_begin, int32_t layer_end, float* out) {
@@ -523,6 +537,7 @@ int32_t okv_amax_scales(int32_t n_src, const okv_layout* src, void* const* src_p
           if (src[i].tp_rank == p) pi = i;
         if (pi < 0) return -2 - p;
         const okv_layout* Lp = &src[pi];
+        if (!holds(Lp, c) || !holds(dst, c)) continue; /* entries of K/V not shared: untouched */
         float amax = 0.0f;
         for (int32_t r = 0; r < n_req; ++r)
           for (int64_t t = 0; t < n_tokens[r]; ++t) {

@@ -38,7 +38,7 @@ class _Layout(C.Structure):
                 ("head_dim", C.c_int32),
                 ("tp_degree", C.c_int32), ("tp_rank", C.c_int32), ("block_size", C.c_int32),
                 ("num_blocks", C.c_int32), ("dtype", C.c_int32), ("axis_order", C.c_int32 * 6),
-                ("scales", C.POINTER(C.c_float))]
+                ("kv_part", C.c_int32), ("dim_split", C.c_int32), ("scales", C.POINTER(C.c_float))]
 
 
 def lib():
@@ -92,6 +92,7 @@ def _mk(lay, keep):
     s.block_size, s.num_blocks, s.dtype = lay["B"], lay["NB"], lay["dtype"]
     for i, a in enumerate(lay["order"]):
         s.axis_order[i] = a
+    s.kv_part, s.dim_split = lay.get("kv_part", 0), lay.get("dim_split", 0)
     sc = lay.get("scales")
     if sc is not None:
         arr = np.ascontiguousarray(np.asarray(sc, dtype=np.float32))
@@ -113,6 +114,13 @@ def csr(tables):
         off[r + 1] = off[r] + len(t)
     ids = np.concatenate([np.asarray(t, dtype=np.int32) for t in tables]) if tables else np.zeros(0, np.int32)
     return off, ids
+
+
+def n_kv(a, b):
+    """How many of K, V both pools hold (kv_part 0 both, 1 K only, 2 V only)."""
+    ha = {0: {0, 1}, 1: {0}, 2: {1}}[a.get("kv_part", 0)]
+    hb = {0: {0, 1}, 1: {0}, 2: {1}}[b.get("kv_part", 0)]
+    return len(ha & hb)
 
 
 def layer_span(a, b):
@@ -187,7 +195,7 @@ def flatten(src_lay, src_pool, dst_lay, n_tokens, src_tables, layer_range=None):
     Hp, Hd = H // src_lay["tp"], H // dst_lay["tp"]
     nh = max(0, min((p + 1) * Hp, (q + 1) * Hd) - max(p * Hp, q * Hd))
     lb, le = layer_range if layer_range else layer_span(src_lay, dst_lay)
-    n = 2 * (le - lb) * nh * int(np.sum(n_tokens)) * src_lay["D"]
+    n = n_kv(src_lay, dst_lay) * (le - lb) * nh * int(np.sum(n_tokens)) * src_lay["D"]
     wire = np.zeros(n, dtype=NPTYPE[NBYTES[wdt]])
     so, si = csr(src_tables)
     w = lib().okv_flatten(C.byref(_mk(src_lay, keep)), src_pool.ctypes.data, C.byref(_mk(dst_lay, keep)), wdt,

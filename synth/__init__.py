@@ -38,10 +38,11 @@ D_ORDER = (BLOCK, LAYER, KV, HEAD, SLOT, DIM)
 CANARY = 0xA5
 
 
-def layout(L, H, D, tp, rank, B, NB, dtype, order, scales=None):
-    """Layout dict used by tests/bench (same fields as kv_layout_desc)."""
+def layout(L, H, D, tp, rank, B, NB, dtype, order, scales=None, kv_part=0, dim_split=0):
+    """Layout dict used by tests/bench (same fields as kv_layout_desc).  kv_part: 0 K and V,
+    1 K only, 2 V only; dim_split: x > 1 stores head_dim as (D/x, ..., x)."""
     return {"L": L, "H": H, "D": D, "tp": tp, "rank": rank, "B": B, "NB": NB, "dtype": dtype,
-            "order": tuple(order), "scales": scales}
+            "order": tuple(order), "scales": scales, "kv_part": kv_part, "dim_split": dim_split}
 
 
 def blocks_for(tokens: int, block_size: int) -> int:

@@ -18,7 +18,7 @@ NAN_GARBAGE = {F16: 0x7E01, BF16: 0x7FC1, E4M3: 0x7F, F32: 0x7FC00001, FNUZ: 0x8
 
 def make_case(L, H, D, tp_p, tp_d, B_p, B_d, n_tokens, src_dt, dst_dt, p_order=synth.P_ORDER,
               d_order=synth.D_ORDER, seed=0, contiguous=False, scales="amax", o1=None, tail_garbage=True,
-              values="random", NB_p=None, NB_d=None):
+              values="random", NB_p=None, NB_d=None, p_kv_part=0, d_kv_part=0, p_split=0, d_split=0):
     """Build src pools (random finite bits), canary dst pools, tables, layouts.
 
     scales: None | "amax" | "pow2" | float -- fp8 dequant scales for fp8 dst ranks."""
@@ -28,8 +28,8 @@ def make_case(L, H, D, tp_p, tp_d, B_p, B_d, n_tokens, src_dt, dst_dt, p_order=s
     dst_tables = synth.block_tables(seed + 2, n_tokens, B_d, NB_d, contiguous)
     src_lays, src_pools = [], []
     for p in range(tp_p):
-        lay = synth.layout(L, H, D, tp_p, p, B_p, NB_p, src_dt, p_order)
-        n = 2 * L * NB_p * B_p * (H // tp_p) * D
+        lay = synth.layout(L, H, D, tp_p, p, B_p, NB_p, src_dt, p_order, kv_part=p_kv_part, dim_split=p_split)
+        n = (1 if p_kv_part else 2) * L * NB_p * B_p * (H // tp_p) * D
         if values == "random":
             pool = synth.random_finite_bits(seed + 100 + p, n, src_dt)
         elif values == "zeros":
@@ -51,8 +51,8 @@ def make_case(L, H, D, tp_p, tp_d, B_p, B_d, n_tokens, src_dt, dst_dt, p_order=s
                 sc = np.exp(rng.uniform(np.log(1e-3), np.log(1e3), size=(L, 2, Hd))).astype(np.float32)
             else:
                 sc = np.full((L, 2, Hd), float(scales), dtype=np.float32)
-        lay = synth.layout(L, H, D, tp_d, q, B_d, NB_d, dst_dt, d_order, sc)
-        n = 2 * L * NB_d * B_d * (H // tp_d) * D
+        lay = synth.layout(L, H, D, tp_d, q, B_d, NB_d, dst_dt, d_order, sc, kv_part=d_kv_part, dim_split=d_split)
+        n = (1 if d_kv_part else 2) * L * NB_d * B_d * (H // tp_d) * D
         pool = np.full(n * NBYTES[dst_dt], synth.CANARY, dtype=np.uint8).view(NPTYPE[NBYTES[dst_dt]])
         dst_lays.append(lay)
         dst_pools.append(pool)
@@ -61,6 +61,11 @@ def make_case(L, H, D, tp_p, tp_d, B_p, B_d, n_tokens, src_dt, dst_dt, p_order=s
     if tail_garbage and o1 is not None:
         put_tail_garbage(case, o1)
     return case
+
+
+def held(lay):
+    """Global K/V indices a pool holds (kv_part 0: both, 1: K only, 2: V only)."""
+    return {0: (0, 1), 1: (0,), 2: (1,)}[lay.get("kv_part", 0)]
 
 
 def put_tail_garbage(case, o1):
@@ -73,7 +78,7 @@ def put_tail_garbage(case, o1):
             for t in range(T, len(tab) * B):
                 blk, slot = tab[t // B], t % B
                 for l in range(lay["L"]):
-                    for c in range(2):
+                    for c in held(lay):
                         for hl in range(lay["H"] // lay["tp"]):
                             for d in range(lay["D"]):
                                 pool[o1.offset(lay, l, c, blk, slot, hl, d)] = g
@@ -105,7 +110,7 @@ def coord_fill(case, o1):
             tab = case["src_tables"][r]
             for t in range(T):
                 for l in range(L):
-                    for c in range(2):
+                    for c in held(lay):
                         for hl in range(Hp):
                             for d in range(D):
                                 pool[o1.offset(lay, l, c, tab[t // B], t % B, hl, d)] = \

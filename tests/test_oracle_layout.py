@@ -298,3 +298,75 @@ def test_missing_source_shard_is_error(o1):
     with pytest.raises(ValueError, match="missing source rank 1"):
         o1.convert(case["src_lays"][:1], case["src_pools"][:1], case["dst_lays"], case["dst_pools"],
                    case["n_tokens"], case["src_tables"], case["dst_tables"])
+
+
+# ---- NEXT-3 layout variants: K-only / V-only pools, x-split head_dim (reading 27) -------
+HELD = {0: (0, 1), 1: (0,), 2: (1,)}
+
+
+@pytest.mark.parametrize("i", range(0, 720, 37))
+@pytest.mark.parametrize("kv_part,x", [(0, 4), (1, 8), (2, 1), (1, 2), (2, 8)])
+def test_split_and_kv_part_numpy_special_case(o1, i, kv_part, x):
+    """Identity tables, one request filling whole blocks, TP 1->1, same dtype: converting a
+    canonical pool into a K-only / V-only pool with an x-split head_dim is numpy's
+    select(K/V) -> reshape(D -> D/x, x) -> transpose(axis order, x innermost)."""
+    L, H, D, B, NB = 2, 3, 8, 4, 3
+    src = synth.layout(L, H, D, 1, 0, B, NB, F16, (LAYER, KV, BLOCK, SLOT, HEAD, DIM))
+    order = ALL_ORDERS[i]
+    dst = synth.layout(L, H, D, 1, 0, B, NB, F16, order, kv_part=kv_part, dim_split=x)
+    X = np.arange(2 * L * NB * B * H * D, dtype=np.uint16).reshape(L, 2, NB, B, H, D)
+    nkv = len(HELD[kv_part])
+    out = np.full(nkv * L * NB * B * H * D, 0xA5A5, np.uint16)
+    o1.convert([src], [X.reshape(-1)], [dst], [out], [NB * B], [list(range(NB))], [list(range(NB))])
+    Y = X[:, list(HELD[kv_part])]                                   # (L, nkv, NB, B, H, D)
+    Y = Y.reshape(L, nkv, NB, B, H, D // x, x)                       # split head_dim
+    Y = np.transpose(Y, list(order) + [6])                          # Y's axes are canonical: axis id = position
+    assert np.array_equal(out, Y.reshape(-1))
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_o1_vs_o2_layout_variants(o1, seed):
+    """O1 == O2 on random tiny cases where either side is K-only / V-only / both and either
+    side splits head_dim (only the K/V both sides hold is written; canary elsewhere)."""
+    rng = np.random.default_rng(1000 + seed)
+    tp_p, tp_d = rng.choice([1, 2], size=2)
+    Bp, Bd = rng.choice([1, 2, 4], size=2)
+    pk = int(rng.integers(0, 3))
+    dk = int(rng.choice([k for k in range(3) if set(HELD[k]) & set(HELD[pk])]))
+    px, dx = int(rng.choice([0, 2, 4])), int(rng.choice([0, 2, 4]))
+    src_dt, dst_dt = [(F16, F16), (BF16, E4M3), (F16, BF16), (BF16, BF16)][seed % 4]
+    n_tokens = [int(t) for t in rng.integers(1, 9, size=int(rng.integers(1, 3)))]
+    case = make_case(2, 4, 4, int(tp_p), int(tp_d), int(Bp), int(Bd), n_tokens, src_dt, dst_dt,
+                     ALL_ORDERS[int(rng.integers(720))], ALL_ORDERS[int(rng.integers(720))], seed=seed, o1=o1,
+                     p_kv_part=pk, d_kv_part=dk, p_split=px, d_split=dx)
+    want = expected(case, o1)
+    lsts = [p.tolist() for p in case["dst_pools"]]
+    o2.convert(case["src_lays"], [p.tolist() for p in case["src_pools"]], case["dst_lays"], lsts,
+               case["n_tokens"], case["src_tables"], case["dst_tables"])
+    for w, g in zip(want, lsts):
+        assert w.tolist() == g
+
+
+def test_k_and_v_pools_reassemble_the_combined_pool(o1):
+    """Converting a K+V source into a K-only and a V-only destination (two calls) puts the
+    same codes where one combined destination gets them: the K/V split is pure placement."""
+    base = dict(L=2, H=4, D=8, tp_p=2, tp_d=1, B_p=4, B_d=8, n_tokens=[9, 3])
+    args = (base["L"], base["H"], base["D"], base["tp_p"], base["tp_d"], base["B_p"], base["B_d"], base["n_tokens"],
+            BF16, F16)
+    both = make_case(*args, seed=5, o1=o1, d_order=(BLOCK, LAYER, KV, HEAD, SLOT, DIM))
+    korder = (BLOCK, HEAD, DIM, SLOT, LAYER, KV)       # x-packed key cache style
+    vorder = (BLOCK, HEAD, DIM, SLOT, LAYER, KV)       # head_dim before slot (value cache style)
+    k = make_case(*args, seed=5, o1=o1, d_order=korder, d_kv_part=1, d_split=4)
+    v = make_case(*args, seed=5, o1=o1, d_order=vorder, d_kv_part=2)
+    wb, wk, wv = expected(both, o1)[0], expected(k, o1)[0], expected(v, o1)[0]
+    B, NB = base["B_d"], both["dst_lays"][0]["NB"]
+    for r, T in enumerate(base["n_tokens"]):
+        for t in range(T):
+            blk, slot = both["dst_tables"][r][t // B], t % B
+            for l in range(2):
+                for hl in range(4):
+                    for d in range(8):
+                        a = wb[o1.offset(both["dst_lays"][0], l, 0, blk, slot, hl, d)]
+                        assert a == wk[o1.offset(k["dst_lays"][0], l, 0, blk, slot, hl, d)]
+                        a = wb[o1.offset(both["dst_lays"][0], l, 1, blk, slot, hl, d)]
+                        assert a == wv[o1.offset(v["dst_lays"][0], l, 1, blk, slot, hl, d)]
