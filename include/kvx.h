@@ -81,6 +81,15 @@ typedef struct {
   int32_t num_blocks;    /* pool capacity in blocks */
   int32_t dtype;         /* kv_dtype */
   int32_t axis_order[6]; /* kv_axis, outermost -> innermost; the pool is dense row-major in it */
+  int32_t kv_part;       /* 0: the pool holds K and V; 1: K only; 2: V only (its KV axis has extent
+                          * 1).  Engines that keep K and V in separate tensors -- possibly with
+                          * different axis orders -- describe each as its own layout; a call
+                          * moves the K/V both pools hold (KV_ESHAPE if none).  NEXT-3. */
+  int32_t dim_split;     /* 0 or 1: none.  x > 1 (a power of two dividing head_dim): head_dim is
+                          * stored as (head_dim/x at DIM's place in axis_order, then x innermost)
+                          * -- the "x-packed" key cache (K [blocks, heads, D/x, block, x], x =
+                          * 16 bytes / element) of other vendors' paged-attention kernels.
+                          * Such pools take the element-wise kernels.  NEXT-3. */
   const float* scales;   /* fp8 dtypes only: DEVICE fp32 [num_layers][2][H/tp] dequant scales s
                           * (real value = code * s), indexed by the pool-local layer; NULL
                           * for other dtypes */
@@ -222,7 +231,7 @@ kv_status kv_unpack(const kv_layout* src, const kv_layout* dst, void* dst_pool, 
  *   24 i32 layer_begin        28 i32 layer_end          32 i32 P tp_degree
  *   36 i32 P tp_rank          40 i32 D tp_degree        44 i32 D tp_rank
  *   48 i32 head_begin         52 i32 head_end (the global overlap heads carried)
- *   56 i32 n_req              60 u32 reserved (0)       64 u64 payload bytes
+ *   56 i32 n_req              60 u32 K/V carried (0 both, 1 K, 2 V)   64 u64 payload bytes
  *   72 i32 n_tokens[n_req]
  * The payload that follows in a file is the kv_pack output (kv_wire_bytes bytes, Fig. 5
  * canonical order).  kv_wire_header_write: KV_ESHAPE if cap is too small or the ranks share
@@ -232,6 +241,7 @@ kv_status kv_unpack(const kv_layout* src, const kv_layout* dst, void* dst_pool, 
 typedef struct {
   int32_t wire_dtype, num_kv_heads, head_dim, layer_begin, layer_end;
   int32_t src_tp_degree, src_tp_rank, dst_tp_degree, dst_tp_rank, head_begin, head_end, n_req;
+  int32_t kv_part;  /* K/V the payload carries: 0 both, 1 K only, 2 V only */
   uint64_t payload_bytes;
   const int32_t* n_tokens; /* points into the header buffer */
 } kv_wire_info;

@@ -32,7 +32,7 @@ class LayoutDesc(C.Structure):
                 ("head_dim", C.c_int32),
                 ("tp_degree", C.c_int32), ("tp_rank", C.c_int32), ("block_size", C.c_int32),
                 ("num_blocks", C.c_int32), ("dtype", C.c_int32), ("axis_order", C.c_int32 * 6),
-                ("scales", C.c_void_p)]
+                ("kv_part", C.c_int32), ("dim_split", C.c_int32), ("scales", C.c_void_p)]
 
 
 class Batch_t(C.Structure):
@@ -47,7 +47,7 @@ class WireInfo(C.Structure):
     _fields_ = [("wire_dtype", C.c_int32), ("num_kv_heads", C.c_int32), ("head_dim", C.c_int32),
                 ("layer_begin", C.c_int32), ("layer_end", C.c_int32), ("src_tp_degree", C.c_int32),
                 ("src_tp_rank", C.c_int32), ("dst_tp_degree", C.c_int32), ("dst_tp_rank", C.c_int32),
-                ("head_begin", C.c_int32), ("head_end", C.c_int32), ("n_req", C.c_int32),
+                ("head_begin", C.c_int32), ("head_end", C.c_int32), ("n_req", C.c_int32), ("kv_part", C.c_int32),
                 ("payload_bytes", C.c_uint64), ("n_tokens", C.POINTER(C.c_int32))]
 
 

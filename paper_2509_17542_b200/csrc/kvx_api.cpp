@@ -29,6 +29,15 @@ kv_status cuda_fail(cudaError_t e, const char* what) {
 
 bool fp8(int32_t dt) { return dt == KV_F8E4M3 || dt == KV_F8E4M3FNUZ; }
 
+kv_status kv_pair(const kv_layout* s, const kv_layout* d, int32_t* kv1, int32_t* c0) {
+  static const int mask[3] = {3, 1, 2};  // bit c set: the pool holds K (c=0) / V (c=1)
+  const int m = mask[s->d.kv_part] & mask[d->d.kv_part];
+  if (!m) return fail(KV_ESHAPE, "P and D layouts share neither K nor V (kv_part)");
+  *kv1 = m == 3 ? 0 : 1;
+  *c0 = m == 2 ? 1 : 0;
+  return KV_OK;
+}
+
 int32_t dtype_bytes(int32_t dt) {
   switch (dt) {
     case KV_F16:
@@ -67,7 +76,7 @@ bool same_instance(const kv_layout* a, const kv_layout* b) {
     return false;
   for (int i = 0; i < 6; ++i)
     if (x.axis_order[i] != y.axis_order[i]) return false;
-  return true;
+  return x.kv_part == y.kv_part && a->dk == b->dk;
 }
 
 kv_status check_batch(const kv_batch* bt, const kv_layout* lay, const char* name) {
@@ -163,22 +172,35 @@ kv_status kv_layout_describe(const kv_layout_desc* desc, kv_layout** out, size_t
     seen[a] = true;
   }
   if (fp8(d.dtype) && !d.scales) return fail(KV_EINVAL, "kv_layout_describe: fp8 layout needs scales");
+  if (d.kv_part < 0 || d.kv_part > 2) return fail(KV_EINVAL, "kv_layout_describe: kv_part must be 0, 1 or 2");
+  int32_t dk = 0;
+  if (d.dim_split > 1) {
+    if ((d.dim_split & (d.dim_split - 1)) || d.head_dim % d.dim_split)
+      return fail(KV_EINVAL, "kv_layout_describe: dim_split must be a power of two dividing head_dim");
+    while ((1 << dk) < d.dim_split) ++dk;
+    if (d.axis_order[5] == KV_AX_DIM) dk = 0;  // DIM innermost: the split changes nothing
+  } else if (d.dim_split < 0) {
+    return fail(KV_EINVAL, "kv_layout_describe: negative dim_split");
+  }
   kv_layout* L = new (std::nothrow) kv_layout;
   if (!L) return fail(KV_EINVAL, "kv_layout_describe: out of host memory");
   L->d = d;
   L->h_local = d.num_kv_heads / d.tp_degree;
   L->elem_bytes = dtype_bytes(d.dtype);
+  L->dk = dk;
   L->extent[KV_AX_LAYER] = d.num_layers;
-  L->extent[KV_AX_KV] = 2;
+  L->extent[KV_AX_KV] = d.kv_part ? 1 : 2;
   L->extent[KV_AX_BLOCK] = d.num_blocks;
   L->extent[KV_AX_SLOT] = d.block_size;
   L->extent[KV_AX_HEAD] = L->h_local;
-  L->extent[KV_AX_DIM] = d.head_dim;
-  int64_t s = 1;
+  L->extent[KV_AX_DIM] = d.head_dim >> dk;
+  int64_t s = 1 << dk;  // the x part of a split head_dim is innermost
   for (int i = 5; i >= 0; --i) {
     L->stride[d.axis_order[i]] = s;
     s *= L->extent[d.axis_order[i]];
   }
+  // a K-only / V-only pool stores its one K/V at index 0: the global index must not move it
+  if (d.kv_part) L->stride[KV_AX_KV] = 0;
   L->pool_bytes = (size_t)s * (size_t)L->elem_bytes;
   if (pool_bytes) *pool_bytes = L->pool_bytes;
   *out = L;
@@ -360,6 +382,8 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
   if (!enc) return KV_OK;
   TileArgs a;
   memset(&a, 0, sizeof(a));
+  kv_status pst = kv_pair(S, D, &a.kv1, &a.c0);
+  if (pst != KV_OK) return pst;
   for (int i = 0; i < KVX_MAX_RANKS; ++i) a.src_of_p[i] = -1;
   const CUtensorMapDataType dt = esize == 1 ? CU_TENSOR_MAP_DATA_TYPE_UINT8
                                  : esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_UINT16
@@ -411,7 +435,7 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
   a.f_nd = make_fastdiv((uint32_t)n_dst);
   a.f_parts = make_fastdiv(nparts);
   a.f_sub = make_fastdiv(nsub);
-  const uint64_t per_layer = (uint64_t)n_dst * nparts * nsub * 2 * (uint64_t)dst_bt->total_blocks;
+  const uint64_t per_layer = (uint64_t)n_dst * nparts * nsub * (a.kv1 ? 1 : 2) * (uint64_t)dst_bt->total_blocks;
   if (per_layer > kMaxChunks) return KV_OK;
   const int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / per_layer);
   for (int32_t l0 = lb; l0 < le; l0 += step) {
@@ -457,6 +481,9 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
     return fail(KV_ESHAPE, "kv_convert_reshard: P and D tables describe different requests");
   ConvArgs a;
   memset(&a, 0, sizeof(a));
+  if ((st = kv_pair(S, D, &a.kv1, &a.c0)) != KV_OK) return st;
+  a.s_dk = S->dk;
+  a.d_dk = D->dk;
   for (int i = 0; i < KVX_MAX_RANKS; ++i) a.src_of_p[i] = -1;
   for (int i = 0; i < n_src; ++i) {
     const int p = src[i]->d.tp_rank;
@@ -542,7 +569,7 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
     }
   }
   // per-layer chunk count; split the layer range so each launch stays under 2^31 chunks
-  const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * 2 * a.Hd_eff * a.Bd * ndch;
+  const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * (a.kv1 ? 1 : 2) * a.Hd_eff * a.Bd * ndch;
   int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / std::max<uint64_t>(per_layer, 1));
   if (per_layer > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_convert_reshard: one layer exceeds 2^31 chunks");
   for (int32_t l0 = lb; l0 < le; l0 += step) {
@@ -595,6 +622,8 @@ kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const vo
   if (src_bt->n_req > 0 && !src_bt->tok_req) return fail(KV_EINVAL, "kv_compute_scales: src_bt has no token map");
   AmaxArgs a;
   memset(&a, 0, sizeof(a));
+  if ((st = kv_pair(S, dst, &a.kv1, &a.c0)) != KV_OK) return st;
+  a.s_dk = S->dk;
   for (int i = 0; i < KVX_MAX_RANKS; ++i) a.src_of_p[i] = -1;
   for (int i = 0; i < n_src; ++i) {
     const int p = src[i]->d.tp_rank;
@@ -629,12 +658,12 @@ kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const vo
   a.f_hd = make_fastdiv((uint32_t)Hd);
   a.f_bp = make_fastdiv((uint32_t)S->d.block_size);
   a.f_hp = make_fastdiv((uint32_t)Hp);
-  const uint64_t items = (uint64_t)ntg * Hd * 2 * (uint64_t)(le - lb);
+  const uint64_t items = (uint64_t)ntg * Hd * (a.kv1 ? 1 : 2) * (uint64_t)(le - lb);
   if (items > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_compute_scales: batch too large for one call");
   a.n_items = (uint32_t)items;
   // row path: head_dim innermost with 16-B rows and aligned pools (every source)
   const int64_t rb = (int64_t)a.D * S->elem_bytes;
-  a.rows = S->d.axis_order[5] == KV_AX_DIM && rb % 16 == 0 && (rb / 16 & (rb / 16 - 1)) == 0 && rb / 16 <= 32;
+  a.rows = S->stride[KV_AX_DIM] == 1 && rb % 16 == 0 && (rb / 16 & (rb / 16 - 1)) == 0 && rb / 16 <= 32;
   for (int i = 0; i < n_src; ++i) a.rows = a.rows && ptr_aligned(src_pools[i], 16);
   if (a.rows)
     while ((1 << a.cpr_shift) < rb / 16) ++a.cpr_shift;
@@ -654,7 +683,11 @@ size_t kv_wire_bytes(const kv_layout* s, const kv_layout* d, int64_t total_token
   int32_t hb, he;
   head_overlap(s, d, &hb, &he);
   if (he <= hb) return 0;
-  return (size_t)2 * (size_t)(le - lb) * (size_t)(he - hb) * (size_t)total_tokens * (size_t)s->d.head_dim *
+  static const int mask[3] = {3, 1, 2};
+  const int m = (s->d.kv_part >= 0 && s->d.kv_part <= 2 && d->d.kv_part >= 0 && d->d.kv_part <= 2)
+                    ? (mask[s->d.kv_part] & mask[d->d.kv_part]) : 0;
+  const size_t nkv = m == 3 ? 2 : (m ? 1 : 0);  // the K/V both pools hold
+  return nkv * (size_t)(le - lb) * (size_t)(he - hb) * (size_t)total_tokens * (size_t)s->d.head_dim *
          (size_t)dtype_bytes(kv_wire_dtype(s, d));
 }
 
@@ -677,6 +710,8 @@ kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_
   if (src_bt->n_req > 0 && !src_bt->tok_req) return fail(KV_EINVAL, "kv_pack: src_bt has no token map");
   PackArgs a;
   memset(&a, 0, sizeof(a));
+  if ((st = kv_pair(s, d, &a.kv1, &a.c0)) != KV_OK) return st;
+  a.s_dk = s->dk;
   const int vec = (fast_ok(s) && ptr_aligned(src_pool, 16) && ptr_aligned(wire, 16)) ? 8 : 1;
   a.src = static_cast<const uint8_t*>(src_pool);
   a.wire = static_cast<uint8_t*>(wire);
@@ -704,7 +739,7 @@ kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_
   a.f_tok = make_fastdiv((uint32_t)src_bt->total_tokens);
   a.f_nh = make_fastdiv((uint32_t)a.nh);
   a.f_bp = make_fastdiv((uint32_t)a.Bp);
-  const uint64_t total = (uint64_t)a.Lc * 2 * a.nh * src_bt->total_tokens * ndch;
+  const uint64_t total = (uint64_t)a.Lc * (a.kv1 ? 1 : 2) * a.nh * src_bt->total_tokens * ndch;
   if (total > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_pack: more than 2^31 chunks in one call; split layers");
   a.total = (uint32_t)total;
   a.f_l = make_fastdiv((uint32_t)a.Lc);
@@ -732,6 +767,8 @@ kv_status kv_unpack(const kv_layout* s, const kv_layout* d, void* dst_pool, cons
   if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
   UnpackArgs a;
   memset(&a, 0, sizeof(a));
+  if ((st = kv_pair(s, d, &a.kv1, &a.c0)) != KV_OK) return st;
+  a.d_dk = d->dk;
   const int vec = (fast_ok(d) && ptr_aligned(dst_pool, 16) && ptr_aligned(wire, 16)) ? 8 : 1;
   a.dst = static_cast<uint8_t*>(dst_pool);
   a.wire = static_cast<const uint8_t*>(wire);
@@ -762,7 +799,7 @@ kv_status kv_unpack(const kv_layout* s, const kv_layout* d, void* dst_pool, cons
   a.f_in1 = make_fastdiv(a.slot_inner ? a.nh : a.Bd);
   a.f_l = make_fastdiv((uint32_t)a.Lc);
   a.f_bd = make_fastdiv((uint32_t)a.Bd);
-  const uint64_t total = (uint64_t)dst_bt->total_blocks * a.Lc * 2 * a.nh * a.Bd * ndch;
+  const uint64_t total = (uint64_t)dst_bt->total_blocks * a.Lc * (a.kv1 ? 1 : 2) * a.nh * a.Bd * ndch;
   if (total > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_unpack: more than 2^31 chunks in one call; split layers");
   a.total = (uint32_t)total;
   a.f_bl = make_fastdiv((uint32_t)dst_bt->total_blocks);
@@ -788,6 +825,7 @@ kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void*
   if (getenv("KVX_PULL_CHUNKED")) return KV_OK;  // A/B switch: per-chunk launches
   PullArgs a;
   memset(&a, 0, sizeof(a));
+  if (kv_pair(src[0], d, &a.kv1, &a.c0) != KV_OK) return KV_OK;  // the chunked path reports it
   int32_t nh = -1;
   for (int i = 0; i < n_src; ++i) {
     if (kv_wire_dtype(src[i], d) != d->d.dtype) return KV_OK;
@@ -831,7 +869,8 @@ kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void*
   a.f_src = make_fastdiv((uint32_t)n_src);
   a.slot_inner = slot_inner_of(d);
   a.n_blk = (uint32_t)dst_bt->total_blocks;
-  const uint64_t items = (uint64_t)n_src * 2 * (uint64_t)step * dst_bt->total_blocks * (uint64_t)a.Bd * (uint64_t)nh;
+  const uint64_t items = (uint64_t)n_src * (a.kv1 ? 1 : 2) * (uint64_t)step * dst_bt->total_blocks * (uint64_t)a.Bd *
+                         (uint64_t)nh;
   if (items > kMaxChunks) return KV_OK;
   a.spin_ns = 128u;
   t_last_kernel = "k_pull_rows";

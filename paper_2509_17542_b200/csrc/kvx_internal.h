@@ -17,6 +17,7 @@ struct kv_layout {
   int64_t stride[6];  // element stride per kv_axis (dense row-major in axis_order)
   int32_t h_local;
   int32_t elem_bytes;
+  int32_t dk;         // log2 of the head_dim split x (0: none); stride[DIM] is the D/x part's
   size_t pool_bytes;
 };
 
@@ -31,6 +32,8 @@ extern std::atomic<int32_t> g_sm_budget[kMaxDevices];  // kv_set_sm_budget per d
 
 int32_t dtype_bytes(int32_t dt);
 bool fp8(int32_t dt);  // KV_F8E4M3 or KV_F8E4M3FNUZ (carries per-head scales)
+// K/V both layouts hold (kv_part): *kv1 = 0 both, else 1 with *c0 the one shared index
+kv_status kv_pair(const kv_layout* s, const kv_layout* d, int32_t* kv1, int32_t* c0);
 
 // n / d for 32-bit n via one umulhi (Granlund-Montgomery round-up method).
 struct FastDiv {
@@ -40,6 +43,8 @@ FastDiv make_fastdiv(uint32_t d);
 
 // ---- kernel argument blocks (by value) -------------------------------------------
 struct ConvArgs {
+  int32_t kv1, c0;
+  int32_t s_dk, d_dk;  // head_dim split (log2 x) of source / destination (element-wise kernel)  // K-only / V-only transfer: kv1 = 1 and c0 the one K/V index (reading 27)
   const uint8_t* src[KVX_MAX_RANKS];
   uint8_t* dst[KVX_MAX_RANKS];
   const float* sscale[KVX_MAX_RANKS];  // per source index (e4m3 sources)
@@ -74,6 +79,7 @@ struct ConvArgs {
 // P rank, source block) lands the sub-tile in smem already in D's order (the tensor map's
 // dimension order is D's), then bulk stores write D's contiguous runs.
 struct TileArgs {
+  int32_t kv1, c0;  // K-only / V-only transfer: kv1 = 1 and c0 the one K/V index (reading 27)
   CUtensorMap maps[KVX_MAX_RANKS][2];  // [source index][K/V]: dims (DIM, A, B, BLOCK, LAYER)
   uint8_t* dst[KVX_MAX_RANKS];
   int8_t dst_rank[KVX_MAX_RANKS];
@@ -94,6 +100,8 @@ struct TileArgs {
 };
 
 struct PackArgs {
+  int32_t kv1, c0;
+  int32_t s_dk;  // K-only / V-only transfer: kv1 = 1 and c0 the one K/V index (reading 27)
   const uint8_t* src;
   uint8_t* wire;
   const float* sscale;  // source scales (unused unless the wire cast needs them)
@@ -114,6 +122,8 @@ struct PackArgs {
 };
 
 struct UnpackArgs {
+  int32_t kv1, c0;
+  int32_t d_dk;  // K-only / V-only transfer: kv1 = 1 and c0 the one K/V index (reading 27)
   uint8_t* dst;
   const uint8_t* wire;
   const float* sscale;  // source scales (widening from e4m3 on the receiver)
@@ -141,6 +151,7 @@ struct UnpackArgs {
 // ((((dst block, local layer), K/V), sub-tile), source).  Same dtype on wire and pool.
 #define KVX_MAX_RING 8
 struct PullArgs {
+  int32_t kv1, c0;  // K-only / V-only transfer: kv1 = 1 and c0 the one K/V index (reading 27)
   uint8_t* dst;
   const uint8_t* ring[KVX_MAX_RANKS][KVX_MAX_RING];  // [source][slot] peer-mapped
   const uint32_t* ready[KVX_MAX_RANKS];               // local words P writes
@@ -165,6 +176,8 @@ struct PullArgs {
 };
 
 struct AmaxArgs {
+  int32_t kv1, c0;
+  int32_t s_dk;  // K-only / V-only transfer: kv1 = 1 and c0 the one K/V index (reading 27)
   const uint8_t* src[KVX_MAX_RANKS];
   const float* sscale[KVX_MAX_RANKS];
   int8_t src_of_p[KVX_MAX_RANKS];

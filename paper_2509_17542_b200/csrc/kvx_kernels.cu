@@ -253,6 +253,24 @@ __device__ __forceinline__ uint32_t divmod(uint32_t& n, const FastDiv& f) {
   return r;
 }
 
+// element offset of head_dim index d: (d >> dk) * stride + (d & (2^dk - 1)) -- the x-split
+// head_dim of reading 27 (dk = log2 x; 0: unsplit, d * stride)
+__device__ __forceinline__ int64_t dim_off(uint32_t d, int64_t stride, int32_t dk) {
+  return (int64_t)(d >> dk) * stride + (int64_t)(d & ((1u << dk) - 1u));
+}
+
+// K/V entries per layer on the wire (Fig. 5 order over the K/V both pools hold)
+__device__ __forceinline__ uint32_t wkv(int32_t kv1) { return kv1 ? 1u : 2u; }
+
+// K/V index of an item: both (n's lowest digit) or, for a K-only / V-only transfer
+// (kv1 != 0, reading 27), always c0 with no digit in n
+__device__ __forceinline__ uint32_t take_kv(uint32_t& n, int32_t kv1, int32_t c0) {
+  if (kv1) return (uint32_t)c0;
+  const uint32_t c = n & 1u;
+  n >>= 1;
+  return c;
+}
+
 constexpr int kThreads = 256;
 #ifndef KVX_MINB
 #define KVX_MINB 4  // >= 4 CTAs/SM for the row kernel: caps it at 64 registers (the 2-byte -> e4m3
@@ -289,8 +307,7 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
         const uint32_t dch = divmod(n, a.f_dch);
         const uint32_t in0 = divmod(n, a.f_in0);
         const uint32_t in1 = divmod(n, a.f_in1);
-        const uint32_t c = n & 1u;
-        n >>= 1;
+        const uint32_t c = take_kv(n, a.kv1, a.c0);
         const uint32_t l = divmod(n, a.f_l);
         const uint32_t bl = divmod(n, a.f_bl);
         const uint32_t qi = n;
@@ -305,7 +322,7 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
         const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
         const int64_t doff = dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
                              (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD] +
-                             (int64_t)dch * VEC * a.ds[KV_AX_DIM];
+                             dim_off(dch * VEC, a.ds[KV_AX_DIM], a.d_dk);
         dp[k] = a.dst[qi] + doff * Tr<DDT>::B;
         if ((int32_t)t >= T) {
           zero[k] = true;
@@ -319,7 +336,7 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
           const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + tb);
           const int64_t soff = sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
                                sblk * a.ss[KV_AX_BLOCK] + (int64_t)sslot * a.ss[KV_AX_SLOT] +
-                               (int64_t)hp * a.ss[KV_AX_HEAD] + (int64_t)dch * VEC * a.ss[KV_AX_DIM];
+                               (int64_t)hp * a.ss[KV_AX_HEAD] + dim_off(dch * VEC, a.ss[KV_AX_DIM], a.s_dk);
           load_chunk<SDT, VEC>(in[k], a.src[si] + soff * Tr<SDT>::B);
           if constexpr (is_fp8(SDT) && SDT != DDT)
             ssc[k] = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
@@ -410,8 +427,7 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
   uint32_t n = item;
   const uint32_t qi = divmod(n, a.f_nd);
   const uint32_t rg = divmod(n, a.f_items);
-  const uint32_t c = n & 1u;
-  n >>= 1;
+  const uint32_t c = take_kv(n, a.kv1, a.c0);
   const uint32_t l = divmod(n, a.f_l);
   const uint32_t bl = n;
   const int32_t r = __ldg(a.d_blk_req + bl);
@@ -658,8 +674,7 @@ __global__ void __launch_bounds__(32) k_tile_copy(const __grid_constant__ TileAr
     const uint32_t qi = divmod(n, a.f_nd);
     const uint32_t part = divmod(n, a.f_parts);
     const uint32_t sub = divmod(n, a.f_sub);
-    c = n & 1u;
-    n >>= 1;
+    c = take_kv(n, a.kv1, a.c0);
     const uint32_t l = divmod(n, a.f_l);
     const uint32_t bl = n;
     const int32_t r = __ldg(a.d_blk_req + bl);
@@ -763,8 +778,8 @@ __global__ void __launch_bounds__(kThreads) k_pack_rows(const __grid_constant__ 
     uint32_t n = item;
     const uint32_t tg = divmod(n, a.f_tg);
     const uint32_t hh = divmod(n, a.f_nh);
-    const uint32_t c = n & 1u;
-    const uint32_t l = n >> 1;
+    const uint32_t c = take_kv(n, a.kv1, a.c0);
+    const uint32_t l = n;
     const int64_t layer = a.lb + (int64_t)l;
     const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
     const uint32_t tok = tg * 32u + lane;
@@ -781,7 +796,7 @@ __global__ void __launch_bounds__(kThreads) k_pack_rows(const __grid_constant__ 
       const uint32_t hp = h - (uint32_t)a.p * (uint32_t)a.Hp;
       sp = (uint64_t)(a.src + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
                                (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
-      dp = (uint64_t)(a.wire + ((((uint64_t)l * 2 + c) * (uint64_t)a.nh + hh) * T_all + tok) * (uint64_t)a.D * Tr<WDT>::B);
+      dp = (uint64_t)(a.wire + ((((uint64_t)l * wkv(a.kv1) + (c - (uint32_t)a.c0)) * (uint64_t)a.nh + hh) * T_all + tok) * (uint64_t)a.D * Tr<WDT>::B);
       const float ds_inv = is_fp8(WDT) && SDT != WDT
                                ? __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)))
                                : 1.f;
@@ -808,8 +823,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
   for (uint32_t item = warp; item < a.n_items; item += nwarps) {
     uint32_t n = item;
     uint32_t sbk = divmod(n, a.f_items);
-    const uint32_t c = n & 1u;
-    n >>= 1;
+    const uint32_t c = take_kv(n, a.kv1, a.c0);
     const uint32_t l = divmod(n, a.f_l);
     const uint32_t bl = n;
     const uint32_t s_blk = divmod(sbk, a.f_sb);
@@ -837,7 +851,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
       if ((int32_t)t >= T) {
         rz = 1;
       } else {
-        sp = (uint64_t)(a.wire + ((((uint64_t)l * 2 + c) * (uint64_t)a.nh + hh) * (uint64_t)a.total_tokens +
+        sp = (uint64_t)(a.wire + ((((uint64_t)l * wkv(a.kv1) + (c - (uint32_t)a.c0)) * (uint64_t)a.nh + hh) * (uint64_t)a.total_tokens +
                                   (uint64_t)(tok0 + t)) * (uint64_t)a.D * Tr<WDT>::B);
         if constexpr (is_fp8(WDT) && WDT != DDT)
           rsc = __ldg(a.sscale + (sl * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
@@ -918,8 +932,7 @@ __global__ void __launch_bounds__(kThreads) k_pull_rows(const __grid_constant__ 
         uint32_t n = item;
         const uint32_t src = divmod(n, a.f_src);
         uint32_t sbk = divmod(n, a.f_items);
-        const uint32_t c = n & 1u;
-        n >>= 1;
+        const uint32_t c = take_kv(n, a.kv1, a.c0);
         const uint32_t lk = divmod(n, f_l);
         const uint32_t bl = n;
         const uint32_t s_blk = divmod(sbk, a.f_sb);
@@ -942,7 +955,7 @@ __global__ void __launch_bounds__(kThreads) k_pull_rows(const __grid_constant__ 
             rz = 1;
           else
             sp = (uint64_t)(a.ring[src][slot_idx] +
-                            ((((uint64_t)lk * 2 + c) * (uint64_t)a.nh + hh) * (uint64_t)a.total_tokens +
+                            ((((uint64_t)lk * wkv(a.kv1) + (c - (uint32_t)a.c0)) * (uint64_t)a.nh + hh) * (uint64_t)a.total_tokens +
                              (uint64_t)(tok0 + t)) * (uint64_t)a.D * Tr<DT>::B);
         }
         stream_rows<DT, DT, U, 8, true>(lane, cs, sp, dp, 1.f, rz);
@@ -990,8 +1003,7 @@ __global__ void __launch_bounds__(kThreads) k_pack(const __grid_constant__ PackA
         const uint32_t dch = divmod(n, a.f_dch);
         const uint32_t tok = divmod(n, a.f_tok);
         const uint32_t hh = divmod(n, a.f_nh);
-        const uint32_t c = n & 1u;
-        n >>= 1;
+        const uint32_t c = take_kv(n, a.kv1, a.c0);
         const uint32_t l = n;
         const int32_t r = __ldg(a.tok_req + tok);
         uint32_t t = tok - (uint32_t)__ldg(a.tok_off + r);
@@ -1003,7 +1015,7 @@ __global__ void __launch_bounds__(kThreads) k_pack(const __grid_constant__ PackA
         const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
         const int64_t soff = sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
                              (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD] +
-                             (int64_t)dch * VEC * a.ss[KV_AX_DIM];
+                             dim_off(dch * VEC, a.ss[KV_AX_DIM], a.s_dk);
         load_chunk<SDT, VEC>(in[k], a.src + soff * Tr<SDT>::B);
         if constexpr (is_fp8(SDT) && SDT != WDT) ssc[k] = __ldg(a.sscale + (sl * 2 + c) * a.Hp + hp);
         if constexpr (is_fp8(WDT) && SDT != WDT)
@@ -1048,8 +1060,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack(const __grid_constant__ Unp
         const uint32_t dch = divmod(n, a.f_dch);
         const uint32_t in0 = divmod(n, a.f_in0);
         const uint32_t in1 = divmod(n, a.f_in1);
-        const uint32_t c = n & 1u;
-        n >>= 1;
+        const uint32_t c = take_kv(n, a.kv1, a.c0);
         const uint32_t l = divmod(n, a.f_l);
         const uint32_t bl = n;
         const uint32_t slot = a.slot_inner ? in0 : in1;
@@ -1065,12 +1076,13 @@ __global__ void __launch_bounds__(kThreads) k_unpack(const __grid_constant__ Unp
         const uint32_t hq = h - (uint32_t)a.q * (uint32_t)a.Hd;
         const int64_t doff = dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK] +
                              (int64_t)slot * a.ds[KV_AX_SLOT] + (int64_t)hq * a.ds[KV_AX_HEAD] +
-                             (int64_t)dch * VEC * a.ds[KV_AX_DIM];
+                             dim_off(dch * VEC, a.ds[KV_AX_DIM], a.d_dk);
         dp[k] = a.dst + doff * Tr<DDT>::B;
         if ((int32_t)t >= T) {
           zero[k] = true;
         } else {
-          const int64_t woff = ((((int64_t)l * 2 + c) * a.nh + hh) * a.total_tokens + tok0 + t) * a.D + (int64_t)dch * VEC;
+          const int64_t woff = ((((int64_t)l * wkv(a.kv1) + (c - (uint32_t)a.c0)) * a.nh + hh) * a.total_tokens + tok0 + t) *
+                                   a.D + (int64_t)dch * VEC;
           load_chunk<WDT, VEC>(in[k], a.wire + woff * Tr<WDT>::B);
           if constexpr (is_fp8(WDT) && WDT != DDT)
             ssc[k] = __ldg(a.sscale + (sl * 2 + c) * a.Hp + (h - (uint32_t)a.p * (uint32_t)a.Hp));
@@ -1108,8 +1120,8 @@ __global__ void __launch_bounds__(kThreads) k_amax(const __grid_constant__ AmaxA
     uint32_t n = item;
     const uint32_t tg = divmod(n, a.f_tg);
     const uint32_t hq = divmod(n, a.f_hd);
-    const uint32_t c = n & 1u;
-    const int64_t layer = a.lb + (int64_t)(n >> 1);
+    const uint32_t c = take_kv(n, a.kv1, a.c0);
+    const int64_t layer = a.lb + (int64_t)n;
     const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
     const uint32_t tok = tg * 32u + lane;
     float m = 0.f;
@@ -1127,10 +1139,10 @@ __global__ void __launch_bounds__(kThreads) k_amax(const __grid_constant__ AmaxA
                                          (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B;
       float sc = 1.f;
       if constexpr (is_fp8(SDT)) sc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
-      const int64_t sd = a.ss[KV_AX_DIM] * Tr<SDT>::B;
+      const int64_t sdim = a.ss[KV_AX_DIM];
       for (int32_t d = 0; d < a.D; ++d) {
         Chunk<SDT, 1> e;
-        load_chunk<SDT, 1>(e, base + d * sd);
+        load_chunk<SDT, 1>(e, base + dim_off((uint32_t)d, sdim, a.s_dk) * Tr<SDT>::B);
         float v = to_f32<SDT>(e.w[0]);
         if constexpr (is_fp8(SDT)) v = __fmul_rn(v, sc);
         v = fabsf(v);
@@ -1163,8 +1175,8 @@ __global__ void __launch_bounds__(kThreads) k_amax_rows(const __grid_constant__ 
     uint32_t n = item;
     const uint32_t tgc = divmod(n, a.f_tgc);
     const uint32_t hq = divmod(n, a.f_hd);
-    const uint32_t c = n & 1u;
-    const int64_t layer = a.lb + (int64_t)(n >> 1);
+    const uint32_t c = take_kv(n, a.kv1, a.c0);
+    const int64_t layer = a.lb + (int64_t)n;
     const int64_t sl = layer - a.s_l0;
     const uint32_t h = (uint32_t)a.q * (uint32_t)a.Hd + hq;
     const uint32_t p = fdiv(h, a.f_hp);
@@ -1207,9 +1219,20 @@ __global__ void __launch_bounds__(kThreads) k_amax_rows(const __grid_constant__ 
   }
 }
 
+// entries [begin, end) of an [L][2][Hd] scale array; a K-only / V-only pass leaves the
+// other half untouched
+__device__ __forceinline__ bool amax_entry(int64_t i, int32_t Hd, int32_t kv1, int32_t c0) {
+  return !kv1 || (int32_t)((i / Hd) & 1) == c0;
+}
+__global__ void k_amax_init(uint32_t* bits, int64_t begin, int64_t end, int32_t Hd, int32_t kv1, int32_t c0) {
+  for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end; i += (int64_t)gridDim.x * blockDim.x)
+    if (amax_entry(i, Hd, kv1, c0)) bits[i] = 0u;
+}
 // s = RN(amax / qmax), qmax = the destination fp8's largest finite value (448 / 240)
-__global__ void k_amax_finalize(uint32_t* bits, int64_t begin, int64_t end, float qmax) {
+__global__ void k_amax_finalize(uint32_t* bits, int64_t begin, int64_t end, float qmax, int32_t Hd, int32_t kv1,
+                                int32_t c0) {
   for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end; i += (int64_t)gridDim.x * blockDim.x) {
+    if (!amax_entry(i, Hd, kv1, c0)) continue;
     const float amax = __uint_as_float(bits[i]);
     const float s = __fdiv_rn(amax, qmax);
     reinterpret_cast<float*>(bits)[i] = s > 0.f ? s : 1.0f;
@@ -1388,7 +1411,7 @@ cudaError_t pack_t(const PackArgs& a0, cudaStream_t s) {
     const uint32_t T_all = a.f_tok.d;
     const uint32_t ntg = (T_all + 31u) / 32u;
     a.f_tg = make_fastdiv(ntg);
-    a.n_items = (uint32_t)a.Lc * 2u * (uint32_t)a.nh * ntg;
+    a.n_items = (uint32_t)a.Lc * (a.kv1 ? 1u : 2u) * (uint32_t)a.nh * ntg;
     auto k = k_pack_rows<SDT, WDT, U>;
     k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
   } else {
@@ -1410,7 +1433,7 @@ cudaError_t unpack_t(const UnpackArgs& a0, cudaStream_t s) {
     const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.nh + th - 1) / th;
     a.f_sb = make_fastdiv(nsb);
     a.f_items = make_fastdiv(nsb * nhb);
-    a.n_items = a.f_bl.d * (uint32_t)a.Lc * 2u * nsb * nhb;
+    a.n_items = a.f_bl.d * (uint32_t)a.Lc * (a.kv1 ? 1u : 2u) * nsb * nhb;
     auto k = k_unpack_rows<WDT, DDT, U>;
     k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
   } else {
@@ -1508,7 +1531,7 @@ cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s) {
   const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.nh + th - 1) / th;
   a.f_sb = make_fastdiv(nsb);
   a.f_items = make_fastdiv(nsb * nhb);
-  const uint32_t per_layer = a.f_src.d * 2u * nsb * nhb * a.n_blk;
+  const uint32_t per_layer = a.f_src.d * (a.kv1 ? 1u : 2u) * nsb * nhb * a.n_blk;
   const uint32_t nl_last = (uint32_t)(a.le - a.lb - (a.nchunks - 1) * a.step);
   a.items_last = per_layer * nl_last;
   a.items_full = per_layer * (uint32_t)a.step;
@@ -1526,12 +1549,13 @@ cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s) {
 
 cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) {
   const int64_t begin = (int64_t)(a.lb - a.d_l0) * 2 * a.Hd, end = (int64_t)(a.lb - a.d_l0 + a.Lc) * 2 * a.Hd;
-  cudaError_t e = cudaMemsetAsync(out + begin, 0, (size_t)(end - begin) * sizeof(float), s);
-  if (e != cudaSuccess) return e;
+  const int fin_grid = (int)std::min<int64_t>(1024, (end - begin + 255) / 256 + 1);
+  k_amax_init<<<fin_grid, 256, 0, s>>>(reinterpret_cast<uint32_t*>(out), begin, end, a.Hd, a.kv1, a.c0);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   if (a.n_items && a.rows) {
     AmaxArgs b = a;
     b.f_tgc = make_fastdiv((a.f_tg.d + kAmaxG - 1) / kAmaxG);
-    b.n_row_items = b.f_tgc.d * (uint32_t)a.Hd * 2u * (uint32_t)a.Lc;
+    b.n_row_items = b.f_tgc.d * (uint32_t)a.Hd * (a.kv1 ? 1u : 2u) * (uint32_t)a.Lc;
     switch (sdt) {
       case KV_F16: k_amax_rows<KV_F16><<<grid_for_items(k_amax_rows<KV_F16>, b.n_row_items), kThreads, 0, s>>>(b); break;
       case KV_BF16: k_amax_rows<KV_BF16><<<grid_for_items(k_amax_rows<KV_BF16>, b.n_row_items), kThreads, 0, s>>>(b); break;
@@ -1558,8 +1582,8 @@ cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) 
     }
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
-  k_amax_finalize<<<(int)std::min<int64_t>(1024, (end - begin + 255) / 256 + 1), 256, 0, s>>>(
-      reinterpret_cast<uint32_t*>(out), begin, end, a.qmax);
+  k_amax_finalize<<<fin_grid, 256, 0, s>>>(reinterpret_cast<uint32_t*>(out), begin, end, a.qmax, a.Hd, a.kv1,
+                                           a.c0);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }

@@ -60,6 +60,9 @@ kv_status kv_wire_header_write(const kv_layout* s, const kv_layout* d, int32_t n
   put32(out + 48, (uint32_t)hb);
   put32(out + 52, (uint32_t)he);
   put32(out + 56, (uint32_t)n_req);
+  int32_t kv1 = 0, c0 = 0;
+  if (kv_pair(s, d, &kv1, &c0) != KV_OK) return KV_ESHAPE;
+  put32(out + 60, kv1 ? (uint32_t)(c0 + 1) : 0u);
   put64(out + 64, (uint64_t)kv_wire_bytes(s, d, tt, lb, le));
   for (int32_t r = 0; r < n_req; ++r) put32(out + kHdrFixed + 4 * r, (uint32_t)nt[r]);
   return KV_OK;
@@ -84,6 +87,8 @@ kv_status kv_wire_header_parse(const uint8_t* h, size_t len, kv_wire_info* o) {
   o->head_begin = (int32_t)get32(h + 48);
   o->head_end = (int32_t)get32(h + 52);
   o->n_req = n_req;
+  o->kv_part = (int32_t)get32(h + 60);
+  if (o->kv_part < 0 || o->kv_part > 2) return fail(KV_EINVAL, "kv_wire_header_parse: bad K/V field");
   o->payload_bytes = get64(h + 64);
   o->n_tokens = reinterpret_cast<const int32_t*>(h + kHdrFixed);  // little-endian host
   return KV_OK;
@@ -102,6 +107,9 @@ kv_status kv_wire_header_check(const uint8_t* h, size_t len, const kv_layout* s,
   if (w.src_tp_degree != s->d.tp_degree || w.src_tp_rank != s->d.tp_rank) return bad("P parallel strategy");
   if (w.dst_tp_degree != d->d.tp_degree || w.dst_tp_rank != d->d.tp_rank) return bad("D parallel strategy");
   if (w.n_req != n_req) return bad("request count");
+  int32_t kv1 = 0, c0 = 0;
+  if (kv_pair(s, d, &kv1, &c0) != KV_OK) return KV_ESHAPE;
+  if (w.kv_part != (kv1 ? c0 + 1 : 0)) return bad("K/V carried");
   int64_t tt = 0;
   for (int32_t r = 0; r < n_req; ++r) {
     if (w.n_tokens[r] != nt[r]) return bad("token counts");

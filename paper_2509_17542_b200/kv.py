@@ -44,7 +44,7 @@ class Layout:
     """kv_layout_describe: one TP rank's paged pool layout."""
 
     def __init__(self, num_layers, num_kv_heads, head_dim, tp_degree, tp_rank, block_size, num_blocks, dtype,
-                 axis_order, scales=None, first_layer=0):
+                 axis_order, scales=None, first_layer=0, kv_part=0, dim_split=0):
         d = LayoutDesc()
         d.num_layers, d.num_kv_heads, d.head_dim = num_layers, num_kv_heads, head_dim
         d.first_layer = first_layer
@@ -53,6 +53,8 @@ class Layout:
         d.block_size, d.num_blocks, d.dtype = block_size, num_blocks, dtype
         for i, a in enumerate(axis_order):
             d.axis_order[i] = a
+        d.kv_part, d.dim_split = kv_part, dim_split
+        self.kv_part, self.dim_split = kv_part, dim_split
         self.scales = scales  # keep the device tensor alive
         d.scales = _ptr(scales)
         h = C.c_void_p()
@@ -69,7 +71,7 @@ class Layout:
     @classmethod
     def from_dict(cls, d, scales=None):
         return cls(d["L"], d["H"], d["D"], d["tp"], d["rank"], d["B"], d["NB"], d["dtype"], d["order"], scales,
-                   d.get("first_layer", 0))
+                   d.get("first_layer", 0), d.get("kv_part", 0), d.get("dim_split", 0))
 
     @property
     def layers(self):

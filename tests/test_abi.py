@@ -206,3 +206,36 @@ def test_row_kernels_fit_four_ctas_per_sm():
     assert len(fns) >= 16
     for name, reg, stack, local in fns:
         assert int(reg) <= 64 and int(stack) == 0 and int(local) == 0, (name, reg, stack, local)
+
+
+def test_layout_variants_describe_wire_and_header(kvx, o1):
+    """NEXT-3 layout variants (reading 27): kv_part / dim_split validation, pool sizes equal
+    the oracle's element counts, the wire carries only the K/V both pools hold, and the
+    header's K/V field (offset 60) is written, parsed and checked."""
+    import struct
+    from paper_2509_17542_b200 import replay
+    import synth
+    order = (2, 4, 5, 3, 0, 1)   # BLOCK, HEAD, DIM(/x), SLOT, LAYER, KV: an x-packed key cache
+    for kp, x in [(0, 0), (1, 8), (2, 0), (1, 4), (0, 16)]:
+        l = kvx.Layout(2, 8, 16, 2, 1, 4, 10, kvx.KV_BF16, order, kv_part=kp, dim_split=x)
+        d = synth.layout(2, 8, 16, 2, 1, 4, 10, synth.BF16, order, kv_part=kp, dim_split=x)
+        assert l.pool_bytes == o1.pool_elems(d) * 2 == (1 if kp else 2) * 2 * 10 * 4 * 4 * 16 * 2
+    with pytest.raises(kvx.KvError, match="KV_EINVAL"):
+        kvx.Layout(2, 8, 16, 2, 1, 4, 10, kvx.KV_BF16, order, kv_part=3)
+    with pytest.raises(kvx.KvError, match="KV_EINVAL"):
+        kvx.Layout(2, 8, 16, 2, 1, 4, 10, kvx.KV_BF16, order, dim_split=3)    # not a power of two
+    with pytest.raises(kvx.KvError, match="KV_EINVAL"):
+        kvx.Layout(2, 8, 16, 2, 1, 4, 10, kvx.KV_BF16, order, dim_split=32)   # does not divide head_dim
+    both = _lay(kvx, tp_degree=2, tp_rank=1, dtype=kvx.KV_BF16)
+    konly = kvx.Layout(2, 8, 16, 2, 1, 4, 10, kvx.KV_BF16, order, kv_part=1, dim_split=8)
+    vonly = kvx.Layout(2, 8, 16, 2, 1, 4, 10, kvx.KV_BF16, order, kv_part=2)
+    assert kvx.wire_bytes(both, konly, 100) == kvx.wire_bytes(both, both, 100) // 2 == 1 * 2 * 4 * 100 * 16 * 2
+    assert kvx.wire_bytes(konly, vonly, 100) == 0          # nothing in common
+    hdr = replay.header(both, vonly, [5, 7])
+    assert struct.unpack_from("<I", hdr, 60)[0] == 2
+    assert replay.parse(hdr)["kv_part"] == 2
+    replay.check_header(hdr, both, vonly, [5, 7])
+    with pytest.raises(kvx.KvError, match="K/V carried"):
+        replay.check_header(hdr, both, konly, [5, 7])
+    with pytest.raises(kvx.KvError, match="share neither"):
+        replay.header(konly, vonly, [1])

@@ -451,3 +451,69 @@ def test_dynamic_scales_row_and_generic_paths(o1, order_i, ddt):
     want = o1.amax_scales(case["src_lays"], case["src_pools"], case["dst_lays"][0], case["n_tokens"],
                           case["src_tables"])
     assert np.array_equal(out.cpu().numpy(), want)
+
+
+# ---- NEXT-3 layout variants (reading 27): K-only / V-only pools, x-split head_dim ---------
+_HELD = {0: (0, 1), 1: (0,), 2: (1,)}
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_layout_variants_convert_and_wire(o1, seed):
+    """Random K-only / V-only / both pools with and without an x-split head_dim on either
+    side, every path: the fused convert and pack -> unpack per pair, bit-exact vs O1."""
+    from tests.gpu_util import DevCase, dev_to_np
+    import paper_2509_17542_b200 as kvx
+    rng = np.random.default_rng(2000 + seed)
+    tp_p, tp_d = [(2, 1), (1, 2), (2, 2), (4, 2)][seed % 4]
+    pk = int(rng.integers(0, 3))
+    dk = int(rng.choice([k for k in range(3) if set(_HELD[k]) & set(_HELD[pk])]))
+    px, dx = int(rng.choice([0, 8, 16])), int(rng.choice([0, 8, 16]))
+    sdt, ddt = [(BF16, BF16), (BF16, E4M3), (F16, FNUZ), (E4M3, BF16)][seed % 4]
+    so, do = ALL_ORDERS[int(rng.integers(720))], ALL_ORDERS[int(rng.integers(720))]
+    case = make_case(2, 8, 32, tp_p, tp_d, 4, 8, [13, 40, 1], sdt, ddt, so, do, seed=seed, o1=o1, scales="pow2",
+                     p_kv_part=pk, d_kv_part=dk, p_split=px, d_split=dx)
+    if sdt in FP8:
+        for i, lay in enumerate(case["src_lays"]):
+            lay["scales"] = synth.pow2_scales(600 + i, 2, 8 // tp_p, -3, 3)
+    run_case(o1, case)
+    dc = DevCase(case)
+    for p, q, _, _ in kvx.plan_pairs(tp_p, tp_d, 8):
+        S, Dl = dc.src_lays[p], dc.dst_lays[q]
+        wire = torch.empty(max(16, kvx.wire_bytes(S, Dl, dc.src_bt.total_tokens)), dtype=torch.uint8, device="cuda")
+        kvx.pack(S, dc.src_pools[p], dc.src_bt, Dl, wire)
+        torch.cuda.synchronize()
+        want_wire = o1.flatten(case["src_lays"][p], case["src_pools"][p], case["dst_lays"][q], case["n_tokens"],
+                               case["src_tables"])
+        assert np.array_equal(dev_to_np(wire, kvx.wire_dtype(S, Dl))[:want_wire.size], want_wire)
+        kvx.unpack(S, Dl, dc.dst_pools[q], dc.dst_bt, wire)
+    torch.cuda.synchronize()
+    assert_pools_match(dc.dst_numpy(), expected(case, o1), ddt)
+
+
+def test_other_vendor_prefill_to_nvidia_decode(o1):
+    """The multi-vendor pairing end to end on one GPU: a P instance whose engine keeps an
+    x-packed key cache (BLOCK, HEAD, D/8, SLOT, [LAYER], x=8) and a head_dim-major value
+    cache (BLOCK, HEAD, DIM, SLOT) in two pools, fp8 e4m3fnuz with per-head scales, TP2 ->
+    a D instance with one block-major K+V pool in OCP e4m3fn, TP1 (merge), block 16 -> 32.
+    Two convert calls (K, then V) == O1 on the same pools."""
+    from tests.gpu_util import DevCase
+    korder = (BLOCK, HEAD, DIM, SLOT, LAYER, KV)
+    vorder = (BLOCK, HEAD, DIM, SLOT, LAYER, KV)
+    args = (3, 8, 64, 2, 1, 16, 32, [70, 5, 33], FNUZ, E4M3)
+    kw = dict(d_order=synth.D_ORDER, seed=77, o1=o1, scales="pow2")
+    kc = make_case(*args, p_order=korder, p_kv_part=1, p_split=8, **kw)
+    vc = make_case(*args, p_order=vorder, p_kv_part=2, **kw)
+    for c in (kc, vc):
+        for i, lay in enumerate(c["src_lays"]):
+            lay["scales"] = synth.pow2_scales(700 + i, 3, 4, -2, 2)
+    # one D pool receives both calls
+    dk_ = DevCase(kc)
+    dv_ = DevCase(vc)
+    dv_.dst_pools = dk_.dst_pools
+    dk_.convert()
+    dv_.convert()
+    want = expected(kc, o1)
+    want = [w.copy() for w in want]
+    o1.convert(vc["src_lays"], vc["src_pools"], vc["dst_lays"], want, vc["n_tokens"], vc["src_tables"],
+               vc["dst_tables"])
+    assert_pools_match(dk_.dst_numpy(), want, E4M3)
