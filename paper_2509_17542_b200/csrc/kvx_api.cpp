@@ -525,7 +525,94 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
     a.dscale[i] = dst[i]->d.scales;
   }
   (void)H;
-  bool fast = fast_ok(S) && fast_ok(D);
+  // row kernel: each side has head_dim-contiguous rows, or an x-split head_dim with x >= 8
+  // (whole 8-element chunks inside each x-group, reading 27)
+  auto rows_side = [](const kv_layout* L, int32_t* ck, int64_t* chs) -> bool {
+    const int32_t cpr = L->d.head_dim / 8;
+    if (L->d.head_dim % 8 || (cpr & (cpr - 1))) return false;
+    if (L->dk == 0) {
+      *ck = 0;
+      *chs = 8 * (int64_t)L->elem_bytes;
+      return L->stride[KV_AX_DIM] == 1;
+    }
+    if (L->dk < 3) return false;
+    *ck = L->dk - 3;
+    *chs = L->stride[KV_AX_DIM] * (int64_t)L->elem_bytes;
+    return true;
+  };
+  // head_dim-major side ((DIM, SLOT) innermost, no split): the smem-transpose kernel, when
+  // the other side is head_dim-major too or has contiguous rows
+  // mode 1: (DIM, SLOT) innermost; mode 2: x-split head_dim with (D/x, SLOT, x) innermost
+  // (x a multiple of 8): whole (block, head) tiles are contiguous and go through smem
+  auto tr_side = [](const kv_layout* L) -> int {
+    if (L->dk == 0 && L->d.axis_order[4] == KV_AX_DIM && L->d.axis_order[5] == KV_AX_SLOT)
+      return L->d.block_size % 8 == 0 ? 1 : -1;
+    if (L->dk >= 3 && L->d.axis_order[4] == KV_AX_DIM && L->d.axis_order[5] == KV_AX_SLOT) return 2;
+    return 0;
+  };
+  auto plain_rows = [](const kv_layout* L) { return L->dk == 0 && L->stride[KV_AX_DIM] == 1; };
+  {
+    const int st = tr_side(S), dt = tr_side(D);
+    const size_t smem = 4 * (size_t)D->d.block_size * (S->d.head_dim + 16 / S->elem_bytes) * S->elem_bytes;
+    auto pow2 = [](int32_t x) { return x > 0 && (x & (x - 1)) == 0; };
+    auto lg = [](int32_t x) {
+      int32_t k = 0;
+      while ((1 << k) < x) ++k;
+      return k;
+    };
+    bool ok = (st > 0 || dt > 0) && st >= 0 && dt >= 0 && (st || plain_rows(S)) && (dt || plain_rows(D)) &&
+              S->d.head_dim % 8 == 0 && pow2(S->d.head_dim / 8) && pow2(S->d.block_size) &&
+              pow2(D->d.block_size) && D->d.block_size % S->d.block_size == 0 && smem <= (size_t)kTrSmemLimit;
+    for (int i = 0; i < n_src && ok; ++i) ok = ptr_aligned(src_pools[i], 16);
+    for (int i = 0; i < n_dst && ok; ++i) ok = ptr_aligned(dst_pools[i], 16);
+    if (ok) {
+      a.s_tr = st;
+      a.d_tr = dt;
+      a.s_x = 1 << S->dk;
+      a.d_x = 1 << D->dk;
+      a.tr_lbp = lg(S->d.block_size);
+      a.tr_lbd = lg(D->d.block_size);
+      a.s_lm = S->dk >= 3 ? S->dk - 3 : 0;
+      a.d_lm = D->dk >= 3 ? D->dk - 3 : 0;
+      a.cpr_shift = lg(S->d.head_dim / 8);
+      for (int ax = 0; ax < 6; ++ax) {
+        a.ss[ax] = S->stride[ax];
+        a.ds[ax] = D->stride[ax];
+      }
+      a.Hp = Hp;
+      a.Hd = Hd;
+      a.D = S->d.head_dim;
+      a.Bp = S->d.block_size;
+      a.Bd = D->d.block_size;
+      a.s_l0 = S->d.first_layer;
+      a.d_l0 = D->d.first_layer;
+      a.s_blk_off = src_bt->blk_off;
+      a.s_blk_ids = src_bt->blk_ids;
+      a.d_blk_off = dst_bt->blk_off;
+      a.d_blk_ids = dst_bt->blk_ids;
+      a.d_blk_req = dst_bt->blk_req;
+      a.tok_off = dst_bt->tok_off;
+      a.f_hp = make_fastdiv(Hp);
+      a.f_hde = make_fastdiv((uint32_t)a.Hd_eff);
+      a.f_bl = make_fastdiv((uint32_t)std::max<int64_t>(dst_bt->total_blocks, 1));
+      if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
+      const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * (a.kv1 ? 1 : 2) * a.Hd_eff;
+      const int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / std::max<uint64_t>(per_layer, 1));
+      for (int32_t l0 = lb; l0 < le; l0 += step) {
+        const int32_t l1 = std::min(le, l0 + step);
+        a.lb = l0;
+        a.Lc = l1 - l0;
+        a.f_l = make_fastdiv((uint32_t)a.Lc);
+        a.n_items = (uint32_t)(per_layer * (uint64_t)a.Lc);
+        t_last_kernel = "k_convert_tr";
+        cudaError_t e = launch_convert_tr(a, S->d.dtype, D->d.dtype, (cudaStream_t)stream);
+        if (e != cudaSuccess) return cuda_fail(e, "kv_convert_reshard: launch");
+      }
+      return KV_OK;
+    }
+  }
+  bool fast = rows_side(S, &a.s_ck, &a.s_chs) && rows_side(D, &a.d_ck, &a.d_chs);
+  a.split = (S->dk || D->dk) ? 1 : 0;
   for (int i = 0; i < n_src && fast; ++i) fast = ptr_aligned(src_pools[i], 16);
   for (int i = 0; i < n_dst && fast; ++i) fast = ptr_aligned(dst_pools[i], 16);
   const int vec = fast ? 8 : 1;
@@ -558,7 +645,7 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
   a.f_cpr = make_fastdiv(ndch);
   a.f_nd = make_fastdiv((uint32_t)n_dst);
   if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
-  if (fast && S->d.dtype == D->d.dtype) {
+  if (fast && !a.split && S->d.dtype == D->d.dtype) {
     bool used = false;
     if ((st = try_tile_copy(n_src, src, src_pools, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, share,
                             &used)) != KV_OK)

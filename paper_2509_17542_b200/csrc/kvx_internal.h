@@ -43,8 +43,18 @@ FastDiv make_fastdiv(uint32_t d);
 
 // ---- kernel argument blocks (by value) -------------------------------------------
 struct ConvArgs {
-  int32_t kv1, c0;
-  int32_t s_dk, d_dk;  // head_dim split (log2 x) of source / destination (element-wise kernel)  // K-only / V-only transfer: kv1 = 1 and c0 the one K/V index (reading 27)
+  int32_t kv1, c0;     // K-only / V-only transfer: kv1 = 1 and c0 the one K/V index (reading 27)
+  int32_t s_dk, d_dk;  // head_dim split (log2 x) of source / destination (element-wise kernel)
+  // row kernel over an x-split head_dim (x >= 8 elements): chunk (8 elements) ch of a row at
+  // byte offset (ch >> ck) * chs + (ch & (2^ck - 1)) * 8 * element bytes; split = 0: plain rows
+  int32_t split, s_ck, d_ck;
+  int64_t s_chs, d_chs;
+  // smem-transpose kernel (k_convert_tr): a side whose two innermost axes are (DIM, SLOT)
+  // -- a head_dim-major value cache -- is read / written as whole (DIM x SLOT) tiles
+  // (mode 1); or whose head_dim is x-split with (D/x, SLOT, x) innermost (mode 2, x = s_x/d_x)
+  int32_t s_tr, d_tr, s_x, d_x;
+  int32_t tr_lbp, tr_lbd, s_lm, d_lm;  // log2 of Bp, Bd, s_x / 8, d_x / 8
+  FastDiv f_hde;  // D-local heads per item loop (Hd_eff)
   const uint8_t* src[KVX_MAX_RANKS];
   uint8_t* dst[KVX_MAX_RANKS];
   const float* sscale[KVX_MAX_RANKS];  // per source index (e4m3 sources)
@@ -79,7 +89,7 @@ struct ConvArgs {
 // P rank, source block) lands the sub-tile in smem already in D's order (the tensor map's
 // dimension order is D's), then bulk stores write D's contiguous runs.
 struct TileArgs {
-  int32_t kv1, c0;  // K-only / V-only transfer: kv1 = 1 and c0 the one K/V index (reading 27)
+  int32_t kv1, c0;  // K-only / V-only transfer (reading 27)
   CUtensorMap maps[KVX_MAX_RANKS][2];  // [source index][K/V]: dims (DIM, A, B, BLOCK, LAYER)
   uint8_t* dst[KVX_MAX_RANKS];
   int8_t dst_rank[KVX_MAX_RANKS];
@@ -151,7 +161,7 @@ struct UnpackArgs {
 // ((((dst block, local layer), K/V), sub-tile), source).  Same dtype on wire and pool.
 #define KVX_MAX_RING 8
 struct PullArgs {
-  int32_t kv1, c0;  // K-only / V-only transfer: kv1 = 1 and c0 the one K/V index (reading 27)
+  int32_t kv1, c0;  // K-only / V-only transfer (reading 27)
   uint8_t* dst;
   const uint8_t* ring[KVX_MAX_RANKS][KVX_MAX_RING];  // [source][slot] peer-mapped
   const uint32_t* ready[KVX_MAX_RANKS];               // local words P writes
@@ -209,6 +219,9 @@ kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void*
 cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s);
 cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out_scales, cudaStream_t s);
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s);
+// k_convert_tr: a side with (DIM, SLOT) innermost (a.s_tr / a.d_tr), items in a.n_items
+cudaError_t launch_convert_tr(const ConvArgs& a, int sdt, int ddt, cudaStream_t s);
+constexpr int kTrSmemLimit = 200 * 1024;  // per CTA (4 warps x one Bd x D tile each)
 cudaError_t launch_tile_copy(const TileArgs& a, cudaStream_t s);
 cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaStream_t s);

@@ -138,6 +138,25 @@ __device__ __forceinline__ uint32_t get_elem(const uint32_t* w, int i) {
 }
 
 template <int DT>
+__device__ __forceinline__ void put_elem(uint32_t* w, int i, uint32_t e) {
+  if constexpr (Tr<DT>::B == 4) w[i] = e;
+  else if constexpr (Tr<DT>::B == 2) w[i >> 1] |= (e & 0xFFFFu) << ((i & 1) * 16);
+  else w[i >> 2] |= (e & 0xFFu) << ((i & 3) * 8);
+}
+
+// shared-memory chunk moves (k_convert_tr's tile rows are 16-B aligned)
+template <int DT, int VEC>
+__device__ __forceinline__ void store_chunk_smem(uint8_t* p, const Chunk<DT, VEC>& c) {
+#pragma unroll
+  for (int i = 0; i < Chunk<DT, VEC>::WORDS; ++i) reinterpret_cast<uint32_t*>(p)[i] = c.w[i];
+}
+template <int DT, int VEC>
+__device__ __forceinline__ void load_chunk_smem(Chunk<DT, VEC>& c, const uint8_t* p) {
+#pragma unroll
+  for (int i = 0; i < Chunk<DT, VEC>::WORDS; ++i) c.w[i] = reinterpret_cast<const uint32_t*>(p)[i];
+}
+
+template <int DT>
 __device__ __forceinline__ float to_f32(uint32_t b) {
   if constexpr (DT == KV_F16) {
     return __half2float(__ushort_as_half((unsigned short)b));
@@ -244,6 +263,17 @@ template <int DT, int VEC>
 __device__ __forceinline__ void zero_chunk(Chunk<DT, VEC>& c) {
 #pragma unroll
   for (int i = 0; i < Chunk<DT, VEC>::WORDS; ++i) c.w[i] = 0;
+}
+// zero elements [k, VEC) of a chunk (slots past the request's last token)
+template <int DT, int VEC>
+__device__ __forceinline__ void zero_tail(Chunk<DT, VEC>& c, uint32_t k) {
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    if ((uint32_t)i < k) continue;
+    if constexpr (Tr<DT>::B == 4) c.w[i] = 0u;
+    else if constexpr (Tr<DT>::B == 2) c.w[i >> 1] &= ~(0xFFFFu << ((i & 1) * 16));
+    else c.w[i >> 2] &= ~(0xFFu << ((i & 3) * 8));
+  }
 }
 
 __device__ __forceinline__ uint32_t divmod(uint32_t& n, const FastDiv& f) {
@@ -367,9 +397,17 @@ __global__ void __launch_bounds__(kThreads) k_convert(const __grid_constant__ Co
 // destination); an fp8 -> other-fp8 cast takes the source scale in rsc and RN(1/s_dst) in
 // rsc2 (the only instantiations that carry the second register).
 // ------------------------------------------------------------------------------------
-template <int SDT, int DDT, int U, int VEC = 8, bool COH = false>
+// Where chunk ch of a row lives when head_dim is x-split (reading 27): chunk ch covers
+// elements [8ch, 8ch + 8), which sit in x-group ch >> k (k = log2(x / 8)) at byte stride hs,
+// at (ch & (2^k - 1)) * 8 elements inside it.  Unsplit: k = 0, hs = 8 * element bytes.
+struct ChunkMap {
+  int32_t sk, dk;
+  int64_t shs, dhs;
+};
+
+template <int SDT, int DDT, int U, int VEC = 8, bool COH = false, bool SPLIT = false>
 __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t sp, uint64_t dp, float rsc,
-                                            uint32_t rz, float rsc2 = 1.f) {
+                                            uint32_t rz, float rsc2 = 1.f, const ChunkMap* cm = nullptr) {
   constexpr bool DUAL = dual_scale(SDT, DDT);
   const uint32_t cmask = (1u << cs) - 1u;
   const uint32_t nch = 32u << cs;
@@ -388,7 +426,10 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
       z[k] = __shfl_sync(0xffffffffu, rz, rr) | (idx >= nch ? 2u : 0u);
       sc[k] = __shfl_sync(0xffffffffu, rsc, rr);
       if constexpr (DUAL) sc2[k] = __shfl_sync(0xffffffffu, rsc2, rr);
-      if (z[k] == 0) load_chunk<SDT, VEC, COH>(in[k], reinterpret_cast<const uint8_t*>(s) + ch[k] * (VEC * Tr<SDT>::B));
+      uint64_t soff = ch[k] * (VEC * Tr<SDT>::B);
+      if constexpr (SPLIT)
+        soff = (uint64_t)(ch[k] >> cm->sk) * (uint64_t)cm->shs + (ch[k] & ((1u << cm->sk) - 1u)) * (VEC * Tr<SDT>::B);
+      if (z[k] == 0) load_chunk<SDT, VEC, COH>(in[k], reinterpret_cast<const uint8_t*>(s) + soff);
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -400,7 +441,10 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
         cast_chunk<SDT, DDT, VEC>(in[k], o, sc[k], sc2[k]);
       else
         cast_chunk<SDT, DDT, VEC>(in[k], o, sc[k], sc[k]);
-      store_chunk<DDT, VEC>(reinterpret_cast<uint8_t*>(d[k]) + ch[k] * (VEC * Tr<DDT>::B), o);
+      uint64_t doff = ch[k] * (VEC * Tr<DDT>::B);
+      if constexpr (SPLIT)
+        doff = (uint64_t)(ch[k] >> cm->dk) * (uint64_t)cm->dhs + (ch[k] & ((1u << cm->dk) - 1u)) * (VEC * Tr<DDT>::B);
+      store_chunk<DDT, VEC>(reinterpret_cast<uint8_t*>(d[k]) + doff, o);
     }
   }
 }
@@ -480,31 +524,26 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
   }
 }
 
-template <int SDT, int DDT, int U, int VEC = 8>
+template <int SDT, int DDT, int U, int VEC = 8, bool SPLIT = false>
 __global__ void __launch_bounds__(kThreads, KVX_MINB) k_convert_rows(const __grid_constant__ ConvArgs a) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
   const uint32_t cs = (uint32_t)a.cpr_shift;
+  const ChunkMap cm{a.s_ck, a.d_ck, a.s_chs, a.d_chs};
   for (uint32_t item = warp; item < a.n_items; item += nwarps) {
     uint64_t sp, dp;
     float rsc, rsc2;
     uint32_t rz;
     conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz, rsc2);
-    stream_rows<SDT, DDT, U, VEC>(lane, cs, sp, dp, rsc, rz, rsc2);
+    stream_rows<SDT, DDT, U, VEC, false, SPLIT>(lane, cs, sp, dp, rsc, rz, rsc2, &cm);
   }
 }
 
 // ------------------------------------------------------------------------------------
-// K1/K4 TMA-staged variant.  Same items and per-lane row decode as k_convert_rows, but
-// the source rows travel HBM -> shared memory through the TMA engine (cp.async.bulk, one
-// bulk copy per row, completion counted on a per-stage mbarrier), so the bytes in flight
-// are bounded by shared memory (kTmaStages stages x 32 rows per warp), not registers.
-// Same dtype: rows go back out smem -> global (or peer) by bulk stores, no register pass.
-// With a cast: lanes read 16-B pieces from smem, convert, and store from registers.
-// ------------------------------------------------------------------------------------
-constexpr int kTmaWarps = 4;
-constexpr int kTmaStages = 4;
+// TMA / bulk-copy helpers (k_tile_copy).  A per-row TMA-staged variant of the convert
+// (one cp.async.bulk per 256-B row into smem) was measured at 0.61 of copy on c2 and 0.27
+// with a cast (profiles/r01/tma_variant_ab.txt) and removed.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -523,13 +562,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_u32(smem_src)),
                "r"(bytes)
@@ -543,92 +575,6 @@ __device__ __forceinline__ void bulk_wait_read() {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-template <int SDT, int DDT>
-__global__ void __launch_bounds__(kTmaWarps * 32) k_convert_tma(const __grid_constant__ ConvArgs a) {
-  extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int VEC = 8;
-  const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t wl = threadIdx.x >> 5;  // warp within the CTA
-  const uint32_t wpc = blockDim.x >> 5;  // warps per CTA (<= kTmaWarps, set by smem)
-  const uint32_t warp = blockIdx.x * wpc + wl;
-  const uint32_t nwarps = gridDim.x * wpc;
-  const uint32_t cs = (uint32_t)a.cpr_shift;
-  const uint32_t RB = (uint32_t)a.D * Tr<SDT>::B;  // source row bytes (multiple of 16)
-  // per-warp region: [stages][32 rows][RB] data, then per-stage row state, then barriers
-  uint8_t* wbase = smem + (size_t)wl * (kTmaStages * 32u * RB + kTmaStages * 32u * 16u + kTmaStages * 8u);
-  uint8_t* data = wbase;
-  uint64_t* st_dp = reinterpret_cast<uint64_t*>(wbase + kTmaStages * 32u * RB);
-  float* st_sc = reinterpret_cast<float*>(st_dp + kTmaStages * 32);
-  uint32_t* st_rz = reinterpret_cast<uint32_t*>(st_sc + kTmaStages * 32);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(st_rz + kTmaStages * 32);
-  if (lane == 0)
-    for (int s = 0; s < kTmaStages; ++s) mbar_init(bars + s, 1);
-  fence_proxy_async();
-  __syncwarp();
-  // issue the loads of the k-th item of this warp into stage s
-  auto issue = [&](uint32_t k, int s) {
-    const uint32_t item = warp + k * nwarps;
-    uint64_t sp, dp;
-    float rsc, rsc2;  // dual-scale casts never take this kernel (launcher)
-    uint32_t rz;
-    conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz, rsc2);
-    st_dp[s * 32 + lane] = dp;
-    st_sc[s * 32 + lane] = rsc;
-    st_rz[s * 32 + lane] = rz;
-    const uint32_t ncopy = __popc(__ballot_sync(0xffffffffu, rz == 0));
-    if (lane == 0) mbar_expect_tx_arrive(bars + s, ncopy * RB);
-    __syncwarp();
-    if (rz == 0) bulk_load(data + ((size_t)s * 32 + lane) * RB, reinterpret_cast<const void*>(sp), RB, bars + s);
-  };
-  const uint32_t my_items = warp < a.n_items ? (a.n_items - warp + nwarps - 1) / nwarps : 0;
-  for (uint32_t k = 0; k < my_items && k < (uint32_t)kTmaStages; ++k) issue(k, (int)k);
-  for (uint32_t k = 0; k < my_items; ++k) {
-    const int s = (int)(k % kTmaStages);
-    mbar_wait(bars + s, (k / kTmaStages) & 1u);
-    const uint64_t dp = st_dp[s * 32 + lane];
-    const uint32_t rz = st_rz[s * 32 + lane];
-    const uint8_t* sbuf = data + (size_t)s * 32 * RB;
-    if constexpr (SDT == DDT) {
-      if (rz == 0) {
-        bulk_store(reinterpret_cast<void*>(dp), sbuf + lane * RB, RB);
-      } else if (rz == 1) {
-        for (uint32_t o = 0; o < RB; o += 16)
-          asm volatile("st.global.v4.u32 [%0], {%1,%1,%1,%1};" ::"l"(dp + o), "r"(0u) : "memory");
-      }
-      bulk_commit();
-      // the stage is reloaded only after its bulk stores have read it: reload the stage
-      // consumed in the previous iteration, whose store group is now the older one
-      bulk_wait_read<1>();
-      __syncwarp();
-      if (k >= 1 && k - 1 + kTmaStages < my_items) issue(k - 1 + kTmaStages, (int)((k - 1) % kTmaStages));
-    } else {
-      const uint32_t cmask = (1u << cs) - 1u;
-      const uint32_t nch = 32u << cs;
-      for (uint32_t idx = lane; idx < nch; idx += 32u) {
-        const uint32_t rr = idx >> cs, ch = idx & cmask;
-        const uint32_t z = st_rz[s * 32 + rr];
-        if (z == 2) continue;
-        const uint64_t d = st_dp[s * 32 + rr];
-        Chunk<DDT, VEC> o;
-        if (z == 1) {
-          zero_chunk(o);
-        } else {
-          Chunk<SDT, VEC> in;
-          const uint8_t* src = sbuf + rr * RB + ch * (VEC * Tr<SDT>::B);
-#pragma unroll
-          for (int w = 0; w < Chunk<SDT, VEC>::WORDS; ++w) in.w[w] = reinterpret_cast<const uint32_t*>(src)[w];
-          const float sc = st_sc[s * 32 + rr];
-          cast_chunk<SDT, DDT, VEC>(in, o, sc, sc);
-        }
-        store_chunk<DDT, VEC>(reinterpret_cast<uint8_t*>(d) + ch * (VEC * Tr<DDT>::B), o);
-      }
-      fence_proxy_async();  // generic-proxy reads of the stage before the async refill
-      __syncwarp();
-      if (k + kTmaStages < my_items) issue(k + kTmaStages, s);
-    }
-  }
-  if constexpr (SDT == DDT) bulk_wait_all();
-}
 
 // ------------------------------------------------------------------------------------
 // K1/K4 same-dtype TMA tile path (k_tile_copy).  One warp per CTA is a copy engine: per
@@ -760,6 +706,166 @@ __global__ void __launch_bounds__(32) k_tile_copy(const __grid_constant__ TileAr
     if (k >= 1 && k - 1 + S < my) issue(k - 1 + S, (k - 1) % S);
   }
   bulk_wait_all();
+}
+
+// ------------------------------------------------------------------------------------
+// K1 with a head_dim-major side (reading 27): a pool whose two innermost axes are
+// (DIM, SLOT) -- the value cache of other vendors' paged-attention kernels, V [blocks,
+// heads, D, block] -- stores one (block, head) tile as D rows of B slots, so a token's
+// head_dim row is strided.  One warp per item = (dst rank, dst block, layer, K/V, dst
+// head): it loads the item's source tile(s) with 8-element vector loads into shared memory
+// in [slot][d] order (scattering each (d, 8 slots) vector when the source is head_dim-
+// major), then writes the destination tile with 8-element vector stores (gathering 8 slots
+// of one d when the destination is head_dim-major), casting on the way; tail slots are
+// zero.  The transpose costs shared-memory traffic only; HBM sees whole-tile reads and
+// writes.
+// ------------------------------------------------------------------------------------
+constexpr int kTrWarps = 4;
+
+template <int SDT, int DDT>
+__global__ void __launch_bounds__(kTrWarps * 32) k_convert_tr(const __grid_constant__ ConvArgs a) {
+  extern __shared__ __align__(16) uint8_t tr_smem[];
+  constexpr int VEC = 8;
+  constexpr uint32_t SB = Tr<SDT>::B;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t wl = threadIdx.x >> 5;
+  const uint32_t warp = blockIdx.x * kTrWarps + wl;
+  const uint32_t nwarps = gridDim.x * kTrWarps;
+  // every extent below is a power of two (checked by the caller): index math is shifts
+  const uint32_t lbp = (uint32_t)a.tr_lbp, lbd = (uint32_t)a.tr_lbd, lcpr = (uint32_t)a.cpr_shift;
+  const uint32_t Bp = 1u << lbp, Bd = 1u << lbd;
+  const uint32_t D = (uint32_t)a.D;
+  const uint32_t LD = D + 16u / SB;  // padded smem row (elements): 16 B of padding per slot row
+  uint8_t* tile = tr_smem + (size_t)wl * Bd * LD * SB;
+  const uint32_t lsm = (uint32_t)a.s_lm, ldm = (uint32_t)a.d_lm;  // log2(x / 8) per side (mode 2)
+  for (uint32_t item = warp; item < a.n_items; item += nwarps) {
+    uint32_t n = item;
+    const uint32_t hl = divmod(n, a.f_hde);
+    const uint32_t c = take_kv(n, a.kv1, a.c0);
+    const uint32_t l = divmod(n, a.f_l);
+    const uint32_t bl = divmod(n, a.f_bl);
+    const uint32_t qi = n;
+    const uint32_t hq = (uint32_t)a.hq_off[qi] + hl;
+    const int32_t r = __ldg(a.d_blk_req + bl);
+    const int32_t tok0 = __ldg(a.tok_off + r);
+    const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+    const uint32_t tb0 = (uint32_t)(bl - __ldg(a.d_blk_off + r)) << lbd;  // first token of the dst block
+    const int64_t layer = a.lb + (int64_t)l;
+    const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;
+    const uint32_t h = (uint32_t)a.dst_rank[qi] * (uint32_t)a.Hd + hq;
+    const uint32_t p = fdiv(h, a.f_hp);
+    const uint32_t hp = h - p * (uint32_t)a.Hp;
+    const int si = a.src_of_p[p];
+    float rsc = 1.f, rsc2 = 1.f;
+    if constexpr (dual_scale(SDT, DDT)) {
+      rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+      rsc2 = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+    } else {
+      if constexpr (is_fp8(SDT) && SDT != DDT) rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+      if constexpr (is_fp8(DDT) && SDT != DDT) rsc = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+    }
+    const uint32_t valid = (int32_t)tb0 >= T ? 0u : min(Bd, (uint32_t)T - tb0);  // slots with data
+    // ---- load: the source blocks covering [tb0, tb0 + valid) into tile[slot][d] ----
+    const uint32_t nsrc = (valid + Bp - 1) >> lbp;
+    const int32_t* sids = a.s_blk_ids + __ldg(a.s_blk_off + r) + (int32_t)(tb0 >> lbp);
+    for (uint32_t j = 0; j < nsrc; ++j) {
+      const int64_t sblk = __ldg(sids + j);
+      const uint8_t* sb = a.src[si] + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] +
+                                       sblk * a.ss[KV_AX_BLOCK] + (int64_t)hp * a.ss[KV_AX_HEAD]) * SB;
+      uint8_t* trow = tile + (size_t)(j << lbp) * LD * SB;
+      const uint32_t nch = Bp << lcpr;  // 8-element chunks in one source tile
+      if (a.s_tr == 1) {        // (D, Bp) tile, contiguous: chunk v = (d, 8 consecutive slots)
+#pragma unroll 8
+        for (uint32_t v = lane; v < nch; v += 32u) {
+          Chunk<SDT, VEC> x;
+          load_chunk<SDT, VEC>(x, sb + (size_t)v * VEC * SB);
+          const uint32_t d = v >> (lbp - 3), s0 = (v & ((Bp >> 3) - 1)) << 3;
+#pragma unroll
+          for (int i = 0; i < VEC; ++i) {
+            const uint32_t e = get_elem<SDT>(x.w, i);
+            uint8_t* dst = trow + ((size_t)(s0 + i) * LD + d) * SB;
+            if constexpr (SB == 1) *dst = (uint8_t)e;
+            else if constexpr (SB == 2) *reinterpret_cast<uint16_t*>(dst) = (uint16_t)e;
+            else *reinterpret_cast<uint32_t*>(dst) = e;
+          }
+        }
+      } else if (a.s_tr == 2) { // (D/x, Bp, x) tile, contiguous: chunk v = (x-group g, 8 of x)
+#pragma unroll 8
+        for (uint32_t v = lane; v < nch; v += 32u) {
+          Chunk<SDT, VEC> x;
+          load_chunk<SDT, VEC>(x, sb + (size_t)v * VEC * SB);
+          const uint32_t g = v >> lsm, s = g & (Bp - 1);
+          const uint32_t d0 = ((g >> lbp) << (lsm + 3)) + ((v & ((1u << lsm) - 1u)) << 3);
+          store_chunk_smem<SDT, VEC>(trow + ((size_t)s * LD + d0) * SB, x);
+        }
+      } else {                  // rows: chunk v = (slot, 8 consecutive d)
+#pragma unroll 8
+        for (uint32_t v = lane; v < nch; v += 32u) {
+          Chunk<SDT, VEC> x;
+          const uint32_t s = v >> lcpr, d0 = (v & ((1u << lcpr) - 1u)) << 3;
+          load_chunk<SDT, VEC>(x, sb + ((int64_t)s * a.ss[KV_AX_SLOT] + d0) * SB);
+          store_chunk_smem<SDT, VEC>(trow + ((size_t)s * LD + d0) * SB, x);
+        }
+      }
+    }
+    __syncwarp();
+    // ---- store: the destination tile, cast, tail slots zero ----
+    uint8_t* db = a.dst[qi] + (dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] +
+                               (int64_t)__ldg(a.d_blk_ids + bl) * a.ds[KV_AX_BLOCK] + (int64_t)hq * a.ds[KV_AX_HEAD]) *
+                              Tr<DDT>::B;
+    const uint32_t nchd = Bd << lcpr;
+    const float s2 = dual_scale(SDT, DDT) ? rsc2 : rsc;
+    if (a.d_tr == 1) {          // (D, Bd) tile: chunk v = (d, 8 consecutive slots)
+#pragma unroll 4
+      for (uint32_t v = lane; v < nchd; v += 32u) {
+        const uint32_t d = v >> (lbd - 3), s0 = (v & ((Bd >> 3) - 1)) << 3;
+        Chunk<SDT, VEC> x;
+        Chunk<DDT, VEC> o;
+#pragma unroll
+        for (int i = 0; i < Chunk<SDT, VEC>::WORDS; ++i) x.w[i] = 0;
+#pragma unroll
+        for (int i = 0; i < VEC; ++i) {
+          const uint8_t* src = tile + ((size_t)(s0 + i) * LD + d) * SB;
+          const uint32_t e = SB == 1 ? *src : SB == 2 ? *reinterpret_cast<const uint16_t*>(src)
+                                                       : *reinterpret_cast<const uint32_t*>(src);
+          put_elem<SDT>(x.w, i, e);
+        }
+        if (s0 >= valid) {
+          zero_chunk(o);
+        } else {
+          cast_chunk<SDT, DDT, VEC>(x, o, rsc, s2);
+          if (s0 + VEC > valid) zero_tail<DDT, VEC>(o, valid - s0);  // slots past T in this chunk
+        }
+        store_chunk<DDT, VEC>(db + (size_t)v * VEC * Tr<DDT>::B, o);
+      }
+    } else {
+#pragma unroll 4
+      for (uint32_t v = lane; v < nchd; v += 32u) {
+        uint32_t s, d0;
+        int64_t doff;
+        if (a.d_tr == 2) {      // (D/x, Bd, x) tile: chunk v = (x-group g, 8 of x)
+          const uint32_t g = v >> ldm;
+          s = g & (Bd - 1);
+          d0 = ((g >> lbd) << (ldm + 3)) + ((v & ((1u << ldm) - 1u)) << 3);
+          doff = (int64_t)v * VEC;
+        } else {                // rows: chunk v = (slot, 8 consecutive d)
+          s = v >> lcpr;
+          d0 = (v & ((1u << lcpr) - 1u)) << 3;
+          doff = (int64_t)s * a.ds[KV_AX_SLOT] + d0;
+        }
+        Chunk<DDT, VEC> o;
+        if (s >= valid) {
+          zero_chunk(o);
+        } else {
+          Chunk<SDT, VEC> x;
+          load_chunk_smem<SDT, VEC>(x, tile + ((size_t)s * LD + d0) * SB);
+          cast_chunk<SDT, DDT, VEC>(x, o, rsc, s2);
+        }
+        store_chunk<DDT, VEC>(db + doff * Tr<DDT>::B, o);
+      }
+    }
+    __syncwarp();
+  }
 }
 
 // ------------------------------------------------------------------------------------
@@ -1360,32 +1466,16 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
     a.f_sb = make_fastdiv(nsb);
     a.f_items = make_fastdiv(nsb * nhb);
     a.n_items = (uint32_t)((uint64_t)a.total / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);
-    // TMA-staged variant (KVX_TMA=1, experiment until measured): source rows must be whole
-    // 16-byte multiples for cp.async.bulk
-    static const int tma = getenv("KVX_TMA") ? atoi(getenv("KVX_TMA")) : 0;
-    static const bool wide = getenv("KVX_VEC16") ? atoi(getenv("KVX_VEC16")) == 1 : false;
-    const uint32_t RB = (uint32_t)a.D * Tr<SDT>::B;
-    if (tma == 1 && RB % 16 == 0 && !dual_scale(SDT, DDT)) {
-      auto k = k_convert_tma<SDT, DDT>;
-      const size_t per_warp = (size_t)kTmaStages * 32 * RB + (size_t)kTmaStages * 32 * 16 + kTmaStages * 8;
-      int nw = (int)std::min<size_t>(kTmaWarps, (200u * 1024u) / per_warp);
-      if (nw < 1) nw = 1;
-      const size_t smem = per_warp * nw;
-      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, nw * 32, smem);
-      if (occ < 1) occ = 1;
-      const uint64_t need = (a.n_items + nw - 1) / nw;
-      const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms() * occ));
-      k<<<grid, nw * 32, smem, s>>>(a);
+    static const int wide1 = getenv("KVX_FP8_VEC16") ? atoi(getenv("KVX_FP8_VEC16")) : 0;
+    if (a.split) {
+      auto k = k_convert_rows<SDT, DDT, U, 8, true>;
+      k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
     } else {
       bool done = false;
-      if constexpr (Tr<SDT>::B == 2 && DDT == KV_F8E4M3) {
-        if (wide && cpr >= 2) {
-          // 16 elements per chunk: two 16-B loads, one 16-B store (peer writes go out as
-          // full 16-B vectors); half the chunks per row, same bytes in flight per lane
+      if constexpr (Tr<SDT>::B == 1 && Tr<DDT>::B <= 2) {
+        if (wide1 && cpr >= 2) {  // 1-byte sources: 16-element chunks = whole 16-B loads (experiment)
           a.cpr_shift = log2_pow2(cpr / 2);
-          auto k = k_convert_rows<SDT, DDT, (U > 1 ? U / 2 : 1), 16>;
+          auto k = k_convert_rows<SDT, DDT, 2, 16>;
           k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
           done = true;
         }
@@ -1465,6 +1555,26 @@ cudaError_t unpack_t(const UnpackArgs& a0, cudaStream_t s) {
   }                                                                            \
   return cudaErrorInvalidValue;
 
+template <int VEC, int SDT, int DDT>
+cudaError_t tr_t(const ConvArgs& a, cudaStream_t s) {
+  const size_t smem = (size_t)kTrWarps * a.Bd * (a.D + 16 / Tr<SDT>::B) * Tr<SDT>::B;
+  auto k = k_convert_tr<SDT, DDT>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kTrWarps * 32, smem);
+  if (occ < 1) occ = 1;
+  const uint64_t need = (a.n_items + kTrWarps - 1) / kTrWarps;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms() * occ));
+  k<<<grid, kTrWarps * 32, smem, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+template <int VEC>
+cudaError_t tr_v(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
+  KVX_DISPATCH(tr_t, VEC, sdt, ddt, a, s)
+}
+
 template <int VEC>
 cudaError_t conv_v(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
   KVX_DISPATCH(conv_t, VEC, sdt, ddt, a, s)
@@ -1480,6 +1590,10 @@ cudaError_t unpack_v(const UnpackArgs& a, int wdt, int ddt, cudaStream_t s) {
 
 }  // namespace
 
+cudaError_t launch_convert_tr(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
+  if (a.n_items == 0) return cudaSuccess;
+  return tr_v<8>(a, sdt, ddt, s);
+}
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s) {
   if (a.total == 0) return cudaSuccess;
   return vec == 8 ? conv_v<8>(a, sdt, ddt, s) : conv_v<1>(a, sdt, ddt, s);

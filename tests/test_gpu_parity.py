@@ -492,13 +492,14 @@ def test_layout_variants_convert_and_wire(o1, seed):
 
 def test_other_vendor_prefill_to_nvidia_decode(o1):
     """The multi-vendor pairing end to end on one GPU: a P instance whose engine keeps an
-    x-packed key cache (BLOCK, HEAD, D/8, SLOT, [LAYER], x=8) and a head_dim-major value
-    cache (BLOCK, HEAD, DIM, SLOT) in two pools, fp8 e4m3fnuz with per-head scales, TP2 ->
+    x-packed key cache ([LAYER], BLOCK, HEAD, D/8, SLOT, x=8) and a head_dim-major value
+    cache ([LAYER], BLOCK, HEAD, DIM, SLOT) in two pools, fp8 e4m3fnuz with per-head scales, TP2 ->
     a D instance with one block-major K+V pool in OCP e4m3fn, TP1 (merge), block 16 -> 32.
     Two convert calls (K, then V) == O1 on the same pools."""
     from tests.gpu_util import DevCase
-    korder = (BLOCK, HEAD, DIM, SLOT, LAYER, KV)
-    vorder = (BLOCK, HEAD, DIM, SLOT, LAYER, KV)
+    import paper_2509_17542_b200 as kvx
+    korder = (LAYER, KV, BLOCK, HEAD, DIM, SLOT)   # per-layer tensors, KV extent 1; x-split below
+    vorder = (LAYER, KV, BLOCK, HEAD, DIM, SLOT)   # head_dim-major: k_convert_tr
     args = (3, 8, 64, 2, 1, 16, 32, [70, 5, 33], FNUZ, E4M3)
     kw = dict(d_order=synth.D_ORDER, seed=77, o1=o1, scales="pow2")
     kc = make_case(*args, p_order=korder, p_kv_part=1, p_split=8, **kw)
@@ -511,7 +512,9 @@ def test_other_vendor_prefill_to_nvidia_decode(o1):
     dv_ = DevCase(vc)
     dv_.dst_pools = dk_.dst_pools
     dk_.convert()
+    assert kvx.last_kernel() == "k_convert_tr"        # x-split (D/x, SLOT, x) tiles: smem staging
     dv_.convert()
+    assert kvx.last_kernel() == "k_convert_tr"        # head_dim-major: smem transpose
     want = expected(kc, o1)
     want = [w.copy() for w in want]
     o1.convert(vc["src_lays"], vc["src_pools"], vc["dst_lays"], want, vc["n_tokens"], vc["src_tables"],
