@@ -213,6 +213,47 @@ __device__ __forceinline__ uint32_t f32x2_to_fnuzx2(float lo, float hi) {
   return fnuz_fix(r & 0xFFu, lo) | (fnuz_fix((r >> 8) & 0xFFu, hi) << 8);
 }
 
+
+// Four e4m3fnuz codes of scaled values f[0..3], branch-free (no divergence on data): the
+// hardware e4m3fn conversion of 2v, then per byte: v > 232 -> 0x7F | sign, NaN -> 0x80,
+// -0 (0x80) -> 0x00 (reading 25).
+__device__ __forceinline__ uint32_t f32x4_to_fnuzx4(const float* f) {
+  uint32_t r = f32x2_to_e4m3x2(__fmul_rn(f[0], 2.0f), __fmul_rn(f[1], 2.0f)) |
+               (f32x2_to_e4m3x2(__fmul_rn(f[2], 2.0f), __fmul_rn(f[3], 2.0f)) << 16);
+  const uint32_t x = r ^ 0x80808080u;  // bytes equal to 0x80 become 0
+  r ^= ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;  // exact per-byte zero test: -0 -> +0
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float a = fabsf(f[i]);
+    const uint32_t sh = 8 * i, sat = (0x7Fu | ((__float_as_uint(f[i]) >> 24) & 0x80u)) << sh;
+    r = a > 232.0f ? ((r & ~(0xFFu << sh)) | sat) : r;
+    r = a != a ? ((r & ~(0xFFu << sh)) | (0x80u << sh)) : r;
+  }
+  return r;
+}
+
+// Four e4m3fnuz codes -> f32, branch-free: every fnuz value is half the e4m3fn value of its
+// bits, so the hardware e4m3fn -> f16 conversion times 0.5 (exact) decodes all but
+// 0x7F / 0xFF (+-240: the fn NaN slot) and 0x80 (NaN), which are selected in.
+__device__ __forceinline__ void fnuzx4_to_f32(uint32_t w, float* f) {
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    uint32_t h2;
+    const unsigned short in = (unsigned short)(w >> (16 * h));
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(in));
+    const __half2 v = __hmul2(*reinterpret_cast<const __half2*>(&h2), __float2half2_rn(0.5f));
+    const float2 ff = __half22float2(v);
+    f[2 * h] = ff.x;
+    f[2 * h + 1] = ff.y;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t b = (w >> (8 * i)) & 0xFFu;
+    f[i] = (b & 0x7Fu) == 0x7Fu ? ((b & 0x80u) ? -240.0f : 240.0f) : f[i];
+    f[i] = b == 0x80u ? __uint_as_float(0x7FFFFFFFu) : f[i];
+  }
+}
+
 // Cast a chunk SDT -> DDT.  ssc: dequant scale of an fp8 source; inv: RN(1/s) of an fp8
 // destination (an fp8 -> other-fp8 cast applies both, in that order).
 template <int SDT, int DDT, int VEC>
@@ -222,9 +263,15 @@ __device__ __forceinline__ void cast_chunk(const Chunk<SDT, VEC>& in, Chunk<DDT,
     for (int i = 0; i < Chunk<SDT, VEC>::WORDS; ++i) out.w[i] = in.w[i];
   } else {
     float f[VEC];
+    if constexpr (SDT == KV_F8E4M3FNUZ && VEC % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < VEC; i += 4) fnuzx4_to_f32(in.w[i >> 2], f + i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) f[i] = to_f32<SDT>(get_elem<SDT>(in.w, i));
+    }
 #pragma unroll
     for (int i = 0; i < VEC; ++i) {
-      f[i] = to_f32<SDT>(get_elem<SDT>(in.w, i));
       if constexpr (is_fp8(SDT)) f[i] = __fmul_rn(f[i], ssc);
       if constexpr (is_fp8(DDT)) f[i] = __fmul_rn(f[i], inv);
     }
@@ -240,6 +287,9 @@ __device__ __forceinline__ void cast_chunk(const Chunk<SDT, VEC>& in, Chunk<DDT,
     } else if constexpr (DDT == KV_F8E4M3FNUZ) {
       if constexpr (VEC == 1) {
         out.w[0] = f32x2_to_fnuzx2(f[0], 0.0f) & 0xFFu;
+      } else if constexpr (VEC % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < VEC; i += 4) out.w[i >> 2] = f32x4_to_fnuzx4(f + i);
       } else {
 #pragma unroll
         for (int i = 0; i < VEC; i += 2) out.w[i >> 2] |= f32x2_to_fnuzx2(f[i], f[i + 1]) << ((i & 3) * 8);
@@ -1466,16 +1516,18 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
     a.f_sb = make_fastdiv(nsb);
     a.f_items = make_fastdiv(nsb * nhb);
     a.n_items = (uint32_t)((uint64_t)a.total / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);
-    static const int wide1 = getenv("KVX_FP8_VEC16") ? atoi(getenv("KVX_FP8_VEC16")) : 0;
+    // 1-byte sources: 16-element chunks (whole 16-B loads, 4 in flight = 64 B per lane, like
+    // the 2-byte sources' 8-element chunks); KVX_FP8_VEC16=0 reverts to 8-element chunks
+    static const int wide1 = getenv("KVX_FP8_VEC16") ? atoi(getenv("KVX_FP8_VEC16")) : 1;
     if (a.split) {
       auto k = k_convert_rows<SDT, DDT, U, 8, true>;
       k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
     } else {
       bool done = false;
       if constexpr (Tr<SDT>::B == 1 && Tr<DDT>::B <= 2) {
-        if (wide1 && cpr >= 2) {  // 1-byte sources: 16-element chunks = whole 16-B loads (experiment)
+        if (wide1 && cpr >= 2) {
           a.cpr_shift = log2_pow2(cpr / 2);
-          auto k = k_convert_rows<SDT, DDT, 2, 16>;
+          auto k = k_convert_rows<SDT, DDT, 4, 16>;
           k<<<grid_for_items(k, a.n_items), kThreads, 0, s>>>(a);
           done = true;
         }

@@ -24,25 +24,27 @@ from synth import BLOCK, DIM, HEAD, KV, LAYER, SLOT  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--src", default="bf16", choices=["bf16", "fnuz"])
+    ap.add_argument("--src", default="bf16", choices=["bf16", "fnuz", "e4m3"])
+    ap.add_argument("--dst", default="e4m3", choices=["e4m3", "bf16", "fnuz"])
     ap.add_argument("--iters", type=int, default=10)
     args = ap.parse_args()
     import paper_2509_17542_b200 as kvx
     from bench import load_peaks
     L, H, D, tp, B = 80, 8, 128, 4, 16
     n_tokens = [4096] * 32
-    sdt = synth.BF16 if args.src == "bf16" else synth.FNUZ
+    names = {"bf16": synth.BF16, "fnuz": synth.FNUZ, "e4m3": synth.E4M3}
+    sdt, ddt = names[args.src], names[args.dst]
     NB = synth.pool_capacity(n_tokens, B)
     st = synth.block_tables(11, n_tokens, B, NB)
     dt_ = synth.block_tables(12, n_tokens, B, NB)
     dev = torch.device("cuda", 0)
-    ssc = torch.from_numpy(synth.pow2_scales(5, L, H // tp)).to(dev) if sdt == synth.FNUZ else None
-    dsc = torch.from_numpy(synth.pow2_scales(6, L, H // tp)).to(dev)
+    ssc = torch.from_numpy(synth.pow2_scales(5, L, H // tp)).to(dev) if sdt in synth.FP8 else None
+    dsc = torch.from_numpy(synth.pow2_scales(6, L, H // tp)).to(dev) if ddt in synth.FP8 else None
     vend = (LAYER, KV, BLOCK, HEAD, DIM, SLOT)   # per-layer tensors; the KV axis has extent 1
     Kl = kvx.Layout(L, H, D, tp, 0, B, NB, sdt, vend, ssc, kv_part=1, dim_split=16 // synth.NBYTES[sdt])
     Vl = kvx.Layout(L, H, D, tp, 0, B, NB, sdt, vend, ssc, kv_part=2)
     Cl = kvx.Layout(L, H, D, tp, 0, B, NB, sdt, synth.P_ORDER, ssc)
-    Dl = kvx.Layout(L, H, D, tp, 0, B, NB, synth.E4M3, synth.D_ORDER, dsc)
+    Dl = kvx.Layout(L, H, D, tp, 0, B, NB, ddt, synth.D_ORDER, dsc)
     pools = {}
     for name, lay in (("K", Kl), ("V", Vl), ("C", Cl)):
         t = lay.new_pool(dev)
@@ -65,7 +67,7 @@ def main():
         return statistics.median(a.elapsed_time(b) for a, b in ev)
 
     src_b = 2 * L * (H // tp) * D * sum(n_tokens) * synth.NBYTES[sdt]
-    dst_b = 2 * L * (H // tp) * D * sum(n_tokens) * 1
+    dst_b = 2 * L * (H // tp) * D * sum(n_tokens) * synth.NBYTES[ddt]
     pk = load_peaks()["hbm_gbs"]
     res = []
     for label, fn in [
@@ -78,7 +80,7 @@ def main():
     ]:
         ms = timed(fn)
         frac_b = (src_b + dst_b) / (2 if "only" in label else 1)
-        res.append({"case": label, "src": args.src, "ms": round(ms, 4), "hbm_GBs": round(frac_b / ms / 1e6, 1),
+        res.append({"case": label, "src": args.src, "dst": args.dst, "ms": round(ms, 4), "hbm_GBs": round(frac_b / ms / 1e6, 1),
                     "frac_measured": round(frac_b / ms / 1e6 / pk, 3), "kernel": kvx.last_kernel()})
         print(json.dumps(res[-1]), flush=True)
 
