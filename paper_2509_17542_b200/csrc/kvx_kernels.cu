@@ -770,10 +770,20 @@ __global__ void __launch_bounds__(32) k_tile_copy(const __grid_constant__ TileAr
 // zero.  The transpose costs shared-memory traffic only; HBM sees whole-tile reads and
 // writes.
 // ------------------------------------------------------------------------------------
-constexpr int kTrWarps = 4;
+#ifndef KVX_TR_WARPS
+#define KVX_TR_WARPS 4
+#endif
+constexpr int kTrWarps = KVX_TR_WARPS;
 
 template <int SDT, int DDT>
+#ifndef KVX_TR_MINB
+#define KVX_TR_MINB 8  // 8 CTAs x 4 warps: caps it at 64 registers (0.707 -> 0.732 on the vendor K+V case)
+#endif
+#if KVX_TR_MINB > 0
+__global__ void __launch_bounds__(kTrWarps * 32, KVX_TR_MINB) k_convert_tr(const __grid_constant__ ConvArgs a) {
+#else
 __global__ void __launch_bounds__(kTrWarps * 32) k_convert_tr(const __grid_constant__ ConvArgs a) {
+#endif
   extern __shared__ __align__(16) uint8_t tr_smem[];
   constexpr int VEC = 8;
   constexpr uint32_t SB = Tr<SDT>::B;
