@@ -182,7 +182,7 @@ def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent, dyn=False):
 
 
 @pytest.mark.parametrize("mode", ["push", "nccl", "pull", "pull_staged", "pull_staged_chunked", "pull_staged_dyn"])
-@pytest.mark.parametrize("shape", ["merge", "split_fp8"])
+@pytest.mark.parametrize("shape", ["merge", "split_fp8", "ragged_vendor"])
 def test_p_to_d_across_gpus(o1, mode, shape):
     if torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
@@ -192,8 +192,14 @@ def test_p_to_d_across_gpus(o1, mode, shape):
     from tests.test_gpu_parity import assert_pools_match
     if mode == "pull_staged_dyn" and shape == "merge":
         pytest.skip("dynamic scales need each P rank to hold all of its D ranks' heads (bf16 merge has no fp8)")
+    if shape == "ragged_vendor" and mode in ("pull_staged_dyn",):
+        pytest.skip("the vendor pools here carry no fp8 destination")
     if shape == "merge":   # c3-like: TP4 -> TP2, block 16 -> 64
         case = make_case(4, 8, 128, 4, 2, 16, 64, [300, 77, 1], BF16, BF16, seed=3, o1=o1)
+    elif shape == "ragged_vendor":  # an empty request, a 1-token one; an x-packed K-only source pool
+        from synth import LAYER, KV, BLOCK, SLOT, HEAD, DIM
+        case = make_case(3, 8, 64, 2, 2, 16, 32, [0, 45, 1, 0], BF16, BF16, (LAYER, KV, BLOCK, HEAD, DIM, SLOT),
+                         seed=5, o1=o1, p_kv_part=1, p_split=8)
     else:                  # c5-like split TP2 -> TP4 with a c4-like fp8 cast
         case = make_case(4, 8, 128, 2, 4, 16, 16, [129, 40], F16, E4M3, seed=4, o1=o1, scales="pow2")
     ctx = mp.get_context("spawn")
