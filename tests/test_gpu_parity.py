@@ -520,3 +520,19 @@ def test_other_vendor_prefill_to_nvidia_decode(o1):
     o1.convert(vc["src_lays"], vc["src_pools"], vc["dst_lays"], want, vc["n_tokens"], vc["src_tables"],
                vc["dst_tables"])
     assert_pools_match(dk_.dst_numpy(), want, E4M3)
+
+
+@pytest.mark.parametrize("dt,Bp,Bd,D", [(BF16, 16, 16, 128), (BF16, 32, 64, 64), (F16, 8, 16, 128), (E4M3, 16, 32, 64)])
+def test_head_dim_major_source_tiles(o1, dt, Bp, Bd, D):
+    """k_convert_tr with a head_dim-major ((DIM, SLOT) innermost) source: the 2-byte path's
+    8x8 register transpose and the per-element path (fp8), ragged requests, TP 2 -> 1."""
+    import paper_2509_17542_b200 as kvx
+    vorder = (LAYER, KV, BLOCK, HEAD, DIM, SLOT)
+    ddt = BF16 if dt == E4M3 else E4M3
+    case = make_case(2, 4, D, 2, 1, Bp, Bd, [70, 1, 33, 0], dt, ddt, vorder, synth.D_ORDER, seed=Bp + D, o1=o1,
+                     scales="pow2")
+    if dt in FP8:
+        for i, lay in enumerate(case["src_lays"]):
+            lay["scales"] = synth.pow2_scales(800 + i, 2, 2, -2, 2)
+    run_case(o1, case)
+    assert kvx.last_kernel() == "k_convert_tr"
