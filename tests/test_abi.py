@@ -242,3 +242,47 @@ def test_layout_variants_describe_wire_and_header(kvx, o1):
         replay.check_header(hdr, both, konly, [5, 7])
     with pytest.raises(kvx.KvError, match="share neither"):
         replay.header(konly, vonly, [1])
+
+
+def test_pull_and_stage_validation_fails_before_enqueue(kvx):
+    """kv_pull / kv_stage / kv_pull_staged reject bad arguments synchronously (no GPU needed:
+    nothing is enqueued on these paths)."""
+    from paper_2509_17542_b200._lib import Batch_t, lib
+
+    def bt(lay, tokens=5):
+        b = Batch_t()
+        b.n_req, b.block_size, b.num_blocks = 1, lay.block_size, lay.num_blocks
+        b.total_tokens, b.total_blocks, b.token_digest = tokens, 2, 7
+        b.tok_off = b.blk_off = b.blk_ids = b.blk_req = b.tok_req = 0x10000
+        return b
+
+    def arr(*xs):
+        return (C.c_void_p * len(xs))(*xs)
+
+    s = _lay(kvx, tp_degree=1, tp_rank=0)
+    d = _lay(kvx, tp_degree=1, tp_rank=0)
+    sb, db = bt(s), bt(d)
+    err = 0x40000
+    # kv_pull: a null ready flag
+    st = lib.kv_pull(1, arr(s.handle.value), arr(0x20000), C.byref(sb), d.handle, 0x30000, C.byref(db),
+                     arr(0), arr(0x50000), 1, 0, 2, 0, 10**9, err, None)
+    assert st == 1 and "null flag" in lib.kv_last_error().decode()
+    # kv_pull: K-only source, V-only destination -> nothing in common
+    ks = kvx.Layout(2, 8, 16, 1, 0, 4, 10, kvx.KV_BF16, (0, 1, 2, 3, 4, 5), kv_part=1)
+    vd = kvx.Layout(2, 8, 16, 1, 0, 4, 10, kvx.KV_BF16, (0, 1, 2, 3, 4, 5), kv_part=2)
+    st = lib.kv_pull(1, arr(ks.handle.value), arr(0x20000), C.byref(bt(ks)), vd.handle, 0x30000, C.byref(bt(vd)),
+                     arr(0x60000), arr(0x50000), 1, 0, 2, 0, 10**9, err, None)
+    assert st == 2 and "share neither" in lib.kv_last_error().decode()
+    # kv_stage: ring slots smaller than one layer chunk's wire
+    need = kvx.wire_bytes(s, d, 5, (0, 1))
+    st = lib.kv_stage(s.handle, 0x20000, C.byref(sb), 1, arr(d.handle.value), arr(0x70000, 0x80000), 2, need - 1,
+                      arr(0x60000), arr(0x50000), None, 0, 0, 2, 1, 10**9, err, None)
+    assert st == 2 and "ring slots smaller" in lib.kv_last_error().decode()
+    # kv_stage: dynamic scales need an fp8 destination
+    st = lib.kv_stage(s.handle, 0x20000, C.byref(sb), 1, arr(d.handle.value), arr(0x70000, 0x80000), 2, need,
+                      arr(0x60000), arr(0x50000), arr(0x90000), 0, 0, 2, 1, 10**9, err, None)
+    assert st == 1 and "dynamic scales" in lib.kv_last_error().decode()
+    # kv_pull_staged: no ring slots
+    st = lib.kv_pull_staged(1, arr(s.handle.value), arr(0x70000), 0, need, d.handle, 0x30000, C.byref(db),
+                            arr(0x60000), arr(0x50000), None, 0, 0, 2, 1, 10**9, err, None)
+    assert st == 1 and "bad argument" in lib.kv_last_error().decode()
