@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--requests", type=int, default=0,
                     help="use only the first N requests of the workload (e.g. 1: batch-1 latency of c3/c4)")
     ap.add_argument("--workload", default=None, help="override: c1..c5")
+    ap.add_argument("--tokens", type=int, default=0, help="one request of this many tokens (paper points)")
+    ap.add_argument("--tp-p", type=int, default=0, help="override the P TP degree")
+    ap.add_argument("--tp-d", type=int, default=0, help="override the D TP degree")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
@@ -332,7 +335,7 @@ def run_single(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype_name(cfg),
         "data": "synthetic (seeded random finite bit patterns, Fisher-Yates block tables)",
         "config": {"workload": f"{wl_name} one GPU: {cfg.note}; all P and D ranks' pools on cuda:0",
-                   "requests": len(cfg.n_tokens), "tokens": cfg.total_tokens,
+                   "requests": len(cfg.n_tokens), "tokens": cfg.total_tokens, "overrides": _overrides(args),
                    "layout": "P (L,KV,BLK,SLOT,H,D) -> D (BLK,L,KV,H,SLOT,D)",
                    "src_bytes_per_step": src_b, "dst_bytes_per_step": dst_b,
                    "l2": "inputs larger than L2 (no flush)", "parallelism": "none (1 GPU)"},
@@ -422,11 +425,25 @@ def _pinned_copy(dev_tensor):
 
 
 def _subset(cfg, args):
-    """--requests N: the first N requests of the configuration (batch-1 latency runs)."""
+    """--requests N: the first N requests of the configuration (batch-1 latency runs);
+    --tokens T: one request of T tokens (the paper's input lengths: 256 / 512 /
+    1024); --tp-p / --tp-d: other TP degrees on the same model (context points)."""
+    import dataclasses
     if getattr(args, "requests", 0):
-        import dataclasses
-        return dataclasses.replace(cfg, n_tokens=cfg.n_tokens[:args.requests])
+        cfg = dataclasses.replace(cfg, n_tokens=cfg.n_tokens[:args.requests])
+    if getattr(args, "tokens", 0):
+        cfg = dataclasses.replace(cfg, n_tokens=[args.tokens])
+    if getattr(args, "tp_p", 0):
+        cfg = dataclasses.replace(cfg, tp_p=args.tp_p)
+    if getattr(args, "tp_d", 0):
+        cfg = dataclasses.replace(cfg, tp_d=args.tp_d)
     return cfg
+
+
+def _overrides(args):
+    """The workload overrides of this run (empty for the BASELINE configurations as named)."""
+    o = {k: getattr(args, k) for k in ("requests", "tokens", "tp_p", "tp_d") if getattr(args, k, 0)}
+    return o or None
 
 
 def _dtype_name(cfg):
@@ -687,7 +704,7 @@ def run_multi(args):
                                    + (f", {world - n_p - n_d} idle GPU(s)" if world > n_p + n_d else ""),
                        "mode": args.mode + (" + dynamic fp8 scales (P amax per chunk, shipped)" if dyn else ""),
                        "layer_chunk": lc, "requests": len(cfg.n_tokens),
-                       "tokens": cfg.total_tokens, "src_bytes_per_step": src_b,
+                       "tokens": cfg.total_tokens, "overrides": _overrides(args), "src_bytes_per_step": src_b,
                        "busiest_link_bytes_per_step": nvl_b, "pairs": [list(x[:2]) for x in pairs],
                        "l2": "inputs larger than L2 (no flush)",
                        "parallelism": f"P TP{cfg.tp_p} x D TP{cfg.tp_d}, {n_p}+{n_d} ranks present"},
