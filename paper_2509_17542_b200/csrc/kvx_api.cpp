@@ -372,11 +372,17 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
     return KV_OK;
   const int32_t Hp = S->h_local, Hd = D->h_local, Bp = S->d.block_size, Bd = D->d.block_size, Dm = S->d.head_dim;
   const int32_t esize = S->elem_bytes;
-  const int32_t nh = std::min(Hp, Hd);
+  int32_t nh = std::min(Hp, Hd);
   if (Bd % Bp != 0 || Bp > 256 || Dm > 256 || nh > 256 || (Hp % nh) || (Hd % nh)) return KV_OK;
   const int64_t row_bytes = (int64_t)Dm * esize;
   if (row_bytes % 16) return KV_OK;
-  const int64_t stage = (int64_t)nh * Bp * row_bytes;
+  int64_t stage = (int64_t)nh * Bp * row_bytes;
+  // a sub-tile bigger than 64 KB (e.g. TP1 -> TP1 of 32 heads: 128 KB) leaves no room for a
+  // second stage: split it by heads into head groups of <= 64 KB
+  while (stage > 64 * 1024 && nh % 2 == 0) {
+    nh /= 2;
+    stage /= 2;
+  }
   if (stage > 100 * 1024 || (mode == 1 && stage < 32 * 1024)) return KV_OK;
   encode_tiled_fn enc = encode_fn();
   if (!enc) return KV_OK;
@@ -431,7 +437,13 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
   a.d_blk_ids = dst_bt->blk_ids;
   a.d_blk_req = dst_bt->blk_req;
   a.tok_off = dst_bt->tok_off;
-  const uint32_t nparts = share ? 1u : (uint32_t)(Hd / nh), nsub = (uint32_t)(Bd / Bp);
+  // head groups per item set: the D rank's Hd heads, or (share) the heads P rank p holds of it
+  int32_t ov = Hd;
+  if (share) {
+    const int32_t p = S->d.tp_rank, q = D->d.tp_rank;
+    ov = std::min((p + 1) * Hp, (q + 1) * Hd) - std::max(p * Hp, q * Hd);
+  }
+  const uint32_t nparts = (uint32_t)(ov / nh), nsub = (uint32_t)(Bd / Bp);
   a.f_nd = make_fastdiv((uint32_t)n_dst);
   a.f_parts = make_fastdiv(nparts);
   a.f_sub = make_fastdiv(nsub);

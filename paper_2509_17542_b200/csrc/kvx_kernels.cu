@@ -680,8 +680,12 @@ __global__ void __launch_bounds__(32) k_tile_copy(const __grid_constant__ TileAr
     const int64_t dblk = __ldg(a.d_blk_ids + bl);
     const int32_t layer = a.lb + (int32_t)l;
     const int32_t q = a.dst_rank[qi];
-    const int32_t p = a.share_p >= 0 ? a.share_p : (q * a.Hd) / a.Hp + (int32_t)part;
-    const int32_t hp0 = max(q * a.Hd - p * a.Hp, 0), hq0 = max(p * a.Hp - q * a.Hd, 0);
+    // head group `part` of nh heads: from the D rank's first head, or (share) from the first
+    // head this P rank holds of it; its P rank and local head offsets on both sides
+    const int32_t hstart = a.share_p >= 0 ? max(a.share_p * a.Hp, q * a.Hd) : q * a.Hd;
+    const int32_t h0 = hstart + (int32_t)part * a.nh;
+    const int32_t p = a.share_p >= 0 ? a.share_p : h0 / a.Hp;
+    const int32_t hp0 = h0 - p * a.Hp, hq0 = h0 - q * a.Hd;
     si = a.src_of_p[p];
     const int32_t t0 = j * a.Bd + (int32_t)sub * a.Bp;
     it.valid = t0 >= T ? 0u : (uint32_t)min(a.Bp, T - t0);

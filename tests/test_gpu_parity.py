@@ -536,3 +536,20 @@ def test_head_dim_major_source_tiles(o1, dt, Bp, Bd, D):
             lay["scales"] = synth.pow2_scales(800 + i, 2, 2, -2, 2)
     run_case(o1, case)
     assert kvx.last_kernel() == "k_convert_tr"
+
+
+@pytest.mark.parametrize("tp_p,tp_d", [(1, 1), (1, 2), (2, 1)])
+def test_tile_copy_head_groups(o1, tp_p, tp_d):
+    """k_tile_copy with sub-tiles over 64 KB (32 heads x 16 slots x 256 B): split into
+    head groups, each with its own P rank and local head offsets (and the share path)."""
+    import paper_2509_17542_b200 as kvx
+    from tests.gpu_util import DevCase
+    case = make_case(2, 64, 128, tp_p, tp_d, 16, 16, [40, 3, 16], BF16, BF16, seed=30 + tp_p * 3 + tp_d, o1=o1)
+    run_case(o1, case)
+    assert kvx.last_kernel() == "k_tile_copy"
+    if tp_p > tp_d:   # per P rank share (the distributed-push primitive) over head groups
+        dc = DevCase(case)
+        for p in range(tp_p):
+            kvx.convert_share(dc.src_lays[p], dc.src_pools[p], dc.src_bt, dc.dst_lays, dc.dst_pools, dc.dst_bt)
+        torch.cuda.synchronize()
+        assert_pools_match(dc.dst_numpy(), expected(case, o1), BF16)
