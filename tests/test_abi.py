@@ -13,8 +13,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 @pytest.fixture(scope="module")
 def kvx():
-    from paper_2509_17542_b200 import build as b
-    b.build()
+    import __graft_entry__ as g   # builds libkvx.so by path (the package needs it to import)
+    g.build()
     import paper_2509_17542_b200 as k
     return k
 
