@@ -13,6 +13,14 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "multigpu: needs >= 2 CUDA devices")
 
 
+def pytest_sessionstart(session):
+    """Build libkvx.so (sm_100a, in-tree) if it is missing or stale before any test module
+    imports the binding -- a fresh checkout carries no built library (nvcc cross-compiles
+    without a GPU; a no-op when the library is up to date)."""
+    import __graft_entry__ as g
+    g._lib_builder().build()
+
+
 @pytest.fixture(scope="session")
 def o1():
     from oracle import o1 as _o1
