@@ -1101,6 +1101,9 @@ def run_stream(args):
 
 def main():
     args = parse()
+    if args.impl != "reference":   # a fresh checkout has no libkvx.so yet (no-op when up to date)
+        import __graft_entry__
+        __graft_entry__._lib_builder().build()
     if args.impl == "reference":
         return run_reference(args)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:

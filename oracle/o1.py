@@ -27,9 +27,17 @@ _lib = None
 
 def build(force: bool = False) -> str:
     """Compile kv_oracle.c with gcc (plain C11, no FMA contraction, no fast-math)."""
-    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
-                               "-Wall", "-shared", "-fPIC", "-o", LIB, SRC, "-lm"])
+    def stale():
+        return force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC)
+
+    if stale():
+        import fcntl
+        with open(LIB + ".lock", "w") as lk:  # concurrent ranks / workers: one compiles
+            fcntl.flock(lk, fcntl.LOCK_EX)
+            if stale():
+                subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
+                                       "-Wall", "-shared", "-fPIC", "-o", LIB + ".tmp", SRC, "-lm"])
+                os.replace(LIB + ".tmp", LIB)
     return LIB
 
 

@@ -39,6 +39,17 @@ def needs_build():
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
+    # several processes (torchrun ranks, pytest workers) may ask at once: one builds, the
+    # others wait on the lock and then find the library up to date
+    import fcntl
+    with open(os.path.join(CSRC, ".build.lock"), "w") as lk:
+        fcntl.flock(lk, fcntl.LOCK_EX)
+        if not force and not needs_build():
+            return LIB
+        return _build_locked(verbose)
+
+
+def _build_locked(verbose: bool) -> str:
     nccl_inc, nccl_lib = _nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
