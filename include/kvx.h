@@ -27,8 +27,9 @@
  *   - No exception crosses the ABI.  Calls on distinct streams and handles are
  *     thread-safe.
  *   - Device pointers may be local or peer-mapped (kv_ipc_open, or peer access):
- *     a destination pool on another GPU turns kv_convert_reshard into the fused
- *     gather + convert + NVLink push (P-side push, D-controlled placement).
+ *     source pools on another GPU turn kv_convert_reshard (run on D's GPU) into the
+ *     D-initiated NVLink read of P:109 (kv_pull, kv_pull_staged); a destination pool
+ *     on another GPU turns it into a P-side push (kv_push).
  */
 #ifndef KVX_H_
 #define KVX_H_

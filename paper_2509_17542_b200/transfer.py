@@ -1,7 +1,7 @@
 """P -> D transfer across GPUs of one box (A8, A10, A11): roles, pair plan, control-plane
-exchange and the two data-plane modes.
+exchange and the data-plane modes (bench.py default: pull).
 
-* ``push`` (default, the fused kernel K4): each D rank exports its pool and a completion
+* ``push`` (the fused kernel K4): each D rank exports its pool and a completion
   flag through CUDA IPC; each P rank maps them and runs ``convert_reshard`` with the
   *peer-mapped* D pool as destination -- one kernel gathers from local HBM, converts and
   stores straight into the D rank's HBM across NVLink -- then ``signal``s the flag with a
