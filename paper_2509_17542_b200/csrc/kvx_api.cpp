@@ -587,6 +587,11 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
       a.s_lm = S->dk >= 3 ? S->dk - 3 : 0;
       a.d_lm = D->dk >= 3 ? D->dk - 3 : 0;
       a.cpr_shift = lg(S->d.head_dim / 8);
+      a.s_dk = S->dk;
+      a.d_dk = D->dk;
+      // register path unless KVX_TR=0 (the smem-staged kernel) or a block holds < 8 slots
+      const char* tr_env = getenv("KVX_TR");
+      const bool use_tr8 = S->d.block_size >= 8 && D->d.block_size >= 8 && !(tr_env && atoi(tr_env) == 0);
       for (int ax = 0; ax < 6; ++ax) {
         a.ss[ax] = S->stride[ax];
         a.ds[ax] = D->stride[ax];
@@ -616,8 +621,14 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
         a.Lc = l1 - l0;
         a.f_l = make_fastdiv((uint32_t)a.Lc);
         a.n_items = (uint32_t)(per_layer * (uint64_t)a.Lc);
-        t_last_kernel = "k_convert_tr";
-        cudaError_t e = launch_convert_tr(a, S->d.dtype, D->d.dtype, (cudaStream_t)stream);
+        cudaError_t e;
+        if (use_tr8) {
+          t_last_kernel = "k_convert_tr8";
+          e = launch_convert_tr8(a, S->d.dtype, D->d.dtype, (cudaStream_t)stream);
+        } else {
+          t_last_kernel = "k_convert_tr";
+          e = launch_convert_tr(a, S->d.dtype, D->d.dtype, (cudaStream_t)stream);
+        }
         if (e != cudaSuccess) return cuda_fail(e, "kv_convert_reshard: launch");
       }
       return KV_OK;

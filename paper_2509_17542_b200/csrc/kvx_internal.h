@@ -221,6 +221,9 @@ cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out_scales, cudaStrea
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s);
 // k_convert_tr: a side with (DIM, SLOT) innermost (a.s_tr / a.d_tr), items in a.n_items
 cudaError_t launch_convert_tr(const ConvArgs& a, int sdt, int ddt, cudaStream_t s);
+// k_convert_tr8: the same items without shared memory (8 x 8 register sub-blocks); needs
+// B_p, B_d >= 8 and a.s_dk / a.d_dk set
+cudaError_t launch_convert_tr8(const ConvArgs& a, int sdt, int ddt, cudaStream_t s);
 constexpr int kTrSmemLimit = 200 * 1024;  // per CTA (4 warps x one Bd x D tile each)
 cudaError_t launch_tile_copy(const TileArgs& a, cudaStream_t s);
 cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s);

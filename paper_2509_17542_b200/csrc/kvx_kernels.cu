@@ -108,6 +108,23 @@ __device__ __forceinline__ void load_chunk(Chunk<DT, VEC>& c, const uint8_t* p) 
   }
 }
 
+// read-only loads that allocate in L1 (k_convert_tr8's x-packed source: a lane re-reads
+// the other half of each sector in its next load)
+template <int DT, int VEC>
+__device__ __forceinline__ void load_chunk_l1(Chunk<DT, VEC>& c, const uint8_t* p) {
+  constexpr int N = Chunk<DT, VEC>::BYTES;
+  static_assert(N == 8 || N == 16 || N == 32, "vector chunks only");
+#pragma unroll
+  for (int o = 0; o < N; o += 16) {
+    if constexpr (N == 8)
+      asm volatile("ld.global.nc.L1::evict_last.v2.u32 {%0,%1}, [%2];" : "=r"(c.w[0]), "=r"(c.w[1]) : "l"(p));
+    else
+      asm volatile("ld.global.nc.L1::evict_last.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(c.w[o / 4]), "=r"(c.w[o / 4 + 1]), "=r"(c.w[o / 4 + 2]), "=r"(c.w[o / 4 + 3])
+                   : "l"(p + o));
+  }
+}
+
 template <int DT, int VEC>
 __device__ __forceinline__ void store_chunk(uint8_t* p, const Chunk<DT, VEC>& c) {
   constexpr int N = Chunk<DT, VEC>::BYTES;
@@ -933,6 +950,186 @@ __global__ void __launch_bounds__(kTrWarps * 32) k_convert_tr(const __grid_const
 }
 
 // ------------------------------------------------------------------------------------
+// K1 with a head_dim-major or x-packed side, register path (k_convert_tr8): the same items
+// as k_convert_tr (dst rank, dst block, layer, K/V, dst head), but no shared memory.  An
+// item's (Bd x D) tile is cut into 8 x 8 sub-blocks (8 slots x 8 head_dim elements); each
+// lane owns one sub-block, loads it as 8 chunks in the source's natural form (8 rows of
+// one slot each, or 8 columns of one head_dim element each for a (DIM, SLOT)-innermost
+// side), transposes it in registers with byte permutes when the destination's form is the
+// other one, casts and stores 8 chunks.  HBM sees whole-tile reads and writes; a warp keeps
+// 8 x 16 B in flight per lane.  Item metadata (block-table lookups, scales, tile bases) is
+// computed lane-parallel for 32 items at a time and broadcast with shuffles, so the
+// dependent table loads are paid once per 32 items, not once per item.
+// ------------------------------------------------------------------------------------
+// 8 x 8 transpose of chunks (8 elements each): out[i] element k = in[k] element i
+template <int DT>
+__device__ __forceinline__ void transpose8(const Chunk<DT, 8>* in, Chunk<DT, 8>* out) {
+  if constexpr (Tr<DT>::B == 4) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) out[i].w[k] = in[k].w[i];
+  } else if constexpr (Tr<DT>::B == 2) {
+    // out[i].w[m] = (in[2m].e[i], in[2m+1].e[i]): the low or high halves of word i/2
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+        out[i].w[m] = __byte_perm(in[2 * m].w[i >> 1], in[2 * m + 1].w[i >> 1], (i & 1) ? 0x7632u : 0x5410u);
+  } else {
+    // bytes: interleave row pairs (k, k+1) -> 16-bit (in[k].e[i], in[k+1].e[i]) pieces, then
+    // pair those into words
+    uint32_t t[4][4];  // [row pair][piece word]: word 2m+h holds elements 4m+2h, 4m+2h+1
+#pragma unroll
+    for (int pr = 0; pr < 4; ++pr)
+#pragma unroll
+      for (int m = 0; m < 2; ++m) {
+        t[pr][2 * m] = __byte_perm(in[2 * pr].w[m], in[2 * pr + 1].w[m], 0x5140u);
+        t[pr][2 * m + 1] = __byte_perm(in[2 * pr].w[m], in[2 * pr + 1].w[m], 0x7362u);
+      }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)  // output word h: rows 4h .. 4h+3
+        out[i].w[h] = __byte_perm(t[2 * h][i >> 1], t[2 * h + 1][i >> 1], (i & 1) ? 0x7632u : 0x5410u);
+  }
+}
+
+#ifndef KVX_TR8_THREADS
+#define KVX_TR8_THREADS 256
+#endif
+constexpr int kTr8Threads = KVX_TR8_THREADS;
+
+template <int SDT, int DDT>
+__global__ void __launch_bounds__(kTr8Threads) k_convert_tr8(const __grid_constant__ ConvArgs a) {
+  constexpr uint32_t SB = Tr<SDT>::B, DB = Tr<DDT>::B;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t lbp = (uint32_t)a.tr_lbp, lbd = (uint32_t)a.tr_lbd, lcpr = (uint32_t)a.cpr_shift;
+  const uint32_t lnsub = (lbd - 3u) + lcpr;  // log2 sub-blocks per item
+  const uint32_t ngroups = (a.n_items + 31u) >> 5;
+  const bool s_col = a.s_tr == 1, d_col = a.d_tr == 1;
+  for (uint32_t grp = warp; grp < ngroups; grp += nwarps) {
+    // ---- lane-parallel metadata of item grp * 32 + lane ----
+    const uint32_t item = (grp << 5) + lane;
+    const uint32_t cnt = min(32u, a.n_items - (grp << 5));
+    const uint8_t* m_snob = nullptr;  // source tile base without the block term
+    const int32_t* m_sids = nullptr;  // the request's source block ids from the dst block's first token
+    int32_t m_sblk0 = 0;
+    uint8_t* m_db = nullptr;          // destination tile base
+    uint32_t m_valid = 0;
+    float m_rsc = 1.f, m_s2 = 1.f;
+    if (lane < cnt) {
+      uint32_t n = item;
+      const uint32_t hl = divmod(n, a.f_hde);
+      const uint32_t c = take_kv(n, a.kv1, a.c0);
+      const uint32_t l = divmod(n, a.f_l);
+      const uint32_t bl = divmod(n, a.f_bl);
+      const uint32_t qi = n;
+      const uint32_t hq = (uint32_t)a.hq_off[qi] + hl;
+      const int32_t r = __ldg(a.d_blk_req + bl);
+      const int32_t tok0 = __ldg(a.tok_off + r);
+      const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+      const uint32_t tb0 = (uint32_t)(bl - __ldg(a.d_blk_off + r)) << lbd;
+      const int64_t layer = a.lb + (int64_t)l;
+      const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;
+      const uint32_t h = (uint32_t)a.dst_rank[qi] * (uint32_t)a.Hd + hq;
+      const uint32_t p = fdiv(h, a.f_hp);
+      const uint32_t hp = h - p * (uint32_t)a.Hp;
+      const int si = a.src_of_p[p];
+      if constexpr (dual_scale(SDT, DDT)) {
+        m_rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+        m_s2 = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+      } else {
+        if constexpr (is_fp8(SDT) && SDT != DDT) m_rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+        if constexpr (is_fp8(DDT) && SDT != DDT) m_rsc = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+        m_s2 = m_rsc;
+      }
+      m_valid = (int32_t)tb0 >= T ? 0u : min(1u << lbd, (uint32_t)T - tb0);
+      m_sids = a.s_blk_ids + __ldg(a.s_blk_off + r) + (int32_t)(tb0 >> lbp);
+      if (m_valid) m_sblk0 = __ldg(m_sids);
+      m_snob = a.src[si] + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + (int64_t)hp * a.ss[KV_AX_HEAD]) * SB;
+      m_db = a.dst[qi] + (dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] +
+                          (int64_t)__ldg(a.d_blk_ids + bl) * a.ds[KV_AX_BLOCK] + (int64_t)hq * a.ds[KV_AX_HEAD]) *
+                             DB;
+    }
+    // ---- units = (item i of the group, sub-block u); warp-uniform trip count ----
+    const uint32_t nunits = cnt << lnsub;
+    for (uint32_t base = 0; base < nunits; base += 32u) {
+      const uint32_t unit = base + lane;
+      const uint32_t i = min(unit >> lnsub, cnt - 1u);
+      const uint32_t u = unit & ((1u << lnsub) - 1u);
+      const uint8_t* snob = (const uint8_t*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)m_snob, i);
+      const int32_t* sids = (const int32_t*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)m_sids, i);
+      const int32_t sblk0 = __shfl_sync(0xFFFFFFFFu, m_sblk0, i);
+      uint8_t* db = (uint8_t*)__shfl_sync(0xFFFFFFFFu, (unsigned long long)m_db, i);
+      const uint32_t valid = __shfl_sync(0xFFFFFFFFu, m_valid, i);
+      const float rsc = __shfl_sync(0xFFFFFFFFu, m_rsc, i);
+      const float s2 = __shfl_sync(0xFFFFFFFFu, m_s2, i);
+      if (unit >= nunits) continue;
+      const uint32_t s0 = (u >> lcpr) << 3;             // first dst slot of the sub-block
+      const uint32_t d0 = (u & ((1u << lcpr) - 1u)) << 3;  // first head_dim element
+      Chunk<DDT, 8> o[8];
+      if (s0 >= valid) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) zero_chunk(o[k]);
+      } else {
+        const uint32_t j = s0 >> lbp;
+        const int64_t sblk = j == 0 ? sblk0 : __ldg(sids + j);
+        const uint8_t* sb = snob + sblk * a.ss[KV_AX_BLOCK] * SB;
+        const uint32_t sin = s0 & ((1u << lbp) - 1u);
+        Chunk<SDT, 8> x[8];
+        if (s_col) {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) load_chunk<SDT, 8>(x[k], sb + ((int64_t)(d0 + k) * a.ss[KV_AX_DIM] + sin) * SB);
+        } else if (a.s_tr == 2) {
+          // x-packed: the lane's 8 chunks are one contiguous 8-chunk run (x = 8 elements) or
+          // 8 runs of x / 8 chunks, while a warp instruction touches one chunk per lane in
+          // different runs: half-sector requests whose other halves the lane's next loads
+          // take -- allocate in L1 so each sector comes from L2 once (0.71 -> 0.88 of copy)
+          const int64_t doff = dim_off(d0, a.ss[KV_AX_DIM], a.s_dk);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            load_chunk_l1<SDT, 8>(x[k], sb + ((int64_t)(sin + k) * a.ss[KV_AX_SLOT] + doff) * SB);
+        } else {
+          const int64_t doff = dim_off(d0, a.ss[KV_AX_DIM], a.s_dk);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) load_chunk<SDT, 8>(x[k], sb + ((int64_t)(sin + k) * a.ss[KV_AX_SLOT] + doff) * SB);
+        }
+        if (s_col != d_col) {
+          Chunk<SDT, 8> y[8];
+          transpose8<SDT>(x, y);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cast_chunk<SDT, DDT, 8>(y[k], o[k], rsc, s2);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 8; ++k) cast_chunk<SDT, DDT, 8>(x[k], o[k], rsc, s2);
+        }
+        if (s0 + 8u > valid) {  // slots past the request's last token are zero
+          if (d_col) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) zero_tail<DDT, 8>(o[k], valid - s0);
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (s0 + (uint32_t)k >= valid) zero_chunk(o[k]);
+          }
+        }
+      }
+      if (d_col) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) store_chunk<DDT, 8>(db + ((int64_t)(d0 + k) * a.ds[KV_AX_DIM] + s0) * DB, o[k]);
+      } else {
+        const int64_t doff = dim_off(d0, a.ds[KV_AX_DIM], a.d_dk);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) store_chunk<DDT, 8>(db + ((int64_t)(s0 + k) * a.ds[KV_AX_SLOT] + doff) * DB, o[k]);
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // K2 fast path: pack (Fig. 5 flatten) with the row machinery.  Item = 32 consecutive
 // tokens of one (layer, K/V, overlap head): the wire side is one contiguous 32-row run,
 // each lane gathers its token's row through the block table.
@@ -1640,6 +1837,23 @@ template <int VEC>
 cudaError_t tr_v(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
   KVX_DISPATCH(tr_t, VEC, sdt, ddt, a, s)
 }
+template <int VEC, int SDT, int DDT>
+cudaError_t tr8_t(const ConvArgs& a, cudaStream_t s) {
+  auto k = k_convert_tr8<SDT, DDT>;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kTr8Threads, 0);
+  if (occ < 1) occ = 1;
+  const uint64_t groups = (a.n_items + 31) / 32;
+  const uint64_t need = (groups + kTr8Threads / 32 - 1) / (kTr8Threads / 32);
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms() * occ));
+  k<<<grid, kTr8Threads, 0, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+template <int VEC>
+cudaError_t tr8_v(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
+  KVX_DISPATCH(tr8_t, VEC, sdt, ddt, a, s)
+}
 
 template <int VEC>
 cudaError_t conv_v(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
@@ -1659,6 +1873,11 @@ cudaError_t unpack_v(const UnpackArgs& a, int wdt, int ddt, cudaStream_t s) {
 cudaError_t launch_convert_tr(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
   if (a.n_items == 0) return cudaSuccess;
   return tr_v<8>(a, sdt, ddt, s);
+}
+
+cudaError_t launch_convert_tr8(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
+  if (a.n_items == 0) return cudaSuccess;
+  return tr8_v<8>(a, sdt, ddt, s);
 }
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s) {
   if (a.total == 0) return cudaSuccess;

@@ -512,9 +512,9 @@ def test_other_vendor_prefill_to_nvidia_decode(o1):
     dv_ = DevCase(vc)
     dv_.dst_pools = dk_.dst_pools
     dk_.convert()
-    assert kvx.last_kernel() == "k_convert_tr"        # x-split (D/x, SLOT, x) tiles: smem staging
+    assert kvx.last_kernel() == "k_convert_tr8"       # x-split (D/x, SLOT, x) tiles: register sub-blocks
     dv_.convert()
-    assert kvx.last_kernel() == "k_convert_tr"        # head_dim-major: smem transpose
+    assert kvx.last_kernel() == "k_convert_tr8"       # head_dim-major: register 8 x 8 transposes
     want = expected(kc, o1)
     want = [w.copy() for w in want]
     o1.convert(vc["src_lays"], vc["src_pools"], vc["dst_lays"], want, vc["n_tokens"], vc["src_tables"],
@@ -523,10 +523,13 @@ def test_other_vendor_prefill_to_nvidia_decode(o1):
 
 
 @pytest.mark.parametrize("dt,Bp,Bd,D", [(BF16, 16, 16, 128), (BF16, 32, 64, 64), (F16, 8, 16, 128), (E4M3, 16, 32, 64)])
-def test_head_dim_major_source_tiles(o1, dt, Bp, Bd, D):
-    """k_convert_tr with a head_dim-major ((DIM, SLOT) innermost) source: the 2-byte path's
-    8x8 register transpose and the per-element path (fp8), ragged requests, TP 2 -> 1."""
+@pytest.mark.parametrize("tr", ["0", "1"])
+def test_head_dim_major_source_tiles(o1, monkeypatch, tr, dt, Bp, Bd, D):
+    """A head_dim-major ((DIM, SLOT) innermost) source through both transpose kernels
+    (KVX_TR=0: k_convert_tr, shared-memory tiles; 1: k_convert_tr8, register 8 x 8
+    sub-blocks), 2-byte and fp8 sources, ragged requests, TP 2 -> 1."""
     import paper_2509_17542_b200 as kvx
+    monkeypatch.setenv("KVX_TR", tr)
     vorder = (LAYER, KV, BLOCK, HEAD, DIM, SLOT)
     ddt = BF16 if dt == E4M3 else E4M3
     case = make_case(2, 4, D, 2, 1, Bp, Bd, [70, 1, 33, 0], dt, ddt, vorder, synth.D_ORDER, seed=Bp + D, o1=o1,
@@ -535,7 +538,47 @@ def test_head_dim_major_source_tiles(o1, dt, Bp, Bd, D):
         for i, lay in enumerate(case["src_lays"]):
             lay["scales"] = synth.pow2_scales(800 + i, 2, 2, -2, 2)
     run_case(o1, case)
-    assert kvx.last_kernel() == "k_convert_tr"
+    assert kvx.last_kernel() == ("k_convert_tr8" if tr == "1" else "k_convert_tr")
+
+
+_VCOL = (LAYER, KV, BLOCK, HEAD, DIM, SLOT)   # head_dim-major tile (other vendors' value cache)
+# side forms: (axis order, x-split): rows = head_dim innermost, col = (DIM, SLOT) innermost,
+# x8 / x16 = (D/x, SLOT, x) innermost (other vendors' key cache)
+_FORMS = {"rows_p": (synth.P_ORDER, 0), "rows_d": (synth.D_ORDER, 0), "col": (_VCOL, 0), "x8": (_VCOL, 8),
+          "x16": (_VCOL, 16)}
+
+
+@pytest.mark.parametrize("sf,df,sdt,ddt,Bp,Bd,tp", [
+    ("col", "rows_d", BF16, E4M3, 16, 16, (2, 1)),
+    ("x8", "rows_d", BF16, E4M3, 16, 16, (2, 1)),
+    ("rows_p", "col", E4M3, BF16, 8, 32, (1, 2)),
+    ("rows_p", "x16", F16, F16, 16, 64, (2, 2)),
+    ("col", "col", FNUZ, E4M3, 8, 16, (2, 1)),
+    ("x16", "col", F32, BF16, 16, 16, (1, 1)),
+    ("col", "x8", E4M3, FNUZ, 16, 32, (4, 2)),
+    ("x8", "x16", BF16, BF16, 8, 8, (1, 2)),
+    ("col", "rows_d", F32, F32, 8, 64, (2, 1)),
+    ("col", "rows_d", E4M3, E4M3, 32, 32, (1, 1)),
+])
+def test_tr8_forms(o1, monkeypatch, sf, df, sdt, ddt, Bp, Bd, tp):
+    """k_convert_tr8 over every pairing of side forms (rows / head_dim-major / x-packed),
+    each dtype width on the transpose (1, 2, 4 bytes), block growth with several source
+    blocks per destination block, ragged requests (0, 1 and non-multiple-of-8 tokens), TP
+    split and merge: bit-exact vs O1, and identical to the shared-memory kernel."""
+    import paper_2509_17542_b200 as kvx
+    (so, px), (do, dx) = _FORMS[sf], _FORMS[df]
+    case = make_case(2, 8, 64, tp[0], tp[1], Bp, Bd, [70, 0, 1, 37, 129], sdt, ddt, so, do, seed=Bp * 7 + Bd,
+                     o1=o1, scales="pow2", p_split=px, d_split=dx)
+    if sdt in FP8:
+        for i, lay in enumerate(case["src_lays"]):
+            lay["scales"] = synth.pow2_scales(900 + i, 2, 8 // tp[0], -2, 2)
+    got = {}
+    for tr in ("1", "0"):
+        monkeypatch.setenv("KVX_TR", tr)
+        _, got[tr], _ = run_case(o1, case)
+        assert kvx.last_kernel() == ("k_convert_tr8" if tr == "1" else "k_convert_tr")
+    for a, b in zip(got["1"], got["0"]):
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("tp_p,tp_d", [(1, 1), (1, 2), (2, 1)])
