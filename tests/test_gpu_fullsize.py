@@ -67,3 +67,60 @@ def test_fullsize_sampled(name, p_ranks, d_ranks, reqs):
             assert ok, det
     for q in d_ranks:
         _tail_and_canary(w, q)
+
+
+def test_fullsize_vendor_layouts(o1):
+    """c4 pair at full size (80 layers, 2 local heads, 32 x 4096 tokens, block 16, TP4 -> 4
+    rank 0 -> 0) from an other-vendor P cache -- x-packed K pool ([LAYER], BLOCK, HEAD,
+    D/8, SLOT, 8) and head_dim-major V pool ([LAYER], BLOCK, HEAD, DIM, SLOT) -- into the
+    NVIDIA-style D pool (BLOCK, LAYER, KV, HEAD, SLOT, DIM), bf16 -> e4m3, in the two
+    calls tools/variants_bench.py times (k_convert_tr8).  Sampled: requests 0 / 17 / 31 x
+    layers 0 / 40 / 79, all their blocks, vs O1 on the extracted blocks; canary outside."""
+    import paper_2509_17542_b200 as kvx
+    from synth import BLOCK, DIM, HEAD, KV, LAYER, SLOT
+    L, H, D, tp, B = 80, 8, 128, 4, 16
+    Hl = H // tp
+    n_tokens = [4096] * 32
+    dev = torch.device("cuda", 0)
+    NB = synth.pool_capacity(n_tokens, B)
+    st = synth.block_tables(11, n_tokens, B, NB)
+    dt_ = synth.block_tables(12, n_tokens, B, NB)
+    dsc_np = synth.pow2_scales(6, L, Hl)
+    dsc = torch.from_numpy(dsc_np).to(dev)
+    vend = (LAYER, KV, BLOCK, HEAD, DIM, SLOT)
+    Kl = kvx.Layout(L, H, D, tp, 0, B, NB, synth.BF16, vend, None, kv_part=1, dim_split=8)
+    Vl = kvx.Layout(L, H, D, tp, 0, B, NB, synth.BF16, vend, None, kv_part=2)
+    Dl = kvx.Layout(L, H, D, tp, 0, B, NB, synth.E4M3, synth.D_ORDER, dsc)
+    Kp, Vp = Kl.new_pool(dev), Vl.new_pool(dev)
+    synth.fill_random_finite_(Kp.view(torch.int16), 40, synth.BF16)
+    synth.fill_random_finite_(Vp.view(torch.int16), 41, synth.BF16)
+    DP = Dl.new_pool(dev, fill=synth.CANARY)
+    sbt = kvx.Batch(Kl, n_tokens, st, dev)
+    dbt = kvx.Batch(Dl, n_tokens, dt_, dev)
+    kvx.convert_reshard([Kl], [Kp], sbt, [Dl], [DP], dbt)
+    assert kvx.last_kernel() == "k_convert_tr8"
+    kvx.convert_reshard([Vl], [Vp], sbt, [Dl], [DP], dbt)
+    assert kvx.last_kernel() == "k_convert_tr8"
+    torch.cuda.synchronize()
+    K6 = Kp.view(torch.int16).view(L, 1, NB, Hl, D // 8, B, 8)
+    V6 = Vp.view(torch.int16).view(L, 1, NB, Hl, D, B)
+    D6 = DP.view(torch.uint8).view(NB, L, 2, Hl, B, D)
+    for r in (0, 17, 31):
+        sb = torch.as_tensor(st[r], device=dev)
+        db = torch.as_tensor(dt_[r], device=dev)
+        nb = len(st[r])
+        for l in (0, 40, 79):
+            ksub = K6[l:l + 1].index_select(2, sb).cpu().numpy().reshape(-1)
+            vsub = V6[l:l + 1].index_select(2, sb).cpu().numpy().reshape(-1)
+            got = D6.index_select(0, db)[:, l:l + 1].cpu().numpy().reshape(-1)
+            want = np.full(got.size, synth.CANARY, np.uint8)
+            sl = lambda part, x: synth.layout(1, H, D, tp, 0, B, nb, synth.BF16, vend, kv_part=part, dim_split=x)
+            dl = synth.layout(1, H, D, tp, 0, B, nb, synth.E4M3, synth.D_ORDER, scales=dsc_np[l:l + 1])
+            ids = [list(range(nb))]
+            o1.convert([sl(1, 8)], [ksub], [dl], [want], [n_tokens[r]], ids, ids)
+            o1.convert([sl(2, 0)], [vsub], [dl], [want], [n_tokens[r]], ids, ids)
+            assert np.array_equal(got, want), f"request {r} layer {l}: {int((got != want).sum())} bytes differ"
+    used = sorted(b for t in dt_ for b in t)
+    free = sorted(set(range(NB)) - set(used))
+    fb = D6.index_select(0, torch.as_tensor(free, device=dev))
+    assert bool((fb == synth.CANARY).all()), "a block outside the tables was written"
