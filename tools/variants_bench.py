@@ -25,14 +25,14 @@ from synth import BLOCK, DIM, HEAD, KV, LAYER, SLOT  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--src", default="bf16", choices=["bf16", "fnuz", "e4m3"])
-    ap.add_argument("--dst", default="e4m3", choices=["e4m3", "bf16", "fnuz"])
+    ap.add_argument("--dst", default="e4m3", choices=["e4m3", "bf16", "fnuz", "f32"])
     ap.add_argument("--iters", type=int, default=10)
     args = ap.parse_args()
     import paper_2509_17542_b200 as kvx
     from bench import load_peaks
     L, H, D, tp, B = 80, 8, 128, 4, 16
     n_tokens = [4096] * 32
-    names = {"bf16": synth.BF16, "fnuz": synth.FNUZ, "e4m3": synth.E4M3}
+    names = {"bf16": synth.BF16, "fnuz": synth.FNUZ, "e4m3": synth.E4M3, "f32": synth.F32}
     sdt, ddt = names[args.src], names[args.dst]
     NB = synth.pool_capacity(n_tokens, B)
     st = synth.block_tables(11, n_tokens, B, NB)
