@@ -296,6 +296,69 @@ __device__ __forceinline__ void fnuzx4_to_f32(uint32_t w, float* f) {
   }
 }
 
+// PTX prmt in its default mode: selector nibble bit 3 replicates the sign bit of the chosen
+// byte over all 8 bits (__byte_perm uses only the low 3 bits)
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// packed f16 pair * 0.5 (exact for every e4m3fn value)
+__device__ __forceinline__ uint32_t half2_times_half(uint32_t h) {
+  __half2 v = *reinterpret_cast<const __half2*>(&h);
+  v = __hmul2(v, __float2half2_rn(0.5f));
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+
+// Four fp8 codes (e4m3fn or e4m3fnuz) -> f32, two codes per conversion
+// (cvt.rn.f16x2.e4m3x2, exact), SIMD fix-ups on the packed halves.  e4m3fnuz: the value is
+// half the e4m3fn value of the same bits (HMUL2 by 0.5, exact: the smallest fn subnormal
+// 2^-9 halves to a normal f16); the codes 0x7F / 0xFF (+-240 in fnuz, NaN in fn) and 0x80
+// (NaN in fnuz, -0 in fn) are patched with per-byte masks -- exact zero-byte tests
+// ((x & 0x7F..) + 0x7F..) | x, expanded to 16-bit lanes by prmt's sign replication.
+// NaN comes out as a NaN; every caller multiplies by the dequant scale next, which
+// canonicalises it (reading 12).
+template <int DT>
+__device__ __forceinline__ void fp8x4_to_f32(uint32_t w, float* f) {
+  uint32_t h[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const unsigned short in = (unsigned short)(w >> (16 * k));
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h[k]) : "h"(in));
+  }
+  if constexpr (DT == KV_F8E4M3FNUZ) {
+    const uint32_t x7 = ~w & 0x7F7F7F7Fu;                          // byte 0 <=> (b & 0x7F) == 0x7F
+    const uint32_t y7 = (x7 + 0x7F7F7F7Fu) | x7;                   // bit 7 clear <=> that byte is 0
+    const uint32_t x8 = w ^ 0x80808080u;                           // byte 0 <=> b == 0x80
+    const uint32_t y8 = ((x8 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x8;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t hv = half2_times_half(h[k]);
+      const uint32_t sel = k ? 0xBBAAu : 0x9988u;                   // sign of bytes 2k, 2k+1 per half
+      const uint32_t m7 = ~prmt(y7, 0u, sel), m8 = ~prmt(y8, 0u, sel);
+      const uint32_t v240 = (prmt(w, 0u, k ? 0x3424u : 0x1404u) & 0x80008000u) | 0x5B805B80u;  // +-240
+      uint32_t r = (hv & ~m7) | (v240 & m7);
+      r = (r & ~m8) | (0x7E007E00u & m8);
+      h[k] = r;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float2 ff = __half22float2(*reinterpret_cast<const __half2*>(&h[k]));
+    f[2 * k] = ff.x;
+    f[2 * k + 1] = ff.y;
+  }
+}
+
+// a, b <- RN(a * s), RN(b * s): one FMUL2 (mul.rn.f32x2, never contracted)
+__device__ __forceinline__ void fmul2_rn(float& a, float& b, float s) {
+  uint64_t x, y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a), "f"(b));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(y) : "l"(x), "l"((uint64_t)__float_as_uint(s) | ((uint64_t)__float_as_uint(s) << 32)));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(y));
+}
+
 // Cast a chunk SDT -> DDT.  ssc: dequant scale of an fp8 source; inv: RN(1/s) of an fp8
 // destination (an fp8 -> other-fp8 cast applies both, in that order).
 template <int SDT, int DDT, int VEC>
@@ -305,17 +368,25 @@ __device__ __forceinline__ void cast_chunk(const Chunk<SDT, VEC>& in, Chunk<DDT,
     for (int i = 0; i < Chunk<SDT, VEC>::WORDS; ++i) out.w[i] = in.w[i];
   } else {
     float f[VEC];
-    if constexpr (SDT == KV_F8E4M3FNUZ && VEC % 4 == 0) {
+    if constexpr (is_fp8(SDT) && VEC % 4 == 0) {
 #pragma unroll
-      for (int i = 0; i < VEC; i += 4) fnuzx4_to_f32(in.w[i >> 2], f + i);
+      for (int i = 0; i < VEC; i += 4) fp8x4_to_f32<SDT>(in.w[i >> 2], f + i);
     } else {
 #pragma unroll
       for (int i = 0; i < VEC; ++i) f[i] = to_f32<SDT>(get_elem<SDT>(in.w, i));
     }
+    if constexpr (VEC % 2 == 0) {
 #pragma unroll
-    for (int i = 0; i < VEC; ++i) {
-      if constexpr (is_fp8(SDT)) f[i] = __fmul_rn(f[i], ssc);
-      if constexpr (is_fp8(DDT)) f[i] = __fmul_rn(f[i], inv);
+      for (int i = 0; i < VEC; i += 2) {
+        if constexpr (is_fp8(SDT)) fmul2_rn(f[i], f[i + 1], ssc);
+        if constexpr (is_fp8(DDT)) fmul2_rn(f[i], f[i + 1], inv);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) {
+        if constexpr (is_fp8(SDT)) f[i] = __fmul_rn(f[i], ssc);
+        if constexpr (is_fp8(DDT)) f[i] = __fmul_rn(f[i], inv);
+      }
     }
 #pragma unroll
     for (int i = 0; i < Chunk<DDT, VEC>::WORDS; ++i) out.w[i] = 0;
