@@ -592,6 +592,9 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
       // register path unless KVX_TR=0 (the smem-staged kernel) or a block holds < 8 slots
       const char* tr_env = getenv("KVX_TR");
       const bool use_tr8 = S->d.block_size >= 8 && D->d.block_size >= 8 && !(tr_env && atoi(tr_env) == 0);
+      const char* w16_env = getenv("KVX_TR_W16");
+      a.tr_w16 = (st == 1 && dt == 0 && S->elem_bytes == 2 && S->d.block_size >= 16 && D->d.block_size >= 16 &&
+                  !(w16_env && atoi(w16_env) == 0)) ? 1 : 0;
       for (int ax = 0; ax < 6; ++ax) {
         a.ss[ax] = S->stride[ax];
         a.ds[ax] = D->stride[ax];

@@ -54,6 +54,7 @@ struct ConvArgs {
   // (mode 1); or whose head_dim is x-split with (D/x, SLOT, x) innermost (mode 2, x = s_x/d_x)
   int32_t s_tr, d_tr, s_x, d_x;
   int32_t tr_lbp, tr_lbd, s_lm, d_lm;  // log2 of Bp, Bd, s_x / 8, d_x / 8
+  int32_t tr_w16;  // k_convert_tr8: 2-byte head_dim-major source -> rows, 16-slot sub-blocks
   FastDiv f_hde;  // D-local heads per item loop (Hd_eff)
   const uint8_t* src[KVX_MAX_RANKS];
   uint8_t* dst[KVX_MAX_RANKS];

@@ -1096,14 +1096,17 @@ __device__ __forceinline__ void transpose8(const Chunk<DT, 8>* in, Chunk<DT, 8>*
 #endif
 constexpr int kTr8Threads = KVX_TR8_THREADS;
 
-template <int SDT, int DDT>
-__global__ void __launch_bounds__(kTr8Threads) k_convert_tr8(const __grid_constant__ ConvArgs a) {
+template <int SDT, int DDT, bool W16>
+__global__ void __launch_bounds__(kTr8Threads, W16 ? 2 : 1) k_convert_tr8(const __grid_constant__ ConvArgs a) {
   constexpr uint32_t SB = Tr<SDT>::B, DB = Tr<DDT>::B;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t lbp = (uint32_t)a.tr_lbp, lbd = (uint32_t)a.tr_lbd, lcpr = (uint32_t)a.cpr_shift;
-  const uint32_t lnsub = (lbd - 3u) + lcpr;  // log2 sub-blocks per item
+  // W16 (2-byte head_dim-major source, B_p, B_d >= 16): a lane owns 8 head_dim rows x 16
+  // slots and reads each 32-B row with one 256-bit load
+  constexpr bool w16 = W16;
+  const uint32_t lnsub = (lbd - (w16 ? 4u : 3u)) + lcpr;  // log2 sub-blocks per item
   const uint32_t ngroups = (a.n_items + 31u) >> 5;
   const bool s_col = a.s_tr == 1, d_col = a.d_tr == 1;
   for (uint32_t grp = warp; grp < ngroups; grp += nwarps) {
@@ -1164,6 +1167,46 @@ __global__ void __launch_bounds__(kTr8Threads) k_convert_tr8(const __grid_consta
       const float rsc = __shfl_sync(0xFFFFFFFFu, m_rsc, i);
       const float s2 = __shfl_sync(0xFFFFFFFFu, m_s2, i);
       if (unit >= nunits) continue;
+      if constexpr (Tr<SDT>::B == 2 && W16) {
+        {
+          const uint32_t s0 = (u >> lcpr) << 4, d0 = (u & ((1u << lcpr) - 1u)) << 3;
+          Chunk<SDT, 16> xr[8];
+          const bool any = s0 < valid;
+          if (any) {
+            const uint32_t j = s0 >> lbp;
+            const int64_t sblk = j == 0 ? sblk0 : __ldg(sids + j);
+            const uint8_t* sb = snob + sblk * a.ss[KV_AX_BLOCK] * SB;
+            const uint32_t sin = s0 & ((1u << lbp) - 1u);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) load_chunk<SDT, 16>(xr[k], sb + ((int64_t)(d0 + k) * a.ss[KV_AX_DIM] + sin) * SB);
+          }
+          const int64_t doff = dim_off(d0, a.ds[KV_AX_DIM], a.d_dk);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t s1 = s0 + 8u * hh;
+            Chunk<DDT, 8> o[8];
+            if (s1 >= valid) {
+#pragma unroll
+              for (int k = 0; k < 8; ++k) zero_chunk(o[k]);
+            } else {
+              Chunk<SDT, 8> x[8], y[8];
+#pragma unroll
+              for (int k = 0; k < 8; ++k)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) x[k].w[m] = xr[k].w[4 * hh + m];
+              transpose8<SDT>(x, y);
+#pragma unroll
+              for (int k = 0; k < 8; ++k) {
+                cast_chunk<SDT, DDT, 8>(y[k], o[k], rsc, s2);
+                if (s1 + (uint32_t)k >= valid) zero_chunk(o[k]);
+              }
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) store_chunk<DDT, 8>(db + ((int64_t)(s1 + k) * a.ds[KV_AX_SLOT] + doff) * DB, o[k]);
+          }
+          continue;
+        }
+      }
       const uint32_t s0 = (u >> lcpr) << 3;             // first dst slot of the sub-block
       const uint32_t d0 = (u & ((1u << lcpr) - 1u)) << 3;  // first head_dim element
       Chunk<DDT, 8> o[8];
@@ -1935,7 +1978,11 @@ cudaError_t tr_v(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
 }
 template <int VEC, int SDT, int DDT>
 cudaError_t tr8_t(const ConvArgs& a, cudaStream_t s) {
-  auto k = k_convert_tr8<SDT, DDT>;
+  auto k = k_convert_tr8<SDT, DDT, false>;
+  // W16 only for 2-byte -> 2-byte: V pool bf16 -> bf16 0.80 -> 0.85 of copy; with an fp8
+  // destination it measured 0.83 vs 0.85 (and a 4-byte destination spills)
+  if constexpr (Tr<SDT>::B == 2 && Tr<DDT>::B == 2)
+    if (a.tr_w16) k = k_convert_tr8<SDT, DDT, true>;
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kTr8Threads, 0);
   if (occ < 1) occ = 1;

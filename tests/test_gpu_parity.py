@@ -581,6 +581,25 @@ def test_tr8_forms(o1, monkeypatch, sf, df, sdt, ddt, Bp, Bd, tp):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("sdt,ddt,Bp,Bd,tp,do", [
+    (BF16, BF16, 16, 16, (2, 1), "rows_d"),
+    (F16, BF16, 16, 64, (1, 2), "rows_p"),
+    (BF16, F16, 32, 32, (2, 2), "x8"),
+])
+def test_tr8_w16(o1, monkeypatch, sdt, ddt, Bp, Bd, tp, do):
+    """k_convert_tr8's W16 sub-blocks (2-byte head_dim-major source, 2-byte destination,
+    blocks of >= 16 slots: one 256-bit load per 32-B head_dim row, two 8 x 8 transposes),
+    ragged requests, on and off (KVX_TR_W16=0): bit-exact vs O1 both ways."""
+    import paper_2509_17542_b200 as kvx
+    (so, _), (dord, dx) = _FORMS["col"], _FORMS[do]
+    case = make_case(2, 8, 64, tp[0], tp[1], Bp, Bd, [70, 0, 1, 37, 129, 16], sdt, ddt, so, dord, seed=Bp + Bd + 5,
+                     o1=o1, d_split=dx)
+    for w in ("1", "0"):
+        monkeypatch.setenv("KVX_TR_W16", w)
+        run_case(o1, case)
+        assert kvx.last_kernel() == "k_convert_tr8"
+
+
 @pytest.mark.parametrize("tp_p,tp_d", [(1, 1), (1, 2), (2, 1)])
 def test_tile_copy_head_groups(o1, tp_p, tp_d):
     """k_tile_copy with sub-tiles over 64 KB (32 heads x 16 slots x 256 B): split into
