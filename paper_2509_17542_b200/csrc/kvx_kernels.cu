@@ -239,6 +239,14 @@ __device__ __forceinline__ uint32_t f32x2_to_e4m3x2(float lo, float hi) {
   return r;
 }
 
+// a, b <- RN(a * s), RN(b * s): one FMUL2 (mul.rn.f32x2, never contracted)
+__device__ __forceinline__ void fmul2_rn(float& a, float& b, float s) {
+  uint64_t x, y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a), "f"(b));
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(y) : "l"(x), "l"((uint64_t)__float_as_uint(s) | ((uint64_t)__float_as_uint(s) << 32)));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(y));
+}
+
 // e4m3fnuz codes of two scaled f32 values (lo -> bits 0..7, hi -> bits 8..15): RNE with
 // satfinite at +-240, NaN -> 0x80, zero results +0 (reading 25).  Every fnuz value is half
 // the e4m3fn value of the same bits (same mantissa grid, bias 8 vs 7), so the hardware
@@ -257,21 +265,23 @@ __device__ __forceinline__ uint32_t f32x2_to_fnuzx2(float lo, float hi) {
 
 
 // Four e4m3fnuz codes of scaled values f[0..3], branch-free (no divergence on data): the
-// hardware e4m3fn conversion of 2v, then per byte: v > 232 -> 0x7F | sign, NaN -> 0x80,
-// -0 (0x80) -> 0x00 (reading 25).
+// hardware e4m3fn conversion of 2v (RNE, satfinite: every |2v| > 432 gives 0x7E | sign),
+// then -0 (0x80) -> +0 by an exact per-byte zero test, then +1 on the bytes whose |2v| >
+// 464 or is NaN (one set.gtu each): 0x7E | s -> 0x7F | s (+-240, v > 232) and the NaN code
+// 0x7F -> 0x80 (fnuz's NaN; the scale multiply before this made every NaN positive)
+// (reading 25).  Runs after the zero fix so a NaN's 0x80 is not taken for -0.
 __device__ __forceinline__ uint32_t f32x4_to_fnuzx4(const float* f) {
-  uint32_t r = f32x2_to_e4m3x2(__fmul_rn(f[0], 2.0f), __fmul_rn(f[1], 2.0f)) |
-               (f32x2_to_e4m3x2(__fmul_rn(f[2], 2.0f), __fmul_rn(f[3], 2.0f)) << 16);
+  float d[4] = {f[0], f[1], f[2], f[3]};
+  fmul2_rn(d[0], d[1], 2.0f);
+  fmul2_rn(d[2], d[3], 2.0f);
+  uint32_t r = f32x2_to_e4m3x2(d[0], d[1]) | (f32x2_to_e4m3x2(d[2], d[3]) << 16);
   const uint32_t x = r ^ 0x80808080u;  // bytes equal to 0x80 become 0
   r ^= ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x) & 0x80808080u;  // exact per-byte zero test: -0 -> +0
+  uint32_t m[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float a = fabsf(f[i]);
-    const uint32_t sh = 8 * i, sat = (0x7Fu | ((__float_as_uint(f[i]) >> 24) & 0x80u)) << sh;
-    r = a > 232.0f ? ((r & ~(0xFFu << sh)) | sat) : r;
-    r = a != a ? ((r & ~(0xFFu << sh)) | (0x80u << sh)) : r;
-  }
-  return r;
+  for (int i = 0; i < 4; ++i) asm("set.gtu.u32.f32 %0, %1, 0f43E80000;" : "=r"(m[i]) : "f"(fabsf(d[i])));  // |2v| > 464
+  const uint32_t inc = __byte_perm(__byte_perm(m[0], m[1], 0x0040u), __byte_perm(m[2], m[3], 0x0040u), 0x5410u);
+  return r + (inc & 0x01010101u);
 }
 
 // Four e4m3fnuz codes -> f32, branch-free: every fnuz value is half the e4m3fn value of its
@@ -349,14 +359,6 @@ __device__ __forceinline__ void fp8x4_to_f32(uint32_t w, float* f) {
     f[2 * k] = ff.x;
     f[2 * k + 1] = ff.y;
   }
-}
-
-// a, b <- RN(a * s), RN(b * s): one FMUL2 (mul.rn.f32x2, never contracted)
-__device__ __forceinline__ void fmul2_rn(float& a, float& b, float s) {
-  uint64_t x, y;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a), "f"(b));
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(y) : "l"(x), "l"((uint64_t)__float_as_uint(s) | ((uint64_t)__float_as_uint(s) << 32)));
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(y));
 }
 
 // Cast a chunk SDT -> DDT.  ssc: dequant scale of an fp8 source; inv: RN(1/s) of an fp8
