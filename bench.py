@@ -533,12 +533,14 @@ def run_multi(args):
             for p in my_p}
         R = max(1, args.ring_slots)
         if narrowing and not args.layer_chunk:
-            # ~64 MiB of wire per chunk, at most 20 chunks (c4 full batch: 4 layers per chunk;
-            # one request: 3 chunks), so the pipeline fill stays small and per-chunk launch
-            # costs on P stay hidden behind D's reads
+            # ~40 MiB of wire per chunk, at most 20 chunks (c4 full batch: 4 layers per chunk;
+            # one request: 4 chunks of 20 layers), so the pipeline fill stays small and
+            # per-chunk launch costs on P stay hidden behind D's reads.  Batch-1 c4 pair
+            # (profiles/r01/batch1_chunks_c4_n2.jsonl): 2 / 4 / 8 / 16 chunks = 0.261 / 0.247 /
+            # 0.286 / 0.359 ms
             pair_wire = 2 * cfg.L * min(cfg.H // cfg.tp_p, cfg.H // cfg.tp_d) * cfg.D * \
                 synth.NBYTES[cfg.dst_dtype] * cfg.total_tokens
-            n_ch = min(20, max(1, round(pair_wire / (64 << 20))))
+            n_ch = min(20, max(1, round(pair_wire / (40 << 20))))
             lc = -(-cfg.L // n_ch)
         ring, slot_bytes, dst_lays = None, 0, {}
         dyn = args.dynamic_scales and narrowing and synth.NBYTES[cfg.src_dtype] > 1
