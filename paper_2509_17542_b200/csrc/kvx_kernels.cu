@@ -284,28 +284,6 @@ __device__ __forceinline__ uint32_t f32x4_to_fnuzx4(const float* f) {
   return r + (inc & 0x01010101u);
 }
 
-// Four e4m3fnuz codes -> f32, branch-free: every fnuz value is half the e4m3fn value of its
-// bits, so the hardware e4m3fn -> f16 conversion times 0.5 (exact) decodes all but
-// 0x7F / 0xFF (+-240: the fn NaN slot) and 0x80 (NaN), which are selected in.
-__device__ __forceinline__ void fnuzx4_to_f32(uint32_t w, float* f) {
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    uint32_t h2;
-    const unsigned short in = (unsigned short)(w >> (16 * h));
-    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(in));
-    const __half2 v = __hmul2(*reinterpret_cast<const __half2*>(&h2), __float2half2_rn(0.5f));
-    const float2 ff = __half22float2(v);
-    f[2 * h] = ff.x;
-    f[2 * h + 1] = ff.y;
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t b = (w >> (8 * i)) & 0xFFu;
-    f[i] = (b & 0x7Fu) == 0x7Fu ? ((b & 0x80u) ? -240.0f : 240.0f) : f[i];
-    f[i] = b == 0x80u ? __uint_as_float(0x7FFFFFFFu) : f[i];
-  }
-}
-
 // PTX prmt in its default mode: selector nibble bit 3 replicates the sign bit of the chosen
 // byte over all 8 bits (__byte_perm uses only the low 3 bits)
 __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
