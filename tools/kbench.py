@@ -72,10 +72,20 @@ def main():
                           "GBs": round(2 * x.numel() * 2 / med / 1e6, 1)}), flush=True)
         del x, y
         torch.cuda.empty_cache()
+    if "copy1g" in sel:  # the same bytes as c2 (1 GiB read + 1 GiB written)
+        x = torch.empty(1 << 29, dtype=torch.bfloat16, device="cuda")
+        y = torch.empty_like(x)
+        med, mn = time_it(lambda: y.copy_(x))
+        print(json.dumps({"case": "torch copy_ 1 GiB r+w (c2's bytes)", "ms_med": round(med, 4),
+                          "GBs": round(2 * x.numel() * 2 / med / 1e6, 1)}), flush=True)
+        del x, y
+        torch.cuda.empty_cache()
     if "c1" in sel:
         case("c1 tiny fp16->bf16 16->32", cf["c1"], [0], [0])
     if "c2" in sel:
         case("c2 TP2->1 fp16 (all ranks one GPU)", cf["c2"], [0, 1], [0])
+    if "c2c" in sel:
+        case("c2 TP2->1 fp16, contiguous tables", cf["c2"], [0, 1], [0], contiguous=True, parity=False)
     if "c3" in sel:
         case("c3 one D rank: P0,P1 -> D0 bf16 16->64", cf["c3"], [0, 1], [0])
     if "c4" in sel:
