@@ -38,7 +38,7 @@ import numpy as np  # noqa: E402
 
 import synth  # noqa: E402
 
-METRIC = "KV transfer GB/s and ms/request (P->D, device-timed) vs HBM/NVLink roofline"
+METRIC = "KV transfer GB/s and ms/request (P\u2192D, device-timed) vs HBM/NVLink roofline"  # BASELINE.json verbatim
 NVLINK_MEASURED_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction
 NVLINK_NOMINAL_GBS = 900.0
 
