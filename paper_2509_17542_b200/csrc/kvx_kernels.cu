@@ -239,12 +239,12 @@ __device__ __forceinline__ uint32_t f32x2_to_e4m3x2(float lo, float hi) {
   return r;
 }
 
-// a, b <- RN(a * s), RN(b * s): one FMUL2 (mul.rn.f32x2, never contracted)
+// a, b <- RN(a * s), RN(b * s): one FMUL2 (__fmul2_rn: round-to-nearest, never contracted
+// into an FMA)
 __device__ __forceinline__ void fmul2_rn(float& a, float& b, float s) {
-  uint64_t x, y;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a), "f"(b));
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(y) : "l"(x), "l"((uint64_t)__float_as_uint(s) | ((uint64_t)__float_as_uint(s) << 32)));
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(y));
+  const float2 r = __fmul2_rn(make_float2(a, b), make_float2(s, s));
+  a = r.x;
+  b = r.y;
 }
 
 // e4m3fnuz codes of two scaled f32 values (lo -> bits 0..7, hi -> bits 8..15): RNE with
