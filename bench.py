@@ -1101,7 +1101,18 @@ def run_stream(args):
     dist.destroy_process_group()
 
 
+def _json_only_stdout():
+    """The driver reads ONE JSON line from stdout, but native libraries write to fd 1 too (NCCL
+    prints its version banner on rank 0 when the first communicator comes up).  Point fd 1 at
+    stderr and give Python's sys.stdout the original descriptor, so only our prints reach it."""
+    sys.stdout.flush()
+    keep = os.dup(1)
+    os.dup2(2, 1)
+    sys.stdout = os.fdopen(keep, "w", buffering=1)
+
+
 def main():
+    _json_only_stdout()
     args = parse()
     if args.impl != "reference":   # a fresh checkout has no libkvx.so yet (no-op when up to date)
         import __graft_entry__

@@ -18,8 +18,8 @@ def _run(args, timeout):
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py")] + args, cwd=ROOT, capture_output=True,
                          text=True, timeout=timeout)
     assert out.returncode == 0, out.stderr[-2000:]
-    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
-    assert len(lines) == 1, out.stdout[-2000:]
+    lines = out.stdout.splitlines()  # exactly one line, nothing else (native banners go to stderr)
+    assert len(lines) == 1 and lines[0].startswith("{"), out.stdout[-2000:]
     return json.loads(lines[0])
 
 

@@ -30,8 +30,8 @@ def _bench(n, *args):
            "--steps", "2", "--warmup", "1", "--no-e2e", *args]
     out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]
-    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
-    assert len(lines) == 1, out.stdout[-2000:]
+    lines = out.stdout.splitlines()  # exactly one line, nothing else (native banners go to stderr)
+    assert len(lines) == 1 and lines[0].startswith("{"), out.stdout[-2000:]
     return json.loads(lines[0])
 
 
