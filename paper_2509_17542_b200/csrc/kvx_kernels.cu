@@ -298,6 +298,13 @@ __device__ __forceinline__ uint32_t half2_times_half(uint32_t h) {
   v = __hmul2(v, __float2half2_rn(0.5f));
   return *reinterpret_cast<const uint32_t*>(&v);
 }
+// packed f16 pair * 128 (exact for the values the fnuz decode builds: at most 1.875 -> 240,
+// subnormals become normals)
+__device__ __forceinline__ uint32_t half2_times_128(uint32_t h) {
+  __half2 v = *reinterpret_cast<const __half2*>(&h);
+  v = __hmul2(v, __float2half2_rn(128.0f));
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
 
 // Four fp8 codes (e4m3fn or e4m3fnuz) -> f32, two codes per conversion
 // (cvt.rn.f16x2.e4m3x2, exact), SIMD fix-ups on the packed halves.  e4m3fnuz: the value is
@@ -307,15 +314,38 @@ __device__ __forceinline__ uint32_t half2_times_half(uint32_t h) {
 // ((x & 0x7F..) + 0x7F..) | x, expanded to 16-bit lanes by prmt's sign replication.
 // NaN comes out as a NaN; every caller multiplies by the dequant scale next, which
 // canonicalises it (reading 12).
+#ifndef KVX_FNUZ_SHIFT
+#define KVX_FNUZ_SHIFT 1
+#endif
 template <int DT>
 __device__ __forceinline__ void fp8x4_to_f32(uint32_t w, float* f) {
   uint32_t h[2];
+  if constexpr (DT == KV_F8E4M3FNUZ && KVX_FNUZ_SHIFT) {
+    // e4m3fnuz without the fn conversion: a code's 7 magnitude bits (4 exponent, 3
+    // mantissa) placed at f16 bits 7..13 with its sign at bit 15 read as an f16 of value
+    // 2^-7 times the fnuz value -- normals 2^(e-15) (1 + m/8), subnormals (m/8) 2^-14 --
+    // so one exact HMUL2 by 2^7 decodes both, and 0x7F / 0xFF come out as +-240 by
+    // themselves (f16's exponent 15 is an ordinary one).  Only 0x80 (fnuz's NaN; -0 here)
+    // is patched: an exact per-byte test, expanded to its 16-bit lane by prmt's sign
+    // replication, selects the canonical f16 NaN 0x7E00.
+    const uint32_t x8 = w ^ 0x80808080u;                           // byte 0 <=> b == 0x80
+    const uint32_t y8 = ((x8 & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x8;  // bit 7 clear <=> b == 0x80
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const uint32_t x = __byte_perm(w, 0u, k ? 0x3424u : 0x1404u);  // codes 2k, 2k+1 at bits 8..15 / 24..31
+      const uint32_t y = x >> 1;                                     // sign at 14 / 30, magnitude at 7..13 / 23..29
+      const uint32_t hv = half2_times_128(y + (y & 0x40004000u));    // sign moved to 15 / 31
+      const uint32_t keep = prmt(y8, 0u, k ? 0xBBAAu : 0x9988u);     // all ones <=> not 0x80
+      h[k] = (hv & keep) | (0x7E007E00u & ~keep);
+    }
+  } else {
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const unsigned short in = (unsigned short)(w >> (16 * k));
     asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h[k]) : "h"(in));
   }
-  if constexpr (DT == KV_F8E4M3FNUZ) {
+  }
+  if constexpr (DT == KV_F8E4M3FNUZ && !KVX_FNUZ_SHIFT) {
     const uint32_t x7 = ~w & 0x7F7F7F7Fu;                          // byte 0 <=> (b & 0x7F) == 0x7F
     const uint32_t y7 = (x7 + 0x7F7F7F7Fu) | x7;                   // bit 7 clear <=> that byte is 0
     const uint32_t x8 = w ^ 0x80808080u;                           // byte 0 <=> b == 0x80
