@@ -114,7 +114,11 @@ def test_exhaustive_fnuz_tables_on_device(o1):
     o = (LAYER, KV, BLOCK, SLOT, HEAD, DIM)
     runs = [(F16, FNUZ, None, 1.0), (BF16, FNUZ, None, 5.5 / 240), (FNUZ, BF16, 0.75, None),
             (FNUZ, F16, 2.0 ** -3, None), (FNUZ, F32, 1.0, None), (FNUZ, E4M3, 0.5, 1.0), (E4M3, FNUZ, 1.0, 2.0),
-            (E4M3, FNUZ, 0.37, 1.3)]
+            (E4M3, FNUZ, 0.37, 1.3),
+            # the fnuz decode folds an exact 2^7 into the source scale when 2^7 s is finite:
+            # both sides of that test (2^125 and 1.7e37 overflow it), f32-subnormal scales
+            (FNUZ, F32, 2.0 ** 125, None), (FNUZ, F32, 0.37, None), (FNUZ, BF16, 3.3e-41, None),
+            (FNUZ, F16, 2.0 ** -140, None), (FNUZ, E4M3, 1.7e37, 3.1e37)]
     for sdt, ddt, ssc, dsc in runs:
         L, H, D, B = 1, 1, 128, 16
         n = 1 << (8 * synth.NBYTES[sdt])
