@@ -479,6 +479,12 @@ constexpr int kThreads = 256;
 #define KVX_MINB 4  // >= 4 CTAs/SM for the row kernel: caps it at 64 registers (the 2-byte -> e4m3
                     // instantiation otherwise takes 76 and drops to 3 CTAs/SM, 0.87 instead of 0.95)
 #endif
+#ifndef KVX_MINB_WIDEN
+#define KVX_MINB_WIDEN 3  // fp8 -> wider casts: 3 CTAs/SM (up to 85 registers) keep more bytes in
+                          // flight (e4m3fnuz -> bf16 0.915 -> 0.956 of copy; 4 stays best for the
+                          // rest: profiles/r01/minb_occupancy_ab.txt)
+#endif
+constexpr int row_minb(int sdt, int ddt) { return is_fp8(sdt) && !is_fp8(ddt) ? KVX_MINB_WIDEN : KVX_MINB; }
 
 // ------------------------------------------------------------------------------------
 // K1/K4: fused pool -> pool convert (+ reshard, + cast, + tail zero-fill)
@@ -698,7 +704,7 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
 }
 
 template <int SDT, int DDT, int U, int VEC = 8, bool SPLIT = false>
-__global__ void __launch_bounds__(kThreads, KVX_MINB) k_convert_rows(const __grid_constant__ ConvArgs a) {
+__global__ void __launch_bounds__(kThreads, row_minb(SDT, DDT)) k_convert_rows(const __grid_constant__ ConvArgs a) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
