@@ -198,7 +198,8 @@ def test_wire_header_layout_roundtrip_and_check(kvx):
 def test_row_kernels_fit_four_ctas_per_sm():
     """Occupancy guard (CPU, from the cubin): every row-kernel instantiation uses <= 64
     registers and no local memory, so 4 CTAs of 256 threads fit an SM (the bf16 -> e4m3 one
-    took 76 registers once and lost 8% of bandwidth)."""
+    took 76 registers once and lost 8% of bandwidth); fp8 -> wider casts are capped at 3 CTAs
+    (<= 80 registers, KVX_MINB_WIDEN: profiles/r01/minb_occupancy_ab.txt)."""
     import subprocess
     so = os.path.join(ROOT, "paper_2509_17542_b200", "libkvx.so")
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-res-usage", so], capture_output=True, text=True).stdout
@@ -208,7 +209,8 @@ def test_row_kernels_fit_four_ctas_per_sm():
         # 1-byte sources in 16-element chunks (4 x 16 B in flight) may keep a few bytes on the
         # stack; every other instantiation must stay in registers
         wide_fp8 = re.search(r"k_convert_rowsILi[24]ELi\dELi\dELi16E", name)
-        assert int(reg) <= 64 and int(local) == 0 and int(stack) <= (32 if wide_fp8 else 0), (name, reg, stack, local)
+        widen = re.search(r"k_convert_rowsILi[24]ELi[013]E", name)
+        assert int(reg) <= (80 if widen else 64) and int(local) == 0 and int(stack) <= (32 if wide_fp8 else 0), (name, reg, stack, local)
 
 
 def test_layout_variants_describe_wire_and_header(kvx, o1):
