@@ -567,7 +567,7 @@ def run_multi(args):
         if me.kind == "D" and narrowing:
             slot_bytes = min(pch.slot_bytes[p] for p in my_p)
         nchunks = kvx.chunk_count((0, cfg.L), lc)
-        counters = torch.zeros(2 * nchunks, dtype=torch.int32, device=dev)
+        counters = torch.zeros(2 * nchunks + 1, dtype=torch.int32, device=dev)
         seq = [0]
 
         def step(ev=None):

@@ -141,6 +141,48 @@ kv_status kv_block_table_update(const kv_layout* lay, int32_t n_req, const int32
                                 const int32_t* host_block_ids, int64_t n_ids, void* dev_buf,
                                 size_t dev_buf_bytes, kv_batch* out, kv_stream stream);
 
+/* ---- A3: control-plane messages ------------------------------------------------
+ * What P and D exchange before a transfer: D learns P's "GPU ranks and parallel strategy"
+ * (III-B3) and the remote locations come "through control plane information
+ * interaction" (III-B1).  One message = one TP rank's layout descriptor, optionally
+ * its fp8 scales (host copy, fp32 [num_layers][2][H/tp]) and optionally a batch's block
+ * tables (T_r per request + the block ids, request-major: the kv_block_table_update
+ * arguments).  Uses: D -> P (D's layout, scales and table: the push and the sender-side
+ * cast of the staged pull), P -> D (P's layout and table: the direct pull).  The library
+ * only (de)serialises; the caller's control plane moves the bytes.
+ * Byte map, little-endian (host byte order must be little-endian for the parse pointers):
+ *    0 char[4] "KVC1"       4 u32 version (1)      8 u32 sections (bit 0 scales, bit 1 tables)
+ *   12 u32 header bytes (128)                     16 u64 total bytes
+ *   24 i32[17] num_layers first_layer num_kv_heads head_dim tp_degree tp_rank block_size
+ *              num_blocks dtype axis_order[6] kv_part dim_split
+ *   92 i32 n_req           96 i64 n_ids          104 i64 n_scales
+ *  112 u64 FNV-1a 64 of bytes [128, total)       120 u32 batch id (caller's tag)  124 u32 0
+ *  128 f32 scales[n_scales], i32 n_tokens[n_req], i32 block_ids[n_ids]
+ * kv_ctrl_msg_write: host_scales NULL = no scale section; n_req < 0 = no table section (then
+ *   n_ids must be 0).  The tables are validated like kv_block_table_update's (KV_ESHAPE:
+ *   count, range, duplicate).  KV_ESHAPE if cap < kv_ctrl_msg_bytes(...); *written = bytes.
+ * kv_ctrl_msg_parse: checks magic, version, section sizes, the payload digest (KV_EINVAL:
+ *   truncated or corrupted), that the descriptor describes (kv_layout_describe rules) and the
+ *   tables' rules; fills *out with pointers INTO msg (4-byte aligned; keep msg alive).
+ *   out->desc.scales is NULL: upload out->scales to the device and set it before describe. */
+typedef struct {
+  kv_layout_desc desc;
+  uint32_t batch_id;
+  int32_t has_tables;
+  const float* scales;     /* host, n_scales floats, or NULL */
+  int64_t n_scales;
+  int32_t n_req;
+  const int32_t* n_tokens; /* [n_req] */
+  int64_t n_ids;
+  const int32_t* block_ids; /* [n_ids] */
+} kv_ctrl_info;
+
+size_t kv_ctrl_msg_bytes(int32_t n_req, int64_t n_ids, int64_t n_scales);
+kv_status kv_ctrl_msg_write(const kv_layout* lay, const float* host_scales, uint32_t batch_id, int32_t n_req,
+                            const int32_t* host_n_tokens, const int32_t* host_block_ids, int64_t n_ids, uint8_t* out,
+                            size_t cap, size_t* written);
+kv_status kv_ctrl_msg_parse(const uint8_t* msg, size_t len, kv_ctrl_info* out);
+
 /* ---- A2: re-shard plan ------------------------------------------------------- */
 
 /* Pairs (p, q) whose head ranges overlap (Fig. 4): writes up to max_pairs
@@ -333,19 +375,24 @@ kv_status kv_recv_pipelined(kv_comm* comm, int32_t n_src, const kv_layout* const
  * When wire and pool share the dtype (the narrowing case this exists for), kv_pull_staged
  * is ONE persistent launch (k_pull_rows): warps take items chunk after chunk from a
  * shared counter, wait in-kernel for each chunk's ready words, and the warp completing a
- * chunk frees its slots -- no per-chunk launch gap.  It needs `counters`, a caller-owned
- * DEVICE scratch of >= 2 x (number of chunks) uint32 that the call zeroes on its stream
+ * chunk frees its slots, strictly in chunk order (a free value v means every chunk below v
+ * has been read) -- no per-chunk launch gap.  It needs `counters`, a caller-owned DEVICE
+ * scratch of >= 2 x (number of chunks) + 1 uint32 that the call zeroes on its stream
  * (NULL: one kv_wait / kv_unpack / kv_signal launch triple per chunk instead).
  * kv_stage with peer_scales != NULL computes dynamic fp8 scales (NEXT-1 i, kv_compute_scales
- * semantics) chunk by chunk from the P rank's data into dst[i]'s own scale array (which must
- * be writable DEVICE memory on P's GPU; the pack quantises with it) and copies each chunk's
- * scales to peer_scales[i] (D rank i's scale array, peer-mapped) before the ready flag, so D
- * holds the codes and the scales that decode them.  Requires a non-fp8 source and the P
- * rank to hold all of dst[i]'s heads (tp_p <= tp_d); NULL: dst[i]'s static scales are used.
+ * semantics) chunk by chunk from the P rank's data, for the D heads this P rank holds, into
+ * dst[i]'s own scale array (writable DEVICE memory on P's GPU; the pack quantises with it)
+ * and stores the same values into peer_scales[i] (on D rank i, peer-mapped) before the ready
+ * flag, so D holds the codes and the scales that decode them.  In a TP merge each P rank
+ * writes only its own heads' entries.  peer_scales[i] is the scale array of THIS BATCH: codes
+ * quantised with per-batch scales decode only with them, so a D pool that keeps requests of
+ * several batches keeps one such [L][2][H/tp_d] array per batch (with its requests), not one
+ * per pool, and a new batch's array must not be one D still decodes an older batch with.
+ * Requires a non-fp8 source and fp8 destinations; NULL: dst[i]'s static scales are used.
  * The caller advances seq0 by the number of chunks per call.  All three validate before
  * enqueueing; a wait that times out sets *err = 1 (device int32 on the waiting GPU) and the
- * stream goes on (the data are then undefined).  Waiter and signaller must be different
- * GPUs (kv_wait). */
+ * stream goes on (the data are then undefined).  P and D may share a GPU (kv_wait); cap the
+ * persistent kernel with kv_set_sm_budget there so P's packs find SMs. */
 kv_status kv_pull(int32_t n_src, const kv_layout* const* src, const void* const* src_pools, const kv_batch* src_bt,
                   const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt, const uint32_t* const* ready_flags,
                   uint32_t* const* done_flags, uint32_t epoch, int32_t layer_begin, int32_t layer_end,
@@ -377,13 +424,55 @@ kv_status kv_peer_enable(int32_t peer_device);
 
 /* A11 completion.  kv_signal: after all prior work on `stream`, a system-scope release
  * store of `value` to *flag (local or peer-mapped 4-byte device word).  kv_wait: enqueue
- * a one-warp kernel that spins (acquire, system scope) until *flag >= value or timeout_ns
- * elapses; on timeout it sets *err = 1 (device int32) and returns.  Do not place a kv_wait
- * and the kv_signal it waits for on the same GPU. */
+ * a one-warp kernel that spins (acquire, system scope) until *flag >= value (in the
+ * wrap-around order (int32_t)(*flag - value) >= 0) or timeout_ns elapses; on timeout it sets
+ * *err = 1 (device int32) and returns, so a lost signal never hangs the stream.  Waiter and
+ * signaller may share a GPU when they are on different streams: the waiting kernel holds one
+ * warp, and the persistent kv_pull_staged kernel holds at most kv_set_sm_budget SMs' worth of
+ * CTAs, so the work that leads to the signal always finds free SMs
+ * (tests/test_gpu_transport.py runs the whole data plane that way on one GPU). */
 kv_status kv_signal(uint32_t* flag, uint32_t value, kv_stream stream);
 kv_status kv_wait(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, int32_t* err, kv_stream stream);
 
+/* ---- K6 diagnostics: full-size conservation check (not on the data path) --------------
+ * SURVEY 8(d) "full size via the on-device coordinate-hash verify"; SPEC S:272 (every valid
+ * element lands exactly once, tail slots are zero, nothing else changes).  Both calls are
+ * element-wise with their own index math, independent of the convert kernels.
+ * kv_verify_fill: writes into every VALID element (t < T_r) of P rank `src`'s pool a value
+ *   drawn from a counter-based hash of (request id, token, global layer, K/V, global head,
+ *   dim) and `seed`, chosen so the cast to the destination dtype is exact: same dtype =
+ *   random finite bits; between fp16 / bf16 / fp32 = a value all of them represent; to e4m3
+ *   / e4m3fnuz = a random finite code k and the source value k x s, s the destination's
+ *   scale, which must be a power of two (else *err = 1, device int32).  dst[n_dst]: the D
+ *   layouts (with their scales, on this GPU) of every D rank holding a head of `src`.
+ *   req_ids: DEVICE int32 [n_req] request ids the hash uses (NULL: the batch index) -- a P
+ *   instance holding a subset of a D batch's requests passes their ids in the D batch.
+ *   Tail slots are left as they are.
+ * kv_verify_check: for EVERY element of D rank `dst`'s pool, compares what must be there
+ *   after a transfer of such a fill: the hashed value's code for valid tokens, 0 for tail
+ *   slots of each request's last block, `canary` (byte pattern) in every block the batch does
+ *   not use.  result: DEVICE uint64 [8]: [0] valid-element mismatches, [1] tail mismatches,
+ *   [2] canary mismatches, [3] valid elements checked, [4] pool element offset + 1 of one
+ *   mismatch (0: none); zeroed on the stream first.  scratch: DEVICE >= num_blocks bytes.
+ * KV_EUNSUPPORTED for fp8 sources, K-only / V-only or x-split pools, or shapes beyond the
+ * hash key (> 65535 requests, > 2^20 tokens, > 255 layers, > 511 heads, head_dim > 1023). */
+kv_status kv_verify_fill(const kv_layout* src, void* src_pool, const kv_batch* src_bt, int32_t n_dst,
+                         const kv_layout* const* dst, const int32_t* req_ids, uint64_t seed, int32_t* err,
+                         kv_stream stream);
+kv_status kv_verify_check(const kv_layout* src, const kv_layout* dst, const void* dst_pool, const kv_batch* dst_bt,
+                          const int32_t* req_ids, uint64_t seed, uint8_t canary, uint8_t* scratch,
+                          size_t scratch_bytes, unsigned long long* result, kv_stream stream);
+
 /* ---- misc ------------------------------------------------------------------------- */
+
+/* Load every kernel of the library on the current device now.  Under CUDA lazy loading (the
+ * CUDA 12 default) a kernel is loaded at its first launch and loading may wait for kernels
+ * already running in the process; a spin-wait (kv_wait, the persistent kv_pull_staged
+ * kernel) that needs a not-yet-loaded kernel of the SAME process to run (P and D on one
+ * GPU) would then end only by its timeout.  kv_wait, kv_signal and the persistent pull call
+ * this once per device themselves; kernels of other libraries (e.g. torch's) that must run
+ * while a wait spins should have run once before.  KV_ECUDA on failure. */
+kv_status kv_preload(void);
 
 /* Cap the SMs the data-path kernels this process launches afterwards on the CURRENT
  * device may occupy (0 = all; the grid is min(work, n_sms x occupancy)).  NVLink pushes saturate the link with

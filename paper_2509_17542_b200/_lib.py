@@ -51,6 +51,12 @@ class WireInfo(C.Structure):
                 ("payload_bytes", C.c_uint64), ("n_tokens", C.POINTER(C.c_int32))]
 
 
+class CtrlInfo(C.Structure):
+    _fields_ = [("desc", LayoutDesc), ("batch_id", C.c_uint32), ("has_tables", C.c_int32),
+                ("scales", C.POINTER(C.c_float)), ("n_scales", C.c_int64), ("n_req", C.c_int32),
+                ("n_tokens", C.POINTER(C.c_int32)), ("n_ids", C.c_int64), ("block_ids", C.POINTER(C.c_int32))]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
@@ -65,6 +71,9 @@ def _load():
         "kv_batch_bytes": (C.c_size_t, [i32, i64, i64]),
         "kv_block_table_update": (st, [p, i32, p, p, i64, p, C.c_size_t, C.POINTER(Batch_t), p]),
         "kv_plan_pairs": (i32, [i32, i32, i32, C.POINTER(i32), i32]),
+        "kv_ctrl_msg_bytes": (C.c_size_t, [i32, i64, i64]),
+        "kv_ctrl_msg_write": (st, [p, p, C.c_uint32, i32, p, p, i64, p, C.c_size_t, C.POINTER(C.c_size_t)]),
+        "kv_ctrl_msg_parse": (st, [p, C.c_size_t, C.POINTER(CtrlInfo)]),
         "kv_convert_reshard": (st, [i32, pp, pp, C.POINTER(Batch_t), i32, pp, pp, C.POINTER(Batch_t), i32, i32, p]),
         "kv_compute_scales": (st, [i32, pp, pp, C.POINTER(Batch_t), p, p, i32, i32, p]),
         "kv_convert_share": (st, [p, p, C.POINTER(Batch_t), i32, pp, pp, C.POINTER(Batch_t), i32, i32, p]),
@@ -104,6 +113,9 @@ def _load():
         "kv_signal": (st, [p, C.c_uint32, p]),
         "kv_wait": (st, [p, C.c_uint32, u64, p, p]),
         "kv_launch_count": (u64, []),
+        "kv_preload": (st, []),
+        "kv_verify_fill": (st, [p, p, C.POINTER(Batch_t), i32, pp, p, u64, p, p]),
+        "kv_verify_check": (st, [p, p, p, C.POINTER(Batch_t), p, u64, C.c_uint8, p, C.c_size_t, p, p]),
         "kv_set_sm_budget": (i32, [i32]),
         "kv_launch_count_reset": (None, []),
         "kv_last_error": (C.c_char_p, []),
@@ -121,12 +133,13 @@ lib = _load()
 
 # Every symbol include/kvx.h declares (checked by tests/test_abi.py).
 EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_block_table_update", "kv_plan_pairs",
+           "kv_ctrl_msg_bytes", "kv_ctrl_msg_write", "kv_ctrl_msg_parse",
            "kv_convert_reshard", "kv_convert_share", "kv_compute_scales", "kv_wire_dtype", "kv_wire_header_bytes",
            "kv_wire_header_write", "kv_wire_header_parse", "kv_wire_header_check", "kv_copy_bytes", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
            "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
            "kv_recv_unpack", "kv_push", "kv_send_pipelined", "kv_recv_pipelined", "kv_pull", "kv_stage",
            "kv_pull_staged", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",
-           "kv_launch_count", "kv_launch_count_reset", "kv_set_sm_budget", "kv_last_error", "kv_last_kernel", "kv_version")
+           "kv_launch_count", "kv_preload", "kv_verify_fill", "kv_verify_check", "kv_launch_count_reset", "kv_set_sm_budget", "kv_last_error", "kv_last_kernel", "kv_version")
 
 
 def check(status):

@@ -716,9 +716,16 @@ kv_status kv_convert_share(const kv_layout* src, const void* src_pool, const kv_
   return convert_impl(1, s1, p1, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, true);
 }
 
-kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
-                            const kv_batch* src_bt, const kv_layout* dst, float* out_scales, int32_t lb, int32_t le,
-                            kv_stream stream) {
+}  // extern "C"
+
+namespace kvx {
+// kv_compute_scales, optionally restricted to the D heads one source rank holds (share:
+// n_src == 1; the dynamic-scale staged pull of a TP merge, where every P rank owns the
+// scales of its own heads) and optionally storing the finished scales a second time into
+// `peer` (D's array, peer-mapped) -- see kv_stage.
+kv_status compute_scales_impl(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                              const kv_batch* src_bt, const kv_layout* dst, float* out_scales, int32_t lb, int32_t le,
+                              kv_stream stream, bool share, float* peer) {
   if (n_src < 1 || n_src > KVX_MAX_RANKS || !src || !src_pools || !dst || !out_scales)
     return fail(KV_EINVAL, "kv_compute_scales: bad argument");
   for (int i = 0; i < n_src; ++i)
@@ -747,9 +754,19 @@ kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const vo
     a.sscale[i] = src[i]->d.scales;
   }
   const int32_t Hp = S->h_local, Hd = dst->h_local, q = dst->d.tp_rank;
-  for (int32_t h = q * Hd; h < (q + 1) * Hd; ++h)
+  int32_t h0 = q * Hd, h1 = (q + 1) * Hd;
+  if (share) {
+    if (n_src != 1) return fail(KV_EINVAL, "kv_compute_scales: a share has one source");
+    h0 = std::max(h0, S->d.tp_rank * Hp);
+    h1 = std::min(h1, (S->d.tp_rank + 1) * Hp);
+    if (h1 <= h0) return fail(KV_ESHAPE, "kv_compute_scales: the source rank holds none of the D rank's heads");
+  }
+  for (int32_t h = h0; h < h1; ++h)
     if (a.src_of_p[h / Hp] < 0)
       return fail(KV_ESHAPE, "kv_compute_scales: missing source shard for P rank " + std::to_string(h / Hp));
+  a.hq0 = h0 - q * Hd;
+  a.nhq = h1 - h0;
+  a.peer = peer;
   for (int ax = 0; ax < 6; ++ax) a.ss[ax] = S->stride[ax];
   a.Hp = Hp;
   a.Hd = Hd;
@@ -768,10 +785,10 @@ kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const vo
   a.n_tok = (uint32_t)src_bt->total_tokens;
   const uint32_t ntg = (a.n_tok + 31u) / 32u;
   a.f_tg = make_fastdiv(std::max<uint32_t>(ntg, 1));
-  a.f_hd = make_fastdiv((uint32_t)Hd);
+  a.f_hd = make_fastdiv((uint32_t)a.nhq);
   a.f_bp = make_fastdiv((uint32_t)S->d.block_size);
   a.f_hp = make_fastdiv((uint32_t)Hp);
-  const uint64_t items = (uint64_t)ntg * Hd * (a.kv1 ? 1 : 2) * (uint64_t)(le - lb);
+  const uint64_t items = (uint64_t)ntg * a.nhq * (a.kv1 ? 1 : 2) * (uint64_t)(le - lb);
   if (items > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_compute_scales: batch too large for one call");
   a.n_items = (uint32_t)items;
   // row path: head_dim innermost with 16-B rows and aligned pools (every source)
@@ -784,6 +801,15 @@ kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const vo
   cudaError_t e = launch_amax(a, S->d.dtype, out_scales, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kv_compute_scales: launch");
   return KV_OK;
+}
+}  // namespace kvx
+
+extern "C" {
+
+kv_status kv_compute_scales(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                            const kv_batch* src_bt, const kv_layout* dst, float* out_scales, int32_t lb, int32_t le,
+                            kv_stream stream) {
+  return compute_scales_impl(n_src, src, src_pools, src_bt, dst, out_scales, lb, le, stream, false, nullptr);
 }
 
 int32_t kv_wire_dtype(const kv_layout* s, const kv_layout* d) {
@@ -986,6 +1012,7 @@ kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void*
                          (uint64_t)nh;
   if (items > kMaxChunks) return KV_OK;
   a.spin_ns = 128u;
+  if (kv_status pst = ensure_preloaded(); pst != KV_OK) return pst;
   t_last_kernel = "k_pull_rows";
   cudaError_t e = launch_pull_rows(a, d->d.dtype, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kv_pull_staged: launch");

@@ -26,6 +26,23 @@ kv_status nccl_fail(ncclResult_t r, const char* what) {
 }
 }  // namespace
 
+namespace kvx {
+// kv_preload once per device (a CUDA context loads modules per device)
+kv_status ensure_preloaded() {
+  static std::mutex mu;
+  static bool done[kMaxDevices] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_preload: device");
+  if (dev < 0 || dev >= kMaxDevices) return fail(KV_EINVAL, "kv_preload: device index out of range");
+  std::lock_guard<std::mutex> g(mu);
+  if (done[dev]) return KV_OK;
+  if ((e = preload_kernels()) != cudaSuccess) return cuda_fail(e, "kv_preload: kernel attributes");
+  done[dev] = true;
+  return KV_OK;
+}
+}  // namespace kvx
+
 extern "C" {
 
 kv_status kv_comm_unique_id(uint8_t out_id[128]) {
@@ -186,14 +203,20 @@ kv_status kv_peer_enable(int32_t peer_device) {
   return e == cudaSuccess ? KV_OK : cuda_fail(e, "cudaDeviceEnablePeerAccess");
 }
 
+kv_status kv_preload(void) { return ensure_preloaded(); }
+
 kv_status kv_signal(uint32_t* flag, uint32_t value, kv_stream stream) {
   if (!flag) return fail(KV_EINVAL, "kv_signal: null flag");
+  kv_status st = ensure_preloaded();
+  if (st != KV_OK) return st;
   cudaError_t e = launch_signal(flag, value, (cudaStream_t)stream);
   return e == cudaSuccess ? KV_OK : cuda_fail(e, "kv_signal: launch");
 }
 
 kv_status kv_wait(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, int32_t* err, kv_stream stream) {
   if (!flag || !err) return fail(KV_EINVAL, "kv_wait: null argument");
+  kv_status st = ensure_preloaded();  // nothing may need loading while this kernel spins
+  if (st != KV_OK) return st;
   cudaError_t e = launch_wait(flag, value, timeout_ns, err, (cudaStream_t)stream);
   return e == cudaSuccess ? KV_OK : cuda_fail(e, "kv_wait: launch");
 }

@@ -168,7 +168,8 @@ struct PullArgs {
   const uint32_t* ready[KVX_MAX_RANKS];               // local words P writes
   uint32_t* freef[KVX_MAX_RANKS];                     // peer words in P's memory
   int32_t hb[KVX_MAX_RANKS];                          // first global head of each overlap
-  uint32_t* counters;                                 // [nchunks] warps done, zero on entry
+  uint32_t* counters;                                 // [2 * nchunks] handed out / done, zero on entry
+  uint32_t* watermark;                                // counters[2 * nchunks]: chunks released in order
   int32_t* err;
   uint64_t timeout_ns;
   uint32_t spin_ns;  // back-off between polls
@@ -200,6 +201,8 @@ struct AmaxArgs {
   const int32_t* tok_off;
   const int32_t* tok_req;
   uint32_t* amax_bits;  // [L][2][Hd] float bits (non-negative floats order like uints)
+  float* peer;          // optional second copy of the finished scales (D's array, peer-mapped)
+  int32_t hq0, nhq;     // D-local heads [hq0, hq0 + nhq) computed (a P rank's share); f_hd = nhq
   float qmax;           // largest finite value of the destination fp8 (448 e4m3fn, 240 e4m3fnuz)
   FastDiv f_tg, f_hd, f_bp, f_hp;
   uint32_t n_tok, n_items;
@@ -219,6 +222,12 @@ kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void*
 // dt: the (common) wire / pool dtype; vec-8 row machinery only
 cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s);
 cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out_scales, cudaStream_t s);
+cudaError_t preload_kernels();         // every data-path kernel (kvx_kernels.cu)
+cudaError_t preload_verify_kernels();  // K6 (kvx_verify.cu)
+kv_status ensure_preloaded();          // once per device, before the first spin-wait
+kv_status compute_scales_impl(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                              const kv_batch* src_bt, const kv_layout* dst, float* out_scales, int32_t lb, int32_t le,
+                              kv_stream stream, bool share, float* peer);
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s);
 // k_convert_tr: a side with (DIM, SLOT) innermost (a.s_tr / a.d_tr), items in a.n_items
 cudaError_t launch_convert_tr(const ConvArgs& a, int sdt, int ddt, cudaStream_t s);

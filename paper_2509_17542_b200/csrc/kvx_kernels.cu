@@ -1482,16 +1482,26 @@ __global__ void __launch_bounds__(kThreads) k_pull_rows(const __grid_constant__ 
         }
         stream_rows<DT, DT, U, 8, true>(lane, cs, sp, dp, 1.f, rz);
       }
-      // the warp that completes chunk k releases its ring slot to every source
+      // the warp that completes chunk k releases its ring slot to every source -- strictly
+      // in chunk order: P reads free >= v as "every chunk below v has been read", so chunk k
+      // is released only after chunk k-1 (watermark == k).  The chunk k-1 items still in
+      // flight belong to warps that grabbed them, i.e. are resident and need nothing more.
       __syncwarp();
       if (lane == 0) {
         __threadfence();
         const uint32_t cnt = end - base;
         if (atomicAdd(done + k, cnt) + cnt == n_k) {
+          uint32_t wm;
+          while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(wm) : "l"(a.watermark) : "memory");
+            if (wm == (uint32_t)k) break;
+            __nanosleep(64);
+          }
           __threadfence_system();
           for (int s = 0; s < a.nsrc; ++s)
             asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.freef[s]), "r"(a.seq0 + (uint32_t)k + 1u)
                          : "memory");
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.watermark), "r"((uint32_t)k + 1u) : "memory");
         }
       }
     }
@@ -1641,7 +1651,7 @@ __global__ void __launch_bounds__(kThreads) k_amax(const __grid_constant__ AmaxA
   for (uint32_t item = warp; item < a.n_items; item += nwarps) {
     uint32_t n = item;
     const uint32_t tg = divmod(n, a.f_tg);
-    const uint32_t hq = divmod(n, a.f_hd);
+    const uint32_t hq = (uint32_t)a.hq0 + divmod(n, a.f_hd);
     const uint32_t c = take_kv(n, a.kv1, a.c0);
     const int64_t layer = a.lb + (int64_t)n;
     const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
@@ -1696,7 +1706,7 @@ __global__ void __launch_bounds__(kThreads) k_amax_rows(const __grid_constant__ 
   for (uint32_t item = warp; item < a.n_row_items; item += nwarps) {
     uint32_t n = item;
     const uint32_t tgc = divmod(n, a.f_tgc);
-    const uint32_t hq = divmod(n, a.f_hd);
+    const uint32_t hq = (uint32_t)a.hq0 + divmod(n, a.f_hd);
     const uint32_t c = take_kv(n, a.kv1, a.c0);
     const int64_t layer = a.lb + (int64_t)n;
     const int64_t sl = layer - a.s_l0;
@@ -1742,22 +1752,27 @@ __global__ void __launch_bounds__(kThreads) k_amax_rows(const __grid_constant__ 
 }
 
 // entries [begin, end) of an [L][2][Hd] scale array; a K-only / V-only pass leaves the
-// other half untouched
-__device__ __forceinline__ bool amax_entry(int64_t i, int32_t Hd, int32_t kv1, int32_t c0) {
-  return !kv1 || (int32_t)((i / Hd) & 1) == c0;
+// other half untouched, a P rank's share ([hq0, hq0 + nhq)) the other heads
+__device__ __forceinline__ bool amax_entry(int64_t i, int32_t Hd, int32_t kv1, int32_t c0, int32_t hq0, int32_t nhq) {
+  const int32_t h = (int32_t)(i % Hd);
+  return (!kv1 || (int32_t)((i / Hd) & 1) == c0) && h >= hq0 && h < hq0 + nhq;
 }
-__global__ void k_amax_init(uint32_t* bits, int64_t begin, int64_t end, int32_t Hd, int32_t kv1, int32_t c0) {
+__global__ void k_amax_init(uint32_t* bits, int64_t begin, int64_t end, int32_t Hd, int32_t kv1, int32_t c0,
+                            int32_t hq0, int32_t nhq) {
   for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end; i += (int64_t)gridDim.x * blockDim.x)
-    if (amax_entry(i, Hd, kv1, c0)) bits[i] = 0u;
+    if (amax_entry(i, Hd, kv1, c0, hq0, nhq)) bits[i] = 0u;
 }
-// s = RN(amax / qmax), qmax = the destination fp8's largest finite value (448 / 240)
+// s = RN(amax / qmax), qmax = the destination fp8's largest finite value (448 / 240); with
+// `peer` the scale is also stored there (D's array over NVLink: the dynamic-scale pull)
 __global__ void k_amax_finalize(uint32_t* bits, int64_t begin, int64_t end, float qmax, int32_t Hd, int32_t kv1,
-                                int32_t c0) {
+                                int32_t c0, int32_t hq0, int32_t nhq, float* peer) {
   for (int64_t i = begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < end; i += (int64_t)gridDim.x * blockDim.x) {
-    if (!amax_entry(i, Hd, kv1, c0)) continue;
+    if (!amax_entry(i, Hd, kv1, c0, hq0, nhq)) continue;
     const float amax = __uint_as_float(bits[i]);
-    const float s = __fdiv_rn(amax, qmax);
-    reinterpret_cast<float*>(bits)[i] = s > 0.f ? s : 1.0f;
+    const float s0 = __fdiv_rn(amax, qmax);
+    const float s = s0 > 0.f ? s0 : 1.0f;
+    reinterpret_cast<float*>(bits)[i] = s;
+    if (peer) peer[i] = s;
   }
 }
 
@@ -2080,7 +2095,8 @@ cudaError_t pull_rows_t(PullArgs& a, cudaStream_t s) {
 
 cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s) {
   if (a.nchunks <= 0) return cudaSuccess;
-  cudaError_t e0 = cudaMemsetAsync(a.counters, 0, 2 * sizeof(uint32_t) * (size_t)a.nchunks, s);
+  a.watermark = a.counters + 2 * (size_t)a.nchunks;
+  cudaError_t e0 = cudaMemsetAsync(a.counters, 0, (2 * (size_t)a.nchunks + 1) * sizeof(uint32_t), s);
   if (e0 != cudaSuccess) return e0;
   a.cpr_shift = log2_pow2((uint32_t)(a.D / 8));
   uint32_t ts, th;
@@ -2108,12 +2124,13 @@ cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s) {
 cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) {
   const int64_t begin = (int64_t)(a.lb - a.d_l0) * 2 * a.Hd, end = (int64_t)(a.lb - a.d_l0 + a.Lc) * 2 * a.Hd;
   const int fin_grid = (int)std::min<int64_t>(1024, (end - begin + 255) / 256 + 1);
-  k_amax_init<<<fin_grid, 256, 0, s>>>(reinterpret_cast<uint32_t*>(out), begin, end, a.Hd, a.kv1, a.c0);
+  k_amax_init<<<fin_grid, 256, 0, s>>>(reinterpret_cast<uint32_t*>(out), begin, end, a.Hd, a.kv1, a.c0, a.hq0,
+                                       a.nhq);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   if (a.n_items && a.rows) {
     AmaxArgs b = a;
     b.f_tgc = make_fastdiv((a.f_tg.d + kAmaxG - 1) / kAmaxG);
-    b.n_row_items = b.f_tgc.d * (uint32_t)a.Hd * (a.kv1 ? 1u : 2u) * (uint32_t)a.Lc;
+    b.n_row_items = b.f_tgc.d * (uint32_t)a.nhq * (a.kv1 ? 1u : 2u) * (uint32_t)a.Lc;
     switch (sdt) {
       case KV_F16: k_amax_rows<KV_F16><<<grid_for_items(k_amax_rows<KV_F16>, b.n_row_items), kThreads, 0, s>>>(b); break;
       case KV_BF16: k_amax_rows<KV_BF16><<<grid_for_items(k_amax_rows<KV_BF16>, b.n_row_items), kThreads, 0, s>>>(b); break;
@@ -2141,7 +2158,7 @@ cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out, cudaStream_t s) 
     g_launches.fetch_add(1, std::memory_order_relaxed);
   }
   k_amax_finalize<<<fin_grid, 256, 0, s>>>(reinterpret_cast<uint32_t*>(out), begin, end, a.qmax, a.Hd, a.kv1,
-                                           a.c0);
+                                           a.c0, a.hq0, a.nhq, a.peer);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
 }
@@ -2175,6 +2192,73 @@ cudaError_t launch_wait(const uint32_t* flag, uint32_t value, uint64_t timeout_n
   k_wait<<<1, 32, 0, s>>>(flag, value, timeout_ns, err);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------------------------
+// Eager loading of every kernel (kv_preload).  Under CUDA lazy loading (the CUDA 12
+// default) a kernel is loaded at its first launch, and loading may wait for the kernels
+// already running in the context.  A spin-waiting kernel (k_wait, the persistent
+// k_pull_rows) whose release depends on a kernel launched for the first time afterwards in
+// the same process would then only end by its timeout (P and D on one GPU).  Asking for a
+// kernel's attributes loads it, so this walks every instantiation the launchers use.
+// ------------------------------------------------------------------------------------
+namespace {
+template <typename K>
+cudaError_t touch(K k) {
+  cudaFuncAttributes at;
+  return cudaFuncGetAttributes(&at, reinterpret_cast<const void*>(k));
+}
+#define KVX_TOUCH(...)                         \
+  do {                                         \
+    cudaError_t e_ = touch(__VA_ARGS__);       \
+    if (e_ != cudaSuccess) return e_;          \
+  } while (0)
+
+template <int SDT, int DDT>
+cudaError_t preload_pair() {
+  constexpr int U8 = unroll_for<SDT, 8>(), U1 = unroll_for<SDT, 1>();
+  KVX_TOUCH(k_convert_rows<SDT, DDT, U8>);
+  KVX_TOUCH(k_convert_rows<SDT, DDT, U8, 8, true>);
+  if constexpr (Tr<SDT>::B == 1 && Tr<DDT>::B <= 2) KVX_TOUCH(k_convert_rows<SDT, DDT, 4, 16>);
+  KVX_TOUCH(k_convert<1, SDT, DDT, U1>);
+  KVX_TOUCH(k_convert_tr<SDT, DDT>);
+  KVX_TOUCH(k_convert_tr8<SDT, DDT, false>);
+  if constexpr (Tr<SDT>::B == 2 && Tr<DDT>::B == 2) KVX_TOUCH(k_convert_tr8<SDT, DDT, true>);
+  KVX_TOUCH(k_pack_rows<SDT, DDT, U8>);
+  KVX_TOUCH(k_pack<1, SDT, DDT, U1>);
+  KVX_TOUCH(k_unpack_rows<SDT, DDT, U8>);
+  KVX_TOUCH(k_unpack<1, SDT, DDT, U1>);
+  return cudaSuccess;
+}
+template <int SDT>
+cudaError_t preload_src() {
+  cudaError_t e;
+  if ((e = preload_pair<SDT, KV_F16>()) != cudaSuccess) return e;
+  if ((e = preload_pair<SDT, KV_BF16>()) != cudaSuccess) return e;
+  if ((e = preload_pair<SDT, KV_F8E4M3>()) != cudaSuccess) return e;
+  if ((e = preload_pair<SDT, KV_F8E4M3FNUZ>()) != cudaSuccess) return e;
+  if ((e = preload_pair<SDT, KV_F32>()) != cudaSuccess) return e;
+  KVX_TOUCH(k_pull_rows<SDT, unroll_for<SDT, 8>()>);
+  KVX_TOUCH(k_amax<SDT>);
+  KVX_TOUCH(k_amax_rows<SDT>);
+  return cudaSuccess;
+}
+}  // namespace
+
+cudaError_t preload_kernels() {
+  cudaError_t e;
+  if ((e = preload_src<KV_F16>()) != cudaSuccess) return e;
+  if ((e = preload_src<KV_BF16>()) != cudaSuccess) return e;
+  if ((e = preload_src<KV_F8E4M3>()) != cudaSuccess) return e;
+  if ((e = preload_src<KV_F8E4M3FNUZ>()) != cudaSuccess) return e;
+  if ((e = preload_src<KV_F32>()) != cudaSuccess) return e;
+  KVX_TOUCH(k_tile_copy);
+  KVX_TOUCH(k_amax_init);
+  KVX_TOUCH(k_amax_finalize);
+  KVX_TOUCH(k_signal);
+  KVX_TOUCH(k_wait);
+  KVX_TOUCH(k_copy_bytes);
+  return preload_verify_kernels();
 }
 
 }  // namespace kvx

@@ -229,8 +229,8 @@ kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* s
                                "arrays and a peer scale array per D rank");
       const kv_layout* const S1[1] = {src};
       const void* const P1[1] = {src_pool};
-      if ((st = kv_compute_scales(1, S1, P1, src_bt, dst[i], const_cast<float*>(dst[i]->d.scales), lb, lb,
-                                  stream)) != KV_OK)
+      if ((st = compute_scales_impl(1, S1, P1, src_bt, dst[i], const_cast<float*>(dst[i]->d.scales), lb, lb, stream,
+                                    true, peer_scales[i])) != KV_OK)
         return st;
     }
   }
@@ -243,16 +243,16 @@ kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* s
           (st = kv_wait(free_flags[i], (uint32_t)(seq + 1 - ring_slots), timeout_ns, err, stream)) != KV_OK)
         return st;
       if (peer_scales) {
-        // NEXT-1 (i): this chunk's per-(layer, K/V, head) scales from the data (one read pass),
-        // into dst[i]'s own array (the pack quantises with it), then shipped to the D rank
-        // ahead of the ready flag (the codes are useless without them)
+        // NEXT-1 (i): this chunk's per-(layer, K/V, head) scales of the D heads this P rank
+        // holds, from its data (one read pass), into dst[i]'s own array (the pack quantises
+        // with it) and -- by the same finalize kernel -- into D's array over NVLink, ahead of
+        // the ready flag (the codes are useless without them).  In a TP merge every P rank
+        // writes only its own heads' entries, so the ranks never overwrite each other.
         const kv_layout* const S1[1] = {src};
         const void* const P1[1] = {src_pool};
         float* own = const_cast<float*>(dst[i]->d.scales);
-        if ((st = kv_compute_scales(1, S1, P1, src_bt, dst[i], own, l0, l1, stream)) != KV_OK) return st;
-        const size_t off = (size_t)(l0 - dst[i]->d.first_layer) * 2 * dst[i]->h_local;
-        const size_t n = (size_t)(l1 - l0) * 2 * dst[i]->h_local * sizeof(float);
-        if ((st = kv_copy_bytes(peer_scales[i] + off, own + off, n, stream)) != KV_OK) return st;
+        if ((st = compute_scales_impl(1, S1, P1, src_bt, dst[i], own, l0, l1, stream, true, peer_scales[i])) != KV_OK)
+          return st;
       }
       if ((st = kv_pack(src, src_pool, src_bt, dst[i], l0, l1, rings[(size_t)i * ring_slots + b], slot_bytes,
                         stream)) != KV_OK)

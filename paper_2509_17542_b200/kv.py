@@ -10,10 +10,10 @@ import ctypes as C
 from contextlib import contextmanager
 
 from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BYTES, KV_BF16, KV_F8E4M3, KV_F16,
-                   KV_F32, KV_F8E4M3FNUZ, Batch_t, KvError, LayoutDesc, check, lib)
+                   KV_F32, KV_F8E4M3FNUZ, Batch_t, CtrlInfo, KvError, LayoutDesc, check, lib)
 
-__all__ = ["Layout", "Batch", "convert_reshard", "convert_share", "push", "pull", "stage", "pull_staged", "chunk_count", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
-           "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "launch_count", "launch_count_reset", "set_sm_budget", "last_kernel",
+__all__ = ["Layout", "Batch", "CtrlMsg", "ctrl_encode", "ctrl_decode", "convert_reshard", "convert_share", "push", "pull", "stage", "pull_staged", "chunk_count", "pull_counter_words", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
+           "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "preload", "verify_fill", "verify_check", "launch_count", "launch_count_reset", "set_sm_budget", "last_kernel",
            "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "KV_F8E4M3FNUZ", "DTYPE_BYTES",
            "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
 
@@ -125,6 +125,85 @@ class Batch:
         return self.bt.total_blocks
 
 
+class CtrlMsg:
+    """A parsed kv_ctrl message (A3 control plane): a TP rank's layout descriptor, its fp8
+    scales (host numpy [L][2][H/tp] or None) and a batch's block tables (or None)."""
+
+    def __init__(self, desc: dict, scales, n_tokens, tables, batch_id):
+        self.desc, self.scales, self.n_tokens, self.tables, self.batch_id = desc, scales, n_tokens, tables, batch_id
+
+    def layout(self, device="cuda"):
+        """kv_layout_describe of the received descriptor, its scales uploaded to `device`."""
+        import torch
+        sc = None
+        if self.scales is not None:
+            sc = torch.from_numpy(self.scales.reshape(-1).copy()).to(device)
+        d = self.desc
+        return Layout(d["L"], d["H"], d["D"], d["tp"], d["rank"], d["B"], d["NB"], d["dtype"], d["order"], sc,
+                      d["first_layer"], d["kv_part"], d["dim_split"])
+
+    def batch(self, layout, device="cuda", stream=None):
+        """kv_block_table_update of the received tables against `layout` (the sender's)."""
+        if self.tables is None:
+            raise KvError(1, "control message carries no block tables")
+        return Batch(layout, self.n_tokens, self.tables, device, stream)
+
+
+def ctrl_encode(layout: Layout, scales=None, n_tokens=None, tables=None, batch_id=0) -> bytes:
+    """kv_ctrl_msg_write: serialise layout (+ host scales) (+ block tables) for the control plane."""
+    import numpy as np
+    sc = None
+    if scales is not None:
+        if hasattr(scales, "detach"):
+            scales = scales.detach().cpu().numpy()
+        sc = np.ascontiguousarray(np.asarray(scales, dtype=np.float32).reshape(-1))
+    if n_tokens is None:
+        n_req, nt, ids = -1, np.zeros(1, np.int32), np.zeros(1, np.int32)
+        n_ids = 0
+    else:
+        n_req = len(n_tokens)
+        nt = np.ascontiguousarray(np.asarray(n_tokens, dtype=np.int32).reshape(-1)) if n_req else np.zeros(1, np.int32)
+        ids = (np.concatenate([np.asarray(t, dtype=np.int32).reshape(-1) for t in tables]) if n_req
+               else np.zeros(0, np.int32))
+        n_ids = len(ids)
+        ids = np.ascontiguousarray(ids) if n_ids else np.zeros(1, np.int32)
+    need = lib.kv_ctrl_msg_bytes(max(n_req, 0), n_ids, 0 if sc is None else sc.size)
+    buf = np.zeros((need + 7) // 8, dtype=np.uint64)
+    written = C.c_size_t()
+    check(lib.kv_ctrl_msg_write(layout.handle, None if sc is None else sc.ctypes.data, batch_id, n_req,
+                                nt.ctypes.data, ids.ctypes.data, n_ids, buf.ctypes.data, need, C.byref(written)))
+    return buf.view(np.uint8)[:written.value].tobytes()
+
+
+def ctrl_decode(msg: bytes) -> CtrlMsg:
+    """kv_ctrl_msg_parse: validate a control message and copy its sections out."""
+    import numpy as np
+    raw = np.frombuffer(msg, dtype=np.uint8)
+    al = np.zeros((len(raw) + 7) // 8, dtype=np.uint64)   # 8-byte aligned copy
+    al.view(np.uint8)[:len(raw)] = raw
+    info = CtrlInfo()
+    check(lib.kv_ctrl_msg_parse(al.ctypes.data, len(raw), C.byref(info)))
+    d = info.desc
+    desc = dict(L=d.num_layers, first_layer=d.first_layer, H=d.num_kv_heads, D=d.head_dim, tp=d.tp_degree,
+                rank=d.tp_rank, B=d.block_size, NB=d.num_blocks, dtype=d.dtype, order=tuple(d.axis_order),
+                kv_part=d.kv_part, dim_split=d.dim_split)
+    scales = None
+    if info.n_scales:
+        scales = np.ctypeslib.as_array(info.scales, shape=(info.n_scales,)).copy().reshape(
+            d.num_layers, 2, d.num_kv_heads // d.tp_degree)
+    n_tokens = tables = None
+    if info.has_tables:
+        nt = np.ctypeslib.as_array(info.n_tokens, shape=(info.n_req,)).copy() if info.n_req else np.zeros(0, np.int32)
+        ids = np.ctypeslib.as_array(info.block_ids, shape=(info.n_ids,)).copy() if info.n_ids else np.zeros(0, np.int32)
+        n_tokens = [int(t) for t in nt]
+        tables, o = [], 0
+        for t in n_tokens:
+            k = -(-t // d.block_size)
+            tables.append(ids[o:o + k])
+            o += k
+    return CtrlMsg(desc, scales, n_tokens, tables, int(info.batch_id))
+
+
 def plan_pairs(tp_p, tp_d, num_kv_heads):
     """kv_plan_pairs: [(p, q, h_begin, h_end)] with non-empty head overlap (Fig. 4)."""
     buf = (C.c_int32 * (4 * 256))()
@@ -208,8 +287,13 @@ def pull_staged(src_layouts, rings, ring_slots, slot_bytes, dst_layout: Layout, 
                 counters=None):
     """kv_pull_staged: D side of a narrowing pull -- per layer chunk wait for every P
     rank's ready flag, unpack straight from its peer-mapped ring slot, free the slot.
-    counters (device uint32/int32 scratch, >= 2 * chunk_count words): one persistent launch."""
+    counters (device uint32/int32 scratch, >= pull_counter_words(...) words): one persistent launch."""
     ns = len(src_layouts)
+    if counters is not None and not isinstance(counters, int):
+        lr = layer_range if layer_range else _common(src_layouts[0], dst_layout)
+        need = pull_counter_words(lr, layer_chunk)
+        if counters.numel() * counters.element_size() < 4 * need:
+            raise KvError(2, f"pull_staged: counters hold {counters.numel()} words, need {need}")
     S = (C.c_void_p * ns)(*[l.handle.value for l in src_layouts])
     RG = (C.c_void_p * len(rings))(*[_ptr(r) for r in rings])
     RF = (C.c_void_p * ns)(*[_ptr(f) for f in ready_flags])
@@ -225,6 +309,11 @@ def chunk_count(layer_range, layer_chunk):
     lb, le = layer_range
     step = layer_chunk if layer_chunk > 0 else max(1, le - lb)
     return (le - lb + step - 1) // step
+
+
+def pull_counter_words(layer_range, layer_chunk):
+    """Device scratch words kv_pull_staged's persistent kernel needs: 2 per chunk + 1."""
+    return 2 * chunk_count(layer_range, layer_chunk) + 1
 
 
 def compute_scales(src_layouts, src_pools, src_batch: Batch, dst_layout: Layout, out, layer_range=None, stream=None):
@@ -365,6 +454,27 @@ def signal(flag, value, stream=None):
 
 def wait(flag, value, err, timeout_s=10.0, stream=None):
     check(lib.kv_wait(_ptr(flag), value, int(timeout_s * 1e9), _ptr(err), _stream(stream)))
+
+
+def preload():
+    """kv_preload: load every library kernel on the current device (see include/kvx.h)."""
+    check(lib.kv_preload())
+
+
+def verify_fill(src: Layout, src_pool, src_batch: Batch, dst_layouts, seed, err, req_ids=None, stream=None):
+    """kv_verify_fill (K6): hash-derived values, exact under the cast, in every valid element."""
+    nd = len(dst_layouts)
+    Dl = (C.c_void_p * nd)(*[l.handle.value for l in dst_layouts])
+    check(lib.kv_verify_fill(src.handle, _ptr(src_pool), C.byref(src_batch.bt), nd, Dl, _ptr(req_ids), int(seed),
+                             _ptr(err), _stream(stream)))
+
+
+def verify_check(src: Layout, dst: Layout, dst_pool, dst_batch: Batch, seed, result, scratch, canary=0xA5,
+                 req_ids=None, stream=None):
+    """kv_verify_check (K6): count mismatches of a whole D pool after a transfer of a K6 fill.
+    result: device int64[8] ([0] value, [1] tail, [2] canary mismatches, [3] checked)."""
+    check(lib.kv_verify_check(src.handle, dst.handle, _ptr(dst_pool), C.byref(dst_batch.bt), _ptr(req_ids),
+                              int(seed), canary, _ptr(scratch), scratch.numel(), _ptr(result), _stream(stream)))
 
 
 def launch_count():

@@ -7,7 +7,8 @@ exchange and the data-plane modes (bench.py default: pull).
   stores straight into the D rank's HBM across NVLink -- then ``signal``s the flag with a
   system-scope release.  The D rank ``wait``s (acquire) on its local flag.  The cast
   happens on the sender, so a narrowing cast halves the NVLink bytes (hard
-  part 2).  D keeps control of placement: its block table travels to P (A3).
+  part 2).  D keeps control of placement: its block table (and fp8 scales) travel to P
+  through the control plane (``ControlPlane``, A3).
 * ``pull`` (the paper's direction, "read(local, remote, location)"): each P rank
   exports its pool (same-width / widening cast) or a staging ring (narrowing cast) plus a
   flag array; each D rank maps them and reads across NVLink.  Without narrowing, D runs
@@ -73,6 +74,58 @@ def exchange(obj, group=None):
     out = [None] * dist.get_world_size(group)
     dist.all_gather_object(out, obj, group=group)
     return out
+
+
+class ControlPlane:
+    """A3: the control-plane exchange before a transfer ("control plane information
+    interaction"; P:125 D obtains P's "GPU ranks and parallel strategy").
+
+    Collective over the job (or ``group``).  Every P / D rank publishes one kv_ctrl message
+    (``kv.ctrl_encode``): its layout descriptor, its fp8 scales when its pool is fp8 (a D
+    rank's scales are what P's sender-side cast quantises with) and, if it passes them, the
+    batch's block tables its instance chose.  Afterwards every rank holds every other rank's
+    parsed message: ``layout(kind, r, device)`` rebuilds a peer's layout (scales uploaded to
+    this rank's GPU) and ``batch(kind, device)`` the peer instance's validated tables.  The
+    bytes travel through torch.distributed (object all-gather); nothing is regenerated from
+    seeds on the receiving side."""
+
+    def __init__(self, role: Role, layout=None, scales=None, n_tokens=None, tables=None, batch_id=0, group=None):
+        mine = None
+        if role.kind in ("P", "D") and layout is not None:
+            mine = {"kind": role.kind, "r": role.tp_rank,
+                    "msg": kv.ctrl_encode(layout, scales, n_tokens, tables, batch_id)}
+        allv = exchange(mine, group)
+        self.role = role
+        self.msgs = {(e["kind"], e["r"]): kv.ctrl_decode(e["msg"]) for e in allv if e is not None}
+        self.bytes_received = sum(len(e["msg"]) for e in allv if e is not None)
+
+    def ranks(self, kind):
+        return sorted(r for k, r in self.msgs if k == kind)
+
+    def message(self, kind, r):
+        return self.msgs[(kind, r)]
+
+    def layout(self, kind, r, device="cuda"):
+        """kv_layout_describe of rank r of instance `kind` (its scales on `device`)."""
+        return self.msgs[(kind, r)].layout(device)
+
+    def tables(self, kind):
+        """(n_tokens, tables) the instance published; every rank of it must agree (one block
+        table per instance, shared by its TP ranks)."""
+        got = [(m.n_tokens, m.tables) for (k, _), m in sorted(self.msgs.items()) if k == kind and m.tables is not None]
+        if not got:
+            raise ValueError(f"no {kind} rank published block tables")
+        nt0, tb0 = got[0]
+        for nt, tb in got[1:]:
+            if nt != nt0 or len(tb) != len(tb0) or any(list(a) != list(b) for a, b in zip(tb, tb0)):
+                raise ValueError(f"{kind} ranks published different block tables")
+        return nt0, tb0
+
+    def batch(self, kind, layout, device="cuda", stream=None):
+        """kv_block_table_update of instance `kind`'s published tables against `layout` (a
+        layout of that instance: block size and pool capacity are validated)."""
+        nt, tb = self.tables(kind)
+        return kv.Batch(layout, nt, tb, device, stream)
 
 
 class PushChannel:

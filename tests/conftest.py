@@ -3,6 +3,12 @@ import sys
 
 import pytest
 
+# One hardware work queue per CUDA stream: the one-GPU transport tests run P and D on
+# separate streams of the same device, with spin-waits between them; with the default 8
+# connections two streams can share a queue, and a wait at its head would block the other
+# stream's work behind it (a false dependency).  Set before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)

@@ -151,7 +151,7 @@ def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent, dyn=False):
         else:
             src = [kvx.ipc_open(h, o) for h, o in other["src"]]
             maps += [(a, o) for a, (h, o) in zip(src, other["src"])]
-        counters = {qq: torch.zeros(2 * L, dtype=torch.int32, device=dev) for qq in range(len(D))}
+        counters = {qq: torch.zeros(2 * L + 1, dtype=torch.int32, device=dev) for qq in range(len(D))}
         for qq in range(len(D)):
             ps = [pp for pp, q2, _, _ in pairs if q2 == qq]
             st = streams[qq] = torch.cuda.Stream()
@@ -170,8 +170,9 @@ def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent, dyn=False):
         assert kvx.last_kernel() == ("k_pull_rows" if persistent else "k_unpack_rows" if staged else kvx.last_kernel())
         if persistent:   # every chunk handed out and completed in full
             for c in counters.values():
-                nxt, done = c[:L].cpu(), c[L:].cpu()
+                nxt, done = c[:L].cpu(), c[L:2 * L].cpu()
                 assert bool((done > 0).all()) and bool((nxt >= done).all())
+                assert int(c[2 * L]) == L   # every chunk released, in order
         res = [a.copy() for a in dc.dst_numpy()]
         if dyn:
             res = (res, [lay.scales.cpu().numpy().reshape(L, 2, -1) for lay in D])

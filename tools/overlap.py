@@ -72,7 +72,7 @@ def main():
         free = torch.zeros(4, dtype=torch.int32, device="cuda:0")
         err0 = torch.zeros(1, dtype=torch.int32, device="cuda:0")
         err1 = torch.zeros(1, dtype=torch.int32, device="cuda:1")
-        counters = torch.zeros(2 * L, dtype=torch.int32, device="cuda:1")
+        counters = torch.zeros(2 * L + 1, dtype=torch.int32, device="cuda:1")
         seq = [0]
 
     def timed(fn):

@@ -52,7 +52,7 @@ def main():
     free = torch.zeros(8, dtype=torch.int32, device="cuda:0")
     err0 = torch.zeros(1, dtype=torch.int32, device="cuda:0")
     err1 = torch.zeros(1, dtype=torch.int32, device="cuda:1")
-    counters = torch.zeros(2 * nch, dtype=torch.int32, device="cuda:1")
+    counters = torch.zeros(2 * nch + 1, dtype=torch.int32, device="cuda:1")
     s0, s1 = torch.cuda.Stream(0), torch.cuda.Stream(1)
     seq = [0]
     nvl = src.src_bytes([0]) * synth.NBYTES[cfg.dst_dtype] // synth.NBYTES[cfg.src_dtype]
