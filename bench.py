@@ -2,23 +2,30 @@
 """bench.py -- KV transfer GB/s and ms/request (P -> D, device-timed) vs the HBM/NVLink
 roofline, for the heterogeneous-compatible KV transmission path (arXiv 2509.17542, III-B).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode push|nccl]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode pull|push|nccl]
 
-N = 1 (default): BASELINE configs[1] (c2: Llama-2-7B KV, one 2048-token prompt, P TP=2 -> D TP=1,
-  fp16, block 16 -> 16, P layout NHD-per-layer -> D layout block-major HND) with all three
-  ranks' pools on one GPU: one fused kv_convert_reshard launch per step, HBM-bound.
-N >= 2 (torchrun, one process per GPU): BASELINE configs[3] (c4: Llama-3-70B GQA KV,
-  32 x 4096 tokens, P TP=4 -> D TP=4, bf16 -> fp8-e4m3 per-head scale) as N/2 independent
-  (P rank p -> D rank p) pairs on disjoint GPUs (P = ranks 0..N/2-1): N=8 is the full c4,
-  N=2/4 its per-GPU-equivalent sub-configs; per-pair work fixed -> weak
-  scaling.  `--workload c3|c2` runs the largest complete sub-transfer that fits (c3 at N=4:
-  P0,P1 -> D0, fan-in 2; N=6 the full c3); `--workload c5` the mixed-length stream.
-  Default mode "push": the fused gather+convert kernel stores into the D rank's
-  IPC-mapped pool over NVLink, then a release flag (K4/K5); "nccl": pack -> ncclSend /
-  ncclRecv -> unpack, per-layer pipelined.
+N = 1 (default): BASELINE configs[3], the north-star workload (c4: Llama-3-70B GQA KV, 32 x
+  4096 tokens, P TP=4 -> D TP=4, bf16 -> fp8-e4m3 with per-head scales, block 16 -> 16, P
+  layout NHD-per-layer -> D layout block-major HND), which fits one B200: all four P ranks'
+  and all four D ranks' pools (71 GB) on cuda:0, one fused kv_convert_reshard launch per step
+  (42.9 GB read + 21.5 GB written), HBM-bound.  `--workload c1|c2|c3` for the others.
+N >= 2 (torchrun, one process per GPU): c4 as (P rank p -> D rank p) pairs on disjoint GPUs
+  (P = ranks 0..N/2-1): N = 8 is the full c4, N = 2 / 4 its per-GPU-equivalent sub-configs
+  (SURVEY 8(d)); per-pair work is fixed -> weak scaling.  `--workload c3|c2` runs the largest
+  complete sub-transfer that fits (transfer.present_ranks); `--workload c5` the mixed-length
+  stream.  Default mode "pull" (the paper's D-initiated read): D reads P's pool, or P's
+  staging ring when the cast narrows, across NVLink; "push": P's fused kernel stores into D's
+  pool; "nccl": pack -> ncclSend / ncclRecv -> unpack, per-layer pipelined.
+  Before the transfer the ranks exchange layouts, block tables and fp8 scales through the
+  control plane (transfer.ControlPlane, A3): each instance chooses its own tables; nothing is
+  regenerated from the other side's seeds.
 
-One JSON line on rank 0 (contract in the task statement); `value` = logical source KV
-GB (2*L*H*D*T*bytes_src summed over all requests and pairs) / max-over-ranks device time.
+Verification on the measured buffers: the oracle O1 on a sample (N = 1: all of c1 / c2 / c3',
+requests {first, last} of c4), and K6 (kv_verify_fill / kv_verify_check) over every element
+of every D pool after one more transfer of a hash-coded fill.
+
+One JSON line on rank 0 (contract in the task statement); `value` = logical source KV GB
+(2*L*H*D*T*bytes_src over all requests and present P ranks) / max-over-ranks device time.
 Inputs are larger than L2 (GBs per step), so no L2 flush is needed.
 """
 from __future__ import annotations
@@ -38,24 +45,24 @@ import numpy as np  # noqa: E402
 
 import synth  # noqa: E402
 
-METRIC = "KV transfer GB/s and ms/request (P\u2192D, device-timed) vs HBM/NVLink roofline"  # BASELINE.json verbatim
-NVLINK_MEASURED_GBS = 770.0   # B200_PROFILING.md: measured peer copy per direction
-NVLINK_NOMINAL_GBS = 900.0
+METRIC = "KV transfer GB/s and ms/request (P→D, device-timed) vs HBM/NVLink roofline"  # BASELINE.json verbatim
+NVLINK_NOMINAL_GBS = 900.0    # north_star: 900 GB/s per direction (the roofline denominator)
+K6_SEED = 0x6B36
 
 
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default="pull", choices=["push", "pull", "nccl"])
     ap.add_argument("--ring-slots", type=int, default=3, help="pull mode, narrowing cast: staging ring depth")
     ap.add_argument("--dynamic-scales", action="store_true",
                     help="pull mode, fp8 destination: P computes per-chunk amax scales and ships them (NEXT-1 i)")
-    ap.add_argument("--layer-chunk", type=int, default=0, help="layers per chunk (0 = whole model)")
+    ap.add_argument("--layer-chunk", type=int, default=0, help="layers per chunk (0 = whole model / auto)")
     ap.add_argument("--chunk-mib", type=int, default=64, help="c5: merge layers until a chunk moves this much")
-    ap.add_argument("--c5-batch", action="store_true", help="c5: push each instance's requests as one batch")
+    ap.add_argument("--c5-batch", action="store_true", help="c5 push: each instance's requests as one batch")
     ap.add_argument("--requests", type=int, default=0,
                     help="use only the first N requests of the workload (e.g. 1: batch-1 latency of c3/c4)")
     ap.add_argument("--workload", default=None, help="override: c1..c5")
@@ -65,6 +72,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--no-verify", action="store_true", help="skip the K6 full-size check")
+    ap.add_argument("--no-nvlink-probe", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=0)
     return ap.parse_args()
 
@@ -74,8 +83,19 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json hbm_gbs)"}
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 # ------------------------------------------------------------------------------------
@@ -133,66 +153,55 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------
-# workload construction (inputs from synth; device memory from torch)
+# inputs (synth: seeded, no method arithmetic; device memory from torch)
 # ------------------------------------------------------------------------------------
-class Workload:
-    """One instance pair's layouts, pools, tables for the P ranks / D ranks on this process."""
+def p_tables(cfg, NB_p, contiguous=False):
+    """The P instance's block tables (P's allocator; D learns them through the control plane)."""
+    return synth.block_tables(cfg.seed + 1, cfg.n_tokens, cfg.B_p, NB_p, contiguous)
 
-    def __init__(self, cfg, p_ranks, d_ranks, device, contiguous=False):
-        import torch
-        import paper_2509_17542_b200 as kvx
-        self.cfg, self.device = cfg, device
-        c = cfg
-        self.NB_p = synth.pool_capacity(c.n_tokens, c.B_p)
-        self.NB_d = synth.pool_capacity(c.n_tokens, c.B_d)
-        self.src_tables = synth.block_tables(c.seed + 1, c.n_tokens, c.B_p, self.NB_p, contiguous)
-        self.dst_tables = synth.block_tables(c.seed + 2, c.n_tokens, c.B_d, self.NB_d, contiguous)
-        self.p_ranks, self.d_ranks = list(p_ranks), list(d_ranks)
-        self.src_dicts, self.src_lays, self.src_pools = {}, {}, {}
-        for p in self.p_ranks:
-            d = synth.layout(c.L, c.H, c.D, c.tp_p, p, c.B_p, self.NB_p, c.src_dtype, c.p_order)
-            lay = kvx.Layout.from_dict(d)
-            pool = lay.new_pool(device)
-            view = pool.view(torch.uint8 if synth.NBYTES[c.src_dtype] == 1 else torch.int16)
-            synth.fill_random_finite_(view, c.seed + 100 + p, c.src_dtype)
-            self.src_dicts[p], self.src_lays[p], self.src_pools[p] = d, lay, pool
-        self.dst_dicts, self.dst_lays, self.dst_pools, self.scales = {}, {}, {}, {}
-        for q in self.d_ranks:
-            sc_np = None
-            sc = None
-            if c.dst_dtype == synth.E4M3:
-                sc_np = synth.pow2_scales(c.seed + 200 + q, c.L, c.H // c.tp_d)
-                sc = torch.from_numpy(sc_np).to(device)
-            d = synth.layout(c.L, c.H, c.D, c.tp_d, q, c.B_d, self.NB_d, c.dst_dtype, c.d_order, sc_np)
-            lay = kvx.Layout.from_dict(d, sc)
-            self.dst_dicts[q], self.dst_lays[q], self.scales[q] = d, lay, sc
-            self.dst_pools[q] = lay.new_pool(device, fill=synth.CANARY)
-        any_src = self.src_lays[self.p_ranks[0]] if self.p_ranks else kvx.Layout.from_dict(
-            synth.layout(c.L, c.H, c.D, c.tp_p, 0, c.B_p, self.NB_p, c.src_dtype, c.p_order))
-        any_dst = self.dst_lays[self.d_ranks[0]] if self.d_ranks else kvx.Layout.from_dict(
-            synth.layout(c.L, c.H, c.D, c.tp_d, 0, c.B_d, self.NB_d, c.dst_dtype, c.d_order,
-                         np.ones((c.L, 2, c.H // c.tp_d), np.float32)),
-            torch.ones(c.L * 2 * (c.H // c.tp_d), device=device))
-        self._keep = (any_src, any_dst)
-        self.src_bt = kvx.Batch(any_src, c.n_tokens, self.src_tables, device)
-        self.dst_bt = kvx.Batch(any_dst, c.n_tokens, self.dst_tables, device)
 
-    # algorithmic bytes (SURVEY 8(d)): what the method must move
-    def src_bytes(self, p_ranks=None):
-        c = self.cfg
-        n = len(p_ranks) if p_ranks is not None else c.tp_p
-        return 2 * c.L * (c.H // c.tp_p) * n * c.D * c.total_tokens * synth.NBYTES[c.src_dtype]
+def d_tables(cfg, NB_d, contiguous=False):
+    """The D instance's block tables (D picks its blocks; P learns them through the control plane)."""
+    return synth.block_tables(cfg.seed + 2, cfg.n_tokens, cfg.B_d, NB_d, contiguous)
 
-    def dst_bytes(self, d_ranks=None):
-        c = self.cfg
-        n = len(d_ranks) if d_ranks is not None else c.tp_d
-        padded = sum(synth.blocks_for(t, c.B_d) * c.B_d for t in c.n_tokens)
-        return 2 * c.L * (c.H // c.tp_d) * n * c.D * padded * synth.NBYTES[c.dst_dtype]
+
+def make_p_rank(cfg, p, NB_p, dev):
+    import torch
+    import paper_2509_17542_b200 as kvx
+    d = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, NB_p, cfg.src_dtype, cfg.p_order)
+    lay = kvx.Layout.from_dict(d)
+    pool = lay.new_pool(dev)
+    synth.fill_random_finite_(pool.view(torch.uint8 if synth.NBYTES[cfg.src_dtype] == 1 else torch.int16),
+                              cfg.seed + 100 + p, cfg.src_dtype)
+    return d, lay, pool
+
+
+def make_d_rank(cfg, q, NB_d, dev):
+    import torch
+    import paper_2509_17542_b200 as kvx
+    sc_np = sc = None
+    if cfg.dst_dtype in synth.FP8:
+        sc_np = synth.pow2_scales(cfg.seed + 200 + q, cfg.L, cfg.H // cfg.tp_d)
+        sc = torch.from_numpy(sc_np.reshape(-1).copy()).to(dev)
+    d = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, NB_d, cfg.dst_dtype, cfg.d_order, sc_np)
+    lay = kvx.Layout.from_dict(d, sc)
+    return d, lay, lay.new_pool(dev, fill=synth.CANARY), sc
+
+
+def src_bytes(cfg, n_p=None):
+    n = cfg.tp_p if n_p is None else n_p
+    return 2 * cfg.L * (cfg.H // cfg.tp_p) * n * cfg.D * cfg.total_tokens * synth.NBYTES[cfg.src_dtype]
+
+
+def dst_bytes(cfg, n_d=None):
+    n = cfg.tp_d if n_d is None else n_d
+    padded = sum(synth.blocks_for(t, cfg.B_d) * cfg.B_d for t in cfg.n_tokens)
+    return 2 * cfg.L * (cfg.H // cfg.tp_d) * n * cfg.D * padded * synth.NBYTES[cfg.dst_dtype]
 
 
 def extract(pool_t, d, layers, block_ids):
-    """Compact host copy of a pool restricted to layers [lb, le) and the given blocks
-    (same axis order) -> (numpy codes, layout dict).  Bench/test infrastructure."""
+    """Compact host copy of a pool restricted to layers [lb, le) and the given blocks (same
+    axis order) -> (numpy codes, layout dict).  Bench infrastructure (oracle input)."""
     import torch
     nb = synth.NBYTES[d["dtype"]]
     tdt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[nb]
@@ -206,46 +215,64 @@ def extract(pool_t, d, layers, block_ids):
     nd = dict(d)
     nd["L"], nd["NB"] = layers[1] - layers[0], len(block_ids)
     if d.get("scales") is not None:
-        nd["scales"] = np.asarray(d["scales"])[layers[0]:layers[1]]
+        nd["scales"] = np.asarray(d["scales"]).reshape(d["L"], 2, -1)[layers[0]:layers[1]]
     return a, nd
 
 
-def sample_parity(w: Workload, layers, req, p_ranks, d_ranks, dst_pool_of=None):
-    """Oracle check of the measured buffers on a sample: request `req`, layers [lb, le),
-    the given ranks.  Returns (ok, detail)."""
+def sample_of(pool_t, d, tables, reqs, layers):
+    """extract() of the blocks of requests `reqs` (in order) -> (codes, layout dict, local tables)."""
+    ids = [b for r in reqs for b in tables[r]]
+    a, nd = extract(pool_t, d, layers, ids)
+    loc, k = [], 0
+    for r in reqs:
+        loc.append(list(range(k, k + len(tables[r]))))
+        k += len(tables[r])
+    return a, nd, loc
+
+
+def o1_compare(src_samples, dst_samples, n_tokens, dst_dtype, threads=1):
+    """O1 over sampled sources -> expected sampled D pools; compare with the device's.
+    src_samples / dst_samples: [(codes, layout dict, local tables)].  threads > 1 splits the
+    layers over host threads (ctypes releases the GIL)."""
+    from concurrent.futures import ThreadPoolExecutor
     from oracle import o1
-    dst_pool_of = dst_pool_of or (lambda q: w.dst_pools[q])
-    c = w.cfg
-    st, dt = w.src_tables[req], w.dst_tables[req]
-    src_lays, src_pools = [], []
-    for p in p_ranks:
-        a, nd = extract(w.src_pools[p], w.src_dicts[p], layers, st)
-        src_lays.append(nd)
-        src_pools.append(a)
-    dst_lays, dst_pools, got = [], [], []
-    for q in d_ranks:
-        g, nd = extract(dst_pool_of(q), w.dst_dicts[q], layers, dt)
-        dst_lays.append(nd)
-        got.append(g)
-        dst_pools.append(np.full_like(g, 0).view(np.uint8).copy().view(g.dtype))
-        dst_pools[-1][:] = np.frombuffer(bytes([synth.CANARY]) * g.nbytes, dtype=g.dtype)
-    o1.convert(src_lays, src_pools, dst_lays, dst_pools, [c.n_tokens[req]], [list(range(len(st)))],
-               [list(range(len(dt)))])
-    bad = 0
-    maxulp = 0
-    for g, want in zip(got, dst_pools):
-        if c.dst_dtype == synth.E4M3:
+    o1.lib()
+    L = dst_samples[0][1]["L"]
+    want = []
+    for g, nd, _ in dst_samples:
+        w = np.frombuffer(bytes([synth.CANARY]) * g.nbytes, dtype=g.dtype).copy()
+        want.append(w)
+    args = ([s[1] for s in src_samples], [s[0] for s in src_samples], [s[1] for s in dst_samples], want, n_tokens,
+            src_samples[0][2], dst_samples[0][2])
+    t0 = time.perf_counter()
+    ranges = [(i * L // threads, (i + 1) * L // threads) for i in range(threads)]
+    ranges = [r for r in ranges if r[1] > r[0]]
+    if len(ranges) <= 1:
+        o1.convert(*args)
+    else:
+        with ThreadPoolExecutor(len(ranges)) as ex:
+            list(ex.map(lambda lr: o1.convert(*args, lr), ranges))
+    t_o1 = time.perf_counter() - t0
+    bad = exact = n = maxulp = 0
+    for (g, _, _), w in zip(dst_samples, want):
+        n += g.size
+        if dst_dtype == synth.E4M3:
             def ordv(x):
                 x = x.astype(np.int32)
                 return np.where(x & 0x80, -(x & 0x7F), x & 0x7F)
-            dd = np.abs(ordv(g) - ordv(want))
+            nan_w, nan_g = (w & 0x7F) == 0x7F, (g & 0x7F) == 0x7F
+            dd = np.abs(ordv(g) - ordv(w))
+            dd[nan_w & nan_g] = 0
+            dd[nan_w != nan_g] = 99
             maxulp = max(maxulp, int(dd.max(initial=0)))
             bad += int((dd > 1).sum())
+            exact += int((g == w).sum())
         else:
-            bad += int((g != want).sum())
-    n = sum(g.size for g in got)
-    return bad == 0, {"elements": int(n), "mismatches": bad, "max_e4m3_ulp": maxulp if c.dst_dtype == synth.E4M3 else None,
-                      "sample": f"request {req}, layers [{layers[0]},{layers[1]}), P ranks {list(p_ranks)} -> D ranks {list(d_ranks)}"}
+            bad += int((g != w).sum())
+            exact += int((g == w).sum())
+    return {"ok": bad == 0, "elements": int(n), "mismatches": int(bad), "bit_exact": int(exact),
+            "max_e4m3_ulp": maxulp if dst_dtype == synth.E4M3 else None, "o1_seconds": round(t_o1, 2),
+            "o1_threads": threads}
 
 
 def cpu_baseline(cfg, layers, p_ranks, d_ranks, req=0, threads=1):
@@ -276,22 +303,68 @@ def cpu_baseline(cfg, layers, p_ranks, d_ranks, req=0, threads=1):
     return nbytes, dt
 
 
+def _subset(cfg, args):
+    """--requests N: the first N requests of the configuration (batch-1 latency runs);
+    --tokens T: one request of T tokens (the paper's input lengths, P:231-277: 256 / 512 /
+    1024); --tp-p / --tp-d: other TP degrees on the same model (context points)."""
+    import dataclasses
+    if getattr(args, "requests", 0):
+        cfg = dataclasses.replace(cfg, n_tokens=cfg.n_tokens[:args.requests])
+    if getattr(args, "tokens", 0):
+        cfg = dataclasses.replace(cfg, n_tokens=[args.tokens])
+    if getattr(args, "tp_p", 0):
+        cfg = dataclasses.replace(cfg, tp_p=args.tp_p)
+    if getattr(args, "tp_d", 0):
+        cfg = dataclasses.replace(cfg, tp_d=args.tp_d)
+    return cfg
+
+
+def _overrides(args):
+    o = {k: getattr(args, k) for k in ("requests", "tokens", "tp_p", "tp_d") if getattr(args, k, 0)}
+    return o or None
+
+
+def _dtype_name(cfg):
+    a, b = synth.DTYPE_NAMES[cfg.src_dtype], synth.DTYPE_NAMES[cfg.dst_dtype]
+    return a if a == b else f"{a}->{b}"
+
+
+def _traffic(key):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture
+    (profiles/traffic.json: "<workload>@1" single GPU, "<workload>:<mode>" NVLink modes)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get(key)
+    return None
+
+
+def _pinned_copy(dev_tensor):
+    """Pinned host copy of a device tensor without a pageable intermediate (GB-sized pools)."""
+    import torch
+    h = torch.empty(dev_tensor.numel(), dtype=dev_tensor.dtype, pin_memory=True)
+    h.copy_(dev_tensor.view(-1))
+    return h
+
+
 # ------------------------------------------------------------------------------------
-# N = 1: c2 on one GPU (HBM-bound fused convert)
+# N = 1: the whole transfer on one GPU (HBM-bound fused convert)
 # ------------------------------------------------------------------------------------
 def run_single(args):
     import torch
     import paper_2509_17542_b200 as kvx
     torch.cuda.set_device(0)
-    cfgs = synth.configs()
-    wl_name = args.workload or "c2"
-    cfg = _subset(cfgs[wl_name], args)
+    wl_name = args.workload or "c4"
+    cfg = _subset(synth.configs()[wl_name], args)
     dev = torch.device("cuda", 0)
-    w = Workload(cfg, range(cfg.tp_p), range(cfg.tp_d), dev)
-    S = [w.src_lays[p] for p in w.p_ranks]
-    SP = [w.src_pools[p] for p in w.p_ranks]
-    Dl = [w.dst_lays[q] for q in w.d_ranks]
-    DP = [w.dst_pools[q] for q in w.d_ranks]
+    NB_p, NB_d = synth.pool_capacity(cfg.n_tokens, cfg.B_p), synth.pool_capacity(cfg.n_tokens, cfg.B_d)
+    P = [make_p_rank(cfg, p, NB_p, dev) for p in range(cfg.tp_p)]
+    Dr = [make_d_rank(cfg, q, NB_d, dev) for q in range(cfg.tp_d)]
+    pt, dt_ = p_tables(cfg, NB_p), d_tables(cfg, NB_d)
+    S, SP = [x[1] for x in P], [x[2] for x in P]
+    Dl, DP = [x[1] for x in Dr], [x[2] for x in Dr]
+    src_bt = kvx.Batch(S[0], cfg.n_tokens, pt, dev)
+    dst_bt = kvx.Batch(Dl[0], cfg.n_tokens, dt_, dev)
     stream = torch.cuda.current_stream()
     lc = args.layer_chunk or cfg.L
 
@@ -299,7 +372,7 @@ def run_single(args):
         for l0 in range(0, cfg.L, lc):
             if ev is not None:
                 ev[0].record(stream)
-            kvx.convert_reshard(S, SP, w.src_bt, Dl, DP, w.dst_bt, (l0, min(cfg.L, l0 + lc)), stream)
+            kvx.convert_reshard(S, SP, src_bt, Dl, DP, dst_bt, (l0, min(cfg.L, l0 + lc)), stream)
             if ev is not None:
                 ev[1].record(stream)
 
@@ -320,150 +393,183 @@ def run_single(args):
     torch.cuda.synchronize()
     launches = kvx.launch_count()
     clk = clocks.stop()
-    total_ms = t0.elapsed_time(t1)
-    ms = total_ms / K
-    src_b, dst_b = w.src_bytes(), w.dst_bytes()
+    kernel = kvx.last_kernel()
+    ms = t0.elapsed_time(t1) / K
+    sb, db = src_bytes(cfg), dst_bytes(cfg)
     kts = [a.elapsed_time(b) for a, b in kev] if lc == cfg.L else [ms]
     kern_ms = statistics.mean(kts)
     peaks = load_peaks()
-    alg = src_b + dst_b  # HBM read + write per launch
+    alg = sb + db  # HBM read + write per launch
     achieved = alg / (kern_ms * 1e-3) / 1e9
     out = {
-        "metric": METRIC, "value": round(src_b / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
+        "metric": METRIC, "value": round(sb / (ms * 1e-3) / 1e9, 2), "unit": "GB/s",
         "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 5),
         "ms_per_request": round(ms / len(cfg.n_tokens), 5),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype_name(cfg),
-        "data": "synthetic (seeded random finite bit patterns, Fisher-Yates block tables)",
-        "config": {"workload": f"{wl_name} one GPU: {cfg.note}; all P and D ranks' pools on cuda:0",
+        "data": "synthetic (seeded random finite bit patterns, Fisher-Yates block tables, power-of-two fp8 scales)",
+        "config": {"workload": f"{wl_name} on one GPU: {cfg.note}; all {cfg.tp_p} P and {cfg.tp_d} D ranks' pools on "
+                               f"cuda:0, one fused convert per step",
                    "requests": len(cfg.n_tokens), "tokens": cfg.total_tokens, "overrides": _overrides(args),
                    "layout": "P (L,KV,BLK,SLOT,H,D) -> D (BLK,L,KV,H,SLOT,D)",
-                   "src_bytes_per_step": src_b, "dst_bytes_per_step": dst_b,
+                   "src_bytes_per_step": sb, "dst_bytes_per_step": db,
                    "l2": "inputs larger than L2 (no flush)", "parallelism": "none (1 GPU)"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": _traffic(f"{wl_name}@1"),
-                     "kernel": kvx.last_kernel(), "kernel_ms": round(kern_ms, 5),
+                     "kernel": kernel, "kernel_ms": round(kern_ms, 5),
                      "kernel_ms_median": round(statistics.median(kts), 5), "kernel_ms_min": round(min(kts), 5),
                      "algorithmic_bytes_per_launch": alg, "peak_source": peaks["source"],
                      "frac_vs_nominal_8TBs": round(achieved / 8000.0, 4)},
         "clocks": clk, "gpu_launches": int(launches),
     }
     if not args.no_parity:
-        ok, det = sample_parity(w, (0, min(2, cfg.L)), 0, w.p_ranks, w.d_ranks)
-        out["parity"] = {"ok": ok, **det}
+        # O1 on the measured buffers: every request when the whole batch is small (c1, c2,
+        # c3), else the first and the last request -- all layers, all ranks
+        ncores = len(os.sched_getaffinity(0))
+        reqs = list(range(len(cfg.n_tokens))) if sb <= (3 << 30) else sorted({0, len(cfg.n_tokens) - 1})
+        ss = [sample_of(SP[p], P[p][0], pt, reqs, (0, cfg.L)) for p in range(cfg.tp_p)]
+        ds = [sample_of(DP[q], Dr[q][0], dt_, reqs, (0, cfg.L)) for q in range(cfg.tp_d)]
+        res = o1_compare(ss, ds, [cfg.n_tokens[r] for r in reqs], cfg.dst_dtype, threads=min(ncores, cfg.L))
+        res["sample"] = (f"requests {reqs} of {len(cfg.n_tokens)} (all layers, all ranks) vs O1" if len(reqs) <
+                         len(cfg.n_tokens) else f"all {len(reqs)} request(s), all layers, all ranks vs O1")
+        out["parity"] = res
+    if not args.no_verify:
+        out["fullsize"] = k6_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, step)
     if not args.no_e2e:
-        out["e2e"] = e2e_single(w, S, Dl, min(K, 10), stream, src_b)
+        out["e2e"] = e2e_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, min(K, 3), stream, sb)
     if not args.no_cpu_baseline:
-        nl = args.cpu_sample_layers or min(cfg.L, 12)
-        nb, dt = cpu_baseline(cfg, nl, w.p_ranks, w.d_ranks)
+        nl = args.cpu_sample_layers or min(cfg.L, 8 if cfg.H * cfg.D * cfg.n_tokens[0] > (1 << 21) else 12)
+        nb, dt = cpu_baseline(cfg, nl, range(cfg.tp_p), range(cfg.tp_d))
         out["cpu_baseline"] = {"value": round(nb / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+                               "cpu": cpu_model(),
                                "sample": f"O1 (plain C, 1 thread) on {wl_name} request 0, layers [0,{nl}) of {cfg.L}, "
-                                         f"{nb} source bytes in {dt:.2f} s"}
+                                         f"all ranks, {nb} source bytes in {dt:.2f} s"}
         ncores = len(os.sched_getaffinity(0))
         nl_mt = min(cfg.L, max(nl, 2 * ncores))
-        nb2, dt2 = cpu_baseline(cfg, nl_mt, w.p_ranks, w.d_ranks, threads=ncores)
+        nb2, dt2 = cpu_baseline(cfg, nl_mt, range(cfg.tp_p), range(cfg.tp_d), threads=ncores)
         out["cpu_baseline_threads"] = {"value": round(nb2 / dt2 / 1e9, 4), "unit": "GB/s", "cores": ncores,
-                                       "kind": "oracle",
+                                       "kind": "oracle", "cpu": cpu_model(),
                                        "sample": f"same O1 split by layer over {ncores} threads, layers [0,{nl_mt}), "
                                                  f"{nb2} source bytes in {dt2:.2f} s"}
     print(json.dumps(out), flush=True)
 
 
-def e2e_single(w, S, Dl, K, stream, src_b):
-    """Same metric through the public API with HOST buffers: every step uploads its source
-    pools from pinned memory, runs the convert call and reads the destination pool back,
-    all inside the timed region.  Steps are software-pipelined over two device buffer sets
-    and three streams (upload, convert, read-back), so step k+1's upload and step k's
-    read-back share the full-duplex PCIe link while step k converts."""
+def k6_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, step):
+    """K6: hash-coded fill of every P pool, one more transfer, every element of every D pool
+    checked (SURVEY 8(d) full-size verification; SPEC S:272 conservation)."""
     import torch
     import paper_2509_17542_b200 as kvx
-    hs = [_pinned_copy(w.src_pools[p]) for p in w.p_ranks]
-    hd = [torch.empty(w.dst_pools[q].numel(), dtype=torch.uint8, pin_memory=True) for q in w.d_ranks]
-    SP = [[w.src_pools[p] for p in w.p_ranks], [torch.empty_like(w.src_pools[p]) for p in w.p_ranks]]
-    DP = [[w.dst_pools[q] for q in w.d_ranks], [w.dst_pools[q].clone() for q in w.d_ranks]]
+    if cfg.src_dtype in synth.FP8:
+        return {"ok": None, "note": "K6 does not cover fp8 sources"}
+    dev = SP[0].device
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    for lay, pool in zip(S, SP):
+        kvx.verify_fill(lay, pool, src_bt, Dl, K6_SEED, err)
+    step()
+    tot = [0] * 4
+    for lay, pool in zip(Dl, DP):
+        res = torch.zeros(8, dtype=torch.int64, device=dev)
+        scratch = torch.empty(lay.num_blocks, dtype=torch.uint8, device=dev)
+        kvx.verify_check(S[0], lay, pool, dst_bt, K6_SEED, res, scratch)
+        r = [int(x) for x in res.cpu()]
+        tot = [a + b for a, b in zip(tot, r[:4])]
+    ok = int(err.item()) == 0 and tot[0] == tot[1] == tot[2] == 0
+    return {"ok": ok, "elements_checked": tot[3], "value_mismatches": tot[0], "tail_mismatches": tot[1],
+            "canary_mismatches": tot[2], "fill_error": int(err.item()),
+            "what": "K6: hash-coded fill of every valid P element, one more transfer, every element of every D pool "
+                    "(valid = hash code, tail = 0, unused blocks = canary)"}
+
+
+def e2e_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, K, stream, sb):
+    """Same metric through the public API with HOST buffers: every step uploads the P pools
+    from pinned memory and reads the D pools back, inside the timed region.  The upload is
+    split by layer chunks (the P pools are layer-major, so a chunk is contiguous) on a copy
+    stream, so chunk k+1 crosses PCIe while chunk k converts; the D pools are read back once
+    the step's last chunk has converted."""
+    import torch
+    import paper_2509_17542_b200 as kvx
+    hs = [_pinned_copy(p) for p in SP]
+    hd = [torch.empty(p.numel(), dtype=torch.uint8, pin_memory=True) for p in DP]
+    lay_major = cfg.p_order[0] == synth.LAYER
+    n_ch = 8 if lay_major else 1
+    bounds = [(i * cfg.L // n_ch, (i + 1) * cfg.L // n_ch) for i in range(n_ch)]
+    per_layer = [p.numel() // cfg.L for p in SP]
     up, down = torch.cuda.Stream(), torch.cuda.Stream()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     up.wait_stream(stream)
     down.wait_stream(stream)
-    read_done = [None, None]
-    for k in range(K):
-        b = k & 1
-        if read_done[b] is not None:          # the set's previous read-back must be done
-            up.wait_event(read_done[b])
-        with torch.cuda.stream(up):
-            for d, h in zip(SP[b], hs):
-                d.copy_(h, non_blocking=True)
-        ev_up = torch.cuda.Event()
-        ev_up.record(up)
-        stream.wait_event(ev_up)
-        kvx.convert_reshard(S, SP[b], w.src_bt, Dl, DP[b], w.dst_bt, None, stream)
-        ev_cv = torch.cuda.Event()
-        ev_cv.record(stream)
-        down.wait_event(ev_cv)
+    for _ in range(K):
+        up.wait_stream(stream)            # the previous step's converts are done reading
+        for l0, l1 in bounds:
+            with torch.cuda.stream(up):
+                for d, h, pl in zip(SP, hs, per_layer):
+                    a, b = (l0 * pl, l1 * pl) if lay_major else (0, d.numel())
+                    d[a:b].copy_(h[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(up)
+            stream.wait_event(ev)
+            stream.wait_stream(down)      # the previous read-back is done with the D pools
+            kvx.convert_reshard(S, SP, src_bt, Dl, DP, dst_bt, (l0, l1), stream)
+        down.wait_stream(stream)
         with torch.cuda.stream(down):
-            for d, h in zip(DP[b], hd):
+            for d, h in zip(DP, hd):
                 h.copy_(d, non_blocking=True)
-        read_done[b] = torch.cuda.Event()
-        read_done[b].record(down)
     stream.wait_stream(down)
     stream.wait_stream(up)
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / K
-    return {"value": round(src_b / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 3),
+    return {"value": round(sb / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 3),
             "h2d_bytes_per_step": int(sum(h.numel() for h in hs)), "d2h_bytes_per_step": int(sum(h.numel() for h in hd)),
-            "steps": K, "pipelined": "2 buffer sets; upload / convert / read-back streams"}
+            "steps": K, "pipelined": f"{len(bounds)} layer chunks uploaded ahead of their convert; D pools read back "
+                                     "after the step (whole pools: the ~10% free-block slack crosses PCIe too)"}
 
 
-def _pinned_copy(dev_tensor):
-    """Pinned host copy of a device tensor without a pageable intermediate (GB-sized pools)."""
+# ------------------------------------------------------------------------------------
+# N >= 2: P -> D across NVLink
+# ------------------------------------------------------------------------------------
+def nvlink_probe(me, my_peer, dev, tr, kvx, barrier, nbytes=1 << 30):
+    """In-run NVLink ceiling: 1 GiB copy-engine copies between each P rank and
+    its first D peer, all pairs at once -- D reading P's buffer (the pull direction) and P
+    writing D's buffer (the push direction) -- plus an SM-driven peer read (kv_copy_bytes,
+    what the pull kernels do).  Returns GB/s per direction (median of 3, this rank)."""
     import torch
-    h = torch.empty(dev_tensor.numel(), dtype=dev_tensor.dtype, pin_memory=True)
-    h.copy_(dev_tensor.view(-1))
-    return h
+    buf = torch.empty(nbytes, dtype=torch.uint8, device=dev) if me.kind in "PD" else None
+    if buf is not None:
+        buf.fill_(1)
+    allx = tr.exchange({"kind": me.kind, "r": me.tp_rank, "h": kvx.ipc_export(buf) if buf is not None else None})
+    peer = None
+    if me.kind in "PD" and my_peer is not None:
+        other = "D" if me.kind == "P" else "P"
+        ent = [e for e in allx if e["kind"] == other and e["r"] == my_peer][0]
+        peer = (kvx.ipc_open(*ent["h"]), ent["h"][1])
+    s = torch.cuda.current_stream()
+    out = {}
+    for name, who, fn in (("ce_read", "D", lambda: kvx.memcpy_engine(buf, peer[0], nbytes, s)),
+                          ("ce_write", "P", lambda: kvx.memcpy_engine(peer[0], buf, nbytes, s)),
+                          ("sm_read", "D", lambda: kvx.copy_bytes(buf, peer[0], nbytes, s))):
+        ts = []
+        for i in range(4):
+            torch.cuda.synchronize()
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            if me.kind == who and peer is not None:
+                fn()
+            e1.record(s)
+            torch.cuda.synchronize()
+            if i:
+                ts.append(e0.elapsed_time(e1))
+        if me.kind == who and peer is not None:
+            out[name] = round(nbytes / (statistics.median(ts) * 1e-3) / 1e9, 1)
+    torch.cuda.synchronize()
+    barrier()
+    if peer is not None:
+        kvx.ipc_close(*peer)
+    return out
 
 
-def _subset(cfg, args):
-    """--requests N: the first N requests of the configuration (batch-1 latency runs);
-    --tokens T: one request of T tokens (the paper's input lengths, P:231-277: 256 / 512 /
-    1024); --tp-p / --tp-d: other TP degrees on the same model (context points)."""
-    import dataclasses
-    if getattr(args, "requests", 0):
-        cfg = dataclasses.replace(cfg, n_tokens=cfg.n_tokens[:args.requests])
-    if getattr(args, "tokens", 0):
-        cfg = dataclasses.replace(cfg, n_tokens=[args.tokens])
-    if getattr(args, "tp_p", 0):
-        cfg = dataclasses.replace(cfg, tp_p=args.tp_p)
-    if getattr(args, "tp_d", 0):
-        cfg = dataclasses.replace(cfg, tp_d=args.tp_d)
-    return cfg
-
-
-def _overrides(args):
-    """The workload overrides of this run (empty for the BASELINE configurations as named)."""
-    o = {k: getattr(args, k) for k in ("requests", "tokens", "tp_p", "tp_d") if getattr(args, k, 0)}
-    return o or None
-
-
-def _dtype_name(cfg):
-    a, b = synth.DTYPE_NAMES[cfg.src_dtype], synth.DTYPE_NAMES[cfg.dst_dtype]
-    return a if a == b else f"{a}->{b}"
-
-
-def _traffic(key):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture
-    (profiles/traffic.json: "c2@1" single GPU, "<workload>:<mode>" for the NVLink modes)."""
-    p = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            return json.load(f).get(key)
-    return None
-
-
-# ------------------------------------------------------------------------------------
-# N >= 2: c4 pairs across NVLink
-# ------------------------------------------------------------------------------------
 def run_multi(args):
     """N >= 2: a configuration's P -> D transfer across NVLink, P and D on disjoint GPUs.
     Ranks [0, n_p) are P TP ranks 0..n_p-1, [n_p, n_p + n_d) D TP ranks 0..n_d-1, the rest
@@ -489,37 +595,57 @@ def run_multi(args):
     pairs = tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks=set(range(n_p)), d_ranks=set(range(n_d)))
     my_q = sorted({q for p, q, _, _ in pairs if me.kind == "P" and p == me.tp_rank})
     my_p = sorted({p for p, q, _, _ in pairs if me.kind == "D" and q == me.tp_rank})
-    w = Workload(cfg, [me.tp_rank] if me.kind == "P" else [], [me.tp_rank] if me.kind == "D" else [], dev)
+    NB_p, NB_d = synth.pool_capacity(cfg.n_tokens, cfg.B_p), synth.pool_capacity(cfg.n_tokens, cfg.B_d)
     stream = torch.cuda.current_stream()
     barrier_t = torch.zeros(1, device=dev)
 
     def barrier():
         dist.all_reduce(barrier_t)
 
+    # ---- my side: only my instance's layout, pool, tables (and D's scales) ----
+    mine = {}
+    if me.kind == "P":
+        d, lay, pool = make_p_rank(cfg, me.tp_rank, NB_p, dev)
+        tabs = p_tables(cfg, NB_p)
+        mine = dict(d=d, lay=lay, pool=pool, tables=tabs, bt=kvx.Batch(lay, cfg.n_tokens, tabs, dev))
+        cp = tr.ControlPlane(me, lay, None, cfg.n_tokens, tabs, batch_id=1)
+    elif me.kind == "D":
+        d, lay, pool, sc = make_d_rank(cfg, me.tp_rank, NB_d, dev)
+        tabs = d_tables(cfg, NB_d)
+        mine = dict(d=d, lay=lay, pool=pool, tables=tabs, scales=sc, bt=kvx.Batch(lay, cfg.n_tokens, tabs, dev))
+        cp = tr.ControlPlane(me, lay, None if sc is None else sc.cpu().numpy(), cfg.n_tokens, tabs, batch_id=1)
+    else:
+        cp = tr.ControlPlane(me)
+    # ---- the peers, as the control plane delivered them ----
+    peer_lays, peer_bt = {}, None
+    if me.kind == "P":
+        peer_lays = {q: cp.layout("D", q, dev) for q in my_q}   # D's scales on P's GPU: the sender casts
+        peer_bt = cp.batch("D", peer_lays[my_q[0]], dev)
+    elif me.kind == "D":
+        peer_lays = {p: cp.layout("P", p, dev) for p in my_p}
+        peer_bt = cp.batch("P", peer_lays[my_p[0]], dev)
+    ctrl_info = {"bytes_received": cp.bytes_received, "messages": len(cp.msgs)}
+    nvl = {}
+    if not args.no_nvlink_probe:
+        peer_of = my_q[0] if me.kind == "P" else my_p[0] if me.kind == "D" else None
+        nvl = nvlink_probe(me, peer_of, dev, tr, kvx, barrier)
+
     flags = torch.zeros(max(n_p, 1), dtype=torch.int32, device=dev)  # one word per P source
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     epoch = [0]
     lc = args.layer_chunk or cfg.L
-
-    def d_view(q):  # P's view of D rank q's layout (D's fp8 scales on P's GPU: the sender casts)
-        sc = None
-        if cfg.dst_dtype == synth.E4M3:
-            sc = torch.from_numpy(synth.pow2_scales(cfg.seed + 200 + q, cfg.L, cfg.H // cfg.tp_d)).to(dev)
-        return kvx.Layout.from_dict(
-            synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, w.NB_d, cfg.dst_dtype, cfg.d_order), sc)
-
     dyn = False
+    S = mine.get("lay")
     if args.mode == "push":
-        ch = tr.PushChannel(me, w.dst_pools.get(me.tp_rank), flags if me.kind == "D" else None)
-        dst_lays = {q: d_view(q) for q in my_q}
+        ch = tr.PushChannel(me, mine.get("pool") if me.kind == "D" else None, flags if me.kind == "D" else None)
 
         def step(ev=None):
             epoch[0] += 1
             if me.kind == "P":
                 if ev is not None:
                     ev[0].record(stream)
-                tr.push_step(w.src_lays[me.tp_rank], w.src_pools[me.tp_rank], w.src_bt, dst_lays, ch.peer_pool,
-                             w.dst_bt, ch.peer_flag, epoch[0], lc, stream, flag_slot=me.tp_rank)
+                tr.push_step(S, mine["pool"], mine["bt"], peer_lays, ch.peer_pool, peer_bt, ch.peer_flag, epoch[0],
+                             lc, stream, flag_slot=me.tp_rank)
                 if ev is not None:
                     ev[1].record(stream)
             elif me.kind == "D":
@@ -528,46 +654,32 @@ def run_multi(args):
     elif args.mode == "pull":
         # D-initiated read: D maps P's pool (or P's staging ring when the cast narrows)
         narrowing = synth.NBYTES[cfg.dst_dtype] < synth.NBYTES[cfg.src_dtype]
-        p_lays = {p: kvx.Layout.from_dict(
-            synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, w.NB_p, cfg.src_dtype, cfg.p_order))
-            for p in my_p}
         R = max(1, args.ring_slots)
         if narrowing and not args.layer_chunk:
             # ~40 MiB of wire per chunk, at most 20 chunks (c4 full batch: 4 layers per chunk;
             # one request: 4 chunks of 20 layers), so the pipeline fill stays small and
-            # per-chunk launch costs on P stay hidden behind D's reads.  Batch-1 c4 pair
-            # (profiles/r01/batch1_chunks_c4_n2.jsonl): 2 / 4 / 8 / 16 chunks = 0.261 / 0.247 /
-            # 0.286 / 0.359 ms
+            # per-chunk launch costs on P stay hidden behind D's reads
+            # (profiles/r01/batch1_chunks_c4_n2.jsonl)
             pair_wire = 2 * cfg.L * min(cfg.H // cfg.tp_p, cfg.H // cfg.tp_d) * cfg.D * \
                 synth.NBYTES[cfg.dst_dtype] * cfg.total_tokens
             n_ch = min(20, max(1, round(pair_wire / (40 << 20))))
             lc = -(-cfg.L // n_ch)
-        ring, slot_bytes, dst_lays = None, 0, {}
+        ring, slot_bytes, ring_ptrs = None, 0, []
         dyn = args.dynamic_scales and narrowing and synth.NBYTES[cfg.src_dtype] > 1
-        own_scales = {}
-        if me.kind == "P":
-            if dyn:   # writable scale arrays on P: kv_stage fills them chunk by chunk
-                own_scales = {q: torch.ones(cfg.L * 2 * (cfg.H // cfg.tp_d), device=dev) for q in my_q}
-                dst_lays = {q: kvx.Layout.from_dict(
-                    synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, w.NB_d, cfg.dst_dtype, cfg.d_order),
-                    own_scales[q]) for q in my_q}
-            else:
-                dst_lays = {q: d_view(q) for q in my_q}
-            S = w.src_lays[me.tp_rank]
-            if narrowing:
-                slot_bytes = max(kvx.wire_bytes(S, dst_lays[q], cfg.total_tokens, (l0, min(cfg.L, l0 + lc)))
-                                 for q in my_q for l0 in range(0, cfg.L, lc))
-                slot_bytes = (slot_bytes + 255) // 256 * 256
-                ring = torch.empty(len(my_q) * R * slot_bytes, dtype=torch.uint8, device=dev)
-                ring_ptrs = [ring.data_ptr() + (i * R + b) * slot_bytes for i in range(len(my_q)) for b in range(R)]
+        if me.kind == "P" and narrowing:
+            slot_bytes = max(kvx.wire_bytes(S, peer_lays[q], cfg.total_tokens, (l0, min(cfg.L, l0 + lc)))
+                             for q in my_q for l0 in range(0, cfg.L, lc))
+            slot_bytes = (slot_bytes + 255) // 256 * 256
+            ring = torch.empty(len(my_q) * R * slot_bytes, dtype=torch.uint8, device=dev)
+            ring_ptrs = [ring.data_ptr() + (i * R + b) * slot_bytes for i in range(len(my_q)) for b in range(R)]
         pflags = torch.zeros(max(n_p, n_d, 1), dtype=torch.int32, device=dev)
-        pch = tr.PullChannel(me, pflags, pool=w.src_pools[me.tp_rank] if me.kind == "P" and not narrowing else None,
+        pch = tr.PullChannel(me, pflags, pool=mine["pool"] if me.kind == "P" and not narrowing else None,
                              ring=ring, ring_dst=my_q if ring is not None else (), ring_slots=R, slot_bytes=slot_bytes,
-                             scales=w.scales.get(me.tp_rank) if dyn and me.kind == "D" else None)
+                             scales=mine.get("scales") if dyn and me.kind == "D" else None)
         if me.kind == "D" and narrowing:
             slot_bytes = min(pch.slot_bytes[p] for p in my_p)
         nchunks = kvx.chunk_count((0, cfg.L), lc)
-        counters = torch.zeros(2 * nchunks + 1, dtype=torch.int32, device=dev)
+        counters = torch.zeros(kvx.pull_counter_words((0, cfg.L), lc), dtype=torch.int32, device=dev)
         seq = [0]
 
         def step(ev=None):
@@ -576,10 +688,9 @@ def run_multi(args):
                 ev[0].record(stream)
             if me.kind == "P":
                 if narrowing:
-                    kvx.stage(S, w.src_pools[me.tp_rank], w.src_bt, [dst_lays[q] for q in my_q],
-                              ring_ptrs, R,
-                              slot_bytes, [pch.peer_flag[q] for q in my_q], [pflags[q:q + 1] for q in my_q],
-                              seq[0], err, (0, cfg.L), lc, 30.0, stream,
+                    kvx.stage(S, mine["pool"], mine["bt"], [peer_lays[q] for q in my_q], ring_ptrs, R, slot_bytes,
+                              [pch.peer_flag[q] for q in my_q], [pflags[q:q + 1] for q in my_q], seq[0], err,
+                              (0, cfg.L), lc, 30.0, stream,
                               peer_scales=[pch.peer_scales[q] for q in my_q] if dyn else None)
                 else:
                     for q in my_q:   # my KV is resident: D may read it; then wait until it has
@@ -587,15 +698,14 @@ def run_multi(args):
                     for q in my_q:
                         kvx.wait(pflags[q:q + 1], epoch[0], err, 30.0, stream)
             elif me.kind == "D":
-                q = me.tp_rank
                 if narrowing:
-                    kvx.pull_staged([p_lays[p] for p in my_p], [a for p in my_p for a in pch.src_ring[p]], R,
-                                    slot_bytes, w.dst_lays[q], w.dst_pools[q], w.dst_bt,
-                                    [pflags[p:p + 1] for p in my_p], [pch.peer_flag[p] for p in my_p], seq[0], err,
-                                    (0, cfg.L), lc, 30.0, stream, counters=counters)
+                    kvx.pull_staged([peer_lays[p] for p in my_p], [a for p in my_p for a in pch.src_ring[p]], R,
+                                    slot_bytes, S, mine["pool"], mine["bt"], [pflags[p:p + 1] for p in my_p],
+                                    [pch.peer_flag[p] for p in my_p], seq[0], err, (0, cfg.L), lc, 30.0, stream,
+                                    counters=counters)
                 else:
-                    kvx.pull([p_lays[p] for p in my_p], [pch.src_pool[p] for p in my_p], w.src_bt, w.dst_lays[q],
-                             w.dst_pools[q], w.dst_bt, [pflags[p:p + 1] for p in my_p],
+                    kvx.pull([peer_lays[p] for p in my_p], [pch.src_pool[p] for p in my_p], peer_bt, S,
+                             mine["pool"], mine["bt"], [pflags[p:p + 1] for p in my_p],
                              [pch.peer_flag[p] for p in my_p], epoch[0], err, (0, cfg.L), lc, 30.0, stream)
             seq[0] += nchunks
             if ev is not None and me.kind == "D":
@@ -607,16 +717,9 @@ def run_multi(args):
         comm = kvx.Comm(world, rank, uid[0], local)
         lc = args.layer_chunk or 4
         s_a, s_b = torch.cuda.Stream(), torch.cuda.Stream()
-        events, wires = {}, {}
-        if me.kind == "P":
-            peers = {q: d_view(q) for q in my_q}
-            S = w.src_lays[me.tp_rank]
-        else:
-            peers = {p: kvx.Layout.from_dict(
-                synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, w.NB_p, cfg.src_dtype, cfg.p_order))
-                for p in my_p}
-        for k, other in peers.items():
-            sl, dl = (S, other) if me.kind == "P" else (other, w.dst_lays[me.tp_rank])
+        wires = {}
+        for k, other in peer_lays.items():
+            sl, dl = (S, other) if me.kind == "P" else (other, S)
             nb = max(kvx.wire_bytes(sl, dl, cfg.total_tokens, (l0, min(cfg.L, l0 + lc))) for l0 in range(0, cfg.L, lc))
             for b in range(2):
                 wires[(k, b)] = torch.empty(nb, dtype=torch.uint8, device=dev)
@@ -629,11 +732,11 @@ def run_multi(args):
             if ev is not None:
                 ev[0].record(stream)
             if me.kind == "P":
-                tr.nccl_send_step(comm, w.src_lays[me.tp_rank], w.src_pools[me.tp_rank], w.src_bt, peers,
-                                  {q: n_p + q for q in peers}, wires, lc, s_a, s_b, events)
+                tr.nccl_send_step(comm, S, mine["pool"], mine["bt"], peer_lays, {q: n_p + q for q in peer_lays},
+                                  wires, lc, s_a, s_b)
             elif me.kind == "D":
-                tr.nccl_recv_step(comm, peers, w.dst_lays[me.tp_rank], w.dst_pools[me.tp_rank], w.dst_bt,
-                                  {p: p for p in peers}, wires, lc, s_a, s_b, events)
+                tr.nccl_recv_step(comm, peer_lays, S, mine["pool"], mine["bt"], {p: p for p in peer_lays}, wires, lc,
+                                  s_a, s_b)
             for s_ in (s_a, s_b):
                 e = torch.cuda.Event()
                 e.record(s_)
@@ -667,35 +770,97 @@ def run_multi(args):
     kern_ms = statistics.mean(kts)
     if int(err.item()):
         raise SystemExit(f"rank {rank}: flag wait timed out")
-    # busiest link: P egress = bytes it sends, D ingress = bytes it receives (wire dtype = dst)
-    nvl_in = w.dst_bytes([0]) if me.kind == "D" else 0
-    nvl_out = sum(w.dst_bytes([0]) * (len([1 for p2, q2, _, _ in pairs if q2 == q and p2 == me.tp_rank])) //
-                  max(1, len([1 for p2, q2, _, _ in pairs if q2 == q])) for q in my_q) if me.kind == "P" else 0
+    # busiest link: P egress = bytes it sends, D ingress = bytes it receives (wire dtype = the narrower)
+    w_b = min(synth.NBYTES[cfg.src_dtype], synth.NBYTES[cfg.dst_dtype])
+    per_head = 2 * cfg.L * cfg.D * cfg.total_tokens * w_b
+    nvl_in = per_head * (cfg.H // cfg.tp_d) if me.kind == "D" else 0
+    nvl_out = sum(per_head * (he - hb) for p, q, hb, he in pairs if me.kind == "P" and p == me.tp_rank)
     stats = {"ms": my_ms, "kern_ms": kern_ms, "kern_med": statistics.median(kts), "kern_min": min(kts),
-             "launches": launches, "kind": me.kind, "nvl": max(nvl_in, nvl_out),
-             "kernel": kvx.last_kernel(),
-             "clk": clk}
+             "launches": launches, "kind": me.kind, "nvl": max(nvl_in, nvl_out), "kernel": kvx.last_kernel(),
+             "clk": clk, "nvlink_probe": nvl}
+    # ---- oracle sample on the measured buffers: P ships request 0, layers [0, 2) of its pool ----
     parity = None
-    if not args.no_parity and me.kind == "D":
-        if dyn:   # decode the received codes with the scales P shipped
-            w.dst_dicts[me.tp_rank]["scales"] = w.scales[me.tp_rank].cpu().numpy().reshape(cfg.L, 2, -1)
-        parity = parity_multi(cfg, w, me, my_p, dev, dyn)
+    if not args.no_parity:
+        samp = None
+        if me.kind == "P":
+            samp = sample_of(mine["pool"], mine["d"], mine["tables"], [0], (0, min(2, cfg.L)))
+            if dyn and cfg.tp_p <= cfg.tp_d:   # O1's amax scales of D heads (all held here), every request
+                from oracle import o1
+                allr = list(range(len(cfg.n_tokens)))
+                a, nd, loc = sample_of(mine["pool"], mine["d"], mine["tables"], allr, (0, min(2, cfg.L)))
+                want_sc = {}
+                for q in my_q:
+                    dd = dict(cp.message("D", q).desc)
+                    dd["L"], dd["scales"] = min(2, cfg.L), None
+                    want_sc[q] = o1.amax_scales([nd], [a], dd, cfg.n_tokens, loc)
+                samp = samp + (want_sc,)
+        allsamp = tr.exchange({"kind": me.kind, "r": me.tp_rank, "samp": samp})
+        if me.kind == "D":
+            srcs = {e["r"]: e["samp"] for e in allsamp if e["kind"] == "P" and e["r"] in my_p}
+            dd = dict(mine["d"])
+            if dyn:   # decode the received codes with the scales P shipped
+                dd["scales"] = mine["scales"].cpu().numpy().reshape(cfg.L, 2, -1)
+            ds = sample_of(mine["pool"], dd, mine["tables"], [0], (0, min(2, cfg.L)))
+            parity = o1_compare([srcs[p][:3] for p in my_p], [ds], [cfg.n_tokens[0]], cfg.dst_dtype)
+            parity["sample"] = f"request 0, layers [0,{min(2, cfg.L)}), P ranks {my_p} -> D{me.tp_rank} (P's sample " \
+                               "shipped over the control plane)"
+            if dyn and cfg.tp_p <= cfg.tp_d:
+                got = dd["scales"][:min(2, cfg.L)]
+                Hd = cfg.H // cfg.tp_d
+                okd = True
+                for p in my_p:   # each P rank computed the heads it holds
+                    hb = max(p * (cfg.H // cfg.tp_p), me.tp_rank * Hd) - me.tp_rank * Hd
+                    he = min((p + 1) * (cfg.H // cfg.tp_p), (me.tp_rank + 1) * Hd) - me.tp_rank * Hd
+                    okd = okd and bool(np.array_equal(got[:, :, hb:he], srcs[p][3][me.tp_rank][:, :, hb:he]))
+                parity["dynamic_scales_ok"] = okd
+                parity["ok"] = parity["ok"] and okd
+            parity["rank"] = f"D{me.tp_rank}"
+    # ---- K6 over every element of every D pool (static scales) ----
+    fullsize = None
+    if not args.no_verify and not dyn:
+        kerr = torch.zeros(1, dtype=torch.int32, device=dev)
+        if me.kind == "P":
+            kvx.verify_fill(S, mine["pool"], mine["bt"], [peer_lays[q] for q in my_q], K6_SEED, kerr)
+        torch.cuda.synchronize()
+        barrier()
+        step()
+        torch.cuda.synchronize()
+        barrier()
+        if me.kind == "D":
+            res = torch.zeros(8, dtype=torch.int64, device=dev)
+            scratch = torch.empty(S.num_blocks, dtype=torch.uint8, device=dev)
+            kvx.verify_check(peer_lays[my_p[0]], S, mine["pool"], mine["bt"], K6_SEED, res, scratch)
+            r = [int(x) for x in res.cpu()]
+            fullsize = {"rank": f"D{me.tp_rank}", "elements_checked": r[3], "value_mismatches": r[0],
+                        "tail_mismatches": r[1], "canary_mismatches": r[2]}
+        elif me.kind == "P":
+            fullsize = {"rank": f"P{me.tp_rank}", "fill_error": int(kerr.item())}
+        if int(err.item()):
+            raise SystemExit(f"rank {rank}: flag wait timed out (K6 step)")
     e2e = None
     if not args.no_e2e and args.mode in ("push", "pull"):
-        e2e = e2e_multi(w, me, step, stream, barrier, err, min(K, 3), rank)
-    allx = tr.exchange({"stats": stats, "parity": parity, "e2e": e2e})
+        e2e = e2e_multi(mine, me, step, stream, barrier, err, min(K, 3), rank)
+    allx = tr.exchange({"stats": stats, "parity": parity, "e2e": e2e, "fullsize": fullsize, "ctrl": ctrl_info})
     if rank == 0:
         sts = [x["stats"] for x in allx]
         max_ms = max(x["ms"] for x in sts)
         ms = max_ms / K
-        mover = "D" if args.mode == "pull" else "P"
         kms = max(x["kern_ms"] for x in sts if x["kind"] == mover)
-        src_b = w.src_bytes(range(n_p))
+        sb = src_bytes(cfg, n_p)
         nvl_b = max(x["nvl"] for x in sts)
         achieved = nvl_b / (ms * 1e-3) / 1e9
         full = n_p == cfg.tp_p and n_d == cfg.tp_d
+        probes = [x["nvlink_probe"] for x in sts if x["nvlink_probe"]]
+        meas = {k: round(statistics.mean([p[k] for p in probes if k in p]), 1)
+                for k in ("ce_read", "ce_write", "sm_read") if any(k in p for p in probes)}
+        ref_key = "ce_read" if args.mode == "pull" else "ce_write"
+        fs = [x["fullsize"] for x in allx if x["fullsize"] is not None]
+        fs_ok = None
+        if fs:
+            fs_ok = all(f.get("fill_error", 0) == 0 and f.get("value_mismatches", 0) == 0 and
+                        f.get("tail_mismatches", 0) == 0 and f.get("canary_mismatches", 0) == 0 for f in fs)
         out = {
-            "metric": METRIC, "value": round(src_b / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "n_gpus": world,
+            "metric": METRIC, "value": round(sb / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "n_gpus": world,
             "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 4),
             "ms_per_request": round(ms / len(cfg.n_tokens), 5), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": _dtype_name(cfg),
@@ -706,12 +871,14 @@ def run_multi(args):
                                    + (f", {world - n_p - n_d} idle GPU(s)" if world > n_p + n_d else ""),
                        "mode": args.mode + (" + dynamic fp8 scales (P amax per chunk, shipped)" if dyn else ""),
                        "layer_chunk": lc, "requests": len(cfg.n_tokens),
-                       "tokens": cfg.total_tokens, "overrides": _overrides(args), "src_bytes_per_step": src_b,
+                       "tokens": cfg.total_tokens, "overrides": _overrides(args), "src_bytes_per_step": sb,
                        "busiest_link_bytes_per_step": nvl_b, "pairs": [list(x[:2]) for x in pairs],
+                       "control_plane": "layouts, block tables and fp8 scales exchanged as kv_ctrl messages "
+                                        f"({allx[0]['ctrl']['bytes_received']} B)",
                        "l2": "inputs larger than L2 (no flush)",
                        "parallelism": f"P TP{cfg.tp_p} x D TP{cfg.tp_d}, {n_p}+{n_d} ranks present"},
-            "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_MEASURED_GBS,
-                         "unit": "GB/s", "frac": round(achieved / NVLINK_MEASURED_GBS, 4),
+            "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_NOMINAL_GBS,
+                         "unit": "GB/s", "frac": round(achieved / NVLINK_NOMINAL_GBS, 4),
                          "traffic": _traffic(f"{wl_name}:{args.mode}"),
                          "kernel": f"{[x['kernel'] for x in sts if x['kind'] == 'P'][0]} (peer-store push)"
                          if args.mode == "push"
@@ -722,17 +889,20 @@ def run_multi(args):
                          "kernel_ms_median": round(max(x["kern_med"] for x in sts if x["kind"] == mover), 4),
                          "kernel_ms_min": round(max(x["kern_min"] for x in sts if x["kind"] == mover), 4),
                          "algorithmic_bytes_per_step": nvl_b,
-                         "note": "busiest GPU link (P egress or D ingress) bytes / step time",
-                         "peak_source": "measured peer copy 770 GB/s/direction (B200_PROFILING.md)",
-                         "frac_vs_nominal_900": round(achieved / NVLINK_NOMINAL_GBS, 4)},
+                         "note": "busiest GPU link (P egress or D ingress) user bytes / step time",
+                         "peak_source": "nominal NVLink 5, 900 GB/s per direction (north_star)",
+                         "measured_in_run_gbs": meas or None,
+                         "frac_vs_measured_copy_engine": round(achieved / meas[ref_key], 4) if ref_key in meas
+                         else None},
             "clocks": sts[0]["clk"], "clocks_all_ranks": [x["clk"].get("reasons") for x in sts],
             "gpu_launches": int(sum(x["launches"] for x in sts)),
             "parity": [x["parity"] for x in allx if x["parity"] is not None],
+            "fullsize": {"ok": fs_ok, "ranks": fs} if fs else None,
         }
         es = [x["e2e"] for x in allx if x["e2e"] is not None]
         if es:
             ms_e = max(e["ms"] for e in es) / es[0]["steps"]
-            out["e2e"] = {"value": round(src_b / (ms_e * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms_e, 3),
+            out["e2e"] = {"value": round(sb / (ms_e * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms_e, 3),
                           "h2d_bytes_per_step": int(sum(e["h2d"] for e in es)),
                           "d2h_bytes_per_step": int(sum(e["d2h"] for e in es)), "steps": es[0]["steps"]}
         print(json.dumps(out), flush=True)
@@ -740,15 +910,15 @@ def run_multi(args):
     dist.destroy_process_group()
 
 
-def e2e_multi(w, me, step, stream, barrier, err, ke, rank):
+def e2e_multi(mine, me, step, stream, barrier, err, ke, rank):
     """Same metric through the public API with host buffers: every step the P rank uploads
-    its source pool from pinned memory before pushing, the D rank reads its pool back."""
+    its source pool from pinned memory before the transfer, the D rank reads its pool back."""
     import torch
     host = None
     if me.kind == "P":
-        host = _pinned_copy(w.src_pools[me.tp_rank])
+        host = _pinned_copy(mine["pool"])
     elif me.kind == "D":
-        host = torch.empty(w.dst_pools[me.tp_rank].numel(), dtype=torch.uint8, pin_memory=True)
+        host = torch.empty(mine["pool"].numel(), dtype=torch.uint8, pin_memory=True)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -756,10 +926,10 @@ def e2e_multi(w, me, step, stream, barrier, err, ke, rank):
     e0.record(stream)
     for _ in range(ke):
         if me.kind == "P":
-            w.src_pools[me.tp_rank].copy_(host, non_blocking=True)
+            mine["pool"].copy_(host, non_blocking=True)
         step()
         if me.kind == "D":
-            host.copy_(w.dst_pools[me.tp_rank], non_blocking=True)
+            host.copy_(mine["pool"], non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     if int(err.item()):
@@ -768,55 +938,17 @@ def e2e_multi(w, me, step, stream, barrier, err, ke, rank):
             "d2h": host.numel() if me.kind == "D" else 0}
 
 
-def parity_multi(cfg, w, me, my_p, dev, dyn=False):
-    """D rank: regenerate its P sources' pools from their seeds on this GPU and check a
-    sample of the received pool against the oracle.  dyn: the fp8 scales were computed and
-    shipped by P -- also check them against O1's amax scales over every request for the
-    sampled layers."""
-    import torch
-    import paper_2509_17542_b200 as kvx
-    q = me.tp_rank
-    for p in my_p:
-        d = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, w.NB_p, cfg.src_dtype, cfg.p_order)
-        pool = kvx.Layout.from_dict(d).new_pool(dev)
-        view = pool.view(torch.uint8 if synth.NBYTES[cfg.src_dtype] == 1 else torch.int16)
-        synth.fill_random_finite_(view, cfg.seed + 100 + p, cfg.src_dtype)
-        w.src_dicts[p], w.src_pools[p] = d, pool
-    ok, det = sample_parity(w, (0, 2), 0, my_p, [q])
-    det["rank"] = f"D{q}"
-    if dyn:
-        from oracle import o1
-        ids = [b for t in w.src_tables for b in t]
-        lays, pools = [], []
-        for p in my_p:
-            a, nd = extract(w.src_pools[p], w.src_dicts[p], (0, 2), ids)
-            lays.append(nd)
-            pools.append(a)
-        k, tabs = 0, []
-        for t in w.src_tables:
-            tabs.append(list(range(k, k + len(t))))
-            k += len(t)
-        dd = dict(w.dst_dicts[q])
-        dd["L"], dd["scales"] = 2, None
-        want = o1.amax_scales(lays, pools, dd, cfg.n_tokens, tabs)
-        got = np.asarray(w.dst_dicts[q]["scales"])[0:2]
-        det["dynamic_scales_ok"] = bool(np.array_equal(got, want))
-        det["dynamic_scales_sample"] = "O1 amax/448 over all requests, layers [0,2)"
-        ok = ok and det["dynamic_scales_ok"]
-    for p in my_p:
-        del w.src_pools[p]
-    return {"ok": ok, **det}
-
-
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    cfg = synth.configs()[args.workload or ("c2" if world == 1 else "c4")]
+    cfg = synth.configs()[args.workload or "c4"]
     nl = args.cpu_sample_layers or 2
     p_ranks = list(range(cfg.tp_p)) if world == 1 else [0]
     d_ranks = list(range(cfg.tp_d)) if world == 1 else [0]
+    if world > 1 and cfg.tp_p != cfg.tp_d:
+        p_ranks, d_ranks = list(range(cfg.tp_p)), list(range(cfg.tp_d))
     for _ in range(max(args.warmup, 0)):
         cpu_baseline(cfg, 1, p_ranks, d_ranks)
     tot_b, tot_t = 0, 0.0
@@ -831,18 +963,20 @@ def run_reference(args):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tot_t / args.steps * 1e3, 2),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": _dtype_name(cfg),
            "data": "synthetic", "config": {"workload": f"{cfg.name}: {cfg.note} (oracle on host, bounded sample)"},
-           "cpu_baseline": {"value": round(v, 5), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+           "cpu_baseline": {"value": round(v, 5), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample,
+                            "cpu": cpu_model()},
            "e2e": {"value": round(v, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
 def run_stream(args):
     """c5: mixed-length request stream (T ~ logU[512, 32k], 64 requests) from two P instances
-    (TP2 each, requests alternate A/B) to one D instance (TP4), per-layer pipelined push.
-    N GPUs: N/2 P ranks (instances A, B; ranks 0.. of each) and N/2 D ranks (0..N/2-1); N=8 is
-    the full c5, N=4 its per-GPU-equivalent sub-config c5' (A0 + B0 -> D0, D1).  Every request
-    is ready at t=0 and pushed in order, one fused convert launch per (request, layer chunk)
-    covering all of the P rank's D peers; per-request completion is a release flag."""
+    (TP2 each, requests alternate A/B) to one D instance (TP4), per-request transfers.  N GPUs:
+    N/2 P ranks (instances A, B; ranks 0.. of each) and N/2 D ranks (0..N/2-1); N=8 is the full
+    c5, N=4 its per-GPU-equivalent sub-config c5' (A0 + B0 -> D0, D1).  Every request is ready
+    at t=0 and moved in order; per-request completion is a release flag (push) or a
+    completion event on D (pull).  The transfer plan (who feeds whom, which flag word) is
+    transfer.StreamPlan; tables and layouts travel through the control plane."""
     import dataclasses
     import torch
     import torch.distributed as dist
@@ -854,183 +988,144 @@ def run_stream(args):
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     cfg = synth.configs()["c5"]
-    n_p = n_d = world // 2
-    n_inst = 2 if n_p >= 2 else 1
-    per_inst = n_p // n_inst
-    inst_req = [list(range(i, len(cfg.n_tokens), 2)) for i in range(n_inst)]
-    is_p = rank < n_p
-    d_ranks = list(range(n_d))
+    plan = tr.StreamPlan(world, cfg.tp_p, cfg.tp_d, cfg.H, len(cfg.n_tokens))
+    me = plan.role(rank)
     stream = torch.cuda.current_stream()
     K = args.steps
-    # D side: one pool for all requests of both instances; flags[p_world] = requests landed
-    d_cfg = cfg
     NB_d = synth.pool_capacity(cfg.n_tokens, cfg.B_d)
-    dst_tables = synth.block_tables(cfg.seed + 2, cfg.n_tokens, cfg.B_d, NB_d)
-    flags = torch.zeros(max(n_p, 1) * 8, dtype=torch.int32, device=dev)
+    flags = torch.zeros(plan.flag_words, dtype=torch.int32, device=dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
-    mine = None
     pull = args.mode == "pull"
-
-    def inst_setup(inst):
-        """P rank tables / layout of instance `inst` (rebuilt from the seeds on D in pull mode)."""
-        reqs = inst_req[inst]
-        icfg = dataclasses.replace(cfg, n_tokens=[cfg.n_tokens[r] for r in reqs], seed=cfg.seed + 10 * inst)
+    # ---- my side ----
+    if me.kind == "P":
+        reqs = plan.requests_of(me.inst)
+        icfg = dataclasses.replace(cfg, n_tokens=[cfg.n_tokens[r] for r in reqs], seed=cfg.seed + 10 * me.inst)
         NB_p = synth.pool_capacity(icfg.n_tokens, cfg.B_p)
-        return reqs, icfg, NB_p, synth.block_tables(icfg.seed + 1, icfg.n_tokens, cfg.B_p, NB_p)
-
-    if pull:
-        if is_p:
-            inst, p = rank // per_inst, rank % per_inst
-            reqs, icfg, NB_p, src_tables = inst_setup(inst)
-            sd = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, NB_p, cfg.src_dtype, cfg.p_order)
-            spool = kvx.Layout.from_dict(sd).new_pool(dev)
-            synth.fill_random_finite_(spool.view(torch.int16), icfg.seed + 100 + p, cfg.src_dtype)
-            mine = {"kind": "P", "r": rank, "pool": kvx.ipc_export(spool), "flags": kvx.ipc_export(flags)}
-        else:
-            q = rank - n_p
-            dd = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, NB_d, cfg.dst_dtype, cfg.d_order)
-            dl = kvx.Layout.from_dict(dd)
-            pool = dl.new_pool(dev, fill=synth.CANARY)
-            mine = {"kind": "D", "r": q, "flags": kvx.ipc_export(flags)}
-    elif not is_p:
-        q = rank - n_p
-        dd = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, NB_d, cfg.dst_dtype, cfg.d_order)
-        dl = kvx.Layout.from_dict(dd)
-        pool = dl.new_pool(dev, fill=synth.CANARY)
-        mine = {"q": q, "pool": kvx.ipc_export(pool), "flags": kvx.ipc_export(flags)}
-    allx = tr.exchange(mine)
-    peers = {e["q"]: e for e in allx if e is not None and "q" in e}
-    src_bytes = 0
-    lat = []
-    if pull and is_p:
-        # my KV is resident: release it to the D ranks, then wait until they have read it
-        d_flag = {e["r"]: kvx.ipc_open(*e["flags"]) + 4 * rank for e in allx if e["kind"] == "D"}
-        pairs = tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks={p}, d_ranks=set(d_ranks))
-        qs = [q for _, q, _, _ in pairs]
-        src_bytes = sum(cfg.L * 2 * cfg.D * (cfg.H // cfg.tp_p) * synth.NBYTES[cfg.src_dtype] * t
-                        for t in icfg.n_tokens)
-        count = [0]
-
-        def step(evs=None):
-            count[0] += 1
-            for q in qs:
-                kvx.signal(d_flag[q], count[0], stream)
-            for q in qs:
-                kvx.wait(flags[q:q + 1], count[0], err, 60.0, stream)
-        expected_per_step = 0
-    elif pull:
-        # D rank q: pull every request, in order, from the P rank of its instance holding q's heads
-        srcs = [pr for pr in range(n_p) if any(qq == q for _, qq, _, _ in
-                                               tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks={pr % per_inst}))]
-        p_ent = {e["r"]: e for e in allx if e["kind"] == "P"}
-        src_pool = {pr: kvx.ipc_open(*p_ent[pr]["pool"]) for pr in srcs}
-        p_flag = {pr: kvx.ipc_open(*p_ent[pr]["flags"]) + 4 * q for pr in srcs}
-        order = []   # (source P world rank, its layout, src Batch, dst Batch) per request, stream order
-        setups = {inst: inst_setup(inst) for inst in range(n_inst)}
-        for r in range(len(cfg.n_tokens)):
-            inst = r % n_inst if n_inst > 1 else 0
-            reqs, icfg, NB_p, src_tables = setups[inst]
-            i = reqs.index(r)
-            pr = [x for x in srcs if x // per_inst == inst][0]
-            sl = kvx.Layout.from_dict(synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, pr % per_inst, cfg.B_p, NB_p,
-                                                   cfg.src_dtype, cfg.p_order))
-            order.append((pr, sl, kvx.Batch(sl, [icfg.n_tokens[i]], [src_tables[i]], dev),
-                          kvx.Batch(dl, [cfg.n_tokens[r]], [dst_tables[r]], dev)))
-        count = [0]
-        # one stream per source P rank, each on its share of the SMs: D pulls the two
-        # instances' requests concurrently, so no P rank's egress carries two D ranks at once
-        side = {pr: torch.cuda.Stream() for pr in srcs}
-        if len(srcs) > 1:
-            kvx.set_sm_budget(torch.cuda.get_device_properties(dev).multi_processor_count // len(srcs))
-
-        def step(evs=None):
-            count[0] += 1
-            st = torch.cuda.Event()
-            st.record(stream)
-            for pr in srcs:
-                side[pr].wait_event(st)
-                kvx.wait(flags[pr:pr + 1], count[0], err, 60.0, side[pr])
-            for j, (pr, sl, sbt, dbt) in enumerate(order):
-                kvx.convert_reshard([sl], [src_pool[pr]], sbt, [dl], [pool], dbt, None, side[pr])
-                if evs is not None:
-                    evs[j].record(side[pr])
-            for pr in srcs:
-                kvx.signal(p_flag[pr], count[0], side[pr])
-                e = torch.cuda.Event()
-                e.record(side[pr])
-                stream.wait_event(e)
-    elif is_p:
-        inst, p = rank // per_inst, rank % per_inst
-        reqs = inst_req[inst]
-        icfg = dataclasses.replace(cfg, n_tokens=[cfg.n_tokens[r] for r in reqs], seed=cfg.seed + 10 * inst)
-        NB_p = synth.pool_capacity(icfg.n_tokens, cfg.B_p)
-        src_tables = synth.block_tables(icfg.seed + 1, icfg.n_tokens, cfg.B_p, NB_p)
-        sd = synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_p, p, cfg.B_p, NB_p, cfg.src_dtype, cfg.p_order)
-        sl = kvx.Layout.from_dict(sd)
-        spool = sl.new_pool(dev)
-        synth.fill_random_finite_(spool.view(torch.int16), icfg.seed + 100 + p, cfg.src_dtype)
-        pairs = tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks={p}, d_ranks=set(d_ranks))
-        qs = [q for _, q, _, _ in pairs]
-        dls = [kvx.Layout.from_dict(synth.layout(cfg.L, cfg.H, cfg.D, cfg.tp_d, q, cfg.B_d, NB_d, cfg.dst_dtype,
-                                                 cfg.d_order)) for q in qs]
-        ppools = [kvx.ipc_open(*peers[q]["pool"]) for q in qs]
-        pflags = [kvx.ipc_open(*peers[q]["flags"]) + 4 * rank for q in qs]
-        # per-request tables (one Batch per request on each side)
-        sbt = [kvx.Batch(sl, [icfg.n_tokens[i]], [src_tables[i]], dev) for i in range(len(reqs))]
-        dbt = [kvx.Batch(dls[0], [cfg.n_tokens[r]], [dst_tables[r]], dev) for r in reqs]
-        per_tok_layer = 2 * cfg.D * (cfg.H // cfg.tp_p) * synth.NBYTES[cfg.src_dtype]
-        chunk_bytes = args.chunk_mib << 20
-        chunks = [max(1, -(-chunk_bytes // (per_tok_layer * t))) for t in icfg.n_tokens]
-        src_bytes = sum(cfg.L * per_tok_layer * t for t in icfg.n_tokens)
-        count = [0]
-
-        if args.c5_batch:  # the whole instance batch in one launch per layer chunk (no per-request handoff)
-            sbt_all = kvx.Batch(sl, icfg.n_tokens, src_tables, dev)
-            dbt_all = kvx.Batch(dls[0], [cfg.n_tokens[r] for r in reqs], [dst_tables[r] for r in reqs], dev)
-
-        def step(evs=None):
-            if args.c5_batch:
-                lc = args.layer_chunk or cfg.L
-                for l0 in range(0, cfg.L, lc):
-                    kvx.convert_share(sl, spool, sbt_all, dls, ppools, dbt_all, (l0, min(cfg.L, l0 + lc)), stream)
-                count[0] += len(reqs)
-                for f in pflags:
-                    kvx.signal(f, count[0], stream)
-                if evs is not None:
-                    for e in evs:
-                        e.record(stream)
-                return
-            for i in range(len(reqs)):
-                lc = args.layer_chunk or chunks[i]
-                for l0 in range(0, cfg.L, lc):
-                    kvx.convert_share(sl, spool, sbt[i], dls, ppools, dbt[i], (l0, min(cfg.L, l0 + lc)), stream)
-                count[0] += 1
-                for f in pflags:
-                    kvx.signal(f, count[0], stream)
-                if evs is not None:
-                    evs[i].record(stream)
-        expected_per_step = 0
+        d, lay, pool = make_p_rank(icfg, me.tp_rank, NB_p, dev)
+        tabs = p_tables(icfg, NB_p)
+        cp = tr.ControlPlane(tr.Role("P", plan.p_index(me.inst, me.tp_rank), rank), lay, None, icfg.n_tokens, tabs)
     else:
-        q = rank - n_p
-        srcs = [pr for pr in range(n_p) if any(qq == q for _, qq, _, _ in
-                                               tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks={pr % per_inst}))]
-        n_req_of = {pr: len(inst_req[pr // per_inst]) for pr in srcs}
-        count = [0]
+        d, lay, pool, _ = make_d_rank(cfg, me.tp_rank, NB_d, dev)
+        tabs = d_tables(cfg, NB_d)
+        cp = tr.ControlPlane(tr.Role("D", me.tp_rank, rank), lay, None, cfg.n_tokens, tabs)
+    # ---- data-plane maps (CUDA IPC) ----
+    exp = {"kind": me.kind, "r": rank, "flags": kvx.ipc_export(flags)}
+    if (me.kind == "P") == pull:
+        exp["pool"] = kvx.ipc_export(pool)
+    allx = tr.exchange(exp)
+    ent = {e["r"]: e for e in allx}
+    maps = []
 
-        def step(evs=None):
-            count[0] += 1
-            for pr in srcs:
-                kvx.wait(flags[pr:pr + 1], count[0] * n_req_of[pr], err, 60.0, stream)
-    barrier_t = torch.zeros(1, device=dev)
+    def opn(h):
+        a = kvx.ipc_open(*h)
+        maps.append((a, h[1]))
+        return a
+    lat = []
+    src_b = 0
+    if me.kind == "P":
+        qs = plan.d_peers(rank)
+        src_b = sum(cfg.L * 2 * cfg.D * (cfg.H // cfg.tp_p) * synth.NBYTES[cfg.src_dtype] * t for t in icfg.n_tokens)
+        count = [0]
+        d_flag = {q: opn(ent[plan.d_world(q)]["flags"]) + 4 * plan.flag_word(rank) for q in qs}
+        if pull:
+            def step(evs=None):
+                # my KV is resident: release it to the D ranks, then wait until they have read it
+                count[0] += 1
+                for q in qs:
+                    kvx.signal(d_flag[q], count[0], stream)
+                for q in qs:
+                    kvx.wait(flags[plan.flag_word(plan.d_world(q)):plan.flag_word(plan.d_world(q)) + 1], count[0],
+                             err, 60.0, stream)
+        else:
+            dls = [cp.layout("D", q, dev) for q in qs]
+            ppools = [opn(ent[plan.d_world(q)]["pool"]) for q in qs]
+            n_d_tok, d_tabs = cp.tables("D")
+            sbt = [kvx.Batch(lay, [icfg.n_tokens[i]], [tabs[i]], dev) for i in range(len(reqs))]
+            dbt = [kvx.Batch(dls[0], [cfg.n_tokens[r]], [d_tabs[r]], dev) for r in reqs]
+            per_tok_layer = 2 * cfg.D * (cfg.H // cfg.tp_p) * synth.NBYTES[cfg.src_dtype]
+            chunk_bytes = args.chunk_mib << 20
+            chunks = [max(1, -(-chunk_bytes // (per_tok_layer * t))) for t in icfg.n_tokens]
+            if args.c5_batch:
+                sbt_all = kvx.Batch(lay, icfg.n_tokens, tabs, dev)
+                dbt_all = kvx.Batch(dls[0], [cfg.n_tokens[r] for r in reqs], [d_tabs[r] for r in reqs], dev)
+
+            def step(evs=None):
+                if args.c5_batch:
+                    lc = args.layer_chunk or cfg.L
+                    for l0 in range(0, cfg.L, lc):
+                        kvx.convert_share(lay, pool, sbt_all, dls, ppools, dbt_all, (l0, min(cfg.L, l0 + lc)), stream)
+                    count[0] += len(reqs)
+                    for q in qs:
+                        kvx.signal(d_flag[q], count[0], stream)
+                    if evs is not None:
+                        for e in evs:
+                            e.record(stream)
+                    return
+                for i in range(len(reqs)):
+                    lc = args.layer_chunk or chunks[i]
+                    for l0 in range(0, cfg.L, lc):
+                        kvx.convert_share(lay, pool, sbt[i], dls, ppools, dbt[i], (l0, min(cfg.L, l0 + lc)), stream)
+                    count[0] += 1
+                    for q in qs:
+                        kvx.signal(d_flag[q], count[0], stream)
+                    if evs is not None:
+                        evs[i].record(stream)
+    else:
+        srcs = plan.p_sources(rank)                    # world ranks of the P ranks feeding me
+        count = [0]
+        if pull:
+            src_pool = {pr: opn(ent[pr]["pool"]) for pr in srcs}
+            p_flag = {pr: opn(ent[pr]["flags"]) + 4 * plan.flag_word(rank) for pr in srcs}
+            order = []   # (source P world rank, its layout, src Batch, dst Batch) per request, stream order
+            for r in range(len(cfg.n_tokens)):
+                inst = plan.inst_of(r)
+                pr = [x for x in srcs if plan.role(x).inst == inst][0]
+                pidx = plan.p_index(inst, plan.role(pr).tp_rank)
+                sl = cp.layout("P", pidx, dev)
+                _, ptabs = cp.message("P", pidx).n_tokens, cp.message("P", pidx).tables
+                i = plan.requests_of(inst).index(r)
+                order.append((pr, sl, kvx.Batch(sl, [cfg.n_tokens[r]], [ptabs[i]], dev),
+                              kvx.Batch(lay, [cfg.n_tokens[r]], [tabs[r]], dev)))
+            # one stream per source P rank, each on its share of the SMs: D pulls the two
+            # instances' requests concurrently, so no P rank's egress carries two D ranks at once
+            side = {pr: torch.cuda.Stream() for pr in srcs}
+            if len(srcs) > 1:
+                kvx.set_sm_budget(torch.cuda.get_device_properties(dev).multi_processor_count // len(srcs))
+
+            def step(evs=None):
+                count[0] += 1
+                st = torch.cuda.Event()
+                st.record(stream)
+                for pr in srcs:
+                    side[pr].wait_event(st)
+                    kvx.wait(flags[plan.flag_word(pr):plan.flag_word(pr) + 1], count[0], err, 60.0, side[pr])
+                for j, (pr, sl, sbt, dbt) in enumerate(order):
+                    kvx.convert_reshard([sl], [src_pool[pr]], sbt, [lay], [pool], dbt, None, side[pr])
+                    if evs is not None:
+                        evs[j].record(side[pr])
+                for pr in srcs:
+                    kvx.signal(p_flag[pr], count[0], side[pr])
+                    e = torch.cuda.Event()
+                    e.record(side[pr])
+                    stream.wait_event(e)
+        else:
+            n_req_of = {pr: len(plan.requests_of(plan.role(pr).inst)) for pr in srcs}
+
+            def step(evs=None):
+                count[0] += 1
+                for pr in srcs:
+                    kvx.wait(flags[plan.flag_word(pr):plan.flag_word(pr) + 1], count[0] * n_req_of[pr], err, 60.0,
+                             stream)
     for _ in range(max(args.warmup, 1)):
         step()
     torch.cuda.synchronize()
+    barrier_t = torch.zeros(1, device=dev)
     dist.all_reduce(barrier_t)
     torch.cuda.synchronize()
     if pull:   # the D ranks run the data path: per-request completion events there
-        nreq_mine = len(cfg.n_tokens) if not is_p else 0
+        nreq_mine = len(cfg.n_tokens) if me.kind == "D" else 0
     else:
-        nreq_mine = len(inst_req[rank // per_inst]) if is_p else 0
+        nreq_mine = len(plan.requests_of(me.inst)) if me.kind == "P" else 0
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nreq_mine)] for _ in range(K)]
     clocks = ClockSampler(local)
@@ -1054,50 +1149,84 @@ def run_stream(args):
             for i in range(nreq_mine):
                 lat.append(prev.elapsed_time(evs[k][i]))
             prev = max(evs[k], key=lambda e: t0.elapsed_time(e))  # the step's last completion
-    info = tr.exchange({"ms": my_ms, "src_bytes": src_bytes, "lat": lat, "launches": launches,
-                        "nreq": nreq_mine})
+    # ---- K6 over every element of every D pool ----
+    fullsize = None
+    if not args.no_verify:
+        kerr = torch.zeros(1, dtype=torch.int32, device=dev)
+        if me.kind == "P":
+            rid = torch.tensor(plan.requests_of(me.inst), dtype=torch.int32, device=dev)
+            bt_all = kvx.Batch(lay, icfg.n_tokens, tabs, dev)
+            dl = [cp.layout("D", q, dev) for q in plan.d_peers(rank)]
+            kvx.verify_fill(lay, pool, bt_all, dl, K6_SEED, kerr, req_ids=rid)
+        torch.cuda.synchronize()
+        dist.all_reduce(barrier_t)
+        step()
+        torch.cuda.synchronize()
+        dist.all_reduce(barrier_t)
+        if me.kind == "D":
+            res = torch.zeros(8, dtype=torch.int64, device=dev)
+            scratch = torch.empty(lay.num_blocks, dtype=torch.uint8, device=dev)
+            sl = cp.layout("P", 0, dev)
+            kvx.verify_check(sl, lay, pool, kvx.Batch(lay, cfg.n_tokens, tabs, dev), K6_SEED, res, scratch)
+            r = [int(x) for x in res.cpu()]
+            fullsize = {"rank": f"D{me.tp_rank}", "elements_checked": r[3], "value_mismatches": r[0],
+                        "tail_mismatches": r[1], "canary_mismatches": r[2]}
+        else:
+            fullsize = {"rank": f"P{plan.p_index(me.inst, me.tp_rank)}", "fill_error": int(kerr.item())}
+    info = tr.exchange({"ms": my_ms, "src_bytes": src_b, "lat": lat, "launches": launches, "nreq": nreq_mine,
+                        "fullsize": fullsize})
     if rank == 0:
         max_ms = max(x["ms"] for x in info)
         ms = max_ms / K
         tot_b = sum(x["src_bytes"] for x in info)
-        nreq = len(cfg.n_tokens) if pull else sum(x["nreq"] for x in info) // max(per_inst, 1)
-        alll = sorted(l for x in info for l in x["lat"])
-        # NVLink roofline: the busiest D rank's ingress (all its heads of every request moved)
+        nreq = len(cfg.n_tokens) if pull else sum(x["nreq"] for x in info) // max(plan.per_inst, 1)
+        alll = sorted(v for x in info for v in x["lat"])
         # NVLink bytes (wire dtype, valid tokens): each present D rank's ingress, and each P
         # rank's egress to the present D ranks -- with unequal instance loads the busier P
         # rank's egress, not a D rank's ingress, is the bound
         per_head = 2 * cfg.L * cfg.D * min(synth.NBYTES[cfg.src_dtype], synth.NBYTES[cfg.dst_dtype])
-        d_in = per_head * (cfg.H // cfg.tp_d) * sum(cfg.n_tokens[r] for i in range(n_inst) for r in inst_req[i])
+        d_in = per_head * (cfg.H // cfg.tp_d) * sum(cfg.n_tokens[r] for i in range(plan.n_inst)
+                                                   for r in plan.requests_of(i))
         heads_out = sum(he - hb for pp, qq, hb, he in tr.pair_plan(cfg.tp_p, cfg.tp_d, cfg.H, p_ranks={0},
-                                                                  d_ranks=set(d_ranks)))
-        p_out = max(per_head * heads_out * sum(cfg.n_tokens[r] for r in inst_req[i]) for i in range(n_inst))
+                                                                  d_ranks=set(range(plan.n_d))))
+        p_out = max(per_head * heads_out * sum(cfg.n_tokens[r] for r in plan.requests_of(i))
+                    for i in range(plan.n_inst))
         busiest = max(d_in, p_out)
-        t_roof = busiest / (NVLINK_MEASURED_GBS * 1e9) * 1e3
+        t_roof = busiest / (NVLINK_NOMINAL_GBS * 1e9) * 1e3
+        fs = [x["fullsize"] for x in info if x["fullsize"] is not None]
+        fs_ok = all(f.get("fill_error", 0) == 0 and f.get("value_mismatches", 0) == 0 and
+                    f.get("tail_mismatches", 0) == 0 and f.get("canary_mismatches", 0) == 0 for f in fs) if fs else None
         out = {"metric": METRIC, "value": round(tot_b / (ms * 1e-3) / 1e9, 2), "unit": "GB/s", "n_gpus": world,
                "steps": K, "warmup": args.warmup, "ms_per_step": round(ms, 3),
                "ms_per_request": round(ms / max(nreq, 1), 4), "higher_is_better": True, "scaling": "weak",
                "vs_baseline": None, "dtype": _dtype_name(cfg), "data": "synthetic (seeded)",
-               "config": {"workload": f"c5 stream: {cfg.note}; {n_inst} P instance(s) x {per_inst} rank(s) -> "
-                                      f"D ranks {d_ranks}" + (" (full c5)" if world == 8 else " (c5' sub-config)"),
+               "config": {"workload": f"c5 stream: {cfg.note}; {plan.n_inst} P instance(s) x {plan.per_inst} "
+                                      f"rank(s) -> D ranks {list(range(plan.n_d))}"
+                                      + (" (full c5)" if world == 8 else " (c5' sub-config)"),
                           "requests": nreq, "src_bytes_per_step": tot_b,
                           "mode": "pull per request (D-initiated NVLink reads, one launch per request)" if pull
                           else "push, whole instance batch per launch" if args.c5_batch else
                           f"push per request, layer chunks >= {args.chunk_mib} MiB",
+                          "control_plane": "layouts and block tables exchanged as kv_ctrl messages",
                           "l2": "inputs larger than L2 (no flush)"},
                "latency_ms": {"p50": round(alll[len(alll) // 2], 3) if alll else None,
                               "p99": round(alll[min(len(alll) - 1, int(0.99 * len(alll)))], 3) if alll else None,
                               "note": "per request, from the step start, requests issued in order"},
                "roofline": {"bound": "nvlink", "achieved": round(busiest / (ms * 1e-3) / 1e9, 1),
-                            "peak": NVLINK_MEASURED_GBS, "unit": "GB/s", "frac": round(t_roof / ms, 4),
+                            "peak": NVLINK_NOMINAL_GBS, "unit": "GB/s", "frac": round(t_roof / ms, 4),
                             "traffic": None,
                             "kernel": "k_convert_rows (peer-load pull on D, per request)" if pull
                             else "k_convert_rows (peer-store push, per request)",
                             "algorithmic_bytes_per_step": busiest, "d_ingress_bytes": d_in, "p_egress_bytes": p_out,
+                            "peak_source": "nominal NVLink 5, 900 GB/s per direction (north_star)",
                             "note": "busiest GPU link (max of D ingress, P egress) / step time"},
-               "clocks": clk, "gpu_launches": int(sum(x["launches"] for x in info))}
+               "clocks": clk, "gpu_launches": int(sum(x["launches"] for x in info)),
+               "fullsize": {"ok": fs_ok, "ranks": fs} if fs else None}
         print(json.dumps(out), flush=True)
     dist.all_reduce(barrier_t)
     torch.cuda.synchronize()
+    for a, o in maps:
+        kvx.ipc_close(a, o)
     dist.destroy_process_group()
 
 

@@ -302,6 +302,11 @@ kv_status kv_wire_header_check(const uint8_t* hdr, size_t len, const kv_layout* 
  * dst/src DEVICE (may be peer-mapped), any alignment. */
 kv_status kv_copy_bytes(void* dst, const void* src, size_t bytes, kv_stream stream);
 
+/* Copy-engine device-to-device (or peer) copy, cudaMemcpyAsync: NOT on the data path -- the
+ * bench's in-run NVLink ceiling (a measured peer copy of 1 GiB per direction).
+ * dst/src DEVICE (local or peer-mapped). */
+kv_status kv_memcpy_engine(void* dst, const void* src, size_t bytes, kv_stream stream);
+
 /* ---- A8: transport over NVLink ------------------------------------------------- */
 
 typedef struct kv_comm kv_comm; /* an NCCL communicator owned by the library */

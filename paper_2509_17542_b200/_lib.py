@@ -83,6 +83,7 @@ def _load():
         "kv_wire_header_parse": (st, [p, C.c_size_t, C.POINTER(WireInfo)]),
         "kv_wire_header_check": (st, [p, C.c_size_t, p, p, i32, p, i32, i32]),
         "kv_copy_bytes": (st, [p, p, C.c_size_t, p]),
+        "kv_memcpy_engine": (st, [p, p, C.c_size_t, p]),
         "kv_wire_bytes": (C.c_size_t, [p, p, i64, i32, i32]),
         "kv_pack": (st, [p, p, C.POINTER(Batch_t), p, i32, i32, p, C.c_size_t, p]),
         "kv_unpack": (st, [p, p, p, C.POINTER(Batch_t), i32, i32, p, C.c_size_t, p]),
@@ -135,7 +136,7 @@ lib = _load()
 EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_block_table_update", "kv_plan_pairs",
            "kv_ctrl_msg_bytes", "kv_ctrl_msg_write", "kv_ctrl_msg_parse",
            "kv_convert_reshard", "kv_convert_share", "kv_compute_scales", "kv_wire_dtype", "kv_wire_header_bytes",
-           "kv_wire_header_write", "kv_wire_header_parse", "kv_wire_header_check", "kv_copy_bytes", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
+           "kv_wire_header_write", "kv_wire_header_parse", "kv_wire_header_check", "kv_copy_bytes", "kv_memcpy_engine", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
            "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
            "kv_recv_unpack", "kv_push", "kv_send_pipelined", "kv_recv_pipelined", "kv_pull", "kv_stage",
            "kv_pull_staged", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",

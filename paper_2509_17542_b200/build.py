@@ -50,17 +50,35 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 def _build_locked(verbose: bool) -> str:
+    """One nvcc -c per translation unit, in parallel, then one shared-library link."""
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
     nccl_inc, nccl_lib = _nccl_dirs()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-Xcompiler", "-fPIC,-O3,-Wall", "-shared", "--expt-relaxed-constexpr",
-           "-I", INCLUDE, "-I", CSRC, "-I", nccl_inc,
-           "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + nccl_lib,
-           "-o", LIB + ".tmp"] + os.environ.get("KVX_NVCC_FLAGS", "").split() + sources()
+    common = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC,-O3,-Wall", "--expt-relaxed-constexpr", "-I", INCLUDE, "-I", CSRC, "-I", nccl_inc]
+    common += os.environ.get("KVX_NVCC_FLAGS", "").split()
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+        common.insert(1, "-Xptxas=-v")
+    with tempfile.TemporaryDirectory(prefix="kvx_build_") as tmp:
+        objs = [os.path.join(tmp, os.path.basename(src) + ".o") for src in sources()]
+
+        def cc(pair):
+            src, obj = pair
+            cmd = common + ["-c", src, "-o", obj]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            return subprocess.run(cmd, capture_output=not verbose, text=True)
+
+        with ThreadPoolExecutor(len(objs)) as ex:
+            res = list(ex.map(cc, zip(sources(), objs)))
+        for src, r in zip(sources(), res):
+            if r.returncode != 0:
+                sys.stderr.write((r.stdout or "") + (r.stderr or ""))
+                raise subprocess.CalledProcessError(r.returncode, f"nvcc -c {src}")
+        link = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fPIC",
+                "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath," + nccl_lib, "-o", LIB + ".tmp"]
+        subprocess.check_call(link[:4] + objs + link[4:])
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

@@ -126,4 +126,11 @@ kv_status kv_copy_bytes(void* dst, const void* src, size_t bytes, kv_stream stre
   return e == cudaSuccess ? KV_OK : cuda_fail(e, "kv_copy_bytes: launch");
 }
 
+kv_status kv_memcpy_engine(void* dst, const void* src, size_t bytes, kv_stream stream) {
+  if (bytes == 0) return KV_OK;
+  if (!dst || !src) return fail(KV_EINVAL, "kv_memcpy_engine: null pointer");
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+  return e == cudaSuccess ? KV_OK : cuda_fail(e, "kv_memcpy_engine");
+}
+
 }  // extern "C"

@@ -13,7 +13,7 @@ from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BY
                    KV_F32, KV_F8E4M3FNUZ, Batch_t, CtrlInfo, KvError, LayoutDesc, check, lib)
 
 __all__ = ["Layout", "Batch", "CtrlMsg", "ctrl_encode", "ctrl_decode", "convert_reshard", "convert_share", "push", "pull", "stage", "pull_staged", "chunk_count", "pull_counter_words", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
-           "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "preload", "verify_fill", "verify_check", "launch_count", "launch_count_reset", "set_sm_budget", "last_kernel",
+           "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "preload", "memcpy_engine", "copy_bytes", "verify_fill", "verify_check", "launch_count", "launch_count_reset", "set_sm_budget", "last_kernel",
            "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "KV_F8E4M3FNUZ", "DTYPE_BYTES",
            "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
 
@@ -475,6 +475,16 @@ def verify_check(src: Layout, dst: Layout, dst_pool, dst_batch: Batch, seed, res
     result: device int64[8] ([0] value, [1] tail, [2] canary mismatches, [3] checked)."""
     check(lib.kv_verify_check(src.handle, dst.handle, _ptr(dst_pool), C.byref(dst_batch.bt), _ptr(req_ids),
                               int(seed), canary, _ptr(scratch), scratch.numel(), _ptr(result), _stream(stream)))
+
+
+def memcpy_engine(dst, src, nbytes, stream=None):
+    """kv_memcpy_engine: copy-engine (peer) copy -- the bench's NVLink ceiling, not the path."""
+    check(lib.kv_memcpy_engine(_ptr(dst), _ptr(src), int(nbytes), _stream(stream)))
+
+
+def copy_bytes(dst, src, nbytes, stream=None):
+    """kv_copy_bytes: SM-driven opaque byte copy (hidden state)."""
+    check(lib.kv_copy_bytes(_ptr(dst), _ptr(src), int(nbytes), _stream(stream)))
 
 
 def launch_count():

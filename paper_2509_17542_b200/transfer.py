@@ -62,6 +62,62 @@ def present_ranks(tp_p: int, tp_d: int, world_size: int):
     return n_p, n_p * ratio
 
 
+@dataclass
+class StreamRole:
+    kind: str        # "P" or "D"
+    inst: int        # P instance (P ranks); -1 for D ranks
+    tp_rank: int
+
+
+class StreamPlan:
+    """Roles and wiring of the c5 stream (several P instances feeding one D instance; the
+    paper's DP-replicated prefill): world ranks [0, n_p) are P ranks -- instance
+    rank // per_inst, TP rank rank % per_inst -- and [n_p, n_p + n_d) the D instance's TP
+    ranks.  Requests alternate over the instances (request r belongs to instance r % n_inst).
+    Completion words: every rank owns an int32 flag array of ``flag_words`` words; the word a
+    peer signals in it is the peer's world rank (``flag_word``)."""
+
+    def __init__(self, world: int, tp_p: int, tp_d: int, num_kv_heads: int, n_req: int):
+        self.world, self.tp_p, self.tp_d, self.H, self.n_req = world, tp_p, tp_d, num_kv_heads, n_req
+        self.n_p = self.n_d = world // 2
+        self.n_inst = 2 if self.n_p >= 2 else 1
+        self.per_inst = self.n_p // self.n_inst
+        self.flag_words = max(world, 1)
+        if self.n_p < 1 or self.per_inst < 1:
+            raise ValueError(f"the stream needs at least 2 GPUs, got {world}")
+
+    def role(self, rank: int) -> StreamRole:
+        if rank < self.n_p:
+            return StreamRole("P", rank // self.per_inst, rank % self.per_inst)
+        return StreamRole("D", -1, rank - self.n_p)
+
+    def requests_of(self, inst: int):
+        return list(range(inst, self.n_req, self.n_inst))
+
+    def inst_of(self, r: int) -> int:
+        return r % self.n_inst
+
+    def p_index(self, inst: int, tp_rank: int) -> int:
+        """Control-plane key of a P rank (unique over the instances) = its world rank."""
+        return inst * self.per_inst + tp_rank
+
+    def d_world(self, q: int) -> int:
+        return self.n_p + q
+
+    def d_peers(self, p_world: int):
+        """D TP ranks (present) the P rank at world rank p_world feeds (A2 pairs of its TP rank)."""
+        tp = self.role(p_world).tp_rank
+        return sorted({q for p, q, _hb, _he in kv.plan_pairs(self.tp_p, self.tp_d, self.H) if p == tp and q < self.n_d})
+
+    def p_sources(self, d_world: int):
+        """World ranks of the P ranks (every instance) that feed the D rank at world rank d_world."""
+        q = self.role(d_world).tp_rank
+        return [pr for pr in range(self.n_p) if q in self.d_peers(pr)]
+
+    def flag_word(self, world_rank: int) -> int:
+        return world_rank
+
+
 def pair_plan(tp_p: int, tp_d: int, num_kv_heads: int, p_ranks=None, d_ranks=None):
     """A2 pairs restricted to the ranks present: [(p, q, h_begin, h_end)]."""
     pairs = kv.plan_pairs(tp_p, tp_d, num_kv_heads)

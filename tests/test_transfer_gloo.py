@@ -45,7 +45,7 @@ def _worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 6, 8])
 def test_roles_plan_and_handle_exchange(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
@@ -134,7 +134,7 @@ def _pull_worker(rank, world, port, q, staged):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,staged", [(2, False), (3, False), (3, True)])
+@pytest.mark.parametrize("world,staged", [(2, False), (3, False), (3, True), (5, True), (8, False)])
 def test_pull_channel_exchange(world, staged):
     """PullChannel: D maps every P rank's pool (or its ring slots for this D rank) and the
     word it owns in P's flag array; P maps its word in D's ready array."""
@@ -167,3 +167,37 @@ def test_pull_channel_exchange(world, staged):
                     assert src_ring[p] == [base + 200 + b * 1000 for b in range(2)]
                 else:
                     assert src_pool[p] == base + 200 and src_ring == {}
+
+
+def test_stream_plan_wiring():
+    """c5 (2 P instances x TP2 -> D TP4): at N = 8 the full stream -- every D rank is fed by
+    one P rank of EACH instance holding its heads, every P rank feeds the two D ranks its heads
+    go to; at N = 4 the c5' sub-config (A0 + B0 -> D0, D1); flag words are world ranks and
+    distinct per peer."""
+    from paper_2509_17542_b200 import transfer as tr
+    pl = tr.StreamPlan(8, 2, 4, 8, 64)
+    assert [(r.kind, r.inst, r.tp_rank) for r in map(pl.role, range(8))] == \
+        [("P", 0, 0), ("P", 0, 1), ("P", 1, 0), ("P", 1, 1), ("D", -1, 0), ("D", -1, 1), ("D", -1, 2), ("D", -1, 3)]
+    assert [pl.d_peers(r) for r in range(4)] == [[0, 1], [2, 3], [0, 1], [2, 3]]
+    assert [pl.p_sources(pl.d_world(q)) for q in range(4)] == [[0, 2], [0, 2], [1, 3], [1, 3]]
+    assert pl.requests_of(0) == list(range(0, 64, 2)) and pl.requests_of(1) == list(range(1, 64, 2))
+    assert all(pl.inst_of(r) == r % 2 for r in range(64))
+    assert sorted(pl.p_index(i, t) for i in range(2) for t in range(2)) == [0, 1, 2, 3]
+    for d in range(4, 8):   # the words a D rank's sources signal in its array never collide
+        words = [pl.flag_word(pr) for pr in pl.p_sources(d)]
+        assert len(set(words)) == len(words) and all(0 <= w < pl.flag_words for w in words)
+    for p in range(4):      # nor do the D peers' words in a P rank's array
+        words = [pl.flag_word(pl.d_world(q)) for q in pl.d_peers(p)]
+        assert len(set(words)) == len(words) and all(0 <= w < pl.flag_words for w in words)
+    # every (request, D rank, head) is delivered by exactly one P rank
+    for r in range(64):
+        inst = pl.inst_of(r)
+        for q in range(4):
+            feeders = [pr for pr in pl.p_sources(pl.d_world(q)) if pl.role(pr).inst == inst]
+            assert len(feeders) == 1
+    small = tr.StreamPlan(4, 2, 4, 8, 64)
+    assert (small.n_inst, small.per_inst, small.n_d) == (2, 1, 2)
+    assert [small.d_peers(r) for r in range(2)] == [[0, 1], [0, 1]]
+    assert [small.p_sources(small.d_world(q)) for q in range(2)] == [[0, 1], [0, 1]]
+    with pytest.raises(ValueError):
+        tr.StreamPlan(1, 2, 4, 8, 64)
