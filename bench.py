@@ -339,11 +339,33 @@ def _traffic(key):
     return None
 
 
+_REGISTERED = []
+
+
+def _pinned_empty(nbytes):
+    """Page-locked host buffer of exactly nbytes (a numpy allocation registered with
+    cudaHostRegister): torch's pinned allocator rounds every block up to a power of two, which
+    would pin ~100 GB for c4's 71 GB of pools."""
+    import torch
+    arr = np.empty(max(int(nbytes), 1), dtype=np.uint8)
+    rc = torch.cuda.cudart().cudaHostRegister(arr.ctypes.data, arr.nbytes, 0)
+    if int(rc) != 0:
+        raise RuntimeError(f"cudaHostRegister of {nbytes} bytes failed ({rc})")
+    _REGISTERED.append(arr)
+    return torch.from_numpy(arr)[:nbytes]
+
+
+def _unpin_all():
+    import torch
+    torch.cuda.synchronize()
+    while _REGISTERED:
+        torch.cuda.cudart().cudaHostUnregister(_REGISTERED.pop().ctypes.data)
+
+
 def _pinned_copy(dev_tensor):
     """Pinned host copy of a device tensor without a pageable intermediate (GB-sized pools)."""
-    import torch
-    h = torch.empty(dev_tensor.numel(), dtype=dev_tensor.dtype, pin_memory=True)
-    h.copy_(dev_tensor.view(-1))
+    h = _pinned_empty(dev_tensor.numel() * dev_tensor.element_size())
+    h.copy_(dev_tensor.view(-1).view(__import__("torch").uint8))
     return h
 
 
@@ -437,7 +459,8 @@ def run_single(args):
     if not args.no_e2e:
         out["e2e"] = e2e_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, min(K, 3), stream, sb)
     if not args.no_cpu_baseline:
-        nl = args.cpu_sample_layers or min(cfg.L, 8 if cfg.H * cfg.D * cfg.n_tokens[0] > (1 << 21) else 12)
+        # about 10-30 s of single-thread O1: c4 (fp8 cast) ~31 MB/s -> 24 layers of request 0
+        nl = args.cpu_sample_layers or min(cfg.L, 24 if cfg.H * cfg.D * cfg.n_tokens[0] > (1 << 21) else 12)
         nb, dt = cpu_baseline(cfg, nl, range(cfg.tp_p), range(cfg.tp_d))
         out["cpu_baseline"] = {"value": round(nb / dt / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
                                "cpu": cpu_model(),
@@ -488,7 +511,7 @@ def e2e_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, K, stream, sb):
     import torch
     import paper_2509_17542_b200 as kvx
     hs = [_pinned_copy(p) for p in SP]
-    hd = [torch.empty(p.numel(), dtype=torch.uint8, pin_memory=True) for p in DP]
+    hd = [_pinned_empty(p.numel()) for p in DP]
     lay_major = cfg.p_order[0] == synth.LAYER
     n_ch = 8 if lay_major else 1
     bounds = [(i * cfg.L // n_ch, (i + 1) * cfg.L // n_ch) for i in range(n_ch)]
@@ -520,8 +543,11 @@ def e2e_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, K, stream, sb):
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / K
+    h2d, d2h = int(sum(h.numel() for h in hs)), int(sum(h.numel() for h in hd))
+    del hs, hd
+    _unpin_all()
     return {"value": round(sb / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 3),
-            "h2d_bytes_per_step": int(sum(h.numel() for h in hs)), "d2h_bytes_per_step": int(sum(h.numel() for h in hd)),
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "steps": K, "pipelined": f"{len(bounds)} layer chunks uploaded ahead of their convert; D pools read back "
                                      "after the step (whole pools: the ~10% free-block slack crosses PCIe too)"}
 
@@ -532,8 +558,8 @@ def e2e_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, K, stream, sb):
 def nvlink_probe(me, my_peer, dev, tr, kvx, barrier, nbytes=1 << 30):
     """In-run NVLink ceiling: 1 GiB copy-engine copies between each P rank and
     its first D peer, all pairs at once -- D reading P's buffer (the pull direction) and P
-    writing D's buffer (the push direction) -- plus an SM-driven peer read (kv_copy_bytes,
-    what the pull kernels do).  Returns GB/s per direction (median of 3, this rank)."""
+    writing D's buffer (the push direction).  Returns GB/s per direction (median of 3, this
+    rank)."""
     import torch
     buf = torch.empty(nbytes, dtype=torch.uint8, device=dev) if me.kind in "PD" else None
     if buf is not None:
@@ -547,8 +573,7 @@ def nvlink_probe(me, my_peer, dev, tr, kvx, barrier, nbytes=1 << 30):
     s = torch.cuda.current_stream()
     out = {}
     for name, who, fn in (("ce_read", "D", lambda: kvx.memcpy_engine(buf, peer[0], nbytes, s)),
-                          ("ce_write", "P", lambda: kvx.memcpy_engine(peer[0], buf, nbytes, s)),
-                          ("sm_read", "D", lambda: kvx.copy_bytes(buf, peer[0], nbytes, s))):
+                          ("ce_write", "P", lambda: kvx.memcpy_engine(peer[0], buf, nbytes, s))):
         ts = []
         for i in range(4):
             torch.cuda.synchronize()
@@ -852,7 +877,7 @@ def run_multi(args):
         full = n_p == cfg.tp_p and n_d == cfg.tp_d
         probes = [x["nvlink_probe"] for x in sts if x["nvlink_probe"]]
         meas = {k: round(statistics.mean([p[k] for p in probes if k in p]), 1)
-                for k in ("ce_read", "ce_write", "sm_read") if any(k in p for p in probes)}
+                for k in ("ce_read", "ce_write") if any(k in p for p in probes)}
         ref_key = "ce_read" if args.mode == "pull" else "ce_write"
         fs = [x["fullsize"] for x in allx if x["fullsize"] is not None]
         fs_ok = None
@@ -918,7 +943,7 @@ def e2e_multi(mine, me, step, stream, barrier, err, ke, rank):
     if me.kind == "P":
         host = _pinned_copy(mine["pool"])
     elif me.kind == "D":
-        host = torch.empty(mine["pool"].numel(), dtype=torch.uint8, pin_memory=True)
+        host = _pinned_empty(mine["pool"].numel())
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -934,8 +959,11 @@ def e2e_multi(mine, me, step, stream, barrier, err, ke, rank):
     torch.cuda.synchronize()
     if int(err.item()):
         raise SystemExit(f"rank {rank}: flag wait timed out (e2e)")
-    return {"ms": e0.elapsed_time(e1), "steps": ke, "h2d": host.numel() if me.kind == "P" else 0,
-            "d2h": host.numel() if me.kind == "D" else 0}
+    n = host.numel() if host is not None else 0
+    del host
+    _unpin_all()
+    return {"ms": e0.elapsed_time(e1), "steps": ke, "h2d": n if me.kind == "P" else 0,
+            "d2h": n if me.kind == "D" else 0}
 
 
 def run_reference(args):

@@ -32,3 +32,15 @@ def o1():
     from oracle import o1 as _o1
     _o1.lib()
     return _o1
+
+
+@pytest.fixture(autouse=True, scope="module")
+def _release_gpu_memory():
+    """Return each module's cached device memory (GB-sized pools) before the next module --
+    e.g. the bench contract test launches bench.py, which needs 71 GB of the same GPU."""
+    yield
+    import gc
+    gc.collect()
+    import torch
+    if torch.cuda.is_available() and torch.cuda.is_initialized():
+        torch.cuda.empty_cache()

@@ -3,8 +3,9 @@
 
 The oracle cannot redo GBs, so: (1) sampled outputs -- requests first / middle / last, a
 few layers, all their blocks, compared element by element with O1 run on the extracted
-source blocks; (2) properties that hold at any size -- every destination block outside
-the batch's tables keeps its canary bytes, and every request's tail slots are zero."""
+source blocks; (2) K6 over the whole D pools after a second transfer of a hash-coded fill
+(kv_verify_fill / kv_verify_check: every valid element, every tail slot, every unused
+block's canary) -- itself pinned to O1 in tests/test_gpu_verify.py."""
 import numpy as np
 import pytest
 import torch
@@ -20,53 +21,49 @@ def _cuda():
         pytest.skip("no CUDA device")
 
 
-def _tail_and_canary(w, q):
-    """Blocks outside every request's table keep 0xA5; tail slots of the last block are 0."""
-    d = w.dst_dicts[q]
-    nb = synth.NBYTES[d["dtype"]]
-    tdt = {1: torch.uint8, 2: torch.int16, 4: torch.int32}[nb]
-    ext = {synth.LAYER: d["L"], synth.KV: 2, synth.BLOCK: d["NB"], synth.SLOT: d["B"], synth.HEAD: d["H"] // d["tp"],
-           synth.DIM: d["D"]}
-    pool = w.dst_pools[q].view(tdt).view([ext[a] for a in d["order"]])
-    bax = d["order"].index(synth.BLOCK)
-    used = sorted(b for t in w.dst_tables for b in t)
-    free = sorted(set(range(d["NB"])) - set(used))
-    if free:
-        fb = pool.index_select(bax, torch.as_tensor(free, device=pool.device))
-        assert bool((fb.view(torch.uint8) == synth.CANARY).all()), "a block outside the tables was written"
-    sax = d["order"].index(synth.SLOT)
-    for r, T in enumerate(w.cfg.n_tokens):
-        tail = T % d["B"]
-        if tail:
-            blk = pool.index_select(bax, torch.as_tensor([w.dst_tables[r][-1]], device=pool.device))
-            slots = blk.index_select(sax, torch.arange(tail, d["B"], device=pool.device))
-            assert bool((slots == 0).all()), f"request {r}: tail slots not zero"
-
-
 @pytest.mark.parametrize("name,p_ranks,d_ranks,reqs", [
     ("c2", [0, 1], [0], [0]),
     ("c3", [0, 1], [0], [0, 7, 15]),
     ("c4", [0], [0], [0, 16, 31]),
     ("c5", [0], [0, 1], [0, 15, 31]),
 ])
-def test_fullsize_sampled(name, p_ranks, d_ranks, reqs):
+def test_fullsize_sampled_and_k6(name, p_ranks, d_ranks, reqs):
     import dataclasses
     import paper_2509_17542_b200 as kvx
-    from bench import Workload, sample_parity
+    from bench import K6_SEED, d_tables, make_d_rank, make_p_rank, o1_compare, p_tables, sample_of
     cfg = synth.configs()[name]
     if name == "c5":  # one P instance (A) of the stream: even requests
         cfg = dataclasses.replace(cfg, n_tokens=cfg.n_tokens[0::2])
-    w = Workload(cfg, p_ranks, d_ranks, torch.device("cuda", 0))
-    kvx.convert_reshard([w.src_lays[p] for p in p_ranks], [w.src_pools[p] for p in p_ranks], w.src_bt,
-                        [w.dst_lays[q] for q in d_ranks], [w.dst_pools[q] for q in d_ranks], w.dst_bt)
+    dev = torch.device("cuda", 0)
+    NB_p, NB_d = synth.pool_capacity(cfg.n_tokens, cfg.B_p), synth.pool_capacity(cfg.n_tokens, cfg.B_d)
+    P = {p: make_p_rank(cfg, p, NB_p, dev) for p in p_ranks}
+    Dr = {q: make_d_rank(cfg, q, NB_d, dev) for q in d_ranks}
+    pt, dt_ = p_tables(cfg, NB_p), d_tables(cfg, NB_d)
+    S, SP = [P[p][1] for p in p_ranks], [P[p][2] for p in p_ranks]
+    Dl, DP = [Dr[q][1] for q in d_ranks], [Dr[q][2] for q in d_ranks]
+    sbt = kvx.Batch(S[0], cfg.n_tokens, pt, dev)
+    dbt = kvx.Batch(Dl[0], cfg.n_tokens, dt_, dev)
+    kvx.convert_reshard(S, SP, sbt, Dl, DP, dbt)
     torch.cuda.synchronize()
     L = cfg.L
     for r in reqs:
         for layers in ((0, 1), (L // 2, L // 2 + 1), (L - 1, L)):
-            ok, det = sample_parity(w, layers, r, p_ranks, d_ranks)
-            assert ok, det
-    for q in d_ranks:
-        _tail_and_canary(w, q)
+            ss = [sample_of(P[p][2], P[p][0], pt, [r], layers) for p in p_ranks]
+            ds = [sample_of(Dr[q][2], Dr[q][0], dt_, [r], layers) for q in d_ranks]
+            res = o1_compare(ss, ds, [cfg.n_tokens[r]], cfg.dst_dtype)
+            assert res["ok"] and res["mismatches"] == 0, (r, layers, res)
+    # K6: a hash-coded fill, the same launch again, every element of every D pool
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    for lay, pool in zip(S, SP):
+        kvx.verify_fill(lay, pool, sbt, Dl, K6_SEED, err)
+    kvx.convert_reshard(S, SP, sbt, Dl, DP, dbt)
+    for lay, pool in zip(Dl, DP):
+        res = torch.zeros(8, dtype=torch.int64, device=dev)
+        scratch = torch.empty(lay.num_blocks, dtype=torch.uint8, device=dev)
+        kvx.verify_check(S[0], lay, pool, dbt, K6_SEED, res, scratch)
+        r6 = [int(x) for x in res.cpu()]
+        assert int(err.item()) == 0 and r6[:3] == [0, 0, 0], r6
+        assert r6[3] == 2 * L * lay.h_local * cfg.D * cfg.total_tokens
 
 
 def test_fullsize_vendor_layouts(o1):

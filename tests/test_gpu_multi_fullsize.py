@@ -1,7 +1,8 @@
 """Multi-GPU parity at BASELINE.json's full sizes, in exactly the launch configuration
-bench.py times: torchrun of bench.py itself (one process per GPU, NCCL control plane),
-each D rank checking a sample of its received pool against the oracle (bench's
-parity_multi: request 0, layers [0, 2), regenerated sources) -- for the default pull
+bench.py times: torchrun of bench.py itself (one process per GPU, layouts / tables / scales
+exchanged through the control plane), each D rank checking a sample of its received pool
+against the oracle (request 0, layers [0, 2), the P rank's source sample shipped over the
+control plane) and K6 checking every element of every D pool -- for the default pull
 transport and the push / NCCL baselines."""
 import json
 import os
@@ -43,6 +44,7 @@ def test_c4_pair_fullsize(mode):
     d = _bench(2, "--mode", mode)
     assert d["parity"] and all(p["ok"] for p in d["parity"]), d["parity"]
     assert d["parity"][0]["mismatches"] == 0
+    assert d["fullsize"]["ok"] is True, d["fullsize"]
 
 
 @pytest.mark.parametrize("workload", ["c3", "c2"])
@@ -52,3 +54,21 @@ def test_fan_in_fullsize_pull(workload):
         pytest.skip("needs 3 GPUs")
     d = _bench(min(4, torch.cuda.device_count()), "--workload", workload, "--mode", "pull")
     assert d["parity"] and all(p["ok"] for p in d["parity"]), d["parity"]
+    assert d["fullsize"]["ok"] is True, d["fullsize"]
+
+
+def test_c4_pair_dynamic_scales():
+    """The staged pull with per-chunk amax scales computed on P and shipped with the codes."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    d = _bench(2, "--mode", "pull", "--dynamic-scales")
+    assert d["parity"] and all(p["ok"] for p in d["parity"]), d["parity"]
+    assert d["parity"][0].get("dynamic_scales_ok") is True
+
+
+def test_c5_stream_pull():
+    """c5' (two P instances' requests, alternating, into one D instance) with K6 full-size."""
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs")
+    d = _bench(4, "--workload", "c5", "--mode", "pull")
+    assert d["fullsize"]["ok"] is True, d["fullsize"]
