@@ -682,15 +682,19 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
     }
   }
   // per-layer chunk count; split the layer range so each launch stays under 2^31 chunks
+  // (element-wise kernel: 32-bit chunk decode) or 2^31 rows (row kernel: 32-bit item decode;
+  // the whole c4 batch, 2.7 G chunks, is one launch)
   const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * (a.kv1 ? 1 : 2) * a.Hd_eff * a.Bd * ndch;
-  int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / std::max<uint64_t>(per_layer, 1));
-  if (per_layer > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_convert_reshard: one layer exceeds 2^31 chunks");
+  const uint64_t per_layer_units = vec == 8 ? per_layer / ndch : per_layer;
+  int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / std::max<uint64_t>(per_layer_units, 1));
+  if (per_layer_units > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_convert_reshard: one layer exceeds 2^31 chunks");
   for (int32_t l0 = lb; l0 < le; l0 += step) {
     const int32_t l1 = std::min(le, l0 + step);
     a.lb = l0;
     a.Lc = l1 - l0;
     a.f_l = make_fastdiv((uint32_t)a.Lc);
-    a.total = (uint32_t)(per_layer * (uint64_t)a.Lc);
+    a.total64 = per_layer * (uint64_t)a.Lc;
+    a.total = (uint32_t)a.total64;  // element-wise kernel only (< 2^31 there)
     t_last_kernel = vec == 8 ? "k_convert_rows" : "k_convert";
     cudaError_t e = launch_convert(a, vec, S->d.dtype, D->d.dtype, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "kv_convert_reshard: launch");

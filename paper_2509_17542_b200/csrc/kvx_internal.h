@@ -77,6 +77,7 @@ struct ConvArgs {
   FastDiv f_dch, f_in0, f_in1, f_l, f_bl, f_hp, f_bp, f_bd;
   int32_t slot_inner;  // 1: slot is the faster of (slot, head)
   uint32_t total;      // chunks in this launch (flat kernel)
+  uint64_t total64;    // chunks in this launch (row kernel: one launch up to 2^31 rows)
   // row-tiled fast path: work item = (dst rank, dst block, layer, K/V, row group)
   FastDiv f_cpr;       // 8-element chunks per head_dim row (D / 8)
   FastDiv f_items;     // row groups per (dst rank, dst block, layer, K/V) tile

@@ -1896,7 +1896,7 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
     const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.Hd_eff + th - 1) / th;
     a.f_sb = make_fastdiv(nsb);
     a.f_items = make_fastdiv(nsb * nhb);
-    a.n_items = (uint32_t)((uint64_t)a.total / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);
+    a.n_items = (uint32_t)(a.total64 / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);
     // 1-byte sources: 16-element chunks (whole 16-B loads, 4 in flight = 64 B per lane, like
     // the 2-byte sources' 8-element chunks); KVX_FP8_VEC16=0 reverts to 8-element chunks
     static const int wide1 = getenv("KVX_FP8_VEC16") ? atoi(getenv("KVX_FP8_VEC16")) : 1;
@@ -2054,7 +2054,7 @@ cudaError_t launch_convert_tr8(const ConvArgs& a, int sdt, int ddt, cudaStream_t
   return tr8_v<8>(a, sdt, ddt, s);
 }
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s) {
-  if (a.total == 0) return cudaSuccess;
+  if (a.total64 == 0) return cudaSuccess;
   return vec == 8 ? conv_v<8>(a, sdt, ddt, s) : conv_v<1>(a, sdt, ddt, s);
 }
 cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s) {

@@ -61,20 +61,27 @@ def launches(csvf, out):
     rows = list(csv.reader(io.StringIO(txt[start:])))
     hdr = rows[0]
     ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    mi = hdr.index("Metric Name")
     agg = {}
     for r in rows[1:]:
         if len(r) <= vi:
             continue
         name = r[ki].split("(")[0][:120]
         v = _num(r[vi])
-        v *= {"msecond": 1e3, "ms": 1e3, "nsecond": 1e-3, "ns": 1e-3}.get(r[ui], 1.0)
         a = agg.setdefault(name, {"launches": 0, "us_total": 0.0})
-        a["launches"] += 1
-        a["us_total"] += v
+        if r[mi] == "gpu__time_duration.sum":
+            v *= {"msecond": 1e3, "ms": 1e3, "nsecond": 1e-3, "ns": 1e-3}.get(r[ui], 1.0)
+            a["launches"] += 1
+            a["us_total"] += v
+        elif r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            v *= {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0, "Tbyte": 1e12}.get(r[ui], 1.0)
+            a["dram_bytes_total"] = a.get("dram_bytes_total", 0.0) + v
     tot = sum(a["us_total"] for a in agg.values())
     for a in agg.values():
         a["share"] = round(a["us_total"] / tot, 4) if tot else None
-        a["us_mean"] = round(a["us_total"] / a["launches"], 2)
+        a["us_mean"] = round(a["us_total"] / a["launches"], 2) if a["launches"] else None
+        if "dram_bytes_total" in a and a["launches"]:
+            a["dram_bytes_per_launch"] = round(a.pop("dram_bytes_total") / a["launches"])
     res = dict(sorted(agg.items(), key=lambda kv: -kv[1]["us_total"]))
     json.dump({"source": os.path.basename(csvf), "note": "ncu --metrics gpu__time_duration.sum --clock-control none "
                "(cold-cache, serialised: compare shares)", "kernels": res}, open(out, "w"), indent=1)
