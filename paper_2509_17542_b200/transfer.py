@@ -311,3 +311,60 @@ def nccl_recv_step(comm, src_layouts, dst_layout, dst_pool, dst_batch, src_world
     comm.recv_pipelined([src_layouts[p] for p in ps], [src_world[p] for p in ps], dst_layout, dst_pool, dst_batch,
                         [wires[(p, b)] for p in ps for b in range(2)], cap, layer_chunk, None, stream, recv_stream,
                         unpack_stream)
+
+
+class HostStaged:
+    """The paper's own transport (P:95 steps 3/5/6), kept as the baseline the NVLink
+    path replaces (NEXT-3): P packs each layer chunk (Fig. 5 flatten + the sender-side cast)
+    and copies it into a pinned host "CPU buffer"; the transfer engine moves it to D's CPU
+    buffer (here both instances share one host, so the buffer is shared: the stand-in RDMA
+    read costs nothing, which makes this the fastest host-staged path the box allows); D
+    copies it up and unpacks it into its pool.  Every chunk is a chain of device work with
+    event edges only (no host round trip): P's stream packs and copies down, D's stream waits
+    for that copy, copies up and unpacks; a host slot is reused after the copy up that read it.
+    P and D may be the same GPU or two GPUs of one process."""
+
+    def __init__(self, src_layout, dst_layout_at_p, dst_layout, total_tokens, layer_range, layer_chunk, p_device,
+                 d_device, slots=3):
+        import torch
+        lb, le = layer_range
+        self.chunks = [(l0, min(le, l0 + layer_chunk)) for l0 in range(lb, le, layer_chunk)]
+        self.nbytes = [kv.wire_bytes(src_layout, dst_layout, total_tokens, c) for c in self.chunks]
+        cap = max(self.nbytes + [16])
+        self.R = max(1, min(slots, len(self.chunks)))
+        self.wp = [torch.empty(cap, dtype=torch.uint8, device=p_device) for _ in range(self.R)]
+        self.wd = [torch.empty(cap, dtype=torch.uint8, device=d_device) for _ in range(self.R)]
+        self.host = [torch.empty(cap, dtype=torch.uint8, pin_memory=True) for _ in range(self.R)]
+        self.sp = torch.cuda.Stream(device=p_device)
+        self.sd = torch.cuda.Stream(device=d_device)
+        self.p_device, self.d_device = p_device, d_device
+        self.S, self.Dp, self.D = src_layout, dst_layout_at_p, dst_layout
+
+    def step(self, src_pool, src_batch, dst_pool, dst_batch, stream_p=None, stream_d=None):
+        """Enqueue one transfer; stream_p / stream_d (optional) wait for all of it."""
+        import torch
+        sp, sd = self.sp, self.sd
+        if stream_p is not None:
+            sp.wait_stream(stream_p)
+        if stream_d is not None:
+            sd.wait_stream(stream_d)
+        up_done = [None] * self.R
+        for k, (lr, n) in enumerate(zip(self.chunks, self.nbytes)):
+            b = k % self.R
+            with torch.cuda.device(self.p_device), torch.cuda.stream(sp):
+                if up_done[b] is not None:
+                    sp.wait_event(up_done[b])       # D copied this host slot up already
+                kv.pack(self.S, src_pool, src_batch, self.Dp, self.wp[b], lr, sp, wire_nbytes=n)
+                self.host[b][:n].copy_(self.wp[b][:n], non_blocking=True)   # P -> CPU buffer
+                down = torch.cuda.Event()
+                down.record(sp)
+            with torch.cuda.device(self.d_device), torch.cuda.stream(sd):
+                sd.wait_event(down)
+                self.wd[b][:n].copy_(self.host[b][:n], non_blocking=True)  # CPU buffer -> D
+                up_done[b] = torch.cuda.Event()
+                up_done[b].record(sd)
+                kv.unpack(self.S, self.D, dst_pool, dst_batch, self.wd[b], lr, sd, wire_nbytes=n)
+        if stream_p is not None:
+            stream_p.wait_stream(sp)
+        if stream_d is not None:
+            stream_d.wait_stream(sd)

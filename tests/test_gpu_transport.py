@@ -282,3 +282,25 @@ def test_sm_budget_parity(o1, budget, share):
     finally:
         assert kvx.set_sm_budget(prev) == budget
     assert_pools_match(dc.dst_numpy(), expected(case, o1), E4M3)
+
+
+@pytest.mark.parametrize("shape", ["identity_fp8", "merge"])
+def test_host_staged_one_gpu(o1, shape):
+    """NEXT-3: the paper's host-staged transport (pack -> D2H into a pinned CPU buffer -> H2D ->
+    unpack, event-chained per layer chunk, 2 host slots reused) with P and D on cuda:0: the D
+    pools equal O1's."""
+    import paper_2509_17542_b200 as kvx
+    from paper_2509_17542_b200 import transfer as tr
+    from tests.gpu_util import DevCase
+    from tests.test_gpu_parity import assert_pools_match
+    case = _case(shape, o1)
+    dc = DevCase(case, "cuda:0")
+    S, D = dc.src_lays, dc.dst_lays
+    DP = _p_view_of_d(kvx, case, False)
+    L = S[0].num_layers
+    torch.cuda.synchronize()
+    for p, q, _, _ in kvx.plan_pairs(S[0].tp_degree, D[0].tp_degree, S[0].num_kv_heads):
+        hs = tr.HostStaged(S[p], DP[q], D[q], dc.src_bt.total_tokens, (0, L), 2, 0, 0, slots=2)
+        hs.step(dc.src_pools[p], dc.src_bt, dc.dst_pools[q], dc.dst_bt)
+        torch.cuda.synchronize()
+    assert_pools_match(dc.dst_numpy(), expected(case, o1), case["dst_lays"][0]["dtype"])

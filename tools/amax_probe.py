@@ -15,7 +15,8 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import synth  # noqa: E402
-from bench import Workload, load_peaks  # noqa: E402
+from bench import load_peaks  # noqa: E402
+from tools._workload import Workload  # noqa: E402
 
 
 def main():

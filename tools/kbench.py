@@ -14,7 +14,8 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import synth  # noqa: E402
-from bench import Workload, load_peaks, sample_parity  # noqa: E402
+from bench import load_peaks  # noqa: E402
+from tools._workload import Workload, sample_parity  # noqa: E402
 
 
 def time_it(fn, iters=20, warm=3):

@@ -26,7 +26,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import synth  # noqa: E402
-from bench import Workload  # noqa: E402
+from tools._workload import Workload  # noqa: E402
 
 
 def main():
@@ -155,7 +155,7 @@ def main():
     if pull:
         res["err"] = int(err0.item()) + int(err1.item())
         dst.src_pools[0], dst.src_dicts[0] = SP, src.src_dicts[0]
-        from bench import sample_parity
+        from tools._workload import sample_parity
         res["parity_ok"] = sample_parity(dst, (0, 1), 0, [0], [0])[0]
     print(json.dumps(res), flush=True)
 

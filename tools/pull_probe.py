@@ -19,7 +19,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 import synth  # noqa: E402
-from bench import Workload, sample_parity  # noqa: E402
+from tools._workload import Workload, sample_parity  # noqa: E402
 
 
 def main():
