@@ -618,6 +618,35 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
       if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
       const uint64_t per_layer = (uint64_t)n_dst * dst_bt->total_blocks * (a.kv1 ? 1 : 2) * a.Hd_eff;
       const int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / std::max<uint64_t>(per_layer, 1));
+      // head_dim-major 2-byte source tiles of 16 slots into D's rows: whole tiles through TMA
+      // (k_convert_tb), unless KVX_TB=0
+      TbArgs tb;
+      memset(&tb, 0, sizeof(tb));
+      bool use_tb = false;
+      {
+        const char* tb_env = getenv("KVX_TB");
+        const int32_t Dm = S->d.head_dim;
+        encode_tiled_fn enc = encode_fn();
+        use_tb = use_tr8 && st == 1 && dt == 0 && S->elem_bytes <= 2 && S->d.block_size == 16 &&
+                 D->d.block_size == 16 && (Dm == 64 || Dm == 128 || Dm == 256) && enc && !(tb_env && atoi(tb_env) == 0);
+        for (int i = 0; i < n_src && use_tb; ++i) {
+          const uint64_t rows = src[i]->pool_bytes / 128;
+          if (src[i]->pool_bytes % 128 || rows >= (1ull << 31) || !ptr_aligned(src_pools[i], 16)) {
+            use_tb = false;
+            break;
+          }
+          cuuint64_t dims[2] = {128, (cuuint64_t)rows};
+          cuuint64_t strides[1] = {128};
+          cuuint32_t box[2] = {128, (cuuint32_t)(Dm * S->elem_bytes / 8)};   // 16 x D elements / 128 B
+          cuuint32_t estr[2] = {1, 1};
+          if (enc(&tb.maps[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(src_pools[i]), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            use_tb = false;
+        }
+        tb.tile_rows = Dm * S->elem_bytes / 8;
+        tb.stages = Dm * S->elem_bytes >= 512 ? 6 : 8;
+      }
       for (int32_t l0 = lb; l0 < le; l0 += step) {
         const int32_t l1 = std::min(le, l0 + step);
         a.lb = l0;
@@ -625,7 +654,11 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
         a.f_l = make_fastdiv((uint32_t)a.Lc);
         a.n_items = (uint32_t)(per_layer * (uint64_t)a.Lc);
         cudaError_t e;
-        if (use_tr8) {
+        if (use_tb) {
+          t_last_kernel = "k_convert_tb";
+          tb.c = a;
+          e = launch_convert_tb(tb, S->d.dtype, D->d.dtype, (cudaStream_t)stream);
+        } else if (use_tr8) {
           t_last_kernel = "k_convert_tr8";
           e = launch_convert_tr8(a, S->d.dtype, D->d.dtype, (cudaStream_t)stream);
         } else {

@@ -237,6 +237,19 @@ cudaError_t launch_convert_tr(const ConvArgs& a, int sdt, int ddt, cudaStream_t 
 cudaError_t launch_convert_tr8(const ConvArgs& a, int sdt, int ddt, cudaStream_t s);
 constexpr int kTrSmemLimit = 200 * 1024;  // per CTA (4 warps x one Bd x D tile each)
 cudaError_t launch_tile_copy(const TileArgs& a, cudaStream_t s);
+
+// Head_dim-major source tiles through TMA (k_convert_tb): a (block, head) tile of a
+// (DIM, SLOT)-innermost source is B x D contiguous elements; one 2-D tensor load (128-B rows,
+// 128B swizzle) per tile lands it in shared memory, consumer warps transpose 8 x 8 sub-blocks
+// out of it (conflict-free thanks to the swizzle) into D's (SLOT, DIM) rows.  The ConvArgs
+// are those of k_convert_tr8; maps[i] views source pool i as rows of 128 bytes.
+struct TbArgs {
+  ConvArgs c;
+  CUtensorMap maps[KVX_MAX_RANKS];
+  int32_t tile_rows;  // 128-B rows per tile (B * D * esize / 128)
+  int32_t stages;
+};
+cudaError_t launch_convert_tb(const TbArgs& a, int sdt, int ddt, cudaStream_t s);
 cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s);
 cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaStream_t s);
 cudaError_t launch_signal(uint32_t* flag, uint32_t value, cudaStream_t s);

@@ -317,6 +317,9 @@ __device__ __forceinline__ uint32_t half2_times_128(uint32_t h) {
 #ifndef KVX_FNUZ_SHIFT
 #define KVX_FNUZ_SHIFT 1
 #endif
+#ifndef KVX_FNUZ_FOLD
+#define KVX_FNUZ_FOLD 1  // row kernel: e4m3fnuz decode with 2^-7 folded into the source scale
+#endif
 template <int DT>
 __device__ __forceinline__ void fp8x4_to_f32(uint32_t w, float* f) {
   uint32_t h[2];
@@ -369,10 +372,91 @@ __device__ __forceinline__ void fp8x4_to_f32(uint32_t w, float* f) {
   }
 }
 
+// Pack VEC f32 values (already scaled) into a DDT chunk (RNE; satfinite for the fp8 types)
+template <int DDT, int VEC>
+__device__ __forceinline__ void cast_out(const float* f, Chunk<DDT, VEC>& out) {
+#pragma unroll
+  for (int i = 0; i < Chunk<DDT, VEC>::WORDS; ++i) out.w[i] = 0;
+  if constexpr (DDT == KV_F8E4M3) {
+    if constexpr (VEC == 1) {
+      out.w[0] = f32x2_to_e4m3x2(f[0], 0.0f) & 0xFFu;
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; i += 2) out.w[i >> 2] |= f32x2_to_e4m3x2(f[i], f[i + 1]) << ((i & 3) * 8);
+    }
+  } else if constexpr (DDT == KV_F8E4M3FNUZ) {
+    if constexpr (VEC == 1) {
+      out.w[0] = f32x2_to_fnuzx2(f[0], 0.0f) & 0xFFu;
+    } else if constexpr (VEC % 4 == 0) {
+#pragma unroll
+      for (int i = 0; i < VEC; i += 4) out.w[i >> 2] = f32x4_to_fnuzx4(f + i);
+    } else {
+#pragma unroll
+      for (int i = 0; i < VEC; i += 2) out.w[i >> 2] |= f32x2_to_fnuzx2(f[i], f[i + 1]) << ((i & 3) * 8);
+    }
+  } else if constexpr (DDT == KV_F32) {
+    // bf16 -> f32 is a bit shift that would keep NaN payloads; reading 12 wants the
+    // canonical NaN on every cast output (cvt.f32.f16 and FMUL already canonicalise)
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) out.w[i] = (f[i] != f[i]) ? 0x7FFFFFFFu : __float_as_uint(f[i]);
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      uint32_t h = (DDT == KV_F16) ? f32_to_f16(f[i]) : f32_to_bf16(f[i]);
+      out.w[i >> 1] |= h << ((i & 1) * 16);
+    }
+  }
+}
+
+// e4m3fnuz codes -> 2^-7 x their values as f32, without the NaN patch: each code's 7
+// magnitude bits at f16 bits 7..13 with its sign at 15 read as an f16 ARE 2^-7 x the fnuz
+// value (normals 2^(e-15)(1 + m/8), subnormals (m/8) 2^-14; 0x7F / 0xFF are +-1.875), and
+// the f16 -> f32 widening is exact.  0x80 (fnuz's NaN) decodes to -0 here: callers route
+// chunks holding it to the exact decode (fp8x4_to_f32).
+__device__ __forceinline__ void fnuzx4_to_f32_scaled(uint32_t w, float* f) {
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint32_t x = __byte_perm(w, 0u, k ? 0x3424u : 0x1404u);  // codes 2k, 2k+1 at bits 8..15 / 24..31
+    const uint32_t y = x >> 1;
+    const uint32_t h = y + (y & 0x40004000u);                      // sign moved to 15 / 31
+    const float2 ff = __half22float2(*reinterpret_cast<const __half2*>(&h));
+    f[2 * k] = ff.x;
+    f[2 * k + 1] = ff.y;
+  }
+}
+// any byte of w equal to 0x80 (exact: the classic zero-byte test on w ^ 0x80808080)
+__device__ __forceinline__ uint32_t has_byte80(uint32_t w) {
+  const uint32_t z = w ^ 0x80808080u;
+  return (z - 0x01010101u) & ~z & 0x80808080u;
+}
+
 // Cast a chunk SDT -> DDT.  ssc: dequant scale of an fp8 source; inv: RN(1/s) of an fp8
 // destination (an fp8 -> other-fp8 cast applies both, in that order).
-template <int SDT, int DDT, int VEC>
+// FOLD (e4m3fnuz sources in the row kernel): ssc arrives as 2^7 s (exact) -- the decode's
+// 2^-7 is folded into it, so RN(f32(2^-7 q) * 2^7 s) = RN(q * s) with no separate rescale --
+// or as -s when 2^7 s would overflow; a chunk with a 0x80 code (NaN) or a negative ssc
+// takes the exact per-code decode with the plain scale instead (rare: not on random data).
+template <int SDT, int DDT, int VEC, bool FOLD = false>
 __device__ __forceinline__ void cast_chunk(const Chunk<SDT, VEC>& in, Chunk<DDT, VEC>& out, float ssc, float inv) {
+  if constexpr (FOLD && SDT == KV_F8E4M3FNUZ && DDT != KV_F8E4M3FNUZ && VEC % 4 == 0) {
+    uint32_t nan = 0;
+#pragma unroll
+    for (int i = 0; i < VEC; i += 4) nan |= has_byte80(in.w[i >> 2]);
+    if (nan == 0 && ssc >= 0.f) {
+      float f[VEC];
+#pragma unroll
+      for (int i = 0; i < VEC; i += 4) fnuzx4_to_f32_scaled(in.w[i >> 2], f + i);
+#pragma unroll
+      for (int i = 0; i < VEC; i += 2) {
+        fmul2_rn(f[i], f[i + 1], ssc);
+        if constexpr (is_fp8(DDT)) fmul2_rn(f[i], f[i + 1], inv);
+      }
+      cast_out<DDT, VEC>(f, out);
+    } else {
+      cast_chunk<SDT, DDT, VEC, false>(in, out, ssc >= 0.f ? __fmul_rn(ssc, 0.0078125f) : -ssc, inv);
+    }
+    return;
+  }
   if constexpr (SDT == DDT) {
 #pragma unroll
     for (int i = 0; i < Chunk<SDT, VEC>::WORDS; ++i) out.w[i] = in.w[i];
@@ -398,37 +482,7 @@ __device__ __forceinline__ void cast_chunk(const Chunk<SDT, VEC>& in, Chunk<DDT,
         if constexpr (is_fp8(DDT)) f[i] = __fmul_rn(f[i], inv);
       }
     }
-#pragma unroll
-    for (int i = 0; i < Chunk<DDT, VEC>::WORDS; ++i) out.w[i] = 0;
-    if constexpr (DDT == KV_F8E4M3) {
-      if constexpr (VEC == 1) {
-        out.w[0] = f32x2_to_e4m3x2(f[0], 0.0f) & 0xFFu;
-      } else {
-#pragma unroll
-        for (int i = 0; i < VEC; i += 2) out.w[i >> 2] |= f32x2_to_e4m3x2(f[i], f[i + 1]) << ((i & 3) * 8);
-      }
-    } else if constexpr (DDT == KV_F8E4M3FNUZ) {
-      if constexpr (VEC == 1) {
-        out.w[0] = f32x2_to_fnuzx2(f[0], 0.0f) & 0xFFu;
-      } else if constexpr (VEC % 4 == 0) {
-#pragma unroll
-        for (int i = 0; i < VEC; i += 4) out.w[i >> 2] = f32x4_to_fnuzx4(f + i);
-      } else {
-#pragma unroll
-        for (int i = 0; i < VEC; i += 2) out.w[i >> 2] |= f32x2_to_fnuzx2(f[i], f[i + 1]) << ((i & 3) * 8);
-      }
-    } else if constexpr (DDT == KV_F32) {
-      // bf16 -> f32 is a bit shift that would keep NaN payloads; reading 12 wants the
-      // canonical NaN on every cast output (cvt.f32.f16 and FMUL already canonicalise)
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) out.w[i] = (f[i] != f[i]) ? 0x7FFFFFFFu : __float_as_uint(f[i]);
-    } else {
-#pragma unroll
-      for (int i = 0; i < VEC; ++i) {
-        uint32_t h = (DDT == KV_F16) ? f32_to_f16(f[i]) : f32_to_bf16(f[i]);
-        out.w[i >> 1] |= h << ((i & 1) * 16);
-      }
-    }
+    cast_out<DDT, VEC>(f, out);
   }
 }
 
@@ -584,7 +638,7 @@ struct ChunkMap {
   int64_t shs, dhs;
 };
 
-template <int SDT, int DDT, int U, int VEC = 8, bool COH = false, bool SPLIT = false>
+template <int SDT, int DDT, int U, int VEC = 8, bool COH = false, bool SPLIT = false, bool FOLD = false>
 __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t sp, uint64_t dp, float rsc,
                                             uint32_t rz, float rsc2 = 1.f, const ChunkMap* cm = nullptr) {
   constexpr bool DUAL = dual_scale(SDT, DDT);
@@ -617,9 +671,9 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
       if (z[k])
         zero_chunk(o);
       else if constexpr (DUAL)
-        cast_chunk<SDT, DDT, VEC>(in[k], o, sc[k], sc2[k]);
+        cast_chunk<SDT, DDT, VEC, FOLD>(in[k], o, sc[k], sc2[k]);
       else
-        cast_chunk<SDT, DDT, VEC>(in[k], o, sc[k], sc[k]);
+        cast_chunk<SDT, DDT, VEC, FOLD>(in[k], o, sc[k], sc[k]);
       uint64_t doff = ch[k] * (VEC * Tr<DDT>::B);
       if constexpr (SPLIT)
         doff = (uint64_t)(ch[k] >> cm->dk) * (uint64_t)cm->dhs + (ch[k] & ((1u << cm->dk) - 1u)) * (VEC * Tr<DDT>::B);
@@ -640,7 +694,13 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
 // ------------------------------------------------------------------------------------
 // Per-lane row state of convert item `item` (see k_convert_rows): lane = row of the
 // 2-D sub-tile.  rz: 0 copy, 1 zero-fill tail row, 2 no row.
-template <int SDT, int DDT>
+// 2^7 s for the folded e4m3fnuz decode (exact), or -s when it would overflow (cast_chunk)
+__device__ __forceinline__ float fnuz_fold_scale(float s) {
+  const float f = __fmul_rn(s, 128.0f);
+  return f <= 3.402823466e38f ? f : -s;
+}
+
+template <int SDT, int DDT, bool FOLD = false>
 __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint32_t lane, uint64_t& sp,
                                          uint64_t& dp, float& rsc, uint32_t& rz, float& rsc2) {
   // destination fastest: with several D ranks (fan-out, e.g. a TP split pushed over
@@ -699,6 +759,7 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
         if constexpr (is_fp8(SDT) && SDT != DDT) rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
         if constexpr (is_fp8(DDT) && SDT != DDT) rsc = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
       }
+      if constexpr (FOLD) rsc = fnuz_fold_scale(rsc);
     }
   }
 }
@@ -710,12 +771,14 @@ __global__ void __launch_bounds__(kThreads, row_minb(SDT, DDT)) k_convert_rows(c
   const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
   const uint32_t cs = (uint32_t)a.cpr_shift;
   const ChunkMap cm{a.s_ck, a.d_ck, a.s_chs, a.d_chs};
+  // e4m3fnuz source to another type: the decode's 2^-7 folded into the source scale
+  constexpr bool FOLD = KVX_FNUZ_FOLD && SDT == KV_F8E4M3FNUZ && DDT != KV_F8E4M3FNUZ && VEC % 4 == 0;
   for (uint32_t item = warp; item < a.n_items; item += nwarps) {
     uint64_t sp, dp;
     float rsc, rsc2;
     uint32_t rz;
-    conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz, rsc2);
-    stream_rows<SDT, DDT, U, VEC, false, SPLIT>(lane, cs, sp, dp, rsc, rz, rsc2, &cm);
+    conv_row<SDT, DDT, FOLD>(a, item, lane, sp, dp, rsc, rz, rsc2);
+    stream_rows<SDT, DDT, U, VEC, false, SPLIT, FOLD>(lane, cs, sp, dp, rsc, rz, rsc2, &cm);
   }
 }
 
@@ -1125,6 +1188,8 @@ __global__ void __launch_bounds__(kTr8Threads, W16 ? 2 : 1) k_convert_tr8(const 
   const uint32_t lnsub = (lbd - (w16 ? 4u : 3u)) + lcpr;  // log2 sub-blocks per item
   const uint32_t ngroups = (a.n_items + 31u) >> 5;
   const bool s_col = a.s_tr == 1, d_col = a.d_tr == 1;
+  // e4m3fnuz source to another type: the decode's 2^-7 folded into the source scale
+  constexpr bool FOLD = KVX_FNUZ_FOLD && SDT == KV_F8E4M3FNUZ && DDT != KV_F8E4M3FNUZ;
   for (uint32_t grp = warp; grp < ngroups; grp += nwarps) {
     // ---- lane-parallel metadata of item grp * 32 + lane ----
     const uint32_t item = (grp << 5) + lane;
@@ -1161,6 +1226,7 @@ __global__ void __launch_bounds__(kTr8Threads, W16 ? 2 : 1) k_convert_tr8(const 
         if constexpr (is_fp8(DDT) && SDT != DDT) m_rsc = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
         m_s2 = m_rsc;
       }
+      if constexpr (FOLD) m_rsc = fnuz_fold_scale(m_rsc);
       m_valid = (int32_t)tb0 >= T ? 0u : min(1u << lbd, (uint32_t)T - tb0);
       m_sids = a.s_blk_ids + __ldg(a.s_blk_off + r) + (int32_t)(tb0 >> lbp);
       if (m_valid) m_sblk0 = __ldg(m_sids);
@@ -1213,7 +1279,7 @@ __global__ void __launch_bounds__(kTr8Threads, W16 ? 2 : 1) k_convert_tr8(const 
               transpose8<SDT>(x, y);
 #pragma unroll
               for (int k = 0; k < 8; ++k) {
-                cast_chunk<SDT, DDT, 8>(y[k], o[k], rsc, s2);
+                cast_chunk<SDT, DDT, 8, FOLD>(y[k], o[k], rsc, s2);
                 if (s1 + (uint32_t)k >= valid) zero_chunk(o[k]);
               }
             }
@@ -1256,10 +1322,10 @@ __global__ void __launch_bounds__(kTr8Threads, W16 ? 2 : 1) k_convert_tr8(const 
           Chunk<SDT, 8> y[8];
           transpose8<SDT>(x, y);
 #pragma unroll
-          for (int k = 0; k < 8; ++k) cast_chunk<SDT, DDT, 8>(y[k], o[k], rsc, s2);
+          for (int k = 0; k < 8; ++k) cast_chunk<SDT, DDT, 8, FOLD>(y[k], o[k], rsc, s2);
         } else {
 #pragma unroll
-          for (int k = 0; k < 8; ++k) cast_chunk<SDT, DDT, 8>(x[k], o[k], rsc, s2);
+          for (int k = 0; k < 8; ++k) cast_chunk<SDT, DDT, 8, FOLD>(x[k], o[k], rsc, s2);
         }
         if (s0 + 8u > valid) {  // slots past the request's last token are zero
           if (d_col) {
@@ -1384,6 +1450,200 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
       }
     }
     stream_rows<WDT, DDT, U>(lane, cs, sp, dp, rsc, rz, rsc2);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K1 for head_dim-major (DIM, SLOT) source tiles through TMA (k_convert_tb).  A (block,
+// head) tile of such a pool -- B x D elements -- is contiguous, so warp 0 of each CTA (the
+// producer) issues ONE 2-D tensor load per tile (rows of 128 B, 128B swizzle) into a ring of
+// shared-memory stages, and NC consumer warps each take a whole tile: lane (d_sub, s_sub)
+// reads its 8 x 8 sub-block's eight 16-B rows from the swizzled stage (the swizzle makes the
+// eight lanes of every LDS.128 phase hit distinct banks), transposes it in registers, casts
+// and stores eight rows of D's (SLOT, DIM) tile.  The HBM side sees only whole 4-KB tile reads
+// issued by the TMA engine (k_convert_tr8's per-lane 16-B loads left it at ~0.8 of copy).
+// Metadata of 32 items at a time is computed lane-parallel by the producer (one dependent-load
+// round trip per 32 tiles) and handed to the consumers through the stage's slot.
+// ------------------------------------------------------------------------------------
+constexpr int kTbConsumers = 4;
+
+struct TbMeta {
+  uint8_t* db;
+  uint32_t valid;
+  float rsc, s2;
+};
+
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// mbar_wait with a watchdog: a pipeline bug must not hang the GPU -- after ~4 s the kernel
+// traps (the launch then fails with an error instead of spinning forever)
+__device__ __forceinline__ void mbar_wait_guarded(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (it > (1u << 22)) __trap();
+    __nanosleep(64);
+  }
+}
+
+// 8 consecutive elements (8 or 16 bytes) from a 32-bit shared-memory address
+template <int DT>
+__device__ __forceinline__ void lds_chunk8(Chunk<DT, 8>& c, uint32_t saddr) {
+  if constexpr (Tr<DT>::B == 2) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3])
+                 : "r"(saddr));
+  } else {
+    static_assert(Tr<DT>::B == 1, "lds_chunk8: 1- or 2-byte elements");
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(c.w[0]), "=r"(c.w[1]) : "r"(saddr));
+  }
+}
+
+template <int SDT, int DDT>
+__global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __grid_constant__ TbArgs A) {
+  constexpr uint32_t DB = Tr<DDT>::B, SB = Tr<SDT>::B;
+  static_assert(SB == 1 || SB == 2, "k_convert_tb: 1- or 2-byte sources");
+  const ConvArgs& a = A.c;
+  // e4m3fnuz source: the decode's 2^-7 folded into the source scale (cast_chunk)
+  constexpr bool FOLD = KVX_FNUZ_FOLD && SDT == KV_F8E4M3FNUZ && DDT != KV_F8E4M3FNUZ;
+  extern __shared__ __align__(1024) uint8_t tb_smem[];
+  // 1024-B aligned stages (the 128B swizzle pattern repeats every 1024 B)
+  uint8_t* stages = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tb_smem) + 1023) & ~uintptr_t(1023));
+  const uint32_t S = (uint32_t)A.stages;
+  const uint32_t tile_bytes = (uint32_t)A.tile_rows * 128u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)S * tile_bytes);
+  uint64_t* empty = full + S;
+  TbMeta* meta = reinterpret_cast<TbMeta*>(empty + S);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // this CTA's items: blockIdx.x + t * gridDim.x
+  const uint32_t n_mine = a.n_items > blockIdx.x ? (a.n_items - 1u - blockIdx.x) / gridDim.x + 1u : 0u;
+  const uint32_t lbp = (uint32_t)a.tr_lbp, lbd = (uint32_t)a.tr_lbd;
+  if (warp == 0) {
+    // ---- producer ----
+    for (uint32_t g = 0; g < n_mine; g += 32u) {
+      const uint32_t cnt = min(32u, n_mine - g);
+      uint8_t* m_db = nullptr;
+      uint32_t m_valid = 0, m_row = 0, m_si = 0;
+      float m_rsc = 1.f, m_s2 = 1.f;
+      if (lane < cnt) {
+        uint32_t n = blockIdx.x + (g + lane) * gridDim.x;
+        const uint32_t hl = divmod(n, a.f_hde);
+        const uint32_t c = take_kv(n, a.kv1, a.c0);
+        const uint32_t l = divmod(n, a.f_l);
+        const uint32_t bl = divmod(n, a.f_bl);
+        const uint32_t qi = n;
+        const uint32_t hq = (uint32_t)a.hq_off[qi] + hl;
+        const int32_t r = __ldg(a.d_blk_req + bl);
+        const int32_t tok0 = __ldg(a.tok_off + r);
+        const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+        const uint32_t tb0 = (uint32_t)(bl - __ldg(a.d_blk_off + r)) << lbd;
+        const int64_t layer = a.lb + (int64_t)l;
+        const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;
+        const uint32_t h = (uint32_t)a.dst_rank[qi] * (uint32_t)a.Hd + hq;
+        const uint32_t p = fdiv(h, a.f_hp);
+        const uint32_t hp = h - p * (uint32_t)a.Hp;
+        const int si = a.src_of_p[p];
+        if constexpr (dual_scale(SDT, DDT)) {
+          m_rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+          m_s2 = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+        } else {
+          if constexpr (is_fp8(SDT) && SDT != DDT) m_rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+          if constexpr (is_fp8(DDT) && SDT != DDT) m_rsc = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+          m_s2 = m_rsc;
+        }
+        if constexpr (FOLD) m_rsc = fnuz_fold_scale(m_rsc);
+        m_valid = (int32_t)tb0 >= T ? 0u : min(1u << lbd, (uint32_t)T - tb0);
+        const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + (int32_t)(tb0 >> lbp));
+        const int64_t off = sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
+                            (int64_t)hp * a.ss[KV_AX_HEAD];  // elements; the tile starts here
+        m_row = (uint32_t)((off * (int64_t)SB) >> 7);
+        m_si = (uint32_t)si;
+        m_db = a.dst[qi] + (dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] +
+                            (int64_t)__ldg(a.d_blk_ids + bl) * a.ds[KV_AX_BLOCK] + (int64_t)hq * a.ds[KV_AX_HEAD]) *
+                               DB;
+      }
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const uint64_t db = __shfl_sync(0xFFFFFFFFu, (unsigned long long)m_db, j);
+        const uint32_t valid = __shfl_sync(0xFFFFFFFFu, m_valid, j);
+        const uint32_t row = __shfl_sync(0xFFFFFFFFu, m_row, j);
+        const uint32_t si = __shfl_sync(0xFFFFFFFFu, m_si, j);
+        const float rsc = __shfl_sync(0xFFFFFFFFu, m_rsc, j);
+        const float s2 = __shfl_sync(0xFFFFFFFFu, m_s2, j);
+        if (lane == 0) {
+          const uint32_t t = g + j, st = t % S;
+          mbar_wait_guarded(empty + st, ((t / S) & 1u) ^ 1u);
+          meta[st] = TbMeta{reinterpret_cast<uint8_t*>(db), valid, rsc, s2};
+          mbar_expect_tx_arrive(full + st, tile_bytes);
+          tma_load_2d(stages + (size_t)st * tile_bytes, &A.maps[si], 0, (int32_t)row, full + st);
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
+  // ---- consumers ----
+  const uint32_t cw = warp - 1u;
+  const uint32_t lcpr = (uint32_t)a.cpr_shift;           // log2(D / 8)
+  const uint32_t nsub = 2u << lcpr;                       // (B = 16) / 8 x D / 8 sub-blocks
+  const uint32_t row_bytes = 16u * SB;                    // one head_dim element's 16 slots
+  const uint32_t stage0 = smem_u32(stages);
+  for (uint32_t t = cw; t < n_mine; t += kTbConsumers) {
+    const uint32_t st = t % S;
+    mbar_wait_guarded(full + st, (t / S) & 1u);
+    const TbMeta m = meta[st];
+    const uint32_t tile = stage0 + st * tile_bytes;
+    for (uint32_t u = lane; u < nsub; u += 32u) {
+      const uint32_t s_sub = u & 1u, d_sub = u >> 1;
+      const uint32_t s0 = s_sub << 3, d0 = d_sub << 3;
+      Chunk<DDT, 8> o[8];
+      if (s0 >= m.valid) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) zero_chunk(o[k]);
+      } else {
+        Chunk<SDT, 8> x[8], y[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          // logical byte offset of (head_dim d0 + k, slots s0..s0+7) in the tile, then the
+          // TMA 128B swizzle: 16-B unit c of 128-B row R sits at unit c ^ (R mod 8)
+          const uint32_t off = (d0 + (uint32_t)k) * row_bytes + s0 * SB;
+          const uint32_t R = off >> 7, c = (off >> 4) & 7u;
+          lds_chunk8<SDT>(x[k], tile + R * 128u + ((c ^ (R & 7u)) << 4) + (off & 15u));
+        }
+        transpose8<SDT>(x, y);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          cast_chunk<SDT, DDT, 8, FOLD>(y[k], o[k], m.rsc, m.s2);
+          if (s0 + (uint32_t)k >= m.valid) zero_chunk(o[k]);
+        }
+      }
+      const int64_t doff = dim_off(d0, a.ds[KV_AX_DIM], a.d_dk);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) store_chunk<DDT, 8>(m.db + ((int64_t)(s0 + k) * a.ds[KV_AX_SLOT] + doff) * DB, o[k]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
   }
 }
 
@@ -2049,6 +2309,45 @@ cudaError_t launch_convert_tr(const ConvArgs& a, int sdt, int ddt, cudaStream_t 
   return tr_v<8>(a, sdt, ddt, s);
 }
 
+namespace {
+template <int SDT, int DDT>
+cudaError_t tb_t(const TbArgs& a, cudaStream_t s) {
+  auto k = k_convert_tb<SDT, DDT>;
+  const size_t tile = (size_t)a.tile_rows * 128u;
+  const size_t smem = 1024 + (size_t)a.stages * tile + (size_t)a.stages * (16 + sizeof(TbMeta));
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32 * (1 + kTbConsumers), smem);
+  if (occ < 1) occ = 1;
+  const uint64_t need = (a.c.n_items + kTbConsumers - 1) / kTbConsumers;
+  const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms() * occ));
+  k<<<grid, 32 * (1 + kTbConsumers), smem, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+template <int SDT>
+cudaError_t tb_d(const TbArgs& a, int ddt, cudaStream_t s) {
+  switch (ddt) {
+    case KV_F16: return tb_t<SDT, KV_F16>(a, s);
+    case KV_BF16: return tb_t<SDT, KV_BF16>(a, s);
+    case KV_F8E4M3: return tb_t<SDT, KV_F8E4M3>(a, s);
+    case KV_F8E4M3FNUZ: return tb_t<SDT, KV_F8E4M3FNUZ>(a, s);
+    case KV_F32: return tb_t<SDT, KV_F32>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+}  // namespace
+
+cudaError_t launch_convert_tb(const TbArgs& a, int sdt, int ddt, cudaStream_t s) {
+  if (a.c.n_items == 0) return cudaSuccess;
+  if (sdt == KV_F16) return tb_d<KV_F16>(a, ddt, s);
+  if (sdt == KV_BF16) return tb_d<KV_BF16>(a, ddt, s);
+  if (sdt == KV_F8E4M3) return tb_d<KV_F8E4M3>(a, ddt, s);
+  if (sdt == KV_F8E4M3FNUZ) return tb_d<KV_F8E4M3FNUZ>(a, ddt, s);
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_convert_tr8(const ConvArgs& a, int sdt, int ddt, cudaStream_t s) {
   if (a.n_items == 0) return cudaSuccess;
   return tr8_v<8>(a, sdt, ddt, s);
@@ -2215,6 +2514,11 @@ cudaError_t touch(K k) {
   } while (0)
 
 template <int SDT, int DDT>
+cudaError_t preload_tb() {
+  if constexpr (Tr<SDT>::B <= 2) KVX_TOUCH(k_convert_tb<SDT, DDT>);
+  return cudaSuccess;
+}
+template <int SDT, int DDT>
 cudaError_t preload_pair() {
   constexpr int U8 = unroll_for<SDT, 8>(), U1 = unroll_for<SDT, 1>();
   KVX_TOUCH(k_convert_rows<SDT, DDT, U8>);
@@ -2228,7 +2532,7 @@ cudaError_t preload_pair() {
   KVX_TOUCH(k_pack<1, SDT, DDT, U1>);
   KVX_TOUCH(k_unpack_rows<SDT, DDT, U8>);
   KVX_TOUCH(k_unpack<1, SDT, DDT, U1>);
-  return cudaSuccess;
+  return preload_tb<SDT, DDT>();
 }
 template <int SDT>
 cudaError_t preload_src() {

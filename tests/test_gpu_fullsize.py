@@ -71,7 +71,7 @@ def test_fullsize_vendor_layouts(o1):
     rank 0 -> 0) from an other-vendor P cache -- x-packed K pool ([LAYER], BLOCK, HEAD,
     D/8, SLOT, 8) and head_dim-major V pool ([LAYER], BLOCK, HEAD, DIM, SLOT) -- into the
     NVIDIA-style D pool (BLOCK, LAYER, KV, HEAD, SLOT, DIM), bf16 -> e4m3, in the two
-    calls tools/variants_bench.py times (k_convert_tr8).  Sampled: requests 0 / 17 / 31 x
+    calls tools/variants_bench.py times (k_convert_tr8 for K, k_convert_tb for V).  Sampled: requests 0 / 17 / 31 x
     layers 0 / 40 / 79, all their blocks, vs O1 on the extracted blocks; canary outside."""
     import paper_2509_17542_b200 as kvx
     from synth import BLOCK, DIM, HEAD, KV, LAYER, SLOT
@@ -97,7 +97,7 @@ def test_fullsize_vendor_layouts(o1):
     kvx.convert_reshard([Kl], [Kp], sbt, [Dl], [DP], dbt)
     assert kvx.last_kernel() == "k_convert_tr8"
     kvx.convert_reshard([Vl], [Vp], sbt, [Dl], [DP], dbt)
-    assert kvx.last_kernel() == "k_convert_tr8"
+    assert kvx.last_kernel() == "k_convert_tb"   # head_dim-major tiles through TMA
     torch.cuda.synchronize()
     K6 = Kp.view(torch.int16).view(L, 1, NB, Hl, D // 8, B, 8)
     V6 = Vp.view(torch.int16).view(L, 1, NB, Hl, D, B)

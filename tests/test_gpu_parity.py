@@ -542,7 +542,8 @@ def test_head_dim_major_source_tiles(o1, monkeypatch, tr, dt, Bp, Bd, D):
         for i, lay in enumerate(case["src_lays"]):
             lay["scales"] = synth.pow2_scales(800 + i, 2, 2, -2, 2)
     run_case(o1, case)
-    assert kvx.last_kernel() == ("k_convert_tr8" if tr == "1" else "k_convert_tr")
+    tb = tr == "1" and dt != F32 and Bp == Bd == 16 and D in (64, 128, 256)
+    assert kvx.last_kernel() == ("k_convert_tb" if tb else "k_convert_tr8" if tr == "1" else "k_convert_tr")
 
 
 _VCOL = (LAYER, KV, BLOCK, HEAD, DIM, SLOT)   # head_dim-major tile (other vendors' value cache)
@@ -570,6 +571,7 @@ def test_tr8_forms(o1, monkeypatch, sf, df, sdt, ddt, Bp, Bd, tp):
     blocks per destination block, ragged requests (0, 1 and non-multiple-of-8 tokens), TP
     split and merge: bit-exact vs O1, and identical to the shared-memory kernel."""
     import paper_2509_17542_b200 as kvx
+    monkeypatch.setenv("KVX_TB", "0")   # the register kernel itself (k_convert_tb: test_tb_tiles)
     (so, px), (do, dx) = _FORMS[sf], _FORMS[df]
     case = make_case(2, 8, 64, tp[0], tp[1], Bp, Bd, [70, 0, 1, 37, 129], sdt, ddt, so, do, seed=Bp * 7 + Bd,
                      o1=o1, scales="pow2", p_split=px, d_split=dx)
@@ -595,6 +597,7 @@ def test_tr8_w16(o1, monkeypatch, sdt, ddt, Bp, Bd, tp, do):
     blocks of >= 16 slots: one 256-bit load per 32-B head_dim row, two 8 x 8 transposes),
     ragged requests, on and off (KVX_TR_W16=0): bit-exact vs O1 both ways."""
     import paper_2509_17542_b200 as kvx
+    monkeypatch.setenv("KVX_TB", "0")
     (so, _), (dord, dx) = _FORMS["col"], _FORMS[do]
     case = make_case(2, 8, 64, tp[0], tp[1], Bp, Bd, [70, 0, 1, 37, 129, 16], sdt, ddt, so, dord, seed=Bp + Bd + 5,
                      o1=o1, d_split=dx)
@@ -602,6 +605,37 @@ def test_tr8_w16(o1, monkeypatch, sdt, ddt, Bp, Bd, tp, do):
         monkeypatch.setenv("KVX_TR_W16", w)
         run_case(o1, case)
         assert kvx.last_kernel() == "k_convert_tr8"
+
+
+@pytest.mark.parametrize("sdt,ddt,D,tp,n_tokens", [
+    (BF16, E4M3, 128, (2, 1), [70, 0, 1, 37, 129, 16]),
+    (BF16, BF16, 128, (1, 1), [300, 15, 17]),
+    (F16, FNUZ, 64, (2, 4), [33, 64, 1]),
+    (BF16, F32, 256, (1, 2), [48, 5]),
+    (F16, F16, 128, (4, 2), [1000, 3, 0, 31]),
+    (E4M3, BF16, 128, (2, 1), [70, 0, 1, 37]),
+    (FNUZ, E4M3, 128, (2, 2), [129, 16, 3]),
+    (FNUZ, F32, 64, (1, 2), [40, 17]),
+    (E4M3, E4M3, 256, (2, 1), [33, 1]),
+])
+def test_tb_tiles(o1, monkeypatch, sdt, ddt, D, tp, n_tokens):
+    """k_convert_tb (head_dim-major 1- or 2-byte source tiles of 16 slots through TMA, swizzled
+    shared-memory stages, warp-specialised producer / consumers) into D's rows: bit-exact vs
+    O1 and identical to k_convert_tr8 (KVX_TB=0), ragged requests (0, 1, 15, 17 tokens),
+    TP merge and split, every destination dtype width."""
+    import paper_2509_17542_b200 as kvx
+    case = make_case(3, 8, D, tp[0], tp[1], 16, 16, n_tokens, sdt, ddt, _VCOL, synth.D_ORDER,
+                     seed=D + tp[0] * 10 + tp[1] + sdt, o1=o1, scales="pow2")
+    if sdt in FP8:
+        for i, lay in enumerate(case["src_lays"]):
+            lay["scales"] = synth.pow2_scales(950 + i, 3, 8 // tp[0], -2, 2)
+    got = {}
+    for tb in ("1", "0"):
+        monkeypatch.setenv("KVX_TB", tb)
+        _, got[tb], _ = run_case(o1, case)
+        assert kvx.last_kernel() == ("k_convert_tb" if tb == "1" else "k_convert_tr8")
+    for a, b in zip(got["1"], got["0"]):
+        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("tp_p,tp_d", [(1, 1), (1, 2), (2, 1)])
