@@ -645,7 +645,12 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
             use_tb = false;
         }
         tb.tile_rows = Dm * S->elem_bytes / 8;
-        tb.stages = Dm * S->elem_bytes >= 512 ? 6 : 8;
+        // tiles in flight per CTA: 64 KB for 2-byte sources (c4-pair V pool bf16 -> e4m3: 0.90 at
+        // 32 KB, 0.97 at 64 KB), 32 KB for 1-byte ones (the 2-KB tiles want more CTAs, hence
+        // less shared memory each: e4m3 0.91 at 32 KB, 0.72 at 64 KB); KVX_TB_STAGE_KB overrides
+        const char* kb_env = getenv("KVX_TB_STAGE_KB");
+        const int32_t kb = kb_env ? std::max(8, atoi(kb_env)) : (S->elem_bytes == 2 ? 64 : 32);
+        tb.stages = std::max(4, std::min(32, kb * 1024 / (tb.tile_rows * 128)));
       }
       for (int32_t l0 = lb; l0 < le; l0 += step) {
         const int32_t l1 = std::min(le, l0 + step);

@@ -1465,7 +1465,10 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
 // Metadata of 32 items at a time is computed lane-parallel by the producer (one dependent-load
 // round trip per 32 tiles) and handed to the consumers through the stage's slot.
 // ------------------------------------------------------------------------------------
-constexpr int kTbConsumers = 4;
+#ifndef KVX_TB_CONSUMERS
+#define KVX_TB_CONSUMERS 8  // consumer warps per CTA (c4-pair V pool: 4 -> 8 lifts e4m3 0.86 -> 0.91)
+#endif
+constexpr int kTbConsumers = KVX_TB_CONSUMERS;
 
 struct TbMeta {
   uint8_t* db;
@@ -1485,7 +1488,9 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // mbar_wait with a watchdog: a pipeline bug must not hang the GPU -- after ~4 s the kernel
-// traps (the launch then fails with an error instead of spinning forever)
+// traps (the launch then fails with an error instead of spinning forever).  A try_wait
+// with a long suspend hint instead of the nanosleep poll measured 2-5% slower on the c4-pair
+// V pools (profiles/r02/tb_variants.txt).
 __device__ __forceinline__ void mbar_wait_guarded(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   for (uint32_t it = 0;; ++it) {
