@@ -89,8 +89,9 @@ typedef struct {
   int32_t dim_split;     /* 0 or 1: none.  x > 1 (a power of two dividing head_dim): head_dim is
                           * stored as (head_dim/x at DIM's place in axis_order, then x innermost)
                           * -- the "x-packed" key cache (K [blocks, heads, D/x, block, x], x =
-                          * 16 bytes / element) of other vendors' paged-attention kernels.
-                          * Such pools take the element-wise kernels.  NEXT-3. */
+                          * 16 bytes / element) of other vendors' paged-attention kernels,
+                          * converted by the register-transpose kernel (k_convert_tr8) when the
+                          * other side has head_dim rows, else element-wise.  NEXT-3. */
   const float* scales;   /* fp8 dtypes only: DEVICE fp32 [num_layers][2][H/tp] dequant scales s
                           * (real value = code * s), indexed by the pool-local layer; NULL
                           * for other dtypes */

@@ -328,17 +328,15 @@ typedef CUresult (*encode_tiled_fn)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 encode_tiled_fn encode_fn() {
-  static encode_tiled_fn fn = nullptr;
-  static bool tried = false;
-  if (!tried) {
-    tried = true;
+  // resolved once, thread-safely (function-local static initialisation)
+  static const encode_tiled_fn fn = []() -> encode_tiled_fn {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess && p)
-      fn = reinterpret_cast<encode_tiled_fn>(p);
-    else
-      cudaGetLastError();
-  }
+      return reinterpret_cast<encode_tiled_fn>(p);
+    cudaGetLastError();
+    return nullptr;
+  }();
   return fn;
 }
 

@@ -1,25 +1,28 @@
 // sm_100a kernels of the KV convert / reshard / transfer path (arXiv 2509.17542, III-B).
 //
 // Everything on the path is data movement plus an elementwise cast, so nothing here is a
-// dense contraction: no tensor cores.  The kernels are HBM-bound (intra-GPU) or
-// NVLink-bound (peer stores).  Design:
-//   * a launch covers a flat space of "chunks": VEC=8 consecutive head_dim elements of
-//     one (request, layer, K/V, head, token) row, i.e. 16 B of a 2-byte source;
-//   * each warp takes segments of 32*U consecutive chunks (grid-stride over segments),
-//     issues all U 16-byte loads per lane before any store (U loads in flight per
-//     thread, ~64 KB in flight per SM at full occupancy), then converts and stores;
-//   * chunk order is destination-driven with head_dim fastest, so a warp's stores are
-//     contiguous; every source row is >= 128 B contiguous (full sectors);
-//   * the decode of a chunk index into (dst block, layer, K/V, head, slot, dim) uses
-//     32-bit multiply-high divisions (FastDiv), block tables are tiny and L1/L2-resident;
-//   * a destination pointer may be peer-mapped (CUDA IPC): the same kernel then stores
-//     across NVLink -- the fused gather + convert + push (K4);
-//   * VEC=1 instantiations are the generic path for layouts whose head_dim is not the
-//     innermost axis on both sides (element-wise, correct for all 720 axis orders).
-// Casts (readings 10-13): same dtype = bit copy; f16/bf16/f32 narrowing via
-// cvt.rn (RNE, canonical NaN); e4m3 via cvt.rn.satfinite.e4m3x2.f32 of x * RN(1/s)
-// with __fmul_rn (never contracted into an FMA); e4m3 widening = cvt.rn.f16x2.e4m3x2
-// (exact) then * s.
+// dense contraction: no tensor cores.  The kernels are HBM-bound (one GPU) or NVLink-bound
+// (peer loads / stores).  DESIGN.md section 5 has each kernel's roofline and bytes; in short:
+//   * k_convert_rows (default whenever head_dim is innermost on both sides): a work item is
+//     32 head_dim rows of one (dst rank, dst block, layer, K/V) tile; each lane decodes one
+//     row (block tables, TP routing, scale) and the warp streams the rows' 16-B chunks with
+//     U loads in flight per lane, fetching row state by shuffles.  A peer-mapped source or
+//     destination makes it the D-side NVLink pull or the P-side push.
+//   * k_tile_copy (same dtype, D's inner axes {HEAD, SLOT} x DIM): one 5-D TMA tensor load per
+//     source sub-tile, already permuted into D's order, then bulk stores.
+//   * k_convert_tb (head_dim-major 1-/2-byte source tiles of 16 slots): one 2-D TMA load per
+//     tile into swizzled shared-memory stages, warp-specialised producer / consumers that
+//     transpose 8 x 8 sub-blocks out of shared memory.
+//   * k_convert_tr8 / k_convert_tr (other head_dim-major or x-packed sides): 8 x 8 register
+//     transposes / shared-memory tiles.
+//   * k_pack_rows / k_unpack_rows (Fig. 5 flatten / restore for the NCCL mode), k_pull_rows
+//     (the persistent staged pull), k_amax_rows (dynamic scales), k_signal / k_wait (flags).
+//   * VEC=1 k_convert / k_pack / k_unpack: the element-wise generic path for any of the 720
+//     axis orders.
+// Casts (readings 10-13, 24-26): same dtype = bit copy; f16/bf16/f32 narrowing via
+// cvt.rn (RNE, canonical NaN); e4m3 via cvt.rn.satfinite.e4m3x2.f32 of x * RN(1/s) with
+// __fmul_rn (never contracted into an FMA); e4m3 widening = cvt.rn.f16x2.e4m3x2 (exact) then
+// * s; e4m3fnuz through the e4m3fn conversions or an exact f16 bit decode.
 #include <cuda_bf16.h>
 #include <algorithm>
 #include <cuda_fp16.h>
