@@ -62,7 +62,11 @@ def parse():
                     help="pull mode, fp8 destination: P computes per-chunk amax scales and ships them (NEXT-1 i)")
     ap.add_argument("--layer-chunk", type=int, default=0, help="layers per chunk (0 = whole model / auto)")
     ap.add_argument("--chunk-mib", type=int, default=64, help="c5: merge layers until a chunk moves this much")
-    ap.add_argument("--c5-batch", action="store_true", help="c5 push: each instance's requests as one batch")
+    ap.add_argument("--c5-batch", action="store_true", help="c5: each instance's requests as one batch (no per-request handoff)")
+    ap.add_argument("--c5-no-sm-split", action="store_true", help="c5 pull: the two source streams share all SMs")
+    ap.add_argument("--c5-per-request-launch", action="store_true",
+                    help="c5 pull: one launch per request (default: one launch per source with in-kernel per-request "
+                         "completion words)")
     ap.add_argument("--requests", type=int, default=0,
                     help="use only the first N requests of the workload (e.g. 1: batch-1 latency of c3/c4)")
     ap.add_argument("--workload", default=None, help="override: c1..c5")
@@ -1114,21 +1118,45 @@ def run_stream(args):
                 i = plan.requests_of(inst).index(r)
                 order.append((pr, sl, kvx.Batch(sl, [cfg.n_tokens[r]], [ptabs[i]], dev),
                               kvx.Batch(lay, [cfg.n_tokens[r]], [tabs[r]], dev)))
+            notify = not args.c5_batch and not args.c5_per_request_launch
+            if args.c5_batch or notify:   # one launch per source P rank over all of its instance's requests
+                order = []
+                for pr in srcs:
+                    inst = plan.role(pr).inst
+                    pidx = plan.p_index(inst, plan.role(pr).tp_rank)
+                    sl = cp.layout("P", pidx, dev)
+                    m = cp.message("P", pidx)
+                    rq = plan.requests_of(inst)
+                    order.append((pr, sl, kvx.Batch(sl, m.n_tokens, m.tables, dev),
+                                  kvx.Batch(lay, [cfg.n_tokens[r] for r in rq], [tabs[r] for r in rq], dev)))
             # one stream per source P rank, each on its share of the SMs: D pulls the two
             # instances' requests concurrently, so no P rank's egress carries two D ranks at once
             side = {pr: torch.cuda.Stream() for pr in srcs}
-            if len(srcs) > 1:
+            if len(srcs) > 1 and not args.c5_no_sm_split:
                 kvx.set_sm_budget(torch.cuda.get_device_properties(dev).multi_processor_count // len(srcs))
+            if notify:   # per-request completion words and times, one row per step
+                n_steps = max(args.warmup, 1) + K + 2
+                nrq = {pr: len(plan.requests_of(plan.role(pr).inst)) for pr in srcs}
+                ncnt = {pr: torch.zeros(nrq[pr], dtype=torch.int32, device=dev) for pr in srcs}
+                nflg = {pr: torch.zeros(nrq[pr], dtype=torch.int32, device=dev) for pr in srcs}
+                nns = {pr: torch.zeros((n_steps, nrq[pr]), dtype=torch.int64, device=dev) for pr in srcs}
+                tst = torch.zeros(n_steps, dtype=torch.int64, device=dev)
 
             def step(evs=None):
                 count[0] += 1
+                if notify:
+                    kvx.timestamp(tst[count[0]:count[0] + 1], stream)
                 st = torch.cuda.Event()
                 st.record(stream)
                 for pr in srcs:
                     side[pr].wait_event(st)
                     kvx.wait(flags[plan.flag_word(pr):plan.flag_word(pr) + 1], count[0], err, 60.0, side[pr])
                 for j, (pr, sl, sbt, dbt) in enumerate(order):
-                    kvx.convert_reshard([sl], [src_pool[pr]], sbt, [lay], [pool], dbt, None, side[pr])
+                    if notify:   # requests handed off one by one as they land, inside one launch
+                        kvx.convert_reshard_notify([sl], [src_pool[pr]], sbt, [lay], [pool], dbt, ncnt[pr], nflg[pr],
+                                                   count[0], nns[pr][count[0]], None, side[pr])
+                    else:
+                        kvx.convert_reshard([sl], [src_pool[pr]], sbt, [lay], [pool], dbt, None, side[pr])
                     if evs is not None:
                         evs[j].record(side[pr])
                 for pr in srcs:
@@ -1150,8 +1178,10 @@ def run_stream(args):
     barrier_t = torch.zeros(1, device=dev)
     dist.all_reduce(barrier_t)
     torch.cuda.synchronize()
+    notify = pull and me.kind == "D" and not args.c5_batch and not args.c5_per_request_launch
+    step0 = count[0]   # steps run so far (warm-up): the timed steps are step0 + 1 .. step0 + K
     if pull:   # the D ranks run the data path: per-request completion events there
-        nreq_mine = len(cfg.n_tokens) if me.kind == "D" else 0
+        nreq_mine = 0 if notify else (len(order) if args.c5_batch else len(cfg.n_tokens)) if me.kind == "D" else 0
     else:
         nreq_mine = len(plan.requests_of(me.inst)) if me.kind == "P" else 0
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -1177,6 +1207,14 @@ def run_stream(args):
             for i in range(nreq_mine):
                 lat.append(prev.elapsed_time(evs[k][i]))
             prev = max(evs[k], key=lambda e: t0.elapsed_time(e))  # the step's last completion
+    if notify:
+        # in-kernel completion times (%globaltimer) of every request - the step's start stamp
+        ts = tst.cpu().tolist()
+        for pr in srcs:
+            rows = nns[pr].cpu().tolist()
+            for k in range(step0 + 1, step0 + K + 1):
+                lat += [(v - ts[k]) * 1e-6 for v in rows[k]]
+        nreq_mine = len(cfg.n_tokens)
     # ---- K6 over every element of every D pool ----
     fullsize = None
     if not args.no_verify:
@@ -1232,7 +1270,11 @@ def run_stream(args):
                                       f"rank(s) -> D ranks {list(range(plan.n_d))}"
                                       + (" (full c5)" if world == 8 else " (c5' sub-config)"),
                           "requests": nreq, "src_bytes_per_step": tot_b,
-                          "mode": "pull per request (D-initiated NVLink reads, one launch per request)" if pull
+                          "mode": ("pull, one launch per source P rank, each request handed off by an in-kernel "
+                                   "completion word as it lands (kv_convert_reshard_notify)" if pull and
+                                   not args.c5_batch and not args.c5_per_request_launch else
+                                   "pull, whole instance batch per launch" if pull and args.c5_batch else
+                                   "pull per request (D-initiated NVLink reads, one launch per request)") if pull
                           else "push, whole instance batch per launch" if args.c5_batch else
                           f"push per request, layer chunks >= {args.chunk_mib} MiB",
                           "control_plane": "layouts and block tables exchanged as kv_ctrl messages",
@@ -1243,7 +1285,7 @@ def run_stream(args):
                "roofline": {"bound": "nvlink", "achieved": round(busiest / (ms * 1e-3) / 1e9, 1),
                             "peak": NVLINK_NOMINAL_GBS, "unit": "GB/s", "frac": round(t_roof / ms, 4),
                             "traffic": None,
-                            "kernel": "k_convert_rows (peer-load pull on D, per request)" if pull
+                            "kernel": "k_convert_rows (peer-load pull on D)" if pull
                             else "k_convert_rows (peer-store push, per request)",
                             "algorithmic_bytes_per_step": busiest, "d_ingress_bytes": d_in, "p_egress_bytes": p_out,
                             "peak_source": "nominal NVLink 5, 900 GB/s per direction (north_star)",

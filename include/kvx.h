@@ -227,6 +227,24 @@ kv_status kv_convert_share(const kv_layout* src, const void* src_pool, const kv_
                            const kv_layout* const* dst, void* const* dst_pools, const kv_batch* dst_bt,
                            int32_t layer_begin, int32_t layer_end, kv_stream stream);
 
+/* A11 per request inside one launch (the c5 stream: many requests in one call, each handed
+ * to decode as soon as its own KV has landed -- P:95 step 6, "D loads and decodes"): exactly
+ * kv_convert_reshard (one call = all listed P ranks -> D ranks), and in addition, once every
+ * element of request r (of dst_bt) is written, a system-scope release store of `epoch` into
+ * done_flags[r] (DEVICE uint32 [n_req], local or peer-mapped) and the %globaltimer value into
+ * done_ns[r] (DEVICE uint64 [n_req], or NULL).  On the row kernel the warp that finishes a
+ * request's last work item does it (so requests complete as they land, in about table
+ * order); on any other kernel every request completes when the launch does.  counters:
+ * DEVICE uint32 [n_req] scratch, zeroed by the call on its stream.  Requests with no tokens
+ * complete immediately.  kv_timestamp writes %globaltimer into *out on the stream (the same
+ * clock, for latencies). */
+kv_status kv_convert_reshard_notify(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                                    const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst,
+                                    void* const* dst_pools, const kv_batch* dst_bt, int32_t layer_begin,
+                                    int32_t layer_end, uint32_t* counters, uint32_t* done_flags, uint64_t* done_ns,
+                                    uint32_t epoch, kv_stream stream);
+kv_status kv_timestamp(uint64_t* out, kv_stream stream);
+
 /* ---- NEXT-1: dynamic fp8 scales --------------------------------------------------- */
 
 /* Per-batch dequant scales for the heads of D rank `dst` (precision alignment):

@@ -77,6 +77,9 @@ def _load():
         "kv_convert_reshard": (st, [i32, pp, pp, C.POINTER(Batch_t), i32, pp, pp, C.POINTER(Batch_t), i32, i32, p]),
         "kv_compute_scales": (st, [i32, pp, pp, C.POINTER(Batch_t), p, p, i32, i32, p]),
         "kv_convert_share": (st, [p, p, C.POINTER(Batch_t), i32, pp, pp, C.POINTER(Batch_t), i32, i32, p]),
+        "kv_convert_reshard_notify": (st, [i32, pp, pp, C.POINTER(Batch_t), i32, pp, pp, C.POINTER(Batch_t), i32, i32,
+                                           p, p, p, C.c_uint32, p]),
+        "kv_timestamp": (st, [p, p]),
         "kv_wire_dtype": (i32, [p, p]),
         "kv_wire_header_bytes": (C.c_size_t, [i32]),
         "kv_wire_header_write": (st, [p, p, i32, p, i32, i32, p, C.c_size_t]),
@@ -135,7 +138,7 @@ lib = _load()
 # Every symbol include/kvx.h declares (checked by tests/test_abi.py).
 EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_block_table_update", "kv_plan_pairs",
            "kv_ctrl_msg_bytes", "kv_ctrl_msg_write", "kv_ctrl_msg_parse",
-           "kv_convert_reshard", "kv_convert_share", "kv_compute_scales", "kv_wire_dtype", "kv_wire_header_bytes",
+           "kv_convert_reshard", "kv_convert_share", "kv_convert_reshard_notify", "kv_timestamp", "kv_compute_scales", "kv_wire_dtype", "kv_wire_header_bytes",
            "kv_wire_header_write", "kv_wire_header_parse", "kv_wire_header_check", "kv_copy_bytes", "kv_memcpy_engine", "kv_wire_bytes", "kv_pack", "kv_unpack", "kv_comm_unique_id",
            "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
            "kv_recv_unpack", "kv_push", "kv_send_pipelined", "kv_recv_pipelined", "kv_pull", "kv_stage",

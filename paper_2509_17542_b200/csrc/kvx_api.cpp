@@ -465,7 +465,8 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
 // share == true: kv_convert_share (one P rank converts only the D heads it holds).
 kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
                        const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst, void* const* dst_pools,
-                       const kv_batch* dst_bt, int32_t lb, int32_t le, kv_stream stream, bool share) {
+                       const kv_batch* dst_bt, int32_t lb, int32_t le, kv_stream stream, bool share,
+                       const Notify* nt = nullptr, bool* notified = nullptr) {
   if (n_src < 1 || n_src > KVX_MAX_RANKS || n_dst < 1 || n_dst > KVX_MAX_RANKS)
     return fail(KV_EINVAL, "kv_convert_reshard: need 1..16 source and destination ranks");
   if (!src || !src_pools || !dst || !dst_pools) return fail(KV_EINVAL, "kv_convert_reshard: null array");
@@ -724,6 +725,16 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
   const uint64_t per_layer_units = vec == 8 ? per_layer / ndch : per_layer;
   int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / std::max<uint64_t>(per_layer_units, 1));
   if (per_layer_units > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_convert_reshard: one layer exceeds 2^31 chunks");
+  if (nt && vec == 8 && step >= le - lb) {
+    // per-request completion counted inside the (single) row-kernel launch
+    cudaError_t e = launch_notify_init(*nt, dst_bt->blk_off, dst_bt->n_req, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(e, "kv_convert_reshard_notify: init");
+    a.req_cnt = nt->counters;
+    a.req_flag = nt->flags;
+    a.req_ns = nt->ns;
+    a.req_epoch = nt->epoch;
+    if (notified) *notified = true;
+  }
   for (int32_t l0 = lb; l0 < le; l0 += step) {
     const int32_t l1 = std::min(le, l0 + step);
     a.lb = l0;
@@ -754,6 +765,29 @@ kv_status kv_convert_share(const kv_layout* src, const void* src_pool, const kv_
   const kv_layout* s1[1] = {src};
   const void* p1[1] = {src_pool};
   return convert_impl(1, s1, p1, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, true);
+}
+
+kv_status kv_convert_reshard_notify(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
+                                    const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst,
+                                    void* const* dst_pools, const kv_batch* dst_bt, int32_t lb, int32_t le,
+                                    uint32_t* counters, uint32_t* done_flags, uint64_t* done_ns, uint32_t epoch,
+                                    kv_stream stream) {
+  if (!dst_bt || (dst_bt->n_req > 0 && (!counters || !done_flags)))
+    return fail(KV_EINVAL, "kv_convert_reshard_notify: null counters / flags");
+  Notify nt{counters, done_flags, done_ns, epoch};
+  bool notified = false;
+  kv_status st = convert_impl(n_src, src, src_pools, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, false,
+                              &nt, &notified);
+  if (st != KV_OK || notified) return st;
+  // another kernel (or several launches) did the work: every request completes with it
+  cudaError_t e = launch_notify_all(nt, dst_bt->n_req, (cudaStream_t)stream);
+  return e == cudaSuccess ? KV_OK : cuda_fail(e, "kv_convert_reshard_notify: completion");
+}
+
+kv_status kv_timestamp(uint64_t* out, kv_stream stream) {
+  if (!out) return fail(KV_EINVAL, "kv_timestamp: null pointer");
+  cudaError_t e = launch_timestamp(out, (cudaStream_t)stream);
+  return e == cudaSuccess ? KV_OK : cuda_fail(e, "kv_timestamp");
 }
 
 }  // extern "C"

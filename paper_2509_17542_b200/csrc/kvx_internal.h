@@ -85,6 +85,12 @@ struct ConvArgs {
   FastDiv f_sb;     // slot sub-tiles per tile
   int32_t ts_log2;  // sub-tile = 2^ts_log2 slots x 2^(5-ts_log2) heads
   uint32_t n_items;
+  // per-request completion inside one launch (kv_convert_reshard_notify, row kernel): the
+  // warp finishing a request's last item release-stores req_epoch into req_flag[r]
+  uint32_t* req_cnt;
+  uint32_t* req_flag;
+  uint64_t* req_ns;
+  uint32_t req_epoch, items_per_block;
 };
 
 // TMA tile path (same dtype): one cp.async.bulk.tensor load per (dst block, layer, K/V,
@@ -230,6 +236,17 @@ kv_status compute_scales_impl(int32_t n_src, const kv_layout* const* src, const 
                               const kv_batch* src_bt, const kv_layout* dst, float* out_scales, int32_t lb, int32_t le,
                               kv_stream stream, bool share, float* peer);
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s);
+// per-request completion words (kv_convert_reshard_notify): before the row kernel, zero the
+// counters and complete the requests with no blocks; or, after any other launch, complete all
+struct Notify {
+  uint32_t* counters;
+  uint32_t* flags;
+  uint64_t* ns;
+  uint32_t epoch;
+};
+cudaError_t launch_notify_init(const Notify& n, const int32_t* blk_off, int32_t n_req, cudaStream_t s);
+cudaError_t launch_notify_all(const Notify& n, int32_t n_req, cudaStream_t s);
+cudaError_t launch_timestamp(uint64_t* out, cudaStream_t s);
 // k_convert_tr: a side with (DIM, SLOT) innermost (a.s_tr / a.d_tr), items in a.n_items
 cudaError_t launch_convert_tr(const ConvArgs& a, int sdt, int ddt, cudaStream_t s);
 // k_convert_tr8: the same items without shared memory (8 x 8 register sub-blocks); needs

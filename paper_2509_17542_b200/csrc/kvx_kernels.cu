@@ -697,6 +697,12 @@ __device__ __forceinline__ void stream_rows(uint32_t lane, uint32_t cs, uint64_t
 // ------------------------------------------------------------------------------------
 // Per-lane row state of convert item `item` (see k_convert_rows): lane = row of the
 // 2-D sub-tile.  rz: 0 copy, 1 zero-fill tail row, 2 no row.
+__device__ __forceinline__ uint64_t gtimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // 2^7 s for the folded e4m3fnuz decode (exact), or -s when it would overflow (cast_chunk)
 __device__ __forceinline__ float fnuz_fold_scale(float s) {
   const float f = __fmul_rn(s, 128.0f);
@@ -705,7 +711,8 @@ __device__ __forceinline__ float fnuz_fold_scale(float s) {
 
 template <int SDT, int DDT, bool FOLD = false>
 __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint32_t lane, uint64_t& sp,
-                                         uint64_t& dp, float& rsc, uint32_t& rz, float& rsc2) {
+                                         uint64_t& dp, float& rsc, uint32_t& rz, float& rsc2,
+                                         int32_t* req_out = nullptr) {
   // destination fastest: with several D ranks (fan-out, e.g. a TP split pushed over
   // NVLink) concurrent warps write every destination at once instead of one link after
   // the other -- with the D rank outermost, all P ranks of a fan-in/fan-out hit the same
@@ -717,6 +724,7 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
   const uint32_t l = divmod(n, a.f_l);
   const uint32_t bl = n;
   const int32_t r = __ldg(a.d_blk_req + bl);
+  if (req_out) *req_out = r;
   const int32_t tok0 = __ldg(a.tok_off + r);
   const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
   const uint32_t tb0 = (uint32_t)(bl - __ldg(a.d_blk_off + r)) * (uint32_t)a.Bd;  // first token of the block
@@ -780,8 +788,24 @@ __global__ void __launch_bounds__(kThreads, row_minb(SDT, DDT)) k_convert_rows(c
     uint64_t sp, dp;
     float rsc, rsc2;
     uint32_t rz;
-    conv_row<SDT, DDT, FOLD>(a, item, lane, sp, dp, rsc, rz, rsc2);
+    int32_t r;
+    conv_row<SDT, DDT, FOLD>(a, item, lane, sp, dp, rsc, rz, rsc2, &r);
     stream_rows<SDT, DDT, U, VEC, false, SPLIT, FOLD>(lane, cs, sp, dp, rsc, rz, rsc2, &cm);
+    if (a.req_cnt) {
+      // per-request completion (kv_convert_reshard_notify): the warp finishing request r's
+      // last item publishes it -- its rows' stores are fenced before the count, and the
+      // last counter owner fences system-wide before the release store of the flag
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        const uint32_t tot = (uint32_t)(__ldg(a.d_blk_off + r + 1) - __ldg(a.d_blk_off + r)) * a.items_per_block;
+        if (atomicAdd(a.req_cnt + r, 1u) + 1u == tot) {
+          __threadfence_system();
+          if (a.req_ns) a.req_ns[r] = gtimer_ns();
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.req_flag + r), "r"(a.req_epoch) : "memory");
+        }
+      }
+    }
   }
 }
 
@@ -2165,6 +2189,7 @@ cudaError_t conv_t(const ConvArgs& a0, cudaStream_t s) {
     a.f_sb = make_fastdiv(nsb);
     a.f_items = make_fastdiv(nsb * nhb);
     a.n_items = (uint32_t)(a.total64 / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);
+    a.items_per_block = a.f_bl.d ? a.n_items / a.f_bl.d : 0;
     // 1-byte sources: 16-element chunks (whole 16-B loads, 4 in flight = 64 B per lane, like
     // the 2-byte sources' 8-element chunks); KVX_FP8_VEC16=0 reverts to 8-element chunks
     static const int wide1 = getenv("KVX_FP8_VEC16") ? atoi(getenv("KVX_FP8_VEC16")) : 1;
@@ -2490,6 +2515,45 @@ cudaError_t launch_copy_bytes(void* dst, const void* src, size_t bytes, cudaStre
   return cudaGetLastError();
 }
 
+// per-request completion words (kv_convert_reshard_notify)
+__global__ void k_notify_init(Notify n, const int32_t* blk_off, int32_t n_req) {
+  const uint64_t now = gtimer_ns();
+  for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_req; r += gridDim.x * blockDim.x) {
+    n.counters[r] = 0u;
+    if (blk_off[r + 1] == blk_off[r]) {   // no block: nothing to wait for
+      if (n.ns) n.ns[r] = now;
+      asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(n.flags + r), "r"(n.epoch) : "memory");
+    }
+  }
+}
+__global__ void k_notify_all(Notify n, int32_t n_req) {
+  __threadfence_system();
+  const uint64_t now = gtimer_ns();
+  for (int32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < n_req; r += gridDim.x * blockDim.x) {
+    if (n.ns) n.ns[r] = now;
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(n.flags + r), "r"(n.epoch) : "memory");
+  }
+}
+__global__ void k_timestamp(uint64_t* out) { *out = gtimer_ns(); }
+
+cudaError_t launch_notify_init(const Notify& n, const int32_t* blk_off, int32_t n_req, cudaStream_t s) {
+  if (n_req <= 0) return cudaSuccess;
+  k_notify_init<<<(n_req + 255) / 256, 256, 0, s>>>(n, blk_off, n_req);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+cudaError_t launch_notify_all(const Notify& n, int32_t n_req, cudaStream_t s) {
+  if (n_req <= 0) return cudaSuccess;
+  k_notify_all<<<(n_req + 255) / 256, 256, 0, s>>>(n, n_req);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+cudaError_t launch_timestamp(uint64_t* out, cudaStream_t s) {
+  k_timestamp<<<1, 1, 0, s>>>(out);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_signal(uint32_t* flag, uint32_t value, cudaStream_t s) {
   k_signal<<<1, 1, 0, s>>>(flag, value);
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -2570,6 +2634,9 @@ cudaError_t preload_kernels() {
   KVX_TOUCH(k_signal);
   KVX_TOUCH(k_wait);
   KVX_TOUCH(k_copy_bytes);
+  KVX_TOUCH(k_notify_init);
+  KVX_TOUCH(k_notify_all);
+  KVX_TOUCH(k_timestamp);
   return preload_verify_kernels();
 }
 

@@ -12,7 +12,7 @@ from contextlib import contextmanager
 from ._lib import (AX_BLOCK, AX_DIM, AX_HEAD, AX_KV, AX_LAYER, AX_SLOT, DTYPE_BYTES, KV_BF16, KV_F8E4M3, KV_F16,
                    KV_F32, KV_F8E4M3FNUZ, Batch_t, CtrlInfo, KvError, LayoutDesc, check, lib)
 
-__all__ = ["Layout", "Batch", "CtrlMsg", "ctrl_encode", "ctrl_decode", "convert_reshard", "convert_share", "push", "pull", "stage", "pull_staged", "chunk_count", "pull_counter_words", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
+__all__ = ["Layout", "Batch", "convert_reshard_notify", "timestamp", "CtrlMsg", "ctrl_encode", "ctrl_decode", "convert_reshard", "convert_share", "push", "pull", "stage", "pull_staged", "chunk_count", "pull_counter_words", "compute_scales", "pack", "unpack", "wire_bytes", "wire_dtype", "plan_pairs",
            "Comm", "ipc_export", "ipc_open", "ipc_close", "peer_enable", "signal", "wait", "preload", "memcpy_engine", "copy_bytes", "verify_fill", "verify_check", "launch_count", "launch_count_reset", "set_sm_budget", "last_kernel",
            "KvError", "KV_F16", "KV_BF16", "KV_F8E4M3", "KV_F32", "KV_F8E4M3FNUZ", "DTYPE_BYTES",
            "AX_LAYER", "AX_KV", "AX_BLOCK", "AX_SLOT", "AX_HEAD", "AX_DIM"]
@@ -224,6 +224,25 @@ def convert_reshard(src_layouts, src_pools, src_batch: Batch, dst_layouts, dst_p
     lb, le = layer_range if layer_range else _common(src_layouts[0], dst_layouts[0])
     check(lib.kv_convert_reshard(ns, S, SP, C.byref(src_batch.bt), nd, Dl, DP, C.byref(dst_batch.bt), lb, le,
                                  _stream(stream)))
+
+
+def convert_reshard_notify(src_layouts, src_pools, src_batch: Batch, dst_layouts, dst_pools, dst_batch: Batch,
+                           counters, done_flags, epoch, done_ns=None, layer_range=None, stream=None):
+    """kv_convert_reshard_notify: kv_convert_reshard + per-request completion words (each
+    request's flag released as soon as its own KV has landed; done_ns: %globaltimer then)."""
+    ns, nd = len(src_layouts), len(dst_layouts)
+    S = (C.c_void_p * ns)(*[l.handle.value for l in src_layouts])
+    SP = (C.c_void_p * ns)(*[_ptr(p) for p in src_pools])
+    Dl = (C.c_void_p * nd)(*[l.handle.value for l in dst_layouts])
+    DP = (C.c_void_p * nd)(*[_ptr(p) for p in dst_pools])
+    lb, le = layer_range if layer_range else _common(src_layouts[0], dst_layouts[0])
+    check(lib.kv_convert_reshard_notify(ns, S, SP, C.byref(src_batch.bt), nd, Dl, DP, C.byref(dst_batch.bt), lb, le,
+                                        _ptr(counters), _ptr(done_flags), _ptr(done_ns), epoch, _stream(stream)))
+
+
+def timestamp(out, stream=None):
+    """kv_timestamp: %globaltimer (ns) into the device word `out` on the stream."""
+    check(lib.kv_timestamp(_ptr(out), _stream(stream)))
 
 
 def convert_share(src_layout, src_pool, src_batch: Batch, dst_layouts, dst_pools, dst_batch: Batch,

@@ -304,3 +304,34 @@ def test_host_staged_one_gpu(o1, shape):
         hs.step(dc.src_pools[p], dc.src_bt, dc.dst_pools[q], dc.dst_bt)
         torch.cuda.synchronize()
     assert_pools_match(dc.dst_numpy(), expected(case, o1), case["dst_lays"][0]["dtype"])
+
+
+@pytest.mark.parametrize("kind", ["rows", "tile"])
+def test_convert_notify_per_request(o1, monkeypatch, kind):
+    """A11 per request inside one launch (kv_convert_reshard_notify, the c5 stream's handoff):
+    every request's flag carries the epoch and a completion time, requests with no tokens
+    complete at once, and the pools equal O1's -- on the row kernel (in-kernel completion
+    counting) and on the TMA tile path (completion when the launch ends)."""
+    import paper_2509_17542_b200 as kvx
+    from tests.gpu_util import DevCase
+    from tests.test_gpu_parity import assert_pools_match
+    if kind == "rows":
+        case = make_case(3, 8, 128, 2, 4, 16, 16, [300, 0, 17, 1, 64], BF16, E4M3, seed=51, o1=o1, scales="pow2")
+    else:
+        monkeypatch.setenv("KVX_TILE", "2")
+        case = make_case(2, 8, 128, 2, 1, 16, 16, [70, 0, 16], F16, F16, seed=52, o1=o1)
+    dc = DevCase(case, "cuda:0")
+    n = len(case["n_tokens"])
+    cnt = torch.zeros(n, dtype=torch.int32, device="cuda:0")
+    flags = torch.zeros(n, dtype=torch.int32, device="cuda:0")
+    ns = torch.zeros(n, dtype=torch.int64, device="cuda:0")
+    t0 = torch.zeros(1, dtype=torch.int64, device="cuda:0")
+    kvx.timestamp(t0)
+    kvx.convert_reshard_notify(dc.src_lays, dc.src_pools, dc.src_bt, dc.dst_lays, dc.dst_pools, dc.dst_bt, cnt, flags,
+                               7, ns)
+    assert kvx.last_kernel() == ("k_convert_rows" if kind == "rows" else "k_tile_copy")
+    torch.cuda.synchronize()
+    assert flags.tolist() == [7] * n
+    start = int(t0.item())
+    assert all(v >= start for v in ns.tolist())
+    assert_pools_match(dc.dst_numpy(), expected(case, o1), case["dst_lays"][0]["dtype"])
