@@ -352,12 +352,21 @@ int tile_mode() {
 // B_d a multiple of B_p, head counts dividing each other: one TMA tensor load per source
 // sub-tile whose map enumerates the source in D's order, bulk stores of D's runs.  Sets
 // *used = false (and launches nothing) when the case does not fit.
+// KVX_TT: the TMA-fed cast variant (k_tile_cast) for converts whose dtypes differ -- 0 off,
+// 1 (default) on.  Read per call.
+int tile_cast_mode() {
+  const char* e = getenv("KVX_TT");
+  return e ? atoi(e) : 1;
+}
+
 kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* const* src_pools,
                         const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst, void* const* dst_pools,
                         const kv_batch* dst_bt, int32_t lb, int32_t le, kv_stream stream, bool share, bool* used) {
   *used = false;
-  const int mode = tile_mode();
+  const bool cast = src[0]->d.dtype != dst[0]->d.dtype;
+  const int mode = cast ? tile_cast_mode() : tile_mode();
   if (mode == 0) return KV_OK;
+  if (cast && src[0]->elem_bytes > 2) return KV_OK;  // 1- and 2-byte sources (LDS of 8 / 16 B per chunk)
   const kv_layout *S = src[0], *D = dst[0];
   const int32_t* o = D->d.axis_order;
   int head_major;
@@ -381,7 +390,10 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
     nh /= 2;
     stage /= 2;
   }
-  if (stage > 100 * 1024 || (mode == 1 && stage < 32 * 1024)) return KV_OK;
+  if (stage > 100 * 1024 || (mode == 1 && !cast && stage < 32 * 1024)) return KV_OK;
+  if (cast && (nh > 8 || (nh & (nh - 1)) || (Bp & (Bp - 1)) || stage < 2048 || stage * kTbConsumers > 200 * 1024 ||
+               (Dm / 8) & (Dm / 8 - 1) || Dm % 8))
+    return KV_OK;
   encode_tiled_fn enc = encode_fn();
   if (!enc) return KV_OK;
   TileArgs a;
@@ -429,6 +441,14 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
   a.share_p = share ? S->d.tp_rank : -1;
   a.stage_bytes = (int32_t)stage;
   a.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(8, (200 * 1024) / stage));
+  if (cast) {
+    a.d_esize = D->elem_bytes;
+    for (int i = 0; i < n_src; ++i) a.sscale[i] = src[i]->d.scales;
+    for (int i = 0; i < n_dst; ++i) a.dscale[i] = dst[i]->d.scales;
+    const char* kb_env = getenv("KVX_TT_STAGE_KB");
+    const int64_t kb = kb_env ? std::max(8, atoi(kb_env)) : 64;
+    a.stages = (int32_t)std::max<int64_t>(kTbConsumers, std::min<int64_t>(16, kb * 1024 / stage));
+  }
   a.s_blk_off = src_bt->blk_off;
   a.s_blk_ids = src_bt->blk_ids;
   a.d_blk_off = dst_bt->blk_off;
@@ -454,7 +474,8 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
     a.Lc = l1 - l0;
     a.f_l = make_fastdiv((uint32_t)a.Lc);
     a.n_items = (uint32_t)(per_layer * (uint64_t)a.Lc);
-    cudaError_t e = launch_tile_copy(a, (cudaStream_t)stream);
+    cudaError_t e = cast ? launch_tile_cast(a, S->d.dtype, D->d.dtype, (cudaStream_t)stream)
+                         : launch_tile_copy(a, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "kv_convert_reshard: tile launch");
   }
   *used = true;
@@ -649,7 +670,7 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
         // less shared memory each: e4m3 0.91 at 32 KB, 0.72 at 64 KB); KVX_TB_STAGE_KB overrides
         const char* kb_env = getenv("KVX_TB_STAGE_KB");
         const int32_t kb = kb_env ? std::max(8, atoi(kb_env)) : (S->elem_bytes == 2 ? 64 : 32);
-        tb.stages = std::max(4, std::min(32, kb * 1024 / (tb.tile_rows * 128)));
+        tb.stages = std::max(kTbConsumers, std::min(32, kb * 1024 / (tb.tile_rows * 128)));
       }
       for (int32_t l0 = lb; l0 < le; l0 += step) {
         const int32_t l1 = std::min(le, l0 + step);
@@ -708,13 +729,13 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
   a.f_cpr = make_fastdiv(ndch);
   a.f_nd = make_fastdiv((uint32_t)n_dst);
   if (dst_bt->total_blocks == 0 || le == lb) return KV_OK;
-  if (fast && !a.split && S->d.dtype == D->d.dtype) {
+  if (fast && !a.split && !(nt && S->d.dtype != D->d.dtype)) {  // notify counts requests in the row kernel
     bool used = false;
     if ((st = try_tile_copy(n_src, src, src_pools, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, share,
                             &used)) != KV_OK)
       return st;
     if (used) {
-      t_last_kernel = "k_tile_copy";
+      t_last_kernel = S->d.dtype == D->d.dtype ? "k_tile_copy" : "k_tile_cast";
       return KV_OK;
     }
   }

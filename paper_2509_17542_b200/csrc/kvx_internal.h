@@ -115,7 +115,13 @@ struct TileArgs {
   const int32_t* tok_off;
   FastDiv f_nd, f_parts, f_sub, f_l;
   uint32_t n_items;
+  // k_tile_cast (a cast on the way: consumer warps convert the staged sub-tile): destination
+  // element size and the fp8 scales of either side ([L][2][H_local] per rank index)
+  int32_t d_esize;
+  const float* sscale[KVX_MAX_RANKS];
+  const float* dscale[KVX_MAX_RANKS];
 };
+cudaError_t launch_tile_cast(const TileArgs& a, int sdt, int ddt, cudaStream_t s);
 
 struct PackArgs {
   int32_t kv1, c0;
@@ -260,6 +266,13 @@ cudaError_t launch_tile_copy(const TileArgs& a, cudaStream_t s);
 // 128B swizzle) per tile lands it in shared memory, consumer warps transpose 8 x 8 sub-blocks
 // out of it (conflict-free thanks to the swizzle) into D's (SLOT, DIM) rows.  The ConvArgs
 // are those of k_convert_tr8; maps[i] views source pool i as rows of 128 bytes.
+#ifndef KVX_TB_CONSUMERS
+#define KVX_TB_CONSUMERS 8  // consumer warps per CTA (c4-pair V pool: 4 -> 8 lifts e4m3 0.86 -> 0.91)
+#endif
+// consumer warps of the warp-specialised TMA kernels (k_convert_tb, k_tile_cast); their rings
+// need at least this many stages (a consumer waits on its stage's phase parity, which aliases
+// when two consumers' rounds of one stage are more than one phase apart)
+constexpr int kTbConsumers = KVX_TB_CONSUMERS;
 struct TbArgs {
   ConvArgs c;
   CUtensorMap maps[KVX_MAX_RANKS];

@@ -1492,10 +1492,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
 // Metadata of 32 items at a time is computed lane-parallel by the producer (one dependent-load
 // round trip per 32 tiles) and handed to the consumers through the stage's slot.
 // ------------------------------------------------------------------------------------
-#ifndef KVX_TB_CONSUMERS
-#define KVX_TB_CONSUMERS 8  // consumer warps per CTA (c4-pair V pool: 4 -> 8 lifts e4m3 0.86 -> 0.91)
-#endif
-constexpr int kTbConsumers = KVX_TB_CONSUMERS;
+// kTbConsumers: kvx_internal.h
 
 struct TbMeta {
   uint8_t* db;
@@ -1673,6 +1670,182 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
       const int64_t doff = dim_off(d0, a.ds[KV_AX_DIM], a.d_dk);
 #pragma unroll
       for (int k = 0; k < 8; ++k) store_chunk<DDT, 8>(m.db + ((int64_t)(s0 + k) * a.ds[KV_AX_SLOT] + doff) * DB, o[k]);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty + st);
+  }
+}
+
+// ------------------------------------------------------------------------------------
+// K1 fast path with a cast, TMA-fed (k_tile_cast): the sub-tiles of k_tile_copy -- one 5-D
+// tensor load each, landing in shared memory already in D's inner order -- feed consumer
+// warps that convert them row by row (16-B LDS, the cast, 8- or 16-B stores of D's rows)
+// instead of bulk-storing them unchanged.  Warp 0 is the producer (decode + TMA issue into a
+// ring of stages with full / empty mbarriers); kTbConsumers warps consume.  Rows of slots
+// >= T are written as zeros.  The HBM side sees one TMA read per sub-tile (8 KB for a c4
+// pair: 2 heads x 16 slots x 128 bf16).
+// ------------------------------------------------------------------------------------
+struct TcMeta {
+  uint8_t* dtile;    // D (layer, K/V, block) tile base (bytes)
+  int32_t hq0, soff; // first D-local head, first slot of the sub-tile in the D block
+  uint32_t valid;    // source slots < T (0: the whole sub-tile is tail)
+  float rsc[8], rsc2[8];  // per head: the cast's scales (see conv_row)
+};
+
+template <int SDT, int DDT>
+__global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_tile_cast(const __grid_constant__ TileArgs a) {
+  constexpr uint32_t SB = Tr<SDT>::B, DB = Tr<DDT>::B;
+  constexpr bool FOLD = KVX_FNUZ_FOLD && SDT == KV_F8E4M3FNUZ && DDT != KV_F8E4M3FNUZ;
+  extern __shared__ __align__(128) uint8_t tc_smem[];
+  const uint32_t S = (uint32_t)a.stages, SBY = (uint32_t)a.stage_bytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tc_smem + (size_t)S * SBY);
+  uint64_t* empty = full + S;
+  TcMeta* meta = reinterpret_cast<TcMeta*>(empty + S);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (uint32_t i = 0; i < S; ++i) {
+      mbar_init(full + i, 1);
+      mbar_init(empty + i, 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t n_mine = a.n_items > blockIdx.x ? (a.n_items - 1u - blockIdx.x) / gridDim.x + 1u : 0u;
+  const uint32_t nh = (uint32_t)a.nh, Bp = (uint32_t)a.Bp;
+  if (warp == 0) {
+    // ---- producer: metadata of 32 items at a time, lane-parallel (one round trip of
+    // dependent table loads per 32 sub-tiles), then one TMA issue per item by lane 0 ----
+    for (uint32_t g = 0; g < n_mine; g += 32u) {
+      const uint32_t cnt = min(32u, n_mine - g);
+      uint64_t m_dtile = 0;
+      int32_t m_hq0 = 0, m_soff = 0, m_si = 0, m_c = 0, m_h1 = 0, m_h2 = 0, m_sblk = 0, m_sl = 0;
+      uint32_t m_valid = 0;
+      float m_rsc[8], m_rsc2[8];
+#pragma unroll
+      for (int h = 0; h < 8; ++h) m_rsc[h] = m_rsc2[h] = 1.f;
+      if (lane < cnt) {
+        uint32_t n = blockIdx.x + (g + lane) * gridDim.x;
+        const uint32_t qi = divmod(n, a.f_nd);
+        const uint32_t part = divmod(n, a.f_parts);
+        const uint32_t sub = divmod(n, a.f_sub);
+        const uint32_t c = take_kv(n, a.kv1, a.c0);
+        const uint32_t l = divmod(n, a.f_l);
+        const uint32_t bl = n;
+        const int32_t r = __ldg(a.d_blk_req + bl);
+        const int32_t tok0 = __ldg(a.tok_off + r);
+        const int32_t T = __ldg(a.tok_off + r + 1) - tok0;
+        const int32_t j = bl - __ldg(a.d_blk_off + r);
+        const int64_t dblk = __ldg(a.d_blk_ids + bl);
+        const int32_t layer = a.lb + (int32_t)l;
+        const int32_t q = a.dst_rank[qi];
+        const int32_t hstart = a.share_p >= 0 ? max(a.share_p * a.Hp, q * a.Hd) : q * a.Hd;
+        const int32_t h0 = hstart + (int32_t)part * a.nh;
+        const int32_t p = a.share_p >= 0 ? a.share_p : h0 / a.Hp;
+        const int32_t hp0 = h0 - p * a.Hp, hq0 = h0 - q * a.Hd;
+        const int si = a.src_of_p[p];
+        const int32_t t0 = j * a.Bd + (int32_t)sub * a.Bp;
+        m_valid = t0 >= T ? 0u : (uint32_t)min(a.Bp, T - t0);
+        if (m_valid) m_sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + (j * (a.Bd / a.Bp) + (int32_t)sub));
+        const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          if ((uint32_t)h >= nh) break;
+          const int32_t hq = hq0 + h, hp = hp0 + h;
+          float rsc = 1.f, rsc2 = 1.f;
+          if constexpr (dual_scale(SDT, DDT)) {
+            rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+            rsc2 = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+          } else {
+            if constexpr (is_fp8(SDT) && SDT != DDT) rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+            if constexpr (is_fp8(DDT) && SDT != DDT) rsc = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+            rsc2 = rsc;   // one-scale casts read the destination's inverse from the second slot too
+          }
+          if constexpr (FOLD) rsc = fnuz_fold_scale(rsc);
+          m_rsc[h] = rsc;
+          m_rsc2[h] = rsc2;
+        }
+        m_dtile = (uint64_t)(a.dst[qi] +
+                             (dl * a.ds[KV_AX_LAYER] + (int64_t)c * a.ds[KV_AX_KV] + dblk * a.ds[KV_AX_BLOCK]) * DB);
+        m_hq0 = hq0;
+        m_soff = (int32_t)sub * a.Bp;
+        m_si = si;
+        m_c = (int32_t)c;
+        m_h1 = a.head_major ? 0 : hp0;
+        m_h2 = a.head_major ? hp0 : 0;
+        m_sl = (int32_t)sl;
+      }
+      for (uint32_t j = 0; j < cnt; ++j) {
+        const uint64_t dtile = __shfl_sync(0xFFFFFFFFu, (unsigned long long)m_dtile, j);
+        const int32_t hq0 = __shfl_sync(0xFFFFFFFFu, m_hq0, j), soff = __shfl_sync(0xFFFFFFFFu, m_soff, j);
+        const uint32_t valid = __shfl_sync(0xFFFFFFFFu, m_valid, j);
+        const int32_t si = __shfl_sync(0xFFFFFFFFu, m_si, j), c = __shfl_sync(0xFFFFFFFFu, m_c, j);
+        const int32_t h1 = __shfl_sync(0xFFFFFFFFu, m_h1, j), h2 = __shfl_sync(0xFFFFFFFFu, m_h2, j);
+        const int32_t sblk = __shfl_sync(0xFFFFFFFFu, m_sblk, j), sl = __shfl_sync(0xFFFFFFFFu, m_sl, j);
+        // lane h < nh takes head h's scales of item j
+        float rsc = 1.f, rsc2 = 1.f;
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const float v = __shfl_sync(0xFFFFFFFFu, m_rsc[h], j), v2 = __shfl_sync(0xFFFFFFFFu, m_rsc2[h], j);
+          if ((uint32_t)h == lane) {
+            rsc = v;
+            rsc2 = v2;
+          }
+        }
+        const uint32_t t = g + j, st = t % S;
+        if (lane == 0) mbar_wait_guarded(empty + st, ((t / S) & 1u) ^ 1u);
+        __syncwarp();
+        if (lane < nh) {
+          meta[st].rsc[lane] = rsc;
+          meta[st].rsc2[lane] = rsc2;
+        }
+        if (lane == 0) {
+          meta[st].dtile = reinterpret_cast<uint8_t*>(dtile);
+          meta[st].hq0 = hq0;
+          meta[st].soff = soff;
+          meta[st].valid = valid;
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_expect_tx_arrive(full + st, valid ? SBY : 0u);
+          if (valid) tma_load_5d(tc_smem + (size_t)st * SBY, &a.maps[si][c], 0, h1, h2, sblk, sl, full + st);
+        }
+      }
+    }
+    return;
+  }
+  // ---- consumers: rows of the staged sub-tile, D's inner order ----
+  const uint32_t cw = warp - 1u;
+  const uint32_t cpr = (uint32_t)a.D / 8u;  // 8-element chunks per row (D / 8 a power of two)
+  uint32_t lcpr = 0;
+  while ((1u << lcpr) < cpr) ++lcpr;
+  const uint32_t nchunks = nh * Bp * cpr;
+  const uint32_t row_bytes = (uint32_t)a.D * SB;
+  const uint32_t stage0 = smem_u32(tc_smem);
+  uint32_t lbp = 0, lnh = 0;   // Bp, nh: powers of two (host check) -- shifts, not divisions
+  while ((1u << lbp) < Bp) ++lbp;
+  while ((1u << lnh) < nh) ++lnh;
+  for (uint32_t t = cw; t < n_mine; t += kTbConsumers) {
+    const uint32_t st = t % S;
+    mbar_wait_guarded(full + st, (t / S) & 1u);
+    const TcMeta& m = meta[st];
+    uint8_t* const dtile = m.dtile;
+    const int32_t hq0 = m.hq0, soff = m.soff;
+    const uint32_t valid = m.valid;
+    const uint32_t buf = stage0 + st * SBY;
+    for (uint32_t idx = lane; idx < nchunks; idx += 32u) {
+      const uint32_t ri = idx >> lcpr, ch = idx & (cpr - 1u);
+      const uint32_t h = a.head_major ? ri >> lbp : ri & (nh - 1u);
+      const uint32_t sl_ = a.head_major ? ri & (Bp - 1u) : ri >> lnh;
+      Chunk<DDT, 8> o;
+      if (sl_ >= valid) {
+        zero_chunk(o);
+      } else {
+        Chunk<SDT, 8> x;
+        lds_chunk8<SDT>(x, buf + ri * row_bytes + ch * 8u * SB);
+        cast_chunk<SDT, DDT, 8, FOLD>(x, o, m.rsc[h], m.rsc2[h]);
+      }
+      store_chunk<DDT, 8>(dtile + ((int64_t)(hq0 + (int32_t)h) * a.ds[KV_AX_HEAD] +
+                                   (int64_t)(soff + (int32_t)sl_) * a.ds[KV_AX_SLOT] + (int64_t)ch * 8) * DB, o);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
@@ -2397,6 +2570,50 @@ cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaSt
   if (a.total == 0) return cudaSuccess;
   return vec == 8 ? unpack_v<8>(a, wdt, ddt, s) : unpack_v<1>(a, wdt, ddt, s);
 }
+namespace {
+template <int SDT, int DDT>
+cudaError_t tc_t(const TileArgs& a, cudaStream_t s) {
+  if constexpr (Tr<SDT>::B > 2) {
+    return cudaErrorInvalidValue;
+  } else {
+    auto k = k_tile_cast<SDT, DDT>;
+    const size_t smem = (size_t)a.stages * (size_t)a.stage_bytes + (size_t)a.stages * (16 + sizeof(TcMeta)) + 16;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, 32 * (1 + kTbConsumers), smem);
+    if (occ < 1) occ = 1;
+    const uint64_t need = (a.n_items + kTbConsumers - 1) / kTbConsumers;
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms() * occ));
+    k<<<grid, 32 * (1 + kTbConsumers), smem, s>>>(a);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+  }
+}
+template <int SDT>
+cudaError_t tc_d(const TileArgs& a, int ddt, cudaStream_t s) {
+  switch (ddt) {
+    case KV_F16: return tc_t<SDT, KV_F16>(a, s);
+    case KV_BF16: return tc_t<SDT, KV_BF16>(a, s);
+    case KV_F8E4M3: return tc_t<SDT, KV_F8E4M3>(a, s);
+    case KV_F8E4M3FNUZ: return tc_t<SDT, KV_F8E4M3FNUZ>(a, s);
+    case KV_F32: return tc_t<SDT, KV_F32>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+}  // namespace
+
+cudaError_t launch_tile_cast(const TileArgs& a, int sdt, int ddt, cudaStream_t s) {
+  if (a.n_items == 0) return cudaSuccess;
+  switch (sdt) {
+    case KV_F16: return tc_d<KV_F16>(a, ddt, s);
+    case KV_BF16: return tc_d<KV_BF16>(a, ddt, s);
+    case KV_F8E4M3: return tc_d<KV_F8E4M3>(a, ddt, s);
+    case KV_F8E4M3FNUZ: return tc_d<KV_F8E4M3FNUZ>(a, ddt, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_tile_copy(const TileArgs& a, cudaStream_t s) {
   if (a.n_items == 0) return cudaSuccess;
   const size_t smem = (size_t)a.stages * (size_t)a.stage_bytes + 8 * (size_t)a.stages;
@@ -2588,6 +2805,7 @@ cudaError_t touch(K k) {
 template <int SDT, int DDT>
 cudaError_t preload_tb() {
   if constexpr (Tr<SDT>::B <= 2) KVX_TOUCH(k_convert_tb<SDT, DDT>);
+  if constexpr (Tr<SDT>::B <= 2) KVX_TOUCH(k_tile_cast<SDT, DDT>);
   return cudaSuccess;
 }
 template <int SDT, int DDT>
