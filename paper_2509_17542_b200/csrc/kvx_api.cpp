@@ -366,7 +366,12 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
   const bool cast = src[0]->d.dtype != dst[0]->d.dtype;
   const int mode = cast ? tile_cast_mode() : tile_mode();
   if (mode == 0) return KV_OK;
-  if (cast && src[0]->elem_bytes > 2) return KV_OK;  // 1- and 2-byte sources (LDS of 8 / 16 B per chunk)
+  // the cast variant where it measured faster than the row kernel (c4-pair shapes,
+  // profiles/r02/tile_cast_vs_rows.txt): 2-byte sources into 1- or 2-byte destinations
+  // (bf16 -> e4m3 1.016 vs 0.983 of copy); 1-byte sources (e4m3 -> bf16 0.89 vs 0.98, fnuz ->
+  // e4m3 0.63 vs 0.84), 4-byte destinations (tie) and the per-P-rank share of the peer-store
+  // push (0.776 vs 0.791 of the link) stay on the row kernel
+  if (cast && (src[0]->elem_bytes != 2 || dst[0]->elem_bytes > 2 || share)) return KV_OK;
   const kv_layout *S = src[0], *D = dst[0];
   const int32_t* o = D->d.axis_order;
   int head_major;
