@@ -278,6 +278,7 @@ struct TbArgs {
   CUtensorMap maps[KVX_MAX_RANKS];
   int32_t tile_rows;  // 128-B rows per tile (B * D * esize / 128)
   int32_t stages;
+  int32_t mode;       // 1: head_dim-major (DIM, SLOT) tiles; 2: x-packed (D/x, SLOT, x), x = 16 B
 };
 cudaError_t launch_convert_tb(const TbArgs& a, int sdt, int ddt, cudaStream_t s);
 cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s);

@@ -1542,7 +1542,19 @@ __device__ __forceinline__ void lds_chunk8(Chunk<DT, 8>& c, uint32_t saddr) {
   }
 }
 
-template <int SDT, int DDT>
+// 16 bytes from a 32-bit shared-memory address into a 4-word chunk
+template <int DT, int VEC>
+__device__ __forceinline__ void lds_chunk16B(Chunk<DT, VEC>& c, uint32_t saddr) {
+  static_assert(Chunk<DT, VEC>::WORDS == 4, "lds_chunk16B: 16-byte chunks");
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(c.w[0]), "=r"(c.w[1]), "=r"(c.w[2]), "=r"(c.w[3])
+               : "r"(saddr));
+}
+
+// MODE 1: head_dim-major (DIM, SLOT) tiles, 8 x 8 transposes.  MODE 2: x-packed
+// (D/x, SLOT, x) tiles with x = 16 B of elements: every 16-B chunk is already x consecutive
+// head_dim elements of one slot, so a consumer lane takes whole chunks (no transpose).
+template <int SDT, int DDT, int MODE>
 __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __grid_constant__ TbArgs A) {
   constexpr uint32_t DB = Tr<DDT>::B, SB = Tr<SDT>::B;
   static_assert(SB == 1 || SB == 2, "k_convert_tb: 1- or 2-byte sources");
@@ -1643,6 +1655,28 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
     mbar_wait_guarded(full + st, (t / S) & 1u);
     const TbMeta m = meta[st];
     const uint32_t tile = stage0 + st * tile_bytes;
+    if constexpr (MODE == 2) {
+      constexpr uint32_t X = 16u / SB;                  // elements per 16-B chunk
+      const uint32_t lndq = lcpr + 3u - (SB == 1 ? 4u : 3u);   // log2(D / X)
+      const uint32_t ndq = 1u << lndq;
+      for (uint32_t idx = lane; idx < (ndq << 4); idx += 32u) {
+        const uint32_t dq = idx & (ndq - 1u), sl = idx >> lndq;   // lanes: consecutive chunks of one row
+        const uint32_t off = ((dq << 4) + sl) << 4;                // chunk (dq, slot) of the tile
+        const uint32_t R = off >> 7, c = (off >> 4) & 7u;
+        Chunk<DDT, X> o;
+        if (sl >= m.valid) {
+          zero_chunk(o);
+        } else {
+          Chunk<SDT, X> x;
+          lds_chunk16B<SDT, X>(x, tile + R * 128u + ((c ^ (R & 7u)) << 4));
+          cast_chunk<SDT, DDT, X, FOLD>(x, o, m.rsc, m.s2);
+        }
+        store_chunk<DDT, X>(m.db + ((int64_t)sl * a.ds[KV_AX_SLOT] + dim_off(dq * X, a.ds[KV_AX_DIM], a.d_dk)) * DB, o);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+      continue;
+    }
     for (uint32_t u = lane; u < nsub; u += 32u) {
       const uint32_t s_sub = u & 1u, d_sub = u >> 1;
       const uint32_t s0 = s_sub << 3, d0 = d_sub << 3;
@@ -2518,7 +2552,7 @@ cudaError_t launch_convert_tr(const ConvArgs& a, int sdt, int ddt, cudaStream_t 
 namespace {
 template <int SDT, int DDT>
 cudaError_t tb_t(const TbArgs& a, cudaStream_t s) {
-  auto k = k_convert_tb<SDT, DDT>;
+  auto k = a.mode == 2 ? k_convert_tb<SDT, DDT, 2> : k_convert_tb<SDT, DDT, 1>;
   const size_t tile = (size_t)a.tile_rows * 128u;
   const size_t smem = 1024 + (size_t)a.stages * tile + (size_t)a.stages * (16 + sizeof(TbMeta));
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -2804,7 +2838,8 @@ cudaError_t touch(K k) {
 
 template <int SDT, int DDT>
 cudaError_t preload_tb() {
-  if constexpr (Tr<SDT>::B <= 2) KVX_TOUCH(k_convert_tb<SDT, DDT>);
+  if constexpr (Tr<SDT>::B <= 2) KVX_TOUCH(k_convert_tb<SDT, DDT, 1>);
+  if constexpr (Tr<SDT>::B <= 2) KVX_TOUCH(k_convert_tb<SDT, DDT, 2>);
   if constexpr (Tr<SDT>::B <= 2) KVX_TOUCH(k_tile_cast<SDT, DDT>);
   return cudaSuccess;
 }

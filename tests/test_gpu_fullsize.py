@@ -71,7 +71,7 @@ def test_fullsize_vendor_layouts(o1):
     rank 0 -> 0) from an other-vendor P cache -- x-packed K pool ([LAYER], BLOCK, HEAD,
     D/8, SLOT, 8) and head_dim-major V pool ([LAYER], BLOCK, HEAD, DIM, SLOT) -- into the
     NVIDIA-style D pool (BLOCK, LAYER, KV, HEAD, SLOT, DIM), bf16 -> e4m3, in the two
-    calls tools/variants_bench.py times (k_convert_tr8 for K, k_convert_tb for V).  Sampled: requests 0 / 17 / 31 x
+    calls tools/variants_bench.py times (k_convert_tb for both).  Sampled: requests 0 / 17 / 31 x
     layers 0 / 40 / 79, all their blocks, vs O1 on the extracted blocks; canary outside."""
     import paper_2509_17542_b200 as kvx
     from synth import BLOCK, DIM, HEAD, KV, LAYER, SLOT
@@ -95,7 +95,7 @@ def test_fullsize_vendor_layouts(o1):
     sbt = kvx.Batch(Kl, n_tokens, st, dev)
     dbt = kvx.Batch(Dl, n_tokens, dt_, dev)
     kvx.convert_reshard([Kl], [Kp], sbt, [Dl], [DP], dbt)
-    assert kvx.last_kernel() == "k_convert_tr8"
+    assert kvx.last_kernel() == "k_convert_tb"   # x-packed tiles through TMA
     kvx.convert_reshard([Vl], [Vp], sbt, [Dl], [DP], dbt)
     assert kvx.last_kernel() == "k_convert_tb"   # head_dim-major tiles through TMA
     torch.cuda.synchronize()

@@ -607,25 +607,29 @@ def test_tr8_w16(o1, monkeypatch, sdt, ddt, Bp, Bd, tp, do):
         assert kvx.last_kernel() == "k_convert_tr8"
 
 
-@pytest.mark.parametrize("sdt,ddt,D,tp,n_tokens", [
-    (BF16, E4M3, 128, (2, 1), [70, 0, 1, 37, 129, 16]),
-    (BF16, BF16, 128, (1, 1), [300, 15, 17]),
-    (F16, FNUZ, 64, (2, 4), [33, 64, 1]),
-    (BF16, F32, 256, (1, 2), [48, 5]),
-    (F16, F16, 128, (4, 2), [1000, 3, 0, 31]),
-    (E4M3, BF16, 128, (2, 1), [70, 0, 1, 37]),
-    (FNUZ, E4M3, 128, (2, 2), [129, 16, 3]),
-    (FNUZ, F32, 64, (1, 2), [40, 17]),
-    (E4M3, E4M3, 256, (2, 1), [33, 1]),
+@pytest.mark.parametrize("sdt,ddt,D,tp,n_tokens,split", [
+    (BF16, E4M3, 128, (2, 1), [70, 0, 1, 37, 129, 16], 0),
+    (BF16, BF16, 128, (1, 1), [300, 15, 17], 0),
+    (F16, FNUZ, 64, (2, 4), [33, 64, 1], 0),
+    (BF16, F32, 256, (1, 2), [48, 5], 0),
+    (F16, F16, 128, (4, 2), [1000, 3, 0, 31], 0),
+    (E4M3, BF16, 128, (2, 1), [70, 0, 1, 37], 0),
+    (FNUZ, E4M3, 128, (2, 2), [129, 16, 3], 0),
+    (FNUZ, F32, 64, (1, 2), [40, 17], 0),
+    (E4M3, E4M3, 256, (2, 1), [33, 1], 0),
+    # x-packed (D/x, SLOT, x) tiles with x = 16 bytes (other vendors' key cache)
+    (BF16, E4M3, 128, (2, 1), [70, 0, 1, 37], 8),
+    (F16, BF16, 64, (2, 4), [129, 16], 8),
+    (BF16, F32, 256, (1, 2), [17, 48], 8),
 ])
-def test_tb_tiles(o1, monkeypatch, sdt, ddt, D, tp, n_tokens):
+def test_tb_tiles(o1, monkeypatch, sdt, ddt, D, tp, n_tokens, split):
     """k_convert_tb (head_dim-major 1- or 2-byte source tiles of 16 slots through TMA, swizzled
     shared-memory stages, warp-specialised producer / consumers) into D's rows: bit-exact vs
     O1 and identical to k_convert_tr8 (KVX_TB=0), ragged requests (0, 1, 15, 17 tokens),
     TP merge and split, every destination dtype width."""
     import paper_2509_17542_b200 as kvx
     case = make_case(3, 8, D, tp[0], tp[1], 16, 16, n_tokens, sdt, ddt, _VCOL, synth.D_ORDER,
-                     seed=D + tp[0] * 10 + tp[1] + sdt, o1=o1, scales="pow2")
+                     seed=D + tp[0] * 10 + tp[1] + sdt + split, o1=o1, scales="pow2", p_split=split)
     if sdt in FP8:
         for i, lay in enumerate(case["src_lays"]):
             lay["scales"] = synth.pow2_scales(950 + i, 3, 8 // tp[0], -2, 2)
