@@ -363,7 +363,9 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
                         const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst, void* const* dst_pools,
                         const kv_batch* dst_bt, int32_t lb, int32_t le, kv_stream stream, bool share, bool* used) {
   *used = false;
-  const bool cast = src[0]->d.dtype != dst[0]->d.dtype;
+  // KVX_TT_SAME=1 (experiment): same-dtype converts through the consumer-warp kernel too
+  const char* same_env = getenv("KVX_TT_SAME");
+  const bool cast = src[0]->d.dtype != dst[0]->d.dtype || (same_env && atoi(same_env) == 1);
   const int mode = cast ? tile_cast_mode() : tile_mode();
   if (mode == 0) return KV_OK;
   // the cast variant where it measured faster than the row kernel (c4-pair shapes,
@@ -479,6 +481,7 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
     a.Lc = l1 - l0;
     a.f_l = make_fastdiv((uint32_t)a.Lc);
     a.n_items = (uint32_t)(per_layer * (uint64_t)a.Lc);
+    t_last_kernel = cast ? "k_tile_cast" : "k_tile_copy";
     cudaError_t e = cast ? launch_tile_cast(a, S->d.dtype, D->d.dtype, (cudaStream_t)stream)
                          : launch_tile_copy(a, (cudaStream_t)stream);
     if (e != cudaSuccess) return cuda_fail(e, "kv_convert_reshard: tile launch");
@@ -744,7 +747,7 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
                             &used)) != KV_OK)
       return st;
     if (used) {
-      t_last_kernel = S->d.dtype == D->d.dtype ? "k_tile_copy" : "k_tile_cast";
+      // (t_last_kernel set by try_tile_copy: k_tile_copy or k_tile_cast)
       return KV_OK;
     }
   }
