@@ -79,6 +79,8 @@ def parse():
     ap.add_argument("--no-verify", action="store_true", help="skip the K6 full-size check")
     ap.add_argument("--no-nvlink-probe", action="store_true")
     ap.add_argument("--cpu-sample-layers", type=int, default=0)
+    ap.add_argument("--oversubscribe", action="store_true",
+                    help="N >= 2 validation on fewer GPUs: ranks share GPUs, gloo control plane (not a bench number)")
     return ap.parse_args()
 
 
@@ -611,9 +613,8 @@ def run_multi(args):
     from paper_2509_17542_b200 import transfer as tr
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
+    local, barrier_t = _init_dist(args, local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
     wl_name = args.workload or "c4"
     cfg = _subset(synth.configs()[wl_name], args)
     n_p, n_d = tr.present_ranks(cfg.tp_p, cfg.tp_d, world)
@@ -626,7 +627,6 @@ def run_multi(args):
     my_p = sorted({p for p, q, _, _ in pairs if me.kind == "D" and q == me.tp_rank})
     NB_p, NB_d = synth.pool_capacity(cfg.n_tokens, cfg.B_p), synth.pool_capacity(cfg.n_tokens, cfg.B_d)
     stream = torch.cuda.current_stream()
-    barrier_t = torch.zeros(1, device=dev)
 
     def barrier():
         dist.all_reduce(barrier_t)
@@ -905,6 +905,8 @@ def run_multi(args):
                        "control_plane": "layouts, block tables and fp8 scales exchanged as kv_ctrl messages "
                                         f"({allx[0]['ctrl']['bytes_received']} B)",
                        "l2": "inputs larger than L2 (no flush)",
+                       "oversubscribed": (f"{world} ranks on {torch.cuda.device_count()} GPUs: validation of the "
+                                          "N-rank path, not a bench number") if args.oversubscribe else None,
                        "parallelism": f"P TP{cfg.tp_p} x D TP{cfg.tp_d}, {n_p}+{n_d} ranks present"},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_NOMINAL_GBS,
                          "unit": "GB/s", "frac": round(achieved / NVLINK_NOMINAL_GBS, 4),
@@ -1016,9 +1018,8 @@ def run_stream(args):
     from paper_2509_17542_b200 import transfer as tr
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
+    local, barrier_t = _init_dist(args, local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
     cfg = synth.configs()["c5"]
     plan = tr.StreamPlan(world, cfg.tp_p, cfg.tp_d, cfg.H, len(cfg.n_tokens))
     me = plan.role(rank)
@@ -1175,7 +1176,6 @@ def run_stream(args):
     for _ in range(max(args.warmup, 1)):
         step()
     torch.cuda.synchronize()
-    barrier_t = torch.zeros(1, device=dev)
     dist.all_reduce(barrier_t)
     torch.cuda.synchronize()
     notify = pull and me.kind == "D" and not args.c5_batch and not args.c5_per_request_launch
@@ -1278,6 +1278,8 @@ def run_stream(args):
                           else "push, whole instance batch per launch" if args.c5_batch else
                           f"push per request, layer chunks >= {args.chunk_mib} MiB",
                           "control_plane": "layouts and block tables exchanged as kv_ctrl messages",
+                          "oversubscribed": (f"{world} ranks on {torch.cuda.device_count()} GPUs: validation of the "
+                                             "N-rank path, not a bench number") if args.oversubscribe else None,
                           "l2": "inputs larger than L2 (no flush)"},
                "latency_ms": {"p50": round(alll[len(alll) // 2], 3) if alll else None,
                               "p99": round(alll[min(len(alll) - 1, int(0.99 * len(alll)))], 3) if alll else None,
@@ -1298,6 +1300,30 @@ def run_stream(args):
     for a, o in maps:
         kvx.ipc_close(a, o)
     dist.destroy_process_group()
+
+
+def _init_dist(args, local):
+    """One process per GPU over NCCL (the contract).  --oversubscribe (validation of the
+    N-rank host logic on fewer GPUs, e.g. world 8 on a 4-GPU box): ranks share GPUs -- rank r
+    on GPU r // ceil(world / n_gpus), so the two ranks of a GPU play the same role -- and the
+    control plane runs over gloo (NCCL refuses two ranks on one GPU).  Timings taken that way
+    are not bench numbers.  Returns (device index, barrier tensor)."""
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ["WORLD_SIZE"])
+    if getattr(args, "oversubscribe", False):
+        if args.mode == "nccl":
+            raise SystemExit("--oversubscribe: the NCCL transport cannot run two ranks on one GPU")
+        ndev = torch.cuda.device_count()
+        per = -(-world // ndev)
+        idx = local // per
+        torch.cuda.set_device(idx)
+        dist.init_process_group("gloo")
+        return idx, torch.zeros(1)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    return local, torch.zeros(1, device=dev)
 
 
 def _json_only_stdout():
