@@ -72,3 +72,22 @@ def test_c5_stream_pull():
         pytest.skip("needs 4 GPUs")
     d = _bench(4, "--workload", "c5", "--mode", "pull")
     assert d["fullsize"]["ok"] is True, d["fullsize"]
+
+
+@pytest.mark.parametrize("workload", ["c4", "c5"])
+def test_world8_oversubscribed(workload):
+    """The full 8-rank configurations (c4: P TP4 -> D TP4, four pairs; c5: two P instances x
+    TP2 -> D TP4) as 8 processes on the GPUs available (two or more ranks per GPU, same role
+    per GPU, gloo control plane): parity and K6 on every D rank (not a performance run)."""
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "bench.py"), "--gpus", "8",
+           "--oversubscribe", "--steps", "1", "--warmup", "1", "--no-e2e", "--no-nvlink-probe", "--workload", workload]
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1200)
+    assert out.returncode == 0, out.stderr[-3000:]
+    d = json.loads(out.stdout.splitlines()[0])
+    assert d["n_gpus"] == 8 and d["config"]["oversubscribed"]
+    assert d["fullsize"]["ok"] is True, d["fullsize"]
+    if workload == "c4":
+        assert len(d["parity"]) == 4 and all(p["ok"] for p in d["parity"]), d["parity"]
