@@ -463,7 +463,7 @@ def run_single(args):
     if not args.no_verify:
         out["fullsize"] = k6_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, step)
     if not args.no_e2e:
-        out["e2e"] = e2e_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, min(K, 3), stream, sb)
+        out["e2e"] = e2e_single(cfg, P, Dr, pt, dt_, S, SP, src_bt, Dl, DP, dst_bt, min(K, 3), stream, sb)
     if not args.no_cpu_baseline:
         # about 10-30 s of single-thread O1: c4 (fp8 cast) ~31 MB/s -> 24 layers of request 0
         nl = args.cpu_sample_layers or min(cfg.L, 24 if cfg.H * cfg.D * cfg.n_tokens[0] > (1 << 21) else 12)
@@ -508,20 +508,48 @@ def k6_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, step):
                     "(valid = hash code, tail = 0, unused blocks = canary)"}
 
 
-def e2e_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, K, stream, sb):
-    """Same metric through the public API with HOST buffers: every step uploads the P pools
-    from pinned memory and reads the D pools back, inside the timed region.  The upload is
-    split by layer chunks (the P pools are layer-major, so a chunk is contiguous) on a copy
-    stream, so chunk k+1 crosses PCIe while chunk k converts; the D pools are read back once
-    the step's last chunk has converted."""
+def _block_view(pool, d):
+    """A pool as [outer, num_blocks, inner] int32 words (outer / inner: the axes before / after
+    BLOCK in its order), for moving whole blocks."""
+    import torch
+    ext = {synth.LAYER: d["L"], synth.KV: 2, synth.BLOCK: d["NB"], synth.SLOT: d["B"], synth.HEAD: d["H"] // d["tp"],
+           synth.DIM: d["D"]}
+    order = d["order"]
+    bi = order.index(synth.BLOCK)
+    outer = int(np.prod([ext[a] for a in order[:bi]])) if bi else 1
+    inner = int(np.prod([ext[a] for a in order[bi + 1:]])) * synth.NBYTES[d["dtype"]]
+    assert inner % 4 == 0
+    return pool.view(torch.uint8).view(torch.int32).view(outer, d["NB"], inner // 4)
+
+
+def e2e_single(cfg, P, Dr, pt, dt_, S, SP, src_bt, Dl, DP, dst_bt, K, stream, sb):
+    """Same metric through the public API with HOST buffers: every step moves the batch's
+    blocks of the P pools up from pinned memory and its D blocks back, inside the timed
+    region -- only the blocks the block tables name (the pools' ~10% free blocks stay put):
+    H2D into a device staging copy, scattered into the pools by block id, the convert, then
+    the D blocks gathered and read back.  The upload is split by the P pools' outer axes
+    (layer-major: layer chunks) on a copy stream, so chunk k+1 crosses PCIe while chunk k
+    converts."""
     import torch
     import paper_2509_17542_b200 as kvx
-    hs = [_pinned_copy(p) for p in SP]
-    hd = [_pinned_empty(p.numel()) for p in DP]
-    lay_major = cfg.p_order[0] == synth.LAYER
+    dev = SP[0].device
+    p_ids = torch.as_tensor(sorted({b for t in pt for b in t}), dtype=torch.long, device=dev)
+    d_ids = torch.as_tensor(sorted({b for t in dt_ for b in t}), dtype=torch.long, device=dev)
+    pv = [_block_view(pool, P[i][0]) for i, pool in enumerate(SP)]
+    dv = [_block_view(pool, Dr[i][0]) for i, pool in enumerate(DP)]
+    # pinned host copies of exactly the batch's blocks; device staging of the same shape
+    hs, stage_p = [], []
+    for v in pv:
+        comp = v.index_select(1, p_ids)
+        h = _pinned_empty(comp.numel() * 4).view(torch.int32).view(comp.shape)
+        h.copy_(comp)
+        hs.append(h)
+        stage_p.append(comp)
+    stage_d = [v.index_select(1, d_ids) for v in dv]
+    hd = [_pinned_empty(x.numel() * 4).view(torch.int32).view(x.shape) for x in stage_d]
+    lay_major = cfg.p_order[0] == synth.LAYER and cfg.p_order[1] == synth.KV
     n_ch = 8 if lay_major else 1
     bounds = [(i * cfg.L // n_ch, (i + 1) * cfg.L // n_ch) for i in range(n_ch)]
-    per_layer = [p.numel() // cfg.L for p in SP]
     up, down = torch.cuda.Stream(), torch.cuda.Stream()
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -529,33 +557,37 @@ def e2e_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, K, stream, sb):
     up.wait_stream(stream)
     down.wait_stream(stream)
     for _ in range(K):
-        up.wait_stream(stream)            # the previous step's converts are done reading
+        up.wait_stream(stream)            # the previous step's scatters / converts are done
         for l0, l1 in bounds:
+            r0, r1 = (2 * l0, 2 * l1) if lay_major else (0, pv[0].shape[0])
             with torch.cuda.stream(up):
-                for d, h, pl in zip(SP, hs, per_layer):
-                    a, b = (l0 * pl, l1 * pl) if lay_major else (0, d.numel())
-                    d[a:b].copy_(h[a:b], non_blocking=True)
+                for st_, h in zip(stage_p, hs):
+                    st_[r0:r1].copy_(h[r0:r1], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(up)
             stream.wait_event(ev)
             stream.wait_stream(down)      # the previous read-back is done with the D pools
+            for v, st_ in zip(pv, stage_p):
+                v[r0:r1].index_copy_(1, p_ids, st_[r0:r1])
             kvx.convert_reshard(S, SP, src_bt, Dl, DP, dst_bt, (l0, l1), stream)
+        for v, st_ in zip(dv, stage_d):
+            torch.index_select(v, 1, d_ids, out=st_)
         down.wait_stream(stream)
         with torch.cuda.stream(down):
-            for d, h in zip(DP, hd):
-                h.copy_(d, non_blocking=True)
+            for st_, h in zip(stage_d, hd):
+                h.copy_(st_, non_blocking=True)
     stream.wait_stream(down)
     stream.wait_stream(up)
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / K
-    h2d, d2h = int(sum(h.numel() for h in hs)), int(sum(h.numel() for h in hd))
-    del hs, hd
+    h2d, d2h = int(sum(h.numel() * 4 for h in hs)), int(sum(h.numel() * 4 for h in hd))
+    del hs, hd, stage_p, stage_d
     _unpin_all()
     return {"value": round(sb / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 3),
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": K, "pipelined": f"{len(bounds)} layer chunks uploaded ahead of their convert; D pools read back "
-                                     "after the step (whole pools: the ~10% free-block slack crosses PCIe too)"}
+            "steps": K, "pipelined": f"{len(bounds)} layer chunks uploaded ahead of their convert; only the batch's "
+                                     "blocks cross PCIe (device staging + block scatter / gather)"}
 
 
 # ------------------------------------------------------------------------------------
@@ -942,14 +974,19 @@ def run_multi(args):
 
 
 def e2e_multi(mine, me, step, stream, barrier, err, ke, rank):
-    """Same metric through the public API with host buffers: every step the P rank uploads
-    its source pool from pinned memory before the transfer, the D rank reads its pool back."""
+    """Same metric through the public API with host buffers: every step the P rank uploads its
+    batch's blocks from pinned memory (staging + scatter by block id) before the transfer, the
+    D rank gathers its batch's blocks and reads them back -- only the blocks the tables name."""
     import torch
-    host = None
-    if me.kind == "P":
-        host = _pinned_copy(mine["pool"])
-    elif me.kind == "D":
-        host = _pinned_empty(mine["pool"].numel())
+    host = stage = view = ids = None
+    if me.kind in ("P", "D"):
+        dev = mine["pool"].device
+        ids = torch.as_tensor(sorted({b for t in mine["tables"] for b in t}), dtype=torch.long, device=dev)
+        view = _block_view(mine["pool"], mine["d"])
+        stage = view.index_select(1, ids)
+        host = _pinned_empty(stage.numel() * 4).view(torch.int32).view(stage.shape)
+        if me.kind == "P":
+            host.copy_(stage)
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
@@ -957,16 +994,18 @@ def e2e_multi(mine, me, step, stream, barrier, err, ke, rank):
     e0.record(stream)
     for _ in range(ke):
         if me.kind == "P":
-            mine["pool"].copy_(host, non_blocking=True)
+            stage.copy_(host, non_blocking=True)
+            view.index_copy_(1, ids, stage)
         step()
         if me.kind == "D":
-            host.copy_(mine["pool"], non_blocking=True)
+            torch.index_select(view, 1, ids, out=stage)
+            host.copy_(stage, non_blocking=True)
     e1.record(stream)
     torch.cuda.synchronize()
     if int(err.item()):
         raise SystemExit(f"rank {rank}: flag wait timed out (e2e)")
-    n = host.numel() if host is not None else 0
-    del host
+    n = host.numel() * 4 if host is not None else 0
+    del host, stage
     _unpin_all()
     return {"ms": e0.elapsed_time(e1), "steps": ke, "h2d": n if me.kind == "P" else 0,
             "d2h": n if me.kind == "D" else 0}
