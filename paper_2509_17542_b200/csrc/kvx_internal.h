@@ -242,6 +242,10 @@ kv_status compute_scales_impl(int32_t n_src, const kv_layout* const* src, const 
                               const kv_batch* src_bt, const kv_layout* dst, float* out_scales, int32_t lb, int32_t le,
                               kv_stream stream, bool share, float* peer);
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s);
+// fp8 -> other fp8 through per-(dst rank, layer, K/V, head) code tables in shared memory
+// (k_requant_rows); the launch's tables must fit kRequantMaxTables x 256 B
+constexpr uint32_t kRequantMaxTables = 384;
+cudaError_t launch_requant(const ConvArgs& a, int sdt, int ddt, cudaStream_t s);
 // per-request completion words (kv_convert_reshard_notify): before the row kernel, zero the
 // counters and complete the requests with no blocks; or, after any other launch, complete all
 struct Notify {

@@ -712,7 +712,7 @@ __device__ __forceinline__ float fnuz_fold_scale(float s) {
 template <int SDT, int DDT, bool FOLD = false>
 __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint32_t lane, uint64_t& sp,
                                          uint64_t& dp, float& rsc, uint32_t& rz, float& rsc2,
-                                         int32_t* req_out = nullptr) {
+                                         int32_t* req_out = nullptr, uint32_t* tbl_out = nullptr) {
   // destination fastest: with several D ranks (fan-out, e.g. a TP split pushed over
   // NVLink) concurrent warps write every destination at once instead of one link after
   // the other -- with the D rank outermost, all P ranks of a fan-in/fan-out hit the same
@@ -739,6 +739,8 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
   const uint32_t lh = a.slot_inner ? (lane >> ts_log2) : (lane & ((1u << (5u - ts_log2)) - 1u));
   const uint32_t slot = (s_blk << ts_log2) + ls;
   const uint32_t hl = (sbk << (5u - ts_log2)) + lh;  // head within the converted range
+  // (dst index, layer, K/V, head) table of the LUT requantisation (k_requant_rows)
+  if (tbl_out) *tbl_out = ((qi * (uint32_t)a.Lc + l) * (a.kv1 ? 1u : 2u) + (a.kv1 ? 0u : c)) * (uint32_t)a.Hd_eff + hl;
   const uint32_t hq = (uint32_t)a.hq_off[qi] + hl;      // D-local head
   sp = 0;
   dp = 0;
@@ -1887,6 +1889,99 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_tile_cast(const __g
 }
 
 // ------------------------------------------------------------------------------------
+// fp8 -> other fp8 requantisation through code tables (k_requant_rows; e4m3fnuz <-> e4m3fn
+// with static scales, readings 24-26).  With both scales fixed per (layer, K/V, head) the
+// cast is a pure function of the 8-bit code, so each CTA first builds the 256-entry tables
+// of every (dst rank, layer, K/V, head) of the launch in shared memory -- each entry by the
+// exact per-code path (fp8x4_to_f32, the two multiplies, the packed conversion), so the
+// tables are bit-identical to the arithmetic kernels -- and the row loop then maps each code
+// with one byte permute (code into the table base) and one LDS.U8.
+// ------------------------------------------------------------------------------------
+constexpr uint32_t kLutMaxTables = 384;  // 96 KB of tables per CTA
+
+template <int SDT, int DDT, int U>
+__global__ void __launch_bounds__(kThreads, 2) k_requant_rows(const __grid_constant__ ConvArgs a) {
+  static_assert(dual_scale(SDT, DDT), "k_requant_rows: fp8 -> other fp8");
+  extern __shared__ __align__(256) uint8_t lut[];
+  const uint32_t kv = a.kv1 ? 1u : 2u;
+  const uint32_t n_tab = a.f_nd.d * (uint32_t)a.Lc * kv * (uint32_t)a.Hd_eff;
+  // ---- tables: entry (t, code) ----
+  for (uint32_t e = threadIdx.x; e < n_tab * 256u; e += blockDim.x) {
+    const uint32_t code = e & 255u;
+    uint32_t t = e >> 8;
+    const uint32_t hl = t % (uint32_t)a.Hd_eff;
+    t /= (uint32_t)a.Hd_eff;
+    const uint32_t c = a.kv1 ? (uint32_t)a.c0 : (t % 2u);
+    if (!a.kv1) t /= 2u;
+    const uint32_t l = t % (uint32_t)a.Lc, qi = t / (uint32_t)a.Lc;
+    const uint32_t hq = (uint32_t)a.hq_off[qi] + hl;
+    const int64_t layer = a.lb + (int64_t)l;
+    const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;
+    const uint32_t h = (uint32_t)a.dst_rank[qi] * (uint32_t)a.Hd + hq;
+    const uint32_t p = fdiv(h, a.f_hp);
+    const uint32_t hp = h - p * (uint32_t)a.Hp;
+    const int si = a.src_of_p[p];
+    const float ssc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
+    const float inv = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
+    Chunk<SDT, 4> in;
+    Chunk<DDT, 4> out;
+    in.w[0] = code;
+    cast_chunk<SDT, DDT, 4>(in, out, ssc, inv);
+    lut[e] = (uint8_t)(out.w[0] & 0xFFu);
+  }
+  __syncthreads();
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
+  const uint32_t cs = (uint32_t)a.cpr_shift;  // log2(16-byte chunks per row)
+  const uint32_t cmask = (1u << cs) - 1u, nch = 32u << cs;
+  const uint32_t lut0 = smem_u32(lut);
+  for (uint32_t item = warp; item < a.n_items; item += nwarps) {
+    uint64_t sp, dp;
+    float rsc, rsc2;
+    uint32_t rz, tbl = 0;
+    conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz, rsc2, nullptr, &tbl);
+    const uint32_t tbase = lut0 + (tbl << 8);
+    for (uint32_t base = 0; base < nch; base += 32u * U) {
+      uint4 in[U];
+      uint64_t d[U];
+      uint32_t z[U], tb[U], ch[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const uint32_t idx = base + (uint32_t)k * 32u + lane;
+        const uint32_t rr = (idx >> cs) & 31u;
+        ch[k] = idx & cmask;
+        const uint64_t s = __shfl_sync(0xffffffffu, sp, rr);
+        d[k] = __shfl_sync(0xffffffffu, dp, rr);
+        z[k] = __shfl_sync(0xffffffffu, rz, rr) | (idx >= nch ? 2u : 0u);
+        tb[k] = __shfl_sync(0xffffffffu, tbase, rr);
+        if (z[k] == 0) in[k] = __ldg(reinterpret_cast<const uint4*>(s + ch[k] * 16u));
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        if (z[k] & 2u) continue;
+        uint4 o = make_uint4(0, 0, 0, 0);
+        if (z[k] == 0) {
+          uint32_t w[4] = {in[k].x, in[k].y, in[k].z, in[k].w}, r[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t b[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const uint32_t addr = __byte_perm(w[q], tb[k], 0x7650u + (uint32_t)j);  // code j | table base
+              asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b[j]) : "r"(addr));
+            }
+            r[q] = __byte_perm(__byte_perm(b[0], b[1], 0x0040u), __byte_perm(b[2], b[3], 0x0040u), 0x5410u);
+          }
+          o = make_uint4(r[0], r[1], r[2], r[3]);
+        }
+        *reinterpret_cast<uint4*>(d[k] + ch[k] * 16u) = o;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------------
 // K3 persistent staged pull (kv_pull_staged, D side): the unpack row machinery over every
 // layer chunk of the call in ONE launch.  Warps take kPullGrab items at a time from a
 // per-chunk counter (chunk after chunk), so all warps leave a chunk within one grab of each
@@ -2592,6 +2687,39 @@ cudaError_t launch_convert_tr8(const ConvArgs& a, int sdt, int ddt, cudaStream_t
   if (a.n_items == 0) return cudaSuccess;
   return tr8_v<8>(a, sdt, ddt, s);
 }
+cudaError_t launch_requant(const ConvArgs& a0, int sdt, int ddt, cudaStream_t s) {
+  if (a0.total64 == 0) return cudaSuccess;
+  ConvArgs a = a0;
+  const uint32_t cpr = a.f_cpr.d;  // 8-element chunks per row (D / 8)
+  if (cpr < 2) return cudaErrorInvalidValue;
+  a.cpr_shift = log2_pow2(cpr / 2);  // 16-byte chunks
+  a.rows_per_tile = a.Bd * a.Hd_eff;
+  uint32_t ts, th;
+  subtile_shape((uint32_t)a.Bd, (uint32_t)a.Hd_eff, &ts, &th);
+  a.ts_log2 = log2_pow2(ts);
+  const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.Hd_eff + th - 1) / th;
+  a.f_sb = make_fastdiv(nsb);
+  a.f_items = make_fastdiv(nsb * nhb);
+  a.n_items = (uint32_t)(a.total64 / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);
+  const uint32_t n_tab = a.f_nd.d * (uint32_t)a.Lc * (a.kv1 ? 1u : 2u) * (uint32_t)a.Hd_eff;
+  const size_t smem = (size_t)n_tab * 256u;
+  auto launch = [&](auto k) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem);
+    if (occ < 1) occ = 1;
+    const uint64_t need = (a.n_items + (kThreads / 32) - 1) / (kThreads / 32);
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms() * occ));
+    k<<<grid, kThreads, smem, s>>>(a);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError();
+  };
+  if (sdt == KV_F8E4M3FNUZ && ddt == KV_F8E4M3) return launch(k_requant_rows<KV_F8E4M3FNUZ, KV_F8E4M3, 8>);
+  if (sdt == KV_F8E4M3 && ddt == KV_F8E4M3FNUZ) return launch(k_requant_rows<KV_F8E4M3, KV_F8E4M3FNUZ, 8>);
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s) {
   if (a.total64 == 0) return cudaSuccess;
   return vec == 8 ? conv_v<8>(a, sdt, ddt, s) : conv_v<1>(a, sdt, ddt, s);
@@ -2882,6 +3010,8 @@ cudaError_t preload_kernels() {
   if ((e = preload_src<KV_F8E4M3FNUZ>()) != cudaSuccess) return e;
   if ((e = preload_src<KV_F32>()) != cudaSuccess) return e;
   KVX_TOUCH(k_tile_copy);
+  KVX_TOUCH((k_requant_rows<KV_F8E4M3FNUZ, KV_F8E4M3, 8>));
+  KVX_TOUCH((k_requant_rows<KV_F8E4M3, KV_F8E4M3FNUZ, 8>));
   KVX_TOUCH(k_amax_init);
   KVX_TOUCH(k_amax_finalize);
   KVX_TOUCH(k_signal);
