@@ -470,8 +470,6 @@ def run_single(args):
 def single_parity(cfg, P, Dr, pt, dt_, SP, DP, sb):
     """O1 on the measured buffers: every request when the whole batch is small (c1, c2, c3),
     else the first and the last request -- all layers, all ranks."""
-    # O1 on the measured buffers: every request when the whole batch is small (c1, c2,
-    # c3), else the first and the last request -- all layers, all ranks
     ncores = len(os.sched_getaffinity(0))
     reqs = list(range(len(cfg.n_tokens))) if sb <= (3 << 30) else sorted({0, len(cfg.n_tokens) - 1})
     ss = [sample_of(SP[p], P[p][0], pt, reqs, (0, cfg.L)) for p in range(cfg.tp_p)]
