@@ -415,6 +415,8 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
     const kv_layout* L = src[i];
     a.src_of_p[L->d.tp_rank] = (int8_t)i;
     const int64_t* st = L->stride;
+    a.src[i] = static_cast<const uint8_t*>(src_pools[i]);
+    for (int ax = 0; ax < 6; ++ax) a.ss[i][ax] = st[ax];
     cuuint64_t dims[5] = {(cuuint64_t)Dm, (cuuint64_t)(head_major ? Bp : Hp), (cuuint64_t)(head_major ? Hp : Bp),
                           (cuuint64_t)L->d.num_blocks, (cuuint64_t)L->d.num_layers};
     cuuint64_t strides[4] = {(cuuint64_t)((head_major ? st[KV_AX_SLOT] : st[KV_AX_HEAD]) * esize),

@@ -120,6 +120,11 @@ struct TileArgs {
   int32_t d_esize;
   const float* sscale[KVX_MAX_RANKS];
   const float* dscale[KVX_MAX_RANKS];
+  // partial sub-tiles (the request's last block, slots >= T present): the valid rows are
+  // loaded with plain 16-B loads from here instead of the TMA box, which would also read the
+  // tail slots (SPEC S:274 -- never read beyond T_r)
+  const uint8_t* src[KVX_MAX_RANKS];
+  int64_t ss[KVX_MAX_RANKS][6];          // source element strides per source index
 };
 cudaError_t launch_tile_cast(const TileArgs& a, int sdt, int ddt, cudaStream_t s);
 

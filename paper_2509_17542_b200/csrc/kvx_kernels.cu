@@ -855,8 +855,8 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // so the sub-tile lands in smem already permuted; tail slots are zeroed in smem; then the
 // lanes issue cp.async.bulk stores of D's contiguous runs (one run when the sub-tile is a
 // whole dst head range).  No register pass, 8-64 KB per TMA operation, `stages` items in
-// flight per CTA.  Source tail slots of the last block are read (inside the pool) but zeroed
-// before they are written.
+// flight per CTA.  A partial sub-tile (the request's last block) takes its valid rows by
+// plain loads instead (tile_rows_ldg): no source tail slot is read; D's tail rows are zeroed.
 // ------------------------------------------------------------------------------------
 __device__ __forceinline__ void tma_load_5d(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1,
                                             int32_t c2, int32_t c3, int32_t c4, uint64_t* bar) {
@@ -865,6 +865,29 @@ __device__ __forceinline__ void tma_load_5d(void* smem_dst, const CUtensorMap* m
           "r"(smem_u32(smem_dst)),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
       : "memory");
+}
+
+// The valid rows (slots < valid) of a partial source sub-tile -- the request's last block --
+// by plain 16-B loads of the whole warp into the stage, in the box's order ([nh][Bp][D]
+// when head_major, else [Bp][nh][D]).  The TMA box would read all Bp slots: the tail slots
+// are never read (reading 5).  Rare (one per request, layer, K/V and head group).
+__device__ __forceinline__ void tile_rows_ldg(const TileArgs& a, uint8_t* sbuf, int si, int32_t c, int32_t sblk,
+                                              int32_t sl, int32_t hp0, uint32_t valid, uint32_t lane) {
+  const int64_t* st = a.ss[si];
+  const uint32_t esize = (uint32_t)a.esize, nh = (uint32_t)a.nh, Bp = (uint32_t)a.Bp;
+  const uint32_t row_bytes = (uint32_t)a.D * esize, r16 = row_bytes / 16u;
+  const uint8_t* base = a.src[si] + (sl * st[KV_AX_LAYER] + (int64_t)c * st[KV_AX_KV] + (int64_t)sblk * st[KV_AX_BLOCK] +
+                                     (int64_t)hp0 * st[KV_AX_HEAD]) * esize;
+  for (uint32_t z = lane; z < valid * nh * r16; z += 32u) {
+    const uint32_t row = z / r16, piece = z - row * r16;
+    const uint32_t slot = row / nh, head = row - slot * nh;
+    const uint32_t ri = a.head_major ? head * Bp + slot : slot * nh + head;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(
+        base + ((int64_t)slot * st[KV_AX_SLOT] + (int64_t)head * st[KV_AX_HEAD]) * esize + piece * 16u));
+    *reinterpret_cast<uint4*>(sbuf + (size_t)ri * row_bytes + piece * 16u) = v;
+  }
+  fence_proxy_async();  // generic writes ordered before later async-proxy use of the stage
+  __syncwarp();
 }
 
 __global__ void __launch_bounds__(32) k_tile_copy(const __grid_constant__ TileArgs a) {
@@ -948,9 +971,12 @@ __global__ void __launch_bounds__(32) k_tile_copy(const __grid_constant__ TileAr
     int32_t c0, c1, c2, c3, c4;
     uint32_t c;
     decode(blockIdx.x + k * gridDim.x, it[s], si, c0, c1, c2, c3, c4, c);
+    const uint32_t v = it[s].valid;
+    if (v > 0u && v < (uint32_t)a.Bp)  // partial: valid rows only, then a plain arrive
+      tile_rows_ldg(a, smem + (size_t)s * SB, si, (int32_t)c, c3, c4, a.head_major ? c2 : c1, v, lane);
     if (lane == 0) {
-      mbar_expect_tx_arrive(bars + s, it[s].valid ? SB : 0u);
-      if (it[s].valid) tma_load_5d(smem + (size_t)s * SB, &a.maps[si][c], c0, c1, c2, c3, c4, bars + s);
+      mbar_expect_tx_arrive(bars + s, v == (uint32_t)a.Bp ? SB : 0u);
+      if (v == (uint32_t)a.Bp) tma_load_5d(smem + (size_t)s * SB, &a.maps[si][c], c0, c1, c2, c3, c4, bars + s);
     }
   };
   for (uint32_t k = 0; k < my && k < S; ++k) issue(k, k);
@@ -1718,7 +1744,8 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
 // warps that convert them row by row (16-B LDS, the cast, 8- or 16-B stores of D's rows)
 // instead of bulk-storing them unchanged.  Warp 0 is the producer (decode + TMA issue into a
 // ring of stages with full / empty mbarriers); kTbConsumers warps consume.  Rows of slots
-// >= T are written as zeros.  The HBM side sees one TMA read per sub-tile (8 KB for a c4
+// >= T are written as zeros; a partial sub-tile's valid rows come by plain loads
+// (tile_rows_ldg), so no source tail slot is read.  The HBM side sees one TMA read per sub-tile (8 KB for a c4
 // pair: 2 heads x 16 slots x 128 bf16).
 // ------------------------------------------------------------------------------------
 struct TcMeta {
@@ -1841,9 +1868,11 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_tile_cast(const __g
           meta[st].valid = valid;
         }
         __syncwarp();
+        if (valid > 0u && valid < Bp)  // partial sub-tile: valid rows only (tile_rows_ldg)
+          tile_rows_ldg(a, tc_smem + (size_t)st * SBY, si, c, sblk, sl, a.head_major ? h2 : h1, valid, lane);
         if (lane == 0) {
-          mbar_expect_tx_arrive(full + st, valid ? SBY : 0u);
-          if (valid) tma_load_5d(tc_smem + (size_t)st * SBY, &a.maps[si][c], 0, h1, h2, sblk, sl, full + st);
+          mbar_expect_tx_arrive(full + st, valid == Bp ? SBY : 0u);
+          if (valid == Bp) tma_load_5d(tc_smem + (size_t)st * SBY, &a.maps[si][c], 0, h1, h2, sblk, sl, full + st);
         }
       }
     }
