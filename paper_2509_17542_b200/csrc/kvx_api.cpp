@@ -760,18 +760,16 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
   const uint64_t per_layer_units = vec == 8 ? per_layer / ndch : per_layer;
   int32_t step = (int32_t)std::max<uint64_t>(1, kMaxChunks / std::max<uint64_t>(per_layer_units, 1));
   if (per_layer_units > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_convert_reshard: one layer exceeds 2^31 chunks");
-  // fp8 -> other fp8 (e4m3fnuz <-> e4m3fn): code tables in shared memory (k_requant_rows),
-  // layer sub-ranges sized so a launch's tables fit.  Measured on the c4-pair shape
-  // (profiles/r02/requant_lut.txt): e4m3fn -> e4m3fnuz 0.706 vs 0.687 of copy for the
-  // arithmetic row kernel (used by default, KVX_LUT=1), e4m3fnuz -> e4m3fn 0.707 vs 0.842
-  // (the arithmetic kernel stays; KVX_LUT=2 forces tables both ways, 0 never): the table
-  // lookups are shared-memory-bound (2.1 wavefronts per LDS.U8 from bank conflicts on random
-  // codes, 16 warps per SM with 80-KB tables)
+  // fp8 -> other fp8 (e4m3fnuz <-> e4m3fn): 128-B magnitude code tables in shared memory
+  // (k_requant_rows), layer sub-ranges sized so a launch's tables stay bounded.  Measured on
+  // the c4-pair shape (profiles/r02/requant_lut.txt): e4m3fn -> e4m3fnuz 0.909 of copy vs
+  // 0.686 for the arithmetic row kernel, e4m3fnuz -> e4m3fn 0.872 vs 0.841 -- tables both ways
+  // by default (KVX_LUT=1 or 2); KVX_LUT=0 forces the arithmetic row kernel
   {
     const char* lut_env = getenv("KVX_LUT");
     const int lut_mode = lut_env ? atoi(lut_env) : 1;
     const bool dual = fp8(S->d.dtype) && fp8(D->d.dtype) && S->d.dtype != D->d.dtype;
-    const bool want = lut_mode == 2 || (lut_mode == 1 && S->d.dtype == KV_F8E4M3);
+    const bool want = lut_mode != 0;
     const uint32_t tab_per_layer = (uint32_t)n_dst * (a.kv1 ? 1u : 2u) * (uint32_t)a.Hd_eff;
     if (vec == 8 && !a.split && dual && !nt && want && tab_per_layer <= kRequantMaxTables && S->d.head_dim >= 16) {
       const int32_t lstep = std::min<int32_t>(step, (int32_t)(kRequantMaxTables / tab_per_layer));

@@ -91,6 +91,9 @@ struct ConvArgs {
   uint32_t* req_flag;
   uint64_t* req_ns;
   uint32_t req_epoch, items_per_block;
+  // k_requant_rows: items per CTA (contiguous, layer-outermost order) and the most layers
+  // one CTA's range spans (its tables: that many layers' worth)
+  uint32_t rq_per_cta, rq_layers;
 };
 
 // TMA tile path (same dtype): one cp.async.bulk.tensor load per (dst block, layer, K/V,
@@ -248,7 +251,7 @@ kv_status compute_scales_impl(int32_t n_src, const kv_layout* const* src, const 
                               kv_stream stream, bool share, float* peer);
 cudaError_t launch_convert(const ConvArgs& a, int vec, int sdt, int ddt, cudaStream_t s);
 // fp8 -> other fp8 through per-(dst rank, layer, K/V, head) code tables in shared memory
-// (k_requant_rows); the launch's tables must fit kRequantMaxTables x 256 B
+// (k_requant_rows); the launch's tables must fit kRequantMaxTables x 128 B
 constexpr uint32_t kRequantMaxTables = 384;
 cudaError_t launch_requant(const ConvArgs& a, int sdt, int ddt, cudaStream_t s);
 // per-request completion words (kv_convert_reshard_notify): before the row kernel, zero the

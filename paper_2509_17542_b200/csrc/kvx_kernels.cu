@@ -740,7 +740,7 @@ __device__ __forceinline__ void conv_row(const ConvArgs& a, uint32_t item, uint3
   const uint32_t slot = (s_blk << ts_log2) + ls;
   const uint32_t hl = (sbk << (5u - ts_log2)) + lh;  // head within the converted range
   // (dst index, layer, K/V, head) table of the LUT requantisation (k_requant_rows)
-  if (tbl_out) *tbl_out = ((qi * (uint32_t)a.Lc + l) * (a.kv1 ? 1u : 2u) + (a.kv1 ? 0u : c)) * (uint32_t)a.Hd_eff + hl;
+  if (tbl_out) *tbl_out = ((l * a.f_nd.d + qi) * (a.kv1 ? 1u : 2u) + (a.kv1 ? 0u : c)) * (uint32_t)a.Hd_eff + hl;
   const uint32_t hq = (uint32_t)a.hq_off[qi] + hl;      // D-local head
   sp = 0;
   dp = 0;
@@ -1920,29 +1920,62 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_tile_cast(const __g
 // ------------------------------------------------------------------------------------
 // fp8 -> other fp8 requantisation through code tables (k_requant_rows; e4m3fnuz <-> e4m3fn
 // with static scales, readings 24-26).  With both scales fixed per (layer, K/V, head) the
-// cast is a pure function of the 8-bit code, so each CTA first builds the 256-entry tables
-// of every (dst rank, layer, K/V, head) of the launch in shared memory -- each entry by the
-// exact per-code path (fp8x4_to_f32, the two multiplies, the packed conversion), so the
-// tables are bit-identical to the arithmetic kernels -- and the row loop then maps each code
-// with one byte permute (code into the table base) and one LDS.U8.
+// cast is a pure function of the 8-bit code.  Both formats are sign-magnitude and every step
+// of the cast (decode, the two round-to-nearest multiplies, the satfinite encode) is odd, so
+// the table holds only the 128 MAGNITUDE codes -- each entry by the exact per-code path
+// (cast_chunk), bit-identical to the arithmetic kernels -- and the sign is put back per byte
+// with the two formats' special codes fixed up in SIMD-within-a-register:
+//   e4m3fn -> fnuz: NaN (0x7F | s) -> 0x80 (entry 0x7F already is 0x80); a zero result is
+//                   +0 whatever the sign (fnuz has no -0: 0x80 is its NaN);
+//   fnuz -> e4m3fn: 0x80 (NaN) -> 0x7F; everything else magnitude | sign.
+// A 128-B table spans the 32 shared-memory banks exactly once, so a warp's 32 lookups into
+// ONE table never conflict; the item's rows are laid out slot-fastest over the lanes
+// (vlane) so the rows of one warp instruction (32 / 16-B chunks per row of them) share
+// their head, hence their table.  Per code: one byte permute (code into the table address),
+// one LDS.U8; per 4 codes: 3 permutes to reassemble and 4-6 integer ops of fix-up,
+// branch-free (a fix-up only in chunks holding a fnuz NaN measured slower: 0.852 vs 0.870).
 // ------------------------------------------------------------------------------------
-constexpr uint32_t kLutMaxTables = 384;  // 96 KB of tables per CTA
+template <int SDT, int DDT>
+__device__ __forceinline__ uint32_t requant_sign4(uint32_t w, uint32_t r) {
+  const uint32_t s4 = w & 0x80808080u;
+  if constexpr (DDT == KV_F8E4M3FNUZ) {
+    // bit 7 of each byte: r != 0 (0x80, the NaN entry, counts as nonzero)
+    const uint32_t nz = (((r & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | r) & 0x80808080u;
+    return r | (s4 & nz);
+  } else {
+    // bit 7 of each byte: magnitude bits of the code nonzero; sign without them = fnuz NaN
+    const uint32_t nzm = ((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & 0x80808080u;
+    return (r | s4) - ((s4 & ~nzm) >> 7);   // 0x80 - 1 = 0x7F in the NaN bytes (no borrows)
+  }
+}
 
-template <int SDT, int DDT, int U>
-__global__ void __launch_bounds__(kThreads, 2) k_requant_rows(const __grid_constant__ ConvArgs a) {
+template <int SDT, int DDT, int U, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB) k_requant_rows(const __grid_constant__ ConvArgs a) {
   static_assert(dual_scale(SDT, DDT), "k_requant_rows: fp8 -> other fp8");
-  extern __shared__ __align__(256) uint8_t lut[];
+  extern __shared__ __align__(256) uint8_t lut_raw[];
+  // table t at byte t * 128 of a 256-B aligned region: table pair base | (t & 1) << 7 | code
+  uint8_t* lut = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(lut_raw) + 255) & ~uintptr_t(255));
   const uint32_t kv = a.kv1 ? 1u : 2u;
-  const uint32_t n_tab = a.f_nd.d * (uint32_t)a.Lc * kv * (uint32_t)a.Hd_eff;
-  // ---- tables: entry (t, code) ----
-  for (uint32_t e = threadIdx.x; e < n_tab * 256u; e += blockDim.x) {
-    const uint32_t code = e & 255u;
-    uint32_t t = e >> 8;
+  // this CTA's items: a contiguous range of the layer-outermost order m (item n of conv_row
+  // = the same (dst block, layer, K/V, sub-tile, dst rank) with the block outermost), so it
+  // needs the tables of a few layers only, not of the launch's Lc
+  const uint32_t inner = kv * a.f_items.d * a.f_nd.d;       // items per (layer, dst block)
+  const uint32_t nbl = a.f_bl.d, per_layer = nbl * inner;
+  const uint32_t m0 = blockIdx.x * a.rq_per_cta;
+  const uint32_t m1 = min(a.n_items, m0 + a.rq_per_cta);
+  if (m0 >= m1) return;
+  const uint32_t l_lo = m0 / per_layer, l_hi = (m1 - 1u) / per_layer;
+  const uint32_t tpl = a.f_nd.d * kv * (uint32_t)a.Hd_eff;  // tables per layer
+  const uint32_t n_tab = (l_hi - l_lo + 1u) * tpl;
+  // ---- tables: entry (t, magnitude code m), t = ((l - l_lo) * nd + qi) * kv + c) * Hd_eff + hl ----
+  for (uint32_t e = threadIdx.x; e < n_tab * 128u; e += blockDim.x) {
+    const uint32_t code = e & 127u;
+    uint32_t t = e >> 7;
     const uint32_t hl = t % (uint32_t)a.Hd_eff;
     t /= (uint32_t)a.Hd_eff;
     const uint32_t c = a.kv1 ? (uint32_t)a.c0 : (t % 2u);
     if (!a.kv1) t /= 2u;
-    const uint32_t l = t % (uint32_t)a.Lc, qi = t / (uint32_t)a.Lc;
+    const uint32_t qi = t % a.f_nd.d, l = l_lo + t / a.f_nd.d;
     const uint32_t hq = (uint32_t)a.hq_off[qi] + hl;
     const int64_t layer = a.lb + (int64_t)l;
     const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;
@@ -1960,17 +1993,21 @@ __global__ void __launch_bounds__(kThreads, 2) k_requant_rows(const __grid_const
   }
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
   const uint32_t cs = (uint32_t)a.cpr_shift;  // log2(16-byte chunks per row)
   const uint32_t cmask = (1u << cs) - 1u, nch = 32u << cs;
-  const uint32_t lut0 = smem_u32(lut);
-  for (uint32_t item = warp; item < a.n_items; item += nwarps) {
+  const uint32_t lut0 = smem_u32(lut), tbl0 = l_lo * tpl;
+  // slot-fastest rows over the lanes whatever D's inner order (conv_row's row index)
+  const uint32_t tsl = (uint32_t)a.ts_log2;
+  const uint32_t vlane = a.slot_inner ? lane : (((lane & ((1u << tsl) - 1u)) << (5u - tsl)) | (lane >> tsl));
+  for (uint32_t m = m0 + (threadIdx.x >> 5); m < m1; m += kThreads / 32u) {
+    const uint32_t r0 = m % inner, q = m / inner;
+    const uint32_t l = q / nbl, bl = q - l * nbl;
+    const uint32_t item = (bl * (uint32_t)a.Lc + l) * inner + r0;
     uint64_t sp, dp;
     float rsc, rsc2;
     uint32_t rz, tbl = 0;
-    conv_row<SDT, DDT>(a, item, lane, sp, dp, rsc, rz, rsc2, nullptr, &tbl);
-    const uint32_t tbase = lut0 + (tbl << 8);
+    conv_row<SDT, DDT>(a, item, vlane, sp, dp, rsc, rz, rsc2, nullptr, &tbl);
+    const uint32_t tbase = lut0 + ((tbl - tbl0) << 7);   // byte 0: the table half bit (pairs 256-B aligned)
     for (uint32_t base = 0; base < nch; base += 32u * U) {
       uint4 in[U];
       uint64_t d[U];
@@ -1992,15 +2029,18 @@ __global__ void __launch_bounds__(kThreads, 2) k_requant_rows(const __grid_const
         uint4 o = make_uint4(0, 0, 0, 0);
         if (z[k] == 0) {
           uint32_t w[4] = {in[k].x, in[k].y, in[k].z, in[k].w}, r[4];
+          const uint32_t half4 = __byte_perm(tb[k], 0u, 0x0000u);  // the half bit in every byte
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
+            const uint32_t mi = (w[q] & 0x7F7F7F7Fu) | half4;   // magnitude codes | table half
             uint32_t b[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-              const uint32_t addr = __byte_perm(w[q], tb[k], 0x7650u + (uint32_t)j);  // code j | table base
+              const uint32_t addr = __byte_perm(mi, tb[k], 0x7650u + (uint32_t)j);  // code j | half into byte 0
               asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b[j]) : "r"(addr));
             }
-            r[q] = __byte_perm(__byte_perm(b[0], b[1], 0x0040u), __byte_perm(b[2], b[3], 0x0040u), 0x5410u);
+            const uint32_t m4 = __byte_perm(__byte_perm(b[0], b[1], 0x0040u), __byte_perm(b[2], b[3], 0x0040u), 0x5410u);
+            r[q] = requant_sign4<SDT, DDT>(w[q], m4);
           }
           o = make_uint4(r[0], r[1], r[2], r[3]);
         }
@@ -2723,29 +2763,36 @@ cudaError_t launch_requant(const ConvArgs& a0, int sdt, int ddt, cudaStream_t s)
   if (cpr < 2) return cudaErrorInvalidValue;
   a.cpr_shift = log2_pow2(cpr / 2);  // 16-byte chunks
   a.rows_per_tile = a.Bd * a.Hd_eff;
-  uint32_t ts, th;
-  subtile_shape((uint32_t)a.Bd, (uint32_t)a.Hd_eff, &ts, &th);
+  // sub-tiles as long along the slots as the block allows: the rows of one warp instruction
+  // (32 / 16-B chunks per row) are consecutive slots of one head -- one code table
+  uint32_t ts = 1;
+  while (ts < (uint32_t)a.Bd && ts < 32u) ts <<= 1;
+  const uint32_t th = 32u / ts;
   a.ts_log2 = log2_pow2(ts);
   const uint32_t nsb = ((uint32_t)a.Bd + ts - 1) / ts, nhb = ((uint32_t)a.Hd_eff + th - 1) / th;
   a.f_sb = make_fastdiv(nsb);
   a.f_items = make_fastdiv(nsb * nhb);
   a.n_items = (uint32_t)(a.total64 / ((uint64_t)a.rows_per_tile * cpr) * nsb * nhb);
-  const uint32_t n_tab = a.f_nd.d * (uint32_t)a.Lc * (a.kv1 ? 1u : 2u) * (uint32_t)a.Hd_eff;
-  const size_t smem = (size_t)n_tab * 256u;
-  auto launch = [&](auto k) -> cudaError_t {
+  const uint32_t tpl = a.f_nd.d * (a.kv1 ? 1u : 2u) * (uint32_t)a.Hd_eff;   // tables per layer
+  const uint32_t per_layer = a.n_items / (uint32_t)a.Lc;                     // items per layer
+  auto launch = [&](auto k, int minb) -> cudaError_t {
+    // one wave of CTAs, each a contiguous range of items (layer-outermost): the tables of
+    // the <= rq_layers layers the range touches
+    const uint64_t need = (a.n_items + (kThreads / 32) - 1) / (kThreads / 32);
+    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms() * minb));
+    a.rq_per_cta = (uint32_t)((a.n_items + (uint64_t)grid - 1) / (uint64_t)grid);
+    a.rq_layers = std::min<uint32_t>((uint32_t)a.Lc, (a.rq_per_cta + per_layer - 1) / per_layer + 1u);
+    const size_t smem = (size_t)a.rq_layers * tpl * 128u + 256u;   // 128-B tables, 256-B alignment slack
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreads, smem);
-    if (occ < 1) occ = 1;
-    const uint64_t need = (a.n_items + (kThreads / 32) - 1) / (kThreads / 32);
-    const int grid = (int)std::max<uint64_t>(1, std::min<uint64_t>(need, (uint64_t)num_sms() * occ));
     k<<<grid, kThreads, smem, s>>>(a);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cudaGetLastError();
   };
-  if (sdt == KV_F8E4M3FNUZ && ddt == KV_F8E4M3) return launch(k_requant_rows<KV_F8E4M3FNUZ, KV_F8E4M3, 8>);
-  if (sdt == KV_F8E4M3 && ddt == KV_F8E4M3FNUZ) return launch(k_requant_rows<KV_F8E4M3, KV_F8E4M3FNUZ, 8>);
+  // 4 loads in flight per lane x 4 CTAs/SM (64 registers): measured best of {8 x 2, 4 x 3,
+  // 4 x 4, 2 x 4, 4 x 5, 2 x 6, 4 x 6} on the c4-pair shape (profiles/r02/requant_lut.txt)
+  if (sdt == KV_F8E4M3FNUZ && ddt == KV_F8E4M3) return launch(k_requant_rows<KV_F8E4M3FNUZ, KV_F8E4M3, 4, 4>, 4);
+  if (sdt == KV_F8E4M3 && ddt == KV_F8E4M3FNUZ) return launch(k_requant_rows<KV_F8E4M3, KV_F8E4M3FNUZ, 4, 4>, 4);
   return cudaErrorInvalidValue;
 }
 
@@ -3039,8 +3086,8 @@ cudaError_t preload_kernels() {
   if ((e = preload_src<KV_F8E4M3FNUZ>()) != cudaSuccess) return e;
   if ((e = preload_src<KV_F32>()) != cudaSuccess) return e;
   KVX_TOUCH(k_tile_copy);
-  KVX_TOUCH((k_requant_rows<KV_F8E4M3FNUZ, KV_F8E4M3, 8>));
-  KVX_TOUCH((k_requant_rows<KV_F8E4M3, KV_F8E4M3FNUZ, 8>));
+  KVX_TOUCH((k_requant_rows<KV_F8E4M3FNUZ, KV_F8E4M3, 4, 4>));
+  KVX_TOUCH((k_requant_rows<KV_F8E4M3, KV_F8E4M3FNUZ, 4, 4>));
   KVX_TOUCH(k_amax_init);
   KVX_TOUCH(k_amax_finalize);
   KVX_TOUCH(k_signal);

@@ -659,13 +659,17 @@ def test_tile_copy_head_groups(o1, tp_p, tp_d):
         assert_pools_match(dc.dst_numpy(), expected(case, o1), BF16)
 
 
+@pytest.mark.parametrize("codes", ["random", "all"])
 @pytest.mark.parametrize("sdt,ddt", [(FNUZ, E4M3), (E4M3, FNUZ)])
 @pytest.mark.parametrize("tp,L", [((2, 4), 3), ((4, 2), 2), ((1, 1), 200)])
-def test_requant_tables(o1, monkeypatch, sdt, ddt, tp, L):
-    """fp8 -> other fp8 through shared-memory code tables (k_requant_rows): bit-identical to
+def test_requant_tables(o1, monkeypatch, sdt, ddt, tp, L, codes):
+    """fp8 -> other fp8 through shared-memory code tables (k_requant_rows: 128 magnitude
+    entries per table, the sign and the special codes restored per byte): bit-identical to
     the arithmetic row kernel (KVX_LUT=0) and to O1, random codes including the NaN codes of
-    both formats, random (non-power-of-two) scales on both sides, ragged requests, TP split /
-    merge, and a layer count whose tables exceed one launch (200 layers x 2 x 8 heads)."""
+    both formats (codes="all": every one of the 256 codes in every row region, both signs of
+    zero and of every underflow), random (non-power-of-two) scales on both sides, ragged
+    requests, TP split / merge, and a layer count whose tables exceed one launch (200 layers
+    x 2 x 8 heads)."""
     import paper_2509_17542_b200 as kvx
     case = make_case(L, 8, 64, tp[0], tp[1], 16, 16, [37, 0, 16, 1], sdt, ddt, seed=60 + L + tp[0],
                      o1=o1, scales="amax")
@@ -673,6 +677,9 @@ def test_requant_tables(o1, monkeypatch, sdt, ddt, tp, L):
     for lay in case["src_lays"]:
         lay["scales"] = np.exp(rng.uniform(np.log(0.01), np.log(100), size=(L, 2, 8 // tp[0]))).astype(np.float32)
     for p_ in case["src_pools"]:   # NaN codes too (synth avoids them): 0x7F / 0xFF in fn, 0x80 in fnuz
+        if codes == "all":         # 7 is odd: each 64-element row holds 64 distinct codes, all 256 cycle
+            p_.view(np.uint8)[:] = (np.arange(p_.size) * 7 % 256).astype(np.uint8)
+            continue
         p_[::97] = 0x80 if sdt == FNUZ else 0x7F
         p_[5::101] = 0xFF if sdt == E4M3 else 0x7F
     got = {}
