@@ -461,7 +461,7 @@ def run_single(args):
     if not args.no_verify:
         guarded("fullsize", lambda: k6_single(cfg, S, SP, src_bt, Dl, DP, dst_bt, step))
     if not args.no_e2e:
-        guarded("e2e", lambda: e2e_single(cfg, P, Dr, pt, dt_, S, SP, src_bt, Dl, DP, dst_bt, min(K, 3), stream, sb))
+        guarded("e2e", lambda: e2e_single(cfg, P, Dr, pt, dt_, S, SP, src_bt, Dl, DP, dst_bt, min(K, 5), stream, sb))
     if not args.no_cpu_baseline:
         guarded("cpu_baseline", lambda: single_cpu_baseline(cfg, args, wl_name, out))
     print(json.dumps(out), flush=True)
@@ -545,9 +545,10 @@ def e2e_single(cfg, P, Dr, pt, dt_, S, SP, src_bt, Dl, DP, dst_bt, K, stream, sb
     blocks of the P pools up from pinned memory and its D blocks back, inside the timed
     region -- only the blocks the block tables name (the pools' ~10% free blocks stay put):
     H2D into a device staging copy, scattered into the pools by block id, the convert, then
-    the D blocks gathered and read back.  The upload is split by the P pools' outer axes
-    (layer-major: layer chunks) on a copy stream, so chunk k+1 crosses PCIe while chunk k
-    converts."""
+    the D blocks gathered and read back.  Both directions are pipelined by layer chunk
+    where the pools' orders allow it (P layer-major: the upload; D block-then-layer: the
+    read-back): chunk k+1 crosses PCIe up while chunk k converts and chunk k-1 goes down,
+    each staging chunk guarded by its own events (no step-wide barriers)."""
     import torch
     import paper_2509_17542_b200 as kvx
     dev = SP[0].device
@@ -563,49 +564,77 @@ def e2e_single(cfg, P, Dr, pt, dt_, S, SP, src_bt, Dl, DP, dst_bt, K, stream, sb
         h.copy_(comp)
         hs.append(h)
         stage_p.append(comp)
-    stage_d = [v.index_select(1, d_ids) for v in dv]
-    hd = [_pinned_empty(x.numel() * 4).view(torch.int32).view(x.shape) for x in stage_d]
-    lay_major = cfg.p_order[0] == synth.LAYER and cfg.p_order[1] == synth.KV
-    n_ch = 8 if lay_major else 1
+    p_lay = cfg.p_order[0] == synth.LAYER and cfg.p_order[1] == synth.KV
+    d_lay = cfg.d_order[0] == synth.BLOCK and cfg.d_order[1] == synth.LAYER
+    n_ch = int(os.environ.get("KVX_E2E_CHUNKS", "8")) if (p_lay or d_lay) else 1
     bounds = [(i * cfg.L // n_ch, (i + 1) * cfg.L // n_ch) for i in range(n_ch)]
+    # D read-back chunks: [1, blocks, layer-chunk words] slices of the block view (D_ORDER:
+    # BLOCK then LAYER outermost), or one whole-step chunk
+    d_words = [v.shape[2] for v in dv]
+    d_cuts = [(l0 * w // cfg.L, l1 * w // cfg.L) for w in d_words for l0, l1 in bounds] if d_lay else None
+    stage_d, hd = [], []
+    for i, v in enumerate(dv):
+        parts = [(a, b) for a, b in (d_cuts[i * n_ch:(i + 1) * n_ch] if d_lay else [(0, d_words[i])])]
+        sd = [torch.empty((v.shape[0], len(d_ids), b - a), dtype=torch.int32, device=dev) for a, b in parts]
+        stage_d.append((parts, sd))
+        hd.append([_pinned_empty(x.numel() * 4).view(torch.int32).view(x.shape) for x in sd])
     up, down = torch.cuda.Stream(), torch.cuda.Stream()
+    ev = lambda: torch.cuda.Event()  # noqa: E731
+    ev_up, ev_scat = [ev() for _ in bounds], [ev() for _ in bounds]
+    nd = n_ch if d_lay else 1
+    ev_gath, ev_down = [ev() for _ in range(nd)], [ev() for _ in range(nd)]
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     up.wait_stream(stream)
     down.wait_stream(stream)
-    for _ in range(K):
-        up.wait_stream(stream)            # the previous step's scatters / converts are done
-        for l0, l1 in bounds:
-            r0, r1 = (2 * l0, 2 * l1) if lay_major else (0, pv[0].shape[0])
-            with torch.cuda.stream(up):
-                for st_, h in zip(stage_p, hs):
-                    st_[r0:r1].copy_(h[r0:r1], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(up)
-            stream.wait_event(ev)
-            stream.wait_stream(down)      # the previous read-back is done with the D pools
-            for v, st_ in zip(pv, stage_p):
-                v[r0:r1].index_copy_(1, p_ids, st_[r0:r1])
-            kvx.convert_reshard(S, SP, src_bt, Dl, DP, dst_bt, (l0, l1), stream)
-        for v, st_ in zip(dv, stage_d):
-            torch.index_select(v, 1, d_ids, out=st_)
-        down.wait_stream(stream)
+
+    def read_back(j, step):
+        if step:   # the previous step's D2H of staging chunk j has left it
+            stream.wait_event(ev_down[j])
+        for (parts, sd), v in zip(stage_d, dv):
+            a, b = parts[j]
+            torch.index_select(v[:, :, a:b], 1, d_ids, out=sd[j])
+        ev_gath[j].record(stream)
+        down.wait_event(ev_gath[j])
         with torch.cuda.stream(down):
-            for st_, h in zip(stage_d, hd):
-                h.copy_(st_, non_blocking=True)
+            for (_, sd), h in zip(stage_d, hd):
+                h[j].copy_(sd[j], non_blocking=True)
+        ev_down[j].record(down)
+
+    for step in range(K):
+        for c, (l0, l1) in enumerate(bounds):
+            r0, r1 = (2 * l0, 2 * l1) if p_lay else (0, pv[0].shape[0])
+            if p_lay or c == 0:
+                if step:   # the previous step's scatter of this staging chunk is done
+                    up.wait_event(ev_scat[c])
+                with torch.cuda.stream(up):
+                    for st_, h in zip(stage_p, hs):
+                        st_[r0:r1].copy_(h[r0:r1], non_blocking=True)
+                ev_up[c].record(up)
+                stream.wait_event(ev_up[c])
+                for v, st_ in zip(pv, stage_p):
+                    v[r0:r1].index_copy_(1, p_ids, st_[r0:r1])
+                ev_scat[c].record(stream)
+            kvx.convert_reshard(S, SP, src_bt, Dl, DP, dst_bt, (l0, l1), stream)
+            if d_lay:
+                read_back(c, step)
+        if not d_lay:
+            read_back(0, step)
     stream.wait_stream(down)
     stream.wait_stream(up)
     t1.record(stream)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / K
-    h2d, d2h = int(sum(h.numel() * 4 for h in hs)), int(sum(h.numel() * 4 for h in hd))
+    h2d = int(sum(h.numel() * 4 for h in hs))
+    d2h = int(sum(x.numel() * 4 for hl in hd for x in hl))
     del hs, hd, stage_p, stage_d
     _unpin_all()
     return {"value": round(sb / (ms * 1e-3) / 1e9, 3), "unit": "GB/s", "ms_per_step": round(ms, 3),
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "steps": K, "pipelined": f"{len(bounds)} layer chunks uploaded ahead of their convert; only the batch's "
-                                     "blocks cross PCIe (device staging + block scatter / gather)"}
+            "steps": K, "pipelined": f"{len(bounds)} layer chunks: upload, convert and read-back overlapped "
+                                     "chunk by chunk; only the batch's blocks cross PCIe (device staging + "
+                                     "block scatter / gather)"}
 
 
 # ------------------------------------------------------------------------------------
@@ -761,16 +790,24 @@ def run_multi(args):
         counters = torch.zeros(kvx.pull_counter_words((0, cfg.L), lc), dtype=torch.int32, device=dev)
         seq = [0]
 
-        def step(ev=None):
+        def step(ev=None, pre=None):
+            """pre (e2e, narrowing pull, P side): (ranges, fn) -- stage the layer ranges one
+            after the other (same chunk numbering as one call), fn(l0, l1) enqueued before each
+            (its host upload), so the upload of range k+1 overlaps the transfer of range k."""
             epoch[0] += 1
             if ev is not None and me.kind == "D":
                 ev[0].record(stream)
             if me.kind == "P":
                 if narrowing:
-                    kvx.stage(S, mine["pool"], mine["bt"], [peer_lays[q] for q in my_q], ring_ptrs, R, slot_bytes,
-                              [pch.peer_flag[q] for q in my_q], [pflags[q:q + 1] for q in my_q], seq[0], err,
-                              (0, cfg.L), lc, 30.0, stream,
-                              peer_scales=[pch.peer_scales[q] for q in my_q] if dyn else None)
+                    s0 = seq[0]
+                    for l0, l1 in (pre[0] if pre else [(0, cfg.L)]):
+                        if pre:
+                            pre[1](l0, l1)
+                        kvx.stage(S, mine["pool"], mine["bt"], [peer_lays[q] for q in my_q], ring_ptrs, R,
+                                  slot_bytes, [pch.peer_flag[q] for q in my_q], [pflags[q:q + 1] for q in my_q], s0,
+                                  err, (l0, l1), lc, 30.0, stream,
+                                  peer_scales=[pch.peer_scales[q] for q in my_q] if dyn else None)
+                        s0 += kvx.chunk_count((l0, l1), lc)
                 else:
                     for q in my_q:   # my KV is resident: D may read it; then wait until it has
                         kvx.signal(pch.peer_flag[q], epoch[0], stream)
@@ -789,6 +826,7 @@ def run_multi(args):
             seq[0] += nchunks
             if ev is not None and me.kind == "D":
                 ev[1].record(stream)
+        step.chunked_upload = (narrowing, lc)
     else:
         # NCCL baseline: pack -> ncclSend / ncclRecv -> unpack, per-layer double-buffered
         uid = [kvx.Comm.unique_id() if rank == 0 else None]
@@ -918,7 +956,7 @@ def run_multi(args):
             raise SystemExit(f"rank {rank}: flag wait timed out (K6 step)")
     e2e = None
     if not args.no_e2e and args.mode in ("push", "pull"):
-        e2e = e2e_multi(mine, me, step, stream, barrier, err, min(K, 3), rank)
+        e2e = e2e_multi(mine, me, step, stream, barrier, err, min(K, 5), rank, cfg.L)
     allx = tr.exchange({"stats": stats, "parity": parity, "e2e": e2e, "fullsize": fullsize, "ctrl": ctrl_info})
     if rank == 0:
         sts = [x["stats"] for x in allx]
@@ -991,10 +1029,14 @@ def run_multi(args):
     dist.destroy_process_group()
 
 
-def e2e_multi(mine, me, step, stream, barrier, err, ke, rank):
+def e2e_multi(mine, me, step, stream, barrier, err, ke, rank, L=None):
     """Same metric through the public API with host buffers: every step the P rank uploads its
     batch's blocks from pinned memory (staging + scatter by block id) before the transfer, the
-    D rank gathers its batch's blocks and reads them back -- only the blocks the tables name."""
+    D rank gathers its batch's blocks and reads them back -- only the blocks the tables name.
+    Narrowing pull (the default c4 path): the P rank uploads layer range by layer range on a
+    copy stream and stages each range as soon as it is resident (kv_stage per range, one
+    chunk numbering), so PCIe and NVLink overlap; the D rank gathers on its transfer stream
+    and reads back on a side stream, so its next pull does not wait for PCIe."""
     import torch
     host = stage = view = ids = None
     if me.kind in ("P", "D"):
@@ -1005,19 +1047,63 @@ def e2e_multi(mine, me, step, stream, barrier, err, ke, rank):
         host = _pinned_empty(stage.numel() * 4).view(torch.int32).view(stage.shape)
         if me.kind == "P":
             host.copy_(stage)
+    narrowing, lc = getattr(step, "chunked_upload", (False, 0))
+    pre = None
+    if me.kind == "P" and narrowing and L and tuple(mine["d"]["order"][:2]) == (synth.LAYER, synth.KV):
+        nck = -(-L // lc)
+        per = max(1, -(-nck // 8)) * lc          # ~8 upload ranges, each whole chunks
+        ranges = [(l0, min(L, l0 + per)) for l0 in range(0, L, per)]
+        up = torch.cuda.Stream()
+        ev_up = [torch.cuda.Event() for _ in ranges]
+        ev_sc = [torch.cuda.Event() for _ in ranges]
+        first = [True]
+        idx = {r: i for i, r in enumerate(ranges)}
+
+        def upload(l0, l1):
+            i = idx[(l0, l1)]
+            if not first[0]:
+                up.wait_event(ev_sc[i])       # the previous step's scatter of this range is done
+            with torch.cuda.stream(up):
+                stage[2 * l0:2 * l1].copy_(host[2 * l0:2 * l1], non_blocking=True)
+            ev_up[i].record(up)
+            stream.wait_event(ev_up[i])
+            view[2 * l0:2 * l1].index_copy_(1, ids, stage[2 * l0:2 * l1])
+            ev_sc[i].record(stream)
+            if i == len(ranges) - 1:
+                first[0] = False
+        pre = (ranges, upload)
+    down, ev_d = torch.cuda.Stream(), None
     torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    down.wait_stream(stream)
     for _ in range(ke):
-        if me.kind == "P":
+        if me.kind == "P" and pre is None:
             stage.copy_(host, non_blocking=True)
             view.index_copy_(1, ids, stage)
-        step()
+        if pre is not None:
+            step(pre=pre)
+        else:
+            step()
         if me.kind == "D":
+            # gather on the transfer stream (the next step overwrites the pool), read back on a
+            # side stream so the next step's pull does not wait for PCIe
+            if ev_d is not None:
+                stream.wait_event(ev_d)      # the previous read-back has left the staging buffer
             torch.index_select(view, 1, ids, out=stage)
-            host.copy_(stage, non_blocking=True)
+            ev_g = torch.cuda.Event()
+            ev_g.record(stream)
+            down.wait_event(ev_g)
+            with torch.cuda.stream(down):
+                host.copy_(stage, non_blocking=True)
+            ev_d = torch.cuda.Event()
+            ev_d.record(down)
+    if pre is not None:
+        stream.wait_stream(up)
+    if me.kind == "D":
+        stream.wait_stream(down)
     e1.record(stream)
     torch.cuda.synchronize()
     if int(err.item()):
@@ -1026,7 +1112,7 @@ def e2e_multi(mine, me, step, stream, barrier, err, ke, rank):
     del host, stage
     _unpin_all()
     return {"ms": e0.elapsed_time(e1), "steps": ke, "h2d": n if me.kind == "P" else 0,
-            "d2h": n if me.kind == "D" else 0}
+            "d2h": n if me.kind == "D" else 0, "pipelined": pre is not None}
 
 
 def run_reference(args):
