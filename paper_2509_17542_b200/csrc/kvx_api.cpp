@@ -678,6 +678,8 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
             use_tb = false;
         }
         tb.mode = st == 1 ? 1 : 2;
+        const char* tl_env = getenv("KVX_TB_LUT");
+        tb.lut = tl_env ? atoi(tl_env) : 1;
         tb.tile_rows = Dm * S->elem_bytes / 8;
         // tiles in flight per CTA: 64 KB for 2-byte sources (c4-pair V pool bf16 -> e4m3: 0.90 at
         // 32 KB, 0.97 at 64 KB), 32 KB for 1-byte ones (the 2-KB tiles want more CTAs, hence

@@ -1522,6 +1522,22 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
 // ------------------------------------------------------------------------------------
 // kTbConsumers: kvx_internal.h
 
+// Sign / special-code restore of the fp8 -> other fp8 code tables (k_requant_rows,
+// k_convert_tb): r holds the looked-up results of the four codes' magnitudes (w & 0x7F).
+template <int SDT, int DDT>
+__device__ __forceinline__ uint32_t requant_sign4(uint32_t w, uint32_t r) {
+  const uint32_t s4 = w & 0x80808080u;
+  if constexpr (DDT == KV_F8E4M3FNUZ) {
+    // bit 7 of each byte: r != 0 (0x80, the NaN entry, counts as nonzero)
+    const uint32_t nz = (((r & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | r) & 0x80808080u;
+    return r | (s4 & nz);
+  } else {
+    // bit 7 of each byte: magnitude bits of the code nonzero; sign without them = fnuz NaN
+    const uint32_t nzm = ((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & 0x80808080u;
+    return (r | s4) - ((s4 & ~nzm) >> 7);   // 0x80 - 1 = 0x7F in the NaN bytes (no borrows)
+  }
+}
+
 struct TbMeta {
   uint8_t* db;
   uint32_t valid;
@@ -1597,6 +1613,8 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
   uint64_t* full = reinterpret_cast<uint64_t*>(stages + (size_t)S * tile_bytes);
   uint64_t* empty = full + S;
   TbMeta* meta = reinterpret_cast<TbMeta*>(empty + S);
+  // fp8 -> other fp8: one 256-B aligned code-table slot per consumer warp after the metadata
+  const uint32_t tab0 = (smem_u32(meta + S) + 255u) & ~255u;
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   if (threadIdx.x == 0) {
     for (uint32_t i = 0; i < S; ++i) {
@@ -1705,6 +1723,20 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
       if (lane == 0) mbar_arrive(empty + st);
       continue;
     }
+    // fp8 -> other fp8: this item's 128-entry magnitude code table (k_requant_rows' scheme),
+    // built by the warp from the exact arithmetic cast -- 4 codes per lane, one cast_chunk --
+    // then one byte permute + one LDS.U8 per code instead of the arithmetic cast
+    constexpr bool LUT_OK = dual_scale(SDT, DDT);
+    const bool LUT = LUT_OK && A.lut;
+    const uint32_t tab = tab0 + cw * 256u;
+    if (LUT) {
+      Chunk<SDT, 4> ci;
+      Chunk<DDT, 4> co;
+      ci.w[0] = 0x03020100u + lane * 0x04040404u;   // codes 4 lane .. 4 lane + 3
+      cast_chunk<SDT, DDT, 4, FOLD>(ci, co, m.rsc, m.s2);
+      asm volatile("st.shared.u32 [%0], %1;" ::"r"(tab + lane * 4u), "r"(co.w[0]) : "memory");
+      __syncwarp();
+    }
     for (uint32_t u = lane; u < nsub; u += 32u) {
       const uint32_t s_sub = u & 1u, d_sub = u >> 1;
       const uint32_t s0 = s_sub << 3, d0 = d_sub << 3;
@@ -1722,11 +1754,33 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
           const uint32_t R = off >> 7, c = (off >> 4) & 7u;
           lds_chunk8<SDT>(x[k], tile + R * 128u + ((c ^ (R & 7u)) << 4) + (off & 15u));
         }
-        transpose8<SDT>(x, y);
+        if (LUT) {
+          // look the codes up (element-wise, so before the byte transpose), then transpose
+          Chunk<DDT, 8> xo[8];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          cast_chunk<SDT, DDT, 8, FOLD>(y[k], o[k], m.rsc, m.s2);
-          if (s0 + (uint32_t)k >= m.valid) zero_chunk(o[k]);
+          for (int k = 0; k < 8; ++k)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const uint32_t w = x[k].w[q], mi = w & 0x7F7F7F7Fu;
+              uint32_t b[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b[j]) : "r"(__byte_perm(mi, tab, 0x7650u + (uint32_t)j)));
+              const uint32_t m4 =
+                  __byte_perm(__byte_perm(b[0], b[1], 0x0040u), __byte_perm(b[2], b[3], 0x0040u), 0x5410u);
+              xo[k].w[q] = requant_sign4<SDT, DDT>(w, m4);
+            }
+          transpose8<DDT>(xo, o);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            if (s0 + (uint32_t)k >= m.valid) zero_chunk(o[k]);
+        } else {
+          transpose8<SDT>(x, y);
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            cast_chunk<SDT, DDT, 8, FOLD>(y[k], o[k], m.rsc, m.s2);
+            if (s0 + (uint32_t)k >= m.valid) zero_chunk(o[k]);
+          }
         }
       }
       const int64_t doff = dim_off(d0, a.ds[KV_AX_DIM], a.d_dk);
@@ -1935,20 +1989,6 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_tile_cast(const __g
 // one LDS.U8; per 4 codes: 3 permutes to reassemble and 4-6 integer ops of fix-up,
 // branch-free (a fix-up only in chunks holding a fnuz NaN measured slower: 0.852 vs 0.870).
 // ------------------------------------------------------------------------------------
-template <int SDT, int DDT>
-__device__ __forceinline__ uint32_t requant_sign4(uint32_t w, uint32_t r) {
-  const uint32_t s4 = w & 0x80808080u;
-  if constexpr (DDT == KV_F8E4M3FNUZ) {
-    // bit 7 of each byte: r != 0 (0x80, the NaN entry, counts as nonzero)
-    const uint32_t nz = (((r & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | r) & 0x80808080u;
-    return r | (s4 & nz);
-  } else {
-    // bit 7 of each byte: magnitude bits of the code nonzero; sign without them = fnuz NaN
-    const uint32_t nzm = ((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & 0x80808080u;
-    return (r | s4) - ((s4 & ~nzm) >> 7);   // 0x80 - 1 = 0x7F in the NaN bytes (no borrows)
-  }
-}
-
 template <int SDT, int DDT, int U, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB) k_requant_rows(const __grid_constant__ ConvArgs a) {
   static_assert(dual_scale(SDT, DDT), "k_requant_rows: fp8 -> other fp8");
@@ -2718,7 +2758,8 @@ template <int SDT, int DDT>
 cudaError_t tb_t(const TbArgs& a, cudaStream_t s) {
   auto k = a.mode == 2 ? k_convert_tb<SDT, DDT, 2> : k_convert_tb<SDT, DDT, 1>;
   const size_t tile = (size_t)a.tile_rows * 128u;
-  const size_t smem = 1024 + (size_t)a.stages * tile + (size_t)a.stages * (16 + sizeof(TbMeta));
+  const size_t lut = dual_scale(SDT, DDT) ? 256u + 256u * kTbConsumers : 0u;   // per-warp code tables
+  const size_t smem = 1024 + (size_t)a.stages * tile + (size_t)a.stages * (16 + sizeof(TbMeta)) + lut;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int occ = 0;

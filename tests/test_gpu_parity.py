@@ -642,6 +642,34 @@ def test_tb_tiles(o1, monkeypatch, sdt, ddt, D, tp, n_tokens, split):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("sdt,ddt", [(FNUZ, E4M3), (E4M3, FNUZ)])
+@pytest.mark.parametrize("codes", ["random", "all"])
+def test_tb_requant_tables(o1, monkeypatch, sdt, ddt, codes):
+    """fp8 -> other fp8 from head_dim-major tiles: k_convert_tb's per-item 128-entry code
+    tables (built by the warp from the arithmetic cast) against k_convert_tr8's arithmetic
+    cast (KVX_TB=0) and O1 -- random non-power-of-two scales on both sides, NaN codes, and
+    (codes="all") every one of the 256 codes in every tile, ragged requests, TP split."""
+    import paper_2509_17542_b200 as kvx
+    case = make_case(3, 8, 128, 2, 4, 16, 16, [129, 16, 3, 0, 40], sdt, ddt, _VCOL, synth.D_ORDER, seed=77,
+                     o1=o1, scales="amax")
+    rng = np.random.default_rng(78)
+    for lay in case["src_lays"]:
+        lay["scales"] = np.exp(rng.uniform(np.log(0.01), np.log(100), size=(3, 2, 4))).astype(np.float32)
+    for p_ in case["src_pools"]:
+        if codes == "all":
+            p_.view(np.uint8)[:] = (np.arange(p_.size) * 7 % 256).astype(np.uint8)
+        else:
+            p_[::97] = 0x80 if sdt == FNUZ else 0x7F
+            p_[5::101] = 0xFF if sdt == E4M3 else 0x7F
+    got = {}
+    for tb in ("1", "0"):
+        monkeypatch.setenv("KVX_TB", tb)
+        _, got[tb], _ = run_case(o1, case)
+        assert kvx.last_kernel() == ("k_convert_tb" if tb == "1" else "k_convert_tr8")
+    for a, b in zip(got["1"], got["0"]):
+        assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("tp_p,tp_d", [(1, 1), (1, 2), (2, 1)])
 def test_tile_copy_head_groups(o1, tp_p, tp_d):
     """k_tile_copy with sub-tiles over 64 KB (32 heads x 16 slots x 256 B): split into
