@@ -1179,6 +1179,22 @@ __global__ void __launch_bounds__(kTrWarps * 32) k_convert_tr(const __grid_const
   }
 }
 
+// Sign / special-code restore of the fp8 -> other fp8 code tables (k_requant_rows,
+// k_convert_tb): r holds the looked-up results of the four codes' magnitudes (w & 0x7F).
+template <int SDT, int DDT>
+__device__ __forceinline__ uint32_t requant_sign4(uint32_t w, uint32_t r) {
+  const uint32_t s4 = w & 0x80808080u;
+  if constexpr (DDT == KV_F8E4M3FNUZ) {
+    // bit 7 of each byte: r != 0 (0x80, the NaN entry, counts as nonzero)
+    const uint32_t nz = (((r & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | r) & 0x80808080u;
+    return r | (s4 & nz);
+  } else {
+    // bit 7 of each byte: magnitude bits of the code nonzero; sign without them = fnuz NaN
+    const uint32_t nzm = ((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & 0x80808080u;
+    return (r | s4) - ((s4 & ~nzm) >> 7);   // 0x80 - 1 = 0x7F in the NaN bytes (no borrows)
+  }
+}
+
 // ------------------------------------------------------------------------------------
 // K1 with a head_dim-major or x-packed side, register path (k_convert_tr8): the same items
 // as k_convert_tr (dst rank, dst block, layer, K/V, dst head), but no shared memory.  An
@@ -1521,22 +1537,6 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
 // round trip per 32 tiles) and handed to the consumers through the stage's slot.
 // ------------------------------------------------------------------------------------
 // kTbConsumers: kvx_internal.h
-
-// Sign / special-code restore of the fp8 -> other fp8 code tables (k_requant_rows,
-// k_convert_tb): r holds the looked-up results of the four codes' magnitudes (w & 0x7F).
-template <int SDT, int DDT>
-__device__ __forceinline__ uint32_t requant_sign4(uint32_t w, uint32_t r) {
-  const uint32_t s4 = w & 0x80808080u;
-  if constexpr (DDT == KV_F8E4M3FNUZ) {
-    // bit 7 of each byte: r != 0 (0x80, the NaN entry, counts as nonzero)
-    const uint32_t nz = (((r & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | r) & 0x80808080u;
-    return r | (s4 & nz);
-  } else {
-    // bit 7 of each byte: magnitude bits of the code nonzero; sign without them = fnuz NaN
-    const uint32_t nzm = ((w & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) & 0x80808080u;
-    return (r | s4) - ((s4 & ~nzm) >> 7);   // 0x80 - 1 = 0x7F in the NaN bytes (no borrows)
-  }
-}
 
 struct TbMeta {
   uint8_t* db;

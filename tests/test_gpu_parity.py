@@ -644,14 +644,18 @@ def test_tb_tiles(o1, monkeypatch, sdt, ddt, D, tp, n_tokens, split):
 
 @pytest.mark.parametrize("sdt,ddt", [(FNUZ, E4M3), (E4M3, FNUZ)])
 @pytest.mark.parametrize("codes", ["random", "all"])
-def test_tb_requant_tables(o1, monkeypatch, sdt, ddt, codes):
-    """fp8 -> other fp8 from head_dim-major tiles: k_convert_tb's per-item 128-entry code
-    tables (built by the warp from the arithmetic cast) against k_convert_tr8's arithmetic
-    cast (KVX_TB=0) and O1 -- random non-power-of-two scales on both sides, NaN codes, and
-    (codes="all") every one of the 256 codes in every tile, ragged requests, TP split."""
+@pytest.mark.parametrize("form", ["col", "xpack"])
+def test_tb_requant_tables(o1, monkeypatch, sdt, ddt, codes, form):
+    """fp8 -> other fp8 from other vendors' tiles -- head_dim-major V (form="col":
+    k_convert_tb's per-item code tables vs its arithmetic cast, KVX_TB_LUT=0, and vs
+    k_convert_tr8, KVX_TB=0) and x-packed K with x = 16 codes (form="xpack": k_convert_tr8)
+    -- all identical and equal to O1: random non-power-of-two scales on both sides, NaN
+    codes, and (codes="all") every one of the 256 codes in every tile, ragged requests, TP
+    split."""
     import paper_2509_17542_b200 as kvx
-    case = make_case(3, 8, 128, 2, 4, 16, 16, [129, 16, 3, 0, 40], sdt, ddt, _VCOL, synth.D_ORDER, seed=77,
-                     o1=o1, scales="amax")
+    so, split = (_VCOL, 0) if form == "col" else ((LAYER, KV, BLOCK, HEAD, DIM, SLOT), 16)
+    case = make_case(3, 8, 128, 2, 4, 16, 16, [129, 16, 3, 0, 40], sdt, ddt, so, synth.D_ORDER, seed=77,
+                     o1=o1, scales="amax", p_split=split)
     rng = np.random.default_rng(78)
     for lay in case["src_lays"]:
         lay["scales"] = np.exp(rng.uniform(np.log(0.01), np.log(100), size=(3, 2, 4))).astype(np.float32)
@@ -662,12 +666,16 @@ def test_tb_requant_tables(o1, monkeypatch, sdt, ddt, codes):
             p_[::97] = 0x80 if sdt == FNUZ else 0x7F
             p_[5::101] = 0xFF if sdt == E4M3 else 0x7F
     got = {}
-    for tb in ("1", "0"):
+    runs = [("1", "1"), ("1", "0"), ("0", "1"), ("0", "0")]   # (KVX_TB, table paths on)
+    for tb, lut in runs:
         monkeypatch.setenv("KVX_TB", tb)
-        _, got[tb], _ = run_case(o1, case)
-        assert kvx.last_kernel() == ("k_convert_tb" if tb == "1" else "k_convert_tr8")
-    for a, b in zip(got["1"], got["0"]):
-        assert np.array_equal(a, b)
+        monkeypatch.setenv("KVX_TB_LUT", lut)
+        _, got[(tb, lut)], _ = run_case(o1, case)
+        want_k = "k_convert_tb" if tb == "1" and form == "col" else "k_convert_tr8"
+        assert kvx.last_kernel() == want_k
+    for r in runs[1:]:
+        for a, b in zip(got[runs[0]], got[r]):
+            assert np.array_equal(a, b), r
 
 
 @pytest.mark.parametrize("tp_p,tp_d", [(1, 1), (1, 2), (2, 1)])
