@@ -662,6 +662,20 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
         const bool xp16 = st == 2 && S->elem_bytes == 2 && (1 << S->dk) * S->elem_bytes == 16;
         use_tb = use_tr8 && (st == 1 || xp16) && dt == 0 && S->elem_bytes <= 2 && S->d.block_size == 16 &&
                  D->d.block_size == 16 && (Dm == 64 || Dm == 128 || Dm == 256) && enc && !(tb_env && atoi(tb_env) == 0);
+        // two heads per item (one TMA box) when a head's source AND destination tiles are
+        // <= 2 KB (fp8 -> fp8, or D = 64 2-byte) and the item's two heads sit next to each
+        // other in the source, belong to the same P rank and map to adjacent D heads: the
+        // per-item pipeline cost is then paid per 4 KB (c4-pair V pool, profiles/r02/tb_hpi_ab.txt:
+        // fnuz -> e4m3 0.657 -> 0.705, e4m3 -> fnuz 0.665 -> 0.755; e4m3 -> bf16, whose
+        // destination tile is 4 KB, 0.951 -> 0.901, so it stays at one head).  KVX_TB_HPI=1: off
+        const int64_t head_tile = (int64_t)Dm * 16 * S->elem_bytes, dst_tile = (int64_t)Dm * 16 * D->elem_bytes;
+        const char* hpi_env = getenv("KVX_TB_HPI");
+        int32_t hpi = (st == 1 && head_tile <= 2048 && dst_tile <= 2048 && !(hpi_env && atoi(hpi_env) < 2) &&
+                       a.Hd_eff % 2 == 0 && Hp % 2 == 0 && Hd % 2 == 0) ? 2 : 1;
+        for (int i = 0; i < n_src && hpi == 2; ++i)
+          if (src[i]->stride[KV_AX_HEAD] * src[i]->elem_bytes != head_tile) hpi = 1;
+        for (int i = 0; i < n_dst && hpi == 2; ++i)
+          if (a.hq_off[i] % 2) hpi = 1;
         for (int i = 0; i < n_src && use_tb; ++i) {
           const uint64_t rows = src[i]->pool_bytes / 128;
           if (src[i]->pool_bytes % 128 || rows >= (1ull << 31) || !ptr_aligned(src_pools[i], 16)) {
@@ -670,7 +684,7 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
           }
           cuuint64_t dims[2] = {128, (cuuint64_t)rows};
           cuuint64_t strides[1] = {128};
-          cuuint32_t box[2] = {128, (cuuint32_t)(Dm * S->elem_bytes / 8)};   // 16 x D elements / 128 B
+          cuuint32_t box[2] = {128, (cuuint32_t)(Dm * S->elem_bytes / 8 * hpi)};   // hpi x 16 x D elements / 128 B
           cuuint32_t estr[2] = {1, 1};
           if (enc(&tb.maps[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(src_pools[i]), dims, strides, box,
                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -680,7 +694,8 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
         tb.mode = st == 1 ? 1 : 2;
         const char* tl_env = getenv("KVX_TB_LUT");
         tb.lut = tl_env ? atoi(tl_env) : 1;
-        tb.tile_rows = Dm * S->elem_bytes / 8;
+        tb.hpi = hpi;
+        tb.tile_rows = Dm * S->elem_bytes / 8 * hpi;
         // tiles in flight per CTA: 64 KB for 2-byte sources (c4-pair V pool bf16 -> e4m3: 0.90 at
         // 32 KB, 0.97 at 64 KB), 32 KB for 1-byte ones (the 2-KB tiles want more CTAs, hence
         // less shared memory each: e4m3 0.91 at 32 KB, 0.72 at 64 KB); KVX_TB_STAGE_KB overrides
@@ -698,6 +713,8 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
         if (use_tb) {
           t_last_kernel = "k_convert_tb";
           tb.c = a;
+          tb.c.n_items = a.n_items / (uint32_t)tb.hpi;
+          tb.c.f_hde = make_fastdiv((uint32_t)(a.Hd_eff / tb.hpi));
           e = launch_convert_tb(tb, S->d.dtype, D->d.dtype, (cudaStream_t)stream);
         } else if (use_tr8) {
           t_last_kernel = "k_convert_tr8";

@@ -292,6 +292,7 @@ struct TbArgs {
   int32_t stages;
   int32_t mode;       // 1: head_dim-major (DIM, SLOT) tiles; 2: x-packed (D/x, SLOT, x), x = 16 B
   int32_t lut;        // fp8 -> other fp8, mode 1: per-item code tables (1) or the arithmetic cast (0)
+  int32_t hpi;        // heads per item (mode 1): 2 when a head's tile is <= 2 KB and the heads are adjacent
 };
 cudaError_t launch_convert_tb(const TbArgs& a, int sdt, int ddt, cudaStream_t s);
 cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s);

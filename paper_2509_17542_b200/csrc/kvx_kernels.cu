@@ -1541,7 +1541,7 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
 struct TbMeta {
   uint8_t* db;
   uint32_t valid;
-  float rsc, s2;
+  float rsc[2], s2[2];   // per head of the item (hpi <= 2)
 };
 
 __device__ __forceinline__ void tma_load_2d(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1,
@@ -1633,10 +1633,10 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
       const uint32_t cnt = min(32u, n_mine - g);
       uint8_t* m_db = nullptr;
       uint32_t m_valid = 0, m_row = 0, m_si = 0;
-      float m_rsc = 1.f, m_s2 = 1.f;
+      float m_rsc[2] = {1.f, 1.f}, m_s2[2] = {1.f, 1.f};
       if (lane < cnt) {
         uint32_t n = blockIdx.x + (g + lane) * gridDim.x;
-        const uint32_t hl = divmod(n, a.f_hde);
+        const uint32_t hl = divmod(n, a.f_hde) * (uint32_t)A.hpi;   // first head of the item
         const uint32_t c = take_kv(n, a.kv1, a.c0);
         const uint32_t l = divmod(n, a.f_l);
         const uint32_t bl = divmod(n, a.f_bl);
@@ -1652,15 +1652,22 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
         const uint32_t p = fdiv(h, a.f_hp);
         const uint32_t hp = h - p * (uint32_t)a.Hp;
         const int si = a.src_of_p[p];
-        if constexpr (dual_scale(SDT, DDT)) {
-          m_rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
-          m_s2 = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
-        } else {
-          if constexpr (is_fp8(SDT) && SDT != DDT) m_rsc = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp);
-          if constexpr (is_fp8(DDT) && SDT != DDT) m_rsc = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq));
-          m_s2 = m_rsc;
+#pragma unroll
+        for (uint32_t e = 0; e < 2; ++e) {   // the item's heads hq + e / hp + e (same P rank: host check)
+          if (e >= (uint32_t)A.hpi) break;
+          float rs = 1.f, s2v = 1.f;
+          if constexpr (dual_scale(SDT, DDT)) {
+            rs = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp + e);
+            s2v = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq + e));
+          } else {
+            if constexpr (is_fp8(SDT) && SDT != DDT) rs = __ldg(a.sscale[si] + (sl * 2 + c) * a.Hp + hp + e);
+            if constexpr (is_fp8(DDT) && SDT != DDT) rs = __frcp_rn(__ldg(a.dscale[qi] + (dl * 2 + c) * a.Hd + hq + e));
+            s2v = rs;
+          }
+          if constexpr (FOLD) rs = fnuz_fold_scale(rs);
+          m_rsc[e] = rs;
+          m_s2[e] = s2v;
         }
-        if constexpr (FOLD) m_rsc = fnuz_fold_scale(m_rsc);
         m_valid = (int32_t)tb0 >= T ? 0u : min(1u << lbd, (uint32_t)T - tb0);
         const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + (int32_t)(tb0 >> lbp));
         const int64_t off = sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
@@ -1676,12 +1683,12 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
         const uint32_t valid = __shfl_sync(0xFFFFFFFFu, m_valid, j);
         const uint32_t row = __shfl_sync(0xFFFFFFFFu, m_row, j);
         const uint32_t si = __shfl_sync(0xFFFFFFFFu, m_si, j);
-        const float rsc = __shfl_sync(0xFFFFFFFFu, m_rsc, j);
-        const float s2 = __shfl_sync(0xFFFFFFFFu, m_s2, j);
+        const float rsc0 = __shfl_sync(0xFFFFFFFFu, m_rsc[0], j), rsc1 = __shfl_sync(0xFFFFFFFFu, m_rsc[1], j);
+        const float s20 = __shfl_sync(0xFFFFFFFFu, m_s2[0], j), s21 = __shfl_sync(0xFFFFFFFFu, m_s2[1], j);
         if (lane == 0) {
           const uint32_t t = g + j, st = t % S;
           mbar_wait_guarded(empty + st, ((t / S) & 1u) ^ 1u);
-          meta[st] = TbMeta{reinterpret_cast<uint8_t*>(db), valid, rsc, s2};
+          meta[st] = TbMeta{reinterpret_cast<uint8_t*>(db), valid, {rsc0, rsc1}, {s20, s21}};
           mbar_expect_tx_arrive(full + st, tile_bytes);
           tma_load_2d(stages + (size_t)st * tile_bytes, &A.maps[si], 0, (int32_t)row, full + st);
         }
@@ -1715,7 +1722,7 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
         } else {
           Chunk<SDT, X> x;
           lds_chunk16B<SDT, X>(x, tile + R * 128u + ((c ^ (R & 7u)) << 4));
-          cast_chunk<SDT, DDT, X, FOLD>(x, o, m.rsc, m.s2);
+          cast_chunk<SDT, DDT, X, FOLD>(x, o, m.rsc[0], m.s2[0]);
         }
         store_chunk<DDT, X>(m.db + ((int64_t)sl * a.ds[KV_AX_SLOT] + dim_off(dq * X, a.ds[KV_AX_DIM], a.d_dk)) * DB, o);
       }
@@ -1728,18 +1735,28 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
     // then one byte permute + one LDS.U8 per code instead of the arithmetic cast
     constexpr bool LUT_OK = dual_scale(SDT, DDT);
     const bool LUT = LUT_OK && A.lut;
-    const uint32_t tab = tab0 + cw * 256u;
+    const uint32_t tab = tab0 + cw * 256u;   // head e's table at tab + 128 e
+    const uint32_t hpi = (uint32_t)A.hpi, head_bytes = tile_bytes / hpi;
     if (LUT) {
-      Chunk<SDT, 4> ci;
-      Chunk<DDT, 4> co;
-      ci.w[0] = 0x03020100u + lane * 0x04040404u;   // codes 4 lane .. 4 lane + 3
-      cast_chunk<SDT, DDT, 4, FOLD>(ci, co, m.rsc, m.s2);
-      asm volatile("st.shared.u32 [%0], %1;" ::"r"(tab + lane * 4u), "r"(co.w[0]) : "memory");
+      for (uint32_t e = 0; e < hpi; ++e) {
+        Chunk<SDT, 4> ci;
+        Chunk<DDT, 4> co;
+        ci.w[0] = 0x03020100u + lane * 0x04040404u;   // codes 4 lane .. 4 lane + 3
+        cast_chunk<SDT, DDT, 4, FOLD>(ci, co, m.rsc[e], m.s2[e]);
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(tab + e * 128u + lane * 4u), "r"(co.w[0]) : "memory");
+      }
       __syncwarp();
     }
-    for (uint32_t u = lane; u < nsub; u += 32u) {
-      const uint32_t s_sub = u & 1u, d_sub = u >> 1;
+    // units (head e of the item, 8 x 8 sub-block): head e's tile follows head e-1's in the
+    // stage (adjacent source heads, one TMA box; a head's rows are a multiple of 8, so the
+    // 128B swizzle phase restarts with each head)
+    for (uint32_t u = lane; u < (nsub * hpi); u += 32u) {
+      const uint32_t e = u >> (lcpr + 1u), uu = u & (nsub - 1u);
+      const uint32_t s_sub = uu & 1u, d_sub = uu >> 1;
       const uint32_t s0 = s_sub << 3, d0 = d_sub << 3;
+      const uint32_t htile = tile + e * head_bytes;
+      uint8_t* const hdb = m.db + (int64_t)e * a.ds[KV_AX_HEAD] * DB;
+      const float rsc = e ? m.rsc[1] : m.rsc[0], s2 = e ? m.s2[1] : m.s2[0];
       Chunk<DDT, 8> o[8];
       if (s0 >= m.valid) {
 #pragma unroll
@@ -1752,7 +1769,7 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
           // TMA 128B swizzle: 16-B unit c of 128-B row R sits at unit c ^ (R mod 8)
           const uint32_t off = (d0 + (uint32_t)k) * row_bytes + s0 * SB;
           const uint32_t R = off >> 7, c = (off >> 4) & 7u;
-          lds_chunk8<SDT>(x[k], tile + R * 128u + ((c ^ (R & 7u)) << 4) + (off & 15u));
+          lds_chunk8<SDT>(x[k], htile + R * 128u + ((c ^ (R & 7u)) << 4) + (off & 15u));
         }
         if (LUT) {
           // look the codes up (element-wise, so before the byte transpose), then transpose
@@ -1761,7 +1778,7 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
           for (int k = 0; k < 8; ++k)
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-              const uint32_t w = x[k].w[q], mi = w & 0x7F7F7F7Fu;
+              const uint32_t w = x[k].w[q], mi = (w & 0x7F7F7F7Fu) | (e ? 0x80808080u : 0u);   // | table half
               uint32_t b[4];
 #pragma unroll
               for (int j = 0; j < 4; ++j)
@@ -1778,14 +1795,14 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
           transpose8<SDT>(x, y);
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
-            cast_chunk<SDT, DDT, 8, FOLD>(y[k], o[k], m.rsc, m.s2);
+            cast_chunk<SDT, DDT, 8, FOLD>(y[k], o[k], rsc, s2);
             if (s0 + (uint32_t)k >= m.valid) zero_chunk(o[k]);
           }
         }
       }
       const int64_t doff = dim_off(d0, a.ds[KV_AX_DIM], a.d_dk);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) store_chunk<DDT, 8>(m.db + ((int64_t)(s0 + k) * a.ds[KV_AX_SLOT] + doff) * DB, o[k]);
+      for (int k = 0; k < 8; ++k) store_chunk<DDT, 8>(hdb + ((int64_t)(s0 + k) * a.ds[KV_AX_SLOT] + doff) * DB, o[k]);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(empty + st);
