@@ -659,7 +659,14 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
         encode_tiled_fn enc = encode_fn();
         // x-packed with x = 16 bytes: 2-byte sources only (bf16 K pool -> e4m3 0.90 -> 0.98 of copy;
         // 1-byte sources measured slower than k_convert_tr8: e4m3 -> bf16 0.89 vs 0.96, fnuz 0.76 vs 0.88)
-        const bool xp16 = st == 2 && S->elem_bytes == 2 && (1 << S->dk) * S->elem_bytes == 16;
+        // x-packed e4m3fn -> e4m3fnuz tiles (x = 16 codes) go through tb's per-item code tables:
+        // K pool 0.627 (k_convert_tr8, arithmetic fnuz encode) -> 0.827; the other direction
+        // stays on tr8, whose folded fnuz decode is cheaper there (0.872 vs 0.772 through tb;
+        // profiles/r02/tb_xpacked_fp8_ab.txt).  KVX_TB_X8=0: tr8 for both
+        const bool fp8_pair = S->d.dtype == KV_F8E4M3 && D->d.dtype == KV_F8E4M3FNUZ;
+        const char* tbx_env = getenv("KVX_TB_X8");
+        const bool xp16 = st == 2 && (1 << S->dk) * S->elem_bytes == 16 &&
+                          (S->elem_bytes == 2 || (fp8_pair && !(tbx_env && atoi(tbx_env) == 0)));
         use_tb = use_tr8 && (st == 1 || xp16) && dt == 0 && S->elem_bytes <= 2 && S->d.block_size == 16 &&
                  D->d.block_size == 16 && (Dm == 64 || Dm == 128 || Dm == 256) && enc && !(tb_env && atoi(tb_env) == 0);
         // two heads per item (one TMA box) when a head's source AND destination tiles are
@@ -670,7 +677,7 @@ kv_status convert_impl(int32_t n_src, const kv_layout* const* src, const void* c
         // destination tile is 4 KB, 0.951 -> 0.901, so it stays at one head).  KVX_TB_HPI=1: off
         const int64_t head_tile = (int64_t)Dm * 16 * S->elem_bytes, dst_tile = (int64_t)Dm * 16 * D->elem_bytes;
         const char* hpi_env = getenv("KVX_TB_HPI");
-        int32_t hpi = (st == 1 && head_tile <= 2048 && dst_tile <= 2048 && !(hpi_env && atoi(hpi_env) < 2) &&
+        int32_t hpi = ((st == 1 || xp16) && head_tile <= 2048 && dst_tile <= 2048 && !(hpi_env && atoi(hpi_env) < 2) &&
                        a.Hd_eff % 2 == 0 && Hp % 2 == 0 && Hd % 2 == 0) ? 2 : 1;
         for (int i = 0; i < n_src && hpi == 2; ++i)
           if (src[i]->stride[KV_AX_HEAD] * src[i]->elem_bytes != head_tile) hpi = 1;

@@ -1538,6 +1538,19 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
 // ------------------------------------------------------------------------------------
 // kTbConsumers: kvx_internal.h
 
+// Four fp8 codes through head e's 128-entry magnitude table of a 256-B table slot at tab
+// (head 0 at tab, head 1 at tab + 128: the half bit rides in each code's bit 7)
+template <int SDT, int DDT>
+__device__ __forceinline__ uint32_t lut_word(uint32_t w, uint32_t tab, uint32_t e) {
+  const uint32_t mi = (w & 0x7F7F7F7Fu) | (e ? 0x80808080u : 0u);
+  uint32_t b[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b[j]) : "r"(__byte_perm(mi, tab, 0x7650u + (uint32_t)j)));
+  return requant_sign4<SDT, DDT>(w, __byte_perm(__byte_perm(b[0], b[1], 0x0040u), __byte_perm(b[2], b[3], 0x0040u),
+                                                0x5410u));
+}
+
 struct TbMeta {
   uint8_t* db;
   uint32_t valid;
@@ -1708,28 +1721,6 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
     mbar_wait_guarded(full + st, (t / S) & 1u);
     const TbMeta m = meta[st];
     const uint32_t tile = stage0 + st * tile_bytes;
-    if constexpr (MODE == 2) {
-      constexpr uint32_t X = 16u / SB;                  // elements per 16-B chunk
-      const uint32_t lndq = lcpr + 3u - (SB == 1 ? 4u : 3u);   // log2(D / X)
-      const uint32_t ndq = 1u << lndq;
-      for (uint32_t idx = lane; idx < (ndq << 4); idx += 32u) {
-        const uint32_t dq = idx & (ndq - 1u), sl = idx >> lndq;   // lanes: consecutive chunks of one row
-        const uint32_t off = ((dq << 4) + sl) << 4;                // chunk (dq, slot) of the tile
-        const uint32_t R = off >> 7, c = (off >> 4) & 7u;
-        Chunk<DDT, X> o;
-        if (sl >= m.valid) {
-          zero_chunk(o);
-        } else {
-          Chunk<SDT, X> x;
-          lds_chunk16B<SDT, X>(x, tile + R * 128u + ((c ^ (R & 7u)) << 4));
-          cast_chunk<SDT, DDT, X, FOLD>(x, o, m.rsc[0], m.s2[0]);
-        }
-        store_chunk<DDT, X>(m.db + ((int64_t)sl * a.ds[KV_AX_SLOT] + dim_off(dq * X, a.ds[KV_AX_DIM], a.d_dk)) * DB, o);
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + st);
-      continue;
-    }
     // fp8 -> other fp8: this item's 128-entry magnitude code table (k_requant_rows' scheme),
     // built by the warp from the exact arithmetic cast -- 4 codes per lane, one cast_chunk --
     // then one byte permute + one LDS.U8 per code instead of the arithmetic cast
@@ -1746,6 +1737,41 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
         asm volatile("st.shared.u32 [%0], %1;" ::"r"(tab + e * 128u + lane * 4u), "r"(co.w[0]) : "memory");
       }
       __syncwarp();
+    }
+    if constexpr (MODE == 2) {
+      // x-packed tiles: 16-B chunks (dq, slot) hold X consecutive head_dim elements of one
+      // slot -- no transpose; head e of the item at tile + e x head_bytes
+      constexpr uint32_t X = 16u / SB;                  // elements per 16-B chunk
+      const uint32_t lndq = lcpr + 3u - (SB == 1 ? 4u : 3u);   // log2(D / X)
+      const uint32_t ndq = 1u << lndq;
+      for (uint32_t idx = lane; idx < ((ndq << 4) * hpi); idx += 32u) {
+        const uint32_t e = idx >> (lndq + 4u), ii = idx & ((ndq << 4) - 1u);
+        const uint32_t dq = ii & (ndq - 1u), sl = ii >> lndq;   // lanes: consecutive chunks of one row
+        const uint32_t off = ((dq << 4) + sl) << 4;                // chunk (dq, slot) of the head's tile
+        const uint32_t R = off >> 7, c = (off >> 4) & 7u;
+        uint8_t* const hdb = m.db + (int64_t)e * a.ds[KV_AX_HEAD] * DB;
+        Chunk<DDT, X> o;
+        if (sl >= m.valid) {
+          zero_chunk(o);
+        } else {
+          Chunk<SDT, X> x;
+          lds_chunk16B<SDT, X>(x, tile + e * head_bytes + R * 128u + ((c ^ (R & 7u)) << 4));
+          if constexpr (LUT_OK && X == 16) {
+            if (LUT) {
+#pragma unroll
+              for (int q = 0; q < 4; ++q) o.w[q] = lut_word<SDT, DDT>(x.w[q], tab, e);
+            } else {
+              cast_chunk<SDT, DDT, X, FOLD>(x, o, e ? m.rsc[1] : m.rsc[0], e ? m.s2[1] : m.s2[0]);
+            }
+          } else {
+            cast_chunk<SDT, DDT, X, FOLD>(x, o, e ? m.rsc[1] : m.rsc[0], e ? m.s2[1] : m.s2[0]);
+          }
+        }
+        store_chunk<DDT, X>(hdb + ((int64_t)sl * a.ds[KV_AX_SLOT] + dim_off(dq * X, a.ds[KV_AX_DIM], a.d_dk)) * DB, o);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + st);
+      continue;
     }
     // units (head e of the item, 8 x 8 sub-block): head e's tile follows head e-1's in the
     // stage (adjacent source heads, one TMA box; a head's rows are a multiple of 8, so the
@@ -1777,16 +1803,7 @@ __global__ void __launch_bounds__(32 * (1 + kTbConsumers)) k_convert_tb(const __
 #pragma unroll
           for (int k = 0; k < 8; ++k)
 #pragma unroll
-            for (int q = 0; q < 2; ++q) {
-              const uint32_t w = x[k].w[q], mi = (w & 0x7F7F7F7Fu) | (e ? 0x80808080u : 0u);   // | table half
-              uint32_t b[4];
-#pragma unroll
-              for (int j = 0; j < 4; ++j)
-                asm volatile("ld.shared.u8 %0, [%1];" : "=r"(b[j]) : "r"(__byte_perm(mi, tab, 0x7650u + (uint32_t)j)));
-              const uint32_t m4 =
-                  __byte_perm(__byte_perm(b[0], b[1], 0x0040u), __byte_perm(b[2], b[3], 0x0040u), 0x5410u);
-              xo[k].w[q] = requant_sign4<SDT, DDT>(w, m4);
-            }
+            for (int q = 0; q < 2; ++q) xo[k].w[q] = lut_word<SDT, DDT>(x[k].w[q], tab, e);
           transpose8<DDT>(xo, o);
 #pragma unroll
           for (int k = 0; k < 8; ++k)

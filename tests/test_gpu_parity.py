@@ -646,9 +646,10 @@ def test_tb_tiles(o1, monkeypatch, sdt, ddt, D, tp, n_tokens, split):
 @pytest.mark.parametrize("codes", ["random", "all"])
 @pytest.mark.parametrize("form", ["col", "xpack"])
 def test_tb_requant_tables(o1, monkeypatch, sdt, ddt, codes, form):
-    """fp8 -> other fp8 from other vendors' tiles -- head_dim-major V (form="col":
-    k_convert_tb's per-item code tables vs its arithmetic cast, KVX_TB_LUT=0, and vs
-    k_convert_tr8, KVX_TB=0) and x-packed K with x = 16 codes (form="xpack": k_convert_tr8)
+    """fp8 -> other fp8 from other vendors' tiles -- head_dim-major V (form="col") and
+    x-packed K with x = 16 codes (form="xpack"; through tb for e4m3fn -> fnuz only):
+    k_convert_tb's per-item code tables (two heads per TMA box) vs its arithmetic cast
+    (KVX_TB_LUT=0) and vs k_convert_tr8 (KVX_TB=0)
     -- all identical and equal to O1: random non-power-of-two scales on both sides, NaN
     codes, and (codes="all") every one of the 256 codes in every tile, ragged requests, TP
     split."""
@@ -671,7 +672,7 @@ def test_tb_requant_tables(o1, monkeypatch, sdt, ddt, codes, form):
         monkeypatch.setenv("KVX_TB", tb)
         monkeypatch.setenv("KVX_TB_LUT", lut)
         _, got[(tb, lut)], _ = run_case(o1, case)
-        want_k = "k_convert_tb" if tb == "1" and form == "col" else "k_convert_tr8"
+        want_k = "k_convert_tb" if tb == "1" and (form == "col" or ddt == FNUZ) else "k_convert_tr8"
         assert kvx.last_kernel() == want_k
     for r in runs[1:]:
         for a, b in zip(got[runs[0]], got[r]):
