@@ -13,7 +13,7 @@ hidden = (sequential - overlapped) / min(compute, push).
 layer l into a ring slot (kv_stage, one chunk) and releases it; the D rank (cuda:1) runs ONE
 persistent kv_pull_staged over all layers that waits in-kernel for each layer.  P's SMs only
 run the short HBM-bound packs, so the prefill loses little; the budget caps the pack.
-    python tools/overlap.py [--mode push|pull] [--budgets 0,64,32,16] [--gemm 4096]
+    python tools/overlap.py [--mode push|pull] [--budgets 0,64,32,16] [--carveouts 16:16,24:24] [--gemm 4096]
 """
 import argparse
 import json
@@ -37,6 +37,10 @@ def main():
     ap.add_argument("--iters", type=int, default=3)
     ap.add_argument("--mode", default="push", choices=["push", "pull"])
     ap.add_argument("--ring", type=int, default=4)
+    ap.add_argument("--carveouts", default="",
+                    help="budget:carveout pairs, e.g. 16:16,24:24 -- the transfer kernels capped at `budget` SMs "
+                         "AND cuBLAS kept off `carveout` SMs (torch._C._set_sm_carveout_experimental), so the "
+                         "prefill GEMMs and the pack / push run side by side instead of taking turns")
     args = ap.parse_args()
     import paper_2509_17542_b200 as kvx
     cfg = synth.configs()[args.workload]
@@ -141,17 +145,24 @@ def main():
             cur.wait_event(e)
 
     res = {"case": f"{args.workload} pair, {L} layers, GEMM {n}^3 bf16 per layer, {args.mode}", "runs": []}
-    t_c = timed(lambda: run(True, False, False))
-    for budget in [int(x) for x in args.budgets.split(",")]:
+    pairs = [(int(x), 0) for x in args.budgets.split(",") if x]
+    pairs += [tuple(int(v) for v in x.split(":")) for x in args.carveouts.split(",") if x]
+    t_c0 = timed(lambda: run(True, False, False))
+    for budget, carve in pairs:
+        torch._C._set_sm_carveout_experimental(carve or None)
+        t_c = timed(lambda: run(True, False, False)) if carve else t_c0
         kvx.set_sm_budget(budget)
         t_x = timed(lambda: run(False, True, False))
         t_seq = timed(lambda: run(True, True, False))
         t_ovl = timed(lambda: run(True, True, True))
-        res["runs"].append({"transfer_sm_budget_on_P": budget or 148, "compute_ms": round(t_c, 3), "push_ms": round(t_x, 3),
+        res["runs"].append({"transfer_sm_budget_on_P": budget or 148, "gemm_sm_carveout": carve,
+                            "compute_ms": round(t_c, 3), "compute_ms_all_sms": round(t_c0, 3), "push_ms": round(t_x, 3),
                             "sequential_ms": round(t_seq, 3), "overlapped_ms": round(t_ovl, 3),
                             "hidden_frac": round((t_seq - t_ovl) / min(t_c, t_x), 3),
+                            "vs_all_sm_prefill_ms": round(t_ovl - t_c0, 3),
                             "push_nvlink_GBs": round(dst.dst_bytes([0]) / t_x / 1e6, 1)})
     kvx.set_sm_budget(0)
+    torch._C._set_sm_carveout_experimental(None)
     if pull:
         res["err"] = int(err0.item()) + int(err1.item())
         dst.src_pools[0], dst.src_dicts[0] = SP, src.src_dicts[0]
