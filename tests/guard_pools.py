@@ -43,6 +43,13 @@ class Guarded:
         acc.flags = cu.CUmemAccess_flags.CU_MEM_ACCESS_FLAGS_PROT_READWRITE
         _ck(cu.cuMemSetAccess(self.ptr, nbytes, [acc], 1))
 
+    @classmethod
+    def tail(cls, cu, dev, nbytes, gran):
+        """nbytes ending exactly at the end of a mapping (the next byte unmapped)."""
+        g = cls(cu, dev, -(-nbytes // gran) * gran)
+        g.ptr_end = g.ptr + g.n - nbytes
+        return g
+
     def upload(self, arr):
         a = np.ascontiguousarray(arr).view(np.uint8)
         assert a.nbytes == self.n
@@ -109,8 +116,50 @@ def run_group(group):
             ("generic", 2, 8, 16, 2, 2, 4, 8, F16, F32, (SLOT, KV, BLOCK, DIM, LAYER, HEAD),
              (DIM, BLOCK, LAYER, KV, SLOT, HEAD), 0, {}, "k_convert"),
         ],
-    }[group]
+    }.get(group, [])
     seen = []
+    if group == "wire":
+        # kv_pack from guarded P pools into a wire buffer that ends at an unmapped page,
+        # kv_unpack from it into guarded D pools, kv_compute_scales over the guarded P pools
+        for so, want in ((synth.P_ORDER, "k_pack_rows"), ((SLOT, KV, BLOCK, DIM, LAYER, HEAD), "k_pack")):
+            L, H, D, tp_p, tp_d, B = 2, 8, 128, 4, 2, 16
+            f = lambda dt, tp: (lambda nb: L * 2 * nb * B * (H // tp) * D * synth.NBYTES[dt])  # noqa: E731
+            NB = max(_nb_for(f(BF16, tp_p), synth.pool_capacity(ragged, B), gran),
+                     _nb_for(f(E4M3, tp_d), synth.pool_capacity(ragged, B), gran))
+            case = make_case(L, H, D, tp_p, tp_d, B, B, ragged, BF16, E4M3, so, synth.D_ORDER, seed=60, o1=O1,
+                             scales="amax", NB_p=NB, NB_d=NB)
+            src_g = [Guarded(cu, dev, p.nbytes) for p in case["src_pools"]]
+            dst_g = [Guarded(cu, dev, p.nbytes) for p in case["dst_pools"]]
+            for g_, p in zip(src_g + dst_g, case["src_pools"] + case["dst_pools"]):
+                g_.upload(p)
+            S = [kvx.Layout.from_dict(lay) for lay in case["src_lays"]]
+            Dl = [kvx.Layout.from_dict(lay, torch.from_numpy(np.asarray(lay["scales"], np.float32)).cuda())
+                  for lay in case["dst_lays"]]
+            sbt = kvx.Batch(S[0], ragged, case["src_tables"], "cuda")
+            dbt = kvx.Batch(Dl[0], ragged, case["dst_tables"], "cuda")
+            for q in range(tp_d):
+                for p in range(tp_p):
+                    nb = kvx.wire_bytes(S[p], Dl[q], sum(ragged))
+                    if nb == 0:
+                        continue
+                    w = Guarded.tail(cu, dev, nb, gran)
+                    kvx.pack(S[p], src_g[p].ptr, sbt, Dl[q], w.ptr_end, wire_nbytes=nb)
+                    assert kvx.last_kernel() == want, kvx.last_kernel()
+                    kvx.unpack(S[p], Dl[q], dst_g[q].ptr, dbt, w.ptr_end, wire_nbytes=nb)
+                    torch.cuda.synchronize()
+                    w.free()
+                    seen += [want, kvx.last_kernel()]
+            got = [g_.download(p) for g_, p in zip(dst_g, case["dst_pools"])]
+            assert_pools_match(got, expected(case, O1), E4M3)
+            for q in range(tp_d):
+                out = torch.empty(L * 2 * (H // tp_d), dtype=torch.float32, device="cuda")
+                kvx.compute_scales(S, [g_.ptr for g_ in src_g], sbt, Dl[q], out)
+                want_sc = O1.amax_scales(case["src_lays"], case["src_pools"], case["dst_lays"][q], ragged,
+                                         case["src_tables"])
+                assert np.array_equal(out.cpu().numpy().reshape(want_sc.shape), want_sc)
+            seen.append("k_amax")
+            for g_ in src_g + dst_g:
+                g_.free()
     for name, L, H, D, tp_p, tp_d, Bp, Bd, sdt, ddt, po, do, psplit, env, want_k in cases:
         nbytes = lambda dt, tp, B: (lambda nb: L * 2 * nb * B * (H // tp) * D * synth.NBYTES[dt])  # noqa: E731
         need_p = synth.pool_capacity(ragged, Bp)
