@@ -844,12 +844,14 @@ kv_status kv_convert_reshard(int32_t n_src, const kv_layout* const* src, const v
                              const kv_batch* src_bt, int32_t n_dst, const kv_layout* const* dst,
                              void* const* dst_pools, const kv_batch* dst_bt, int32_t lb, int32_t le,
                              kv_stream stream) {
+  NvtxRange nvtx_("kv_convert_reshard", lb);
   return convert_impl(n_src, src, src_pools, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, false);
 }
 
 kv_status kv_convert_share(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, int32_t n_dst,
                            const kv_layout* const* dst, void* const* dst_pools, const kv_batch* dst_bt, int32_t lb,
                            int32_t le, kv_stream stream) {
+  NvtxRange nvtx_("kv_convert_share", lb);
   const kv_layout* s1[1] = {src};
   const void* p1[1] = {src_pool};
   return convert_impl(1, s1, p1, src_bt, n_dst, dst, dst_pools, dst_bt, lb, le, stream, true);
@@ -860,6 +862,7 @@ kv_status kv_convert_reshard_notify(int32_t n_src, const kv_layout* const* src, 
                                     void* const* dst_pools, const kv_batch* dst_bt, int32_t lb, int32_t le,
                                     uint32_t* counters, uint32_t* done_flags, uint64_t* done_ns, uint32_t epoch,
                                     kv_stream stream) {
+  NvtxRange nvtx_("kv_convert_reshard_notify", lb);
   if (!dst_bt || (dst_bt->n_req > 0 && (!counters || !done_flags)))
     return fail(KV_EINVAL, "kv_convert_reshard_notify: null counters / flags");
   Notify nt{counters, done_flags, done_ns, epoch};
@@ -994,6 +997,7 @@ size_t kv_wire_bytes(const kv_layout* s, const kv_layout* d, int64_t total_token
 
 kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_bt, const kv_layout* d, int32_t lb,
                   int32_t le, void* wire, size_t wire_bytes, kv_stream stream) {
+  NvtxRange nvtx_("kv_pack", lb);
   if (!s || !d || !src_pool || !wire) return fail(KV_EINVAL, "kv_pack: null argument");
   kv_status st;
   if ((st = same_model(s, d)) != KV_OK) return st;
@@ -1052,6 +1056,7 @@ kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_
 
 kv_status kv_unpack(const kv_layout* s, const kv_layout* d, void* dst_pool, const kv_batch* dst_bt, int32_t lb,
                     int32_t le, const void* wire, size_t wire_bytes, kv_stream stream) {
+  NvtxRange nvtx_("kv_unpack", lb);
   if (!s || !d || !dst_pool || !wire) return fail(KV_EINVAL, "kv_unpack: null argument");
   kv_status st;
   if ((st = same_model(s, d)) != KV_OK) return st;

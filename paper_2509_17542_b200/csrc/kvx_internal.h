@@ -1,5 +1,6 @@
 // Internal declarations shared by the library's translation units (not part of the ABI).
 #pragma once
+#include <nvtx3/nvToolsExt.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -291,8 +292,8 @@ struct TbArgs {
   int32_t tile_rows;  // 128-B rows per tile (B * D * esize / 128)
   int32_t stages;
   int32_t mode;       // 1: head_dim-major (DIM, SLOT) tiles; 2: x-packed (D/x, SLOT, x), x = 16 B
-  int32_t lut;        // fp8 -> other fp8, mode 1: per-item code tables (1) or the arithmetic cast (0)
-  int32_t hpi;        // heads per item (mode 1): 2 when a head's tile is <= 2 KB and the heads are adjacent
+  int32_t lut;        // fp8 -> other fp8: per-item code tables (1) or the arithmetic cast (0)
+  int32_t hpi;        // heads per item: 2 when both head tiles are <= 2 KB and the heads are adjacent
 };
 cudaError_t launch_convert_tb(const TbArgs& a, int sdt, int ddt, cudaStream_t s);
 cudaError_t launch_pack(const PackArgs& a, int vec, int sdt, int wdt, cudaStream_t s);
@@ -300,5 +301,27 @@ cudaError_t launch_unpack(const UnpackArgs& a, int vec, int wdt, int ddt, cudaSt
 cudaError_t launch_signal(uint32_t* flag, uint32_t value, cudaStream_t s);
 cudaError_t launch_copy_bytes(void* dst, const void* src, size_t bytes, cudaStream_t s);
 cudaError_t launch_wait(const uint32_t* flag, uint32_t value, uint64_t timeout_ns, int32_t* err, cudaStream_t s);
+
+// NVTX range over a host call (SURVEY §5 tracing: the layer-chunk structure of the
+// schedulers shows up in any NVTX-aware profiler, e.g. `ncu --nvtx`); `payload` is the
+// chunk's first layer.  nvtx3 is header-only: with no tool attached push / pop are a
+// branch each.
+struct NvtxRange {
+  explicit NvtxRange(const char* name, int64_t payload = -1) {
+    nvtxEventAttributes_t at = {};
+    at.version = NVTX_VERSION;
+    at.size = NVTX_EVENT_ATTRIB_STRUCT_SIZE;
+    at.messageType = NVTX_MESSAGE_TYPE_ASCII;
+    at.message.ascii = name;
+    if (payload >= 0) {
+      at.payloadType = NVTX_PAYLOAD_TYPE_INT64;
+      at.payload.llValue = payload;
+    }
+    nvtxRangePushEx(&at);
+  }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 }  // namespace kvx

@@ -78,10 +78,12 @@ kv_status kv_push(const kv_layout* src, const void* src_pool, const kv_batch* sr
   if ((st = kv_convert_share(src, src_pool, src_bt, n_dst, dst, dst_pools, dst_bt, le, le, stream)) != KV_OK)
     return st;
   const int32_t step = layer_chunk > 0 ? layer_chunk : std::max(1, le - lb);
-  for (int32_t l0 = lb; l0 < le; l0 += step)
+  for (int32_t l0 = lb; l0 < le; l0 += step) {
+    NvtxRange r("kv_push chunk", l0);
     if ((st = kv_convert_share(src, src_pool, src_bt, n_dst, dst, dst_pools, dst_bt, l0, std::min(le, l0 + step),
                                stream)) != KV_OK)
       return st;
+  }
   for (int i = 0; i < n_dst; ++i)
     if ((st = kv_signal(peer_flags[i], epoch, stream)) != KV_OK) return st;
   return KV_OK;
@@ -107,6 +109,7 @@ kv_status kv_send_pipelined(kv_comm* comm, const kv_layout* src, const void* src
   if (st != KV_OK) return st;
   int32_t k = 0;
   for (int32_t l0 = lb; l0 < le; l0 += step, ++k) {
+    NvtxRange r("kv_send_pipelined chunk", l0);
     const int32_t l1 = std::min(le, l0 + step), b = k & 1;
     for (int i = 0; i < n_dst; ++i) {
       const int j = 2 * i + b;
@@ -133,6 +136,7 @@ kv_status kv_recv_pipelined(kv_comm* comm, int32_t n_src, const kv_layout* const
                             const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt, void* const* wires,
                             size_t wire_cap, int32_t lb, int32_t le, int32_t layer_chunk, kv_stream stream,
                             kv_stream recv_stream, kv_stream unpack_stream) {
+  NvtxRange nvtx_("kv_recv_pipelined");
   if (!comm || !src || !dst || !dst_bt || !peer_ranks || !wires || n_src < 1)
     return fail(KV_EINVAL, "kv_recv_pipelined: bad argument");
   const int32_t step = layer_chunk > 0 ? layer_chunk : std::max(1, le - lb);
@@ -178,6 +182,7 @@ kv_status kv_pull(int32_t n_src, const kv_layout* const* src, const void* const*
                   const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt, const uint32_t* const* ready_flags,
                   uint32_t* const* done_flags, uint32_t epoch, int32_t lb, int32_t le, int32_t layer_chunk,
                   uint64_t timeout_ns, int32_t* err, kv_stream stream) {
+  NvtxRange nvtx_("kv_pull");
   if (n_src < 1 || !ready_flags || !done_flags || !err) return fail(KV_EINVAL, "kv_pull: bad argument");
   for (int i = 0; i < n_src; ++i)
     if (!ready_flags[i] || !done_flags[i]) return fail(KV_EINVAL, "kv_pull: null flag");
@@ -236,6 +241,7 @@ kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* s
   }
   uint64_t seq = seq0;
   for (int32_t l0 = lb; l0 < le; l0 += step, ++seq) {
+    NvtxRange r("kv_stage chunk", l0);
     const int32_t l1 = std::min(le, l0 + step), b = ring_slot(seq, ring_slots);
     for (int i = 0; i < n_dst; ++i) {
       // slot b last held chunk seq - R: the D rank must have released it (free >= seq - R + 1)
@@ -269,6 +275,7 @@ kv_status kv_pull_staged(int32_t n_src, const kv_layout* const* src, const void*
                          const uint32_t* const* ready_flags, uint32_t* const* free_flags, uint32_t* counters,
                          uint32_t seq0, int32_t lb, int32_t le, int32_t layer_chunk, uint64_t timeout_ns, int32_t* err,
                          kv_stream stream) {
+  NvtxRange nvtx_("kv_pull_staged");
   if (n_src < 1 || !src || !rings || ring_slots < 1 || !dst || !dst_bt || !ready_flags || !free_flags || !err)
     return fail(KV_EINVAL, "kv_pull_staged: bad argument");
   for (int i = 0; i < n_src; ++i) {
