@@ -10,9 +10,14 @@
 //     destination makes it the D-side NVLink pull or the P-side push.
 //   * k_tile_copy (same dtype, D's inner axes {HEAD, SLOT} x DIM): one 5-D TMA tensor load per
 //     source sub-tile, already permuted into D's order, then bulk stores.
-//   * k_convert_tb (head_dim-major 1-/2-byte source tiles of 16 slots): one 2-D TMA load per
-//     tile into swizzled shared-memory stages, warp-specialised producer / consumers that
-//     transpose 8 x 8 sub-blocks out of shared memory.
+//   * k_tile_cast (the same sub-tiles with a cast: TMA-fed stages, 8 consumer warps convert
+//     the rows; the N = 1 default for 2-byte sources).
+//   * k_convert_tb (head_dim-major 1-/2-byte source tiles of 16 slots, x-packed 2-byte and
+//     fp8 tiles): one 2-D TMA load per tile (or two heads) into swizzled shared-memory
+//     stages, warp-specialised producer / consumers that transpose 8 x 8 sub-blocks out of
+//     shared memory.
+//   * k_requant_rows (fp8 -> other fp8): the row items with 128-entry shared-memory code
+//     tables instead of the arithmetic cast.
 //   * k_convert_tr8 / k_convert_tr (other head_dim-major or x-packed sides): 8 x 8 register
 //     transposes / shared-memory tiles.
 //   * k_pack_rows / k_unpack_rows (Fig. 5 flatten / restore for the NCCL mode), k_pull_rows
@@ -1534,7 +1539,12 @@ __global__ void __launch_bounds__(kThreads) k_unpack_rows(const __grid_constant_
 // and stores eight rows of D's (SLOT, DIM) tile.  The HBM side sees only whole 4-KB tile reads
 // issued by the TMA engine (k_convert_tr8's per-lane 16-B loads left it at ~0.8 of copy).
 // Metadata of 32 items at a time is computed lane-parallel by the producer (one dependent-load
-// round trip per 32 tiles) and handed to the consumers through the stage's slot.
+// round trip per 32 tiles) and handed to the consumers through the stage's slot.  Mode 2
+// takes x-packed (D/x, SLOT, x = 16 B) tiles the same way (no transpose: a 16-B chunk is x
+// head_dim elements of one slot).  When both sides' head tiles are <= 2 KB an item is two
+// adjacent heads (one TMA box, A.hpi = 2); an fp8 -> other fp8 item first builds its
+// heads' 128-entry code tables in the consumer warp's table slot (k_requant_rows' scheme)
+// and looks the codes up instead of the arithmetic cast.
 // ------------------------------------------------------------------------------------
 // kTbConsumers: kvx_internal.h
 
