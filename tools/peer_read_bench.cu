@@ -118,5 +118,50 @@ int main() {
       timeit(nm, [&] { k_bulk<<<148 * per_sm, 32, smem, st>>>(src, dst, N / chunk, chunk, S); });
     }
   }
+  // reads by GPU0's SMs from GPU1 and writes by GPU1's SMs into GPU0 at the same time:
+  // both carry data GPU1 -> GPU0 -- does mixing them beat either alone?
+  {
+    uint8_t *src1b, *dst0b;   // GPU1 -> GPU0 write pair: source on GPU1, destination on GPU0
+    CK(cudaSetDevice(0));
+    CK(cudaMalloc(&dst0b, N));
+    CK(cudaSetDevice(1));
+    CK(cudaDeviceEnablePeerAccess(0, 0));
+    CK(cudaMalloc(&src1b, N));
+    CK(cudaMemset(src1b, 2, N));
+    cudaStream_t st1;
+    CK(cudaStreamCreate(&st1));
+    cudaEvent_t f0, f1;
+    CK(cudaEventCreate(&f0));
+    CK(cudaEventCreate(&f1));
+    for (double frac : {0.0, 0.25, 0.4, 0.5, 0.6, 1.0}) {
+      const size_t nr = (size_t)(N * frac) / 4096 * 4096, nw = N - nr;   // bytes read by GPU0 / written by GPU1
+      std::vector<float> ts;
+      for (int i = 0; i < 6; ++i) {
+        CK(cudaSetDevice(0));
+        CK(cudaDeviceSynchronize());
+        CK(cudaSetDevice(1));
+        CK(cudaDeviceSynchronize());
+        CK(cudaSetDevice(0));
+        CK(cudaEventRecord(e0, st));
+        CK(cudaStreamWaitEvent(st1, e0, 0));   // start both together
+        if (nr) k_ldg<4><<<148 * 4, 256, 0, st>>>((const uint4*)src, (uint4*)dst, nr / 16);
+        CK(cudaSetDevice(1));
+        if (nw) k_ldg<4><<<148 * 4, 256, 0, st1>>>((const uint4*)src1b, (uint4*)dst0b, nw / 16);   // stores go over NVLink
+        CK(cudaEventRecord(f1, st1));
+        CK(cudaSetDevice(0));
+        CK(cudaStreamWaitEvent(st, f1, 0));
+        CK(cudaEventRecord(e1, st));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaGetLastError());
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (i) ts.push_back(ms);
+      }
+      std::sort(ts.begin(), ts.end());
+      const float ms = ts[ts.size() / 2];
+      printf("mixed: %.0f%% by GPU0 SM reads + %.0f%% by GPU1 SM writes  %8.3f ms  %7.1f GB/s GPU1->GPU0\n",
+             100 * frac, 100 * (1 - frac), ms, N / (ms * 1e-3) / 1e9);
+    }
+  }
   return 0;
 }
