@@ -67,7 +67,11 @@ def _p_view_of_d(kvx, case, dyn):
     return out
 
 
-def _run(o1, case, mode):
+def _run(o1, case, mode, serial_safe=False):
+    """serial_safe (the smoke): ring slots for every chunk and P's stages enqueued before D's
+    persistent pulls, so the transfer also completes when every kernel runs alone in launch
+    order (a profiler's replay, e.g. ncu over smoke()) -- P never waits for a free slot and
+    each spin-wait is launched after the work it waits for."""
     import paper_2509_17542_b200 as kvx
     from tests.gpu_util import DevCase
     dc = DevCase(case, "cuda:0")
@@ -94,31 +98,44 @@ def _run(o1, case, mode):
         nb = max(kvx.wire_bytes(S[p], D[q], dc.src_bt.total_tokens, (l, l + 1)) for p, q, _, _ in pairs
                  for l in range(L))
         nb = max(16, (nb + 255) // 256 * 256)
-        rings = {(p, q): torch.empty(R * nb, dtype=torch.uint8, device="cuda:0") for p, q, _, _ in pairs}
+        Rr = L if serial_safe else R
+        rings = {(p, q): torch.empty(Rr * nb, dtype=torch.uint8, device="cuda:0") for p, q, _, _ in pairs}
         persistent = mode != "pull_staged_chunked"
+
+        def d_pulls():
+            prev = kvx.set_sm_budget(BUDGET)
+            try:
+                for q in range(len(D)):
+                    ps = [p for p, q2, _, _ in pairs if q2 == q]
+                    if persistent:
+                        counters[q] = torch.zeros(kvx.pull_counter_words((0, L), lc), dtype=torch.int32,
+                                                  device="cuda:0")
+                    with torch.cuda.stream(d_streams[q]):
+                        kvx.pull_staged([S[p] for p in ps],
+                                        [rings[(p, q)].data_ptr() + b * nb for p in ps for b in range(Rr)], Rr, nb,
+                                        D[q], dc.dst_pools[q], dc.dst_bt, [w(ready, q * 8 + p) for p in ps],
+                                        [w(freew, p * 8 + q) for p in ps], 0, err, (0, L), lc, TIMEOUT, d_streams[q],
+                                        counters=counters.get(q))
+                    kernels.add(kvx.last_kernel())
+            finally:
+                kvx.set_sm_budget(prev)
+
         # D first: the persistent kernels sit on their SM budget waiting for P's ready words
-        prev = kvx.set_sm_budget(BUDGET)
-        try:
-            for q in range(len(D)):
-                ps = [p for p, q2, _, _ in pairs if q2 == q]
-                if persistent:
-                    counters[q] = torch.zeros(kvx.pull_counter_words((0, L), lc), dtype=torch.int32, device="cuda:0")
-                with torch.cuda.stream(d_streams[q]):
-                    kvx.pull_staged([S[p] for p in ps], [rings[(p, q)].data_ptr() + b * nb for p in ps for b in range(R)],
-                                    R, nb, D[q], dc.dst_pools[q], dc.dst_bt, [w(ready, q * 8 + p) for p in ps],
-                                    [w(freew, p * 8 + q) for p in ps], 0, err, (0, L), lc, TIMEOUT, d_streams[q],
-                                    counters=counters.get(q))
-                kernels.add(kvx.last_kernel())
-        finally:
-            kvx.set_sm_budget(prev)
+        if not serial_safe:
+            d_pulls()
         for p in range(len(S)):
             qs = [q for p2, q, _, _ in pairs if p2 == p]
             with torch.cuda.stream(p_streams[p]):
                 kvx.stage(S[p], dc.src_pools[p], dc.src_bt, [DP[q] for q in qs],
-                          [rings[(p, q)].data_ptr() + b * nb for q in qs for b in range(R)], R, nb,
+                          [rings[(p, q)].data_ptr() + b * nb for q in qs for b in range(Rr)], Rr, nb,
                           [w(ready, q * 8 + p) for q in qs], [w(freew, p * 8 + q) for q in qs], 0, err, (0, L), lc,
                           TIMEOUT, p_streams[p], peer_scales=[D[q].scales for q in qs] if dyn else None)
                 kernels.add(kvx.last_kernel())
+        if serial_safe:
+            d_pulls()
+        for p in range(len(S)):
+            qs = [q for p2, q, _, _ in pairs if p2 == p]
+            with torch.cuda.stream(p_streams[p]):
                 for q in qs:   # every chunk consumed: P may reuse its ring
                     kvx.wait(w(freew, p * 8 + q), L, err, TIMEOUT, p_streams[p])
     elif mode == "pull":
@@ -186,6 +203,20 @@ def test_transport_one_gpu(o1, mode, shape):
         assert "k_pack_rows" in kernels or "k_pack" in kernels, kernels
     want = _scales_and_want(o1, case, dc) if mode == "pull_staged_dyn" else expected(case, o1)
     assert_pools_match(dc.dst_numpy(), want, case["dst_lays"][0]["dtype"])
+
+
+def test_smoke_with_serialized_launches():
+    """smoke() (one-GPU staged pull included) with every launch synchronous, as when a
+    profiler (ncu over smoke()) runs each kernel alone in launch order: no spin-wait may be
+    launched ahead of the work that releases it."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1", KVX_TEST_TIMEOUT="10")
+    r = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; g.smoke()"], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "smoke ok" in r.stdout and "k_pull_rows" in r.stdout, r.stdout[-2000:]
 
 
 def test_staged_pull_two_calls_seq0(o1):
