@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--dynamic-scales", action="store_true",
                     help="pull mode, fp8 destination: P computes per-chunk amax scales and ships them (NEXT-1 i)")
     ap.add_argument("--layer-chunk", type=int, default=0, help="layers per chunk (0 = whole model / auto)")
+    ap.add_argument("--chunk-ramp", action="store_true",
+                    help="staged pull: ramp the first three layer chunks up (negative layer_chunk, kv_chunk_count); "
+                         "measured slower on the c4 pair, so off by default")
     ap.add_argument("--chunk-mib", type=int, default=64, help="c5: merge layers until a chunk moves this much")
     ap.add_argument("--c5-batch", action="store_true", help="c5: each instance's requests as one batch (no per-request handoff)")
     ap.add_argument("--c5-no-sm-split", action="store_true", help="c5 pull: the two source streams share all SMs")
@@ -786,14 +789,21 @@ def run_multi(args):
                              scales=mine.get("scales") if dyn and me.kind == "D" else None)
         if me.kind == "D" and narrowing:
             slot_bytes = min(pch.slot_bytes[p] for p in my_p)
-        nchunks = kvx.chunk_count((0, cfg.L), lc)
-        counters = torch.zeros(kvx.pull_counter_words((0, cfg.L), lc), dtype=torch.int32, device=dev)
+        # --chunk-ramp: the timed step ramps its first chunks (negative layer_chunk,
+        # kv_chunk_count); the e2e step stages whole uniform chunks range by range, so both
+        # sides use uniform chunks there
+        lc_ramp = -lc if args.chunk_ramp else lc
+        counters = torch.zeros(max(kvx.pull_counter_words((0, cfg.L), x) for x in (lc, lc_ramp)), dtype=torch.int32,
+                               device=dev)
         seq = [0]
 
-        def step(ev=None, pre=None):
+        def step(ev=None, pre=None, uniform=False):
             """pre (e2e, narrowing pull, P side): (ranges, fn) -- stage the layer ranges one
             after the other (same chunk numbering as one call), fn(l0, l1) enqueued before each
-            (its host upload), so the upload of range k+1 overlaps the transfer of range k."""
+            (its host upload), so the upload of range k+1 overlaps the transfer of range k.
+            uniform (the e2e steps, both sides): uniform layer chunks instead of the ramp."""
+            lcx = lc if uniform or pre else lc_ramp
+            nchunks = kvx.chunk_count((0, cfg.L), lcx)
             epoch[0] += 1
             if ev is not None and me.kind == "D":
                 ev[0].record(stream)
@@ -805,9 +815,9 @@ def run_multi(args):
                             pre[1](l0, l1)
                         kvx.stage(S, mine["pool"], mine["bt"], [peer_lays[q] for q in my_q], ring_ptrs, R,
                                   slot_bytes, [pch.peer_flag[q] for q in my_q], [pflags[q:q + 1] for q in my_q], s0,
-                                  err, (l0, l1), lc, 30.0, stream,
+                                  err, (l0, l1), lcx, 30.0, stream,
                                   peer_scales=[pch.peer_scales[q] for q in my_q] if dyn else None)
-                        s0 += kvx.chunk_count((l0, l1), lc)
+                        s0 += kvx.chunk_count((l0, l1), lcx)
                 else:
                     for q in my_q:   # my KV is resident: D may read it; then wait until it has
                         kvx.signal(pch.peer_flag[q], epoch[0], stream)
@@ -817,7 +827,7 @@ def run_multi(args):
                 if narrowing:
                     kvx.pull_staged([peer_lays[p] for p in my_p], [a for p in my_p for a in pch.src_ring[p]], R,
                                     slot_bytes, S, mine["pool"], mine["bt"], [pflags[p:p + 1] for p in my_p],
-                                    [pch.peer_flag[p] for p in my_p], seq[0], err, (0, cfg.L), lc, 30.0, stream,
+                                    [pch.peer_flag[p] for p in my_p], seq[0], err, (0, cfg.L), lcx, 30.0, stream,
                                     counters=counters)
                 else:
                     kvx.pull([peer_lays[p] for p in my_p], [pch.src_pool[p] for p in my_p], peer_bt, S,
@@ -987,7 +997,10 @@ def run_multi(args):
                                    + (" (full transfer)" if full else " (per-GPU-equivalent sub-config)")
                                    + (f", {world - n_p - n_d} idle GPU(s)" if world > n_p + n_d else ""),
                        "mode": args.mode + (" + dynamic fp8 scales (P amax per chunk, shipped)" if dyn else ""),
-                       "layer_chunk": lc, "requests": len(cfg.n_tokens),
+                       "layer_chunk": lc,
+                       "chunks": (kvx.chunk_count((0, cfg.L), -lc if args.chunk_ramp else lc)
+                                  if args.mode == "pull" and narrowing else None),
+                       "requests": len(cfg.n_tokens),
                        "tokens": cfg.total_tokens, "overrides": _overrides(args), "src_bytes_per_step": sb,
                        "busiest_link_bytes_per_step": nvl_b, "pairs": [list(x[:2]) for x in pairs],
                        "control_plane": "layouts, block tables and fp8 scales exchanged as kv_ctrl messages "
@@ -1085,6 +1098,8 @@ def e2e_multi(mine, me, step, stream, barrier, err, ke, rank, L=None):
             view.index_copy_(1, ids, stage)
         if pre is not None:
             step(pre=pre)
+        elif getattr(step, "chunked_upload", None):
+            step(uniform=True)   # the same uniform chunks P stages range by range
         else:
             step()
         if me.kind == "D":

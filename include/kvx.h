@@ -16,8 +16,9 @@
  *
  * Conventions (all calls):
  *   - Ownership: the caller owns every device buffer (pools, tables, wire and
- *     scratch).  Hot calls allocate no device memory.  Handles hold host
- *     metadata only.
+ *     scratch).  Hot calls allocate no device memory (one exception: kv_stage's
+ *     opt-in KVX_STAGE_PERSISTENT path takes its counters from the stream-ordered
+ *     pool).  Handles hold host metadata only.
  *   - Asynchrony: calls validate synchronously, then enqueue on `stream` (a
  *     cudaStream_t passed as void*; NULL = legacy default stream) and return
  *     before device work completes.  Buffers must outlive the stream work.
@@ -401,8 +402,16 @@ kv_status kv_recv_pipelined(kv_comm* comm, int32_t n_src, const kv_layout* const
  * shared counter, wait in-kernel for each chunk's ready words, and the warp completing a
  * chunk frees its slots, strictly in chunk order (a free value v means every chunk below v
  * has been read) -- no per-chunk launch gap.  It needs `counters`, a caller-owned DEVICE
- * scratch of >= 2 x (number of chunks) + 1 uint32 that the call zeroes on its stream
+ * scratch of >= 2 x kv_chunk_count + 1 uint32 that the call zeroes on its stream
  * (NULL: one kv_wait / kv_unpack / kv_signal launch triple per chunk instead).
+ * kv_stage enqueues a kv_wait / kv_pack / kv_signal triple per chunk.  With the
+ * environment variable KVX_STAGE_PERSISTENT=1 (opt-in: measured no faster),
+ * one destination (n_dst = 1), static scales, head_dim innermost with 16-B aligned pool and
+ * slots, a 2- / 4-byte source and a wire no wider, it is ONE persistent launch
+ * (k_stage_rows): warps take pack items chunk after chunk, wait in-kernel for the chunk's
+ * slot to be free, and the warp completing a chunk release-stores the ready word, in chunk
+ * order; its counters are stream-ordered scratch (cudaMallocAsync / cudaFreeAsync on
+ * `stream`).
  * kv_stage with peer_scales != NULL computes dynamic fp8 scales (NEXT-1 i, kv_compute_scales
  * semantics) chunk by chunk from the P rank's data, for the D heads this P rank holds, into
  * dst[i]'s own scale array (writable DEVICE memory on P's GPU; the pack quantises with it)
@@ -413,7 +422,13 @@ kv_status kv_recv_pipelined(kv_comm* comm, int32_t n_src, const kv_layout* const
  * several batches keeps one such [L][2][H/tp_d] array per batch (with its requests), not one
  * per pool, and a new batch's array must not be one D still decodes an older batch with.
  * Requires a non-fp8 source and fp8 destinations; NULL: dst[i]'s static scales are used.
- * The caller advances seq0 by the number of chunks per call.  All three validate before
+ * Chunks (A10, P:289 by-layer transmission): |layer_chunk| layers each (0: the whole
+ * range), the last one partial.  layer_chunk < 0 asks for a ramp: when the range holds >= 2
+ * chunks and |layer_chunk| >= 4, the first three chunks take |layer_chunk|/8, /4, /2 layers
+ * (>= 1), so D's first read waits only for a small pack (the pipeline fill; measured slower
+ * on the c4 pair, where each extra chunk costs more than the fill it saves: DESIGN.md §5).  Both sides must
+ * pass the same range and layer_chunk; kv_chunk_count gives the number of chunks, and the
+ * caller advances seq0 by it per call.  All three validate before
  * enqueueing; a wait that times out sets *err = 1 (device int32 on the waiting GPU) and the
  * stream goes on (the data are then undefined).  P and D may share a GPU (kv_wait); cap the
  * persistent kernel with kv_set_sm_budget there so P's packs find SMs. */
@@ -426,6 +441,9 @@ kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* s
                    uint32_t* const* ready_flags, const uint32_t* const* free_flags, float* const* peer_scales,
                    uint32_t seq0, int32_t layer_begin, int32_t layer_end, int32_t layer_chunk, uint64_t timeout_ns,
                    int32_t* err, kv_stream stream);
+/* Number of chunks kv_stage / kv_pull_staged split [layer_begin, layer_end) into with
+ * this layer_chunk (the ramped schedule above); 0 for an empty range.  Pure host function. */
+int32_t kv_chunk_count(int32_t layer_begin, int32_t layer_end, int32_t layer_chunk);
 kv_status kv_pull_staged(int32_t n_src, const kv_layout* const* src, const void* const* rings, int32_t ring_slots,
                          size_t slot_bytes, const kv_layout* dst, void* dst_pool, const kv_batch* dst_bt,
                          const uint32_t* const* ready_flags, uint32_t* const* free_flags, uint32_t* counters,

@@ -121,6 +121,7 @@ def _load():
         "kv_verify_fill": (st, [p, p, C.POINTER(Batch_t), i32, pp, p, u64, p, p]),
         "kv_verify_check": (st, [p, p, p, C.POINTER(Batch_t), p, u64, C.c_uint8, p, C.c_size_t, p, p]),
         "kv_set_sm_budget": (i32, [i32]),
+        "kv_chunk_count": (i32, [i32, i32, i32]),
         "kv_launch_count_reset": (None, []),
         "kv_last_error": (C.c_char_p, []),
         "kv_last_kernel": (C.c_char_p, []),
@@ -143,7 +144,7 @@ EXPORTS = ("kv_layout_describe", "kv_layout_destroy", "kv_batch_bytes", "kv_bloc
            "kv_comm_init", "kv_comm_destroy", "kv_comm_group_start", "kv_comm_group_end", "kv_send", "kv_recv",
            "kv_recv_unpack", "kv_push", "kv_send_pipelined", "kv_recv_pipelined", "kv_pull", "kv_stage",
            "kv_pull_staged", "kv_ipc_export", "kv_ipc_open", "kv_ipc_close", "kv_peer_enable", "kv_signal", "kv_wait",
-           "kv_launch_count", "kv_preload", "kv_verify_fill", "kv_verify_check", "kv_launch_count_reset", "kv_set_sm_budget", "kv_last_error", "kv_last_kernel", "kv_version")
+           "kv_launch_count", "kv_preload", "kv_verify_fill", "kv_verify_check", "kv_launch_count_reset", "kv_set_sm_budget", "kv_chunk_count", "kv_last_error", "kv_last_kernel", "kv_version")
 
 
 def check(status):

@@ -995,9 +995,13 @@ size_t kv_wire_bytes(const kv_layout* s, const kv_layout* d, int64_t total_token
          (size_t)dtype_bytes(kv_wire_dtype(s, d));
 }
 
-kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_bt, const kv_layout* d, int32_t lb,
-                  int32_t le, void* wire, size_t wire_bytes, kv_stream stream) {
-  NvtxRange nvtx_("kv_pack", lb);
+}  // extern "C"
+
+namespace {
+// kv_pack's validation and argument block (shared with kv_stage's one-launch path): *vec = 8
+// for the row kernel, 1 for the element-wise one; *need = the chunk's wire bytes (0: nothing)
+kv_status pack_args(const kv_layout* s, const void* src_pool, const kv_batch* src_bt, const kv_layout* d, int32_t lb,
+                    int32_t le, const void* wire, size_t wire_bytes, PackArgs* out, int* vec_out, size_t* need_out) {
   if (!s || !d || !src_pool || !wire) return fail(KV_EINVAL, "kv_pack: null argument");
   kv_status st;
   if ((st = same_model(s, d)) != KV_OK) return st;
@@ -1011,15 +1015,17 @@ kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_
   const size_t need = kv_wire_bytes(s, d, src_bt->total_tokens, lb, le);
   if (wire_bytes < need)
     return fail(KV_ESHAPE, "kv_pack: wire buffer " + std::to_string(wire_bytes) + " < " + std::to_string(need));
+  *need_out = need;
   if (need == 0) return KV_OK;
   if (src_bt->n_req > 0 && !src_bt->tok_req) return fail(KV_EINVAL, "kv_pack: src_bt has no token map");
-  PackArgs a;
+  PackArgs& a = *out;
   memset(&a, 0, sizeof(a));
   if ((st = kv_pair(s, d, &a.kv1, &a.c0)) != KV_OK) return st;
   a.s_dk = s->dk;
   const int vec = (fast_ok(s) && ptr_aligned(src_pool, 16) && ptr_aligned(wire, 16)) ? 8 : 1;
+  *vec_out = vec;
   a.src = static_cast<const uint8_t*>(src_pool);
-  a.wire = static_cast<uint8_t*>(wire);
+  a.wire = static_cast<uint8_t*>(const_cast<void*>(wire));
   a.sscale = s->d.scales;
   a.dscale = d->d.scales;
   for (int ax = 0; ax < 6; ++ax) a.ss[ax] = s->stride[ax];
@@ -1048,6 +1054,20 @@ kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_
   if (total > kMaxChunks) return fail(KV_EUNSUPPORTED, "kv_pack: more than 2^31 chunks in one call; split layers");
   a.total = (uint32_t)total;
   a.f_l = make_fastdiv((uint32_t)a.Lc);
+  return KV_OK;
+}
+}  // namespace
+
+extern "C" {
+
+kv_status kv_pack(const kv_layout* s, const void* src_pool, const kv_batch* src_bt, const kv_layout* d, int32_t lb,
+                  int32_t le, void* wire, size_t wire_bytes, kv_stream stream) {
+  NvtxRange nvtx_("kv_pack", lb);
+  PackArgs a;
+  int vec = 1;
+  size_t need = 0;
+  kv_status st = pack_args(s, src_pool, src_bt, d, lb, le, wire, wire_bytes, &a, &vec, &need);
+  if (st != KV_OK || need == 0) return st;
   t_last_kernel = vec == 8 ? "k_pack_rows" : "k_pack";
   cudaError_t e = launch_pack(a, vec, s->d.dtype, kv_wire_dtype(s, d), (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kv_pack: launch");
@@ -1124,8 +1144,9 @@ namespace kvx {
 // source overlaps the destination in the same number of heads.  Otherwise *used = false.
 kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void* const* rings, int32_t R,
                          const kv_layout* d, void* dst_pool, const kv_batch* dst_bt, const uint32_t* const* ready,
-                         uint32_t* const* freef, uint32_t* counters, uint32_t seq0, int32_t lb, int32_t le,
-                         int32_t step, uint64_t timeout_ns, int32_t* err, kv_stream stream, bool* used) {
+                         uint32_t* const* freef, uint32_t* counters, uint32_t seq0, const ChunkPlan& plan,
+                         uint64_t timeout_ns, int32_t* err, kv_stream stream, bool* used) {
+  const int32_t lb = plan.lb, le = plan.le, step = plan.step;
   *used = false;
   if (!counters || n_src > KVX_MAX_RANKS || R > KVX_MAX_RING || !fast_ok(d) || !ptr_aligned(dst_pool, 16)) return KV_OK;
   if (getenv("KVX_PULL_CHUNKED")) return KV_OK;  // A/B switch: per-chunk launches
@@ -1162,7 +1183,14 @@ kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void*
   a.lb = lb;
   a.le = le;
   a.step = step;
-  a.nchunks = (le - lb + step - 1) / step;
+  a.nchunks = plan.n;
+  a.nramp = plan.nramp;
+  a.rsum = plan.rsum;
+  for (int32_t k = 0; k < plan.nramp; ++k) {
+    int32_t l0, l1;
+    plan.bounds(k, &l0, &l1);
+    a.ramp_l0[k] = l0;
+  }
   a.q = d->d.tp_rank;
   a.nh = nh;
   a.d_l0 = d->d.first_layer;
@@ -1183,6 +1211,89 @@ kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void*
   t_last_kernel = "k_pull_rows";
   cudaError_t e = launch_pull_rows(a, d->d.dtype, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "kv_pull_staged: launch");
+  *used = true;
+  return KV_OK;
+}
+
+// kv_stage's one-launch path (k_stage_rows, opt-in): one destination rank, no dynamic scales, the
+// row machinery (head_dim innermost, 16-B aligned pool and ring slots), a 2- / 4-byte source
+// and a narrower-or-equal wire.  The counters live in stream-ordered scratch (freed on the
+// stream after the launch).  Otherwise *used = false and kv_stage enqueues per chunk.
+kv_status stage_rows_fast(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, const kv_layout* dst,
+                          void* const* rings, int32_t R, size_t slot_bytes, uint32_t* ready, const uint32_t* freef,
+                          uint32_t seq0, const ChunkPlan& plan, uint64_t timeout_ns, int32_t* err, kv_stream stream,
+                          bool* used) {
+  *used = false;
+  // opt-in (KVX_STAGE_PERSISTENT=1): on the c4 pair it measured no faster than the per-chunk
+  // launches (batch-1: 0.261 vs 0.248 ms; full batch: equal), DESIGN.md §5
+  const char* on = getenv("KVX_STAGE_PERSISTENT");
+  if (!on || !*on || *on == '0' || R > KVX_MAX_RING || plan.n <= 0) return KV_OK;
+  const int32_t wdt = kv_wire_dtype(src, dst), sdt = src->d.dtype;
+  if (!(sdt == KV_F32 || sdt == KV_F16 || sdt == KV_BF16) || wdt == KV_F32 || dtype_bytes(wdt) > dtype_bytes(sdt))
+    return KV_OK;
+  StageArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int b = 0; b < R; ++b) {
+    if (!ptr_aligned(rings[b], 16)) return KV_OK;
+    a.ring[b] = static_cast<uint8_t*>(rings[b]);
+  }
+  int vec = 1;
+  size_t need = 0;
+  int32_t l0, l1;
+  plan.bounds(0, &l0, &l1);  // validates the pair and builds the pack block (lb / wire per chunk in-kernel)
+  kv_status st = pack_args(src, src_pool, src_bt, dst, l0, l1, rings[0], slot_bytes, &a.p, &vec, &need);
+  if (st != KV_OK) return st;
+  if (vec != 8 || need == 0) return KV_OK;
+  {  // the last chunk too (chunks are contiguous: first and last in range = all in range)
+    PackArgs last;
+    int v2 = 1;
+    size_t n2 = 0;
+    plan.bounds(plan.n - 1, &l0, &l1);
+    if ((st = pack_args(src, src_pool, src_bt, dst, l0, l1, rings[0], slot_bytes, &last, &v2, &n2)) != KV_OK) return st;
+  }
+  const uint64_t per_layer = (uint64_t)(a.p.kv1 ? 1 : 2) * a.p.nh * (((uint64_t)src_bt->total_tokens + 31) / 32);
+  if (per_layer * (uint64_t)plan.step > kMaxChunks) return KV_OK;
+  a.ready = ready;
+  a.freef = freef;
+  a.err = err;
+  a.timeout_ns = timeout_ns;
+  a.spin_ns = 128u;
+  a.seq0 = seq0;
+  a.R = R;
+  a.nchunks = plan.n;
+  a.lb = plan.lb;
+  a.le = plan.le;
+  a.step = plan.step;
+  a.nramp = plan.nramp;
+  a.rsum = plan.rsum;
+  for (int32_t k = 0; k < plan.nramp; ++k) {
+    plan.bounds(k, &l0, &l1);
+    a.ramp_l0[k] = l0;
+    a.ramp_nl[k] = l1 - l0;
+  }
+  if (kv_status pst = ensure_preloaded(); pst != KV_OK) return pst;
+  {  // keep freed scratch in the device's default pool across synchronizations (the default
+     // release threshold 0 would hand it back to the driver at every sync)
+    static std::atomic<uint64_t> pooled{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !(pooled.load() & (1ull << dev))) {
+      cudaMemPool_t pool;
+      uint64_t thr = 64ull << 20;
+      if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess)
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      pooled.fetch_or(1ull << dev);
+    }
+  }
+  void* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, (2 * (size_t)plan.n + 1) * sizeof(uint32_t), (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_stage: counters");
+  a.counters = static_cast<uint32_t*>(scratch);
+  t_last_kernel = "k_stage_rows";
+  e = launch_stage_rows(a, sdt, wdt, (cudaStream_t)stream);
+  cudaError_t e2 = cudaFreeAsync(scratch, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "kv_stage: launch");
+  if (e2 != cudaSuccess) return cuda_fail(e2, "kv_stage: counters");
   *used = true;
   return KV_OK;
 }

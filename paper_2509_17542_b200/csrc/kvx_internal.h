@@ -183,6 +183,7 @@ struct UnpackArgs {
 // out of a chunk releases its ring slots.  Item (chunk-relative) =
 // ((((dst block, local layer), K/V), sub-tile), source).  Same dtype on wire and pool.
 #define KVX_MAX_RING 8
+constexpr int kMaxRampArgs = 3;  // ramp chunks of ChunkPlan (below)
 struct PullArgs {
   int32_t kv1, c0;  // K-only / V-only transfer (reading 27)
   uint8_t* dst;
@@ -207,6 +208,30 @@ struct PullArgs {
   int32_t slot_inner, cpr_shift, ts_log2;
   uint32_t n_blk;                   // dst blocks of the batch
   uint32_t items_full, items_last;  // items per chunk (all sources), set by the launcher
+  // ramp chunks (ChunkPlan): chunk k < nramp covers layers [ramp_l0[k], ramp_l0[k] + nl);
+  // chunk k >= nramp starts at lb + rsum + (k - nramp) * step
+  int32_t nramp, rsum;
+  int32_t ramp_l0[kMaxRampArgs];
+  uint32_t ramp_items[kMaxRampArgs];
+  FastDiv f_l_ramp[kMaxRampArgs];
+};
+
+// kv_stage's one-launch path (k_stage_rows, the P-side mirror of k_pull_rows): warps take
+// pack items chunk after chunk from a shared counter, wait in-kernel for the chunk's ring
+// slot to be free, and the warp completing chunk k release-stores the ready word (in chunk
+// order) -- no per-chunk wait / pack / signal launch triple.
+struct StageArgs {
+  PackArgs p;                      // the pack of one destination; lb / wire set per chunk in-kernel
+  uint8_t* ring[KVX_MAX_RING];     // [slot] on this GPU
+  uint32_t* ready;                 // peer word on D (D waits ready >= seq + 1)
+  const uint32_t* freef;           // local word D writes (slot of chunk seq free: free >= seq + 1 - R)
+  uint32_t* counters;              // [2 * nchunks] handed out / done, then the watermark; zero on entry
+  int32_t* err;
+  uint64_t timeout_ns;
+  uint32_t spin_ns, seq0;
+  int32_t R, nchunks, lb, le, step, nramp, rsum;
+  int32_t ramp_l0[kMaxRampArgs], ramp_nl[kMaxRampArgs];
+  uint32_t items_per_layer;
 };
 
 struct AmaxArgs {
@@ -235,14 +260,43 @@ struct AmaxArgs {
   uint32_t n_row_items;
 };
 
+// A10 chunk schedule of kv_stage / kv_pull_staged over [lb, le): |layer_chunk|-layer chunks
+// (0: one chunk), the last one partial; layer_chunk < 0 with |layer_chunk| >= 4 and a range
+// of at least two chunks: the first chunks ramp up (step/8, step/4, step/2 layers) so D's
+// first NVLink read waits only for a small pack (the pipeline fill).  Both sides and the
+// persistent pull kernel enumerate chunks through this one plan.
+constexpr int kMaxRamp = kMaxRampArgs;
+struct ChunkPlan {
+  int32_t lb = 0, le = 0, step = 1, nramp = 0, rsum = 0, n = 0;
+  int32_t ramp[kMaxRamp] = {0, 0, 0};
+  void bounds(int32_t k, int32_t* l0, int32_t* l1) const {
+    if (k < nramp) {
+      int32_t s = lb;
+      for (int32_t i = 0; i < k; ++i) s += ramp[i];
+      *l0 = s;
+      *l1 = s + ramp[k];
+      return;
+    }
+    *l0 = lb + rsum + (k - nramp) * step;
+    *l1 = *l0 + step < le ? *l0 + step : le;
+  }
+};
+ChunkPlan chunk_plan(int32_t lb, int32_t le, int32_t layer_chunk);
+
 // launchers (kvx_kernels.cu); vec = 8 (fast path, DIM innermost) or 1 (generic)
 // kvx_api.cpp: kv_pull_staged's one-launch path (sets *used when it took it)
 kv_status pull_rows_fast(int32_t n_src, const kv_layout* const* src, const void* const* rings, int32_t R,
                          const kv_layout* d, void* dst_pool, const kv_batch* dst_bt, const uint32_t* const* ready,
-                         uint32_t* const* freef, uint32_t* counters, uint32_t seq0, int32_t lb, int32_t le,
-                         int32_t step, uint64_t timeout_ns, int32_t* err, kv_stream stream, bool* used);
+                         uint32_t* const* freef, uint32_t* counters, uint32_t seq0, const ChunkPlan& plan,
+                         uint64_t timeout_ns, int32_t* err, kv_stream stream, bool* used);
 // dt: the (common) wire / pool dtype; vec-8 row machinery only
 cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s);
+cudaError_t launch_stage_rows(StageArgs& a, int sdt, int wdt, cudaStream_t s);
+// kvx_api.cpp: kv_stage's one-launch path (sets *used when it took it)
+kv_status stage_rows_fast(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, const kv_layout* dst,
+                          void* const* rings, int32_t R, size_t slot_bytes, uint32_t* ready, const uint32_t* freef,
+                          uint32_t seq0, const ChunkPlan& plan, uint64_t timeout_ns, int32_t* err, kv_stream stream,
+                          bool* used);
 cudaError_t launch_amax(const AmaxArgs& a, int sdt, float* out_scales, cudaStream_t s);
 cudaError_t preload_kernels();         // every data-path kernel (kvx_kernels.cu)
 cudaError_t preload_verify_kernels();  // K6 (kvx_verify.cu)

@@ -1431,47 +1431,54 @@ __global__ void __launch_bounds__(kTr8Threads, W16 ? 2 : 1) k_convert_tr8(const 
 // tokens of one (layer, K/V, overlap head): the wire side is one contiguous 32-row run,
 // each lane gathers its token's row through the block table.
 // ------------------------------------------------------------------------------------
+// one pack item (32 consecutive tokens of one (layer lb + l, K/V, overlap head)) of the
+// chunk whose wire starts at `wire` (k_pack_rows: the launch's layer range; k_stage_rows:
+// one ring chunk)
+template <int SDT, int WDT, int U>
+__device__ __forceinline__ void pack_item(const PackArgs& a, uint32_t item, int64_t lb, uint8_t* wire, uint32_t lane,
+                                          uint32_t cs) {
+  const uint32_t T_all = a.f_tok.d;
+  uint32_t n = item;
+  const uint32_t tg = divmod(n, a.f_tg);
+  const uint32_t hh = divmod(n, a.f_nh);
+  const uint32_t c = take_kv(n, a.kv1, a.c0);
+  const uint32_t l = n;
+  const int64_t layer = lb + (int64_t)l;
+  const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
+  const uint32_t tok = tg * 32u + lane;
+  uint64_t sp = 0, dp = 0;
+  float rsc = 1.f, rsc2 = 1.f;
+  uint32_t rz = 2;
+  if (tok < T_all) {
+    rz = 0;
+    const int32_t r = __ldg(a.tok_req + tok);
+    uint32_t t = tok - (uint32_t)__ldg(a.tok_off + r);
+    const uint32_t sslot = divmod(t, a.f_bp);
+    const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + t);
+    const uint32_t h = (uint32_t)a.hb + hh;
+    const uint32_t hp = h - (uint32_t)a.p * (uint32_t)a.Hp;
+    sp = (uint64_t)(a.src + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
+                             (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
+    dp = (uint64_t)(wire + ((((uint64_t)l * wkv(a.kv1) + (c - (uint32_t)a.c0)) * (uint64_t)a.nh + hh) * T_all + tok) * (uint64_t)a.D * Tr<WDT>::B);
+    const float ds_inv = is_fp8(WDT) && SDT != WDT
+                             ? __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)))
+                             : 1.f;
+    if constexpr (is_fp8(SDT) && SDT != WDT) rsc = __ldg(a.sscale + (sl * 2 + c) * a.Hp + hp);
+    if constexpr (dual_scale(SDT, WDT))
+      rsc2 = ds_inv;
+    else if constexpr (is_fp8(WDT) && SDT != WDT)
+      rsc = ds_inv;
+  }
+  stream_rows<SDT, WDT, U>(lane, cs, sp, dp, rsc, rz, rsc2);
+}
+
 template <int SDT, int WDT, int U>
 __global__ void __launch_bounds__(kThreads) k_pack_rows(const __grid_constant__ PackArgs a) {
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = (blockIdx.x * (uint32_t)kThreads + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * (uint32_t)kThreads) >> 5;
   const uint32_t cs = (uint32_t)a.cpr_shift;
-  const uint32_t T_all = a.f_tok.d;
-  for (uint32_t item = warp; item < a.n_items; item += nwarps) {
-    uint32_t n = item;
-    const uint32_t tg = divmod(n, a.f_tg);
-    const uint32_t hh = divmod(n, a.f_nh);
-    const uint32_t c = take_kv(n, a.kv1, a.c0);
-    const uint32_t l = n;
-    const int64_t layer = a.lb + (int64_t)l;
-    const int64_t sl = layer - a.s_l0, dl = layer - a.d_l0;  // pool-local layers
-    const uint32_t tok = tg * 32u + lane;
-    uint64_t sp = 0, dp = 0;
-    float rsc = 1.f, rsc2 = 1.f;
-    uint32_t rz = 2;
-    if (tok < T_all) {
-      rz = 0;
-      const int32_t r = __ldg(a.tok_req + tok);
-      uint32_t t = tok - (uint32_t)__ldg(a.tok_off + r);
-      const uint32_t sslot = divmod(t, a.f_bp);
-      const int64_t sblk = __ldg(a.s_blk_ids + __ldg(a.s_blk_off + r) + t);
-      const uint32_t h = (uint32_t)a.hb + hh;
-      const uint32_t hp = h - (uint32_t)a.p * (uint32_t)a.Hp;
-      sp = (uint64_t)(a.src + (sl * a.ss[KV_AX_LAYER] + (int64_t)c * a.ss[KV_AX_KV] + sblk * a.ss[KV_AX_BLOCK] +
-                               (int64_t)sslot * a.ss[KV_AX_SLOT] + (int64_t)hp * a.ss[KV_AX_HEAD]) * Tr<SDT>::B);
-      dp = (uint64_t)(a.wire + ((((uint64_t)l * wkv(a.kv1) + (c - (uint32_t)a.c0)) * (uint64_t)a.nh + hh) * T_all + tok) * (uint64_t)a.D * Tr<WDT>::B);
-      const float ds_inv = is_fp8(WDT) && SDT != WDT
-                               ? __frcp_rn(__ldg(a.dscale + (dl * 2 + c) * a.Hd + (h - (uint32_t)a.q * (uint32_t)a.Hd)))
-                               : 1.f;
-      if constexpr (is_fp8(SDT) && SDT != WDT) rsc = __ldg(a.sscale + (sl * 2 + c) * a.Hp + hp);
-      if constexpr (dual_scale(SDT, WDT))
-        rsc2 = ds_inv;
-      else if constexpr (is_fp8(WDT) && SDT != WDT)
-        rsc = ds_inv;
-    }
-    stream_rows<SDT, WDT, U>(lane, cs, sp, dp, rsc, rz, rsc2);
-  }
+  for (uint32_t item = warp; item < a.n_items; item += nwarps) pack_item<SDT, WDT, U>(a, item, a.lb, a.wire, lane, cs);
 }
 
 // ------------------------------------------------------------------------------------
@@ -2177,11 +2184,12 @@ __global__ void __launch_bounds__(kThreads) k_pull_rows(const __grid_constant__ 
   uint32_t* next = a.counters;               // [nchunks] items handed out
   uint32_t* done = a.counters + a.nchunks;   // [nchunks] items finished
   for (int32_t k = 0; k < a.nchunks; ++k) {
-    const bool last = k == a.nchunks - 1;
-    const uint32_t n_k = last ? a.items_last : a.items_full;
-    const FastDiv& f_l = last ? a.f_l_last : a.f_l_full;
+    // chunk k of the ChunkPlan: a ramp chunk, or a step-layer chunk (the last one partial)
+    const bool ramp = k < a.nramp, last = k == a.nchunks - 1;
+    const uint32_t n_k = ramp ? a.ramp_items[k] : last ? a.items_last : a.items_full;
+    const FastDiv& f_l = ramp ? a.f_l_ramp[k] : last ? a.f_l_last : a.f_l_full;
     const uint32_t slot_idx = (a.seq0 + (uint32_t)k) % (uint32_t)a.R;
-    const int64_t l0 = (int64_t)a.lb + (int64_t)k * a.step;
+    const int64_t l0 = ramp ? (int64_t)a.ramp_l0[k] : (int64_t)a.lb + a.rsum + (int64_t)(k - a.nramp) * a.step;
     bool waited = false;
     while (true) {
       // dynamic hand-out: every warp leaves chunk k within one grab of the others, so the
@@ -2249,6 +2257,97 @@ __global__ void __launch_bounds__(kThreads) k_pull_rows(const __grid_constant__ 
             asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.freef[s]), "r"(a.seq0 + (uint32_t)k + 1u)
                          : "memory");
           asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a.watermark), "r"((uint32_t)k + 1u) : "memory");
+        }
+      }
+    }
+  }
+}
+
+// kv_stage's one-launch path: the P side of the staged pull as ONE persistent launch.
+// Chunk k (ChunkPlan order, layers [l0, l0 + nl)) is packed into ring slot (seq0 + k) % R
+// once D freed it; the warp that completes chunk k release-stores ready = seq0 + k + 1 into
+// D's word, strictly in chunk order (D reads ready >= v as "every chunk below v is packed").
+// A warp waits for a slot only holding items it grabbed from that chunk, and the chunk R
+// earlier is held by warps already past their wait (resident), so no co-residency is needed.
+template <int SDT, int WDT, int U>
+__global__ void __launch_bounds__(kThreads) k_stage_rows(const __grid_constant__ StageArgs a) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t cs = (uint32_t)a.p.cpr_shift;
+  uint32_t* next = a.counters;               // [nchunks] items handed out
+  uint32_t* done = a.counters + a.nchunks;   // [nchunks] items finished
+  uint32_t* watermark = a.counters + 2 * a.nchunks;
+  // free-slot waits: P runs ahead of the link, so its warps would spend most of the launch
+  // polling D's free word -- one warp per CTA polls global memory at a time (smem token),
+  // the others read the CTA's cached value (an acquire by the poller, re-released at CTA
+  // scope), keeping the polls off the L2 slice D's NVLink reads also go through
+  __shared__ uint32_t s_free, s_token;
+  if (threadIdx.x == 0) {
+    s_free = a.seq0 >= (1u << 30) ? a.seq0 - (1u << 30) : 0u;  // below any value waited for
+    s_token = 0;
+  }
+  __syncthreads();
+  for (int32_t k = 0; k < a.nchunks; ++k) {
+    int32_t l0, nl;
+    if (k < a.nramp) {
+      l0 = a.ramp_l0[k];
+      nl = a.ramp_nl[k];
+    } else {
+      l0 = a.lb + a.rsum + (k - a.nramp) * a.step;
+      nl = min(a.step, a.le - l0);
+    }
+    const uint32_t n_k = (uint32_t)nl * a.items_per_layer;
+    const uint32_t seq = a.seq0 + (uint32_t)k;
+    uint8_t* wire = a.ring[seq % (uint32_t)a.R];
+    bool waited = false;
+    while (true) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(next + k, kPullGrab);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= n_k) break;
+      if (!waited) {  // the slot last held chunk seq - R: D must have read it
+        if (lane == 0 && (uint64_t)a.seq0 + (uint64_t)k + 1u > (uint64_t)a.R) {
+          const uint32_t need = seq + 1u - (uint32_t)a.R;
+          const uint64_t t0 = globaltimer_ns();
+          while (true) {
+            uint32_t v;
+            asm volatile("ld.acquire.cta.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(&s_free)) : "memory");
+            if ((int32_t)(v - need) >= 0) break;
+            if (atomicCAS(&s_token, 0u, 1u) == 0u) {
+              // every value stored is a read of the (monotone) global word, so s_free never
+              // exceeds it; the release passes this acquire on to the CTA's readers
+              uint32_t x;
+              asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(x) : "l"(a.freef) : "memory");
+              if ((int32_t)(x - v) > 0)
+                asm volatile("st.release.cta.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_free)), "r"(x) : "memory");
+              atomicExch(&s_token, 0u);
+              if ((int32_t)(x - need) >= 0) break;
+            }
+            if (globaltimer_ns() - t0 > a.timeout_ns) {
+              *a.err = 1;
+              break;
+            }
+            __nanosleep(a.spin_ns);
+          }
+        }
+        __syncwarp();
+        waited = true;
+      }
+      const uint32_t end = min(n_k, base + kPullGrab);
+      for (uint32_t item = base; item < end; ++item) pack_item<SDT, WDT, U>(a.p, item, l0, wire, lane, cs);
+      __syncwarp();
+      if (lane == 0) {
+        __threadfence();
+        const uint32_t cnt = end - base;
+        if (atomicAdd(done + k, cnt) + cnt == n_k) {
+          uint32_t wm;
+          while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(wm) : "l"(watermark) : "memory");
+            if (wm == (uint32_t)k) break;
+            __nanosleep(64);
+          }
+          __threadfence_system();
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(a.ready), "r"(seq + 1u) : "memory");
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(watermark), "r"((uint32_t)k + 1u) : "memory");
         }
       }
     }
@@ -2978,7 +3077,12 @@ cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s) {
   a.f_sb = make_fastdiv(nsb);
   a.f_items = make_fastdiv(nsb * nhb);
   const uint32_t per_layer = a.f_src.d * (a.kv1 ? 1u : 2u) * nsb * nhb * a.n_blk;
-  const uint32_t nl_last = (uint32_t)(a.le - a.lb - (a.nchunks - 1) * a.step);
+  for (int32_t k = 0; k < a.nramp; ++k) {  // ramp chunks (ChunkPlan)
+    const int32_t l1 = k + 1 < a.nramp ? a.ramp_l0[k + 1] : a.lb + a.rsum;
+    a.ramp_items[k] = per_layer * (uint32_t)(l1 - a.ramp_l0[k]);
+    a.f_l_ramp[k] = make_fastdiv((uint32_t)(l1 - a.ramp_l0[k]));
+  }
+  const uint32_t nl_last = (uint32_t)(a.le - (a.lb + a.rsum + (a.nchunks - a.nramp - 1) * a.step));
   a.items_last = per_layer * nl_last;
   a.items_full = per_layer * (uint32_t)a.step;
   a.f_l_full = make_fastdiv((uint32_t)a.step);
@@ -2989,6 +3093,47 @@ cudaError_t launch_pull_rows(PullArgs& a, int dt, cudaStream_t s) {
     case KV_F8E4M3: return pull_rows_t<KV_F8E4M3>(a, s);
     case KV_F8E4M3FNUZ: return pull_rows_t<KV_F8E4M3FNUZ>(a, s);
     case KV_F32: return pull_rows_t<KV_F32>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+namespace {
+template <int SDT, int WDT>
+cudaError_t stage_rows_t(StageArgs& a, cudaStream_t s) {
+  constexpr int U = unroll_for<SDT, 8>();
+  auto k = k_stage_rows<SDT, WDT, U>;
+  PackArgs& p = a.p;
+  p.cpr_shift = log2_pow2(p.f_dch.d);
+  const uint32_t ntg = (p.f_tok.d + 31u) / 32u;
+  p.f_tg = make_fastdiv(ntg);
+  a.items_per_layer = (p.kv1 ? 1u : 2u) * (uint32_t)p.nh * ntg;
+  // P only has to out-run the link (it reads 2x and writes 1x the wire bytes): two CTAs
+  // per SM keep ~2x the link's rate in flight with fewer spinning warps
+  const int grid = std::min(grid_for_items(k, (uint64_t)a.items_per_layer * (uint64_t)a.step), 2 * num_sms());
+  k<<<grid, kThreads, 0, s>>>(a);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaGetLastError();
+}
+template <int SDT>
+cudaError_t stage_rows_w(StageArgs& a, int wdt, cudaStream_t s) {
+  switch (wdt) {
+    case KV_F16: return stage_rows_t<SDT, KV_F16>(a, s);
+    case KV_BF16: return stage_rows_t<SDT, KV_BF16>(a, s);
+    case KV_F8E4M3: return stage_rows_t<SDT, KV_F8E4M3>(a, s);
+    case KV_F8E4M3FNUZ: return stage_rows_t<SDT, KV_F8E4M3FNUZ>(a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+}  // namespace
+
+cudaError_t launch_stage_rows(StageArgs& a, int sdt, int wdt, cudaStream_t s) {
+  if (a.nchunks <= 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(a.counters, 0, (2 * (size_t)a.nchunks + 1) * sizeof(uint32_t), s);
+  if (e != cudaSuccess) return e;
+  switch (sdt) {  // narrowing casts (the staged pull's reason): 4- / 2-byte sources
+    case KV_F32: return stage_rows_w<KV_F32>(a, wdt, s);
+    case KV_F16: return stage_rows_w<KV_F16>(a, wdt, s);
+    case KV_BF16: return stage_rows_w<KV_BF16>(a, wdt, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -3143,6 +3288,7 @@ cudaError_t preload_pair() {
   KVX_TOUCH(k_convert_tr8<SDT, DDT, false>);
   if constexpr (Tr<SDT>::B == 2 && Tr<DDT>::B == 2) KVX_TOUCH(k_convert_tr8<SDT, DDT, true>);
   KVX_TOUCH(k_pack_rows<SDT, DDT, U8>);
+  if constexpr (Tr<SDT>::B >= 2 && DDT != KV_F32) KVX_TOUCH(k_stage_rows<SDT, DDT, U8>);
   KVX_TOUCH(k_pack<1, SDT, DDT, U1>);
   KVX_TOUCH(k_unpack_rows<SDT, DDT, U8>);
   KVX_TOUCH(k_unpack<1, SDT, DDT, U1>);

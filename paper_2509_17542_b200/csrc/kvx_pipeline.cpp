@@ -63,6 +63,26 @@ kv_status join(cudaStream_t stream, cudaEvent_t ea, cudaEvent_t eb, cudaStream_t
 
 }  // namespace
 
+namespace kvx {
+ChunkPlan chunk_plan(int32_t lb, int32_t le, int32_t layer_chunk) {
+  ChunkPlan p;
+  p.lb = lb;
+  p.le = le;
+  const int32_t mag = layer_chunk < 0 ? -layer_chunk : layer_chunk;
+  p.step = mag > 0 ? mag : std::max(1, le - lb);
+  if (layer_chunk < 0 && p.step >= 4 && le - lb >= 2 * p.step) {
+    p.nramp = kMaxRamp;
+    for (int i = 0; i < kMaxRamp; ++i) {  // step/8, step/4, step/2 (>= 1 layer each)
+      p.ramp[i] = std::max(1, p.step >> (kMaxRamp - i));
+      p.rsum += p.ramp[i];
+    }
+  }
+  const int32_t rest = std::max(0, le - lb - p.rsum);
+  p.n = p.nramp + (rest + p.step - 1) / p.step;
+  return p;
+}
+}  // namespace kvx
+
 extern "C" {
 
 kv_status kv_push(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, int32_t n_dst,
@@ -209,6 +229,11 @@ namespace {
 inline int32_t ring_slot(uint64_t seq, int32_t R) { return (int32_t)(seq % (uint64_t)R); }
 }  // namespace
 
+int32_t kv_chunk_count(int32_t layer_begin, int32_t layer_end, int32_t layer_chunk) {
+  if (layer_end <= layer_begin) return 0;
+  return chunk_plan(layer_begin, layer_end, layer_chunk).n;
+}
+
 kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* src_bt, int32_t n_dst,
                    const kv_layout* const* dst, void* const* rings, int32_t ring_slots, size_t slot_bytes,
                    uint32_t* const* ready_flags, const uint32_t* const* free_flags, float* const* peer_scales,
@@ -221,11 +246,14 @@ kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* s
     for (int b = 0; b < ring_slots; ++b)
       if (!rings[(size_t)i * ring_slots + b]) return fail(KV_EINVAL, "kv_stage: null ring slot");
   }
-  const int32_t step = layer_chunk > 0 ? layer_chunk : std::max(1, le - lb);
-  for (int32_t l0 = lb; l0 < le; l0 += step)
+  const ChunkPlan plan = chunk_plan(lb, le, layer_chunk);
+  for (int32_t k = 0; k < plan.n; ++k) {
+    int32_t l0, l1;
+    plan.bounds(k, &l0, &l1);
     for (int i = 0; i < n_dst; ++i)
-      if (kv_wire_bytes(src, dst[i], src_bt->total_tokens, l0, std::min(le, l0 + step)) > slot_bytes)
+      if (kv_wire_bytes(src, dst[i], src_bt->total_tokens, l0, l1) > slot_bytes)
         return fail(KV_ESHAPE, "kv_stage: ring slots smaller than a layer chunk");
+  }
   kv_status st;
   if (peer_scales) {  // dynamic scales: validate (empty ranges) before the first enqueue
     for (int i = 0; i < n_dst; ++i) {
@@ -239,10 +267,18 @@ kv_status kv_stage(const kv_layout* src, const void* src_pool, const kv_batch* s
         return st;
     }
   }
+  if (n_dst == 1 && !peer_scales) {  // one persistent launch (k_stage_rows) when the row machinery fits
+    bool used = false;
+    st = stage_rows_fast(src, src_pool, src_bt, dst[0], rings, ring_slots, slot_bytes, ready_flags[0], free_flags[0],
+                         seq0, plan, timeout_ns, err, stream, &used);
+    if (st != KV_OK || used) return st;
+  }
   uint64_t seq = seq0;
-  for (int32_t l0 = lb; l0 < le; l0 += step, ++seq) {
+  for (int32_t k = 0; k < plan.n; ++k, ++seq) {
+    int32_t l0, l1;
+    plan.bounds(k, &l0, &l1);
     NvtxRange r("kv_stage chunk", l0);
-    const int32_t l1 = std::min(le, l0 + step), b = ring_slot(seq, ring_slots);
+    const int32_t b = ring_slot(seq, ring_slots);
     for (int i = 0; i < n_dst; ++i) {
       // slot b last held chunk seq - R: the D rank must have released it (free >= seq - R + 1)
       if (seq + 1 > (uint64_t)ring_slots &&
@@ -283,11 +319,14 @@ kv_status kv_pull_staged(int32_t n_src, const kv_layout* const* src, const void*
     for (int b = 0; b < ring_slots; ++b)
       if (!rings[(size_t)i * ring_slots + b]) return fail(KV_EINVAL, "kv_pull_staged: null ring slot");
   }
-  const int32_t step = layer_chunk > 0 ? layer_chunk : std::max(1, le - lb);
-  for (int32_t l0 = lb; l0 < le; l0 += step)
+  const ChunkPlan plan = chunk_plan(lb, le, layer_chunk);
+  for (int32_t k = 0; k < plan.n; ++k) {
+    int32_t l0, l1;
+    plan.bounds(k, &l0, &l1);
     for (int i = 0; i < n_src; ++i)
-      if (kv_wire_bytes(src[i], dst, dst_bt->total_tokens, l0, std::min(le, l0 + step)) > slot_bytes)
+      if (kv_wire_bytes(src[i], dst, dst_bt->total_tokens, l0, l1) > slot_bytes)
         return fail(KV_ESHAPE, "kv_pull_staged: ring slots smaller than a layer chunk");
+  }
   for (int i = 0; i < n_src; ++i) {  // validate the unpacks once (empty ranges)
     kv_status v = kv_unpack(src[i], dst, dst_pool, dst_bt, lb, lb, rings[(size_t)i * ring_slots], slot_bytes, stream);
     if (v != KV_OK) return v;
@@ -297,11 +336,13 @@ kv_status kv_pull_staged(int32_t n_src, const kv_layout* const* src, const void*
   }
   bool used = false;
   kv_status st = pull_rows_fast(n_src, src, rings, ring_slots, dst, dst_pool, dst_bt, ready_flags, free_flags,
-                                counters, seq0, lb, le, step, timeout_ns, err, stream, &used);
+                                counters, seq0, plan, timeout_ns, err, stream, &used);
   if (st != KV_OK || used) return st;
   uint64_t seq = seq0;
-  for (int32_t l0 = lb; l0 < le; l0 += step, ++seq) {
-    const int32_t l1 = std::min(le, l0 + step), b = ring_slot(seq, ring_slots);
+  for (int32_t k = 0; k < plan.n; ++k, ++seq) {
+    int32_t l0, l1;
+    plan.bounds(k, &l0, &l1);
+    const int32_t b = ring_slot(seq, ring_slots);
     for (int i = 0; i < n_src; ++i)
       if ((st = kv_wait(ready_flags[i], (uint32_t)(seq + 1), timeout_ns, err, stream)) != KV_OK) return st;
     for (int i = 0; i < n_src; ++i) {

@@ -324,10 +324,10 @@ def pull_staged(src_layouts, rings, ring_slots, slot_bytes, dst_layout: Layout, 
 
 
 def chunk_count(layer_range, layer_chunk):
-    """Chunks a kv_stage / kv_pull_staged call over layer_range takes (seq0 advances by it)."""
+    """kv_chunk_count: chunks a kv_stage / kv_pull_staged call over layer_range takes (the
+    ramped schedule; seq0 advances by it)."""
     lb, le = layer_range
-    step = layer_chunk if layer_chunk > 0 else max(1, le - lb)
-    return (le - lb + step - 1) // step
+    return int(lib.kv_chunk_count(int(lb), int(le), int(layer_chunk)))
 
 
 def pull_counter_words(layer_range, layer_chunk):

@@ -288,3 +288,22 @@ def test_pull_and_stage_validation_fails_before_enqueue(kvx):
     st = lib.kv_pull_staged(1, arr(s.handle.value), arr(0x70000), 0, need, d.handle, 0x30000, C.byref(db),
                             arr(0x60000), arr(0x50000), None, 0, 0, 2, 1, 10**9, err, None)
     assert st == 1 and "bad argument" in lib.kv_last_error().decode()
+
+
+@pytest.mark.parametrize("lb,le,lc,want", [
+    (0, 80, 20, [(0, 20), (20, 40), (40, 60), (60, 80)]),
+    (0, 80, 0, [(0, 80)]),
+    (0, 80, -20, [(0, 2), (2, 7), (7, 17), (17, 37), (37, 57), (57, 77), (77, 80)]),
+    (0, 80, -4, [(0, 1), (1, 2), (2, 4)] + [(l, l + 4) for l in range(4, 80, 4)]),
+    (10, 40, -20, [(10, 30), (30, 40)]),          # fewer than two chunks: no ramp
+    (0, 80, -3, [(l, min(80, l + 3)) for l in range(0, 80, 3)]),   # |layer_chunk| < 4: no ramp
+    (5, 5, -20, []),
+])
+def test_chunk_count_and_schedule(kvx, lb, le, lc, want):
+    """kv_chunk_count: the A10 chunk schedule of kv_stage / kv_pull_staged -- the
+    chunks tile [lb, le) in order, uniform |layer_chunk| layers after an optional ramp of
+    |layer_chunk|/8, /4, /2 (negative layer_chunk).  Here the expected chunk lists are
+    written out by hand; the count must equal their number."""
+    assert sum(b - a for a, b in want) == le - lb
+    assert all(want[i][1] == want[i + 1][0] for i in range(len(want) - 1))
+    assert kvx.chunk_count((lb, le), lc) == len(want)

@@ -67,7 +67,7 @@ def _p_view_of_d(kvx, case, dyn):
     return out
 
 
-def _run(o1, case, mode, serial_safe=False):
+def _run(o1, case, mode, serial_safe=False, lc=1):
     """serial_safe (the smoke): ring slots for every chunk and P's stages enqueued before D's
     persistent pulls, so the transfer also completes when every kernel runs alone in launch
     order (a profiler's replay, e.g. ncu over smoke()) -- P never waits for a free slot and
@@ -83,7 +83,7 @@ def _run(o1, case, mode, serial_safe=False):
             lay.scales.fill_(-2.0)             # D's scale arrays: written by P (peer stores)
     pairs = kvx.plan_pairs(S[0].tp_degree, D[0].tp_degree, S[0].num_kv_heads)
     L = S[0].num_layers
-    lc = 1
+    nch = kvx.chunk_count((0, L), lc)   # lc < 0: ramped chunk schedule (kv_chunk_count)
     ready = torch.zeros(128, dtype=torch.int32, device="cuda:0")   # D side: [q * 8 + p], P writes
     freew = torch.zeros(128, dtype=torch.int32, device="cuda:0")   # P side: [p * 8 + q], D writes
     err = torch.zeros(1, dtype=torch.int32, device="cuda:0")
@@ -95,10 +95,10 @@ def _run(o1, case, mode, serial_safe=False):
     counters = {}
     torch.cuda.synchronize()
     if mode.startswith("pull_staged"):
-        nb = max(kvx.wire_bytes(S[p], D[q], dc.src_bt.total_tokens, (l, l + 1)) for p, q, _, _ in pairs
+        nb = max(kvx.wire_bytes(S[p], D[q], dc.src_bt.total_tokens, (l, min(L, l + abs(lc)))) for p, q, _, _ in pairs
                  for l in range(L))
         nb = max(16, (nb + 255) // 256 * 256)
-        Rr = L if serial_safe else R
+        Rr = nch if serial_safe else R
         rings = {(p, q): torch.empty(Rr * nb, dtype=torch.uint8, device="cuda:0") for p, q, _, _ in pairs}
         persistent = mode != "pull_staged_chunked"
 
@@ -137,7 +137,7 @@ def _run(o1, case, mode, serial_safe=False):
             qs = [q for p2, q, _, _ in pairs if p2 == p]
             with torch.cuda.stream(p_streams[p]):
                 for q in qs:   # every chunk consumed: P may reuse its ring
-                    kvx.wait(w(freew, p * 8 + q), L, err, TIMEOUT, p_streams[p])
+                    kvx.wait(w(freew, p * 8 + q), nch, err, TIMEOUT, p_streams[p])
     elif mode == "pull":
         prev = kvx.set_sm_budget(BUDGET)
         try:
@@ -175,8 +175,8 @@ def _run(o1, case, mode, serial_safe=False):
     assert int(err.item()) == 0, "a flag wait timed out"
     if counters:   # every chunk handed out, completed and released in order
         for c in counters.values():
-            assert int(c[2 * L].item()) == L, "ring slots not all released"
-            assert bool((c[L:2 * L] > 0).all())
+            assert int(c[2 * nch].item()) == nch, "ring slots not all released"
+            assert bool((c[nch:2 * nch] > 0).all())
     return dc, kernels
 
 
@@ -203,6 +203,35 @@ def test_transport_one_gpu(o1, mode, shape):
         assert "k_pack_rows" in kernels or "k_pack" in kernels, kernels
     want = _scales_and_want(o1, case, dc) if mode == "pull_staged_dyn" else expected(case, o1)
     assert_pools_match(dc.dst_numpy(), want, case["dst_lays"][0]["dtype"])
+
+
+@pytest.mark.parametrize("persistent_p", [False, True])
+@pytest.mark.parametrize("lc", [-4, 4, -8])
+def test_staged_pull_chunk_ramp(o1, lc, persistent_p, monkeypatch):
+    """The ramped chunk schedule (negative layer_chunk: 1, 1, 2 layers, then |lc|) through the
+    persistent pull with a 2-slot ring, against O1 -- both sides and the kernels enumerate
+    the same chunks (A10); P as per-chunk packs or as the opt-in persistent
+    k_stage_rows (KVX_STAGE_PERSISTENT=1, in-kernel free-slot waits and ready release)."""
+    from tests.test_gpu_parity import assert_pools_match
+    if persistent_p:
+        monkeypatch.setenv("KVX_STAGE_PERSISTENT", "1")
+    case = make_case(16, 4, 128, 2, 2, 16, 16, [200, 17, 1], BF16, E4M3, seed=37, o1=o1, scales="pow2")
+    dc, kernels = _run(o1, case, "pull_staged", lc=lc)
+    assert "k_pull_rows" in kernels, kernels
+    assert ("k_stage_rows" if persistent_p else "k_pack_rows") in kernels, kernels
+    assert_pools_match(dc.dst_numpy(), expected(case, o1), case["dst_lays"][0]["dtype"])
+
+
+@pytest.mark.parametrize("shape", ["merge_fp8", "identity_fp8", "merge"])
+def test_staged_pull_persistent_stage(o1, shape, monkeypatch):
+    """kv_stage as one persistent k_stage_rows launch (opt-in) on the one-destination shapes,
+    2-slot ring reused three times, against O1."""
+    from tests.test_gpu_parity import assert_pools_match
+    monkeypatch.setenv("KVX_STAGE_PERSISTENT", "1")
+    case = _case(shape, o1)
+    dc, kernels = _run(o1, case, "pull_staged")
+    assert {"k_pull_rows", "k_stage_rows"} <= kernels, kernels
+    assert_pools_match(dc.dst_numpy(), expected(case, o1), case["dst_lays"][0]["dtype"])
 
 
 def test_smoke_with_serialized_launches():

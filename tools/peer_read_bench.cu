@@ -3,10 +3,12 @@
 //   (b) 1-D bulk TMA (cp.async.bulk G->S from the peer, S->G bulk store locally),
 //   (c) the copy engine (cudaMemcpyAsync).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/peer_read_bench tools/peer_read_bench.cu  (2 GPUs)
+// build/peer_read_bench sizes: isolated single launches at one request's transfer sizes
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>
 #include <vector>
+#include <string>
 #include <algorithm>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s:%d %s\n", __FILE__, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
@@ -67,7 +69,7 @@ __global__ void k_bulk(const uint8_t* __restrict__ src, uint8_t* __restrict__ ds
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
-int main() {
+int main(int argc, char** argv) {
   int nd = 0;
   CK(cudaGetDeviceCount(&nd));
   if (nd < 2) { printf("need 2 GPUs\n"); return 1; }
@@ -99,6 +101,35 @@ int main() {
     std::sort(ts.begin(), ts.end());
     printf("%-36s %8.3f ms  %7.1f GB/s\n", name, ts[ts.size() / 2], N / (ts[ts.size() / 2] * 1e-3) / 1e9);
   };
+  if (argc > 1 && std::string(argv[1]) == "sizes") {
+    // one isolated launch per timing (launch, ramp and tail included) at transfer sizes of one
+    // request: the floor of a single-request pull (c4 pair: 168 MB of fp8 per request)
+    for (size_t n : {(size_t)4 << 20, (size_t)21 << 20, (size_t)42 << 20, (size_t)84 << 20, (size_t)168 << 20,
+                     (size_t)336 << 20}) {
+      std::vector<float> tc, tk;
+      for (int i = 0; i < 12; ++i) {
+        float ms;
+        CK(cudaEventRecord(e0, st));
+        CK(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToDevice, st));
+        CK(cudaEventRecord(e1, st));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (i >= 2) tc.push_back(ms);
+        CK(cudaEventRecord(e0, st));
+        k_ldg<4><<<148 * 4, 256, 0, st>>>((const uint4*)src, (uint4*)dst, n / 16);
+        CK(cudaEventRecord(e1, st));
+        CK(cudaEventSynchronize(e1));
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (i >= 2) tk.push_back(ms);
+      }
+      std::sort(tc.begin(), tc.end());
+      std::sort(tk.begin(), tk.end());
+      const float mc = tc[tc.size() / 2], mk = tk[tk.size() / 2];
+      printf("size %7.1f MB  copy engine %7.4f ms %6.1f GB/s   ldg16 U=4 4 CTA/SM %7.4f ms %6.1f GB/s\n", n / 1048576.0,
+             mc, n / (mc * 1e-3) / 1e9, mk, n / (mk * 1e-3) / 1e9);
+    }
+    return 0;
+  }
   timeit("copy engine cudaMemcpyAsync", [&] { CK(cudaMemcpyAsync(dst, src, N, cudaMemcpyDeviceToDevice, st)); });
   for (int cpsm : {2, 4, 8}) {
     char nm[64];

@@ -5,7 +5,7 @@ layer chunks into a ring, D = cuda:1 unpacks them straight from the peer-mapped 
                   timed (the kernel's own NVLink read rate, no pipeline effects);
   --mode overlap: P and D run concurrently with a ring of --ring slots (the real pipeline).
 Each is run with the persistent one-launch D kernel (counters) and the per-chunk path.
-    python tools/pull_probe.py [--workload c4] [--layer-chunk 8] [--ring 3] [--iters 5]
+    python tools/pull_probe.py [--workload c4] [--layer-chunk 8] [--ring 3] [--iters 5] [--requests 1]
 """
 import argparse
 import json
@@ -29,9 +29,13 @@ def main():
     ap.add_argument("--ring", type=int, default=3)
     ap.add_argument("--iters", type=int, default=5)
     ap.add_argument("--modes", default="d_only,overlap")
+    ap.add_argument("--requests", type=int, default=0, help="first N requests only (1: batch-1 latency)")
     args = ap.parse_args()
     import paper_2509_17542_b200 as kvx
     cfg = synth.configs()[args.workload]
+    if args.requests:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, n_tokens=cfg.n_tokens[:args.requests])
     torch.cuda.set_device(0)
     kvx.peer_enable(1)
     src = Workload(cfg, [0], [], torch.device("cuda", 0))
@@ -46,7 +50,8 @@ def main():
     Sd = kvx.Layout.from_dict(src.src_dicts[0])  # P layout handle for D's calls (no device data)
     L, lc = cfg.L, args.layer_chunk
     nch = kvx.chunk_count((0, L), lc)
-    slot = max(kvx.wire_bytes(S, Dv, cfg.total_tokens, (l0, min(L, l0 + lc))) for l0 in range(0, L, lc))
+    step = abs(lc) or L   # lc < 0: the ramped schedule (its chunks are never larger than |lc|)
+    slot = max(kvx.wire_bytes(S, Dv, cfg.total_tokens, (l0, min(L, l0 + step))) for l0 in range(0, L, step))
     slot = (slot + 255) // 256 * 256
     ready = torch.zeros(8, dtype=torch.int32, device="cuda:1")
     free = torch.zeros(8, dtype=torch.int32, device="cuda:0")
