@@ -20,8 +20,9 @@
 //     tables instead of the arithmetic cast.
 //   * k_convert_tr8 / k_convert_tr (other head_dim-major or x-packed sides): 8 x 8 register
 //     transposes / shared-memory tiles.
-//   * k_pack_rows / k_unpack_rows (Fig. 5 flatten / restore for the NCCL mode), k_pull_rows
-//     (the persistent staged pull), k_amax_rows (dynamic scales), k_signal / k_wait (flags).
+//   * k_pack_rows / k_unpack_rows (Fig. 5 flatten / restore: the NCCL mode and the staged
+//     pull's P side), k_pull_rows (the persistent staged pull, D side), k_stage_rows (the
+//     opt-in persistent P side), k_amax_rows (dynamic scales), k_signal / k_wait (flags).
 //   * VEC=1 k_convert / k_pack / k_unpack: the element-wise generic path for any of the 720
 //     axis orders.
 // Casts (readings 10-13, 24-26): same dtype = bit copy; f16/bf16/f32 narrowing via
