@@ -4,6 +4,7 @@
 //   (c) the copy engine (cudaMemcpyAsync).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/peer_read_bench tools/peer_read_bench.cu  (2 GPUs)
 // build/peer_read_bench sizes: isolated single launches at one request's transfer sizes
+// build/peer_read_bench hybrid: one read split between the copy engine and SM loads, concurrently
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdint>
@@ -101,6 +102,36 @@ int main(int argc, char** argv) {
     std::sort(ts.begin(), ts.end());
     printf("%-36s %8.3f ms  %7.1f GB/s\n", name, ts[ts.size() / 2], N / (ts[ts.size() / 2] * 1e-3) / 1e9);
   };
+  if (argc > 1 && std::string(argv[1]) == "hybrid") {
+    // one peer read of N bytes split between the copy engine (fraction f, its own stream) and
+    // SM loads (the rest) running at the same time: does the CE's protocol add to the SMs'?
+    cudaStream_t st2;
+    CK(cudaStreamCreate(&st2));
+    cudaEvent_t ej;
+    CK(cudaEventCreateWithFlags(&ej, cudaEventDisableTiming));
+    for (double f : {0.0, 0.2, 0.35, 0.5, 0.65, 0.8, 1.0}) {
+      const size_t nce = (size_t)(N * f) / 4096 * 4096, nsm = N - nce;
+      std::vector<float> ts;
+      for (int i = 0; i < 6; ++i) {
+        CK(cudaEventRecord(e0, st));
+        CK(cudaStreamWaitEvent(st2, e0, 0));
+        if (nce) CK(cudaMemcpyAsync(dst, src, nce, cudaMemcpyDeviceToDevice, st2));
+        if (nsm) k_ldg<4><<<148 * 4, 256, 0, st>>>((const uint4*)(src + nce), (uint4*)(dst + nce), nsm / 16);
+        CK(cudaEventRecord(ej, st2));
+        CK(cudaStreamWaitEvent(st, ej, 0));
+        CK(cudaEventRecord(e1, st));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (i) ts.push_back(ms);
+      }
+      std::sort(ts.begin(), ts.end());
+      const float m = ts[ts.size() / 2];
+      printf("hybrid: %3.0f%% by copy engine + %3.0f%% by SM loads  %7.3f ms  %6.1f GB/s\n", 100 * f, 100 * (1 - f), m,
+             N / (m * 1e-3) / 1e9);
+    }
+    return 0;
+  }
   if (argc > 1 && std::string(argv[1]) == "sizes") {
     // one isolated launch per timing (launch, ramp and tail included) at transfer sizes of one
     // request: the floor of a single-request pull (c4 pair: 168 MB of fp8 per request)
