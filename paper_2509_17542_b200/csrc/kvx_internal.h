@@ -278,7 +278,8 @@ struct ChunkPlan {
       return;
     }
     *l0 = lb + rsum + (k - nramp) * step;
-    *l1 = *l0 + step < le ? *l0 + step : le;
+    const int64_t e = (int64_t)*l0 + step;
+    *l1 = e < le ? (int32_t)e : le;
   }
 };
 ChunkPlan chunk_plan(int32_t lb, int32_t le, int32_t layer_chunk);

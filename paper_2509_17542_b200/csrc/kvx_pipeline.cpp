@@ -68,9 +68,9 @@ ChunkPlan chunk_plan(int32_t lb, int32_t le, int32_t layer_chunk) {
   ChunkPlan p;
   p.lb = lb;
   p.le = le;
-  const int32_t mag = layer_chunk < 0 ? -layer_chunk : layer_chunk;
+  const int32_t mag = layer_chunk == INT32_MIN ? INT32_MAX : (layer_chunk < 0 ? -layer_chunk : layer_chunk);
   p.step = mag > 0 ? mag : std::max(1, le - lb);
-  if (layer_chunk < 0 && p.step >= 4 && le - lb >= 2 * p.step) {
+  if (layer_chunk < 0 && p.step >= 4 && (int64_t)(le - lb) >= 2 * (int64_t)p.step) {
     p.nramp = kMaxRamp;
     for (int i = 0; i < kMaxRamp; ++i) {  // step/8, step/4, step/2 (>= 1 layer each)
       p.ramp[i] = std::max(1, p.step >> (kMaxRamp - i));
@@ -78,7 +78,7 @@ ChunkPlan chunk_plan(int32_t lb, int32_t le, int32_t layer_chunk) {
     }
   }
   const int32_t rest = std::max(0, le - lb - p.rsum);
-  p.n = p.nramp + (rest + p.step - 1) / p.step;
+  p.n = p.nramp + (int32_t)(((int64_t)rest + p.step - 1) / p.step);
   return p;
 }
 }  // namespace kvx

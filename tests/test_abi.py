@@ -298,6 +298,7 @@ def test_pull_and_stage_validation_fails_before_enqueue(kvx):
     (10, 40, -20, [(10, 30), (30, 40)]),          # fewer than two chunks: no ramp
     (0, 80, -3, [(l, min(80, l + 3)) for l in range(0, 80, 3)]),   # |layer_chunk| < 4: no ramp
     (5, 5, -20, []),
+    (0, 80, -2**31, [(0, 80)]),                    # |INT32_MIN| saturates: one chunk
 ])
 def test_chunk_count_and_schedule(kvx, lb, le, lc, want):
     """kv_chunk_count: the A10 chunk schedule of kv_stage / kv_pull_staged -- the
