@@ -411,7 +411,8 @@ kv_status kv_recv_pipelined(kv_comm* comm, int32_t n_src, const kv_layout* const
  * (k_stage_rows): warps take pack items chunk after chunk, wait in-kernel for the chunk's
  * slot to be free, and the warp completing a chunk release-stores the ready word, in chunk
  * order; its counters are stream-ordered scratch (cudaMallocAsync / cudaFreeAsync on
- * `stream`).
+ * `stream`).  Like the persistent pull, several of them sharing one GPU need an SM budget
+ * (kv_set_sm_budget) so that every one stays resident while the others spin.
  * kv_stage with peer_scales != NULL computes dynamic fp8 scales (NEXT-1 i, kv_compute_scales
  * semantics) chunk by chunk from the P rank's data, for the D heads this P rank holds, into
  * dst[i]'s own scale array (writable DEVICE memory on P's GPU; the pack quantises with it)

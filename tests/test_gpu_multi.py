@@ -32,6 +32,8 @@ def _worker(rank, port, blob, mode, q):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(rank)
+    if mode == "pull_staged_pp":  # P side as the opt-in persistent k_stage_rows
+        os.environ["KVX_STAGE_PERSISTENT"] = "1"
     dist.init_process_group("gloo", rank=rank, world_size=2)
     try:
         import paper_2509_17542_b200 as kvx
@@ -64,7 +66,7 @@ def _worker(rank, port, blob, mode, q):
                 dist.barrier()
         elif mode.startswith("pull"):
             _pull_worker(rank, dc, kvx, tr, dist, q, mode.startswith("pull_staged"),
-                         mode in ("pull_staged", "pull_staged_dyn"), mode == "pull_staged_dyn")
+                         mode in ("pull_staged", "pull_staged_dyn", "pull_staged_pp"), mode == "pull_staged_dyn")
         else:
             uid = kvx.Comm.unique_id() if rank == 0 else None
             lst = [uid]
@@ -122,6 +124,9 @@ def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent, dyn=False):
     if rank == 0 and dyn:
         peer_sc = [kvx.ipc_open(h, o) for h, o in other["scales"]]
         maps += [(a, o) for a, (h, o) in zip(peer_sc, other["scales"])]
+    # every P rank of the test shares GPU0: persistent P kernels (KVX_STAGE_PERSISTENT) each
+    # get an SM budget so all of them stay resident (a spinning one must not starve another)
+    prev_budget = kvx.set_sm_budget(16) if rank == 0 and os.environ.get("KVX_STAGE_PERSISTENT") else None
     if rank == 0:
         for p in range(len(S)):
             qs = [qq for pp, qq, _, _ in pairs if pp == p]
@@ -140,6 +145,8 @@ def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent, dyn=False):
                         kvx.signal(fbase + 4 * (qq * 8 + p), 1, st)
                     for qq in qs:
                         kvx.wait(flags[p * 8 + qq:p * 8 + qq + 1], 1, err, 20.0, st)
+        if prev_budget is not None:
+            kvx.set_sm_budget(prev_budget)
         torch.cuda.synchronize()
         assert int(err.item()) == 0, "P-side wait timed out"
         dist.barrier()
@@ -182,7 +189,8 @@ def _pull_worker(rank, dc, kvx, tr, dist, q, staged, persistent, dyn=False):
         kvx.ipc_close(a, o)
 
 
-@pytest.mark.parametrize("mode", ["push", "nccl", "pull", "pull_staged", "pull_staged_chunked", "pull_staged_dyn"])
+@pytest.mark.parametrize("mode", ["push", "nccl", "pull", "pull_staged", "pull_staged_chunked", "pull_staged_dyn",
+                                  "pull_staged_pp"])
 @pytest.mark.parametrize("shape", ["merge", "split_fp8", "ragged_vendor"])
 def test_p_to_d_across_gpus(o1, mode, shape):
     if torch.cuda.device_count() < 2:
