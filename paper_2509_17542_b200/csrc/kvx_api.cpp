@@ -450,6 +450,11 @@ kv_status try_tile_copy(int32_t n_src, const kv_layout* const* src, const void* 
   a.share_p = share ? S->d.tp_rank : -1;
   a.stage_bytes = (int32_t)stage;
   a.stages = (int32_t)std::max<int64_t>(2, std::min<int64_t>(8, (200 * 1024) / stage));
+  {  // k_tile_copy: L2 evict-first on its streaming loads and stores (c2: 0.943 -> 0.957 of copy,
+     // profiles/r02/c2_evict_first.jsonl); KVX_TC_EVICT=0 turns it off
+    const char* ev = getenv("KVX_TC_EVICT");
+    a.evict_first = !(ev && *ev == '0');
+  }
   if (cast) {
     a.d_esize = D->elem_bytes;
     for (int i = 0; i < n_src; ++i) a.sscale[i] = src[i]->d.scales;

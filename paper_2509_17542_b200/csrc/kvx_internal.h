@@ -111,6 +111,7 @@ struct TileArgs {
   int32_t head_major;  // D inner order (HEAD, SLOT, DIM): smem [nh][Bp][D]; else (SLOT, HEAD, DIM): [Bp][nh][D]
   int32_t share_p;     // >= 0: only this P rank (kv_convert_share); -1: every P rank of each D rank
   int32_t stage_bytes, stages;
+  int32_t evict_first;  // k_tile_copy: L2 evict-first hints on the TMA loads and bulk stores (default; KVX_TC_EVICT=0 off)
   const int32_t* s_blk_off;
   const int32_t* s_blk_ids;
   const int32_t* d_blk_off;

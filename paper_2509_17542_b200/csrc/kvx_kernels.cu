@@ -844,6 +844,16 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uin
                "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void bulk_store_hint(void* gdst, const void* smem_src, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_u32(smem_src)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void bulk_wait_read() {
@@ -872,6 +882,14 @@ __device__ __forceinline__ void tma_load_5d(void* smem_dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d_hint(void* smem_dst, const CUtensorMap* map, int32_t c0, int32_t c1,
+                                                 int32_t c2, int32_t c3, int32_t c4, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::
+          "r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 
 // The valid rows (slots < valid) of a partial source sub-tile -- the request's last block --
 // by plain 16-B loads of the whole warp into the stage, in the box's order ([nh][Bp][D]
@@ -898,6 +916,7 @@ __device__ __forceinline__ void tile_rows_ldg(const TileArgs& a, uint8_t* sbuf, 
 
 __global__ void __launch_bounds__(32) k_tile_copy(const __grid_constant__ TileArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
+  const uint64_t pol = a.evict_first ? policy_evict_first() : 0ull;
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t S = (uint32_t)a.stages;
   const uint32_t SB = (uint32_t)a.stage_bytes;
@@ -982,7 +1001,12 @@ __global__ void __launch_bounds__(32) k_tile_copy(const __grid_constant__ TileAr
       tile_rows_ldg(a, smem + (size_t)s * SB, si, (int32_t)c, c3, c4, a.head_major ? c2 : c1, v, lane);
     if (lane == 0) {
       mbar_expect_tx_arrive(bars + s, v == (uint32_t)a.Bp ? SB : 0u);
-      if (v == (uint32_t)a.Bp) tma_load_5d(smem + (size_t)s * SB, &a.maps[si][c], c0, c1, c2, c3, c4, bars + s);
+      if (v == (uint32_t)a.Bp) {
+        if (a.evict_first)
+          tma_load_5d_hint(smem + (size_t)s * SB, &a.maps[si][c], c0, c1, c2, c3, c4, bars + s, pol);
+        else
+          tma_load_5d(smem + (size_t)s * SB, &a.maps[si][c], c0, c1, c2, c3, c4, bars + s);
+      }
     }
   };
   for (uint32_t k = 0; k < my && k < S; ++k) issue(k, k);
@@ -1005,7 +1029,10 @@ __global__ void __launch_bounds__(32) k_tile_copy(const __grid_constant__ TileAr
       __syncwarp();
     }
     for (uint32_t run = lane; run < cur.nruns; run += 32)
-      bulk_store(cur.dbase + (int64_t)run * cur.run_gap, buf + (size_t)run * cur.run_bytes, cur.run_bytes);
+      if (a.evict_first)
+        bulk_store_hint(cur.dbase + (int64_t)run * cur.run_gap, buf + (size_t)run * cur.run_bytes, cur.run_bytes, pol);
+      else
+        bulk_store(cur.dbase + (int64_t)run * cur.run_gap, buf + (size_t)run * cur.run_bytes, cur.run_bytes);
     bulk_commit();
     // reload the stage consumed in the previous iteration once its stores have read it
     bulk_wait_read<1>();
